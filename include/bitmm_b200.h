@@ -1,0 +1,149 @@
+/*
+ * bitmm_b200 — C ABI of the B200 (sm_100a) bitwise-GEMM hot path.
+ *
+ * Drop-in boundary for the reference's kernel layer (namespace bitmm in
+ * /root/reference/proj/include/bitmm/kernels.hpp and apb.hpp). Every entry point
+ * takes plain pointers and sizes in the reference's own packed layouts:
+ *
+ *   BitMatrix (tensor.hpp:59-112): rows x wpr uint64 words, row-major; element i
+ *     of a row is bit (i % 64) of word (i / 64); bit 1 decodes to +1, bit 0 to -1;
+ *     wpr >= ceil(cols / 64) and every padding bit is zero.
+ *   ThmPlanes (tensor.hpp:134-145): three BitMatrix payloads t, h, m of equal shape
+ *     plus scale and optional gamma (has_gamma = 0 means std::nullopt).
+ *   DenseMatrix (tensor.hpp:123-154): rows x cols float, row-major.
+ *   CsrMatrix (tensor.hpp:115-128): row_ptr[rows+1], col_idx[nnz] (uint64), vals[nnz].
+ *
+ * "b_packed" / "a_packed" operands are packed along K per OUTPUT COLUMN, exactly as
+ * the reference (kernels.hpp:44-46): row c of the packed operand is column c of the
+ * logical K x N operand. Outputs are row-major with leading dimension ldc.
+ *
+ * Two flavours per routine:
+ *   *_dev  : device pointers, stream-ordered on `stream` (a cudaStream_t, may be 0);
+ *            operand-encoding errors detected on the device are latched and reported
+ *            by bitmm_device_status().
+ *   *_host : host pointers; copies in, computes, copies out and synchronises. This is
+ *            the flavour a reference DenseMatrix-returning wrapper calls.
+ *
+ * Error codes mirror the reference's exception types:
+ *   BITMM_ERR_INVALID_ARGUMENT  <-> std::invalid_argument (kernels.cpp:52, 70-73, 115-118,
+ *                                    165-166, 187-188, 226-227, 301, 335-338; tensor.cpp:74)
+ *   BITMM_ERR_INVALID_ENCODING  <-> bitmm::InvalidEncoding (tensor.cpp:133-153)
+ * bitmm_last_error() returns the message of the most recent failure on this thread.
+ *
+ * There is no CPU fallback: without a CUDA device every compute entry point
+ * returns BITMM_ERR_NO_DEVICE.
+ */
+#ifndef BITMM_B200_H
+#define BITMM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  BITMM_OK = 0,
+  BITMM_ERR_INVALID_ARGUMENT = 1,
+  BITMM_ERR_INVALID_ENCODING = 2,
+  BITMM_ERR_CUDA = 3,
+  BITMM_ERR_NO_DEVICE = 4
+};
+
+/* Shared-dimension cap (tensor.hpp:21, kMaxSharedDim = 2^20). */
+#define BITMM_MAX_SHARED_DIM (INT64_C(1) << 20)
+
+int bitmm_abi_version(void);
+const char* bitmm_last_error(void);
+/* Number of SMs of the current device, or 0 if no device. */
+int bitmm_device_sm_count(void);
+/* Synchronises `stream`, returns and clears the latched device-side encoding status. */
+int bitmm_device_status(void* stream);
+/* Pre-grows the internal device workspace so no allocation happens inside timed loops. */
+int bitmm_reserve_workspace(size_t bytes);
+/* Workspace bytes a routine needs for the given shape (routine: 0=1x1, 1=1x2, 2=2x2, 3=1x32/APB). */
+size_t bitmm_workspace_bytes(int routine, int64_t m, int64_t n, int64_t k);
+/* Number of kernels launched by the most recent compute call on this thread. */
+int bitmm_last_launch_count(void);
+
+/* ---- 1/1: replaces gemm_1x1 (kernels.hpp:47-48, kernels.cpp:163-183) ----
+ * C[r][c] = (gamma_a * gamma_b) * float(K - 2*popcount(a_r xor b_c)).
+ * Writes int32 units to c_units and/or scaled floats to c (either may be NULL). */
+int bitmm_gemm_1x1_dev(const uint64_t* a, int64_t m, const uint64_t* b_packed, int64_t n, int64_t k,
+                       int64_t wpr, float gamma_a, float gamma_b, int32_t* c_units, float* c,
+                       int64_t ldc, void* stream);
+int bitmm_gemm_1x1_host(const uint64_t* a, int64_t m, const uint64_t* b_packed, int64_t n,
+                        int64_t k, int64_t wpr, float gamma_a, float gamma_b, int32_t* c_units,
+                        float* c, int64_t ldc);
+/* Same contract, evaluated by the CUDA-core LOP3+POPC kernel (measured alternative). */
+int bitmm_gemm_1x1_popc_dev(const uint64_t* a, int64_t m, const uint64_t* b_packed, int64_t n,
+                            int64_t k, int64_t wpr, float gamma_a, float gamma_b,
+                            int32_t* c_units, float* c, int64_t ldc, void* stream);
+
+/* ---- 1/2: replaces gemm_1x2 (kernels.hpp:55, kernels.cpp:185-221) ----
+ * w: m x wpr binary rows; planes t/h/mm: n x wpr, packed along K per output column.
+ * units = 2 * sum_k sign(w[r][k]) * p[c][k]; scale = 0.5f*gamma*a_scale*(a_gamma or 1)
+ * (kernels.cpp:193). Optional per-row (row_scale[m]) and per-column (col_scale[n])
+ * multipliers extend the scalar: C = ((scale*row_scale[r])*col_scale[c]) * float(units). */
+int bitmm_gemm_1x2_dev(const uint64_t* w, int64_t m, float gamma, const uint64_t* t,
+                       const uint64_t* h, const uint64_t* mm, int64_t n, int64_t k, int64_t wpr,
+                       float a_scale, int has_a_gamma, float a_gamma, const float* row_scale,
+                       const float* col_scale, int32_t* c_units, float* c, int64_t ldc,
+                       void* stream);
+int bitmm_gemm_1x2_host(const uint64_t* w, int64_t m, float gamma, const uint64_t* t,
+                        const uint64_t* h, const uint64_t* mm, int64_t n, int64_t k, int64_t wpr,
+                        float a_scale, int has_a_gamma, float a_gamma, const float* row_scale,
+                        const float* col_scale, int32_t* c_units, float* c, int64_t ldc);
+
+/* ---- 2/2: replaces gemm_2x2 (kernels.hpp:62, kernels.cpp:223-275) ----
+ * units = 4 * sum_k p_w[r][k] * p_a[c][k];
+ * scale = 0.25f*w_scale*a_scale*(w_gamma or 1)*(a_gamma or 1) (kernels.cpp:232-233). */
+int bitmm_gemm_2x2_dev(const uint64_t* wt, const uint64_t* wh, const uint64_t* wm, int64_t m,
+                       float w_scale, int has_w_gamma, float w_gamma, const uint64_t* at,
+                       const uint64_t* ah, const uint64_t* am, int64_t n, int64_t k, int64_t wpr,
+                       float a_scale, int has_a_gamma, float a_gamma, const float* row_scale,
+                       const float* col_scale, int32_t* c_units, float* c, int64_t ldc,
+                       void* stream);
+int bitmm_gemm_2x2_host(const uint64_t* wt, const uint64_t* wh, const uint64_t* wm, int64_t m,
+                        float w_scale, int has_w_gamma, float w_gamma, const uint64_t* at,
+                        const uint64_t* ah, const uint64_t* am, int64_t n, int64_t k, int64_t wpr,
+                        float a_scale, int has_a_gamma, float a_gamma, const float* row_scale,
+                        const float* col_scale, int32_t* c_units, float* c, int64_t ldc);
+
+/* ---- 1/32 binary x fp32: replaces gemm_1x32_ref (kernels.hpp:73, kernels.cpp:300-332) ----
+ * C[r][c] = gamma_r * sum_k sign(w[r][k]) * b[k][c], gamma_r = row_gamma ? row_gamma[r] : gamma.
+ * b is K x n fp32 row-major with leading dimension ldb. */
+int bitmm_gemm_1x32_dev(const uint64_t* w, int64_t m, int64_t k, int64_t wpr, float gamma,
+                        const float* row_gamma, const float* b, int64_t n, int64_t ldb, float* c,
+                        int64_t ldc, void* stream);
+int bitmm_gemm_1x32_host(const uint64_t* w, int64_t m, int64_t k, int64_t wpr, float gamma,
+                         const float* row_gamma, const float* b, int64_t n, int64_t ldb, float* c,
+                         int64_t ldc);
+
+/* ---- sparse x dense: replaces spmm_csr (kernels.hpp:76, kernels.cpp:334-352) ---- */
+int bitmm_spmm_csr_dev(int64_t rows, int64_t cols, const uint64_t* row_ptr, const uint64_t* col_idx,
+                       const float* vals, const float* b, int64_t n, int64_t ldb, float* c,
+                       int64_t ldc, void* stream);
+int bitmm_spmm_csr_host(int64_t rows, int64_t cols, const uint64_t* row_ptr,
+                        const uint64_t* col_idx, const float* vals, int64_t nnz, const float* b,
+                        int64_t n, int64_t ldb, float* c, int64_t ldc);
+
+/* ---- APB layer forward: replaces layer_forward (apb.hpp:65, apb.cpp:158-164) ----
+ * C = alpha_r * (sign(bin) . b) + residual . b, fused in one GEMM epilogue.
+ * alpha_r = row_alpha ? row_alpha[r] : alpha (the reference ApbLayer holds a scalar alpha,
+ * apb.hpp:48). bin: rows x wpr; residual CSR over rows x cols; b: cols x n fp32. */
+int bitmm_layer_forward_dev(int64_t rows, int64_t cols, float alpha, const float* row_alpha,
+                            const uint64_t* bin, int64_t wpr, const uint64_t* row_ptr,
+                            const uint64_t* col_idx, const float* vals, const float* b, int64_t n,
+                            int64_t ldb, float* c, int64_t ldc, void* stream);
+int bitmm_layer_forward_host(int64_t rows, int64_t cols, float alpha, const float* row_alpha,
+                             const uint64_t* bin, int64_t wpr, const uint64_t* row_ptr,
+                             const uint64_t* col_idx, const float* vals, int64_t nnz,
+                             const float* b, int64_t n, int64_t ldb, float* c, int64_t ldc);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BITMM_B200_H */

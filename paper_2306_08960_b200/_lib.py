@@ -1,0 +1,105 @@
+"""ctypes binding of the C ABI declared in include/bitmm_b200.h.
+
+The product path is the in-tree CUDA library `libbitmm_b200.so`. There is no
+CPU fallback: if the library is missing this module raises on load.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(PKG_DIR)
+LIB_PATH = os.path.join(PKG_DIR, "libbitmm_b200.so")
+HEADER = os.path.join(REPO, "include", "bitmm_b200.h")
+
+OK = 0
+ERR_INVALID_ARGUMENT = 1
+ERR_INVALID_ENCODING = 2
+ERR_CUDA = 3
+ERR_NO_DEVICE = 4
+
+_p = C.c_void_p
+_i64 = C.c_int64
+_f = C.c_float
+_i = C.c_int
+
+# name -> (restype, argtypes); mirrors include/bitmm_b200.h
+SIGNATURES = {
+    "bitmm_abi_version": (_i, []),
+    "bitmm_last_error": (C.c_char_p, []),
+    "bitmm_device_sm_count": (_i, []),
+    "bitmm_device_status": (_i, [_p]),
+    "bitmm_reserve_workspace": (_i, [C.c_size_t]),
+    "bitmm_workspace_bytes": (C.c_size_t, [_i, _i64, _i64, _i64]),
+    "bitmm_last_launch_count": (_i, []),
+    "bitmm_gemm_1x1_dev": (_i, [_p, _i64, _p, _i64, _i64, _i64, _f, _f, _p, _p, _i64, _p]),
+    "bitmm_gemm_1x1_host": (_i, [_p, _i64, _p, _i64, _i64, _i64, _f, _f, _p, _p, _i64]),
+    "bitmm_gemm_1x1_popc_dev": (_i, [_p, _i64, _p, _i64, _i64, _i64, _f, _f, _p, _p, _i64, _p]),
+    "bitmm_gemm_1x2_dev": (
+        _i,
+        [_p, _i64, _f, _p, _p, _p, _i64, _i64, _i64, _f, _i, _f, _p, _p, _p, _p, _i64, _p],
+    ),
+    "bitmm_gemm_1x2_host": (
+        _i,
+        [_p, _i64, _f, _p, _p, _p, _i64, _i64, _i64, _f, _i, _f, _p, _p, _p, _p, _i64],
+    ),
+    "bitmm_gemm_2x2_dev": (
+        _i,
+        [_p, _p, _p, _i64, _f, _i, _f, _p, _p, _p, _i64, _i64, _i64, _f, _i, _f, _p, _p, _p, _p,
+         _i64, _p],
+    ),
+    "bitmm_gemm_2x2_host": (
+        _i,
+        [_p, _p, _p, _i64, _f, _i, _f, _p, _p, _p, _i64, _i64, _i64, _f, _i, _f, _p, _p, _p, _p,
+         _i64],
+    ),
+    "bitmm_gemm_1x32_dev": (_i, [_p, _i64, _i64, _i64, _f, _p, _p, _i64, _i64, _p, _i64, _p]),
+    "bitmm_gemm_1x32_host": (_i, [_p, _i64, _i64, _i64, _f, _p, _p, _i64, _i64, _p, _i64]),
+    "bitmm_spmm_csr_dev": (_i, [_i64, _i64, _p, _p, _p, _p, _i64, _i64, _p, _i64, _p]),
+    "bitmm_spmm_csr_host": (_i, [_i64, _i64, _p, _p, _p, _i64, _p, _i64, _i64, _p, _i64]),
+    "bitmm_layer_forward_dev": (
+        _i,
+        [_i64, _i64, _f, _p, _p, _i64, _p, _p, _p, _p, _i64, _i64, _p, _i64, _p],
+    ),
+    "bitmm_layer_forward_host": (
+        _i,
+        [_i64, _i64, _f, _p, _p, _i64, _p, _p, _p, _i64, _p, _i64, _i64, _p, _i64],
+    ),
+}
+
+
+class BitmmError(RuntimeError):
+    """Raised for BITMM_ERR_CUDA / BITMM_ERR_NO_DEVICE."""
+
+
+def header_symbols(path: str = HEADER) -> list[str]:
+    """Every function name declared in include/bitmm_b200.h."""
+    text = open(path).read()
+    return sorted(set(re.findall(r"\b(bitmm_[a-z0-9_]+)\s*\(", text)))
+
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise BitmmError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2306_08960_b200.build` "
+            "(there is no CPU fallback)"
+        )
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    return load().bitmm_last_error().decode(errors="replace")

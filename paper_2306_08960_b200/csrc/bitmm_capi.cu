@@ -1,0 +1,777 @@
+// extern "C" implementation of include/bitmm_b200.h: argument validation in the
+// reference's order, workspace management, TMA descriptor encoding and the
+// launch sequence (unpack -> tcgen05 GEMM with fused epilogue) per routine.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "bitmm_b200.h"
+#include "popc_gemm.cuh"
+#include "ptx.cuh"
+#include "tc_gemm.cuh"
+#include "unpack.cuh"
+
+using namespace bitmm_dev;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define BITMM_CUDA_TRY(expr)                                                              \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(BITMM_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));    \
+  } while (0)
+
+#define BITMM_TRY(expr)         \
+  do {                          \
+    int rc_ = (expr);           \
+    if (rc_ != BITMM_OK) return rc_; \
+  } while (0)
+
+constexpr int kMaxDevices = 16;
+
+struct Arena {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+struct DeviceState {
+  bool init = false;
+  int sms = 0;
+  int* status = nullptr;  // latched device-side encoding flags
+  Arena ws;               // intermediates (expanded operands)
+  Arena io;               // host-flavour staging of inputs/outputs
+  cudaStream_t stream = nullptr;  // host-flavour private stream
+  unsigned attr_mask = 0;
+};
+
+std::mutex g_mu;
+DeviceState g_state[kMaxDevices];
+
+int device_state(DeviceState** out) {
+  int dev = 0;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return fail(BITMM_ERR_NO_DEVICE, "no CUDA device available (bitmm_b200 has no CPU fallback)");
+  }
+  BITMM_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev >= kMaxDevices) return fail(BITMM_ERR_CUDA, "device index out of range");
+  DeviceState& st = g_state[dev];
+  if (!st.init) {
+    BITMM_CUDA_TRY(cudaDeviceGetAttribute(&st.sms, cudaDevAttrMultiProcessorCount, dev));
+    BITMM_CUDA_TRY(cudaMalloc(&st.status, sizeof(int)));
+    BITMM_CUDA_TRY(cudaMemset(st.status, 0, sizeof(int)));
+    BITMM_CUDA_TRY(cudaStreamCreateWithFlags(&st.stream, cudaStreamNonBlocking));
+    st.init = true;
+  }
+  *out = &st;
+  return BITMM_OK;
+}
+
+int arena_reserve(Arena& a, size_t bytes) {
+  if (bytes <= a.bytes) return BITMM_OK;
+  if (a.ptr) {
+    BITMM_CUDA_TRY(cudaDeviceSynchronize());
+    BITMM_CUDA_TRY(cudaFree(a.ptr));
+    a.ptr = nullptr;
+    a.bytes = 0;
+  }
+  size_t grown = std::max(bytes, static_cast<size_t>(1) << 20);
+  BITMM_CUDA_TRY(cudaMalloc(&a.ptr, grown));
+  a.bytes = grown;
+  return BITMM_OK;
+}
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+// ---------------- TMA descriptors (driver entry point, no -lcuda) ----------------
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                      const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                      const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                      CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled_t encode_fn() {
+  static PFN_encodeTiled_t fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+  });
+  return fn;
+}
+
+// K-major operand [rows][inner] with 128-byte rows per box, 128B swizzle.
+int make_operand_map(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int elem_bytes,
+                     uint64_t inner_elems, uint64_t rows, uint32_t box_rows) {
+  PFN_encodeTiled_t enc = encode_fn();
+  if (!enc) return fail(BITMM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {inner_elems, rows};
+  cuuint64_t strides[1] = {inner_elems * static_cast<uint64_t>(elem_bytes)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(TC_BK_BYTES / elem_bytes), box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(BITMM_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return BITMM_OK;
+}
+
+// ---------------- launches ----------------
+int launch_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(BITMM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  ++g_launches;
+  return BITMM_OK;
+}
+
+unsigned blocks_for(long long total, int threads) {
+  return static_cast<unsigned>((total + threads - 1) / threads);
+}
+
+int run_unpack_sign_i8(const uint64_t* words, int64_t rows, int64_t wpr, int64_t k, int64_t kpad,
+                       uint8_t* out, int* flag, cudaStream_t s) {
+  const int wpr32 = static_cast<int>(wpr * 2);
+  const long long total = rows * std::max<long long>(kpad / 32, wpr32);
+  if (total == 0) return BITMM_OK;
+  unpack_sign_i8<<<blocks_for(total, 256), 256, 0, s>>>(reinterpret_cast<const uint32_t*>(words),
+                                                        rows, wpr32, static_cast<int>(k),
+                                                        static_cast<int>(kpad), out, flag);
+  return launch_check("unpack_sign_i8");
+}
+
+int run_unpack_level_i8(const uint64_t* t, const uint64_t* h, const uint64_t* m, int64_t rows,
+                        int64_t wpr, int64_t k, int64_t kpad, uint8_t* out, int* flag,
+                        cudaStream_t s) {
+  const int wpr32 = static_cast<int>(wpr * 2);
+  const long long total = rows * std::max<long long>(kpad / 32, wpr32);
+  if (total == 0) return BITMM_OK;
+  unpack_level_i8<<<blocks_for(total, 256), 256, 0, s>>>(
+      reinterpret_cast<const uint32_t*>(t), reinterpret_cast<const uint32_t*>(h),
+      reinterpret_cast<const uint32_t*>(m), rows, wpr32, static_cast<int>(k),
+      static_cast<int>(kpad), out, flag);
+  return launch_check("unpack_level_i8");
+}
+
+template <Kind KIND, Epi EPI>
+int run_tc_gemm(DeviceState& st, const CUtensorMap& ta, const CUtensorMap& tb, TcParams p,
+                cudaStream_t s) {
+  constexpr unsigned bit = 1u << (static_cast<int>(KIND) * 3 + static_cast<int>(EPI));
+  if (!(st.attr_mask & bit)) {
+    BITMM_CUDA_TRY(cudaFuncSetAttribute(tc_gemm_kernel<KIND, EPI>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        TC_SMEM_BYTES));
+    st.attr_mask |= bit;
+  }
+  p.num_m_blocks = static_cast<int>((p.M + TC_BM - 1) / TC_BM);
+  p.num_n_blocks = static_cast<int>((p.N + TC_BN - 1) / TC_BN);
+  p.num_tiles = p.num_m_blocks * p.num_n_blocks;
+  const int grid = std::min(p.num_tiles, st.sms);
+  tc_gemm_kernel<KIND, EPI><<<grid, TC_THREADS, TC_SMEM_BYTES, s>>>(ta, tb, p);
+  return launch_check("tc_gemm_kernel");
+}
+
+// Common integer-GEMM tail: A8 [m][kpad], B8 [n][kpad] already expanded.
+int run_int_gemm(DeviceState& st, const uint8_t* A8, const uint8_t* B8, int64_t m, int64_t n,
+                 int64_t kpad, int shift, float scale, const float* row_scale,
+                 const float* col_scale, int32_t* c_units, float* c, int64_t ldc, cudaStream_t s) {
+  CUtensorMap ta, tb;
+  BITMM_TRY(make_operand_map(&ta, A8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad, m, TC_BM));
+  BITMM_TRY(make_operand_map(&tb, B8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad, n, TC_BN));
+  TcParams p{};
+  p.M = static_cast<int>(m);
+  p.N = static_cast<int>(n);
+  p.num_kb = static_cast<int>(kpad / TC_BK_BYTES);
+  p.a_kb_period = p.num_kb;
+  p.shift = shift;
+  p.scale = scale;
+  p.row_scale = row_scale;
+  p.col_scale = col_scale;
+  p.ldc = ldc;
+  if (c_units) {
+    p.out_i32 = c_units;
+    BITMM_TRY((run_tc_gemm<Kind::I8, Epi::I32>(st, ta, tb, p, s)));
+  }
+  if (c) {
+    p.out_f32 = c;
+    BITMM_TRY((run_tc_gemm<Kind::I8, Epi::F32>(st, ta, tb, p, s)));
+  }
+  return BITMM_OK;
+}
+
+int check_gemm_dims(int64_t m, int64_t n, int64_t k, int64_t wpr, int64_t ldc) {
+  if (m <= 0 || k <= 0 || n <= 0) return fail(BITMM_ERR_INVALID_ARGUMENT, "gemm dimensions must be positive");
+  if (k > BITMM_MAX_SHARED_DIM)
+    return fail(BITMM_ERR_INVALID_ARGUMENT, "shared dimension exceeds the 2^20 accumulator bound");
+  if (wpr * 64 < k) return fail(BITMM_ERR_INVALID_ARGUMENT, "words_per_row too small for the column count");
+  if (ldc < n) return fail(BITMM_ERR_INVALID_ARGUMENT, "ldc smaller than the output column count");
+  if (m > INT32_MAX / 2 || n > INT32_MAX / 2) return fail(BITMM_ERR_INVALID_ARGUMENT, "gemm dimension too large");
+  return BITMM_OK;
+}
+
+int read_status(DeviceState& st, cudaStream_t s) {
+  BITMM_CUDA_TRY(cudaStreamSynchronize(s));
+  int flag = 0;
+  BITMM_CUDA_TRY(cudaMemcpy(&flag, st.status, sizeof(int), cudaMemcpyDeviceToHost));
+  BITMM_CUDA_TRY(cudaMemset(st.status, 0, sizeof(int)));
+  if (flag & ERR_ENCODING) return fail(BITMM_ERR_INVALID_ENCODING, "invalid ternary plane encoding or nonzero plane padding");
+  if (flag & ERR_PADDING) return fail(BITMM_ERR_INVALID_ARGUMENT, "bit matrix padding must be zero");
+  return BITMM_OK;
+}
+
+struct Carve {
+  uint8_t* base;
+  size_t off = 0;
+  explicit Carve(void* b) : base(static_cast<uint8_t*>(b)) {}
+  template <typename T>
+  T* take(size_t bytes) {
+    T* p = reinterpret_cast<T*>(base + off);
+    off = align_up(off + bytes, 1024);
+    return p;
+  }
+};
+
+size_t ws_bytes_int(int64_t m, int64_t n, int64_t k) {
+  const int64_t kpad = round_up(k, TC_BK_BYTES);
+  return align_up(m * kpad, 1024) + align_up(n * kpad, 1024) + 2048;
+}
+size_t ws_bytes_1x32(int64_t m, int64_t n, int64_t k) {
+  const int64_t kpad = round_up(k, 64);
+  return align_up(m * kpad * 2, 1024) + align_up(n * 3 * kpad * 2, 1024) + 2048;
+}
+
+// ---------------- routine bodies on device pointers ----------------
+int gemm_1x1_dev_impl(DeviceState& st, const uint64_t* a, int64_t m, const uint64_t* b, int64_t n,
+                      int64_t k, int64_t wpr, float gamma_a, float gamma_b, int32_t* c_units,
+                      float* c, int64_t ldc, cudaStream_t s) {
+  const int64_t kpad = round_up(k, TC_BK_BYTES);
+  BITMM_TRY(arena_reserve(st.ws, ws_bytes_int(m, n, k)));
+  Carve cv(st.ws.ptr);
+  uint8_t* A8 = cv.take<uint8_t>(m * kpad);
+  uint8_t* B8 = cv.take<uint8_t>(n * kpad);
+  BITMM_TRY(run_unpack_sign_i8(a, m, wpr, k, kpad, A8, st.status, s));
+  BITMM_TRY(run_unpack_sign_i8(b, n, wpr, k, kpad, B8, st.status, s));
+  const float scale = gamma_a * gamma_b;  // kernels.cpp:170
+  return run_int_gemm(st, A8, B8, m, n, kpad, 0, scale, nullptr, nullptr, c_units, c, ldc, s);
+}
+
+int gemm_1x2_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, float gamma, const uint64_t* t,
+                      const uint64_t* h, const uint64_t* mm, int64_t n, int64_t k, int64_t wpr,
+                      float a_scale, int has_a_gamma, float a_gamma, const float* row_scale,
+                      const float* col_scale, int32_t* c_units, float* c, int64_t ldc,
+                      cudaStream_t s) {
+  const int64_t kpad = round_up(k, TC_BK_BYTES);
+  BITMM_TRY(arena_reserve(st.ws, ws_bytes_int(m, n, k)));
+  Carve cv(st.ws.ptr);
+  uint8_t* A8 = cv.take<uint8_t>(m * kpad);
+  uint8_t* B8 = cv.take<uint8_t>(n * kpad);
+  BITMM_TRY(run_unpack_level_i8(t, h, mm, n, wpr, k, kpad, B8, st.status, s));
+  BITMM_TRY(run_unpack_sign_i8(w, m, wpr, k, kpad, A8, st.status, s));
+  // kernels.cpp:193: half_scale = 0.5f * gamma * a_packed.scale * a_packed.gamma.value_or(1.0f)
+  const float scale = 0.5f * gamma * a_scale * (has_a_gamma ? a_gamma : 1.0f);
+  return run_int_gemm(st, A8, B8, m, n, kpad, 1, scale, row_scale, col_scale, c_units, c, ldc, s);
+}
+
+int gemm_2x2_dev_impl(DeviceState& st, const uint64_t* wt, const uint64_t* wh, const uint64_t* wm,
+                      int64_t m, float w_scale, int has_w_gamma, float w_gamma, const uint64_t* at,
+                      const uint64_t* ah, const uint64_t* am, int64_t n, int64_t k, int64_t wpr,
+                      float a_scale, int has_a_gamma, float a_gamma, const float* row_scale,
+                      const float* col_scale, int32_t* c_units, float* c, int64_t ldc,
+                      cudaStream_t s) {
+  const int64_t kpad = round_up(k, TC_BK_BYTES);
+  BITMM_TRY(arena_reserve(st.ws, ws_bytes_int(m, n, k)));
+  Carve cv(st.ws.ptr);
+  uint8_t* A8 = cv.take<uint8_t>(m * kpad);
+  uint8_t* B8 = cv.take<uint8_t>(n * kpad);
+  BITMM_TRY(run_unpack_level_i8(wt, wh, wm, m, wpr, k, kpad, A8, st.status, s));
+  BITMM_TRY(run_unpack_level_i8(at, ah, am, n, wpr, k, kpad, B8, st.status, s));
+  // kernels.cpp:232-233
+  const float scale = 0.25f * w_scale * a_scale * (has_w_gamma ? w_gamma : 1.0f) *
+                      (has_a_gamma ? a_gamma : 1.0f);
+  return run_int_gemm(st, A8, B8, m, n, kpad, 2, scale, row_scale, col_scale, c_units, c, ldc, s);
+}
+
+int apb_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, int64_t k, int64_t wpr, float gamma,
+                 const float* row_gamma, const float* b, int64_t n, int64_t ldb,
+                 const uint64_t* row_ptr, const uint64_t* col_idx, const float* vals, float* c,
+                 int64_t ldc, cudaStream_t s) {
+  constexpr int kParts = 3;
+  const int64_t kpad = round_up(k, 64);
+  BITMM_TRY(arena_reserve(st.ws, ws_bytes_1x32(m, n, k)));
+  Carve cv(st.ws.ptr);
+  uint16_t* Abf = cv.take<uint16_t>(m * kpad * 2);
+  uint16_t* XT = cv.take<uint16_t>(n * kParts * kpad * 2);
+  {
+    const int wpr32 = static_cast<int>(wpr * 2);
+    const long long total = m * std::max<long long>(kpad / 32, wpr32);
+    unpack_sign_bf16<<<blocks_for(total, 256), 256, 0, s>>>(
+        reinterpret_cast<const uint32_t*>(w), m, wpr32, static_cast<int>(k),
+        static_cast<int>(kpad), Abf, st.status);
+    BITMM_TRY(launch_check("unpack_sign_bf16"));
+  }
+  {
+    dim3 grid(static_cast<unsigned>(kpad / 64), static_cast<unsigned>((n + 31) / 32));
+    split_x_bf16<<<grid, 256, 0, s>>>(b, ldb, static_cast<int>(k), static_cast<int>(n),
+                                      static_cast<int>(kpad), kParts, XT);
+    BITMM_TRY(launch_check("split_x_bf16"));
+  }
+  CUtensorMap ta, tb;
+  BITMM_TRY(make_operand_map(&ta, Abf, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kpad, m, TC_BM));
+  BITMM_TRY(make_operand_map(&tb, XT, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kParts * kpad, n, TC_BN));
+  TcParams p{};
+  p.M = static_cast<int>(m);
+  p.N = static_cast<int>(n);
+  p.a_kb_period = static_cast<int>(kpad / 64);
+  p.num_kb = kParts * p.a_kb_period;
+  p.scale = gamma;
+  p.row_scale = row_gamma;
+  p.out_f32 = c;
+  p.ldc = ldc;
+  p.csr_row_ptr = reinterpret_cast<const unsigned long long*>(row_ptr);
+  p.csr_col = reinterpret_cast<const unsigned long long*>(col_idx);
+  p.csr_val = vals;
+  p.X = b;
+  p.ldx = ldb;
+  return run_tc_gemm<Kind::BF16, Epi::APB>(st, ta, tb, p, s);
+}
+
+int with_device(DeviceState** st) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return device_state(st);
+}
+
+int check_csr_host(int64_t rows, int64_t cols, const uint64_t* row_ptr, const uint64_t* col_idx,
+                   const float* vals, int64_t nnz) {
+  // CsrMatrix::validate (tensor.cpp:104-123)
+  if (rows < 0 || cols < 0) return fail(BITMM_ERR_INVALID_ARGUMENT, "matrix dimensions must be non-negative");
+  if (row_ptr[0] != 0) return fail(BITMM_ERR_INVALID_ARGUMENT, "csr row_ptr must start at 0");
+  for (int64_t r = 0; r < rows; ++r)
+    if (row_ptr[r] > row_ptr[r + 1]) return fail(BITMM_ERR_INVALID_ARGUMENT, "csr row_ptr must be monotone");
+  if (static_cast<int64_t>(row_ptr[rows]) != nnz) return fail(BITMM_ERR_INVALID_ARGUMENT, "csr payload sizes must match nnz");
+  for (int64_t r = 0; r < rows; ++r)
+    for (uint64_t i = row_ptr[r]; i < row_ptr[r + 1]; ++i) {
+      if (col_idx[i] >= static_cast<uint64_t>(cols)) return fail(BITMM_ERR_INVALID_ARGUMENT, "csr column index out of range");
+      if (i > row_ptr[r] && col_idx[i - 1] >= col_idx[i])
+        return fail(BITMM_ERR_INVALID_ARGUMENT, "csr column indices must be strictly increasing per row");
+    }
+  (void)vals;
+  return BITMM_OK;
+}
+
+}  // namespace
+
+// =========================== exported ABI ===========================
+extern "C" {
+
+int bitmm_abi_version(void) { return 1; }
+
+const char* bitmm_last_error(void) { return g_err.c_str(); }
+
+int bitmm_last_launch_count(void) { return g_launches; }
+
+int bitmm_device_sm_count(void) {
+  DeviceState* st = nullptr;
+  if (with_device(&st) != BITMM_OK) return 0;
+  return st->sms;
+}
+
+int bitmm_device_status(void* stream) {
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  return read_status(*st, static_cast<cudaStream_t>(stream));
+}
+
+int bitmm_reserve_workspace(size_t bytes) {
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  return arena_reserve(st->ws, bytes);
+}
+
+size_t bitmm_workspace_bytes(int routine, int64_t m, int64_t n, int64_t k) {
+  if (m <= 0 || n <= 0 || k <= 0) return 0;
+  return routine == 3 ? ws_bytes_1x32(m, n, k) : ws_bytes_int(m, n, k);
+}
+
+// ---------------- 1/1 ----------------
+int bitmm_gemm_1x1_dev(const uint64_t* a, int64_t m, const uint64_t* b_packed, int64_t n, int64_t k,
+                       int64_t wpr, float gamma_a, float gamma_b, int32_t* c_units, float* c,
+                       int64_t ldc, void* stream) {
+  g_launches = 0;
+  BITMM_TRY(check_gemm_dims(m, n, k, wpr, ldc));
+  if (!a || !b_packed || (!c_units && !c)) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  return gemm_1x1_dev_impl(*st, a, m, b_packed, n, k, wpr, gamma_a, gamma_b, c_units, c, ldc,
+                           static_cast<cudaStream_t>(stream));
+}
+
+int bitmm_gemm_1x1_popc_dev(const uint64_t* a, int64_t m, const uint64_t* b_packed, int64_t n,
+                            int64_t k, int64_t wpr, float gamma_a, float gamma_b,
+                            int32_t* c_units, float* c, int64_t ldc, void* stream) {
+  g_launches = 0;
+  BITMM_TRY(check_gemm_dims(m, n, k, wpr, ldc));
+  if (!a || !b_packed || (!c_units && !c)) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  dim3 grid(static_cast<unsigned>((n + PC_BN - 1) / PC_BN), static_cast<unsigned>((m + PC_BM - 1) / PC_BM));
+  const float scale = gamma_a * gamma_b;
+  const auto* A = reinterpret_cast<const uint32_t*>(a);
+  const auto* B = reinterpret_cast<const uint32_t*>(b_packed);
+  if (c_units) {
+    popc_gemm_1x1<false><<<grid, PC_THREADS, 0, s>>>(A, B, (int)m, (int)n, (int)k, (int)(wpr * 2), scale,
+                                                     c_units, nullptr, ldc);
+    BITMM_TRY(launch_check("popc_gemm_1x1"));
+  }
+  if (c) {
+    popc_gemm_1x1<true><<<grid, PC_THREADS, 0, s>>>(A, B, (int)m, (int)n, (int)k, (int)(wpr * 2), scale,
+                                                    nullptr, c, ldc);
+    BITMM_TRY(launch_check("popc_gemm_1x1"));
+  }
+  return BITMM_OK;
+}
+
+int bitmm_gemm_1x1_host(const uint64_t* a, int64_t m, const uint64_t* b_packed, int64_t n,
+                        int64_t k, int64_t wpr, float gamma_a, float gamma_b, int32_t* c_units,
+                        float* c, int64_t ldc) {
+  g_launches = 0;
+  BITMM_TRY(check_gemm_dims(m, n, k, wpr, ldc));
+  if (!a || !b_packed || (!c_units && !c)) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  cudaStream_t s = st->stream;
+  const size_t a_bytes = m * wpr * 8, b_bytes = n * wpr * 8, c_bytes = m * ldc * 4;
+  BITMM_TRY(arena_reserve(st->io, align_up(a_bytes, 1024) + align_up(b_bytes, 1024) + 2 * align_up(c_bytes, 1024)));
+  Carve cv(st->io.ptr);
+  uint64_t* da = cv.take<uint64_t>(a_bytes);
+  uint64_t* db = cv.take<uint64_t>(b_bytes);
+  int32_t* dcu = c_units ? cv.take<int32_t>(c_bytes) : nullptr;
+  float* dc = c ? cv.take<float>(c_bytes) : nullptr;
+  BITMM_CUDA_TRY(cudaMemcpyAsync(da, a, a_bytes, cudaMemcpyHostToDevice, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(db, b_packed, b_bytes, cudaMemcpyHostToDevice, s));
+  BITMM_TRY(gemm_1x1_dev_impl(*st, da, m, db, n, k, wpr, gamma_a, gamma_b, dcu, dc, ldc, s));
+  if (dcu) BITMM_CUDA_TRY(cudaMemcpyAsync(c_units, dcu, c_bytes, cudaMemcpyDeviceToHost, s));
+  if (dc) BITMM_CUDA_TRY(cudaMemcpyAsync(c, dc, c_bytes, cudaMemcpyDeviceToHost, s));
+  return read_status(*st, s);
+}
+
+// ---------------- 1/2 ----------------
+int bitmm_gemm_1x2_dev(const uint64_t* w, int64_t m, float gamma, const uint64_t* t,
+                       const uint64_t* h, const uint64_t* mm, int64_t n, int64_t k, int64_t wpr,
+                       float a_scale, int has_a_gamma, float a_gamma, const float* row_scale,
+                       const float* col_scale, int32_t* c_units, float* c, int64_t ldc,
+                       void* stream) {
+  g_launches = 0;
+  if (!(a_scale > 0.0f)) return fail(BITMM_ERR_INVALID_ENCODING, "plane scale must be positive");
+  BITMM_TRY(check_gemm_dims(m, n, k, wpr, ldc));
+  if (!w || !t || !h || !mm || (!c_units && !c)) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  return gemm_1x2_dev_impl(*st, w, m, gamma, t, h, mm, n, k, wpr, a_scale, has_a_gamma, a_gamma,
+                           row_scale, col_scale, c_units, c, ldc, static_cast<cudaStream_t>(stream));
+}
+
+int bitmm_gemm_1x2_host(const uint64_t* w, int64_t m, float gamma, const uint64_t* t,
+                        const uint64_t* h, const uint64_t* mm, int64_t n, int64_t k, int64_t wpr,
+                        float a_scale, int has_a_gamma, float a_gamma, const float* row_scale,
+                        const float* col_scale, int32_t* c_units, float* c, int64_t ldc) {
+  g_launches = 0;
+  // ThmPlanes::validate runs first in the reference (kernels.cpp:186): scale, then legality.
+  if (!(a_scale > 0.0f)) return fail(BITMM_ERR_INVALID_ENCODING, "plane scale must be positive");
+  if (!t || !h || !mm || !w || (!c_units && !c)) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  cudaStream_t s = st->stream;
+  const int rc_dims = check_gemm_dims(m, n, k, wpr, ldc);
+  const std::string dims_msg = g_err;
+  const bool planes_ok_shape = n >= 0 && k >= 0 && wpr >= 0 && wpr * 64 >= k;
+  const size_t p_bytes = (planes_ok_shape ? n * wpr * 8 : 0), w_bytes = (rc_dims == BITMM_OK ? m * wpr * 8 : 0);
+  const size_t c_bytes = (rc_dims == BITMM_OK ? m * ldc * 4 : 0);
+  BITMM_TRY(arena_reserve(st->io, 3 * align_up(p_bytes, 1024) + align_up(w_bytes, 1024) +
+                                      2 * align_up(c_bytes, 1024) + align_up(m > 0 ? m * 4 : 0, 1024) +
+                                      align_up(n > 0 ? n * 4 : 0, 1024) + 4096));
+  Carve cv(st->io.ptr);
+  uint64_t* dt = cv.take<uint64_t>(p_bytes);
+  uint64_t* dh = cv.take<uint64_t>(p_bytes);
+  uint64_t* dm = cv.take<uint64_t>(p_bytes);
+  if (p_bytes) {
+    BITMM_CUDA_TRY(cudaMemcpyAsync(dt, t, p_bytes, cudaMemcpyHostToDevice, s));
+    BITMM_CUDA_TRY(cudaMemcpyAsync(dh, h, p_bytes, cudaMemcpyHostToDevice, s));
+    BITMM_CUDA_TRY(cudaMemcpyAsync(dm, mm, p_bytes, cudaMemcpyHostToDevice, s));
+  }
+  if (rc_dims != BITMM_OK) {
+    // plane legality still wins over shape errors (reference precedence)
+    if (planes_ok_shape && n > 0 && k > 0) {
+      const int64_t kpad = round_up(k, TC_BK_BYTES);
+      BITMM_TRY(arena_reserve(st->ws, align_up(n * kpad, 1024) + 1024));
+      BITMM_TRY(run_unpack_level_i8(dt, dh, dm, n, wpr, k, kpad, static_cast<uint8_t*>(st->ws.ptr), st->status, s));
+      BITMM_TRY(read_status(*st, s));
+    }
+    return fail(rc_dims, dims_msg);
+  }
+  uint64_t* dw = cv.take<uint64_t>(w_bytes);
+  float* drs = row_scale ? cv.take<float>(m * 4) : nullptr;
+  float* dcs = col_scale ? cv.take<float>(n * 4) : nullptr;
+  int32_t* dcu = c_units ? cv.take<int32_t>(c_bytes) : nullptr;
+  float* dc = c ? cv.take<float>(c_bytes) : nullptr;
+  BITMM_CUDA_TRY(cudaMemcpyAsync(dw, w, w_bytes, cudaMemcpyHostToDevice, s));
+  if (drs) BITMM_CUDA_TRY(cudaMemcpyAsync(drs, row_scale, m * 4, cudaMemcpyHostToDevice, s));
+  if (dcs) BITMM_CUDA_TRY(cudaMemcpyAsync(dcs, col_scale, n * 4, cudaMemcpyHostToDevice, s));
+  BITMM_TRY(gemm_1x2_dev_impl(*st, dw, m, gamma, dt, dh, dm, n, k, wpr, a_scale, has_a_gamma,
+                              a_gamma, drs, dcs, dcu, dc, ldc, s));
+  if (dcu) BITMM_CUDA_TRY(cudaMemcpyAsync(c_units, dcu, c_bytes, cudaMemcpyDeviceToHost, s));
+  if (dc) BITMM_CUDA_TRY(cudaMemcpyAsync(c, dc, c_bytes, cudaMemcpyDeviceToHost, s));
+  return read_status(*st, s);
+}
+
+// ---------------- 2/2 ----------------
+int bitmm_gemm_2x2_dev(const uint64_t* wt, const uint64_t* wh, const uint64_t* wm, int64_t m,
+                       float w_scale, int has_w_gamma, float w_gamma, const uint64_t* at,
+                       const uint64_t* ah, const uint64_t* am, int64_t n, int64_t k, int64_t wpr,
+                       float a_scale, int has_a_gamma, float a_gamma, const float* row_scale,
+                       const float* col_scale, int32_t* c_units, float* c, int64_t ldc,
+                       void* stream) {
+  g_launches = 0;
+  if (!(w_scale > 0.0f) || !(a_scale > 0.0f))
+    return fail(BITMM_ERR_INVALID_ENCODING, "plane scale must be positive");
+  BITMM_TRY(check_gemm_dims(m, n, k, wpr, ldc));
+  if (!wt || !wh || !wm || !at || !ah || !am || (!c_units && !c))
+    return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  return gemm_2x2_dev_impl(*st, wt, wh, wm, m, w_scale, has_w_gamma, w_gamma, at, ah, am, n, k,
+                           wpr, a_scale, has_a_gamma, a_gamma, row_scale, col_scale, c_units, c,
+                           ldc, static_cast<cudaStream_t>(stream));
+}
+
+int bitmm_gemm_2x2_host(const uint64_t* wt, const uint64_t* wh, const uint64_t* wm, int64_t m,
+                        float w_scale, int has_w_gamma, float w_gamma, const uint64_t* at,
+                        const uint64_t* ah, const uint64_t* am, int64_t n, int64_t k, int64_t wpr,
+                        float a_scale, int has_a_gamma, float a_gamma, const float* row_scale,
+                        const float* col_scale, int32_t* c_units, float* c, int64_t ldc) {
+  g_launches = 0;
+  // w.validate(); a_packed.validate(); then shapes (kernels.cpp:224-228)
+  if (!(w_scale > 0.0f) || !(a_scale > 0.0f))
+    return fail(BITMM_ERR_INVALID_ENCODING, "plane scale must be positive");
+  if (!wt || !wh || !wm || !at || !ah || !am || (!c_units && !c))
+    return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  cudaStream_t s = st->stream;
+  const int rc_dims = check_gemm_dims(m, n, k, wpr, ldc);
+  const std::string dims_msg = g_err;
+  const bool shape_ok = k >= 0 && wpr >= 0 && wpr * 64 >= k;
+  const size_t pw = (shape_ok && m > 0 ? m * wpr * 8 : 0), pa = (shape_ok && n > 0 ? n * wpr * 8 : 0);
+  const size_t c_bytes = (rc_dims == BITMM_OK ? m * ldc * 4 : 0);
+  BITMM_TRY(arena_reserve(st->io, 3 * align_up(pw, 1024) + 3 * align_up(pa, 1024) +
+                                      2 * align_up(c_bytes, 1024) + align_up(m > 0 ? m * 4 : 0, 1024) +
+                                      align_up(n > 0 ? n * 4 : 0, 1024) + 4096));
+  Carve cv(st->io.ptr);
+  uint64_t* d[6];
+  const uint64_t* src[6] = {wt, wh, wm, at, ah, am};
+  for (int i = 0; i < 6; ++i) {
+    const size_t bytes = i < 3 ? pw : pa;
+    d[i] = cv.take<uint64_t>(bytes);
+    if (bytes) BITMM_CUDA_TRY(cudaMemcpyAsync(d[i], src[i], bytes, cudaMemcpyHostToDevice, s));
+  }
+  if (rc_dims != BITMM_OK) {
+    if (shape_ok && k > 0) {
+      const int64_t kpad = round_up(k, TC_BK_BYTES);
+      BITMM_TRY(arena_reserve(st->ws, align_up(std::max<int64_t>(m, n) * kpad, 1024) + 1024));
+      if (m > 0) BITMM_TRY(run_unpack_level_i8(d[0], d[1], d[2], m, wpr, k, kpad, static_cast<uint8_t*>(st->ws.ptr), st->status, s));
+      if (n > 0) BITMM_TRY(run_unpack_level_i8(d[3], d[4], d[5], n, wpr, k, kpad, static_cast<uint8_t*>(st->ws.ptr), st->status, s));
+      BITMM_TRY(read_status(*st, s));
+    }
+    return fail(rc_dims, dims_msg);
+  }
+  float* drs = row_scale ? cv.take<float>(m * 4) : nullptr;
+  float* dcs = col_scale ? cv.take<float>(n * 4) : nullptr;
+  int32_t* dcu = c_units ? cv.take<int32_t>(c_bytes) : nullptr;
+  float* dc = c ? cv.take<float>(c_bytes) : nullptr;
+  if (drs) BITMM_CUDA_TRY(cudaMemcpyAsync(drs, row_scale, m * 4, cudaMemcpyHostToDevice, s));
+  if (dcs) BITMM_CUDA_TRY(cudaMemcpyAsync(dcs, col_scale, n * 4, cudaMemcpyHostToDevice, s));
+  BITMM_TRY(gemm_2x2_dev_impl(*st, d[0], d[1], d[2], m, w_scale, has_w_gamma, w_gamma, d[3], d[4],
+                              d[5], n, k, wpr, a_scale, has_a_gamma, a_gamma, drs, dcs, dcu, dc,
+                              ldc, s));
+  if (dcu) BITMM_CUDA_TRY(cudaMemcpyAsync(c_units, dcu, c_bytes, cudaMemcpyDeviceToHost, s));
+  if (dc) BITMM_CUDA_TRY(cudaMemcpyAsync(c, dc, c_bytes, cudaMemcpyDeviceToHost, s));
+  return read_status(*st, s);
+}
+
+// ---------------- 1/32 and APB ----------------
+static int check_1x32_dims(int64_t m, int64_t k, int64_t wpr, int64_t n, int64_t ldb, int64_t ldc) {
+  if (m <= 0 || k <= 0 || n <= 0) return fail(BITMM_ERR_INVALID_ARGUMENT, "gemm dimensions must be positive");
+  if (k > BITMM_MAX_SHARED_DIM)
+    return fail(BITMM_ERR_INVALID_ARGUMENT, "shared dimension exceeds the 2^20 accumulator bound");
+  if (wpr * 64 < k) return fail(BITMM_ERR_INVALID_ARGUMENT, "words_per_row too small for the column count");
+  if (ldb < n || ldc < n) return fail(BITMM_ERR_INVALID_ARGUMENT, "leading dimension smaller than the column count");
+  if (m > INT32_MAX / 2 || n > INT32_MAX / 2) return fail(BITMM_ERR_INVALID_ARGUMENT, "gemm dimension too large");
+  return BITMM_OK;
+}
+
+int bitmm_gemm_1x32_dev(const uint64_t* w, int64_t m, int64_t k, int64_t wpr, float gamma,
+                        const float* row_gamma, const float* b, int64_t n, int64_t ldb, float* c,
+                        int64_t ldc, void* stream) {
+  g_launches = 0;
+  BITMM_TRY(check_1x32_dims(m, k, wpr, n, ldb, ldc));
+  if (!w || !b || !c) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  return apb_dev_impl(*st, w, m, k, wpr, gamma, row_gamma, b, n, ldb, nullptr, nullptr, nullptr, c,
+                      ldc, static_cast<cudaStream_t>(stream));
+}
+
+int bitmm_gemm_1x32_host(const uint64_t* w, int64_t m, int64_t k, int64_t wpr, float gamma,
+                         const float* row_gamma, const float* b, int64_t n, int64_t ldb, float* c,
+                         int64_t ldc) {
+  g_launches = 0;
+  BITMM_TRY(check_1x32_dims(m, k, wpr, n, ldb, ldc));
+  if (!w || !b || !c) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  cudaStream_t s = st->stream;
+  const size_t w_bytes = m * wpr * 8, b_bytes = k * ldb * 4, c_bytes = m * ldc * 4;
+  BITMM_TRY(arena_reserve(st->io, align_up(w_bytes, 1024) + align_up(b_bytes, 1024) +
+                                      align_up(c_bytes, 1024) + align_up(m * 4, 1024) + 4096));
+  Carve cv(st->io.ptr);
+  uint64_t* dw = cv.take<uint64_t>(w_bytes);
+  float* db = cv.take<float>(b_bytes);
+  float* dc = cv.take<float>(c_bytes);
+  float* dg = row_gamma ? cv.take<float>(m * 4) : nullptr;
+  BITMM_CUDA_TRY(cudaMemcpyAsync(dw, w, w_bytes, cudaMemcpyHostToDevice, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(db, b, b_bytes, cudaMemcpyHostToDevice, s));
+  if (dg) BITMM_CUDA_TRY(cudaMemcpyAsync(dg, row_gamma, m * 4, cudaMemcpyHostToDevice, s));
+  BITMM_TRY(apb_dev_impl(*st, dw, m, k, wpr, gamma, dg, db, n, ldb, nullptr, nullptr, nullptr, dc, ldc, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(c, dc, c_bytes, cudaMemcpyDeviceToHost, s));
+  return read_status(*st, s);
+}
+
+int bitmm_layer_forward_dev(int64_t rows, int64_t cols, float alpha, const float* row_alpha,
+                            const uint64_t* bin, int64_t wpr, const uint64_t* row_ptr,
+                            const uint64_t* col_idx, const float* vals, const float* b, int64_t n,
+                            int64_t ldb, float* c, int64_t ldc, void* stream) {
+  g_launches = 0;
+  BITMM_TRY(check_1x32_dims(rows, cols, wpr, n, ldb, ldc));
+  if (!bin || !b || !c || !row_ptr) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  return apb_dev_impl(*st, bin, rows, cols, wpr, alpha, row_alpha, b, n, ldb, row_ptr, col_idx, vals,
+                      c, ldc, static_cast<cudaStream_t>(stream));
+}
+
+int bitmm_layer_forward_host(int64_t rows, int64_t cols, float alpha, const float* row_alpha,
+                             const uint64_t* bin, int64_t wpr, const uint64_t* row_ptr,
+                             const uint64_t* col_idx, const float* vals, int64_t nnz,
+                             const float* b, int64_t n, int64_t ldb, float* c, int64_t ldc) {
+  g_launches = 0;
+  BITMM_TRY(check_1x32_dims(rows, cols, wpr, n, ldb, ldc));
+  if (!bin || !b || !c || !row_ptr || (nnz > 0 && (!col_idx || !vals)))
+    return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  BITMM_TRY(check_csr_host(rows, cols, row_ptr, col_idx, vals, nnz));
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  cudaStream_t s = st->stream;
+  const size_t w_bytes = rows * wpr * 8, b_bytes = cols * ldb * 4, c_bytes = rows * ldc * 4;
+  const size_t rp_bytes = (rows + 1) * 8, ci_bytes = std::max<int64_t>(nnz, 1) * 8,
+               v_bytes = std::max<int64_t>(nnz, 1) * 4;
+  BITMM_TRY(arena_reserve(st->io, align_up(w_bytes, 1024) + align_up(b_bytes, 1024) +
+                                      align_up(c_bytes, 1024) + align_up(rows * 4, 1024) +
+                                      align_up(rp_bytes, 1024) + align_up(ci_bytes, 1024) +
+                                      align_up(v_bytes, 1024) + 4096));
+  Carve cv(st->io.ptr);
+  uint64_t* dw = cv.take<uint64_t>(w_bytes);
+  float* db = cv.take<float>(b_bytes);
+  float* dc = cv.take<float>(c_bytes);
+  float* da = row_alpha ? cv.take<float>(rows * 4) : nullptr;
+  uint64_t* drp = cv.take<uint64_t>(rp_bytes);
+  uint64_t* dci = cv.take<uint64_t>(ci_bytes);
+  float* dv = cv.take<float>(v_bytes);
+  BITMM_CUDA_TRY(cudaMemcpyAsync(dw, bin, w_bytes, cudaMemcpyHostToDevice, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(db, b, b_bytes, cudaMemcpyHostToDevice, s));
+  if (da) BITMM_CUDA_TRY(cudaMemcpyAsync(da, row_alpha, rows * 4, cudaMemcpyHostToDevice, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(drp, row_ptr, rp_bytes, cudaMemcpyHostToDevice, s));
+  if (nnz > 0) {
+    BITMM_CUDA_TRY(cudaMemcpyAsync(dci, col_idx, nnz * 8, cudaMemcpyHostToDevice, s));
+    BITMM_CUDA_TRY(cudaMemcpyAsync(dv, vals, nnz * 4, cudaMemcpyHostToDevice, s));
+  }
+  BITMM_TRY(apb_dev_impl(*st, dw, rows, cols, wpr, alpha, da, db, n, ldb, drp, dci, dv, dc, ldc, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(c, dc, c_bytes, cudaMemcpyDeviceToHost, s));
+  return read_status(*st, s);
+}
+
+// ---------------- standalone SpMM ----------------
+int bitmm_spmm_csr_dev(int64_t rows, int64_t cols, const uint64_t* row_ptr, const uint64_t* col_idx,
+                       const float* vals, const float* b, int64_t n, int64_t ldb, float* c,
+                       int64_t ldc, void* stream) {
+  g_launches = 0;
+  // kernels.cpp:335-338
+  if (rows <= 0 || n <= 0 || cols <= 0) return fail(BITMM_ERR_INVALID_ARGUMENT, "gemm dimensions must be positive");
+  if (cols > BITMM_MAX_SHARED_DIM)
+    return fail(BITMM_ERR_INVALID_ARGUMENT, "shared dimension exceeds the 2^20 accumulator bound");
+  if (ldb < n || ldc < n) return fail(BITMM_ERR_INVALID_ARGUMENT, "leading dimension smaller than the column count");
+  if (!row_ptr || !b || !c) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  const long long warps = rows * ((n + 127) / 128);
+  spmm_csr_kernel<<<blocks_for(warps * 32, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      rows, reinterpret_cast<const unsigned long long*>(row_ptr),
+      reinterpret_cast<const unsigned long long*>(col_idx), vals, b, ldb, static_cast<int>(n), c,
+      ldc);
+  return launch_check("spmm_csr_kernel");
+}
+
+int bitmm_spmm_csr_host(int64_t rows, int64_t cols, const uint64_t* row_ptr,
+                        const uint64_t* col_idx, const float* vals, int64_t nnz, const float* b,
+                        int64_t n, int64_t ldb, float* c, int64_t ldc) {
+  g_launches = 0;
+  if (rows <= 0 || n <= 0 || cols <= 0) return fail(BITMM_ERR_INVALID_ARGUMENT, "gemm dimensions must be positive");
+  if (cols > BITMM_MAX_SHARED_DIM)
+    return fail(BITMM_ERR_INVALID_ARGUMENT, "shared dimension exceeds the 2^20 accumulator bound");
+  if (ldb < n || ldc < n) return fail(BITMM_ERR_INVALID_ARGUMENT, "leading dimension smaller than the column count");
+  if (!row_ptr || !b || !c || (nnz > 0 && (!col_idx || !vals))) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  BITMM_TRY(check_csr_host(rows, cols, row_ptr, col_idx, vals, nnz));
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  cudaStream_t s = st->stream;
+  const size_t b_bytes = cols * ldb * 4, c_bytes = rows * ldc * 4, rp_bytes = (rows + 1) * 8;
+  const size_t ci_bytes = std::max<int64_t>(nnz, 1) * 8, v_bytes = std::max<int64_t>(nnz, 1) * 4;
+  BITMM_TRY(arena_reserve(st->io, align_up(b_bytes, 1024) + align_up(c_bytes, 1024) +
+                                      align_up(rp_bytes, 1024) + align_up(ci_bytes, 1024) +
+                                      align_up(v_bytes, 1024) + 4096));
+  Carve cv(st->io.ptr);
+  float* db = cv.take<float>(b_bytes);
+  float* dc = cv.take<float>(c_bytes);
+  uint64_t* drp = cv.take<uint64_t>(rp_bytes);
+  uint64_t* dci = cv.take<uint64_t>(ci_bytes);
+  float* dv = cv.take<float>(v_bytes);
+  BITMM_CUDA_TRY(cudaMemcpyAsync(db, b, b_bytes, cudaMemcpyHostToDevice, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(drp, row_ptr, rp_bytes, cudaMemcpyHostToDevice, s));
+  if (nnz > 0) {
+    BITMM_CUDA_TRY(cudaMemcpyAsync(dci, col_idx, nnz * 8, cudaMemcpyHostToDevice, s));
+    BITMM_CUDA_TRY(cudaMemcpyAsync(dv, vals, nnz * 4, cudaMemcpyHostToDevice, s));
+  }
+  BITMM_TRY(bitmm_spmm_csr_dev(rows, cols, drp, dci, dv, db, n, ldb, dc, ldc, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(c, dc, c_bytes, cudaMemcpyDeviceToHost, s));
+  BITMM_CUDA_TRY(cudaStreamSynchronize(s));
+  return BITMM_OK;
+}
+
+}  // extern "C"

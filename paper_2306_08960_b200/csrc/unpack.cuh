@@ -1,0 +1,167 @@
+// Operand expansion: reference packed layouts -> tensor-core operand rows.
+//
+// Input layouts are exactly the reference's (proj/include/bitmm/tensor.hpp:59-112):
+// row-major uint64 words, bit i of a row in word i/64 at position i%64, padded to
+// words_per_row (512-bit lanes by default) with zero padding. Read as uint32 the
+// order is unchanged on little-endian (element i -> u32 i/32, bit i%32).
+//
+// Outputs are K-major operand rows padded to kpad elements with zeros, so the
+// padding never contributes to a product:
+//   unpack_sign_i8   : bit b -> int8 (2b-1)               (BitMatrix, tensor.hpp:59)
+//   unpack_level_i8  : planes {t,h,m} -> int8 level p      (ThmPlanes, tensor.hpp:134;
+//                      legal states per transform.cpp:47-75: p0=(0,0,1) p1=(0,0,0)
+//                      p2=(0,1,0) p3=(1,0,1), so p = 2(t|h) + (t | ~(h|m)))
+//   unpack_sign_bf16 : bit b -> bf16 (+1/-1)               (APB binary plane)
+//   split_x_bf16     : fp32 X[K][N] -> bf16 parts XT[N][part*kpad + k] with
+//                      x = hi + mid + lo exactly (3 parts) — transposed to K-major.
+// Validation folded into the same pass (the reference checks these on the host,
+// tensor.cpp:78-89 and tensor.cpp:133-153): nonzero padding of a BitMatrix sets
+// ERR_PADDING, an illegal plane triple or nonzero plane padding sets ERR_ENCODING.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cstdint>
+
+namespace bitmm_dev {
+
+constexpr int ERR_PADDING = 1;
+constexpr int ERR_ENCODING = 2;
+
+// 4 bits -> 4 bytes holding 0/1 (no carries: the shifted copies never overlap).
+__device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
+
+__device__ __forceinline__ uint32_t valid_mask32(int kbase, int K) {
+  if (kbase + 32 <= K) return 0xFFFFFFFFu;
+  if (kbase >= K) return 0u;
+  return (1u << (K - kbase)) - 1u;
+}
+
+// One thread per (row, 32-element group). Groups beyond kpad only validate padding.
+__global__ void unpack_sign_i8(const uint32_t* __restrict__ words, long long rows, int wpr32, int K,
+                               int kpad, uint8_t* __restrict__ out, int* __restrict__ err) {
+  const int groups_out = kpad / 32;
+  const int groups = max(groups_out, wpr32);
+  const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (gid >= rows * groups) return;
+  const long long r = gid / groups;
+  const int g = static_cast<int>(gid - r * groups);
+  const uint32_t w = (g < wpr32) ? words[r * wpr32 + g] : 0u;
+  const uint32_t valid = valid_mask32(g * 32, K);
+  if (w & ~valid) atomicOr(err, ERR_PADDING);
+  if (g >= groups_out) return;
+  uint32_t o[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint32_t b = spread4((w >> (4 * q)) & 0xFu);
+    const uint32_t vm = spread4((valid >> (4 * q)) & 0xFu);
+    o[q] = ((b * 0xFEu) ^ 0xFFFFFFFFu) & (vm * 0xFFu);  // 1 -> 0x01, 0 -> 0xFF, pad -> 0
+  }
+  uint4* dst = reinterpret_cast<uint4*>(out + r * kpad + g * 32);
+  dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+  dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+}
+
+__global__ void unpack_level_i8(const uint32_t* __restrict__ t, const uint32_t* __restrict__ h,
+                                const uint32_t* __restrict__ m, long long rows, int wpr32, int K,
+                                int kpad, uint8_t* __restrict__ out, int* __restrict__ err) {
+  const int groups_out = kpad / 32;
+  const int groups = max(groups_out, wpr32);
+  const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (gid >= rows * groups) return;
+  const long long r = gid / groups;
+  const int g = static_cast<int>(gid - r * groups);
+  uint32_t tw = 0, hw = 0, mw = 0;
+  if (g < wpr32) {
+    tw = t[r * wpr32 + g];
+    hw = h[r * wpr32 + g];
+    mw = m[r * wpr32 + g];
+  }
+  const uint32_t valid = valid_mask32(g * 32, K);
+  if (((tw | hw | mw) & ~valid) | (tw & hw) | (tw & ~mw) | (hw & mw)) atomicOr(err, ERR_ENCODING);
+  if (g >= groups_out) return;
+  const uint32_t hi = (tw | hw) & valid;
+  const uint32_t lo = (tw | ~(hw | mw)) & valid;
+  uint32_t o[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    o[q] = (spread4((hi >> (4 * q)) & 0xFu) << 1) + spread4((lo >> (4 * q)) & 0xFu);
+  }
+  uint4* dst = reinterpret_cast<uint4*>(out + r * kpad + g * 32);
+  dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+  dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+}
+
+__global__ void unpack_sign_bf16(const uint32_t* __restrict__ words, long long rows, int wpr32,
+                                 int K, int kpad, uint16_t* __restrict__ out,
+                                 int* __restrict__ err) {
+  const int groups_out = kpad / 32;
+  const int groups = max(groups_out, wpr32);
+  const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (gid >= rows * groups) return;
+  const long long r = gid / groups;
+  const int g = static_cast<int>(gid - r * groups);
+  const uint32_t w = (g < wpr32) ? words[r * wpr32 + g] : 0u;
+  const uint32_t valid = valid_mask32(g * 32, K);
+  if (w & ~valid) atomicOr(err, ERR_PADDING);
+  if (g >= groups_out) return;
+  uint32_t o[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const uint32_t b0 = (w >> (2 * q)) & 1u, b1 = (w >> (2 * q + 1)) & 1u;
+    const uint32_t v0 = (valid >> (2 * q)) & 1u, v1 = (valid >> (2 * q + 1)) & 1u;
+    const uint32_t e0 = v0 ? (b0 ? 0x3F80u : 0xBF80u) : 0u;  // +1.0 / -1.0 bf16
+    const uint32_t e1 = v1 ? (b1 ? 0x3F80u : 0xBF80u) : 0u;
+    o[q] = e0 | (e1 << 16);
+  }
+  uint4* dst = reinterpret_cast<uint4*>(out + r * kpad + g * 32);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) dst[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+}
+
+// X [K][ldx] fp32 -> XT [N][nparts*kpad] bf16, part p at column offset p*kpad.
+// Block = 256 threads, tile 64 k x 32 n; reads coalesced along n, writes 128 B
+// segments along k per part.
+__global__ void split_x_bf16(const float* __restrict__ X, long long ldx, int K, int N, int kpad,
+                             int nparts, uint16_t* __restrict__ XT) {
+  __shared__ float tile[64][33];
+  const int k0 = blockIdx.x * 64;
+  const int n0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int k = k0 + ty + 8 * i;
+    const int n = n0 + tx;
+    tile[ty + 8 * i][tx] = (k < K && n < N) ? X[static_cast<long long>(k) * ldx + n] : 0.0f;
+  }
+  __syncthreads();
+  const int nl = threadIdx.x >> 3;        // 0..31
+  const int kl = (threadIdx.x & 7) * 8;   // 0..56
+  const int n = n0 + nl;
+  if (n >= N) return;
+  uint32_t parts[3][4];
+#pragma unroll
+  for (int e = 0; e < 8; e += 2) {
+    uint32_t pe[3][2];
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+      float x = tile[kl + e + d][nl];
+      const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+      const float r1 = x - __bfloat162float(hi);
+      const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+      const float r2 = r1 - __bfloat162float(mid);
+      const __nv_bfloat16 lo = __float2bfloat16_rn(r2);
+      pe[0][d] = __bfloat16_as_ushort(hi);
+      pe[1][d] = __bfloat16_as_ushort(mid);
+      pe[2][d] = __bfloat16_as_ushort(lo);
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) parts[q][e / 2] = pe[q][0] | (pe[q][1] << 16);
+  }
+  const long long row_off = static_cast<long long>(n) * nparts * kpad;
+  for (int q = 0; q < nparts; ++q) {
+    uint4* dst = reinterpret_cast<uint4*>(XT + row_off + static_cast<long long>(q) * kpad + k0 + kl);
+    *dst = make_uint4(parts[q][0], parts[q][1], parts[q][2], parts[q][3]);
+  }
+}
+
+}  // namespace bitmm_dev
