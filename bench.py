@@ -1,0 +1,536 @@
+#!/usr/bin/env python
+"""bench.py — B200 bitwise-GEMM hot path (arXiv 2306.08960: 1/1, 1/2, 2/2).
+
+One step = one pass of BASELINE.json configs 0-2 over synthetic seeded operands in the
+reference's packed layouts (the metric "binary GEMM Tera-updates/s ... 1/1.1/2.2/2"):
+    1/1  M=N=K=4096                       int32 units out          (configs[0])
+    1/2  binary weights 4096 x K=4096 x 2-bit activations 8192,
+         per-row gamma and per-column beta, fp32 out (reference orientation; configs[2])
+    2/2  M=N=K=4096                       int32 units out          (configs[1])
+updates = M*K*N per GEMM (bench.cpp:175). Every step starts from the PACKED operands
+resident in HBM; the bit -> int8 expansion kernels are inside the timed region.
+
+With N>1 ranks (torchrun, NCCL) every GEMM's output-column dimension is sharded across
+ranks (rank g owns b_packed rows [g*N/G, (g+1)*N/G)), each rank computes its M x N/G
+block and the blocks are gathered to rank 0 over NCCL (the only collective); strong
+scaling. `--impl reference` times the reference CPU implementation instead (rank 0).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "binary GEMM Tera-updates/s and % of B200 int-op roofline, 1/1·1/2·2/2"
+UNIT = "T-updates/s"
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+SEED = 2306_08960
+
+ROUTINES = [  # name, m (output rows), n (output columns), k
+    ("1x1", 4096, 4096, 4096),
+    ("1x2", 4096, 8192, 4096),
+    ("2x2", 4096, 4096, 4096),
+]
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- operands
+def make_operands(rng):
+    """Packed host operands for the three GEMMs (reference layouts, numpy)."""
+    from paper_2306_08960_b200 import data
+    ops = {}
+    m, n, k = ROUTINES[0][1:]
+    ops["1x1"] = dict(a=data.random_words(rng, m, k)[0], b=data.random_words(rng, n, k)[0])
+    m, n, k = ROUTINES[1][1:]
+    t, h, mm, _ = data.random_planes(rng, n, k)
+    ops["1x2"] = dict(w=data.random_words(rng, m, k)[0], t=t, h=h, m=mm,
+                      gamma=rng.uniform(0.5, 1.5, m).astype(np.float32),
+                      beta=rng.uniform(0.5, 1.5, n).astype(np.float32))
+    m, n, k = ROUTINES[2][1:]
+    wt, wh, wm, _ = data.random_planes(rng, m, k)
+    at, ah, am, _ = data.random_planes(rng, n, k)
+    ops["2x2"] = dict(wt=wt, wh=wh, wm=wm, at=at, ah=ah, am=am)
+    return ops
+
+
+def shard_cols(n, rank, world):
+    per = (n + world - 1) // world
+    lo = min(n, rank * per)
+    return lo, min(n, lo + per)
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index=0):
+        self.idx = device_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- peaks
+def measured_peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d, "MEASURED_PEAKS.json"
+    except (OSError, ValueError):
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
+
+
+def int8_peak_probe(torch):
+    """cuBLASLt int8 GEMM (torch._int_mm) 8192^3, best of 5 — context for the int8 roofline."""
+    try:
+        n = 8192
+        a = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda")
+        b = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda").t()
+        for _ in range(2):
+            torch._int_mm(a, b)
+        best = 1e9
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return 2 * n ** 3 / (best * 1e-3) / 1e12
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- CPU side
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_reference_step(ops, threads, rows_sample):
+    """One pass of the three GEMMs through the unmodified reference (oracle/_ref), or the
+    oracle port when the reference library is absent. Returns (seconds, updates, kind)."""
+    import oracle
+    ref = oracle.load_ref()
+    kind = "reference" if ref is not None else "port"
+    secs, upd = 0.0, 0
+    for name, m, n, k in ROUTINES:
+        wpr = (k + 511) // 512 * 8
+        s = min(m, rows_sample)
+        o = ops[name]
+        if ref is not None:
+            if name == "1x1":
+                _, t = ref.gemm_1x1(o["a"][:s], o["b"], k, wpr, 1.0, 1.0, threads)
+            elif name == "1x2":
+                _, t = ref.gemm_1x2(o["w"][:s], 1.0, o["t"], o["h"], o["m"], k, wpr, 1.0, None, threads)
+            else:
+                _, t = ref.gemm_2x2(o["wt"][:s], o["wh"][:s], o["wm"][:s], o["at"], o["ah"], o["am"],
+                                    k, wpr, 1.0, 1.0, None, None, threads)
+        else:
+            orc = oracle.Oracle()
+            t0 = time.perf_counter()
+            if name == "1x1":
+                orc.gemm_1x1(o["a"][:s], o["b"], k, wpr)
+            elif name == "1x2":
+                orc.gemm_1x2(o["w"][:s], 1.0, o["t"], o["h"], o["m"], k, wpr)
+            else:
+                orc.gemm_2x2(o["wt"][:s], o["wh"][:s], o["wm"][:s], o["at"], o["ah"], o["am"], k, wpr)
+            t = time.perf_counter() - t0
+        secs += t
+        upd += s * n * k
+    return secs, upd, kind
+
+
+def pick_rows_sample(ops, threads, target_s):
+    """Rows of each routine's M to evaluate on the CPU so one step takes about target_s."""
+    probe = 32
+    secs, _, _ = cpu_reference_step(ops, threads, probe)
+    per_row = max(secs / probe, 1e-6)
+    return int(max(8, min(4096, target_s / per_row)))
+
+
+def run_reference_arm(args):
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    rng = np.random.default_rng(SEED)
+    ops = make_operands(rng)
+    threads = host_threads()
+    rows = pick_rows_sample(ops, threads, target_s=min(3.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_reference_step(ops, threads, rows)
+    secs, upd = 0.0, 0
+    kind = "reference"
+    for _ in range(args.steps):
+        s, u, kind = cpu_reference_step(ops, threads, rows)
+        secs += s
+        upd += u
+    value = upd / secs / 1e12
+    sample = (f"rows [0,{rows}) of each GEMM's M (full N and K) per step; reference time "
+              f"includes its output allocation (bench.cpp:129-153)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u64 bit-packed (int popcount)", "data": "synthetic",
+        "config": workload_config(args.gpus),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(world):
+    return {
+        "workload": "BASELINE configs 0-2 per step: 1/1 4096^3 (int32 out) + 1/2 binary 4096 x "
+                    "K 4096 x 2-bit 8192 with per-row gamma / per-column beta (fp32 out) + 2/2 "
+                    "4096^3 (int32 out); packed uint64 operands resident in HBM",
+        "routines": {r[0]: {"m": r[1], "n": r[2], "k": r[3]} for r in ROUTINES},
+        "updates_per_step": sum(m * n * k for _, m, n, k in ROUTINES),
+        "parallelism": f"N-shard x{world} + NCCL gather" if world > 1 else "single GPU",
+        "l2": "flushed between steps (256 MiB memset outside the per-step CUDA events)",
+        "seed": SEED,
+    }
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2306_08960_b200 import _lib, device
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local_rank = env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    lib = _lib.load()
+    dev = torch.device("cuda", local_rank)
+
+    rng = np.random.default_rng(SEED)
+    ops = make_operands(rng)
+    T = lambda x: torch.from_numpy(np.ascontiguousarray(x).view(np.int64)).to(dev)  # noqa: E731
+    Tf = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # noqa: E731
+
+    # device-resident packed operands; rank's column shard of every GEMM
+    d = {}
+    for name, m, n, k in ROUTINES:
+        lo, hi = shard_cols(n, rank, world)
+        o = ops[name]
+        if name == "1x1":
+            d[name] = dict(a=T(o["a"]), b=T(o["b"][lo:hi]))
+            d[name]["units"] = torch.empty((m, hi - lo), dtype=torch.int32, device=dev)
+        elif name == "1x2":
+            d[name] = dict(w=T(o["w"]), t=T(o["t"][lo:hi]), h=T(o["h"][lo:hi]), m=T(o["m"][lo:hi]),
+                           gamma=Tf(o["gamma"]), beta=Tf(o["beta"][lo:hi]))
+            d[name]["out"] = torch.empty((m, hi - lo), dtype=torch.float32, device=dev)
+        else:
+            d[name] = dict(wt=T(o["wt"]), wh=T(o["wh"]), wm=T(o["wm"]), at=T(o["at"][lo:hi]),
+                           ah=T(o["ah"][lo:hi]), am=T(o["am"][lo:hi]))
+            d[name]["units"] = torch.empty((m, hi - lo), dtype=torch.int32, device=dev)
+        d[name]["cols"] = (lo, hi)
+    gathered = {}
+    if world > 1 and rank == 0:
+        for name, m, n, k in ROUTINES:
+            dt = torch.float32 if name == "1x2" else torch.int32
+            gathered[name] = torch.empty((m, n), dtype=dt, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def run_routine(name, m, n, k):
+        x = d[name]
+        if name == "1x1":
+            device.gemm_1x1(x["a"], x["b"], k, units=x["units"])
+        elif name == "1x2":
+            device.gemm_1x2(x["w"], 1.0, x["t"], x["h"], x["m"], k, row_scale=x["gamma"],
+                            col_scale=x["beta"], out=x["out"])
+        else:
+            device.gemm_2x2(x["wt"], x["wh"], x["wm"], x["at"], x["ah"], x["am"], k, units=x["units"])
+        return device.launch_count()
+
+    def gather(name):
+        if world == 1:
+            return
+        src = d[name]["units"] if name != "1x2" else d[name]["out"]
+        n = [r for r in ROUTINES if r[0] == name][0][2]
+        parts = None
+        if rank == 0:
+            parts = []
+            for g in range(world):
+                lo, hi = shard_cols(n, g, world)
+                parts.append(torch.empty((src.shape[0], hi - lo), dtype=src.dtype, device=dev))
+        dist.gather(src, parts, dst=0)
+        if rank == 0:
+            for g, p in enumerate(parts):
+                lo, hi = shard_cols(n, g, world)
+                gathered[name][:, lo:hi].copy_(p)
+
+    def step(events):
+        launches = 0
+        events[0].record(stream)
+        for i, (name, m, n, k) in enumerate(ROUTINES):
+            launches += run_routine(name, m, n, k)
+            gather(name)
+            events[i + 1].record(stream)
+        return launches
+
+    for name, m, n, k in ROUTINES:
+        lo, hi = d[name]["cols"]
+        device.reserve_workspace(0, m, hi - lo, k)
+
+    # ---- warmup ----
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(ROUTINES) + 1)]
+    for _ in range(max(args.warmup, 0)):
+        flush.zero_()
+        step(ev)
+    device.status()
+    torch.cuda.synchronize()
+
+    # ---- timed region: exactly K steps, per-step events, L2 flushed between steps ----
+    sampler = ClockSampler(local_rank)
+    if rank == 0:
+        sampler.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(ROUTINES) + 1)]
+               for _ in range(args.steps)]
+    launches = 0
+    for s in range(args.steps):
+        flush.zero_()
+        launches += step(step_ev[s])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if rank == 0 else None
+    device.status()
+    per_routine_ms = {name: 0.0 for name, *_ in ROUTINES}
+    total_ms = 0.0
+    for evs in step_ev:
+        total_ms += evs[0].elapsed_time(evs[-1])
+        for i, (name, *_rest) in enumerate(ROUTINES):
+            per_routine_ms[name] += evs[i].elapsed_time(evs[i + 1])
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    upd_per_step = sum(m * n * k for _, m, n, k in ROUTINES)
+    value = upd_per_step / (ms_per_step * 1e-3) / 1e12
+
+    # ---- live roofline pass: library-internal events around every launch ----
+    lib.bitmm_profile_reset()
+    lib.bitmm_profile_enable(1)
+    for s in range(args.steps):
+        flush.zero_()
+        step(ev)
+    torch.cuda.synchronize()
+    lib.bitmm_profile_collect()
+    lib.bitmm_profile_enable(0)
+    kernels = {}
+    for i in range(lib.bitmm_profile_kernel_count()):
+        kernels[lib.bitmm_profile_kernel_name(i).decode()] = {
+            "launches": lib.bitmm_profile_kernel_launches(i), "ms": lib.bitmm_profile_kernel_ms(i)}
+
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+
+    peaks, peaks_src = measured_peaks()
+    probe = int8_peak_probe(torch)
+    peak_from_bf16 = 2.0 * float(peaks.get("bf16_tflops", 1590.0))
+    peak = max(peak_from_bf16, probe or 0.0)
+    peak_src = (f"int8 dense = 2 x bf16 burst of {peaks_src} ({peak_from_bf16:.1f})"
+                if peak == peak_from_bf16 else f"cuBLASLt int8 _int_mm 8192^3 burst ({probe:.1f})")
+    tc = kernels.get("tc_gemm_i8", {"launches": 0, "ms": 0.0})
+    macs_per_step = sum(m * (shard_cols(n, rank, world)[1] - shard_cols(n, rank, world)[0]) * k
+                        for _, m, n, k in ROUTINES)
+    achieved = (2.0 * macs_per_step * args.steps) / (tc["ms"] * 1e-3) / 1e12 if tc["ms"] else 0.0
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "traffic_r01.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("tc_gemm_i8_dram_bytes_per_launch")
+        except ValueError:
+            traffic = None
+    kernel_share = tc["ms"] / sum(v["ms"] for v in kernels.values()) if kernels else None
+
+    routines = {}
+    for name, m, n, k in ROUTINES:
+        ms = per_routine_ms[name] / args.steps
+        routines[name] = {"ms": ms, "T_updates_per_s": m * n * k / (ms * 1e-3) / 1e12,
+                          "frac_of_int8_peak": (2 * m * n * k / (ms * 1e-3) / 1e12) / peak}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "u64 bit-packed -> s8 tcgen05.mma kind::i8, s32 accumulate",
+        "data": "synthetic (seeded uniform words = i.i.d. Bernoulli(0.5) bits; uniform 2-bit codes)",
+        "config": workload_config(world),
+        "gpu_launches": launches,
+        "routines": routines,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak if peak else None, "traffic": traffic,
+                     "kernel": "tc_gemm_i8 (int8 tensor ops = 2 per MAC)", "peak_source": peak_src,
+                     "kernel_share_of_step": kernel_share, "int8_probe_tops": probe,
+                     "popc_roofline_T_updates_per_s": 148 * 16 * 32 * 1.965e9 / 1e12},
+        "kernels": kernels,
+        "clocks": clocks,
+    }
+
+    if world == 1 and not args.no_e2e:
+        line["e2e"] = e2e_pass(args, ops, torch, lib)
+    if world == 1 and not args.no_cpu_baseline:
+        threads = host_threads()
+        rows = pick_rows_sample(ops, threads, target_s=10.0)
+        secs, upd, kind = cpu_reference_step(ops, threads, rows)
+        line["cpu_baseline"] = {
+            "value": upd / secs / 1e12, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"one step restricted to rows [0,{rows}) of each GEMM's M (full N, K); "
+                      f"{secs:.1f} s of CPU time"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def e2e_pass(args, ops, torch, lib):
+    """The same step through the reference-facing host C ABI: pinned host inputs copied in,
+    results copied back to pinned host memory, inside the timed region (wall clock around
+    synchronous calls)."""
+    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory()  # noqa: E731
+    P = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    h = {}
+    h2d = d2h = 0
+    for name, m, n, k in ROUTINES:
+        o = ops[name]
+        h[name] = {kk: pin(v) for kk, v in o.items()}
+        dt = torch.float32 if name == "1x2" else torch.int32
+        h[name]["out"] = torch.empty((m, n), dtype=dt).pin_memory()
+        h2d += sum(v.numel() * v.element_size() for kk, v in h[name].items() if kk != "out")
+        d2h += m * n * 4
+
+    def call(name, m, n, k):
+        x = h[name]
+        wpr = (k + 511) // 512 * 8
+        if name == "1x1":
+            rc = lib.bitmm_gemm_1x1_host(P(x["a"]), m, P(x["b"]), n, k, wpr, 1.0, 1.0, P(x["out"]),
+                                         None, n)
+        elif name == "1x2":
+            rc = lib.bitmm_gemm_1x2_host(P(x["w"]), m, 1.0, P(x["t"]), P(x["h"]), P(x["m"]), n, k, wpr,
+                                         1.0, 0, 1.0, P(x["gamma"]), P(x["beta"]), None, P(x["out"]), n)
+        else:
+            rc = lib.bitmm_gemm_2x2_host(P(x["wt"]), P(x["wh"]), P(x["wm"]), m, 1.0, 0, 1.0, P(x["at"]),
+                                         P(x["ah"]), P(x["am"]), n, k, wpr, 1.0, 0, 1.0, None, None,
+                                         P(x["out"]), None, n)
+        if rc != 0:
+            raise RuntimeError(f"e2e {name}: {rc} {lib.bitmm_last_error().decode()}")
+
+    for _ in range(max(args.warmup, 1)):
+        for r in ROUTINES:
+            call(*r)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for r in ROUTINES:
+            call(*r)
+    secs = (time.perf_counter() - t0) / args.steps
+    upd = sum(m * n * k for _, m, n, k in ROUTINES)
+    return {"value": upd / secs / 1e12, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": secs * 1e3,
+            "path": "bitmm_gemm_{1x1,1x2,2x2}_host (include/bitmm_b200.h), pinned host buffers"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -67,6 +67,18 @@ size_t bitmm_workspace_bytes(int routine, int64_t m, int64_t n, int64_t k);
 /* Number of kernels launched by the most recent compute call on this thread. */
 int bitmm_last_launch_count(void);
 
+/* Stream-ordered kernel timing (used by bench.py for the roofline): while enabled, every
+ * kernel the library launches is bracketed by CUDA events on its launching stream.
+ * bitmm_profile_collect() synchronises those events and folds them into per-kernel totals
+ * readable by index; bitmm_profile_reset() clears them. */
+int bitmm_profile_enable(int on);
+int bitmm_profile_collect(void);
+int bitmm_profile_reset(void);
+int bitmm_profile_kernel_count(void);
+const char* bitmm_profile_kernel_name(int i);
+int bitmm_profile_kernel_launches(int i);
+double bitmm_profile_kernel_ms(int i);
+
 /* ---- 1/1: replaces gemm_1x1 (kernels.hpp:47-48, kernels.cpp:163-183) ----
  * C[r][c] = (gamma_a * gamma_b) * float(K - 2*popcount(a_r xor b_c)).
  * Writes int32 units to c_units and/or scaled floats to c (either may be NULL). */

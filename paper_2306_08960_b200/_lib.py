@@ -34,6 +34,13 @@ SIGNATURES = {
     "bitmm_reserve_workspace": (_i, [C.c_size_t]),
     "bitmm_workspace_bytes": (C.c_size_t, [_i, _i64, _i64, _i64]),
     "bitmm_last_launch_count": (_i, []),
+    "bitmm_profile_enable": (_i, [_i]),
+    "bitmm_profile_collect": (_i, []),
+    "bitmm_profile_reset": (_i, []),
+    "bitmm_profile_kernel_count": (_i, []),
+    "bitmm_profile_kernel_name": (C.c_char_p, [_i]),
+    "bitmm_profile_kernel_launches": (_i, [_i]),
+    "bitmm_profile_kernel_ms": (C.c_double, [_i]),
     "bitmm_gemm_1x1_dev": (_i, [_p, _i64, _p, _i64, _i64, _i64, _f, _f, _p, _p, _i64, _p]),
     "bitmm_gemm_1x1_host": (_i, [_p, _i64, _p, _i64, _i64, _i64, _f, _f, _p, _p, _i64]),
     "bitmm_gemm_1x1_popc_dev": (_i, [_p, _i64, _p, _i64, _i64, _i64, _f, _f, _p, _p, _i64, _p]),

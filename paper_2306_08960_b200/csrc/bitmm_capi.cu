@@ -9,6 +9,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "bitmm_b200.h"
 #include "popc_gemm.cuh"
@@ -135,6 +136,66 @@ int make_operand_map(CUtensorMap* map, const void* base, CUtensorMapDataType dt,
   return BITMM_OK;
 }
 
+// ---------------- stream-ordered kernel profiler ----------------
+struct ProfRecord {
+  int kernel;
+  cudaEvent_t e0, e1;
+};
+
+struct Profiler {
+  std::mutex mu;
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<ProfRecord> pending;
+  std::vector<std::string> names;
+  std::vector<int> launches;
+  std::vector<double> ms;
+
+  int id(const char* name) {
+    for (size_t i = 0; i < names.size(); ++i)
+      if (names[i] == name) return static_cast<int>(i);
+    names.emplace_back(name);
+    launches.push_back(0);
+    ms.push_back(0.0);
+    return static_cast<int>(names.size() - 1);
+  }
+  cudaEvent_t take() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+
+Profiler g_prof;
+
+// Brackets one kernel launch with events on its stream when profiling is enabled.
+class ProfScope {
+ public:
+  ProfScope(const char* name, cudaStream_t s) : name_(name), s_(s) {
+    if (!g_prof.on) return;
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    e0_ = g_prof.take();
+    e1_ = g_prof.take();
+    cudaEventRecord(e0_, s_);
+  }
+  ~ProfScope() {
+    if (!e0_) return;
+    cudaEventRecord(e1_, s_);
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.pending.push_back({g_prof.id(name_), e0_, e1_});
+  }
+
+ private:
+  const char* name_;
+  cudaStream_t s_;
+  cudaEvent_t e0_ = nullptr, e1_ = nullptr;
+};
+
 // ---------------- launches ----------------
 int launch_check(const char* what) {
   cudaError_t e = cudaGetLastError();
@@ -152,6 +213,7 @@ int run_unpack_sign_i8(const uint64_t* words, int64_t rows, int64_t wpr, int64_t
   const int wpr32 = static_cast<int>(wpr * 2);
   const long long total = rows * std::max<long long>(kpad / 32, wpr32);
   if (total == 0) return BITMM_OK;
+  ProfScope ps("unpack_sign_i8", s);
   unpack_sign_i8<<<blocks_for(total, 256), 256, 0, s>>>(reinterpret_cast<const uint32_t*>(words),
                                                         rows, wpr32, static_cast<int>(k),
                                                         static_cast<int>(kpad), out, flag);
@@ -164,6 +226,7 @@ int run_unpack_level_i8(const uint64_t* t, const uint64_t* h, const uint64_t* m,
   const int wpr32 = static_cast<int>(wpr * 2);
   const long long total = rows * std::max<long long>(kpad / 32, wpr32);
   if (total == 0) return BITMM_OK;
+  ProfScope ps("unpack_level_i8", s);
   unpack_level_i8<<<blocks_for(total, 256), 256, 0, s>>>(
       reinterpret_cast<const uint32_t*>(t), reinterpret_cast<const uint32_t*>(h),
       reinterpret_cast<const uint32_t*>(m), rows, wpr32, static_cast<int>(k),
@@ -171,21 +234,34 @@ int run_unpack_level_i8(const uint64_t* t, const uint64_t* h, const uint64_t* m,
   return launch_check("unpack_level_i8");
 }
 
-template <Kind KIND, Epi EPI>
+template <Kind KIND, Epi EPI, bool PAIR>
 int run_tc_gemm(DeviceState& st, const CUtensorMap& ta, const CUtensorMap& tb, TcParams p,
                 cudaStream_t s) {
-  constexpr unsigned bit = 1u << (static_cast<int>(KIND) * 3 + static_cast<int>(EPI));
+  using S = TcShape<PAIR>;
+  auto kern = tc_gemm_kernel<KIND, EPI, PAIR>;
+  constexpr unsigned bit = 1u << (static_cast<int>(KIND) * 6 + static_cast<int>(EPI) * 2 + (PAIR ? 1 : 0));
   if (!(st.attr_mask & bit)) {
-    BITMM_CUDA_TRY(cudaFuncSetAttribute(tc_gemm_kernel<KIND, EPI>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        TC_SMEM_BYTES));
+    BITMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM));
     st.attr_mask |= bit;
   }
-  p.num_m_blocks = static_cast<int>((p.M + TC_BM - 1) / TC_BM);
+  p.num_m_blocks = static_cast<int>((p.M + S::TILE_M - 1) / S::TILE_M);
   p.num_n_blocks = static_cast<int>((p.N + TC_BN - 1) / TC_BN);
   p.num_tiles = p.num_m_blocks * p.num_n_blocks;
-  const int grid = std::min(p.num_tiles, st.sms);
-  tc_gemm_kernel<KIND, EPI><<<grid, TC_THREADS, TC_SMEM_BYTES, s>>>(ta, tb, p);
+  const int units = std::min(p.num_tiles, PAIR ? st.sms / 2 : st.sms);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(PAIR ? 2 * units : units));
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = S::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = PAIR ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ProfScope ps(KIND == Kind::I8 ? "tc_gemm_i8" : "tc_gemm_bf16_apb", s);
+  BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
   return launch_check("tc_gemm_kernel");
 }
 
@@ -193,9 +269,10 @@ int run_tc_gemm(DeviceState& st, const CUtensorMap& ta, const CUtensorMap& tb, T
 int run_int_gemm(DeviceState& st, const uint8_t* A8, const uint8_t* B8, int64_t m, int64_t n,
                  int64_t kpad, int shift, float scale, const float* row_scale,
                  const float* col_scale, int32_t* c_units, float* c, int64_t ldc, cudaStream_t s) {
+  constexpr bool kPair = true;  // cta_group::2, 256 x 256 tiles per CTA pair
   CUtensorMap ta, tb;
-  BITMM_TRY(make_operand_map(&ta, A8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad, m, TC_BM));
-  BITMM_TRY(make_operand_map(&tb, B8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad, n, TC_BN));
+  BITMM_TRY(make_operand_map(&ta, A8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad, m, TcShape<kPair>::A_ROWS));
+  BITMM_TRY(make_operand_map(&tb, B8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad, n, TcShape<kPair>::B_ROWS));
   TcParams p{};
   p.M = static_cast<int>(m);
   p.N = static_cast<int>(n);
@@ -208,11 +285,11 @@ int run_int_gemm(DeviceState& st, const uint8_t* A8, const uint8_t* B8, int64_t 
   p.ldc = ldc;
   if (c_units) {
     p.out_i32 = c_units;
-    BITMM_TRY((run_tc_gemm<Kind::I8, Epi::I32>(st, ta, tb, p, s)));
+    BITMM_TRY((run_tc_gemm<Kind::I8, Epi::I32, kPair>(st, ta, tb, p, s)));
   }
   if (c) {
     p.out_f32 = c;
-    BITMM_TRY((run_tc_gemm<Kind::I8, Epi::F32>(st, ta, tb, p, s)));
+    BITMM_TRY((run_tc_gemm<Kind::I8, Epi::F32, kPair>(st, ta, tb, p, s)));
   }
   return BITMM_OK;
 }
@@ -322,6 +399,7 @@ int apb_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, int64_t k, int64
   {
     const int wpr32 = static_cast<int>(wpr * 2);
     const long long total = m * std::max<long long>(kpad / 32, wpr32);
+    ProfScope ps("unpack_sign_bf16", s);
     unpack_sign_bf16<<<blocks_for(total, 256), 256, 0, s>>>(
         reinterpret_cast<const uint32_t*>(w), m, wpr32, static_cast<int>(k),
         static_cast<int>(kpad), Abf, st.status);
@@ -329,13 +407,14 @@ int apb_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, int64_t k, int64
   }
   {
     dim3 grid(static_cast<unsigned>(kpad / 64), static_cast<unsigned>((n + 31) / 32));
+    ProfScope ps("split_x_bf16", s);
     split_x_bf16<<<grid, 256, 0, s>>>(b, ldb, static_cast<int>(k), static_cast<int>(n),
                                       static_cast<int>(kpad), kParts, XT);
     BITMM_TRY(launch_check("split_x_bf16"));
   }
   CUtensorMap ta, tb;
-  BITMM_TRY(make_operand_map(&ta, Abf, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kpad, m, TC_BM));
-  BITMM_TRY(make_operand_map(&tb, XT, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kParts * kpad, n, TC_BN));
+  BITMM_TRY(make_operand_map(&ta, Abf, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kpad, m, TcShape<false>::A_ROWS));
+  BITMM_TRY(make_operand_map(&tb, XT, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kParts * kpad, n, TcShape<false>::B_ROWS));
   TcParams p{};
   p.M = static_cast<int>(m);
   p.N = static_cast<int>(n);
@@ -350,7 +429,7 @@ int apb_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, int64_t k, int64
   p.csr_val = vals;
   p.X = b;
   p.ldx = ldb;
-  return run_tc_gemm<Kind::BF16, Epi::APB>(st, ta, tb, p, s);
+  return run_tc_gemm<Kind::BF16, Epi::APB, false>(st, ta, tb, p, s);
 }
 
 int with_device(DeviceState** st) {
@@ -386,6 +465,50 @@ int bitmm_abi_version(void) { return 1; }
 const char* bitmm_last_error(void) { return g_err.c_str(); }
 
 int bitmm_last_launch_count(void) { return g_launches; }
+
+int bitmm_profile_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  g_prof.on = on != 0;
+  return BITMM_OK;
+}
+
+int bitmm_profile_collect(void) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  for (const ProfRecord& r : g_prof.pending) {
+    BITMM_CUDA_TRY(cudaEventSynchronize(r.e1));
+    float ms = 0.f;
+    BITMM_CUDA_TRY(cudaEventElapsedTime(&ms, r.e0, r.e1));
+    g_prof.ms[r.kernel] += ms;
+    g_prof.launches[r.kernel] += 1;
+    g_prof.pool.push_back(r.e0);
+    g_prof.pool.push_back(r.e1);
+  }
+  g_prof.pending.clear();
+  return BITMM_OK;
+}
+
+int bitmm_profile_reset(void) {
+  BITMM_TRY(bitmm_profile_collect());
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  g_prof.names.clear();
+  g_prof.launches.clear();
+  g_prof.ms.clear();
+  return BITMM_OK;
+}
+
+int bitmm_profile_kernel_count(void) { return static_cast<int>(g_prof.names.size()); }
+
+const char* bitmm_profile_kernel_name(int i) {
+  return (i >= 0 && i < static_cast<int>(g_prof.names.size())) ? g_prof.names[i].c_str() : "";
+}
+
+int bitmm_profile_kernel_launches(int i) {
+  return (i >= 0 && i < static_cast<int>(g_prof.launches.size())) ? g_prof.launches[i] : 0;
+}
+
+double bitmm_profile_kernel_ms(int i) {
+  return (i >= 0 && i < static_cast<int>(g_prof.ms.size())) ? g_prof.ms[i] : 0.0;
+}
 
 int bitmm_device_sm_count(void) {
   DeviceState* st = nullptr;
@@ -437,11 +560,13 @@ int bitmm_gemm_1x1_popc_dev(const uint64_t* a, int64_t m, const uint64_t* b_pack
   const auto* A = reinterpret_cast<const uint32_t*>(a);
   const auto* B = reinterpret_cast<const uint32_t*>(b_packed);
   if (c_units) {
+    ProfScope ps("popc_gemm_1x1", s);
     popc_gemm_1x1<false><<<grid, PC_THREADS, 0, s>>>(A, B, (int)m, (int)n, (int)k, (int)(wpr * 2), scale,
                                                      c_units, nullptr, ldc);
     BITMM_TRY(launch_check("popc_gemm_1x1"));
   }
   if (c) {
+    ProfScope ps("popc_gemm_1x1", s);
     popc_gemm_1x1<true><<<grid, PC_THREADS, 0, s>>>(A, B, (int)m, (int)n, (int)k, (int)(wpr * 2), scale,
                                                     nullptr, c, ldc);
     BITMM_TRY(launch_check("popc_gemm_1x1"));
@@ -731,6 +856,7 @@ int bitmm_spmm_csr_dev(int64_t rows, int64_t cols, const uint64_t* row_ptr, cons
   DeviceState* st = nullptr;
   BITMM_TRY(with_device(&st));
   const long long warps = rows * ((n + 127) / 128);
+  ProfScope ps("spmm_csr", static_cast<cudaStream_t>(stream));
   spmm_csr_kernel<<<blocks_for(warps * 32, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       rows, reinterpret_cast<const unsigned long long*>(row_ptr),
       reinterpret_cast<const unsigned long long*>(col_idx), vals, b, ldb, static_cast<int>(n), c,

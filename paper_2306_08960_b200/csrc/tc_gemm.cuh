@@ -15,12 +15,16 @@
 // activations, f32 accumulate) and fuses the CSR residual SpMM
 // (kernels.cpp:334-352) into the epilogue.
 //
-// Structure (one CTA per SM, persistent over output tiles of 128 x 256):
-//   warp 0      : TMA producer, 4-stage smem ring (A 128x128B, B 256x128B)
+// Structure (persistent; one CTA, or one CTA pair, per SM / SM pair):
+//   warp 0      : TMA producer, multi-stage smem ring of 128-byte K slices
 //   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 2..5  : epilogue, TMEM -> registers -> smem transpose -> coalesced
 //                 global stores; two TMEM accumulators (2 x 256 columns) so the
 //                 epilogue of tile i overlaps the MMAs of tile i+1.
+// PAIR = true runs cta_group::2: a cluster of two CTAs owns a 256 x 256 output
+// tile; each CTA stages 128 rows of A and 128 rows of B per K slice (half the
+// operand bytes per SM of the single-CTA 128 x 256 tile) and the leader CTA
+// issues M=256 MMAs that accumulate into both CTAs' TMEM.
 #pragma once
 
 #include "ptx.cuh"
@@ -30,20 +34,24 @@ namespace bitmm_dev {
 enum class Kind : int { I8 = 0, BF16 = 1 };
 enum class Epi : int { I32 = 0, F32 = 1, APB = 2 };
 
-constexpr int TC_BM = 128;
-constexpr int TC_BN = 256;
-constexpr int TC_BK_BYTES = 128;  // one 128-byte swizzle row per operand row per stage
-constexpr int TC_STAGES = 4;
+constexpr int TC_BN = 256;         // output columns per tile (TMEM columns per accumulator)
+constexpr int TC_BK_BYTES = 128;   // one 128-byte swizzle row per operand row per stage
 constexpr int TC_THREADS = 192;
 constexpr int TC_EPI_STRIDE = 36;  // staged row stride in words (16B aligned, conflict-free)
-constexpr int TC_GROUP_M = 16;     // tile raster: groups of 16 M-blocks for L2 reuse
-
-constexpr int TC_A_STAGE_BYTES = TC_BM * TC_BK_BYTES;
-constexpr int TC_B_STAGE_BYTES = TC_BN * TC_BK_BYTES;
+constexpr int TC_GROUP_M = 16;     // tile raster: groups of 16 M-tiles for L2 reuse
 constexpr int TC_EPI_BYTES = 4 * 32 * TC_EPI_STRIDE * 4;
-constexpr int TC_BAR_BYTES = (2 * TC_STAGES + 4) * 8 + 16;
-constexpr int TC_SMEM_BYTES =
-    1024 + TC_STAGES * (TC_A_STAGE_BYTES + TC_B_STAGE_BYTES) + TC_EPI_BYTES + TC_BAR_BYTES;
+
+template <bool PAIR>
+struct TcShape {
+  static constexpr int A_ROWS = 128;                 // A rows staged per CTA
+  static constexpr int B_ROWS = PAIR ? 128 : 256;    // B rows staged per CTA
+  static constexpr int TILE_M = PAIR ? 256 : 128;    // output rows per tile
+  static constexpr int STAGES = PAIR ? 6 : 4;
+  static constexpr int A_STAGE = A_ROWS * TC_BK_BYTES;
+  static constexpr int B_STAGE = B_ROWS * TC_BK_BYTES;
+  static constexpr int BAR_BYTES = (2 * STAGES + 4) * 8 + 16;
+  static constexpr int SMEM = 1024 + STAGES * (A_STAGE + B_STAGE) + TC_EPI_BYTES + BAR_BYTES;
+};
 
 struct TcParams {
   int M, N;          // output rows / columns
@@ -75,61 +83,195 @@ __device__ __forceinline__ void tc_tile_coords(int t, const TcParams& p, int& mb
   nb = within / gm;
 }
 
-template <Kind KIND, Epi EPI>
+// Drains one 128-row x 256-column TMEM accumulator owned by this CTA into global
+// memory. Warp w (2..5) reads TMEM lanes 32*(w%4).. and stages 32x32 blocks
+// through smem so global stores are row-contiguous 128-byte segments.
+template <Epi EPI>
+__device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, uint32_t tmem_acc, int quad,
+                                                 int lane, int row_base, int col_base, float* stg) {
+  const bool vec_ok = (p.N & 3) == 0;
+  const int my_row = row_base + lane;
+  float row_mul = p.scale;
+  if constexpr (EPI == Epi::F32 || EPI == Epi::APB) {
+    if (p.row_scale != nullptr && my_row < p.M)
+      row_mul = (EPI == Epi::APB) ? p.row_scale[my_row] : p.scale * p.row_scale[my_row];
+  }
+#pragma unroll 1
+  for (int c = 0; c < TC_BN / 32; ++c) {
+    const int col0 = col_base + c * 32;
+    if (col0 >= p.N) break;
+    uint32_t v[32];
+    tmem_ld_32x32b_x32(tmem_acc + (static_cast<uint32_t>(quad * 32) << 16) + c * 32, v);
+    tmem_ld_wait();
+    // ---- per-thread (row) transform, staged row-major into smem ----
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+      float4 o;
+      float* of = reinterpret_cast<float*>(&o);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if constexpr (EPI == Epi::I32) {
+          of[e] = __int_as_float(static_cast<int>(v[j + e]) << p.shift);
+        } else if constexpr (EPI == Epi::F32) {
+          const float units = static_cast<float>(static_cast<int>(v[j + e]) << p.shift);
+          float s = row_mul;
+          if (p.col_scale != nullptr) {
+            const int cc = col0 + j + e;
+            s = __fmul_rn(s, cc < p.N ? p.col_scale[cc] : 0.0f);
+          }
+          of[e] = __fmul_rn(s, units);
+        } else {
+          of[e] = __fmul_rn(row_mul, __uint_as_float(v[j + e]));
+        }
+      }
+      *reinterpret_cast<float4*>(&stg[lane * TC_EPI_STRIDE + j]) = o;
+    }
+    __syncwarp();
+    if constexpr (EPI != Epi::APB) {
+      // ---- coalesced write-out: 4 rows x 128 B per warp instruction ----
+#pragma unroll
+      for (int r8 = 0; r8 < 8; ++r8) {
+        const int rl = r8 * 4 + (lane >> 3);
+        const int cl = (lane & 7) * 4;
+        const int grow = row_base + rl;
+        const int gcol = col0 + cl;
+        if (grow < p.M) {
+          const float4 val = *reinterpret_cast<const float4*>(&stg[rl * TC_EPI_STRIDE + cl]);
+          void* dst_base = (EPI == Epi::I32) ? static_cast<void*>(p.out_i32)
+                                             : static_cast<void*>(p.out_f32);
+          uint32_t* dst = static_cast<uint32_t*>(dst_base) + static_cast<long long>(grow) * p.ldc;
+          if (vec_ok && gcol + 3 < p.N) {
+            *reinterpret_cast<float4*>(dst + gcol) = val;
+          } else {
+            const float* vf = reinterpret_cast<const float*>(&val);
+            for (int e = 0; e < 4; ++e)
+              if (gcol + e < p.N) dst[gcol + e] = __float_as_uint(vf[e]);
+          }
+        }
+      }
+    } else {
+      // ---- APB: add the CSR residual rows (kernels.cpp:341-350 order), store ----
+      const int g = lane >> 3;
+      const int sub = lane & 7;
+#pragma unroll 1
+      for (int r8 = 0; r8 < 8; ++r8) {
+        const int rl = r8 * 4 + g;
+        const int grow = row_base + rl;
+        if (grow >= p.M) continue;
+        const int gcol = col0 + sub * 4;
+        float4 o = *reinterpret_cast<const float4*>(&stg[rl * TC_EPI_STRIDE + sub * 4]);
+        float res[4] = {0.f, 0.f, 0.f, 0.f};
+        if (p.csr_row_ptr != nullptr) {
+          const unsigned long long i0 = p.csr_row_ptr[grow];
+          const unsigned long long i1 = p.csr_row_ptr[grow + 1];
+          for (unsigned long long i = i0; i < i1; ++i) {
+            const float val = p.csr_val[i];
+            const float* xr = p.X + static_cast<long long>(p.csr_col[i]) * p.ldx;
+            if (vec_ok && gcol + 3 < p.N) {
+              const float4 x4 = *reinterpret_cast<const float4*>(xr + gcol);
+              res[0] = __fadd_rn(res[0], __fmul_rn(val, x4.x));
+              res[1] = __fadd_rn(res[1], __fmul_rn(val, x4.y));
+              res[2] = __fadd_rn(res[2], __fmul_rn(val, x4.z));
+              res[3] = __fadd_rn(res[3], __fmul_rn(val, x4.w));
+            } else {
+              for (int e = 0; e < 4; ++e)
+                if (gcol + e < p.N) res[e] = __fadd_rn(res[e], __fmul_rn(val, xr[gcol + e]));
+            }
+          }
+        }
+        o.x = __fadd_rn(o.x, res[0]);
+        o.y = __fadd_rn(o.y, res[1]);
+        o.z = __fadd_rn(o.z, res[2]);
+        o.w = __fadd_rn(o.w, res[3]);
+        float* dst = p.out_f32 + static_cast<long long>(grow) * p.ldc;
+        if (vec_ok && gcol + 3 < p.N) {
+          *reinterpret_cast<float4*>(dst + gcol) = o;
+        } else {
+          const float* of = reinterpret_cast<const float*>(&o);
+          for (int e = 0; e < 4; ++e)
+            if (gcol + e < p.N) dst[gcol + e] = of[e];
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <Kind KIND, Epi EPI, bool PAIR>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const TcParams p) {
+  using S = TcShape<PAIR>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024u - (base_u32 & 1023u)) & 1023u);
   uint8_t* sA = smem;
-  uint8_t* sB = sA + TC_STAGES * TC_A_STAGE_BYTES;
-  float* sEpi = reinterpret_cast<float*>(sB + TC_STAGES * TC_B_STAGE_BYTES);
+  uint8_t* sB = sA + S::STAGES * S::A_STAGE;
+  float* sEpi = reinterpret_cast<float*>(sB + S::STAGES * S::B_STAGE);
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sEpi) + TC_EPI_BYTES);
-  uint64_t* empty = full + TC_STAGES;
-  uint64_t* tfull = empty + TC_STAGES;
+  uint64_t* empty = full + S::STAGES;
+  uint64_t* tfull = empty + S::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  const int unit = PAIR ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
+  const int num_units = PAIR ? static_cast<int>(num_clusters_x()) : static_cast<int>(gridDim.x);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    for (int s = 0; s < TC_STAGES; ++s) {
+    for (int s = 0; s < S::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], PAIR ? 256 : 128);
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == 1) {
+    if constexpr (PAIR)
+      tmem_alloc_pair(tmem_slot, 512);
+    else
+      tmem_alloc(tmem_slot, 512);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   constexpr int BK_ELEMS = (KIND == Kind::I8) ? TC_BK_BYTES : TC_BK_BYTES / 2;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer (both CTAs of a pair) =====================
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      for (int tile = unit; tile < p.num_tiles; tile += num_units) {
         int mb, nb;
         tc_tile_coords(tile, p, mb, nb);
+        const int a_row = mb * S::TILE_M + static_cast<int>(rank) * S::A_ROWS;
+        const int b_row = nb * TC_BN + static_cast<int>(rank) * S::B_ROWS;
         for (int kb = 0; kb < p.num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1u);
           const int ka = kb % p.a_kb_period;
-          mbar_arrive_expect_tx(&full[stage], TC_A_STAGE_BYTES + TC_B_STAGE_BYTES);
-          tma_load_2d(sA + stage * TC_A_STAGE_BYTES, &tmA, &full[stage], ka * BK_ELEMS, mb * TC_BM);
-          tma_load_2d(sB + stage * TC_B_STAGE_BYTES, &tmB, &full[stage], kb * BK_ELEMS, nb * TC_BN);
-          if (++stage == TC_STAGES) {
+          if constexpr (PAIR) {
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (S::A_STAGE + S::B_STAGE));
+            tma_load_2d_pair(sA + stage * S::A_STAGE, &tmA, &full[stage], ka * BK_ELEMS, a_row);
+            tma_load_2d_pair(sB + stage * S::B_STAGE, &tmB, &full[stage], kb * BK_ELEMS, b_row);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], S::A_STAGE + S::B_STAGE);
+            tma_load_2d(sA + stage * S::A_STAGE, &tmA, &full[stage], ka * BK_ELEMS, a_row);
+            tma_load_2d(sB + stage * S::B_STAGE, &tmB, &full[stage], kb * BK_ELEMS, b_row);
+          }
+          if (++stage == S::STAGES) {
             stage = 0;
             phase ^= 1u;
           }
@@ -137,14 +279,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    if (lane == 0) {
-      constexpr uint32_t idesc = (KIND == Kind::I8) ? make_idesc(2u, 1u, 1u, TC_BM, TC_BN)
-                                                    : make_idesc(1u, 1u, 1u, TC_BM, TC_BN);
+    // ===================== MMA issuer (leader CTA only) =====================
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = (KIND == Kind::I8) ? make_idesc(2u, 1u, 1u, S::TILE_M, TC_BN)
+                                                    : make_idesc(1u, 1u, 1u, S::TILE_M, TC_BN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
+      for (int tile = unit; tile < p.num_tiles; tile += num_units, ++it) {
         const int acc = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], aphase ^ 1u);
@@ -153,156 +295,72 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int kb = 0; kb < p.num_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + stage * TC_A_STAGE_BYTES);
-          const uint32_t b_addr = smem_u32(sB + stage * TC_B_STAGE_BYTES);
+          const uint32_t a_addr = smem_u32(sA + stage * S::A_STAGE);
+          const uint32_t b_addr = smem_u32(sB + stage * S::B_STAGE);
 #pragma unroll
           for (int k = 0; k < TC_BK_BYTES / 32; ++k) {
             const uint64_t ad = sw128_kmajor_desc(a_addr + k * 32);
             const uint64_t bd = sw128_kmajor_desc(b_addr + k * 32);
-            if constexpr (KIND == Kind::I8)
-              mma_i8(d_tmem, ad, bd, idesc, (kb | k) != 0);
-            else
-              mma_f16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            if constexpr (PAIR) {
+              if constexpr (KIND == Kind::I8)
+                mma_i8_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
+              else
+                mma_f16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            } else {
+              if constexpr (KIND == Kind::I8)
+                mma_i8(d_tmem, ad, bd, idesc, (kb | k) != 0);
+              else
+                mma_f16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            }
           }
-          mma_commit(&empty[stage]);
-          if (++stage == TC_STAGES) {
+          if constexpr (PAIR)
+            mma_commit_pair(&empty[stage], 0x3);
+          else
+            mma_commit(&empty[stage]);
+          if (++stage == S::STAGES) {
             stage = 0;
             phase ^= 1u;
           }
         }
-        mma_commit(&tfull[acc]);
+        if constexpr (PAIR)
+          mma_commit_pair(&tfull[acc], 0x3);
+        else
+          mma_commit(&tfull[acc]);
       }
     }
   } else {
-    // ===================== epilogue (warps 2..5) =====================
+    // ===================== epilogue (warps 2..5 of every CTA) =====================
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     float* stg = sEpi + (warp - 2) * 32 * TC_EPI_STRIDE;
-    const bool vec_ok = (p.N & 3) == 0;
     int it = 0;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
+    for (int tile = unit; tile < p.num_tiles; tile += num_units, ++it) {
       int mb, nb;
       tc_tile_coords(tile, p, mb, nb);
       const int acc = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
-      const int row_base = mb * TC_BM + quad * 32;
-      const int my_row = row_base + lane;
-      float row_mul = p.scale;
-      if constexpr (EPI == Epi::F32 || EPI == Epi::APB) {
-        if (p.row_scale != nullptr && my_row < p.M) {
-          row_mul = (EPI == Epi::APB) ? p.row_scale[my_row] : p.scale * p.row_scale[my_row];
-        }
-      }
-#pragma unroll 1
-      for (int c = 0; c < TC_BN / 32; ++c) {
-        const int col0 = nb * TC_BN + c * 32;
-        if (col0 >= p.N) break;
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * TC_BN + c * 32,
-                           v);
-        tmem_ld_wait();
-        // ---- per-thread (row) transform, staged row-major into smem ----
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          float4 o;
-          float* of = reinterpret_cast<float*>(&o);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            if constexpr (EPI == Epi::I32) {
-              of[e] = __int_as_float(static_cast<int>(v[j + e]) << p.shift);
-            } else if constexpr (EPI == Epi::F32) {
-              const float units = static_cast<float>(static_cast<int>(v[j + e]) << p.shift);
-              float s = row_mul;
-              if (p.col_scale != nullptr) {
-                const int cc = col0 + j + e;
-                s = __fmul_rn(s, cc < p.N ? p.col_scale[cc] : 0.0f);
-              }
-              of[e] = __fmul_rn(s, units);
-            } else {
-              of[e] = __fmul_rn(row_mul, __uint_as_float(v[j + e]));
-            }
-          }
-          *reinterpret_cast<float4*>(&stg[lane * TC_EPI_STRIDE + j]) = o;
-        }
-        __syncwarp();
-        if constexpr (EPI != Epi::APB) {
-          // ---- coalesced write-out: 4 rows x 128 B per warp instruction ----
-#pragma unroll
-          for (int r8 = 0; r8 < 8; ++r8) {
-            const int rl = r8 * 4 + (lane >> 3);
-            const int cl = (lane & 7) * 4;
-            const int grow = row_base + rl;
-            const int gcol = col0 + cl;
-            if (grow < p.M) {
-              const float4 val = *reinterpret_cast<const float4*>(&stg[rl * TC_EPI_STRIDE + cl]);
-              void* dst_base = (EPI == Epi::I32) ? static_cast<void*>(p.out_i32)
-                                                 : static_cast<void*>(p.out_f32);
-              uint32_t* dst = static_cast<uint32_t*>(dst_base) + static_cast<long long>(grow) * p.ldc;
-              if (vec_ok && gcol + 3 < p.N) {
-                *reinterpret_cast<float4*>(dst + gcol) = val;
-              } else {
-                const float* vf = reinterpret_cast<const float*>(&val);
-                for (int e = 0; e < 4; ++e)
-                  if (gcol + e < p.N) dst[gcol + e] = __float_as_uint(vf[e]);
-              }
-            }
-          }
-        } else {
-          // ---- APB: add the CSR residual rows (kernels.cpp:341-350 order), store ----
-          const int g = lane >> 3;
-          const int sub = lane & 7;
-#pragma unroll 1
-          for (int r8 = 0; r8 < 8; ++r8) {
-            const int rl = r8 * 4 + g;
-            const int grow = row_base + rl;
-            if (grow >= p.M) continue;
-            const int gcol = col0 + sub * 4;
-            float4 o = *reinterpret_cast<const float4*>(&stg[rl * TC_EPI_STRIDE + sub * 4]);
-            float res[4] = {0.f, 0.f, 0.f, 0.f};
-            if (p.csr_row_ptr != nullptr) {
-              const unsigned long long i0 = p.csr_row_ptr[grow];
-              const unsigned long long i1 = p.csr_row_ptr[grow + 1];
-              for (unsigned long long i = i0; i < i1; ++i) {
-                const float val = p.csr_val[i];
-                const float* xr = p.X + static_cast<long long>(p.csr_col[i]) * p.ldx;
-                if (vec_ok && gcol + 3 < p.N) {
-                  const float4 x4 = *reinterpret_cast<const float4*>(xr + gcol);
-                  res[0] = __fadd_rn(res[0], __fmul_rn(val, x4.x));
-                  res[1] = __fadd_rn(res[1], __fmul_rn(val, x4.y));
-                  res[2] = __fadd_rn(res[2], __fmul_rn(val, x4.z));
-                  res[3] = __fadd_rn(res[3], __fmul_rn(val, x4.w));
-                } else {
-                  for (int e = 0; e < 4; ++e)
-                    if (gcol + e < p.N) res[e] = __fadd_rn(res[e], __fmul_rn(val, xr[gcol + e]));
-                }
-              }
-            }
-            o.x = __fadd_rn(o.x, res[0]);
-            o.y = __fadd_rn(o.y, res[1]);
-            o.z = __fadd_rn(o.z, res[2]);
-            o.w = __fadd_rn(o.w, res[3]);
-            float* dst = p.out_f32 + static_cast<long long>(grow) * p.ldc;
-            if (vec_ok && gcol + 3 < p.N) {
-              *reinterpret_cast<float4*>(dst + gcol) = o;
-            } else {
-              const float* of = reinterpret_cast<const float*>(&o);
-              for (int e = 0; e < 4; ++e)
-                if (gcol + e < p.N) dst[gcol + e] = of[e];
-            }
-          }
-        }
-        __syncwarp();
-      }
+      const int row_base = mb * S::TILE_M + static_cast<int>(rank) * 128 + quad * 32;
+      tc_epilogue_tile<EPI>(p, tmem_base + acc * TC_BN, quad, lane, row_base, nb * TC_BN, stg);
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if constexpr (PAIR)
+        mbar_arrive_cluster(smem_u32(&tempty[acc]) & kPeerBitMask);
+      else
+        mbar_arrive(&tempty[acc]);
     }
   }
 
-  __syncthreads();
+  tc_fence_before();
+  if constexpr (PAIR)
+    cluster_sync();
+  else
+    __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 512);
+    if constexpr (PAIR)
+      tmem_dealloc_pair(tmem_base, 512);
+    else
+      tmem_dealloc(tmem_base, 512);
   }
 }
 

@@ -1,0 +1,111 @@
+"""Device-resident entry points: torch CUDA tensors in, results written in place.
+
+Thin wrappers over the `*_dev` C ABI (include/bitmm_b200.h). PyTorch is plumbing here
+(device memory, the current stream); all compute is the sm_100a library. Packed words
+travel as int64 tensors (a bit-identical view of the reference's uint64 words).
+Encoding errors detected on the device are latched; `status()` synchronises the
+stream and raises them (InvalidEncoding / ValueError) like the host flavour does.
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+
+from . import _lib
+from .api import _raise
+
+
+def _stream(stream: Optional[torch.cuda.Stream]):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValueError("device entry points need contiguous CUDA tensors")
+    return t.data_ptr()
+
+
+def status(stream: Optional[torch.cuda.Stream] = None) -> None:
+    _raise(_lib.load().bitmm_device_status(_stream(stream)))
+
+
+def launch_count() -> int:
+    """Kernels launched by the most recent compute call on this thread."""
+    return _lib.load().bitmm_last_launch_count()
+
+
+def reserve_workspace(routine: int, m: int, n: int, k: int) -> None:
+    lib = _lib.load()
+    _raise(lib.bitmm_reserve_workspace(lib.bitmm_workspace_bytes(routine, m, n, k)))
+
+
+def gemm_1x1(a: torch.Tensor, b_packed: torch.Tensor, k: int, gamma_a: float = 1.0,
+             gamma_b: float = 1.0, units: Optional[torch.Tensor] = None,
+             out: Optional[torch.Tensor] = None, stream=None, popc: bool = False) -> None:
+    m, wpr = a.shape
+    n = b_packed.shape[0]
+    ldc = (units if units is not None else out).shape[1]
+    fn = _lib.load().bitmm_gemm_1x1_popc_dev if popc else _lib.load().bitmm_gemm_1x1_dev
+    _raise(fn(_ptr(a), m, _ptr(b_packed), n, k, wpr, gamma_a, gamma_b, _ptr(units), _ptr(out),
+              ldc, _stream(stream)))
+
+
+def gemm_1x2(w: torch.Tensor, gamma: float, t: torch.Tensor, h: torch.Tensor, mm: torch.Tensor,
+             k: int, a_scale: float = 1.0, a_gamma: Optional[float] = None,
+             row_scale: Optional[torch.Tensor] = None, col_scale: Optional[torch.Tensor] = None,
+             units: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+             stream=None) -> None:
+    m, wpr = w.shape
+    n = t.shape[0]
+    ldc = (units if units is not None else out).shape[1]
+    _raise(_lib.load().bitmm_gemm_1x2_dev(
+        _ptr(w), m, gamma, _ptr(t), _ptr(h), _ptr(mm), n, k, wpr, a_scale,
+        int(a_gamma is not None), 1.0 if a_gamma is None else a_gamma, _ptr(row_scale),
+        _ptr(col_scale), _ptr(units), _ptr(out), ldc, _stream(stream)))
+
+
+def gemm_2x2(wt, wh, wm, at, ah, am, k: int, w_scale: float = 1.0, a_scale: float = 1.0,
+             w_gamma: Optional[float] = None, a_gamma: Optional[float] = None,
+             row_scale=None, col_scale=None, units=None, out=None, stream=None) -> None:
+    m, wpr = wt.shape
+    n = at.shape[0]
+    ldc = (units if units is not None else out).shape[1]
+    _raise(_lib.load().bitmm_gemm_2x2_dev(
+        _ptr(wt), _ptr(wh), _ptr(wm), m, w_scale, int(w_gamma is not None),
+        1.0 if w_gamma is None else w_gamma, _ptr(at), _ptr(ah), _ptr(am), n, k, wpr, a_scale,
+        int(a_gamma is not None), 1.0 if a_gamma is None else a_gamma, _ptr(row_scale),
+        _ptr(col_scale), _ptr(units), _ptr(out), ldc, _stream(stream)))
+
+
+def gemm_1x32(w: torch.Tensor, k: int, gamma: float, b: torch.Tensor, out: torch.Tensor,
+              row_gamma: Optional[torch.Tensor] = None, stream=None) -> None:
+    m, wpr = w.shape
+    n = b.shape[1]
+    _raise(_lib.load().bitmm_gemm_1x32_dev(_ptr(w), m, k, wpr, gamma, _ptr(row_gamma), _ptr(b), n,
+                                           b.shape[1], _ptr(out), out.shape[1], _stream(stream)))
+
+
+def spmm_csr(rows: int, cols: int, row_ptr, col_idx, vals, b: torch.Tensor, out: torch.Tensor,
+             stream=None) -> None:
+    n = b.shape[1]
+    _raise(_lib.load().bitmm_spmm_csr_dev(rows, cols, _ptr(row_ptr), _ptr(col_idx), _ptr(vals),
+                                          _ptr(b), n, b.shape[1], _ptr(out), out.shape[1],
+                                          _stream(stream)))
+
+
+def layer_forward(bin_words: torch.Tensor, cols: int, alpha, row_ptr, col_idx, vals,
+                  b: torch.Tensor, out: torch.Tensor, stream=None) -> None:
+    """alpha: python float (reference scalar) or a CUDA float32 tensor [rows]."""
+    rows, wpr = bin_words.shape
+    n = b.shape[1]
+    if isinstance(alpha, torch.Tensor):
+        a_scalar, a_vec = 1.0, alpha
+    else:
+        a_scalar, a_vec = float(alpha), None
+    _raise(_lib.load().bitmm_layer_forward_dev(
+        rows, cols, a_scalar, _ptr(a_vec), _ptr(bin_words), wpr, _ptr(row_ptr), _ptr(col_idx),
+        _ptr(vals), _ptr(b), n, b.shape[1], _ptr(out), out.shape[1], _stream(stream)))
