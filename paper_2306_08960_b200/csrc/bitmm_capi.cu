@@ -234,6 +234,54 @@ int run_unpack_level_i8(const uint64_t* t, const uint64_t* h, const uint64_t* m,
   return launch_check("unpack_level_i8");
 }
 
+// Operand description for the fused pair-unpack launch.
+struct OperandSrc {
+  const uint64_t* w0;
+  const uint64_t* w1;
+  const uint64_t* w2;
+  int64_t rows;
+  bool levels;
+};
+
+UnpackOperand make_unpack_operand(const OperandSrc& src, int64_t wpr, int64_t kpad, uint8_t* out) {
+  UnpackOperand o{};
+  o.w0 = reinterpret_cast<const uint32_t*>(src.w0);
+  o.w1 = reinterpret_cast<const uint32_t*>(src.w1);
+  o.w2 = reinterpret_cast<const uint32_t*>(src.w2);
+  o.out = out;
+  o.rows = src.rows;
+  o.wpr32 = static_cast<int>(wpr * 2);
+  o.groups_per_row = (std::max<long long>(kpad / 32, o.wpr32) + 127) / 128;  // 128-word slices
+  o.levels = src.levels ? 1 : 0;
+  return o;
+}
+
+// Expands both GEMM operands (bits or ternary planes) to int8 rows in one launch.
+int run_unpack_pair(const OperandSrc& a, const OperandSrc& b, int64_t wpr, int64_t k, int64_t kpad,
+                    uint8_t* A8, uint8_t* B8, int* flag, cudaStream_t s) {
+  UnpackPair P{};
+  P.op[0] = make_unpack_operand(a, wpr, kpad, A8);
+  P.op[1] = make_unpack_operand(b, wpr, kpad, B8);
+  P.K = static_cast<int>(k);
+  P.kpad = static_cast<int>(kpad);
+  P.err = flag;
+  const long long work = std::max(P.op[0].rows * P.op[0].groups_per_row,
+                                  P.op[1].rows * P.op[1].groups_per_row);
+  if (work == 0) return BITMM_OK;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks_for(work * 32, 256), 2);  // one warp per slice
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ProfScope ps("unpack_pair_i8", s);
+  BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, unpack_pair_i8, P));
+  return launch_check("unpack_pair_i8");
+}
+
 template <Kind KIND, Epi EPI, bool PAIR>
 int run_tc_gemm(DeviceState& st, const CUtensorMap& ta, const CUtensorMap& tb, TcParams p,
                 cudaStream_t s) {
@@ -253,13 +301,15 @@ int run_tc_gemm(DeviceState& st, const CUtensorMap& ta, const CUtensorMap& tb, T
   cfg.blockDim = dim3(TC_THREADS);
   cfg.dynamicSmemBytes = S::SMEM;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = PAIR ? 2 : 1;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   ProfScope ps(KIND == Kind::I8 ? "tc_gemm_i8" : "tc_gemm_bf16_apb", s);
   BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
   return launch_check("tc_gemm_kernel");
@@ -344,8 +394,8 @@ int gemm_1x1_dev_impl(DeviceState& st, const uint64_t* a, int64_t m, const uint6
   Carve cv(st.ws.ptr);
   uint8_t* A8 = cv.take<uint8_t>(m * kpad);
   uint8_t* B8 = cv.take<uint8_t>(n * kpad);
-  BITMM_TRY(run_unpack_sign_i8(a, m, wpr, k, kpad, A8, st.status, s));
-  BITMM_TRY(run_unpack_sign_i8(b, n, wpr, k, kpad, B8, st.status, s));
+  BITMM_TRY(run_unpack_pair({a, nullptr, nullptr, m, false}, {b, nullptr, nullptr, n, false}, wpr,
+                            k, kpad, A8, B8, st.status, s));
   const float scale = gamma_a * gamma_b;  // kernels.cpp:170
   return run_int_gemm(st, A8, B8, m, n, kpad, 0, scale, nullptr, nullptr, c_units, c, ldc, s);
 }
@@ -360,8 +410,8 @@ int gemm_1x2_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, float gamma
   Carve cv(st.ws.ptr);
   uint8_t* A8 = cv.take<uint8_t>(m * kpad);
   uint8_t* B8 = cv.take<uint8_t>(n * kpad);
-  BITMM_TRY(run_unpack_level_i8(t, h, mm, n, wpr, k, kpad, B8, st.status, s));
-  BITMM_TRY(run_unpack_sign_i8(w, m, wpr, k, kpad, A8, st.status, s));
+  BITMM_TRY(run_unpack_pair({w, nullptr, nullptr, m, false}, {t, h, mm, n, true}, wpr, k, kpad, A8,
+                            B8, st.status, s));
   // kernels.cpp:193: half_scale = 0.5f * gamma * a_packed.scale * a_packed.gamma.value_or(1.0f)
   const float scale = 0.5f * gamma * a_scale * (has_a_gamma ? a_gamma : 1.0f);
   return run_int_gemm(st, A8, B8, m, n, kpad, 1, scale, row_scale, col_scale, c_units, c, ldc, s);
@@ -378,8 +428,8 @@ int gemm_2x2_dev_impl(DeviceState& st, const uint64_t* wt, const uint64_t* wh, c
   Carve cv(st.ws.ptr);
   uint8_t* A8 = cv.take<uint8_t>(m * kpad);
   uint8_t* B8 = cv.take<uint8_t>(n * kpad);
-  BITMM_TRY(run_unpack_level_i8(wt, wh, wm, m, wpr, k, kpad, A8, st.status, s));
-  BITMM_TRY(run_unpack_level_i8(at, ah, am, n, wpr, k, kpad, B8, st.status, s));
+  BITMM_TRY(run_unpack_pair({wt, wh, wm, m, true}, {at, ah, am, n, true}, wpr, k, kpad, A8, B8,
+                            st.status, s));
   // kernels.cpp:232-233
   const float scale = 0.25f * w_scale * a_scale * (has_w_gamma ? w_gamma : 1.0f) *
                       (has_a_gamma ? a_gamma : 1.0f);

@@ -246,6 +246,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Everything above overlapped the producer of our operands (PDL); from here on
+  // we read its output.
+  pdl_wait();
 
   constexpr int BK_ELEMS = (KIND == Kind::I8) ? TC_BK_BYTES : TC_BK_BYTES / 2;
 

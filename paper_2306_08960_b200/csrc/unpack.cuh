@@ -22,6 +22,8 @@
 #include <cuda_bf16.h>
 #include <cstdint>
 
+#include "ptx.cuh"
+
 namespace bitmm_dev {
 
 constexpr int ERR_PADDING = 1;
@@ -59,6 +61,96 @@ __global__ void unpack_sign_i8(const uint32_t* __restrict__ words, long long row
   uint4* dst = reinterpret_cast<uint4*>(out + r * kpad + g * 32);
   dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
   dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+}
+
+// Both GEMM operands in one launch (blockIdx.y selects the operand). Each thread
+// expands 4 consecutive 32-bit words (128 elements) of one row into 128 output
+// bytes: 16-byte loads/stores, 8 stores in flight per thread.
+struct UnpackOperand {
+  const uint32_t* w0;  // sign words, or the t plane
+  const uint32_t* w1;  // h plane (levels only)
+  const uint32_t* w2;  // m plane (levels only)
+  uint8_t* out;        // [rows][kpad]
+  long long rows;
+  long long groups_per_row;  // ceil(max(kpad/32, wpr32) / 4)
+  int wpr32;
+  int levels;  // 0: +-1 signs, 1: 2-bit levels
+};
+
+struct UnpackPair {
+  UnpackOperand op[2];
+  int K;
+  int kpad;
+  int* err;
+};
+
+// Work unit = one warp x one 4096-element slice of a row (128 input words, 4 KB of
+// output). Store v of lane t writes output bytes [16*(32v+t), +16) of the slice, so every
+// warp store instruction covers 512 contiguous bytes; the lane reads the 16 input bits
+// it needs from word (32v+t)/2 (lane pairs share a word, an L1 hit).
+__global__ void __launch_bounds__(256) unpack_pair_i8(const __grid_constant__ UnpackPair P) {
+  pdl_wait();  // the previous kernel may still be reading the workspace we overwrite
+  pdl_launch_dependents();
+  const UnpackOperand& o = P.op[blockIdx.y];
+  const long long unit = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long slices = o.groups_per_row;  // slices of 128 words per row
+  if (unit >= o.rows * slices) return;
+  const long long r = unit / slices;
+  const int sl = static_cast<int>(unit - r * slices);
+  const long long rbase = r * o.wpr32;
+  const int word0 = sl * 128;
+  int bad = 0;
+  // validation: every word of the slice that exists in the source
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int g = word0 + j * 32 + lane;
+    if (g < o.wpr32) {
+      const uint32_t valid = valid_mask32(g * 32, P.K);
+      if (o.levels == 0) {
+        const uint32_t w = __ldg(o.w0 + rbase + g);
+        bad |= (w & ~valid) ? ERR_PADDING : 0;
+      } else {
+        const uint32_t tw = __ldg(o.w0 + rbase + g), hw = __ldg(o.w1 + rbase + g),
+                       mw = __ldg(o.w2 + rbase + g);
+        if (((tw | hw | mw) & ~valid) | (tw & hw) | (tw & ~mw) | (hw & mw)) bad |= ERR_ENCODING;
+      }
+    }
+  }
+  if (bad) atomicOr(P.err, bad);
+  uint8_t* out_row = o.out + r * P.kpad;
+#pragma unroll 2
+  for (int v = 0; v < 8; ++v) {
+    const int chunk = v * 32 + lane;        // 16-byte output chunk within the slice
+    const int elem = word0 * 32 + chunk * 16;
+    if (elem >= P.kpad) break;
+    const int g = word0 + (chunk >> 1);
+    const int shift = (chunk & 1) * 16;
+    const uint32_t valid = (valid_mask32(g * 32, P.K) >> shift) & 0xFFFFu;
+    uint32_t ow[4];
+    if (o.levels == 0) {
+      const uint32_t w = (g < o.wpr32) ? (__ldg(o.w0 + rbase + g) >> shift) & 0xFFFFu : 0u;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t b = spread4((w >> (4 * q)) & 0xFu);
+        const uint32_t vm = spread4((valid >> (4 * q)) & 0xFu);
+        ow[q] = ((b * 0xFEu) ^ 0xFFFFFFFFu) & (vm * 0xFFu);
+      }
+    } else {
+      uint32_t tw = 0, hw = 0, mw = 0;
+      if (g < o.wpr32) {
+        tw = (__ldg(o.w0 + rbase + g) >> shift) & 0xFFFFu;
+        hw = (__ldg(o.w1 + rbase + g) >> shift) & 0xFFFFu;
+        mw = (__ldg(o.w2 + rbase + g) >> shift) & 0xFFFFu;
+      }
+      const uint32_t hi = (tw | hw) & valid;
+      const uint32_t lo = (tw | ~(hw | mw)) & valid;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        ow[q] = (spread4((hi >> (4 * q)) & 0xFu) << 1) + spread4((lo >> (4 * q)) & 0xFu);
+    }
+    *reinterpret_cast<uint4*>(out_row + elem) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+  }
 }
 
 __global__ void unpack_level_i8(const uint32_t* __restrict__ t, const uint32_t* __restrict__ h,
