@@ -1,0 +1,371 @@
+// APB layer forward (apb.cpp:158-164): C = alpha_r * (sign(bin) . X) + residual . X.
+//
+// Two kernels, chained with programmatic dependent launch:
+//
+// 1. spmm_xchunk_kernel — the sparse full-precision residual (spmm_csr,
+//    kernels.cpp:334-352). A block stages an X column chunk [K][64] fp32 in shared
+//    memory (coalesced, read once from L2), then walks CSR rows: a half-warp owns one
+//    output row, lane l owns 4 consecutive columns, nonzeros are broadcast with
+//    half-warp shuffles and accumulated in col_idx order. It writes R.X into C.
+//    EXACT = true reproduces the reference's rounding (separate fp32 multiply and add,
+//    in order); the fused layer uses fma.
+//
+// 2. apb_gemm_kernel — the binary part on the tensor cores, cta_group::2 (a CTA pair
+//    owns 256 output rows x 128 columns). A = sign(bin) as bf16 +-1 (exact); B = X^T
+//    split into three bf16 parts x = hi + mid + lo (exact, unpack.cuh). One smem stage
+//    holds one 64-wide K slice of A and of all three B parts, so A is fetched once per
+//    slice. The hi products accumulate in one TMEM accumulator and the mid+lo products
+//    in a second one: the tensor core's fp32 accumulation truncates small addends
+//    against a large running sum, and keeping the magnitudes apart removes that bias
+//    (measured: 3e-6 -> ~1e-7 relative at K=768). TMEM holds 2 tiles x 2 accumulators
+//    x 128 columns = 512 columns, so the epilogue of tile i overlaps the MMAs of i+1.
+//    Epilogue: C = fma(alpha_r, hi + lo, C) with C holding R.X from kernel 1
+//    (= the reference's bin_part + res_part, apb.cpp:161-162, up to rounding).
+#pragma once
+
+#include "ptx.cuh"
+#include "tc_gemm.cuh"
+
+namespace bitmm_dev {
+
+constexpr int SPMM_TOK = 32;       // columns per block (X chunk [K][32] fp32 in smem)
+constexpr int SPMM_THREADS = 512;  // 64 octets: an 8-lane octet owns one output row, 4 columns/lane
+constexpr int SPMM_QUADS = SPMM_THREADS / 8;  // rows in flight per block
+
+// Dynamic smem: X chunk [K][SPMM_TOK] fp32, then the block's row offsets (u32).
+inline int spmm_smem_bytes(long long K, int rows_per_split) {
+  return static_cast<int>(K * SPMM_TOK * 4 + (rows_per_split + 1) * 4);
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+template <bool EXACT, bool PDL_CHAIN>
+__global__ void __launch_bounds__(SPMM_THREADS, 2)
+    spmm_xchunk_kernel(int rows, int K, int N, const unsigned long long* __restrict__ row_ptr,
+                       const unsigned long long* __restrict__ col_idx,
+                       const float* __restrict__ vals, const float* __restrict__ X, long long ldx,
+                       float* __restrict__ C, long long ldc, int rows_per_split) {
+  extern __shared__ float xs[];  // [K][SPMM_TOK], then u32 row offsets
+  if (PDL_CHAIN) pdl_launch_dependents();
+  unsigned* rps = reinterpret_cast<unsigned*>(xs + static_cast<long long>(K) * SPMM_TOK);
+  const int c0 = blockIdx.x * SPMM_TOK;
+  const int r0 = blockIdx.y * rows_per_split;
+  const int r1 = min(rows, r0 + rows_per_split);
+  const bool vec = ((N & 3) == 0) && ((ldx & 3) == 0) && ((ldc & 3) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+  // X chunk: every 16-byte piece in flight at once (cp.async), zero-filled past N
+  for (int i = threadIdx.x; i < K * (SPMM_TOK / 4); i += SPMM_THREADS) {
+    const int k = i / (SPMM_TOK / 4), q = (i % (SPMM_TOK / 4)) * 4;
+    const float* src = X + static_cast<long long>(k) * ldx + c0 + q;
+    float* dst = &xs[k * SPMM_TOK + q];
+    if (vec && c0 + q + 3 < N) {
+      cp_async16(dst, src);
+    } else {
+      for (int e = 0; e < 4; ++e) dst[e] = (c0 + q + e < N) ? src[e] : 0.f;
+    }
+  }
+  const unsigned long long nz0 = row_ptr[r0];
+  for (int i = threadIdx.x; i <= r1 - r0; i += SPMM_THREADS)
+    rps[i] = static_cast<unsigned>(row_ptr[r0 + i] - nz0);
+  cp_async_wait_all();
+  __syncthreads();
+
+  // All loops below are warp-uniform (trip counts are warp maxima; short rows are padded
+  // with zero weights) so the full-warp shuffles never need divergence handling.
+  // An octet (8 lanes) owns one output row and its 32 columns: each shared-memory phase
+  // then reads one whole 128-byte X row (conflict-free). Loops are warp-uniform (trip
+  // counts are warp maxima, short rows padded with zero weights) so the full-warp
+  // shuffles never need divergence handling.
+  const int oct = threadIdx.x >> 3;
+  const int ol = threadIdx.x & 7;
+  const int lane = threadIdx.x & 31;
+  const int obase = lane & ~7;
+  const int col = c0 + ol * 4;
+  const unsigned long long* cbase = col_idx + nz0;
+  const float* vbase = vals + nz0;
+  const int iters = (r1 - r0 + SPMM_QUADS - 1) / SPMM_QUADS;
+  for (int it = 0; it < iters; ++it) {
+    const int r = r0 + it * SPMM_QUADS + oct;
+    const bool live = r < r1;
+    const unsigned i0 = live ? rps[r - r0] : 0u;
+    const unsigned n = live ? rps[r - r0 + 1] - i0 : 0u;
+    const unsigned nmax = __reduce_max_sync(0xFFFFFFFFu, n);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (unsigned base = 0; base < nmax; base += 8) {
+      const unsigned idx = base + ol;
+      const unsigned kk = idx < n ? static_cast<unsigned>(cbase[i0 + idx]) * (SPMM_TOK * 4) : 0u;
+      const float vv = idx < n ? vbase[i0 + idx] : 0.f;
+      const char* xrow = reinterpret_cast<const char*>(xs) + ol * 16;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const unsigned koff = __shfl_sync(0xFFFFFFFFu, kk, obase + j);
+        const float v = __shfl_sync(0xFFFFFFFFu, vv, obase + j);
+        const float4 x = *reinterpret_cast<const float4*>(xrow + koff);
+        if (EXACT) {
+          if (base + j < n) {  // padded entries must not touch the reference's rounding order
+            acc[0] = __fadd_rn(acc[0], __fmul_rn(v, x.x));
+            acc[1] = __fadd_rn(acc[1], __fmul_rn(v, x.y));
+            acc[2] = __fadd_rn(acc[2], __fmul_rn(v, x.z));
+            acc[3] = __fadd_rn(acc[3], __fmul_rn(v, x.w));
+          }
+        } else {
+          // padded entries carry v = 0 (and row 0, a valid address): fma(0, x, acc) == acc
+          acc[0] = __fmaf_rn(v, x.x, acc[0]);
+          acc[1] = __fmaf_rn(v, x.y, acc[1]);
+          acc[2] = __fmaf_rn(v, x.z, acc[2]);
+          acc[3] = __fmaf_rn(v, x.w, acc[3]);
+        }
+      }
+    }
+    if (live) {
+      float* dst = C + static_cast<long long>(r) * ldc + col;
+      if (vec && col + 3 < N) {
+        *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      } else {
+        for (int e = 0; e < 4; ++e)
+          if (col + e < N) dst[e] = acc[e];
+      }
+    }
+  }
+  // completion of this grid must imply completion of the kernels before it
+  if (PDL_CHAIN) pdl_wait();
+}
+
+// ----------------------------------------------------------------------------------
+constexpr int APB_BN = 128;        // output columns per pair tile
+constexpr int APB_PARTS = 3;       // bf16 split parts of X
+constexpr int APB_STAGES = 5;
+constexpr int APB_A_STAGE = 128 * TC_BK_BYTES;                       // 128 rows x 64 bf16
+constexpr int APB_B_PART = (APB_BN / 2) * TC_BK_BYTES;               // 64 rows x 64 bf16
+constexpr int APB_STAGE = APB_A_STAGE + APB_PARTS * APB_B_PART;      // 40 KB
+constexpr int APB_SMEM = 1024 + APB_STAGES * APB_STAGE + TC_EPI_BYTES + (2 * APB_STAGES + 4) * 8 + 16;
+
+struct ApbParams {
+  int M, N, kb_per_part;     // kb_per_part = kpad / 64
+  int kpad;                  // elements per part row segment
+  float alpha;               // scalar alpha (row_alpha == nullptr)
+  const float* row_alpha;
+  float* C;                  // holds R.X on entry (accumulate_c), the layer output on exit
+  long long ldc;
+  int accumulate_c;          // 1: C += alpha*S.X (residual already in C); 0: C = alpha*S.X
+  int num_m_blocks, num_n_blocks, num_tiles;
+};
+
+__device__ __forceinline__ void apb_tile_coords(int t, const ApbParams& p, int& mb, int& nb) {
+  const int group_tiles = TC_GROUP_M * p.num_n_blocks;
+  const int g = t / group_tiles;
+  const int first_m = g * TC_GROUP_M;
+  const int gm = min(TC_GROUP_M, p.num_m_blocks - first_m);
+  const int within = t - g * group_tiles;
+  mb = first_m + within % gm;
+  nb = within / gm;
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    apb_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const ApbParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base_u32 = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024u - (base_u32 & 1023u)) & 1023u);
+  uint8_t* stages = smem;
+  float* sEpi = reinterpret_cast<float*>(stages + APB_STAGES * APB_STAGE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sEpi) + TC_EPI_BYTES);
+  uint64_t* empty = full + APB_STAGES;
+  uint64_t* tfull = empty + APB_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int unit = static_cast<int>(cluster_id_x());
+  const int num_units = static_cast<int>(num_clusters_x());
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < APB_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 256);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // operands (split X, bf16 signs) and C = R.X come from the preceding kernels
+  const int num_kb = p.kb_per_part;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = unit; tile < p.num_tiles; tile += num_units) {
+        int mb, nb;
+        apb_tile_coords(tile, p, mb, nb);
+        const int a_row = mb * 256 + static_cast<int>(rank) * 128;
+        const int b_row = nb * APB_BN + static_cast<int>(rank) * (APB_BN / 2);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * APB_STAGE);
+          uint8_t* st = stages + stage * APB_STAGE;
+          tma_load_2d_pair(st, &tmA, &full[stage], kb * 64, a_row);
+#pragma unroll
+          for (int q = 0; q < APB_PARTS; ++q)
+            tma_load_2d_pair(st + APB_A_STAGE + q * APB_B_PART, &tmB, &full[stage],
+                             q * p.kpad + kb * 64, b_row);
+          if (++stage == APB_STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = make_idesc(1u, 1u, 1u, 256, APB_BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = unit; tile < p.num_tiles; tile += num_units, ++it) {
+        const int buf = it & 1;
+        const uint32_t bphase = (it >> 1) & 1;
+        mbar_wait(&tempty[buf], bphase ^ 1u);
+        tc_fence_after();
+        const uint32_t d_hi = tmem_base + buf * 2 * APB_BN;
+        const uint32_t d_lo = d_hi + APB_BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(stages + stage * APB_STAGE);
+#pragma unroll
+          for (int q = 0; q < APB_PARTS; ++q) {
+            const uint32_t b_addr = a_addr + APB_A_STAGE + q * APB_B_PART;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t ad = sw128_kmajor_desc(a_addr + k * 32);
+              const uint64_t bd = sw128_kmajor_desc(b_addr + k * 32);
+              const uint32_t acc = (q == 0) ? ((kb | k) != 0) : !(q == 1 && kb == 0 && k == 0);
+              mma_f16_pair(q == 0 ? d_hi : d_lo, ad, bd, idesc, acc);
+            }
+          }
+          mma_commit_pair(&empty[stage], 0x3);
+          if (++stage == APB_STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        mma_commit_pair(&tfull[buf], 0x3);
+      }
+    }
+  } else {
+    const int quad = warp & 3;
+    float* stg = sEpi + (warp - 2) * 32 * TC_EPI_STRIDE;
+    const bool vec_ok = ((p.N & 3) == 0) && ((p.ldc & 3) == 0);
+    int it = 0;
+    for (int tile = unit; tile < p.num_tiles; tile += num_units, ++it) {
+      int mb, nb;
+      apb_tile_coords(tile, p, mb, nb);
+      const int buf = it & 1;
+      const uint32_t bphase = (it >> 1) & 1;
+      mbar_wait(&tfull[buf], bphase);
+      tc_fence_after();
+      const int row_base = mb * 256 + static_cast<int>(rank) * 128 + quad * 32;
+      const int my_row = row_base + lane;
+      const float alpha = (p.row_alpha != nullptr) ? (my_row < p.M ? p.row_alpha[my_row] : 0.f)
+                                                   : p.alpha;
+      const uint32_t t_hi = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + buf * 2 * APB_BN;
+      const int cl = (lane & 7) * 4;
+      // C (= R.X) for chunk c is loaded one chunk ahead: 8 independent 16-byte loads per
+      // lane in flight while the previous chunk is drained from TMEM and stored.
+      float4 cin[8], cnext[8];
+      auto load_c = [&](int c, float4 (&dst)[8]) {
+#pragma unroll
+        for (int r8 = 0; r8 < 8; ++r8) {
+          const int grow = row_base + r8 * 4 + (lane >> 3);
+          const int gcol = nb * APB_BN + c * 32 + cl;
+          dst[r8] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (p.accumulate_c && grow < p.M && gcol < p.N) {
+            const float* src = p.C + static_cast<long long>(grow) * p.ldc + gcol;
+            if (vec_ok && gcol + 3 < p.N) {
+              dst[r8] = *reinterpret_cast<const float4*>(src);
+            } else {
+              float* df = reinterpret_cast<float*>(&dst[r8]);
+              for (int e = 0; e < 4; ++e)
+                if (gcol + e < p.N) df[e] = src[e];
+            }
+          }
+        }
+      };
+      load_c(0, cin);
+#pragma unroll 1
+      for (int c = 0; c < APB_BN / 32; ++c) {
+        const int col0 = nb * APB_BN + c * 32;
+        if (col0 >= p.N) break;
+        if (c + 1 < APB_BN / 32) load_c(c + 1, cnext);
+        uint32_t vh[32], vl[32];
+        tmem_ld_32x32b_x32(t_hi + c * 32, vh);
+        tmem_ld_32x32b_x32(t_hi + APB_BN + c * 32, vl);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          float4 o;
+          o.x = __fmul_rn(alpha, __fadd_rn(__uint_as_float(vh[j + 0]), __uint_as_float(vl[j + 0])));
+          o.y = __fmul_rn(alpha, __fadd_rn(__uint_as_float(vh[j + 1]), __uint_as_float(vl[j + 1])));
+          o.z = __fmul_rn(alpha, __fadd_rn(__uint_as_float(vh[j + 2]), __uint_as_float(vl[j + 2])));
+          o.w = __fmul_rn(alpha, __fadd_rn(__uint_as_float(vh[j + 3]), __uint_as_float(vl[j + 3])));
+          *reinterpret_cast<float4*>(&stg[lane * TC_EPI_STRIDE + j]) = o;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int r8 = 0; r8 < 8; ++r8) {
+          const int rl = r8 * 4 + (lane >> 3);
+          const int grow = row_base + rl;
+          const int gcol = col0 + cl;
+          if (grow < p.M && gcol < p.N) {
+            const float4 b = *reinterpret_cast<const float4*>(&stg[rl * TC_EPI_STRIDE + cl]);
+            float4 r;
+            r.x = __fadd_rn(b.x, cin[r8].x);
+            r.y = __fadd_rn(b.y, cin[r8].y);
+            r.z = __fadd_rn(b.z, cin[r8].z);
+            r.w = __fadd_rn(b.w, cin[r8].w);
+            float* dst = p.C + static_cast<long long>(grow) * p.ldc + gcol;
+            if (vec_ok && gcol + 3 < p.N) {
+              *reinterpret_cast<float4*>(dst) = r;
+            } else {
+              const float* rf = reinterpret_cast<const float*>(&r);
+              for (int e = 0; e < 4; ++e)
+                if (gcol + e < p.N) dst[e] = rf[e];
+            }
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int r8 = 0; r8 < 8; ++r8) cin[r8] = cnext[r8];
+      }
+      tc_fence_before();
+      mbar_arrive_cluster(smem_u32(&tempty[buf]) & kPeerBitMask);
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, 512);
+  }
+}
+
+}  // namespace bitmm_dev

@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include "apb_gemm.cuh"
 #include "bitmm_b200.h"
 #include "popc_gemm.cuh"
 #include "ptx.cuh"
@@ -436,50 +437,143 @@ int gemm_2x2_dev_impl(DeviceState& st, const uint64_t* wt, const uint64_t* wh, c
   return run_int_gemm(st, A8, B8, m, n, kpad, 2, scale, row_scale, col_scale, c_units, c, ldc, s);
 }
 
+cudaLaunchAttribute pdl_attr() {
+  cudaLaunchAttribute a;
+  a.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a.val.programmaticStreamSerializationAllowed = 1;
+  return a;
+}
+
+constexpr int kMaxDynSmem = 232448;  // 227 KB opt-in per block on sm_100
+
+bool spmm_chunk_fits(int64_t k, int64_t rows_per_split) {
+  return spmm_smem_bytes(k, static_cast<int>(rows_per_split)) <= kMaxDynSmem;
+}
+
+// R.X for CSR rows, X [k][ldb] fp32. EXACT reproduces the reference rounding
+// (kernels.cpp:347); the fused layer uses fma and chains into the GEMM with PDL.
+template <bool EXACT, bool PDL_CHAIN>
+int run_spmm(DeviceState& st, int64_t rows, int64_t k, const uint64_t* row_ptr,
+             const uint64_t* col_idx, const float* vals, const float* b, int64_t n, int64_t ldb,
+             float* c, int64_t ldc, cudaStream_t s) {
+  const auto* rp = reinterpret_cast<const unsigned long long*>(row_ptr);
+  const auto* ci = reinterpret_cast<const unsigned long long*>(col_idx);
+  // ~6 waves of blocks at 2 resident blocks per SM, rows split evenly
+  const int chunks = static_cast<int>((n + SPMM_TOK - 1) / SPMM_TOK);
+  const int target = 12 * st.sms;
+  const int splits = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>((rows + SPMM_QUADS - 1) / SPMM_QUADS, (target + chunks - 1) / chunks)));
+  const int rows_per_split = static_cast<int>((rows + splits - 1) / splits);
+  if (!spmm_chunk_fits(k, rows_per_split)) {
+    // large K: X chunk does not fit in shared memory, gather rows from L2 instead
+    const long long warps = rows * ((n + 127) / 128);
+    ProfScope ps("spmm_csr_gather", s);
+    spmm_csr_kernel<<<blocks_for(warps * 32, 256), 256, 0, s>>>(rows, rp, ci, vals, b, ldb,
+                                                                static_cast<int>(n), c, ldc);
+    return launch_check("spmm_csr_kernel");
+  }
+  auto kern = spmm_xchunk_kernel<EXACT, PDL_CHAIN>;
+  const int smem = spmm_smem_bytes(k, rows_per_split);
+  const unsigned bit = 1u << (20 + (EXACT ? 1 : 0) + (PDL_CHAIN ? 2 : 0));
+  if (!(st.attr_mask & bit)) {
+    BITMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    st.attr_mask |= bit;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(chunks), static_cast<unsigned>(splits));
+  cfg.blockDim = dim3(SPMM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1] = {pdl_attr()};
+  cfg.attrs = attr;
+  cfg.numAttrs = PDL_CHAIN ? 1 : 0;
+  ProfScope ps(EXACT ? "spmm_xchunk_exact" : "spmm_xchunk", s);
+  BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, static_cast<int>(rows), static_cast<int>(k),
+                                    static_cast<int>(n), rp, ci, vals, b, ldb, c, ldc,
+                                    rows_per_split));
+  return launch_check("spmm_xchunk_kernel");
+}
+
 int apb_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, int64_t k, int64_t wpr, float gamma,
                  const float* row_gamma, const float* b, int64_t n, int64_t ldb,
                  const uint64_t* row_ptr, const uint64_t* col_idx, const float* vals, float* c,
                  int64_t ldc, cudaStream_t s) {
-  constexpr int kParts = 3;
   const int64_t kpad = round_up(k, 64);
   BITMM_TRY(arena_reserve(st.ws, ws_bytes_1x32(m, n, k)));
   Carve cv(st.ws.ptr);
   uint16_t* Abf = cv.take<uint16_t>(m * kpad * 2);
-  uint16_t* XT = cv.take<uint16_t>(n * kParts * kpad * 2);
+  uint16_t* XT = cv.take<uint16_t>(n * APB_PARTS * kpad * 2);
+  cudaLaunchAttribute pdl[1] = {pdl_attr()};
   {
     const int wpr32 = static_cast<int>(wpr * 2);
     const long long total = m * std::max<long long>(kpad / 32, wpr32);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks_for(total, 256));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cfg.attrs = pdl;
+    cfg.numAttrs = 1;
     ProfScope ps("unpack_sign_bf16", s);
-    unpack_sign_bf16<<<blocks_for(total, 256), 256, 0, s>>>(
-        reinterpret_cast<const uint32_t*>(w), m, wpr32, static_cast<int>(k),
-        static_cast<int>(kpad), Abf, st.status);
+    BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, unpack_sign_bf16, reinterpret_cast<const uint32_t*>(w),
+                                      static_cast<long long>(m), wpr32, static_cast<int>(k),
+                                      static_cast<int>(kpad), Abf, st.status));
     BITMM_TRY(launch_check("unpack_sign_bf16"));
   }
   {
-    dim3 grid(static_cast<unsigned>(kpad / 64), static_cast<unsigned>((n + 31) / 32));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(kpad / 64), static_cast<unsigned>((n + 31) / 32));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cfg.attrs = pdl;
+    cfg.numAttrs = 1;
     ProfScope ps("split_x_bf16", s);
-    split_x_bf16<<<grid, 256, 0, s>>>(b, ldb, static_cast<int>(k), static_cast<int>(n),
-                                      static_cast<int>(kpad), kParts, XT);
+    BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, split_x_bf16, b, static_cast<long long>(ldb),
+                                      static_cast<int>(k), static_cast<int>(n),
+                                      static_cast<int>(kpad), APB_PARTS, XT));
     BITMM_TRY(launch_check("split_x_bf16"));
   }
+  const bool has_res = row_ptr != nullptr;
+  if (has_res)
+    BITMM_TRY((run_spmm<false, true>(st, m, k, row_ptr, col_idx, vals, b, n, ldb, c, ldc, s)));
+
   CUtensorMap ta, tb;
-  BITMM_TRY(make_operand_map(&ta, Abf, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kpad, m, TcShape<false>::A_ROWS));
-  BITMM_TRY(make_operand_map(&tb, XT, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kParts * kpad, n, TcShape<false>::B_ROWS));
-  TcParams p{};
+  BITMM_TRY(make_operand_map(&ta, Abf, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kpad, m, 128));
+  BITMM_TRY(make_operand_map(&tb, XT, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, APB_PARTS * kpad, n, APB_BN / 2));
+  ApbParams p{};
   p.M = static_cast<int>(m);
   p.N = static_cast<int>(n);
-  p.a_kb_period = static_cast<int>(kpad / 64);
-  p.num_kb = kParts * p.a_kb_period;
-  p.scale = gamma;
-  p.row_scale = row_gamma;
-  p.out_f32 = c;
+  p.kb_per_part = static_cast<int>(kpad / 64);
+  p.kpad = static_cast<int>(kpad);
+  p.alpha = gamma;
+  p.row_alpha = row_gamma;
+  p.C = c;
   p.ldc = ldc;
-  p.csr_row_ptr = reinterpret_cast<const unsigned long long*>(row_ptr);
-  p.csr_col = reinterpret_cast<const unsigned long long*>(col_idx);
-  p.csr_val = vals;
-  p.X = b;
-  p.ldx = ldb;
-  return run_tc_gemm<Kind::BF16, Epi::APB, false>(st, ta, tb, p, s);
+  p.accumulate_c = has_res ? 1 : 0;
+  p.num_m_blocks = static_cast<int>((m + 255) / 256);
+  p.num_n_blocks = static_cast<int>((n + APB_BN - 1) / APB_BN);
+  p.num_tiles = p.num_m_blocks * p.num_n_blocks;
+  const unsigned bit = 1u << 28;
+  if (!(st.attr_mask & bit)) {
+    BITMM_CUDA_TRY(cudaFuncSetAttribute(apb_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, APB_SMEM));
+    st.attr_mask |= bit;
+  }
+  const int units = std::min(p.num_tiles, st.sms / 2);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(2 * units));
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = APB_SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1] = pdl_attr();
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  ProfScope ps("apb_gemm_bf16x3", s);
+  BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, apb_gemm_kernel, ta, tb, p));
+  return launch_check("apb_gemm_kernel");
 }
 
 int with_device(DeviceState** st) {
@@ -905,13 +999,8 @@ int bitmm_spmm_csr_dev(int64_t rows, int64_t cols, const uint64_t* row_ptr, cons
   if (!row_ptr || !b || !c) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
   DeviceState* st = nullptr;
   BITMM_TRY(with_device(&st));
-  const long long warps = rows * ((n + 127) / 128);
-  ProfScope ps("spmm_csr", static_cast<cudaStream_t>(stream));
-  spmm_csr_kernel<<<blocks_for(warps * 32, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      rows, reinterpret_cast<const unsigned long long*>(row_ptr),
-      reinterpret_cast<const unsigned long long*>(col_idx), vals, b, ldb, static_cast<int>(n), c,
-      ldc);
-  return launch_check("spmm_csr_kernel");
+  return run_spmm<true, false>(*st, rows, cols, row_ptr, col_idx, vals, b, n, ldb, c, ldc,
+                               static_cast<cudaStream_t>(stream));
 }
 
 int bitmm_spmm_csr_host(int64_t rows, int64_t cols, const uint64_t* row_ptr,

@@ -186,6 +186,8 @@ __global__ void unpack_level_i8(const uint32_t* __restrict__ t, const uint32_t* 
 __global__ void unpack_sign_bf16(const uint32_t* __restrict__ words, long long rows, int wpr32,
                                  int K, int kpad, uint16_t* __restrict__ out,
                                  int* __restrict__ err) {
+  pdl_wait();  // the previous kernel may still read the workspace we overwrite
+  pdl_launch_dependents();
   const int groups_out = kpad / 32;
   const int groups = max(groups_out, wpr32);
   const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -216,6 +218,8 @@ __global__ void unpack_sign_bf16(const uint32_t* __restrict__ words, long long r
 __global__ void split_x_bf16(const float* __restrict__ X, long long ldx, int K, int N, int kpad,
                              int nparts, uint16_t* __restrict__ XT) {
   __shared__ float tile[64][33];
+  pdl_wait();
+  pdl_launch_dependents();
   const int k0 = blockIdx.x * 64;
   const int n0 = blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;

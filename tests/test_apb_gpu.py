@@ -140,3 +140,36 @@ def test_layer_forward_empty_residual_and_odd_shapes(orc):
         got = api.layer_forward(layer, b)
         want = orc.gemm_1x32(layer.bin.words, k, layer.bin.words_per_row(), alpha, b)
         check_close(got, want)
+
+
+@pytest.mark.parametrize("k", [900, 1000, 4096])
+def test_large_k_layer_forward(orc, k):
+    """K past the shared-memory X chunk (spmm falls back to the L2 gather kernel) and K=4096,
+    where split accumulators keep the tensor-core fp32 accumulation within tolerance."""
+    rng = np.random.default_rng(k)
+    rows, tokens = 96, 200
+    a, alpha, _ = data.apb_weights(rng, rows, k)
+    layer = api.decompose_apb(a, alpha)
+    x = rng.standard_normal((k, tokens)).astype(np.float32)
+    got = api.layer_forward(layer, x)
+    r = layer.residual
+    want = orc.layer_forward(rows, k, 1.0, layer.bin.words, layer.bin.words_per_row(), r.row_ptr,
+                             r.col_idx, r.vals, x, row_alpha=alpha)
+    check_close(got, want)
+
+
+def test_spmm_exact_odd_shapes(orc):
+    # ragged columns (N % 4 != 0), empty rows, rows with > 8 nonzeros, single column
+    rng = np.random.default_rng(99)
+    for (rows, cols, n) in [(5, 3, 1), (33, 700, 37), (7, 64, 130), (300, 50, 33)]:
+        dens = rng.uniform(0.0, 0.6)
+        mask = rng.random((rows, cols)) < dens
+        mask[0] = False  # an empty row
+        vals = rng.standard_normal((rows, cols)).astype(np.float32)
+        r_idx, c_idx = np.nonzero(mask)
+        rp = np.zeros(rows + 1, np.uint64)
+        rp[1:] = np.cumsum(np.bincount(r_idx, minlength=rows))
+        csr = api.CsrMatrix.create(rows, cols, rp, c_idx.astype(np.uint64), vals[mask])
+        b = rng.standard_normal((cols, n)).astype(np.float32)
+        assert np.array_equal(api.spmm_csr(csr, b), orc.spmm_csr(rows, csr.row_ptr, csr.col_idx,
+                                                                 csr.vals, b))
