@@ -341,29 +341,37 @@ def main():
             device.gemm_2x2(x["wt"], x["wh"], x["wm"], x["at"], x["ah"], x["am"], k, units=x["units"])
         return device.launch_count()
 
-    def gather(name):
-        if world == 1:
-            return
-        src = d[name]["units"] if name != "1x2" else d[name]["out"]
-        n = [r for r in ROUTINES if r[0] == name][0][2]
-        parts = None
-        if rank == 0:
-            parts = []
-            for g in range(world):
-                lo, hi = shard_cols(n, g, world)
-                parts.append(torch.empty((src.shape[0], hi - lo), dtype=src.dtype, device=dev))
-        dist.gather(src, parts, dst=0)
-        if rank == 0:
-            for g, p in enumerate(parts):
-                lo, hi = shard_cols(n, g, world)
-                gathered[name][:, lo:hi].copy_(p)
+    from paper_2306_08960_b200 import shard
+
+    def sharded(name, m, n, k):
+        """N>1: each rank computes its column block in row chunks; blocks are gathered to
+        rank 0 over NCCL behind the next chunk's compute (paper_2306_08960_b200.shard)."""
+        x = d[name]
+        lo, _ = x["cols"]
+        dt = torch.float32 if name == "1x2" else torch.int32
+        launches = [0]
+
+        def compute(clo, chi, r0, r1, block):
+            if name == "1x1":
+                device.gemm_1x1(x["a"][r0:r1], x["b"], k, units=block)
+            elif name == "1x2":
+                device.gemm_1x2(x["w"][r0:r1], 1.0, x["t"], x["h"], x["m"], k,
+                                row_scale=x["gamma"][r0:r1], col_scale=x["beta"], out=block)
+            else:
+                device.gemm_2x2(x["wt"][r0:r1], x["wh"][r0:r1], x["wm"][r0:r1], x["at"], x["ah"],
+                                x["am"], k, units=block)
+            launches[0] += device.launch_count()
+
+        wire = shard.popcount_wire(k) if name == "1x1" else None
+        shard.run_sharded(m, n, dt, compute, dev, chunk_rows=m // 4, wire=wire,
+                          out=gathered.get(name))
+        return launches[0]
 
     def step(events):
         launches = 0
         events[0].record(stream)
         for i, (name, m, n, k) in enumerate(ROUTINES):
-            launches += run_routine(name, m, n, k)
-            gather(name)
+            launches += run_routine(name, m, n, k) if world == 1 else sharded(name, m, n, k)
             events[i + 1].record(stream)
         return launches
 
@@ -482,6 +490,7 @@ def main():
 
     if world == 1:
         line["apb"] = apb_pass(args, torch, lib, l2_flush, peaks)
+        line["c5_single_gpu"] = c5_pass(torch, peak)
     if world == 1 and not args.no_e2e:
         line["e2e"] = e2e_pass(args, ops, torch, lib)
     if world == 1 and not args.no_cpu_baseline:
@@ -496,6 +505,38 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def c5_pass(torch, peak):
+    """BASELINE config 5 at N=1: 1/1 M=N=K=32768, int32 units (the N-sharded sweep's single
+    GPU point). Two timed repetitions after one warm call (inputs >> L2)."""
+    from paper_2306_08960_b200 import data, device
+    rng = np.random.default_rng(SEED + 5)
+    m = n = k = 32768
+    a, _ = data.random_words(rng, m, k)
+    b, _ = data.random_words(rng, n, k)
+    da = torch.from_numpy(a.view(np.int64)).cuda()
+    db = torch.from_numpy(b.view(np.int64)).cuda()
+    u = torch.empty((m, n), dtype=torch.int32, device="cuda")
+    device.reserve_workspace(0, m, n, k)
+    device.gemm_1x1(da, db, k, units=u)
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(2):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        device.gemm_1x1(da, db, k, units=u)
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    device.status()
+    ms = min(times)
+    upd = m * n * k
+    del da, db, u
+    torch.cuda.empty_cache()
+    return {"workload": "1/1 32768^3, int32 units, packed operands resident", "ms": ms,
+            "T_updates_per_s": upd / (ms * 1e-3) / 1e12,
+            "frac_of_int8_peak": 2 * upd / (ms * 1e-3) / 1e12 / peak}
 
 
 def apb_pass(args, torch, lib, l2_flush, peaks):
