@@ -1,0 +1,134 @@
+// kernels_b200.cpp — reference-side binding of the B200 library (drop-in for the GEMM
+// bodies of /root/reference/proj/src/kernels.cpp:163-352 and apb.cpp:158-164).
+//
+// Compiled against the reference's OWN headers (include/bitmm/*.hpp) and linked in place
+// of those function bodies, it keeps every public signature, argument check, exception
+// type and message order of the reference, and routes the arithmetic through the C ABI
+// in include/bitmm_b200.h (host-pointer flavour: the result comes back as the
+// reference's DenseMatrix). The `threads` argument is validated and otherwise ignored
+// (results never depended on it, kernels.cpp:47-49).
+//
+// Build recipe (see INTEGRATION.md and oracle/Makefile target `dropin`): compile the
+// reference sources unmodified, weaken the six replaced symbols in their objects
+// (objcopy --weaken-symbol), link this file plus libbitmm_b200.so.
+#include <stdexcept>
+#include <string>
+
+#include "bitmm/apb.hpp"
+#include "bitmm/errors.hpp"
+#include "bitmm/kernels.hpp"
+#include "bitmm/tensor.hpp"
+#include "bitmm_b200.h"
+
+namespace bitmm {
+
+namespace {
+
+void raise_on(int rc) {
+  if (rc == BITMM_OK) return;
+  const std::string msg = bitmm_last_error();
+  if (rc == BITMM_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  if (rc == BITMM_ERR_INVALID_ENCODING) throw InvalidEncoding(msg);
+  throw std::runtime_error("bitmm_b200: " + msg);
+}
+
+void check_threads(int threads) {
+  if (threads < 1) throw std::invalid_argument("thread count must be at least 1");
+}
+
+void check_packed_pair(std::int64_t cols_a, std::size_t wpr_a, std::int64_t cols_b,
+                       std::size_t wpr_b) {
+  if (cols_a != cols_b || wpr_a != wpr_b)
+    throw std::invalid_argument("gemm dimension mismatch (packed rows must share K and padding)");
+}
+
+float plane_gamma(const ThmPlanes& p) { return p.gamma.value_or(1.0f); }
+
+}  // namespace
+
+DenseMatrix gemm_1x1(const BitMatrix& a, const BitMatrix& b_packed, float gamma_a, float gamma_b,
+                     int threads) {
+  check_packed_pair(a.cols(), a.words_per_row(), b_packed.cols(), b_packed.words_per_row());
+  GemmProblem{a.rows(), a.cols(), b_packed.rows()}.validate();
+  check_threads(threads);
+  DenseMatrix c(a.rows(), b_packed.rows());
+  raise_on(bitmm_gemm_1x1_host(a.row_data(0), a.rows(), b_packed.row_data(0), b_packed.rows(),
+                               a.cols(), static_cast<std::int64_t>(a.words_per_row()), gamma_a,
+                               gamma_b, nullptr, c.row_data(0), c.cols()));
+  return c;
+}
+
+DenseMatrix gemm_1x2(const BitMatrix& w, float gamma, const ThmPlanes& a_packed, int threads) {
+  a_packed.validate();  // InvalidEncoding first, as kernels.cpp:186
+  check_packed_pair(w.cols(), w.words_per_row(), a_packed.cols(), a_packed.t.words_per_row());
+  GemmProblem{w.rows(), w.cols(), a_packed.rows()}.validate();
+  check_threads(threads);
+  DenseMatrix c(w.rows(), a_packed.rows());
+  raise_on(bitmm_gemm_1x2_host(w.row_data(0), w.rows(), gamma, a_packed.t.row_data(0),
+                               a_packed.h.row_data(0), a_packed.m.row_data(0), a_packed.rows(),
+                               w.cols(), static_cast<std::int64_t>(w.words_per_row()),
+                               a_packed.scale, a_packed.gamma.has_value() ? 1 : 0,
+                               plane_gamma(a_packed), nullptr, nullptr, nullptr, c.row_data(0),
+                               c.cols()));
+  return c;
+}
+
+DenseMatrix gemm_2x2(const ThmPlanes& w, const ThmPlanes& a_packed, int threads) {
+  w.validate();  // kernels.cpp:224-225
+  a_packed.validate();
+  check_packed_pair(w.cols(), w.t.words_per_row(), a_packed.cols(), a_packed.t.words_per_row());
+  GemmProblem{w.rows(), w.cols(), a_packed.rows()}.validate();
+  check_threads(threads);
+  DenseMatrix c(w.rows(), a_packed.rows());
+  raise_on(bitmm_gemm_2x2_host(
+      w.t.row_data(0), w.h.row_data(0), w.m.row_data(0), w.rows(), w.scale,
+      w.gamma.has_value() ? 1 : 0, plane_gamma(w), a_packed.t.row_data(0), a_packed.h.row_data(0),
+      a_packed.m.row_data(0), a_packed.rows(), w.cols(),
+      static_cast<std::int64_t>(w.t.words_per_row()), a_packed.scale,
+      a_packed.gamma.has_value() ? 1 : 0, plane_gamma(a_packed), nullptr, nullptr, nullptr,
+      c.row_data(0), c.cols()));
+  return c;
+}
+
+DenseMatrix gemm_1x32_ref(const BitMatrix& w, float gamma, const DenseMatrix& b, int threads) {
+  if (w.cols() != b.rows()) throw std::invalid_argument("gemm dimension mismatch");
+  GemmProblem{w.rows(), w.cols(), b.cols()}.validate();
+  check_threads(threads);
+  DenseMatrix c(w.rows(), b.cols());
+  raise_on(bitmm_gemm_1x32_host(w.row_data(0), w.rows(), w.cols(),
+                                static_cast<std::int64_t>(w.words_per_row()), gamma, nullptr,
+                                b.row_data(0), b.cols(), b.cols(), c.row_data(0), c.cols()));
+  return c;
+}
+
+DenseMatrix spmm_csr(const CsrMatrix& a, const DenseMatrix& b, int threads) {
+  if (a.cols != b.rows()) throw std::invalid_argument("gemm dimension mismatch");
+  if (a.rows <= 0 || b.cols() <= 0 || a.cols <= 0)
+    throw std::invalid_argument("gemm dimensions must be positive");
+  if (a.cols > kMaxSharedDim)
+    throw std::invalid_argument("shared dimension exceeds the 2^20 accumulator bound");
+  check_threads(threads);
+  DenseMatrix c(a.rows, b.cols());
+  raise_on(bitmm_spmm_csr_host(a.rows, a.cols, a.row_ptr.data(), a.col_idx.data(), a.vals.data(),
+                               static_cast<std::int64_t>(a.nnz()), b.row_data(0), b.cols(),
+                               b.cols(), c.row_data(0), c.cols()));
+  return c;
+}
+
+DenseMatrix layer_forward(const ApbLayer& l, const DenseMatrix& b, int threads) {
+  // the reference's two calls (apb.cpp:159-160) perform these checks in this order
+  if (l.bin.cols() != b.rows()) throw std::invalid_argument("gemm dimension mismatch");
+  GemmProblem{l.bin.rows(), l.bin.cols(), b.cols()}.validate();
+  check_threads(threads);
+  if (l.residual.cols != b.rows()) throw std::invalid_argument("gemm dimension mismatch");
+  DenseMatrix c(l.bin.rows(), b.cols());
+  raise_on(bitmm_layer_forward_host(
+      l.bin.rows(), l.bin.cols(), l.alpha, nullptr, l.bin.row_data(0),
+      static_cast<std::int64_t>(l.bin.words_per_row()), l.residual.row_ptr.data(),
+      l.residual.col_idx.data(), l.residual.vals.data(),
+      static_cast<std::int64_t>(l.residual.nnz()), b.row_data(0), b.cols(), b.cols(),
+      c.row_data(0), c.cols()));
+  return c;
+}
+
+}  // namespace bitmm

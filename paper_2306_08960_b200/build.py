@@ -63,7 +63,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         + NVCC_FLAGS
         + ["-I", INCLUDE, "-I", CSRC, "-shared", "-o", tmp]
         + [os.path.join(CSRC, s) for s in SOURCES]
-        + ["-cudart", "static"]
+        + ["-cudart", "static", "-Xlinker", "-soname=libbitmm_b200.so"]
     )
     proc = subprocess.run(cmd, capture_output=True, text=True)
     log_path = os.path.join(PKG_DIR, "build.log")
