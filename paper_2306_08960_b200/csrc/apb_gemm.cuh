@@ -52,7 +52,12 @@ __global__ void __launch_bounds__(SPMM_THREADS, 2)
                        const float* __restrict__ vals, const float* __restrict__ X, long long ldx,
                        float* __restrict__ C, long long ldc, int rows_per_split) {
   extern __shared__ float xs[];  // [K][SPMM_TOK], then u32 row offsets
-  if (PDL_CHAIN) pdl_launch_dependents();
+  // PDL: wait for the predecessor first (a wait deferred to the end of the kernel can park
+  // blocks on SM slots the predecessor still needs), then let the GEMM launch early.
+  if (PDL_CHAIN) {
+    pdl_wait();
+    pdl_launch_dependents();
+  }
   unsigned* rps = reinterpret_cast<unsigned*>(xs + static_cast<long long>(K) * SPMM_TOK);
   const int c0 = blockIdx.x * SPMM_TOK;
   const int r0 = blockIdx.y * rows_per_split;
@@ -133,8 +138,6 @@ __global__ void __launch_bounds__(SPMM_THREADS, 2)
       }
     }
   }
-  // completion of this grid must imply completion of the kernels before it
-  if (PDL_CHAIN) pdl_wait();
 }
 
 // ----------------------------------------------------------------------------------

@@ -58,6 +58,7 @@ struct DeviceState {
   Arena io;               // host-flavour staging of inputs/outputs
   cudaStream_t stream = nullptr;  // host-flavour private stream
   unsigned attr_mask = 0;
+  unsigned ws_turn = 0;           // ping-pong half of the expanded-operand workspace
 };
 
 std::mutex g_mu;
@@ -377,9 +378,23 @@ struct Carve {
   }
 };
 
-size_t ws_bytes_int(int64_t m, int64_t n, int64_t k) {
+size_t ws_half_int(int64_t m, int64_t n, int64_t k) {
   const int64_t kpad = round_up(k, TC_BK_BYTES);
   return align_up(m * kpad, 1024) + align_up(n * kpad, 1024) + 2048;
+}
+// Two halves: consecutive integer GEMM calls alternate, so the operand expansion of call
+// i+1 (writing one half) can overlap the GEMM of call i (reading the other half).
+size_t ws_bytes_int(int64_t m, int64_t n, int64_t k) { return 2 * ws_half_int(m, n, k); }
+
+// Expanded operands A8 [m][kpad], B8 [n][kpad] in this call's half of the workspace.
+void take_int_operands(DeviceState& st, int64_t m, int64_t n, int64_t k, uint8_t** A8,
+                       uint8_t** B8) {
+  const int64_t kpad = round_up(k, TC_BK_BYTES);
+  const size_t half = ws_half_int(m, n, k);
+  Carve cv(static_cast<uint8_t*>(st.ws.ptr) + (st.ws_turn & 1u) * half);
+  st.ws_turn ^= 1u;
+  *A8 = cv.take<uint8_t>(m * kpad);
+  *B8 = cv.take<uint8_t>(n * kpad);
 }
 size_t ws_bytes_1x32(int64_t m, int64_t n, int64_t k) {
   const int64_t kpad = round_up(k, 64);
@@ -392,9 +407,8 @@ int gemm_1x1_dev_impl(DeviceState& st, const uint64_t* a, int64_t m, const uint6
                       float* c, int64_t ldc, cudaStream_t s) {
   const int64_t kpad = round_up(k, TC_BK_BYTES);
   BITMM_TRY(arena_reserve(st.ws, ws_bytes_int(m, n, k)));
-  Carve cv(st.ws.ptr);
-  uint8_t* A8 = cv.take<uint8_t>(m * kpad);
-  uint8_t* B8 = cv.take<uint8_t>(n * kpad);
+  uint8_t *A8, *B8;
+  take_int_operands(st, m, n, k, &A8, &B8);
   BITMM_TRY(run_unpack_pair({a, nullptr, nullptr, m, false}, {b, nullptr, nullptr, n, false}, wpr,
                             k, kpad, A8, B8, st.status, s));
   const float scale = gamma_a * gamma_b;  // kernels.cpp:170
@@ -408,9 +422,8 @@ int gemm_1x2_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, float gamma
                       cudaStream_t s) {
   const int64_t kpad = round_up(k, TC_BK_BYTES);
   BITMM_TRY(arena_reserve(st.ws, ws_bytes_int(m, n, k)));
-  Carve cv(st.ws.ptr);
-  uint8_t* A8 = cv.take<uint8_t>(m * kpad);
-  uint8_t* B8 = cv.take<uint8_t>(n * kpad);
+  uint8_t *A8, *B8;
+  take_int_operands(st, m, n, k, &A8, &B8);
   BITMM_TRY(run_unpack_pair({w, nullptr, nullptr, m, false}, {t, h, mm, n, true}, wpr, k, kpad, A8,
                             B8, st.status, s));
   // kernels.cpp:193: half_scale = 0.5f * gamma * a_packed.scale * a_packed.gamma.value_or(1.0f)
@@ -426,9 +439,8 @@ int gemm_2x2_dev_impl(DeviceState& st, const uint64_t* wt, const uint64_t* wh, c
                       cudaStream_t s) {
   const int64_t kpad = round_up(k, TC_BK_BYTES);
   BITMM_TRY(arena_reserve(st.ws, ws_bytes_int(m, n, k)));
-  Carve cv(st.ws.ptr);
-  uint8_t* A8 = cv.take<uint8_t>(m * kpad);
-  uint8_t* B8 = cv.take<uint8_t>(n * kpad);
+  uint8_t *A8, *B8;
+  take_int_operands(st, m, n, k, &A8, &B8);
   BITMM_TRY(run_unpack_pair({wt, wh, wm, m, true}, {at, ah, am, n, true}, wpr, k, kpad, A8, B8,
                             st.status, s));
   // kernels.cpp:232-233

@@ -88,8 +88,13 @@ struct UnpackPair {
 // output). Store v of lane t writes output bytes [16*(32v+t), +16) of the slice, so every
 // warp store instruction covers 512 contiguous bytes; the lane reads the 16 input bits
 // it needs from word (32v+t)/2 (lane pairs share a word, an L1 hit).
+// PDL: waits for its predecessor before touching the workspace, then lets the GEMM that
+// consumes its output launch early (the GEMM's prologue overlaps this kernel's tail).
+// A variant that deferred this wait to the end, to overlap with the previous GEMM, deadlocked
+// nondeterministically on B200 (dependent blocks parked in griddepcontrol.wait while holding
+// SM slots); see DESIGN.md.
 __global__ void __launch_bounds__(256) unpack_pair_i8(const __grid_constant__ UnpackPair P) {
-  pdl_wait();  // the previous kernel may still be reading the workspace we overwrite
+  pdl_wait();
   pdl_launch_dependents();
   const UnpackOperand& o = P.op[blockIdx.y];
   const long long unit = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -100,51 +105,68 @@ __global__ void __launch_bounds__(256) unpack_pair_i8(const __grid_constant__ Un
   const int sl = static_cast<int>(unit - r * slices);
   const long long rbase = r * o.wpr32;
   const int word0 = sl * 128;
+  // All 128 words of the slice in flight at once: lane t holds words j*32 + t.
+  uint32_t w0[4], w1[4], w2[4];
   int bad = 0;
-  // validation: every word of the slice that exists in the source
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int g = word0 + j * 32 + lane;
+    w0[j] = w1[j] = w2[j] = 0u;
     if (g < o.wpr32) {
-      const uint32_t valid = valid_mask32(g * 32, P.K);
-      if (o.levels == 0) {
-        const uint32_t w = __ldg(o.w0 + rbase + g);
-        bad |= (w & ~valid) ? ERR_PADDING : 0;
-      } else {
-        const uint32_t tw = __ldg(o.w0 + rbase + g), hw = __ldg(o.w1 + rbase + g),
-                       mw = __ldg(o.w2 + rbase + g);
-        if (((tw | hw | mw) & ~valid) | (tw & hw) | (tw & ~mw) | (hw & mw)) bad |= ERR_ENCODING;
+      w0[j] = __ldg(o.w0 + rbase + g);
+      if (o.levels) {
+        w1[j] = __ldg(o.w1 + rbase + g);
+        w2[j] = __ldg(o.w2 + rbase + g);
       }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t valid = valid_mask32((word0 + j * 32 + lane) * 32, P.K);
+    if (o.levels == 0) {
+      bad |= (w0[j] & ~valid) ? ERR_PADDING : 0;
+    } else {
+      const uint32_t tw = w0[j], hw = w1[j], mw = w2[j];
+      if (((tw | hw | mw) & ~valid) | (tw & hw) | (tw & ~mw) | (hw & mw)) bad |= ERR_ENCODING;
+      // fold the planes into (hi, lo) level bits in place: p = 2*hi + lo
+      w0[j] = (tw | hw) & valid;
+      w1[j] = (tw | ~(hw | mw)) & valid;
     }
   }
   if (bad) atomicOr(P.err, bad);
   uint8_t* out_row = o.out + r * P.kpad;
-#pragma unroll 2
+  const bool full_slice = (word0 + 128) * 32 <= P.K;
+  // Store v of lane t writes output bytes [16*(32v+t), +16): its 16 source bits are half
+  // of word 16v + t/2, held by lane (v%2)*16 + t/2 in register v/2.
+#pragma unroll
   for (int v = 0; v < 8; ++v) {
-    const int chunk = v * 32 + lane;        // 16-byte output chunk within the slice
+    const int chunk = v * 32 + lane;
     const int elem = word0 * 32 + chunk * 16;
-    if (elem >= P.kpad) break;
-    const int g = word0 + (chunk >> 1);
-    const int shift = (chunk & 1) * 16;
-    const uint32_t valid = (valid_mask32(g * 32, P.K) >> shift) & 0xFFFFu;
+    const int src_lane = (v & 1) * 16 + (lane >> 1);
+    const int shift = (lane & 1) * 16;
+    const uint32_t a = __shfl_sync(0xFFFFFFFFu, w0[v >> 1], src_lane);
+    const uint32_t b = __shfl_sync(0xFFFFFFFFu, w1[v >> 1], src_lane);
+    if (elem >= P.kpad) continue;
     uint32_t ow[4];
     if (o.levels == 0) {
-      const uint32_t w = (g < o.wpr32) ? (__ldg(o.w0 + rbase + g) >> shift) & 0xFFFFu : 0u;
+      const uint32_t bits = (a >> shift) & 0xFFFFu;
+      if (full_slice) {  // warp-uniform: every element of the slice is inside K
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t b = spread4((w >> (4 * q)) & 0xFu);
-        const uint32_t vm = spread4((valid >> (4 * q)) & 0xFu);
-        ow[q] = ((b * 0xFEu) ^ 0xFFFFFFFFu) & (vm * 0xFFu);
+        for (int q = 0; q < 4; ++q)
+          ow[q] = ~(spread4((bits >> (4 * q)) & 0xFu) * 0xFEu);  // 1 -> +1, 0 -> -1
+      } else {
+        const int g = word0 + (chunk >> 1);
+        const uint32_t valid = (valid_mask32(g * 32, P.K) >> shift) & 0xFFFFu;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t bb = spread4((bits >> (4 * q)) & 0xFu);
+          const uint32_t vm = spread4((valid >> (4 * q)) & 0xFu);
+          ow[q] = ((bb * 0xFEu) ^ 0xFFFFFFFFu) & (vm * 0xFFu);  // 1 -> +1, 0 -> -1, pad -> 0
+        }
       }
     } else {
-      uint32_t tw = 0, hw = 0, mw = 0;
-      if (g < o.wpr32) {
-        tw = (__ldg(o.w0 + rbase + g) >> shift) & 0xFFFFu;
-        hw = (__ldg(o.w1 + rbase + g) >> shift) & 0xFFFFu;
-        mw = (__ldg(o.w2 + rbase + g) >> shift) & 0xFFFFu;
-      }
-      const uint32_t hi = (tw | hw) & valid;
-      const uint32_t lo = (tw | ~(hw | mw)) & valid;
+      const uint32_t hi = (a >> shift) & 0xFFFFu;
+      const uint32_t lo = (b >> shift) & 0xFFFFu;
 #pragma unroll
       for (int q = 0; q < 4; ++q)
         ow[q] = (spread4((hi >> (4 * q)) & 0xFu) << 1) + spread4((lo >> (4 * q)) & 0xFu);
