@@ -210,18 +210,6 @@ unsigned blocks_for(long long total, int threads) {
   return static_cast<unsigned>((total + threads - 1) / threads);
 }
 
-int run_unpack_sign_i8(const uint64_t* words, int64_t rows, int64_t wpr, int64_t k, int64_t kpad,
-                       uint8_t* out, int* flag, cudaStream_t s) {
-  const int wpr32 = static_cast<int>(wpr * 2);
-  const long long total = rows * std::max<long long>(kpad / 32, wpr32);
-  if (total == 0) return BITMM_OK;
-  ProfScope ps("unpack_sign_i8", s);
-  unpack_sign_i8<<<blocks_for(total, 256), 256, 0, s>>>(reinterpret_cast<const uint32_t*>(words),
-                                                        rows, wpr32, static_cast<int>(k),
-                                                        static_cast<int>(kpad), out, flag);
-  return launch_check("unpack_sign_i8");
-}
-
 int run_unpack_level_i8(const uint64_t* t, const uint64_t* h, const uint64_t* m, int64_t rows,
                         int64_t wpr, int64_t k, int64_t kpad, uint8_t* out, int* flag,
                         cudaStream_t s) {

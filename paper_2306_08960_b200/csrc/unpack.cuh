@@ -7,8 +7,9 @@
 //
 // Outputs are K-major operand rows padded to kpad elements with zeros, so the
 // padding never contributes to a product:
-//   unpack_sign_i8   : bit b -> int8 (2b-1)               (BitMatrix, tensor.hpp:59)
-//   unpack_level_i8  : planes {t,h,m} -> int8 level p      (ThmPlanes, tensor.hpp:134;
+//   unpack_pair_i8   : both GEMM operands in one launch:
+//                      bit b -> int8 (2b-1)                (BitMatrix, tensor.hpp:59)
+//                      planes {t,h,m} -> int8 level p      (ThmPlanes, tensor.hpp:134;
 //                      legal states per transform.cpp:47-75: p0=(0,0,1) p1=(0,0,0)
 //                      p2=(0,1,0) p3=(1,0,1), so p = 2(t|h) + (t | ~(h|m)))
 //   unpack_sign_bf16 : bit b -> bf16 (+1/-1)               (APB binary plane)
@@ -38,41 +39,14 @@ __device__ __forceinline__ uint32_t valid_mask32(int kbase, int K) {
   return (1u << (K - kbase)) - 1u;
 }
 
-// One thread per (row, 32-element group). Groups beyond kpad only validate padding.
-__global__ void unpack_sign_i8(const uint32_t* __restrict__ words, long long rows, int wpr32, int K,
-                               int kpad, uint8_t* __restrict__ out, int* __restrict__ err) {
-  const int groups_out = kpad / 32;
-  const int groups = max(groups_out, wpr32);
-  const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (gid >= rows * groups) return;
-  const long long r = gid / groups;
-  const int g = static_cast<int>(gid - r * groups);
-  const uint32_t w = (g < wpr32) ? words[r * wpr32 + g] : 0u;
-  const uint32_t valid = valid_mask32(g * 32, K);
-  if (w & ~valid) atomicOr(err, ERR_PADDING);
-  if (g >= groups_out) return;
-  uint32_t o[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const uint32_t b = spread4((w >> (4 * q)) & 0xFu);
-    const uint32_t vm = spread4((valid >> (4 * q)) & 0xFu);
-    o[q] = ((b * 0xFEu) ^ 0xFFFFFFFFu) & (vm * 0xFFu);  // 1 -> 0x01, 0 -> 0xFF, pad -> 0
-  }
-  uint4* dst = reinterpret_cast<uint4*>(out + r * kpad + g * 32);
-  dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
-  dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
-}
-
-// Both GEMM operands in one launch (blockIdx.y selects the operand). Each thread
-// expands 4 consecutive 32-bit words (128 elements) of one row into 128 output
-// bytes: 16-byte loads/stores, 8 stores in flight per thread.
+// Operand descriptors for the pair expansion (blockIdx.y / op index selects the operand).
 struct UnpackOperand {
   const uint32_t* w0;  // sign words, or the t plane
   const uint32_t* w1;  // h plane (levels only)
   const uint32_t* w2;  // m plane (levels only)
   uint8_t* out;        // [rows][kpad]
   long long rows;
-  long long groups_per_row;  // ceil(max(kpad/32, wpr32) / 4)
+  long long groups_per_row;  // slices of 128 words (4096 elements) per row
   int wpr32;
   int levels;  // 0: +-1 signs, 1: 2-bit levels
 };
@@ -84,69 +58,63 @@ struct UnpackPair {
   int* err;
 };
 
-// Work unit = one warp x one 4096-element slice of a row (128 input words, 4 KB of
-// output). Store v of lane t writes output bytes [16*(32v+t), +16) of the slice, so every
-// warp store instruction covers 512 contiguous bytes; the lane reads the 16 input bits
-// it needs from word (32v+t)/2 (lane pairs share a word, an L1 hit).
-// PDL: waits for its predecessor before touching the workspace, then lets the GEMM that
-// consumes its output launch early (the GEMM's prologue overlaps this kernel's tail).
-// A variant that deferred this wait to the end, to overlap with the previous GEMM, deadlocked
-// nondeterministically on B200 (dependent blocks parked in griddepcontrol.wait while holding
-// SM slots); see DESIGN.md.
-__global__ void __launch_bounds__(256) unpack_pair_i8(const __grid_constant__ UnpackPair P) {
-  pdl_wait();
-  pdl_launch_dependents();
-  const UnpackOperand& o = P.op[blockIdx.y];
-  const long long unit = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const long long slices = o.groups_per_row;  // slices of 128 words per row
-  if (unit >= o.rows * slices) return;
-  const long long r = unit / slices;
-  const int sl = static_cast<int>(unit - r * slices);
+// One warp expands one 4096-element slice of one operand row (128 input words, 4 KB of
+// int8 output), split into a load step (all 128 words in flight: lane t holds words
+// j*32 + t) and an expand/store step, so a warp looping over slices can prefetch the next
+// slice while expanding the current one. Store v of lane t writes output bytes
+// [16*(32v+t), +16): every warp store instruction covers 512 contiguous bytes, and its 16
+// source bits (half of word 16v + t/2) come from the loading lane via a shuffle.
+struct SliceWords {
+  uint32_t w0[4], w1[4], w2[4];
+};
+
+__device__ __forceinline__ void load_slice_warp(const UnpackOperand& o, long long r, int sl,
+                                                int lane, SliceWords& s) {
   const long long rbase = r * o.wpr32;
   const int word0 = sl * 128;
-  // All 128 words of the slice in flight at once: lane t holds words j*32 + t.
-  uint32_t w0[4], w1[4], w2[4];
-  int bad = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int g = word0 + j * 32 + lane;
-    w0[j] = w1[j] = w2[j] = 0u;
+    s.w0[j] = s.w1[j] = s.w2[j] = 0u;
     if (g < o.wpr32) {
-      w0[j] = __ldg(o.w0 + rbase + g);
+      s.w0[j] = __ldg(o.w0 + rbase + g);
       if (o.levels) {
-        w1[j] = __ldg(o.w1 + rbase + g);
-        w2[j] = __ldg(o.w2 + rbase + g);
+        s.w1[j] = __ldg(o.w1 + rbase + g);
+        s.w2[j] = __ldg(o.w2 + rbase + g);
       }
     }
   }
+}
+
+// Returns the warp-wide OR of the slice's error flags.
+__device__ __forceinline__ int expand_slice_warp(const UnpackOperand& o, long long r, int sl,
+                                                 int K, int kpad, int lane, SliceWords& s) {
+  const int word0 = sl * 128;
+  int bad = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const uint32_t valid = valid_mask32((word0 + j * 32 + lane) * 32, P.K);
+    const uint32_t valid = valid_mask32((word0 + j * 32 + lane) * 32, K);
     if (o.levels == 0) {
-      bad |= (w0[j] & ~valid) ? ERR_PADDING : 0;
+      bad |= (s.w0[j] & ~valid) ? ERR_PADDING : 0;
     } else {
-      const uint32_t tw = w0[j], hw = w1[j], mw = w2[j];
+      const uint32_t tw = s.w0[j], hw = s.w1[j], mw = s.w2[j];
       if (((tw | hw | mw) & ~valid) | (tw & hw) | (tw & ~mw) | (hw & mw)) bad |= ERR_ENCODING;
       // fold the planes into (hi, lo) level bits in place: p = 2*hi + lo
-      w0[j] = (tw | hw) & valid;
-      w1[j] = (tw | ~(hw | mw)) & valid;
+      s.w0[j] = (tw | hw) & valid;
+      s.w1[j] = (tw | ~(hw | mw)) & valid;
     }
   }
-  if (bad) atomicOr(P.err, bad);
-  uint8_t* out_row = o.out + r * P.kpad;
-  const bool full_slice = (word0 + 128) * 32 <= P.K;
-  // Store v of lane t writes output bytes [16*(32v+t), +16): its 16 source bits are half
-  // of word 16v + t/2, held by lane (v%2)*16 + t/2 in register v/2.
+  uint8_t* out_row = o.out + r * kpad;
+  const bool full_slice = (word0 + 128) * 32 <= K;
 #pragma unroll
   for (int v = 0; v < 8; ++v) {
     const int chunk = v * 32 + lane;
     const int elem = word0 * 32 + chunk * 16;
     const int src_lane = (v & 1) * 16 + (lane >> 1);
     const int shift = (lane & 1) * 16;
-    const uint32_t a = __shfl_sync(0xFFFFFFFFu, w0[v >> 1], src_lane);
-    const uint32_t b = __shfl_sync(0xFFFFFFFFu, w1[v >> 1], src_lane);
-    if (elem >= P.kpad) continue;
+    const uint32_t a = __shfl_sync(0xFFFFFFFFu, s.w0[v >> 1], src_lane);
+    const uint32_t b = __shfl_sync(0xFFFFFFFFu, s.w1[v >> 1], src_lane);
+    if (elem >= kpad) continue;
     uint32_t ow[4];
     if (o.levels == 0) {
       const uint32_t bits = (a >> shift) & 0xFFFFu;
@@ -156,7 +124,7 @@ __global__ void __launch_bounds__(256) unpack_pair_i8(const __grid_constant__ Un
           ow[q] = ~(spread4((bits >> (4 * q)) & 0xFu) * 0xFEu);  // 1 -> +1, 0 -> -1
       } else {
         const int g = word0 + (chunk >> 1);
-        const uint32_t valid = (valid_mask32(g * 32, P.K) >> shift) & 0xFFFFu;
+        const uint32_t valid = (valid_mask32(g * 32, K) >> shift) & 0xFFFFu;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const uint32_t bb = spread4((bits >> (4 * q)) & 0xFu);
@@ -173,6 +141,34 @@ __global__ void __launch_bounds__(256) unpack_pair_i8(const __grid_constant__ Un
     }
     *reinterpret_cast<uint4*>(out_row + elem) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
   }
+  return __reduce_or_sync(0xFFFFFFFFu, bad);
+}
+
+__device__ __forceinline__ int unpack_slice_warp(const UnpackOperand& o, long long r, int sl, int K,
+                                                 int kpad, int lane) {
+  SliceWords s;
+  load_slice_warp(o, r, sl, lane, s);
+  return expand_slice_warp(o, r, sl, K, kpad, lane, s);
+}
+
+// Standalone expansion of both GEMM operands (blockIdx.y selects the operand).
+// PDL: waits for its predecessor before touching the workspace, then lets the GEMM that
+// consumes its output launch early (the GEMM's prologue overlaps this kernel's tail).
+// A variant that deferred this wait to the end, to overlap with the previous GEMM, deadlocked
+// nondeterministically on B200 (dependent blocks parked in griddepcontrol.wait while holding
+// SM slots); see DESIGN.md.
+__global__ void __launch_bounds__(256) unpack_pair_i8(const __grid_constant__ UnpackPair P) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const UnpackOperand& o = P.op[blockIdx.y];
+  const long long unit = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long slices = o.groups_per_row;  // slices of 128 words per row
+  if (unit >= o.rows * slices) return;
+  const long long r = unit / slices;
+  const int sl = static_cast<int>(unit - r * slices);
+  const int bad = unpack_slice_warp(o, r, sl, P.K, P.kpad, lane);
+  if (bad && lane == 0) atomicOr(P.err, bad);
 }
 
 __global__ void unpack_level_i8(const uint32_t* __restrict__ t, const uint32_t* __restrict__ h,
