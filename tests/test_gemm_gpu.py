@@ -324,3 +324,28 @@ def test_full_size_1x1_32768_sampled(orc):
     cols = _sample_rows(rng, n, 4)
     wantc = orc.gemm_1x1(a, b[cols], k, wpr)[0]
     assert np.array_equal(u[:, torch.from_numpy(cols).cuda()].cpu().numpy(), wantc)
+
+
+@pytest.mark.parametrize("m,n,k", [(256, 256, 1 << 16), (8192, 4352, 2048), (300, 700, 4000)])
+def test_long_k_and_ragged_tiles_exact(orc, m, n, k):
+    """Long K (one tile, 512 K-blocks), a partial last N-tile (4352 = 17 x 256) and ragged
+    M/N: every sampled row equals the integer oracle and all cells match the independent
+    CUDA-core kernel; repeated launches are bit-identical."""
+    import torch
+    from paper_2306_08960_b200 import device
+    rng = np.random.default_rng(m + n + k)
+    a, wpr = data.random_words(rng, m, k)
+    b, _ = data.random_words(rng, n, k)
+    u = torch.empty((m, n), dtype=torch.int32, device="cuda")
+    f = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    T = lambda x: torch.from_numpy(x.view(np.int64)).cuda()  # noqa: E731
+    for _ in range(3):
+        device.gemm_1x1(T(a), T(b), k, 0.5, 0.75, units=u, out=f)
+    device.status()
+    rows = np.unique(np.concatenate([np.arange(min(m, 4)), rng.choice(m, 12), [m - 1]]))
+    want_u, want_f = orc.gemm_1x1(a[rows], b, k, wpr, 0.5, 0.75)
+    assert np.array_equal(u.cpu().numpy()[rows], want_u)
+    assert np.array_equal(f.cpu().numpy()[rows], want_f)
+    up = torch.empty_like(u)
+    device.gemm_1x1(T(a), T(b), k, units=up, popc=True)
+    assert torch.equal(u, up)
