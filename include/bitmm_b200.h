@@ -154,6 +154,21 @@ int bitmm_layer_forward_host(int64_t rows, int64_t cols, float alpha, const floa
                              const uint64_t* col_idx, const float* vals, int64_t nnz,
                              const float* b, int64_t n, int64_t ldb, float* c, int64_t ldc);
 
+/* ---- GPU packers (dense fp32 -> reference packed layouts) ----
+ * pack_signs: replaces pack_signs (tensor.hpp:248, tensor.cpp:155-164): bit i of row r is
+ *   (a[r][i] >= 0) (sign(0) = +1), rows of `wpr` u64 words with zero padding (wpr >= ceil(cols/64);
+ *   the reference's default 512-bit lanes give wpr = ceil(cols/512)*8).
+ * quantize_thm: replaces quantize_uniform_2bit + decompose_thm (transform.hpp:29,47;
+ *   transform.cpp:21-36, 47-75): level = clamp(lround(a/s), 0, 3) -> {t,h,m} planes. */
+int bitmm_pack_signs_dev(const float* a, int64_t rows, int64_t cols, int64_t lda, uint64_t* words,
+                         int64_t wpr, void* stream);
+int bitmm_pack_signs_host(const float* a, int64_t rows, int64_t cols, int64_t lda, uint64_t* words,
+                          int64_t wpr);
+int bitmm_quantize_thm_dev(const float* a, int64_t rows, int64_t cols, int64_t lda, float s,
+                           uint64_t* t, uint64_t* h, uint64_t* m, int64_t wpr, void* stream);
+int bitmm_quantize_thm_host(const float* a, int64_t rows, int64_t cols, int64_t lda, float s,
+                            uint64_t* t, uint64_t* h, uint64_t* m, int64_t wpr);
+
 #ifdef __cplusplus
 }
 #endif

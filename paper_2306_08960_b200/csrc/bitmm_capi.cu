@@ -13,6 +13,7 @@
 
 #include "apb_gemm.cuh"
 #include "bitmm_b200.h"
+#include "pack.cuh"
 #include "popc_gemm.cuh"
 #include "ptx.cuh"
 #include "tc_gemm.cuh"
@@ -1035,6 +1036,100 @@ int bitmm_spmm_csr_host(int64_t rows, int64_t cols, const uint64_t* row_ptr,
   }
   BITMM_TRY(bitmm_spmm_csr_dev(rows, cols, drp, dci, dv, db, n, ldb, dc, ldc, s));
   BITMM_CUDA_TRY(cudaMemcpyAsync(c, dc, c_bytes, cudaMemcpyDeviceToHost, s));
+  BITMM_CUDA_TRY(cudaStreamSynchronize(s));
+  return BITMM_OK;
+}
+
+// ---------------- GPU packers ----------------
+static int check_pack_args(int64_t rows, int64_t cols, int64_t lda, int64_t wpr) {
+  if (rows < 0 || cols < 0) return fail(BITMM_ERR_INVALID_ARGUMENT, "matrix dimensions must be non-negative");
+  if (wpr * 64 < cols) return fail(BITMM_ERR_INVALID_ARGUMENT, "words_per_row too small for the column count");
+  if (lda < cols) return fail(BITMM_ERR_INVALID_ARGUMENT, "leading dimension smaller than the column count");
+  if (cols > INT32_MAX / 2 || wpr > INT32_MAX / 128) return fail(BITMM_ERR_INVALID_ARGUMENT, "matrix too wide");
+  return BITMM_OK;
+}
+
+static unsigned pack_blocks(const DeviceState& st, int64_t rows, int64_t wpr) {
+  const long long units = rows * ((wpr + PACK_WORDS_PER_WARP - 1) / PACK_WORDS_PER_WARP);
+  const long long blocks = (units + 7) / 8;  // 8 warps per 256-thread block
+  return static_cast<unsigned>(std::max<long long>(1, std::min<long long>(blocks, 32LL * st.sms)));
+}
+
+int bitmm_pack_signs_dev(const float* a, int64_t rows, int64_t cols, int64_t lda, uint64_t* words,
+                         int64_t wpr, void* stream) {
+  g_launches = 0;
+  BITMM_TRY(check_pack_args(rows, cols, lda, wpr));
+  if (rows == 0 || wpr == 0) return BITMM_OK;
+  if (!words || (cols > 0 && !a)) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ProfScope ps("pack_signs", s);
+  pack_signs_kernel<<<pack_blocks(*st, rows, wpr), 256, 0, s>>>(
+      a, rows, static_cast<int>(cols), lda, static_cast<int>(wpr),
+      reinterpret_cast<unsigned long long*>(words));
+  return launch_check("pack_signs_kernel");
+}
+
+int bitmm_quantize_thm_dev(const float* a, int64_t rows, int64_t cols, int64_t lda, float s_step,
+                           uint64_t* t, uint64_t* h, uint64_t* m, int64_t wpr, void* stream) {
+  g_launches = 0;
+  if (!(s_step > 0.0f)) return fail(BITMM_ERR_INVALID_ARGUMENT, "quantization step must be positive");
+  BITMM_TRY(check_pack_args(rows, cols, lda, wpr));
+  if (rows == 0 || wpr == 0) return BITMM_OK;
+  if (!t || !h || !m || (cols > 0 && !a)) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ProfScope ps("quantize_thm", s);
+  quantize_thm_kernel<<<pack_blocks(*st, rows, wpr), 256, 0, s>>>(
+      a, rows, static_cast<int>(cols), lda, s_step, static_cast<int>(wpr),
+      reinterpret_cast<unsigned long long*>(t), reinterpret_cast<unsigned long long*>(h),
+      reinterpret_cast<unsigned long long*>(m));
+  return launch_check("quantize_thm_kernel");
+}
+
+int bitmm_pack_signs_host(const float* a, int64_t rows, int64_t cols, int64_t lda, uint64_t* words,
+                          int64_t wpr) {
+  g_launches = 0;
+  BITMM_TRY(check_pack_args(rows, cols, lda, wpr));
+  if (rows == 0 || wpr == 0) return BITMM_OK;
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  cudaStream_t s = st->stream;
+  const size_t a_bytes = rows * lda * 4, w_bytes = rows * wpr * 8;
+  BITMM_TRY(arena_reserve(st->io, align_up(a_bytes, 1024) + align_up(w_bytes, 1024) + 2048));
+  Carve cv(st->io.ptr);
+  float* da = cv.take<float>(a_bytes);
+  uint64_t* dw = cv.take<uint64_t>(w_bytes);
+  BITMM_CUDA_TRY(cudaMemcpyAsync(da, a, a_bytes, cudaMemcpyHostToDevice, s));
+  BITMM_TRY(bitmm_pack_signs_dev(da, rows, cols, lda, dw, wpr, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(words, dw, w_bytes, cudaMemcpyDeviceToHost, s));
+  BITMM_CUDA_TRY(cudaStreamSynchronize(s));
+  return BITMM_OK;
+}
+
+int bitmm_quantize_thm_host(const float* a, int64_t rows, int64_t cols, int64_t lda, float s_step,
+                            uint64_t* t, uint64_t* h, uint64_t* m, int64_t wpr) {
+  g_launches = 0;
+  if (!(s_step > 0.0f)) return fail(BITMM_ERR_INVALID_ARGUMENT, "quantization step must be positive");
+  BITMM_TRY(check_pack_args(rows, cols, lda, wpr));
+  if (rows == 0 || wpr == 0) return BITMM_OK;
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  cudaStream_t s = st->stream;
+  const size_t a_bytes = rows * lda * 4, w_bytes = rows * wpr * 8;
+  BITMM_TRY(arena_reserve(st->io, align_up(a_bytes, 1024) + 3 * align_up(w_bytes, 1024) + 4096));
+  Carve cv(st->io.ptr);
+  float* da = cv.take<float>(a_bytes);
+  uint64_t* dt = cv.take<uint64_t>(w_bytes);
+  uint64_t* dh = cv.take<uint64_t>(w_bytes);
+  uint64_t* dm = cv.take<uint64_t>(w_bytes);
+  BITMM_CUDA_TRY(cudaMemcpyAsync(da, a, a_bytes, cudaMemcpyHostToDevice, s));
+  BITMM_TRY(bitmm_quantize_thm_dev(da, rows, cols, lda, s_step, dt, dh, dm, wpr, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(t, dt, w_bytes, cudaMemcpyDeviceToHost, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(h, dh, w_bytes, cudaMemcpyDeviceToHost, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(m, dm, w_bytes, cudaMemcpyDeviceToHost, s));
   BITMM_CUDA_TRY(cudaStreamSynchronize(s));
   return BITMM_OK;
 }

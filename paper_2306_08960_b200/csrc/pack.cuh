@@ -1,0 +1,90 @@
+// GPU packers: dense fp32 -> the reference's packed layouts.
+//
+//   pack_signs_kernel      : tensor.cpp:155-164 — bit i of row r = (a[r][i] >= 0), sign(0)=+1
+//   quantize_thm_kernel    : transform.cpp:21-36 (lround(v/s), clamp to [0,3]) followed by
+//                            decompose_thm, transform.cpp:47-75 (p0=(0,0,1) p1=(0,0,0)
+//                            p2=(0,1,0) p3=(1,0,1))
+//
+// Output rows are `wpr` uint64 words (wpr >= ceil(cols/64), e.g. 512-bit lanes), element i
+// at word i/64 bit i%64, and every padding bit is zero (tensor.hpp:14-16). A warp covers 32
+// consecutive elements per __ballot_sync; two ballots form one uint64 word, written by lane 0.
+// Reads are coalesced (32 consecutive floats per warp step); each warp walks a row segment of
+// 64 * WORDS_PER_WARP elements so every warp writes whole words.
+#pragma once
+
+#include <cstdint>
+
+namespace bitmm_dev {
+
+constexpr int PACK_WORDS_PER_WARP = 4;  // 256 elements per warp work unit
+
+// lround(v / s) clamped to [0, 3]: halves away from zero (std::lround) on the fp32 quotient,
+// as quantize_uniform_2bit computes `v / s` in float (transform.cpp:224). `/` is IEEE
+// round-to-nearest division here (no fast-math), matching the host.
+__device__ __forceinline__ int quantize_level(float v, float s) {
+  long p = lroundf(v / s);
+  p = p < 0 ? 0 : p;
+  return static_cast<int>(p > 3 ? 3 : p);
+}
+
+// One warp per (row, 256-element segment); grid-stride over units.
+__global__ void pack_signs_kernel(const float* __restrict__ a, long long rows, int cols,
+                                  long long lda, int wpr, unsigned long long* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  const int segs = (wpr + PACK_WORDS_PER_WARP - 1) / PACK_WORDS_PER_WARP;
+  for (long long u = warp; u < rows * segs; u += nwarps) {
+    const long long r = u / segs;
+    const int w0 = static_cast<int>(u - r * segs) * PACK_WORDS_PER_WARP;
+    const float* row = a + r * lda;
+#pragma unroll
+    for (int w = 0; w < PACK_WORDS_PER_WARP; ++w) {
+      const int word = w0 + w;
+      if (word >= wpr) break;
+      const int e0 = word * 64 + lane, e1 = e0 + 32;
+      const unsigned lo = __ballot_sync(0xFFFFFFFFu, e0 < cols && row[e0] >= 0.0f);
+      const unsigned hi = __ballot_sync(0xFFFFFFFFu, e1 < cols && row[e1] >= 0.0f);
+      if (lane == 0)
+        out[r * wpr + word] = (static_cast<unsigned long long>(hi) << 32) | lo;
+    }
+  }
+}
+
+__global__ void quantize_thm_kernel(const float* __restrict__ a, long long rows, int cols,
+                                    long long lda, float s, int wpr,
+                                    unsigned long long* __restrict__ t,
+                                    unsigned long long* __restrict__ h,
+                                    unsigned long long* __restrict__ m) {
+  const int lane = threadIdx.x & 31;
+  const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  const int segs = (wpr + PACK_WORDS_PER_WARP - 1) / PACK_WORDS_PER_WARP;
+  for (long long u = warp; u < rows * segs; u += nwarps) {
+    const long long r = u / segs;
+    const int w0 = static_cast<int>(u - r * segs) * PACK_WORDS_PER_WARP;
+    const float* row = a + r * lda;
+#pragma unroll
+    for (int w = 0; w < PACK_WORDS_PER_WARP; ++w) {
+      const int word = w0 + w;
+      if (word >= wpr) break;
+      unsigned tb[2], hb[2], mb[2];
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int e = word * 64 + half * 32 + lane;
+        const int p = e < cols ? quantize_level(row[e], s) : 1;  // padding: (0,0,0)
+        tb[half] = __ballot_sync(0xFFFFFFFFu, p == 3);
+        hb[half] = __ballot_sync(0xFFFFFFFFu, p == 2);
+        mb[half] = __ballot_sync(0xFFFFFFFFu, p == 0 || p == 3);
+      }
+      if (lane == 0) {
+        const long long o = r * wpr + word;
+        t[o] = (static_cast<unsigned long long>(tb[1]) << 32) | tb[0];
+        h[o] = (static_cast<unsigned long long>(hb[1]) << 32) | hb[0];
+        m[o] = (static_cast<unsigned long long>(mb[1]) << 32) | mb[0];
+      }
+    }
+  }
+}
+
+}  // namespace bitmm_dev

@@ -109,3 +109,29 @@ def layer_forward(bin_words: torch.Tensor, cols: int, alpha, row_ptr, col_idx, v
     _raise(_lib.load().bitmm_layer_forward_dev(
         rows, cols, a_scalar, _ptr(a_vec), _ptr(bin_words), wpr, _ptr(row_ptr), _ptr(col_idx),
         _ptr(vals), _ptr(b), n, b.shape[1], _ptr(out), out.shape[1], _stream(stream)))
+
+
+def pack_signs(a: torch.Tensor, lane_bits: int = 512, out: Optional[torch.Tensor] = None,
+               stream=None) -> torch.Tensor:
+    """GPU pack_signs (tensor.cpp:155-164): fp32 [rows, cols] -> int64 view of the BitMatrix
+    words [rows, wpr], wpr = ceil(cols / lane_bits) * lane_bits / 64, zero padding."""
+    from .data import padded_words
+    rows, cols = a.shape
+    wpr = padded_words(cols, lane_bits)
+    if out is None:
+        out = torch.empty((rows, wpr), dtype=torch.int64, device=a.device)
+    _raise(_lib.load().bitmm_pack_signs_dev(_ptr(a), rows, cols, a.stride(0), _ptr(out), wpr,
+                                            _stream(stream)))
+    return out
+
+
+def quantize_thm(a: torch.Tensor, s: float, lane_bits: int = 512, stream=None):
+    """GPU quantize_uniform_2bit + decompose_thm (transform.cpp:21-36, 47-75): fp32 ->
+    (t, h, m) int64 views of the plane words [rows, wpr]."""
+    from .data import padded_words
+    rows, cols = a.shape
+    wpr = padded_words(cols, lane_bits)
+    t, h, m = (torch.empty((rows, wpr), dtype=torch.int64, device=a.device) for _ in range(3))
+    _raise(_lib.load().bitmm_quantize_thm_dev(_ptr(a), rows, cols, a.stride(0), s, _ptr(t), _ptr(h),
+                                              _ptr(m), wpr, _stream(stream)))
+    return t, h, m
