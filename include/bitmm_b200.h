@@ -62,7 +62,8 @@ int bitmm_device_sm_count(void);
 int bitmm_device_status(void* stream);
 /* Pre-grows the internal device workspace so no allocation happens inside timed loops. */
 int bitmm_reserve_workspace(size_t bytes);
-/* Workspace bytes a routine needs for the given shape (routine: 0=1x1, 1=1x2, 2=2x2, 3=1x32/APB). */
+/* Workspace bytes a routine needs for the given shape (routine: 0=1x1, 1=1x2, 2=2x2, 3=1x32/APB,
+ * 4=APB with 2-bit activations; m = rows, n = tokens, k = cols). */
 size_t bitmm_workspace_bytes(int routine, int64_t m, int64_t n, int64_t k);
 /* Number of kernels launched by the most recent compute call on this thread. */
 int bitmm_last_launch_count(void);
@@ -153,6 +154,27 @@ int bitmm_layer_forward_host(int64_t rows, int64_t cols, float alpha, const floa
                              const uint64_t* bin, int64_t wpr, const uint64_t* row_ptr,
                              const uint64_t* col_idx, const float* vals, int64_t nnz,
                              const float* b, int64_t n, int64_t ldb, float* c, int64_t ldc);
+
+/* ---- APB layer with 2-bit activations (paper-faithful inference) ----
+ * No single reference entry point: it is the composition of reference calls
+ *   C = gemm_1x2(bin, alpha_r, planes)            (kernels.hpp:55, kernels.cpp:185-221)
+ *     + spmm_csr(residual, D)                      (kernels.hpp:76, kernels.cpp:334-352)
+ * added like layer_forward (apb.cpp:161-162), where planes {t,h,m} are tokens x wpr (K-packed
+ * per token, gemm_1x2's a_packed) and D[k][c] = float(p[c][k]) * (a_scale * gamma_a) is the
+ * dequantized level. Per-row alpha uses gemm_1x2's scale order ((0.5*alpha_r)*s)*gamma_a.
+ * C: rows x tokens. Bit-identical to that composition. */
+int bitmm_layer_forward_2bit_dev(int64_t rows, int64_t cols, float alpha, const float* row_alpha,
+                                 const uint64_t* bin, int64_t wpr, const uint64_t* row_ptr,
+                                 const uint64_t* col_idx, const float* vals, const uint64_t* t,
+                                 const uint64_t* h, const uint64_t* m, int64_t tokens,
+                                 float a_scale, int has_a_gamma, float a_gamma, float* c,
+                                 int64_t ldc, void* stream);
+int bitmm_layer_forward_2bit_host(int64_t rows, int64_t cols, float alpha, const float* row_alpha,
+                                  const uint64_t* bin, int64_t wpr, const uint64_t* row_ptr,
+                                  const uint64_t* col_idx, const float* vals, int64_t nnz,
+                                  const uint64_t* t, const uint64_t* h, const uint64_t* m,
+                                  int64_t tokens, float a_scale, int has_a_gamma, float a_gamma,
+                                  float* c, int64_t ldc);
 
 /* ---- GPU packers (dense fp32 -> reference packed layouts) ----
  * pack_signs: replaces pack_signs (tensor.hpp:248, tensor.cpp:155-164): bit i of row r is

@@ -59,6 +59,8 @@ class Oracle:
             "oracle_spmm_csr": (None, [_i64, _p, _p, _p, _p, _i64, _i64, _p]),
             "oracle_layer_forward": (None, [_i64, _i64, _f, _p, _p, _i64, _p, _p, _p, _p, _i64,
                                             _i64, _p]),
+            "oracle_layer_forward_2bit": (None, [_i64, _i64, _f, _p, _p, _i64, _p, _p, _p, _p,
+                                                 _p, _p, _i64, _f, _i, _f, _p]),
             "oracle_padded_words": (_i64, [_i64, _i]),
             "oracle_pack_signs": (None, [_p, _i64, _i64, _i64, _p]),
             "oracle_decompose_thm": (None, [_p, _i64, _i64, _i64, _p, _p, _p]),
@@ -135,6 +137,18 @@ class Oracle:
         return o
 
     # ---- packing ----
+    def layer_forward_2bit(self, rows, cols, alpha, bin_words, wpr, row_ptr, col_idx, vals, t, h,
+                           mm, a_scale=1.0, a_gamma=None, row_alpha=None):
+        n = t.shape[0]
+        o = np.empty((rows, n), np.float32)
+        ra = None if row_alpha is None else np.ascontiguousarray(row_alpha, np.float32)
+        self.lib.oracle_layer_forward_2bit(rows, cols, alpha, _ptr(ra), _ptr(bin_words), wpr,
+                                           _ptr(row_ptr), _ptr(col_idx), _ptr(vals), _ptr(t),
+                                           _ptr(h), _ptr(mm), n, a_scale,
+                                           int(a_gamma is not None),
+                                           1.0 if a_gamma is None else a_gamma, _ptr(o))
+        return o
+
     def pack_signs(self, a, lane_bits=512):
         rows, cols = a.shape
         wpr = self.lib.oracle_padded_words(cols, lane_bits)

@@ -74,6 +74,14 @@ SIGNATURES = {
         _i,
         [_i64, _i64, _f, _p, _p, _i64, _p, _p, _p, _i64, _p, _i64, _i64, _p, _i64],
     ),
+    "bitmm_layer_forward_2bit_dev": (
+        _i,
+        [_i64, _i64, _f, _p, _p, _i64, _p, _p, _p, _p, _p, _p, _i64, _f, _i, _f, _p, _i64, _p],
+    ),
+    "bitmm_layer_forward_2bit_host": (
+        _i,
+        [_i64, _i64, _f, _p, _p, _i64, _p, _p, _p, _i64, _p, _p, _p, _i64, _f, _i, _f, _p, _i64],
+    ),
     "bitmm_pack_signs_dev": (_i, [_p, _i64, _i64, _i64, _p, _i64, _p]),
     "bitmm_pack_signs_host": (_i, [_p, _i64, _i64, _i64, _p, _i64]),
     "bitmm_quantize_thm_dev": (_i, [_p, _i64, _i64, _i64, _f, _p, _p, _p, _i64, _p]),

@@ -423,3 +423,26 @@ def layer_forward(l: ApbLayer, b: np.ndarray, threads: int = 1) -> np.ndarray:
         l.bin.words_per_row(), _ptr(r.row_ptr), _ptr(r.col_idx), _ptr(r.vals), r.nnz(), _ptr(b),
         n, n, _ptr(out), n))
     return out
+
+
+def layer_forward_2bit(l: ApbLayer, a_packed: ThmPlanes, threads: int = 1) -> np.ndarray:
+    """APB inference with 2-bit activations: the composition
+    gemm_1x2(bin, alpha, a_packed) + spmm_csr(residual, dequant(a_packed)) of reference calls
+    (kernels.cpp:185-221, 334-352; added as in apb.cpp:161-162). a_packed holds one row per
+    token, K-packed; the result is rows x tokens, bit-identical to that composition."""
+    a_packed.validate()
+    if l.bin.cols() != a_packed.cols() or l.bin.words_per_row() != a_packed.t.words_per_row():
+        raise ValueError("gemm dimension mismatch (packed rows must share K and padding)")
+    _check_gemm(l.bin.rows(), l.bin.cols(), a_packed.rows())
+    _check_threads(threads)
+    m, n = l.rows, a_packed.rows()
+    a_vec = None if np.ndim(l.alpha) == 0 else np.ascontiguousarray(l.alpha, np.float32)
+    out = np.empty((m, n), np.float32)
+    r = l.residual
+    _raise(_lib.load().bitmm_layer_forward_2bit_host(
+        m, l.cols, float(l.alpha) if a_vec is None else 1.0, _ptr(a_vec), _ptr(l.bin.words),
+        l.bin.words_per_row(), _ptr(r.row_ptr), _ptr(r.col_idx), _ptr(r.vals), r.nnz(),
+        _ptr(a_packed.t.words), _ptr(a_packed.h.words), _ptr(a_packed.m.words), n,
+        float(a_packed.scale), int(a_packed.gamma is not None),
+        1.0 if a_packed.gamma is None else float(a_packed.gamma), _ptr(out), n))
+    return out

@@ -32,9 +32,10 @@ constexpr int SPMM_TOK = 32;       // columns per block (X chunk [K][32] fp32 in
 constexpr int SPMM_THREADS = 512;  // 64 octets: an 8-lane octet owns one output row, 4 columns/lane
 constexpr int SPMM_QUADS = SPMM_THREADS / 8;  // rows in flight per block
 
-// Dynamic smem: X chunk [K][SPMM_TOK] fp32, then the block's row offsets (u32).
+// Dynamic smem: X chunk [K][SPMM_TOK] fp32 plus one zero row (the target of padded
+// nonzeros, so they contribute 0 * 0 without a branch), then the row offsets (u32).
 inline int spmm_smem_bytes(long long K, int rows_per_split) {
-  return static_cast<int>(K * SPMM_TOK * 4 + (rows_per_split + 1) * 4);
+  return static_cast<int>((K + 1) * SPMM_TOK * 4 + (rows_per_split + 1) * 4);
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -45,12 +46,26 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
 
-template <bool EXACT, bool PDL_CHAIN>
+// LEVELS source: activation planes {t,h,m} [tokens][wpr] (K-packed per token, the
+// a_packed orientation of gemm_1x2) dequantized to d[p] = float(p) * (s * gamma_a) while
+// staging; the chunk is the same [K][SPMM_TOK] fp32 tile the X path stages.
+struct SpmmLevels {
+  const unsigned long long* t;
+  const unsigned long long* h;
+  const unsigned long long* m;
+  int wpr;
+  float d1, d2, d3;  // d0 = 0
+};
+
+// LEVELS also accumulates: the 2-bit layer's GEMM has already stored the binary part in C,
+// and each output row becomes C = bin + R.D (apb.cpp:161-162; fp32 add commutes).
+template <bool EXACT, bool PDL_CHAIN, bool LEVELS>
 __global__ void __launch_bounds__(SPMM_THREADS, 2)
     spmm_xchunk_kernel(int rows, int K, int N, const unsigned long long* __restrict__ row_ptr,
                        const unsigned long long* __restrict__ col_idx,
                        const float* __restrict__ vals, const float* __restrict__ X, long long ldx,
-                       float* __restrict__ C, long long ldc, int rows_per_split) {
+                       float* __restrict__ C, long long ldc, int rows_per_split,
+                       const SpmmLevels lv) {
   extern __shared__ float xs[];  // [K][SPMM_TOK], then u32 row offsets
   // PDL: wait for the predecessor first (a wait deferred to the end of the kernel can park
   // blocks on SM slots the predecessor still needs), then let the GEMM launch early.
@@ -58,21 +73,62 @@ __global__ void __launch_bounds__(SPMM_THREADS, 2)
     pdl_wait();
     pdl_launch_dependents();
   }
-  unsigned* rps = reinterpret_cast<unsigned*>(xs + static_cast<long long>(K) * SPMM_TOK);
+  unsigned* rps = reinterpret_cast<unsigned*>(xs + static_cast<long long>(K + 1) * SPMM_TOK);
+  if (threadIdx.x < SPMM_TOK) xs[K * SPMM_TOK + threadIdx.x] = 0.f;
   const int c0 = blockIdx.x * SPMM_TOK;
   const int r0 = blockIdx.y * rows_per_split;
   const int r1 = min(rows, r0 + rows_per_split);
-  const bool vec = ((N & 3) == 0) && ((ldx & 3) == 0) && ((ldc & 3) == 0) &&
-                   ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
-  // X chunk: every 16-byte piece in flight at once (cp.async), zero-filled past N
-  for (int i = threadIdx.x; i < K * (SPMM_TOK / 4); i += SPMM_THREADS) {
-    const int k = i / (SPMM_TOK / 4), q = (i % (SPMM_TOK / 4)) * 4;
-    const float* src = X + static_cast<long long>(k) * ldx + c0 + q;
-    float* dst = &xs[k * SPMM_TOK + q];
-    if (vec && c0 + q + 3 < N) {
-      cp_async16(dst, src);
-    } else {
-      for (int e = 0; e < 4; ++e) dst[e] = (c0 + q + e < N) ? src[e] : 0.f;
+  const bool vec = ((N & 3) == 0) && ((ldc & 3) == 0) &&
+                   (LEVELS || (((ldx & 3) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0)));
+  if constexpr (LEVELS) {
+    // lane = token, warp step = one 64-bit plane word: each smem store instruction writes
+    // 32 tokens of one k (conflict-free). Level p = 2*(t|h) + (t | ~(h|m)) per bit
+    // (decompose_thm states, transform.cpp:56-71); tokens past N stage zeros.
+    const int words = (K + 63) >> 6;
+    for (int i = threadIdx.x; i < words * SPMM_TOK; i += SPMM_THREADS) {
+      const int tok = i & (SPMM_TOK - 1), word = i / SPMM_TOK;
+      const int c = c0 + tok;
+      unsigned long long hi = 0, lo = 0;
+      if (c < N) {
+        const long long o = static_cast<long long>(c) * lv.wpr + word;
+        const unsigned long long t = lv.t[o], h = lv.h[o], m = lv.m[o];
+        hi = t | h;
+        lo = t | ~(h | m);
+      }
+      const int k0 = word * 64;
+      const int nb = min(64, K - k0);
+      float* dst = &xs[k0 * SPMM_TOK + tok];
+      if (nb == 64) {
+        // constant bit positions: each element is two predicate tests, two selects, one store
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          const unsigned hw = static_cast<unsigned>(hi >> (32 * half));
+          const unsigned lw = static_cast<unsigned>(lo >> (32 * half));
+#pragma unroll
+          for (int b = 0; b < 32; ++b) {
+            const float lo_v = (lw & (1u << b)) ? lv.d1 : 0.f;
+            const float hi_v = (lw & (1u << b)) ? lv.d3 : lv.d2;
+            dst[(32 * half + b) * SPMM_TOK] = (hw & (1u << b)) ? hi_v : lo_v;
+          }
+        }
+      } else {
+        for (int b = 0; b < nb; ++b) {
+          const int lvl = static_cast<int>(((hi >> b) & 1ull) * 2ull + ((lo >> b) & 1ull));
+          dst[b * SPMM_TOK] = lvl == 0 ? 0.f : lvl == 1 ? lv.d1 : lvl == 2 ? lv.d2 : lv.d3;
+        }
+      }
+    }
+  } else {
+    // X chunk: every 16-byte piece in flight at once (cp.async), zero-filled past N
+    for (int i = threadIdx.x; i < K * (SPMM_TOK / 4); i += SPMM_THREADS) {
+      const int k = i / (SPMM_TOK / 4), q = (i % (SPMM_TOK / 4)) * 4;
+      const float* src = X + static_cast<long long>(k) * ldx + c0 + q;
+      float* dst = &xs[k * SPMM_TOK + q];
+      if (vec && c0 + q + 3 < N) {
+        cp_async16(dst, src);
+      } else {
+        for (int e = 0; e < 4; ++e) dst[e] = (c0 + q + e < N) ? src[e] : 0.f;
+      }
     }
   }
   const unsigned long long nz0 = row_ptr[r0];
@@ -95,47 +151,121 @@ __global__ void __launch_bounds__(SPMM_THREADS, 2)
   const unsigned long long* cbase = col_idx + nz0;
   const float* vbase = vals + nz0;
   const int iters = (r1 - r0 + SPMM_QUADS - 1) / SPMM_QUADS;
+  const unsigned zero_row = static_cast<unsigned>(K) * (SPMM_TOK * 4);
+  // Nonzero slot `idx` of a row as (byte offset of its X row in smem, weight); padded slots
+  // point at the zero row with weight 0 (0 * 0 leaves an accumulator that started at +0
+  // bit-identical: it can never be -0, so no branch is needed, and EXACT keeps the order).
+  auto fetch = [&](unsigned i0, unsigned n, unsigned idx, unsigned& kk, float& vv) {
+    kk = idx < n ? static_cast<unsigned>(cbase[i0 + idx]) * (SPMM_TOK * 4) : zero_row;
+    vv = idx < n ? vbase[i0 + idx] : 0.f;
+  };
+  const char* xrow = reinterpret_cast<const char*>(xs) + ol * 16;
+  auto step8 = [&](unsigned kk, float vv, float (&acc)[4]) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const unsigned koff = __shfl_sync(0xFFFFFFFFu, kk, obase + j);
+      const float v = __shfl_sync(0xFFFFFFFFu, vv, obase + j);
+      const float4 x = *reinterpret_cast<const float4*>(xrow + koff);
+      if (EXACT) {
+        acc[0] = __fadd_rn(acc[0], __fmul_rn(v, x.x));
+        acc[1] = __fadd_rn(acc[1], __fmul_rn(v, x.y));
+        acc[2] = __fadd_rn(acc[2], __fmul_rn(v, x.z));
+        acc[3] = __fadd_rn(acc[3], __fmul_rn(v, x.w));
+      } else {
+        acc[0] = __fmaf_rn(v, x.x, acc[0]);
+        acc[1] = __fmaf_rn(v, x.y, acc[1]);
+        acc[2] = __fmaf_rn(v, x.z, acc[2]);
+        acc[3] = __fmaf_rn(v, x.w, acc[3]);
+      }
+    }
+  };
+  // Software pipeline: the first 16 nonzero slots of the next row are loaded from global
+  // memory while the current row computes (rows of a 2% residual rarely have more).
+  unsigned i0 = 0, n = 0, kk0 = zero_row, kk1 = zero_row;
+  float vv0 = 0.f, vv1 = 0.f;
+  {
+    const int r = r0 + oct;
+    if (r < r1) {
+      i0 = rps[r - r0];
+      n = rps[r - r0 + 1] - i0;
+    }
+    fetch(i0, n, ol, kk0, vv0);
+    fetch(i0, n, ol + 8, kk1, vv1);
+  }
   for (int it = 0; it < iters; ++it) {
     const int r = r0 + it * SPMM_QUADS + oct;
     const bool live = r < r1;
-    const unsigned i0 = live ? rps[r - r0] : 0u;
-    const unsigned n = live ? rps[r - r0 + 1] - i0 : 0u;
     const unsigned nmax = __reduce_max_sync(0xFFFFFFFFu, n);
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    for (unsigned base = 0; base < nmax; base += 8) {
-      const unsigned idx = base + ol;
-      const unsigned kk = idx < n ? static_cast<unsigned>(cbase[i0 + idx]) * (SPMM_TOK * 4) : 0u;
-      const float vv = idx < n ? vbase[i0 + idx] : 0.f;
-      const char* xrow = reinterpret_cast<const char*>(xs) + ol * 16;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const unsigned koff = __shfl_sync(0xFFFFFFFFu, kk, obase + j);
-        const float v = __shfl_sync(0xFFFFFFFFu, vv, obase + j);
-        const float4 x = *reinterpret_cast<const float4*>(xrow + koff);
-        if (EXACT) {
-          if (base + j < n) {  // padded entries must not touch the reference's rounding order
-            acc[0] = __fadd_rn(acc[0], __fmul_rn(v, x.x));
-            acc[1] = __fadd_rn(acc[1], __fmul_rn(v, x.y));
-            acc[2] = __fadd_rn(acc[2], __fmul_rn(v, x.z));
-            acc[3] = __fadd_rn(acc[3], __fmul_rn(v, x.w));
-          }
-        } else {
-          // padded entries carry v = 0 (and row 0, a valid address): fma(0, x, acc) == acc
-          acc[0] = __fmaf_rn(v, x.x, acc[0]);
-          acc[1] = __fmaf_rn(v, x.y, acc[1]);
-          acc[2] = __fmaf_rn(v, x.z, acc[2]);
-          acc[3] = __fmaf_rn(v, x.w, acc[3]);
-        }
+    float* dst = C + static_cast<long long>(r) * ldc + col;
+    float prev[4] = {0.f, 0.f, 0.f, 0.f};
+    if (LEVELS && live) {  // issued before the nonzero loop so its latency overlaps it
+      if (vec && col + 3 < N) {
+        const float4 p4 = *reinterpret_cast<const float4*>(dst);
+        prev[0] = p4.x; prev[1] = p4.y; prev[2] = p4.z; prev[3] = p4.w;
+      } else {
+        for (int e = 0; e < 4; ++e)
+          if (col + e < N) prev[e] = dst[e];
       }
     }
+    // prefetch the next row's first 16 slots
+    unsigned ni0 = 0, nn = 0, nkk0 = zero_row, nkk1 = zero_row;
+    float nvv0 = 0.f, nvv1 = 0.f;
+    {
+      const int rn = r + SPMM_QUADS;
+      if (rn < r1) {
+        ni0 = rps[rn - r0];
+        nn = rps[rn - r0 + 1] - ni0;
+      }
+      fetch(ni0, nn, ol, nkk0, nvv0);
+      fetch(ni0, nn, ol + 8, nkk1, nvv1);
+    }
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    if (nmax > 0) step8(kk0, vv0, acc);
+    if (nmax > 8) step8(kk1, vv1, acc);
+    for (unsigned base = 16; base < nmax; base += 8) {
+      unsigned kk;
+      float vv;
+      fetch(i0, n, base + ol, kk, vv);
+      step8(kk, vv, acc);
+    }
+    if (LEVELS) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[e] = __fadd_rn(prev[e], acc[e]);
+    }
     if (live) {
-      float* dst = C + static_cast<long long>(r) * ldc + col;
       if (vec && col + 3 < N) {
         *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
       } else {
         for (int e = 0; e < 4; ++e)
           if (col + e < N) dst[e] = acc[e];
       }
+    }
+    i0 = ni0;
+    n = nn;
+    kk0 = nkk0;
+    kk1 = nkk1;
+    vv0 = nvv0;
+    vv1 = nvv1;
+  }
+}
+
+// Large-K fallback of the LEVELS source: dequantize the planes into a dense [K][N] fp32
+// matrix (the layout spmm_csr's b operand has, kernels.hpp:76) for the global-gather SpMM.
+// Adjacent threads own adjacent tokens, so every store instruction is coalesced.
+__global__ void dequant_levels_kernel(const SpmmLevels lv, int K, int N, float* __restrict__ out) {
+  const int words = (K + 63) >> 6;
+  const long long total = static_cast<long long>(words) * N;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % N), word = static_cast<int>(i / N);
+    const long long o = static_cast<long long>(c) * lv.wpr + word;
+    const unsigned long long t = lv.t[o], h = lv.h[o], m = lv.m[o];
+    const unsigned long long hi = t | h, lo = t | ~(h | m);
+    const int k0 = word * 64, nb = min(64, K - k0);
+    for (int b = 0; b < nb; ++b) {
+      const int lvl = static_cast<int>(((hi >> b) & 1ull) * 2ull + ((lo >> b) & 1ull));
+      out[static_cast<long long>(k0 + b) * N + c] =
+          lvl == 0 ? 0.f : lvl == 1 ? lv.d1 : lvl == 2 ? lv.d2 : lv.d3;
     }
   }
 }
@@ -147,7 +277,8 @@ constexpr int APB_STAGES = 5;
 constexpr int APB_A_STAGE = 128 * TC_BK_BYTES;                       // 128 rows x 64 bf16
 constexpr int APB_B_PART = (APB_BN / 2) * TC_BK_BYTES;               // 64 rows x 64 bf16
 constexpr int APB_STAGE = APB_A_STAGE + APB_PARTS * APB_B_PART;      // 40 KB
-constexpr int APB_SMEM = 1024 + APB_STAGES * APB_STAGE + TC_EPI_BYTES + (2 * APB_STAGES + 4) * 8 + 16;
+constexpr int APB_EPI_BYTES = 4 * 32 * TC_EPI_STRIDE * 4;
+constexpr int APB_SMEM = 1024 + APB_STAGES * APB_STAGE + APB_EPI_BYTES + (2 * APB_STAGES + 4) * 8 + 16;
 
 struct ApbParams {
   int M, N, kb_per_part;     // kb_per_part = kpad / 64
@@ -178,7 +309,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint8_t* smem = smem_raw + ((1024u - (base_u32 & 1023u)) & 1023u);
   uint8_t* stages = smem;
   float* sEpi = reinterpret_cast<float*>(stages + APB_STAGES * APB_STAGE);
-  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sEpi) + TC_EPI_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sEpi) + APB_EPI_BYTES);
   uint64_t* empty = full + APB_STAGES;
   uint64_t* tfull = empty + APB_STAGES;
   uint64_t* tempty = tfull + 2;

@@ -139,6 +139,23 @@ int make_operand_map(CUtensorMap* map, const void* base, CUtensorMapDataType dt,
   return BITMM_OK;
 }
 
+// Output map for the GEMM epilogue's bulk tensor stores: [rows][ldc] 4-byte cells, box 32x32,
+// 128B swizzle (the epilogue's staging layout). Returns false when the layout does not allow
+// TMA (row pitch not a multiple of 16 bytes or base not 16-byte aligned).
+bool make_output_map(CUtensorMap* map, void* base, CUtensorMapDataType dt, uint64_t cols,
+                     uint64_t rows, uint64_t ldc) {
+  if (base == nullptr || (ldc & 3) != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  PFN_encodeTiled_t enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ldc * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(map, dt, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // ---------------- stream-ordered kernel profiler ----------------
 struct ProfRecord {
   int kernel;
@@ -301,8 +318,13 @@ int run_tc_gemm(DeviceState& st, const CUtensorMap& ta, const CUtensorMap& tb, T
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
+  CUtensorMap tc{};
+  void* out = (EPI == Epi::I32) ? static_cast<void*>(p.out_i32) : static_cast<void*>(p.out_f32);
+  p.tma_store = make_output_map(&tc, out, EPI == Epi::I32 ? CU_TENSOR_MAP_DATA_TYPE_INT32
+                                                          : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                p.N, p.M, p.ldc) ? 1 : 0;
   ProfScope ps(KIND == Kind::I8 ? "tc_gemm_i8" : "tc_gemm_bf16_apb", s);
-  BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
+  BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, p));
   return launch_check("tc_gemm_kernel");
 }
 
@@ -451,31 +473,55 @@ bool spmm_chunk_fits(int64_t k, int64_t rows_per_split) {
   return spmm_smem_bytes(k, static_cast<int>(rows_per_split)) <= kMaxDynSmem;
 }
 
-// R.X for CSR rows, X [k][ldb] fp32. EXACT reproduces the reference rounding
-// (kernels.cpp:347); the fused layer uses fma and chains into the GEMM with PDL.
-template <bool EXACT, bool PDL_CHAIN>
+// ~6 waves of blocks at 2 resident blocks per SM, rows split evenly
+void spmm_grid(const DeviceState& st, int64_t rows, int64_t n, int* chunks, int* splits,
+               int* rows_per_split) {
+  *chunks = static_cast<int>((n + SPMM_TOK - 1) / SPMM_TOK);
+  const int target = 6 * st.sms;  // measured: 6 waves-worth beats 4..24 (restaging vs balance)
+  *splits = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>((rows + SPMM_QUADS - 1) / SPMM_QUADS, (target + *chunks - 1) / *chunks)));
+  *rows_per_split = static_cast<int>((rows + *splits - 1) / *splits);
+}
+
+bool spmm_staged(const DeviceState& st, int64_t rows, int64_t k, int64_t n) {
+  int chunks, splits, rps;
+  spmm_grid(st, rows, n, &chunks, &splits, &rps);
+  return spmm_chunk_fits(k, rps);
+}
+
+// R.X for CSR rows, X [k][ldb] fp32 (or, LEVELS, the dequantized activation planes `lv`).
+// EXACT reproduces the reference rounding (kernels.cpp:347); the fp32 APB layer uses fma and
+// chains into the GEMM with PDL. When the staged chunk does not fit in shared memory, LEVELS
+// first dequantizes into `deq` [k][n] and both sources take the global-gather kernel.
+template <bool EXACT, bool PDL_CHAIN, bool LEVELS = false>
 int run_spmm(DeviceState& st, int64_t rows, int64_t k, const uint64_t* row_ptr,
              const uint64_t* col_idx, const float* vals, const float* b, int64_t n, int64_t ldb,
-             float* c, int64_t ldc, cudaStream_t s) {
+             float* c, int64_t ldc, cudaStream_t s, const SpmmLevels& lv = SpmmLevels{},
+             float* deq = nullptr) {
   const auto* rp = reinterpret_cast<const unsigned long long*>(row_ptr);
   const auto* ci = reinterpret_cast<const unsigned long long*>(col_idx);
-  // ~6 waves of blocks at 2 resident blocks per SM, rows split evenly
-  const int chunks = static_cast<int>((n + SPMM_TOK - 1) / SPMM_TOK);
-  const int target = 12 * st.sms;
-  const int splits = static_cast<int>(std::max<int64_t>(
-      1, std::min<int64_t>((rows + SPMM_QUADS - 1) / SPMM_QUADS, (target + chunks - 1) / chunks)));
-  const int rows_per_split = static_cast<int>((rows + splits - 1) / splits);
+  int chunks, splits, rows_per_split;
+  spmm_grid(st, rows, n, &chunks, &splits, &rows_per_split);
   if (!spmm_chunk_fits(k, rows_per_split)) {
+    if (LEVELS) {
+      ProfScope pd("dequant_levels", s);
+      dequant_levels_kernel<<<blocks_for(((k + 63) / 64) * n, 256), 256, 0, s>>>(
+          lv, static_cast<int>(k), static_cast<int>(n), deq);
+      BITMM_TRY(launch_check("dequant_levels_kernel"));
+      b = deq;
+      ldb = n;
+    }
     // large K: X chunk does not fit in shared memory, gather rows from L2 instead
     const long long warps = rows * ((n + 127) / 128);
     ProfScope ps("spmm_csr_gather", s);
     spmm_csr_kernel<<<blocks_for(warps * 32, 256), 256, 0, s>>>(rows, rp, ci, vals, b, ldb,
-                                                                static_cast<int>(n), c, ldc);
+                                                                static_cast<int>(n), c, ldc,
+                                                                LEVELS ? 1 : 0);
     return launch_check("spmm_csr_kernel");
   }
-  auto kern = spmm_xchunk_kernel<EXACT, PDL_CHAIN>;
+  auto kern = spmm_xchunk_kernel<EXACT, PDL_CHAIN, LEVELS>;
   const int smem = spmm_smem_bytes(k, rows_per_split);
-  const unsigned bit = 1u << (20 + (EXACT ? 1 : 0) + (PDL_CHAIN ? 2 : 0));
+  const unsigned bit = 1u << (20 + (EXACT ? 1 : 0) + (PDL_CHAIN ? 2 : 0) + (LEVELS ? 4 : 0));
   if (!(st.attr_mask & bit)) {
     BITMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
     st.attr_mask |= bit;
@@ -488,10 +534,10 @@ int run_spmm(DeviceState& st, int64_t rows, int64_t k, const uint64_t* row_ptr,
   cudaLaunchAttribute attr[1] = {pdl_attr()};
   cfg.attrs = attr;
   cfg.numAttrs = PDL_CHAIN ? 1 : 0;
-  ProfScope ps(EXACT ? "spmm_xchunk_exact" : "spmm_xchunk", s);
+  ProfScope ps(LEVELS ? "spmm_levels_exact" : EXACT ? "spmm_xchunk_exact" : "spmm_xchunk", s);
   BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, static_cast<int>(rows), static_cast<int>(k),
                                     static_cast<int>(n), rp, ci, vals, b, ldb, c, ldc,
-                                    rows_per_split));
+                                    rows_per_split, lv));
   return launch_check("spmm_xchunk_kernel");
 }
 
@@ -575,6 +621,63 @@ int apb_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, int64_t k, int64
   ProfScope ps("apb_gemm_bf16x3", s);
   BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, apb_gemm_kernel, ta, tb, p));
   return launch_check("apb_gemm_kernel");
+}
+
+// Paper-faithful APB with 2-bit activations:
+//   C = gemm_1x2(bin, alpha_r, planes)  +  spmm_csr(residual, dequant(planes))
+// 1. unpack_pair : sign(bin) and the levels p to int8 (as gemm_1x2)
+// 2. tc_gemm F32R (store): C = (((0.5 * alpha_r) * s) * gamma_a) * units (kernels.cpp:193,216)
+// 3. spmm_levels : residual rows over the planes dequantized while staging, d_p =
+//                  float(p) * (s * gamma_a), reference rounding, then C = C + R.D (apb.cpp:161)
+// The GEMM stores without reading C (its epilogue warps are few and latency-bound on loads);
+// the SpMM's many warps absorb the read-modify-write. Bit-identical to the reference
+// composition.
+size_t ws_bytes_apb2(const DeviceState& st, int64_t rows, int64_t cols, int64_t tokens) {
+  const size_t deq = spmm_staged(st, rows, cols, tokens) ? 0 : align_up(cols * tokens * 4, 1024);
+  return ws_bytes_int(rows, tokens, cols) + deq;
+}
+
+int apb2_dev_impl(DeviceState& st, int64_t rows, int64_t cols, int64_t wpr, float alpha,
+                  const float* row_alpha, const uint64_t* bin, const uint64_t* row_ptr,
+                  const uint64_t* col_idx, const float* vals, const uint64_t* t, const uint64_t* h,
+                  const uint64_t* m, int64_t tokens, float a_scale, float a_gamma, float* c,
+                  int64_t ldc, cudaStream_t s) {
+  const int64_t kpad = round_up(cols, TC_BK_BYTES);
+  BITMM_TRY(arena_reserve(st.ws, ws_bytes_apb2(st, rows, cols, tokens)));
+  float* deq = reinterpret_cast<float*>(static_cast<uint8_t*>(st.ws.ptr) + ws_bytes_int(rows, tokens, cols));
+  uint8_t *A8, *B8;
+  take_int_operands(st, rows, tokens, cols, &A8, &B8);
+  BITMM_TRY(run_unpack_pair({bin, nullptr, nullptr, rows, false}, {t, h, m, tokens, true}, wpr, cols,
+                            kpad, A8, B8, st.status, s));
+  constexpr bool kPair = true;
+  CUtensorMap ta, tb;
+  BITMM_TRY(make_operand_map(&ta, A8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad, rows, TcShape<kPair>::A_ROWS));
+  BITMM_TRY(make_operand_map(&tb, B8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad, tokens, TcShape<kPair>::B_ROWS));
+  TcParams p{};
+  p.M = static_cast<int>(rows);
+  p.N = static_cast<int>(tokens);
+  p.num_kb = static_cast<int>(kpad / TC_BK_BYTES);
+  p.a_kb_period = p.num_kb;
+  p.shift = 1;
+  p.scale = 0.5f * alpha * a_scale * a_gamma;  // kernels.cpp:193 order
+  p.row_scale = row_alpha;
+  p.row_pre = 0.5f;
+  p.act_scale = a_scale;
+  p.act_gamma = a_gamma;
+  p.out_f32 = c;
+  p.ldc = ldc;
+  BITMM_TRY((run_tc_gemm<Kind::I8, Epi::F32R, kPair>(st, ta, tb, p, s)));
+  SpmmLevels lv{};
+  lv.t = reinterpret_cast<const unsigned long long*>(t);
+  lv.h = reinterpret_cast<const unsigned long long*>(h);
+  lv.m = reinterpret_cast<const unsigned long long*>(m);
+  lv.wpr = static_cast<int>(wpr);
+  const float sg = a_scale * a_gamma;
+  lv.d1 = 1.0f * sg;
+  lv.d2 = 2.0f * sg;
+  lv.d3 = 3.0f * sg;
+  return run_spmm<true, true, true>(st, rows, cols, row_ptr, col_idx, vals, nullptr, tokens, tokens,
+                                    c, ldc, s, lv, deq);
 }
 
 int with_device(DeviceState** st) {
@@ -675,7 +778,10 @@ int bitmm_reserve_workspace(size_t bytes) {
 
 size_t bitmm_workspace_bytes(int routine, int64_t m, int64_t n, int64_t k) {
   if (m <= 0 || n <= 0 || k <= 0) return 0;
-  return routine == 3 ? ws_bytes_1x32(m, n, k) : ws_bytes_int(m, n, k);
+  if (routine == 3) return ws_bytes_1x32(m, n, k);
+  if (routine == 4)  // dequantized [k][n] operand only when the staged SpMM chunk cannot fit
+    return ws_bytes_int(m, n, k) + (spmm_chunk_fits(k, m) ? 0 : align_up(k * n * 4, 1024));
+  return ws_bytes_int(m, n, k);
 }
 
 // ---------------- 1/1 ----------------
@@ -1132,6 +1238,72 @@ int bitmm_quantize_thm_host(const float* a, int64_t rows, int64_t cols, int64_t 
   BITMM_CUDA_TRY(cudaMemcpyAsync(m, dm, w_bytes, cudaMemcpyDeviceToHost, s));
   BITMM_CUDA_TRY(cudaStreamSynchronize(s));
   return BITMM_OK;
+}
+
+// ---------------- APB with 2-bit activations ----------------
+int bitmm_layer_forward_2bit_dev(int64_t rows, int64_t cols, float alpha, const float* row_alpha,
+                                 const uint64_t* bin, int64_t wpr, const uint64_t* row_ptr,
+                                 const uint64_t* col_idx, const float* vals, const uint64_t* t,
+                                 const uint64_t* h, const uint64_t* m, int64_t tokens,
+                                 float a_scale, int has_a_gamma, float a_gamma, float* c,
+                                 int64_t ldc, void* stream) {
+  g_launches = 0;
+  if (!(a_scale > 0.0f)) return fail(BITMM_ERR_INVALID_ENCODING, "plane scale must be positive");
+  BITMM_TRY(check_gemm_dims(rows, tokens, cols, wpr, ldc));
+  if (!bin || !row_ptr || !t || !h || !m || !c) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  return apb2_dev_impl(*st, rows, cols, wpr, alpha, row_alpha, bin, row_ptr, col_idx, vals, t, h, m,
+                       tokens, a_scale, has_a_gamma ? a_gamma : 1.0f, c, ldc,
+                       static_cast<cudaStream_t>(stream));
+}
+
+int bitmm_layer_forward_2bit_host(int64_t rows, int64_t cols, float alpha, const float* row_alpha,
+                                  const uint64_t* bin, int64_t wpr, const uint64_t* row_ptr,
+                                  const uint64_t* col_idx, const float* vals, int64_t nnz,
+                                  const uint64_t* t, const uint64_t* h, const uint64_t* m,
+                                  int64_t tokens, float a_scale, int has_a_gamma, float a_gamma,
+                                  float* c, int64_t ldc) {
+  g_launches = 0;
+  if (!(a_scale > 0.0f)) return fail(BITMM_ERR_INVALID_ENCODING, "plane scale must be positive");
+  BITMM_TRY(check_gemm_dims(rows, tokens, cols, wpr, ldc));
+  if (!bin || !row_ptr || !t || !h || !m || !c || (nnz > 0 && (!col_idx || !vals)))
+    return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  BITMM_TRY(check_csr_host(rows, cols, row_ptr, col_idx, vals, nnz));
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  cudaStream_t s = st->stream;
+  const size_t w_bytes = rows * wpr * 8, p_bytes = tokens * wpr * 8, c_bytes = rows * ldc * 4;
+  const size_t rp_bytes = (rows + 1) * 8, ci_bytes = std::max<int64_t>(nnz, 1) * 8,
+               v_bytes = std::max<int64_t>(nnz, 1) * 4;
+  BITMM_TRY(arena_reserve(st->io, align_up(w_bytes, 1024) + 3 * align_up(p_bytes, 1024) +
+                                      align_up(c_bytes, 1024) + align_up(rows * 4, 1024) +
+                                      align_up(rp_bytes, 1024) + align_up(ci_bytes, 1024) +
+                                      align_up(v_bytes, 1024) + 4096));
+  Carve cv(st->io.ptr);
+  uint64_t* dw = cv.take<uint64_t>(w_bytes);
+  uint64_t* dt = cv.take<uint64_t>(p_bytes);
+  uint64_t* dh = cv.take<uint64_t>(p_bytes);
+  uint64_t* dm = cv.take<uint64_t>(p_bytes);
+  float* dc = cv.take<float>(c_bytes);
+  float* da = row_alpha ? cv.take<float>(rows * 4) : nullptr;
+  uint64_t* drp = cv.take<uint64_t>(rp_bytes);
+  uint64_t* dci = cv.take<uint64_t>(ci_bytes);
+  float* dv = cv.take<float>(v_bytes);
+  BITMM_CUDA_TRY(cudaMemcpyAsync(dw, bin, w_bytes, cudaMemcpyHostToDevice, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(dt, t, p_bytes, cudaMemcpyHostToDevice, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(dh, h, p_bytes, cudaMemcpyHostToDevice, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(dm, m, p_bytes, cudaMemcpyHostToDevice, s));
+  if (da) BITMM_CUDA_TRY(cudaMemcpyAsync(da, row_alpha, rows * 4, cudaMemcpyHostToDevice, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(drp, row_ptr, rp_bytes, cudaMemcpyHostToDevice, s));
+  if (nnz > 0) {
+    BITMM_CUDA_TRY(cudaMemcpyAsync(dci, col_idx, nnz * 8, cudaMemcpyHostToDevice, s));
+    BITMM_CUDA_TRY(cudaMemcpyAsync(dv, vals, nnz * 4, cudaMemcpyHostToDevice, s));
+  }
+  BITMM_TRY(apb2_dev_impl(*st, rows, cols, wpr, alpha, da, dw, drp, dci, dv, dt, dh, dm, tokens,
+                          a_scale, has_a_gamma ? a_gamma : 1.0f, dc, ldc, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(c, dc, c_bytes, cudaMemcpyDeviceToHost, s));
+  return read_status(*st, s);
 }
 
 }  // extern "C"

@@ -101,11 +101,13 @@ __global__ void __launch_bounds__(PC_THREADS)
 
 // Plain CSR x dense product, standalone spmm_csr (kernels.cpp:334-352): one warp
 // per output row segment of 128 columns, nonzeros walked in col_idx order,
-// separate fp32 multiply and add exactly as the reference row loop.
+// separate fp32 multiply and add exactly as the reference row loop. accumulate: C += R.B
+// (one more fp32 add per cell, the layer's bin_part + res_part).
 __global__ void spmm_csr_kernel(long long rows, const unsigned long long* __restrict__ row_ptr,
                                 const unsigned long long* __restrict__ col_idx,
                                 const float* __restrict__ vals, const float* __restrict__ b,
-                                long long ldb, int N, float* __restrict__ c, long long ldc) {
+                                long long ldb, int N, float* __restrict__ c, long long ldc,
+                                int accumulate) {
   const long long warp_global = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int segs = (N + 127) / 128;
@@ -126,7 +128,7 @@ __global__ void spmm_csr_kernel(long long rows, const unsigned long long* __rest
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const int cc = col0 + lane + 32 * e;
-    if (cc < N) c[r * ldc + cc] = acc[e];
+    if (cc < N) c[r * ldc + cc] = accumulate ? __fadd_rn(c[r * ldc + cc], acc[e]) : acc[e];
   }
 }
 

@@ -10,10 +10,9 @@
 //   1/2 : A = sign(w) in {-1,+1},  B = level p in {0..3}   units = 2*acc
 //   2/2 : A = level p_w in {0..3}, B = level p_a in {0..3} units = 4*acc
 // with acc = sum_k A[r][k]*B[c][k] accumulated exactly in s32 TMEM.
-// The APB binary part (kernels.cpp:300-332) runs the same pipeline with
-// kind::f16 (bf16 +-1 weights times a 3-way bf16 split of the fp32
-// activations, f32 accumulate) and fuses the CSR residual SpMM
-// (kernels.cpp:334-352) into the epilogue.
+// The fp32-activation APB layer has its own bf16 kernel (apb_gemm.cuh); the
+// 2-bit-activation APB layer runs this kernel with the F32ACC epilogue, which
+// adds the binary part onto the residual SpMM already stored in C.
 //
 // Structure (persistent; one CTA, or one CTA pair, per SM / SM pair):
 //   warp 0      : TMA producer, multi-stage smem ring of 128-byte K slices
@@ -32,14 +31,18 @@
 namespace bitmm_dev {
 
 enum class Kind : int { I8 = 0, BF16 = 1 };
-enum class Epi : int { I32 = 0, F32 = 1, APB = 2 };
+// I32: integer units. F32: scale * units. F32R: half_r * units with the reference's per-row
+// scale order ((row_pre * alpha_r) * act_scale) * act_gamma (kernels.cpp:193), used by the
+// 2-bit-activation APB layer (whose residual SpMM then adds onto C).
+enum class Epi : int { I32 = 0, F32 = 1, F32R = 2 };
 
 constexpr int TC_BN = 256;         // output columns per tile (TMEM columns per accumulator)
 constexpr int TC_BK_BYTES = 128;   // one 128-byte swizzle row per operand row per stage
 constexpr int TC_THREADS = 192;
-constexpr int TC_EPI_STRIDE = 36;  // staged row stride in words (16B aligned, conflict-free)
+constexpr int TC_EPI_STRIDE = 36;  // fallback staging row stride in words (conflict-free)
 constexpr int TC_GROUP_M = 16;     // tile raster: groups of 16 M-tiles for L2 reuse
-constexpr int TC_EPI_BYTES = 4 * 32 * TC_EPI_STRIDE * 4;
+constexpr int TC_EPI_BUF = 32 * 32 * 4;        // one 32x32 fp32/int32 block, 128B-swizzled
+constexpr int TC_EPI_BYTES = 4 * 2 * TC_EPI_BUF;  // 4 epilogue warps x 2 buffers
 
 template <bool PAIR>
 struct TcShape {
@@ -64,12 +67,9 @@ struct TcParams {
   int32_t* out_i32;
   float* out_f32;
   long long ldc;
-  // APB residual (CSR rows = output rows), activations X [K][ldx] fp32
-  const unsigned long long* csr_row_ptr;
-  const unsigned long long* csr_col;
-  const float* csr_val;
-  const float* X;
-  long long ldx;
+  // F32R: per-row scale factors in the reference's multiplication order
+  float row_pre, act_scale, act_gamma;
+  int tma_store;     // 1: output through the tensor map (ldc*4 % 16 == 0, 16B-aligned base)
   int num_m_blocks, num_n_blocks, num_tiles;
 };
 
@@ -84,17 +84,26 @@ __device__ __forceinline__ void tc_tile_coords(int t, const TcParams& p, int& mb
 }
 
 // Drains one 128-row x 256-column TMEM accumulator owned by this CTA into global
-// memory. Warp w (2..5) reads TMEM lanes 32*(w%4).. and stages 32x32 blocks
-// through smem so global stores are row-contiguous 128-byte segments.
+// memory. Warp w (2..5) reads TMEM lanes 32*(w%4).. (one output row per thread) in
+// 32-column blocks. TMA path: the block is written into one of the warp's two 4 KB
+// buffers in the 128B-swizzled layout (16-byte chunk j of row r at chunk j ^ (r & 7):
+// conflict-free), then lane 0 issues one bulk tensor store and moves on; a buffer is
+// rewritten only after the store issued from it two blocks earlier has finished reading.
+// Fallback (unaligned ldc): stride-36 staging and coalesced 4-row x 128 B stores.
 template <Epi EPI>
-__device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, uint32_t tmem_acc, int quad,
-                                                 int lane, int row_base, int col_base, float* stg) {
+__device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, const CUtensorMap* tmC,
+                                                 uint32_t tmem_acc, int quad, int lane,
+                                                 int row_base, int col_base, float* stg,
+                                                 uint32_t& buf) {
   const bool vec_ok = (p.N & 3) == 0;
   const int my_row = row_base + lane;
   float row_mul = p.scale;
-  if constexpr (EPI == Epi::F32 || EPI == Epi::APB) {
+  if constexpr (EPI == Epi::F32) {
+    if (p.row_scale != nullptr && my_row < p.M) row_mul = p.scale * p.row_scale[my_row];
+  } else if constexpr (EPI == Epi::F32R) {
     if (p.row_scale != nullptr && my_row < p.M)
-      row_mul = (EPI == Epi::APB) ? p.row_scale[my_row] : p.scale * p.row_scale[my_row];
+      row_mul = __fmul_rn(__fmul_rn(__fmul_rn(p.row_pre, p.row_scale[my_row]), p.act_scale),
+                          p.act_gamma);
   }
 #pragma unroll 1
   for (int c = 0; c < TC_BN / 32; ++c) {
@@ -103,7 +112,12 @@ __device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, uint32_t tme
     uint32_t v[32];
     tmem_ld_32x32b_x32(tmem_acc + (static_cast<uint32_t>(quad * 32) << 16) + c * 32, v);
     tmem_ld_wait();
-    // ---- per-thread (row) transform, staged row-major into smem ----
+    float* sb = stg + buf * (TC_EPI_BUF / 4);
+    if (p.tma_store) {
+      if (lane == 0) bulk_wait_group_read<1>();
+      __syncwarp();
+    }
+    // ---- per-thread (row) transform into smem ----
 #pragma unroll
     for (int j = 0; j < 32; j += 4) {
       float4 o;
@@ -121,75 +135,41 @@ __device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, uint32_t tme
           }
           of[e] = __fmul_rn(s, units);
         } else {
-          of[e] = __fmul_rn(row_mul, __uint_as_float(v[j + e]));
+          of[e] = __fmul_rn(row_mul, static_cast<float>(static_cast<int>(v[j + e]) << p.shift));
         }
       }
-      *reinterpret_cast<float4*>(&stg[lane * TC_EPI_STRIDE + j]) = o;
+      const int off = p.tma_store ? lane * 32 + (((j >> 2) ^ (lane & 7)) << 2) : lane * TC_EPI_STRIDE + j;
+      *reinterpret_cast<float4*>(&sb[off]) = o;
+    }
+    if (p.tma_store) {
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(tmC, sb, col0, row_base);
+        bulk_commit_group();
+      }
+      buf ^= 1u;
+      continue;
     }
     __syncwarp();
-    if constexpr (EPI != Epi::APB) {
-      // ---- coalesced write-out: 4 rows x 128 B per warp instruction ----
+    // ---- fallback write-out: 4 rows x 128 B per warp instruction ----
 #pragma unroll
-      for (int r8 = 0; r8 < 8; ++r8) {
-        const int rl = r8 * 4 + (lane >> 3);
-        const int cl = (lane & 7) * 4;
-        const int grow = row_base + rl;
-        const int gcol = col0 + cl;
-        if (grow < p.M) {
-          const float4 val = *reinterpret_cast<const float4*>(&stg[rl * TC_EPI_STRIDE + cl]);
-          void* dst_base = (EPI == Epi::I32) ? static_cast<void*>(p.out_i32)
-                                             : static_cast<void*>(p.out_f32);
-          uint32_t* dst = static_cast<uint32_t*>(dst_base) + static_cast<long long>(grow) * p.ldc;
-          if (vec_ok && gcol + 3 < p.N) {
-            *reinterpret_cast<float4*>(dst + gcol) = val;
-          } else {
-            const float* vf = reinterpret_cast<const float*>(&val);
-            for (int e = 0; e < 4; ++e)
-              if (gcol + e < p.N) dst[gcol + e] = __float_as_uint(vf[e]);
-          }
-        }
-      }
-    } else {
-      // ---- APB: add the CSR residual rows (kernels.cpp:341-350 order), store ----
-      const int g = lane >> 3;
-      const int sub = lane & 7;
-#pragma unroll 1
-      for (int r8 = 0; r8 < 8; ++r8) {
-        const int rl = r8 * 4 + g;
-        const int grow = row_base + rl;
-        if (grow >= p.M) continue;
-        const int gcol = col0 + sub * 4;
-        float4 o = *reinterpret_cast<const float4*>(&stg[rl * TC_EPI_STRIDE + sub * 4]);
-        float res[4] = {0.f, 0.f, 0.f, 0.f};
-        if (p.csr_row_ptr != nullptr) {
-          const unsigned long long i0 = p.csr_row_ptr[grow];
-          const unsigned long long i1 = p.csr_row_ptr[grow + 1];
-          for (unsigned long long i = i0; i < i1; ++i) {
-            const float val = p.csr_val[i];
-            const float* xr = p.X + static_cast<long long>(p.csr_col[i]) * p.ldx;
-            if (vec_ok && gcol + 3 < p.N) {
-              const float4 x4 = *reinterpret_cast<const float4*>(xr + gcol);
-              res[0] = __fadd_rn(res[0], __fmul_rn(val, x4.x));
-              res[1] = __fadd_rn(res[1], __fmul_rn(val, x4.y));
-              res[2] = __fadd_rn(res[2], __fmul_rn(val, x4.z));
-              res[3] = __fadd_rn(res[3], __fmul_rn(val, x4.w));
-            } else {
-              for (int e = 0; e < 4; ++e)
-                if (gcol + e < p.N) res[e] = __fadd_rn(res[e], __fmul_rn(val, xr[gcol + e]));
-            }
-          }
-        }
-        o.x = __fadd_rn(o.x, res[0]);
-        o.y = __fadd_rn(o.y, res[1]);
-        o.z = __fadd_rn(o.z, res[2]);
-        o.w = __fadd_rn(o.w, res[3]);
-        float* dst = p.out_f32 + static_cast<long long>(grow) * p.ldc;
+    for (int r8 = 0; r8 < 8; ++r8) {
+      const int rl = r8 * 4 + (lane >> 3);
+      const int cl = (lane & 7) * 4;
+      const int grow = row_base + rl;
+      const int gcol = col0 + cl;
+      if (grow < p.M) {
+        const float4 val = *reinterpret_cast<const float4*>(&sb[rl * TC_EPI_STRIDE + cl]);
+        void* dst_base = (EPI == Epi::I32) ? static_cast<void*>(p.out_i32)
+                                           : static_cast<void*>(p.out_f32);
+        uint32_t* dst = static_cast<uint32_t*>(dst_base) + static_cast<long long>(grow) * p.ldc;
         if (vec_ok && gcol + 3 < p.N) {
-          *reinterpret_cast<float4*>(dst + gcol) = o;
+          *reinterpret_cast<float4*>(dst + gcol) = val;
         } else {
-          const float* of = reinterpret_cast<const float*>(&o);
+          const float* vf = reinterpret_cast<const float*>(&val);
           for (int e = 0; e < 4; ++e)
-            if (gcol + e < p.N) dst[gcol + e] = of[e];
+            if (gcol + e < p.N) dst[gcol + e] = __float_as_uint(vf[e]);
         }
       }
     }
@@ -200,7 +180,7 @@ __device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, uint32_t tme
 template <Kind KIND, Epi EPI, bool PAIR>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const TcParams p) {
+                   const __grid_constant__ CUtensorMap tmC, const TcParams p) {
   using S = TcShape<PAIR>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = smem_u32(smem_raw);
@@ -223,6 +203,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (p.tma_store) tma_prefetch_desc(&tmC);
     for (int s = 0; s < S::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -334,7 +315,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else {
     // ===================== epilogue (warps 2..5 of every CTA) =====================
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
-    float* stg = sEpi + (warp - 2) * 32 * TC_EPI_STRIDE;
+    float* stg = sEpi + (warp - 2) * (2 * TC_EPI_BUF / 4);
+    uint32_t buf = 0;
     int it = 0;
     for (int tile = unit; tile < p.num_tiles; tile += num_units, ++it) {
       int mb, nb;
@@ -344,13 +326,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const int row_base = mb * S::TILE_M + static_cast<int>(rank) * 128 + quad * 32;
-      tc_epilogue_tile<EPI>(p, tmem_base + acc * TC_BN, quad, lane, row_base, nb * TC_BN, stg);
+      tc_epilogue_tile<EPI>(p, &tmC, tmem_base + acc * TC_BN, quad, lane, row_base, nb * TC_BN, stg,
+                            buf);
       tc_fence_before();
       if constexpr (PAIR)
         mbar_arrive_cluster(smem_u32(&tempty[acc]) & kPeerBitMask);
       else
         mbar_arrive(&tempty[acc]);
     }
+    if (p.tma_store && lane == 0) bulk_wait_group_all();  // stores land before the grid ends
   }
 
   tc_fence_before();

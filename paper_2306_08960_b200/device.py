@@ -111,6 +111,22 @@ def layer_forward(bin_words: torch.Tensor, cols: int, alpha, row_ptr, col_idx, v
         _ptr(vals), _ptr(b), n, b.shape[1], _ptr(out), out.shape[1], _stream(stream)))
 
 
+def layer_forward_2bit(bin_words: torch.Tensor, cols: int, alpha, row_ptr, col_idx, vals,
+                       t: torch.Tensor, h: torch.Tensor, m: torch.Tensor, out: torch.Tensor,
+                       a_scale: float = 1.0, a_gamma: Optional[float] = None, stream=None) -> None:
+    """APB with 2-bit activations: out[rows][tokens] = gemm_1x2(bin, alpha, planes) +
+    spmm_csr(residual, dequant(planes)); planes are tokens x wpr."""
+    rows, wpr = bin_words.shape
+    if isinstance(alpha, torch.Tensor):
+        a_scalar, a_vec = 1.0, alpha
+    else:
+        a_scalar, a_vec = float(alpha), None
+    _raise(_lib.load().bitmm_layer_forward_2bit_dev(
+        rows, cols, a_scalar, _ptr(a_vec), _ptr(bin_words), wpr, _ptr(row_ptr), _ptr(col_idx),
+        _ptr(vals), _ptr(t), _ptr(h), _ptr(m), t.shape[0], a_scale, int(a_gamma is not None),
+        1.0 if a_gamma is None else a_gamma, _ptr(out), out.shape[1], _stream(stream)))
+
+
 def pack_signs(a: torch.Tensor, lane_bits: int = 512, out: Optional[torch.Tensor] = None,
                stream=None) -> torch.Tensor:
     """GPU pack_signs (tensor.cpp:155-164): fp32 [rows, cols] -> int64 view of the BitMatrix
