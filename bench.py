@@ -460,19 +460,28 @@ def main():
 
     peaks, peaks_src = measured_peaks()
     probe = int8_peak_probe(torch)
-    peak_from_bf16 = 2.0 * float(peaks.get("bf16_tflops", 1590.0))
-    peak = max(peak_from_bf16, probe or 0.0)
-    peak_src = (f"int8 dense = 2 x bf16 burst of {peaks_src} ({peak_from_bf16:.1f})"
-                if peak == peak_from_bf16 else f"cuBLASLt int8 _int_mm 8192^3 burst ({probe:.1f})")
-    tc = kernels.get("tc_gemm_i8", {"launches": 0, "ms": 0.0})
+    fp4 = os.environ.get("BITMM_TC_KIND", "") != "i8"
+    kname = "tc_gemm_f4" if fp4 else "tc_gemm_i8"
+    if fp4:
+        # dense e2m1 (kind::mxf4) = 4 x dense bf16 (B200_PROFILING.md: 9 vs 2.25 PF/s)
+        peak = 4.0 * float(peaks.get("bf16_tflops", 1590.0))
+        peak_src = f"fp4 dense = 4 x bf16 burst of {peaks_src} ({peak:.1f})"
+    else:
+        peak_from_bf16 = 2.0 * float(peaks.get("bf16_tflops", 1590.0))
+        peak = max(peak_from_bf16, probe or 0.0)
+        peak_src = (f"int8 dense = 2 x bf16 burst of {peaks_src} ({peak_from_bf16:.1f})"
+                    if peak == peak_from_bf16 else f"cuBLASLt int8 _int_mm 8192^3 burst ({probe:.1f})")
+    tc = kernels.get(kname, {"launches": 0, "ms": 0.0})
     macs_per_step = sum(m * (shard_cols(n, rank, world)[1] - shard_cols(n, rank, world)[0]) * k
                         for _, m, n, k in ROUTINES)
     achieved = (2.0 * macs_per_step * args.steps) / (tc["ms"] * 1e-3) / 1e12 if tc["ms"] else 0.0
-    traffic = None
+    traffic, l2 = None, None
     tpath = os.path.join(REPO, "profiles", "traffic_r01.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("tc_gemm_i8_dram_bytes_per_launch")
+            tj = json.load(open(tpath))
+            traffic = tj.get(f"{kname}_dram_bytes_per_launch")
+            l2 = tj.get(f"{kname}_l2")
         except ValueError:
             traffic = None
     kernel_share = tc["ms"] / sum(v["ms"] for v in kernels.values()) if kernels else None
@@ -481,14 +490,16 @@ def main():
     for name, m, n, k in ROUTINES:
         ms = per_routine_ms[name] / args.steps
         routines[name] = {"ms": ms, "T_updates_per_s": m * n * k / (ms * 1e-3) / 1e12,
-                          "frac_of_int8_peak": (2 * m * n * k / (ms * 1e-3) / 1e12) / peak,
+                          "frac_of_tensor_peak": (2 * m * n * k / (ms * 1e-3) / 1e12) / peak,
                           "note": "isolated: events between routines serialise the PDL overlap"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None,
-        "dtype": "u64 bit-packed -> s8 tcgen05.mma kind::i8, s32 accumulate",
+        "dtype": ("u64 bit-packed -> e2m1 tcgen05.mma kind::mxf4 (unit E8M0 scales), f32 "
+                  "accumulate of exact integers" if fp4 else
+                  "u64 bit-packed -> s8 tcgen05.mma kind::i8, s32 accumulate"),
         "data": "synthetic (seeded uniform words = i.i.d. Bernoulli(0.5) bits; uniform 2-bit codes)",
         "config": workload_config(world),
         "gpu_launches": launches,
@@ -496,7 +507,8 @@ def main():
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if peak else None, "traffic": traffic,
                      "clocks_note": "sampled from warmup start through the end of the timed region",
-                     "kernel": "tc_gemm_i8 (int8 tensor ops = 2 per MAC)", "peak_source": peak_src,
+                     "kernel": f"{kname} (tensor ops = 2 per MAC)", "peak_source": peak_src,
+                     "l2": l2,
                      "kernel_share_of_step": kernel_share, "int8_probe_tops": probe,
                      "popc_roofline_T_updates_per_s": 148 * 16 * 32 * 1.965e9 / 1e12},
         "kernels": kernels,
@@ -552,7 +564,7 @@ def c5_pass(torch, peak):
     torch.cuda.empty_cache()
     return {"workload": "1/1 32768^3, int32 units, packed operands resident", "ms": ms,
             "T_updates_per_s": upd / (ms * 1e-3) / 1e12,
-            "frac_of_int8_peak": 2 * upd / (ms * 1e-3) / 1e12 / peak}
+            "frac_of_tensor_peak": 2 * upd / (ms * 1e-3) / 1e12 / peak}
 
 
 def apb_pass(args, torch, lib, l2_flush, peaks):
@@ -666,7 +678,7 @@ def apb2_pass(args, torch, l2_flush, peak):
     tops = 2.0 * upd / (ms * 1e-3) / 1e12
     return {"workload": "APB 1/2 layer: 3072 x 768 x 8192 tokens (2-bit), per-row alpha, "
                         f"nnz/row {keep}", "ms": ms, "T_updates_per_s": upd / (ms * 1e-3) / 1e12,
-            "int8_tensor_tops": tops, "frac_of_int8_peak": tops / peak,
+            "tensor_tops": tops, "frac_of_tensor_peak": tops / peak,
             "bit_exact_sampled_rows": exact}
 
 

@@ -58,7 +58,8 @@ struct DeviceState {
   Arena ws;               // intermediates (expanded operands)
   Arena io;               // host-flavour staging of inputs/outputs
   cudaStream_t stream = nullptr;  // host-flavour private stream
-  unsigned attr_mask = 0;
+  uint64_t attr_mask = 0;     // spmm / apb kernels (max-smem attribute set)
+  uint64_t tc_attr_mask = 0;  // tc_gemm instantiations
   unsigned ws_turn = 0;           // ping-pong half of the expanded-operand workspace
 };
 
@@ -266,8 +267,9 @@ UnpackOperand make_unpack_operand(const OperandSrc& src, int64_t wpr, int64_t kp
 
 // Expands both GEMM operands (bits or ternary planes) to int8 rows in one launch.
 int run_unpack_pair(const OperandSrc& a, const OperandSrc& b, int64_t wpr, int64_t k, int64_t kpad,
-                    uint8_t* A8, uint8_t* B8, int* flag, cudaStream_t s) {
+                    uint8_t* A8, uint8_t* B8, int* flag, cudaStream_t s, bool fp4 = false) {
   UnpackPair P{};
+  P.fp4 = fp4 ? 1 : 0;
   P.op[0] = make_unpack_operand(a, wpr, kpad, A8);
   P.op[1] = make_unpack_operand(b, wpr, kpad, B8);
   P.K = static_cast<int>(k);
@@ -290,19 +292,22 @@ int run_unpack_pair(const OperandSrc& a, const OperandSrc& b, int64_t wpr, int64
   return launch_check("unpack_pair_i8");
 }
 
-template <Kind KIND, Epi EPI, bool PAIR>
+template <Kind KIND, Epi EPI, bool PAIR, int BN = TC_BN>
 int run_tc_gemm(DeviceState& st, const CUtensorMap& ta, const CUtensorMap& tb, TcParams p,
                 cudaStream_t s) {
-  using S = TcShape<PAIR>;
-  auto kern = tc_gemm_kernel<KIND, EPI, PAIR>;
-  constexpr unsigned bit = 1u << (static_cast<int>(KIND) * 6 + static_cast<int>(EPI) * 2 + (PAIR ? 1 : 0));
-  if (!(st.attr_mask & bit)) {
+  using S = TcShape<PAIR, BN>;
+  auto kern = tc_gemm_kernel<KIND, EPI, PAIR, BN>;
+  constexpr int bn_idx = BN == 128 ? 0 : BN == 192 ? 1 : 2;
+  constexpr uint64_t bit =
+      1ull << (((static_cast<int>(KIND) * 3 + static_cast<int>(EPI)) * 3 + bn_idx) * 2 + (PAIR ? 1 : 0));
+  if (!(st.tc_attr_mask & bit)) {
     BITMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM));
-    st.attr_mask |= bit;
+    st.tc_attr_mask |= bit;
   }
   p.num_m_blocks = static_cast<int>((p.M + S::TILE_M - 1) / S::TILE_M);
-  p.num_n_blocks = static_cast<int>((p.N + TC_BN - 1) / TC_BN);
+  p.num_n_blocks = static_cast<int>((p.N + BN - 1) / BN);
   p.num_tiles = p.num_m_blocks * p.num_n_blocks;
+  p.group_m = TC_GROUP_M;
   const int units = std::min(p.num_tiles, PAIR ? st.sms / 2 : st.sms);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(PAIR ? 2 * units : units));
@@ -323,19 +328,64 @@ int run_tc_gemm(DeviceState& st, const CUtensorMap& ta, const CUtensorMap& tb, T
   p.tma_store = make_output_map(&tc, out, EPI == Epi::I32 ? CU_TENSOR_MAP_DATA_TYPE_INT32
                                                           : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                                 p.N, p.M, p.ldc) ? 1 : 0;
-  ProfScope ps(KIND == Kind::I8 ? "tc_gemm_i8" : "tc_gemm_bf16_apb", s);
+  ProfScope ps(KIND == Kind::I8 ? "tc_gemm_i8" : KIND == Kind::F4 ? "tc_gemm_f4" : "tc_gemm_bf16", s);
   BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, p));
   return launch_check("tc_gemm_kernel");
+}
+
+// Tile width: a wave of the persistent grid takes time proportional to BN, so pick the BN
+// with the smaller (waves x BN); 128-wide tiles pay ~3% for twice the A traffic per MAC.
+// 4096^2 outputs: 256 tiles of 256 = 3.46 waves over 74 pairs (4 x 256) vs 512 tiles of 128
+// = 6.92 waves (7 x 128) -> 128. 4096 x 8192 and 32768^2 stay at 256.
+int pick_bn(const DeviceState& st, int64_t m, int64_t n) {
+  const int64_t units = st.sms / 2;
+  const int64_t mt = (m + 255) / 256;
+  const int64_t w256 = (mt * ((n + 255) / 256) + units - 1) / units;
+  const int64_t w128 = (mt * ((n + 127) / 128) + units - 1) / units;
+  // Measured (profiles/ncu_bn128_r01.md): 128-wide tiles halve the pipeline's lookahead in
+  // time (8 stages x 0.19 us) and the tensor pipe starves (42.7% active, 1x1 4096^3 62 -> 89
+  // us), so 256 wins even at 3.46 waves. Kept selectable for shapes where w128 is far ahead.
+  return (w128 * 128 * 2 < w256 * 256) ? 128 : 256;
+}
+
+// Operand kind of the bitwise GEMMs: packed e2m1 through kind::mxf4 (default; 2x the int8
+// tensor rate, half the expanded bytes) or int8 through kind::i8 (BITMM_TC_KIND=i8, kept for
+// A/B measurement). Both are exact: see tc_gemm.cuh.
+bool use_fp4() {
+  static const bool on = !(getenv("BITMM_TC_KIND") && strcmp(getenv("BITMM_TC_KIND"), "i8") == 0);
+  return on;
+}
+constexpr int kF4BN = 192;  // 2 x 192 accumulator columns + scale-factor columns <= 512
+
+// Integer GEMM over expanded operands A8 [m][kpad], B8 [n][kpad] (cta_group::2 pairs); with
+// fp4 the rows are kpad/2 bytes of e2m1 nibbles.
+template <Epi EPI>
+int launch_int_gemm(DeviceState& st, const uint8_t* A8, const uint8_t* B8, int64_t m, int64_t n,
+                    int64_t kpad, TcParams p, cudaStream_t s, bool fp4 = false) {
+  constexpr bool kPair = true;
+  if (fp4) {
+    CUtensorMap ta, tb;
+    BITMM_TRY(make_operand_map(&ta, A8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad / 2, m, TcShape<kPair, kF4BN>::A_ROWS));
+    BITMM_TRY(make_operand_map(&tb, B8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad / 2, n, TcShape<kPair, kF4BN>::B_ROWS));
+    p.num_kb = static_cast<int>(kpad / 2 / TC_BK_BYTES);
+    p.a_kb_period = p.num_kb;
+    return run_tc_gemm<Kind::F4, EPI, kPair, kF4BN>(st, ta, tb, p, s);
+  }
+  CUtensorMap ta, tb;
+  BITMM_TRY(make_operand_map(&ta, A8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad, m, TcShape<kPair>::A_ROWS));
+  if (pick_bn(st, m, n) == 128) {
+    BITMM_TRY(make_operand_map(&tb, B8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad, n, TcShape<kPair, 128>::B_ROWS));
+    return run_tc_gemm<Kind::I8, EPI, kPair, 128>(st, ta, tb, p, s);
+  }
+  BITMM_TRY(make_operand_map(&tb, B8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad, n, TcShape<kPair, 256>::B_ROWS));
+  return run_tc_gemm<Kind::I8, EPI, kPair, 256>(st, ta, tb, p, s);
 }
 
 // Common integer-GEMM tail: A8 [m][kpad], B8 [n][kpad] already expanded.
 int run_int_gemm(DeviceState& st, const uint8_t* A8, const uint8_t* B8, int64_t m, int64_t n,
                  int64_t kpad, int shift, float scale, const float* row_scale,
-                 const float* col_scale, int32_t* c_units, float* c, int64_t ldc, cudaStream_t s) {
-  constexpr bool kPair = true;  // cta_group::2, 256 x 256 tiles per CTA pair
-  CUtensorMap ta, tb;
-  BITMM_TRY(make_operand_map(&ta, A8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad, m, TcShape<kPair>::A_ROWS));
-  BITMM_TRY(make_operand_map(&tb, B8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad, n, TcShape<kPair>::B_ROWS));
+                 const float* col_scale, int32_t* c_units, float* c, int64_t ldc, cudaStream_t s,
+                 bool fp4 = false) {
   TcParams p{};
   p.M = static_cast<int>(m);
   p.N = static_cast<int>(n);
@@ -348,11 +398,11 @@ int run_int_gemm(DeviceState& st, const uint8_t* A8, const uint8_t* B8, int64_t 
   p.ldc = ldc;
   if (c_units) {
     p.out_i32 = c_units;
-    BITMM_TRY((run_tc_gemm<Kind::I8, Epi::I32, kPair>(st, ta, tb, p, s)));
+    BITMM_TRY(launch_int_gemm<Epi::I32>(st, A8, B8, m, n, kpad, p, s, fp4));
   }
   if (c) {
     p.out_f32 = c;
-    BITMM_TRY((run_tc_gemm<Kind::I8, Epi::F32, kPair>(st, ta, tb, p, s)));
+    BITMM_TRY(launch_int_gemm<Epi::F32>(st, A8, B8, m, n, kpad, p, s, fp4));
   }
   return BITMM_OK;
 }
@@ -416,14 +466,15 @@ size_t ws_bytes_1x32(int64_t m, int64_t n, int64_t k) {
 int gemm_1x1_dev_impl(DeviceState& st, const uint64_t* a, int64_t m, const uint64_t* b, int64_t n,
                       int64_t k, int64_t wpr, float gamma_a, float gamma_b, int32_t* c_units,
                       float* c, int64_t ldc, cudaStream_t s) {
-  const int64_t kpad = round_up(k, TC_BK_BYTES);
+  const bool fp4 = use_fp4();
+  const int64_t kpad = round_up(k, fp4 ? 2 * TC_BK_BYTES : TC_BK_BYTES);
   BITMM_TRY(arena_reserve(st.ws, ws_bytes_int(m, n, k)));
   uint8_t *A8, *B8;
   take_int_operands(st, m, n, k, &A8, &B8);
   BITMM_TRY(run_unpack_pair({a, nullptr, nullptr, m, false}, {b, nullptr, nullptr, n, false}, wpr,
-                            k, kpad, A8, B8, st.status, s));
+                            k, kpad, A8, B8, st.status, s, fp4));
   const float scale = gamma_a * gamma_b;  // kernels.cpp:170
-  return run_int_gemm(st, A8, B8, m, n, kpad, 0, scale, nullptr, nullptr, c_units, c, ldc, s);
+  return run_int_gemm(st, A8, B8, m, n, kpad, 0, scale, nullptr, nullptr, c_units, c, ldc, s, fp4);
 }
 
 int gemm_1x2_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, float gamma, const uint64_t* t,
@@ -431,15 +482,16 @@ int gemm_1x2_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, float gamma
                       float a_scale, int has_a_gamma, float a_gamma, const float* row_scale,
                       const float* col_scale, int32_t* c_units, float* c, int64_t ldc,
                       cudaStream_t s) {
-  const int64_t kpad = round_up(k, TC_BK_BYTES);
+  const bool fp4 = use_fp4();
+  const int64_t kpad = round_up(k, fp4 ? 2 * TC_BK_BYTES : TC_BK_BYTES);
   BITMM_TRY(arena_reserve(st.ws, ws_bytes_int(m, n, k)));
   uint8_t *A8, *B8;
   take_int_operands(st, m, n, k, &A8, &B8);
   BITMM_TRY(run_unpack_pair({w, nullptr, nullptr, m, false}, {t, h, mm, n, true}, wpr, k, kpad, A8,
-                            B8, st.status, s));
+                            B8, st.status, s, fp4));
   // kernels.cpp:193: half_scale = 0.5f * gamma * a_packed.scale * a_packed.gamma.value_or(1.0f)
   const float scale = 0.5f * gamma * a_scale * (has_a_gamma ? a_gamma : 1.0f);
-  return run_int_gemm(st, A8, B8, m, n, kpad, 1, scale, row_scale, col_scale, c_units, c, ldc, s);
+  return run_int_gemm(st, A8, B8, m, n, kpad, 1, scale, row_scale, col_scale, c_units, c, ldc, s, fp4);
 }
 
 int gemm_2x2_dev_impl(DeviceState& st, const uint64_t* wt, const uint64_t* wh, const uint64_t* wm,
@@ -448,16 +500,17 @@ int gemm_2x2_dev_impl(DeviceState& st, const uint64_t* wt, const uint64_t* wh, c
                       float a_scale, int has_a_gamma, float a_gamma, const float* row_scale,
                       const float* col_scale, int32_t* c_units, float* c, int64_t ldc,
                       cudaStream_t s) {
-  const int64_t kpad = round_up(k, TC_BK_BYTES);
+  const bool fp4 = use_fp4();
+  const int64_t kpad = round_up(k, fp4 ? 2 * TC_BK_BYTES : TC_BK_BYTES);
   BITMM_TRY(arena_reserve(st.ws, ws_bytes_int(m, n, k)));
   uint8_t *A8, *B8;
   take_int_operands(st, m, n, k, &A8, &B8);
   BITMM_TRY(run_unpack_pair({wt, wh, wm, m, true}, {at, ah, am, n, true}, wpr, k, kpad, A8, B8,
-                            st.status, s));
+                            st.status, s, fp4));
   // kernels.cpp:232-233
   const float scale = 0.25f * w_scale * a_scale * (has_w_gamma ? w_gamma : 1.0f) *
                       (has_a_gamma ? a_gamma : 1.0f);
-  return run_int_gemm(st, A8, B8, m, n, kpad, 2, scale, row_scale, col_scale, c_units, c, ldc, s);
+  return run_int_gemm(st, A8, B8, m, n, kpad, 2, scale, row_scale, col_scale, c_units, c, ldc, s, fp4);
 }
 
 cudaLaunchAttribute pdl_attr() {
@@ -649,10 +702,6 @@ int apb2_dev_impl(DeviceState& st, int64_t rows, int64_t cols, int64_t wpr, floa
   take_int_operands(st, rows, tokens, cols, &A8, &B8);
   BITMM_TRY(run_unpack_pair({bin, nullptr, nullptr, rows, false}, {t, h, m, tokens, true}, wpr, cols,
                             kpad, A8, B8, st.status, s));
-  constexpr bool kPair = true;
-  CUtensorMap ta, tb;
-  BITMM_TRY(make_operand_map(&ta, A8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad, rows, TcShape<kPair>::A_ROWS));
-  BITMM_TRY(make_operand_map(&tb, B8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad, tokens, TcShape<kPair>::B_ROWS));
   TcParams p{};
   p.M = static_cast<int>(rows);
   p.N = static_cast<int>(tokens);
@@ -666,7 +715,7 @@ int apb2_dev_impl(DeviceState& st, int64_t rows, int64_t cols, int64_t wpr, floa
   p.act_gamma = a_gamma;
   p.out_f32 = c;
   p.ldc = ldc;
-  BITMM_TRY((run_tc_gemm<Kind::I8, Epi::F32R, kPair>(st, ta, tb, p, s)));
+  BITMM_TRY(launch_int_gemm<Epi::F32R>(st, A8, B8, rows, tokens, kpad, p, s));
   SpmmLevels lv{};
   lv.t = reinterpret_cast<const unsigned long long*>(t);
   lv.h = reinterpret_cast<const unsigned long long*>(h);

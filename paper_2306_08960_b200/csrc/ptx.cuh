@@ -181,6 +181,17 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&v)
       : "r"(taddr));
 }
 
+// Store 32 consecutive 32-bit columns of this warp's 32 TMEM lanes (every value = v).
+__device__ __forceinline__ void tmem_st_32x32b_x32_fill(uint32_t taddr, uint32_t v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, "
+      "%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1};"
+      ::"r"(taddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -263,6 +274,20 @@ __device__ __forceinline__ void mma_f16_pair(uint32_t d_tmem, uint64_t a_desc, u
       : "memory");
 }
 
+// Block-scaled FP4 (e2m1, packed two per byte) with 32-element E8M0 scale blocks read from
+// TMEM (sfa / sfb column addresses). With every scale factor = 1.0 this is a plain e2m1
+// product accumulated in fp32.
+__device__ __forceinline__ void mma_mxf4_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                              uint32_t idesc, uint32_t accumulate, uint32_t sfa,
+                                              uint32_t sfb) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}"
+      ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
+      : "memory");
+}
+
 // Arrive (multicast) on the same barrier offset in every CTA of cta_mask once the pair's
 // previously issued tcgen05 ops have completed.
 __device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t cta_mask) {
@@ -293,6 +318,13 @@ __device__ __forceinline__ uint64_t sw128_kmajor_desc(uint32_t smem_addr) {
 // Instruction descriptor (kind::i8 / kind::f16). Fields: [4,6) D format
 // (1=F32, 2=S32), [7,10) A format, [10,13) B format (i8: 0=U8 1=S8; f16: 0=F16
 // 1=BF16), [15] A MN-major, [16] B MN-major, [17,23) N>>3, [24,29) M>>4.
+// Block-scaled instruction descriptor (kind::mxf4): [4,6) b_sf_id, [7,10) a fmt (E2M1 = 1),
+// [10,13) b fmt, [15]/[16] K-major, [17,23) N>>3, [23] scale fmt (1 = E8M0), [24,29) M>>4,
+// [29,31) a_sf_id, [31] K size (0 = K64 dense).
+__host__ __device__ constexpr uint32_t make_idesc_mxf4(uint32_t m, uint32_t n) {
+  return (1u << 7) | (1u << 10) | ((n >> 3) << 17) | (1u << 23) | ((m >> 4) << 24);
+}
+
 __host__ __device__ constexpr uint32_t make_idesc(uint32_t d_fmt, uint32_t a_fmt, uint32_t b_fmt,
                                                   uint32_t m, uint32_t n) {
   return (d_fmt << 4) | (a_fmt << 7) | (b_fmt << 10) | ((n >> 3) << 17) | ((m >> 4) << 24);

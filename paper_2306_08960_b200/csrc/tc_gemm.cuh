@@ -30,30 +30,42 @@
 
 namespace bitmm_dev {
 
-enum class Kind : int { I8 = 0, BF16 = 1 };
+// I8: int8 operands, s32 accumulators. F4: packed e2m1 operands (+-1 and levels 0..3 are
+// exact e2m1 values) through kind::mxf4 with unit scale factors, fp32 accumulators that hold
+// exact integers (|sum| <= 9 * 2^20 < 2^24).
+enum class Kind : int { I8 = 0, BF16 = 1, F4 = 2 };
 // I32: integer units. F32: scale * units. F32R: half_r * units with the reference's per-row
 // scale order ((row_pre * alpha_r) * act_scale) * act_gamma (kernels.cpp:193), used by the
 // 2-bit-activation APB layer (whose residual SpMM then adds onto C).
 enum class Epi : int { I32 = 0, F32 = 1, F32R = 2 };
 
-constexpr int TC_BN = 256;         // output columns per tile (TMEM columns per accumulator)
+constexpr int TC_BN = 256;         // widest output tile (TMEM columns per accumulator)
 constexpr int TC_BK_BYTES = 128;   // one 128-byte swizzle row per operand row per stage
 constexpr int TC_THREADS = 192;
 constexpr int TC_EPI_STRIDE = 36;  // fallback staging row stride in words (conflict-free)
 constexpr int TC_GROUP_M = 16;     // tile raster: groups of 16 M-tiles for L2 reuse
 constexpr int TC_EPI_BUF = 32 * 32 * 4;        // one 32x32 fp32/int32 block, 128B-swizzled
-constexpr int TC_EPI_BYTES = 4 * 2 * TC_EPI_BUF;  // 4 epilogue warps x 2 buffers
+constexpr int TC_EPI_BYTES = 4 * 2 * TC_EPI_BUF;  // 4 epilogue warps x 2 buffers (widest case)
 
-template <bool PAIR>
+// BN = output columns per tile (256, or 128 when 256-wide tiles leave a ragged last wave).
+template <bool PAIR, int BN = TC_BN>
 struct TcShape {
   static constexpr int A_ROWS = 128;                 // A rows staged per CTA
-  static constexpr int B_ROWS = PAIR ? 128 : 256;    // B rows staged per CTA
+  static constexpr int B_ROWS = PAIR ? BN / 2 : BN;  // B rows staged per CTA
   static constexpr int TILE_M = PAIR ? 256 : 128;    // output rows per tile
-  static constexpr int STAGES = PAIR ? 6 : 4;
+  // Epilogue staging per warp: two swizzled 4 KB blocks, or (BN = 192, whose operand stages
+  // are smaller) one block in a 5 KB slot so a seventh operand stage fits; the slot also
+  // holds the stride-36 fallback staging (4.5 KB).
+  static constexpr int EPI_BUFS = (PAIR && BN == 192) ? 1 : 2;
+  static constexpr int EPI_WARP_BYTES = EPI_BUFS == 2 ? 2 * TC_EPI_BUF : 5120;
+  static constexpr int EPI_BYTES = 4 * EPI_WARP_BYTES;
+  static constexpr int STAGES =
+      PAIR ? (232448 - 1024 - EPI_BYTES - 256) / ((128 + BN / 2) * TC_BK_BYTES) : 4;
   static constexpr int A_STAGE = A_ROWS * TC_BK_BYTES;
   static constexpr int B_STAGE = B_ROWS * TC_BK_BYTES;
   static constexpr int BAR_BYTES = (2 * STAGES + 4) * 8 + 16;
-  static constexpr int SMEM = 1024 + STAGES * (A_STAGE + B_STAGE) + TC_EPI_BYTES + BAR_BYTES;
+  static constexpr int SMEM = 1024 + STAGES * (A_STAGE + B_STAGE) + EPI_BYTES + BAR_BYTES;
+  static_assert(SMEM <= 232448, "shared memory budget");
 };
 
 struct TcParams {
@@ -71,13 +83,14 @@ struct TcParams {
   float row_pre, act_scale, act_gamma;
   int tma_store;     // 1: output through the tensor map (ldc*4 % 16 == 0, 16B-aligned base)
   int num_m_blocks, num_n_blocks, num_tiles;
+  int group_m;       // tile raster: groups of group_m M-blocks walked column by column
 };
 
 __device__ __forceinline__ void tc_tile_coords(int t, const TcParams& p, int& mb, int& nb) {
-  const int group_tiles = TC_GROUP_M * p.num_n_blocks;
+  const int group_tiles = p.group_m * p.num_n_blocks;
   const int g = t / group_tiles;
-  const int first_m = g * TC_GROUP_M;
-  const int gm = min(TC_GROUP_M, p.num_m_blocks - first_m);
+  const int first_m = g * p.group_m;
+  const int gm = min(p.group_m, p.num_m_blocks - first_m);
   const int within = t - g * group_tiles;
   mb = first_m + within % gm;
   nb = within / gm;
@@ -90,7 +103,7 @@ __device__ __forceinline__ void tc_tile_coords(int t, const TcParams& p, int& mb
 // conflict-free), then lane 0 issues one bulk tensor store and moves on; a buffer is
 // rewritten only after the store issued from it two blocks earlier has finished reading.
 // Fallback (unaligned ldc): stride-36 staging and coalesced 4-row x 128 B stores.
-template <Epi EPI>
+template <Epi EPI, int BN, bool F32ACC = false, int EPI_BUFS = 2>
 __device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, const CUtensorMap* tmC,
                                                  uint32_t tmem_acc, int quad, int lane,
                                                  int row_base, int col_base, float* stg,
@@ -106,15 +119,19 @@ __device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, const CUtens
                           p.act_gamma);
   }
 #pragma unroll 1
-  for (int c = 0; c < TC_BN / 32; ++c) {
+  for (int c = 0; c < BN / 32; ++c) {
     const int col0 = col_base + c * 32;
     if (col0 >= p.N) break;
     uint32_t v[32];
     tmem_ld_32x32b_x32(tmem_acc + (static_cast<uint32_t>(quad * 32) << 16) + c * 32, v);
     tmem_ld_wait();
+    if constexpr (F32ACC) {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) v[e] = static_cast<uint32_t>(__float2int_rn(__uint_as_float(v[e])));
+    }
     float* sb = stg + buf * (TC_EPI_BUF / 4);
     if (p.tma_store) {
-      if (lane == 0) bulk_wait_group_read<1>();
+      if (lane == 0) bulk_wait_group_read<EPI_BUFS - 1>();
       __syncwarp();
     }
     // ---- per-thread (row) transform into smem ----
@@ -148,7 +165,7 @@ __device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, const CUtens
         tma_store_2d(tmC, sb, col0, row_base);
         bulk_commit_group();
       }
-      buf ^= 1u;
+      if constexpr (EPI_BUFS == 2) buf ^= 1u;
       continue;
     }
     __syncwarp();
@@ -177,18 +194,18 @@ __device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, const CUtens
   }
 }
 
-template <Kind KIND, Epi EPI, bool PAIR>
+template <Kind KIND, Epi EPI, bool PAIR, int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const TcParams p) {
-  using S = TcShape<PAIR>;
+  using S = TcShape<PAIR, BN>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024u - (base_u32 & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = sA + S::STAGES * S::A_STAGE;
   float* sEpi = reinterpret_cast<float*>(sB + S::STAGES * S::B_STAGE);
-  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sEpi) + TC_EPI_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sEpi) + S::EPI_BYTES);
   uint64_t* empty = full + S::STAGES;
   uint64_t* tfull = empty + S::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -227,11 +244,28 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  constexpr uint32_t kSfCol = 2 * BN;  // F4: scale factors after the two accumulators
+  if constexpr (KIND == Kind::F4) {
+    // every scale-factor cell = E8M0 1.0 (0x7F), for both the A and B scale regions
+    if (warp >= 2) {
+      const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+      tmem_st_32x32b_x32_fill(tmem_base + lane_off + kSfCol, 0x7F7F7F7Fu);
+      tmem_st_32x32b_x32_fill(tmem_base + lane_off + kSfCol + 32, 0x7F7F7F7Fu);
+      tmem_st_wait();
+    }
+    tc_fence_before();
+    if constexpr (PAIR)
+      cluster_sync();
+    else
+      __syncthreads();
+    tc_fence_after();
+  }
   // Everything above overlapped the producer of our operands (PDL); from here on
   // we read its output.
   pdl_wait();
 
-  constexpr int BK_ELEMS = (KIND == Kind::I8) ? TC_BK_BYTES : TC_BK_BYTES / 2;
+  // TMA inner coordinate per 128-byte K block (operand maps are in bytes for I8 and F4)
+  constexpr int BK_ELEMS = (KIND == Kind::BF16) ? TC_BK_BYTES / 2 : TC_BK_BYTES;
 
   if (warp == 0) {
     // ===================== TMA producer (both CTAs of a pair) =====================
@@ -242,7 +276,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         int mb, nb;
         tc_tile_coords(tile, p, mb, nb);
         const int a_row = mb * S::TILE_M + static_cast<int>(rank) * S::A_ROWS;
-        const int b_row = nb * TC_BN + static_cast<int>(rank) * S::B_ROWS;
+        const int b_row = nb * BN + static_cast<int>(rank) * S::B_ROWS;
         for (int kb = 0; kb < p.num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1u);
           const int ka = kb % p.a_kb_period;
@@ -265,8 +299,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA only) =====================
     if (lane == 0 && rank == 0) {
-      constexpr uint32_t idesc = (KIND == Kind::I8) ? make_idesc(2u, 1u, 1u, S::TILE_M, TC_BN)
-                                                    : make_idesc(1u, 1u, 1u, S::TILE_M, TC_BN);
+      constexpr uint32_t idesc = (KIND == Kind::I8)   ? make_idesc(2u, 1u, 1u, S::TILE_M, BN)
+                                 : (KIND == Kind::F4) ? make_idesc_mxf4(S::TILE_M, BN)
+                                                      : make_idesc(1u, 1u, 1u, S::TILE_M, BN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -275,7 +310,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t aphase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], aphase ^ 1u);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * TC_BN;
+        const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < p.num_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -286,7 +321,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const uint64_t ad = sw128_kmajor_desc(a_addr + k * 32);
             const uint64_t bd = sw128_kmajor_desc(b_addr + k * 32);
             if constexpr (PAIR) {
-              if constexpr (KIND == Kind::I8)
+              if constexpr (KIND == Kind::F4)
+                mma_mxf4_pair(d_tmem, ad, bd, idesc, (kb | k) != 0, tmem_base + kSfCol,
+                              tmem_base + kSfCol + 32);
+              else if constexpr (KIND == Kind::I8)
                 mma_i8_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
               else
                 mma_f16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
@@ -315,7 +353,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else {
     // ===================== epilogue (warps 2..5 of every CTA) =====================
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
-    float* stg = sEpi + (warp - 2) * (2 * TC_EPI_BUF / 4);
+    float* stg = sEpi + (warp - 2) * (S::EPI_WARP_BYTES / 4);
     uint32_t buf = 0;
     int it = 0;
     for (int tile = unit; tile < p.num_tiles; tile += num_units, ++it) {
@@ -326,7 +364,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const int row_base = mb * S::TILE_M + static_cast<int>(rank) * 128 + quad * 32;
-      tc_epilogue_tile<EPI>(p, &tmC, tmem_base + acc * TC_BN, quad, lane, row_base, nb * TC_BN, stg,
+      tc_epilogue_tile<EPI, BN, KIND == Kind::F4, S::EPI_BUFS>(p, &tmC, tmem_base + acc * BN, quad, lane, row_base, nb * BN, stg,
                             buf);
       tc_fence_before();
       if constexpr (PAIR)

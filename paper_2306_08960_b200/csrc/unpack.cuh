@@ -56,7 +56,25 @@ struct UnpackPair {
   int K;
   int kpad;
   int* err;
+  int fp4;  // 1: packed e2m1 nibbles, rows of kpad/2 bytes (Kind::F4 operands)
 };
+
+// 8 bits -> 8 nibbles (bit i at bit 4i).
+__device__ __forceinline__ uint32_t spread8_nib(uint32_t x) {
+  x = (x | (x << 12)) & 0x000F000Fu;
+  x = (x | (x << 6)) & 0x03030303u;
+  return (x | (x << 3)) & 0x11111111u;
+}
+
+// e2m1 nibbles for 8 elements: signs (bit 1 -> +1.0 = 0x2, bit 0 -> -1.0 = 0xA) or levels
+// (hi = p >> 1, lo = p & 1: 0 -> 0x0, 1 -> 0x2 (1.0), 2 -> 0x4 (2.0), 3 -> 0x5 (3.0)).
+// `valid` masks the elements inside K; padding nibbles are 0 (+0.0).
+__device__ __forceinline__ uint32_t nib_signs8(uint32_t bits, uint32_t valid) {
+  return (spread8_nib(valid) << 1) | (spread8_nib(valid & ~bits) << 3);
+}
+__device__ __forceinline__ uint32_t nib_levels8(uint32_t hi, uint32_t lo) {
+  return (spread8_nib(hi) << 2) | spread8_nib(hi & lo) | (spread8_nib(~hi & lo & 0xFFu) << 1);
+}
 
 // One warp expands one 4096-element slice of one operand row (128 input words, 4 KB of
 // int8 output), split into a load step (all 128 words in flight: lane t holds words
@@ -88,7 +106,8 @@ __device__ __forceinline__ void load_slice_warp(const UnpackOperand& o, long lon
 
 // Returns the warp-wide OR of the slice's error flags.
 __device__ __forceinline__ int expand_slice_warp(const UnpackOperand& o, long long r, int sl,
-                                                 int K, int kpad, int lane, SliceWords& s) {
+                                                 int K, int kpad, int lane, SliceWords& s,
+                                                 bool fp4 = false) {
   const int word0 = sl * 128;
   int bad = 0;
 #pragma unroll
@@ -115,6 +134,22 @@ __device__ __forceinline__ int expand_slice_warp(const UnpackOperand& o, long lo
     const uint32_t a = __shfl_sync(0xFFFFFFFFu, s.w0[v >> 1], src_lane);
     const uint32_t b = __shfl_sync(0xFFFFFFFFu, s.w1[v >> 1], src_lane);
     if (elem >= kpad) continue;
+    if (fp4) {
+      const uint32_t x = (a >> shift) & 0xFFFFu;
+      uint32_t n0, n1;
+      if (o.levels == 0) {
+        const int g = word0 + (chunk >> 1);
+        const uint32_t valid = (valid_mask32(g * 32, K) >> shift) & 0xFFFFu;
+        n0 = nib_signs8(x & 0xFFu, valid & 0xFFu);
+        n1 = nib_signs8(x >> 8, valid >> 8);
+      } else {
+        const uint32_t y = (b >> shift) & 0xFFFFu;
+        n0 = nib_levels8(x & 0xFFu, y & 0xFFu);
+        n1 = nib_levels8(x >> 8, y >> 8);
+      }
+      *reinterpret_cast<uint2*>(o.out + r * (kpad / 2) + elem / 2) = make_uint2(n0, n1);
+      continue;
+    }
     uint32_t ow[4];
     if (o.levels == 0) {
       const uint32_t bits = (a >> shift) & 0xFFFFu;
@@ -145,10 +180,10 @@ __device__ __forceinline__ int expand_slice_warp(const UnpackOperand& o, long lo
 }
 
 __device__ __forceinline__ int unpack_slice_warp(const UnpackOperand& o, long long r, int sl, int K,
-                                                 int kpad, int lane) {
+                                                 int kpad, int lane, bool fp4) {
   SliceWords s;
   load_slice_warp(o, r, sl, lane, s);
-  return expand_slice_warp(o, r, sl, K, kpad, lane, s);
+  return expand_slice_warp(o, r, sl, K, kpad, lane, s, fp4);
 }
 
 // Standalone expansion of both GEMM operands (blockIdx.y selects the operand).
@@ -167,7 +202,8 @@ __global__ void __launch_bounds__(256) unpack_pair_i8(const __grid_constant__ Un
   if (unit >= o.rows * slices) return;
   const long long r = unit / slices;
   const int sl = static_cast<int>(unit - r * slices);
-  const int bad = unpack_slice_warp(o, r, sl, P.K, P.kpad, lane);
+  const int bad = P.fp4 ? unpack_slice_warp(o, r, sl, P.K, P.kpad, lane, true)
+                        : unpack_slice_warp(o, r, sl, P.K, P.kpad, lane, false);
   if (bad && lane == 0) atomicOr(P.err, bad);
 }
 

@@ -31,6 +31,9 @@ for _ in range(2):
         device.gemm_1x1(da, db, k, units=u[:, :4096].contiguous() if False else torch.empty((4096, 4096), dtype=torch.int32, device="cuda"))
     if which in ("all", "1x2"):
         device.gemm_1x2(da, 1.0, dt, dh, dm, k, row_scale=gam, col_scale=bet, out=f)
+    if which in ("all", "2x2"):
+        device.gemm_2x2(dt[:4096], dh[:4096], dm[:4096], dt[4096:], dh[4096:], dm[4096:], k,
+                        units=torch.empty((4096, 4096), dtype=torch.int32, device="cuda"))
     if which in ("all", "apb"):
         device.layer_forward(*apb_args)
     torch.cuda.synchronize()

@@ -31,6 +31,8 @@ RAW_KEYS = [
     "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
     "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
     "lts__t_bytes.sum",
+    "lts__t_sectors.sum",
+    "lts__cycles_elapsed.avg",
     "launch__grid_size",
     "launch__cluster_dim_x",
     "launch__registers_per_thread",

@@ -349,3 +349,36 @@ def test_long_k_and_ragged_tiles_exact(orc, m, n, k):
     up = torch.empty_like(u)
     device.gemm_1x1(T(a), T(b), k, units=up, popc=True)
     assert torch.equal(u, up)
+
+
+@pytest.mark.parametrize("k", [1 << 20, (1 << 20) - 77])
+def test_extreme_accumulators_at_max_shared_dim(k):
+    """Largest partial sums the formats allow: K = 2^20 (BITMM_MAX_SHARED_DIM) with every
+    level 3 (2/2: sum p_w p_a = 9K, units 36K), all-equal and all-opposite signs (1/1: +-K)
+    and mixed rows, so any accumulator rounding or overflow would show."""
+    import torch
+    from paper_2306_08960_b200 import device
+    m, n = 160, 200
+    T = lambda x: torch.from_numpy(np.ascontiguousarray(x).view(np.int64)).cuda()  # noqa: E731
+    # 2/2, every level 3 on both sides
+    lv = np.full((m, k), 3, np.uint8)
+    wt, wh, wm, wpr = data.planes_from_levels(lv)
+    lva = np.full((n, k), 3, np.uint8)
+    at, ah, am, _ = data.planes_from_levels(lva)
+    u = torch.empty((m, n), dtype=torch.int32, device="cuda")
+    device.gemm_2x2(T(wt), T(wh), T(wm), T(at), T(ah), T(am), k, units=u)
+    device.status()
+    assert bool((u == 36 * k).all())
+    # 1/1: rows of A all +1 or all -1 (alternating), B all +1 -> units = +-K
+    sign_rows = (np.arange(m) % 2 == 0)
+    bits = np.repeat(sign_rows[:, None], k, axis=1).astype(np.uint8)
+    a, _ = data.pack_bits(bits)
+    b, _ = data.pack_bits(np.ones((n, k), np.uint8))
+    device.gemm_1x1(T(a), T(b), k, units=u)
+    device.status()
+    want = np.where(sign_rows, k, -k)[:, None].repeat(n, axis=1)
+    assert np.array_equal(u.cpu().numpy(), want)
+    # 1/2: w all +1, activations all level 3 -> units = 2 * 3K
+    device.gemm_1x2(T(b[:m] if m <= n else a), 1.0, T(at), T(ah), T(am), k, units=u)
+    device.status()
+    assert bool((u == 6 * k).all())
