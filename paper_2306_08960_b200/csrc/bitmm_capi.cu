@@ -59,7 +59,6 @@ struct DeviceState {
   Arena io;               // host-flavour staging of inputs/outputs
   cudaStream_t stream = nullptr;  // host-flavour private stream
   uint64_t attr_mask = 0;     // spmm / apb kernels (max-smem attribute set)
-  uint64_t tc_attr_mask = 0;  // tc_gemm instantiations
   unsigned ws_turn = 0;           // ping-pong half of the expanded-operand workspace
 };
 
@@ -292,37 +291,48 @@ int run_unpack_pair(const OperandSrc& a, const OperandSrc& b, int64_t wpr, int64
   return launch_check("unpack_pair_i8");
 }
 
-template <Kind KIND, Epi EPI, bool PAIR, int BN = TC_BN>
+template <Kind KIND, Epi EPI, bool PAIR, int BN = TC_BN, int MC = 1>
 int run_tc_gemm(DeviceState& st, const CUtensorMap& ta, const CUtensorMap& tb, TcParams p,
                 cudaStream_t s) {
   using S = TcShape<PAIR, BN>;
-  auto kern = tc_gemm_kernel<KIND, EPI, PAIR, BN>;
-  constexpr int bn_idx = BN == 128 ? 0 : BN == 192 ? 1 : 2;
-  constexpr uint64_t bit =
-      1ull << (((static_cast<int>(KIND) * 3 + static_cast<int>(EPI)) * 3 + bn_idx) * 2 + (PAIR ? 1 : 0));
-  if (!(st.tc_attr_mask & bit)) {
+  auto kern = tc_gemm_kernel<KIND, EPI, PAIR, BN, MC>;
+  constexpr int kCluster = PAIR ? 2 * MC : 1;
+  // per-instantiation launch facts (the library drives one device per process)
+  static bool attrs_set = false;
+  static int max_clusters = 0;  // co-resident clusters of this instantiation
+  if (!attrs_set) {
     BITMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM));
-    st.tc_attr_mask |= bit;
+    attrs_set = true;
   }
   p.num_m_blocks = static_cast<int>((p.M + S::TILE_M - 1) / S::TILE_M);
   p.num_n_blocks = static_cast<int>((p.N + BN - 1) / BN);
   p.num_tiles = p.num_m_blocks * p.num_n_blocks;
   p.group_m = TC_GROUP_M;
-  const int units = std::min(p.num_tiles, PAIR ? st.sms / 2 : st.sms);
+  const int num_ctiles = p.num_m_blocks * ((p.num_n_blocks + MC - 1) / MC);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(PAIR ? 2 * units : units));
   cfg.blockDim = dim3(TC_THREADS);
   cfg.dynamicSmemBytes = S::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = PAIR ? 2 : 1;
+  attr[0].val.clusterDim.x = kCluster;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
+  if (max_clusters == 0) {
+    cfg.gridDim = dim3(static_cast<unsigned>(kCluster * (st.sms / kCluster)));
+    int n = 0;
+    if (kCluster > 1 && cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0)
+      max_clusters = n;
+    else
+      max_clusters = st.sms / kCluster;
+    cudaGetLastError();
+  }
+  const int units = std::min(num_ctiles, max_clusters);
+  cfg.gridDim = dim3(static_cast<unsigned>(kCluster * units));
   CUtensorMap tc{};
   void* out = (EPI == Epi::I32) ? static_cast<void*>(p.out_i32) : static_cast<void*>(p.out_f32);
   p.tma_store = make_output_map(&tc, out, EPI == Epi::I32 ? CU_TENSOR_MAP_DATA_TYPE_INT32
@@ -364,8 +374,12 @@ int launch_int_gemm(DeviceState& st, const uint8_t* A8, const uint8_t* B8, int64
                     int64_t kpad, TcParams p, cudaStream_t s, bool fp4 = false) {
   constexpr bool kPair = true;
   if (fp4) {
+    // MC = 2 (4-CTA clusters multicasting A) cuts L2 sectors 18% but runs on 132 SMs and is
+    // slower (profiles/ncu_mc2_r01.md); the single-pair form is the default.
+    constexpr int mc = 1;
     CUtensorMap ta, tb;
-    BITMM_TRY(make_operand_map(&ta, A8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad / 2, m, TcShape<kPair, kF4BN>::A_ROWS));
+    BITMM_TRY(make_operand_map(&ta, A8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad / 2, m,
+                               TcShape<kPair, kF4BN>::A_ROWS / (mc == 2 ? 2 : 1)));
     BITMM_TRY(make_operand_map(&tb, B8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad / 2, n, TcShape<kPair, kF4BN>::B_ROWS));
     p.num_kb = static_cast<int>(kpad / 2 / TC_BK_BYTES);
     p.a_kb_period = p.num_kb;

@@ -86,8 +86,10 @@ struct TcParams {
   int group_m;       // tile raster: groups of group_m M-blocks walked column by column
 };
 
-__device__ __forceinline__ void tc_tile_coords(int t, const TcParams& p, int& mb, int& nb) {
-  const int group_tiles = p.group_m * p.num_n_blocks;
+// Tile t of a grid with num_n column groups -> (mb, n-group), raster in groups of group_m
+// M-blocks so the CTAs working at the same time share operand blocks in L2.
+__device__ __forceinline__ void tc_tile_coords(int t, const TcParams& p, int num_n, int& mb, int& nb) {
+  const int group_tiles = p.group_m * num_n;
   const int g = t / group_tiles;
   const int first_m = g * p.group_m;
   const int gm = min(p.group_m, p.num_m_blocks - first_m);
@@ -194,7 +196,12 @@ __device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, const CUtens
   }
 }
 
-template <Kind KIND, Epi EPI, bool PAIR, int BN>
+// MC = CTA pairs per cluster. MC = 2: a cluster of four CTAs runs two pairs on horizontally
+// adjacent tiles (same 256 A rows, N blocks 2j and 2j+1). Each pair loads one half of the
+// shared A rows and multicasts it to the same-rank CTA of the other pair, halving A's L2
+// traffic (the GEMM is L2-throughput bound: profiles/ncu_r01f4.md); every stage release is
+// committed to all four CTAs, so a producer refills a stage only when both pairs are done.
+template <Kind KIND, Epi EPI, bool PAIR, int BN, int MC = 1>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const TcParams p) {
@@ -213,9 +220,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  static_assert(MC == 1 || PAIR, "multicast clusters are built from CTA pairs");
+  const uint32_t crank = PAIR ? cluster_ctarank() : 0u;
+  const uint32_t rank = crank & 1u;                 // rank within the CTA pair
+  const int pair = static_cast<int>(crank >> 1);    // pair within the cluster (MC = 2)
   const int unit = PAIR ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
   const int num_units = PAIR ? static_cast<int>(num_clusters_x()) : static_cast<int>(gridDim.x);
+  // cluster tiles: MC horizontally adjacent pair tiles
+  const int nb_groups = (p.num_n_blocks + MC - 1) / MC;
+  const int num_ctiles = p.num_m_blocks * nb_groups;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -223,7 +236,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (p.tma_store) tma_prefetch_desc(&tmC);
     for (int s = 0; s < S::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC);  // one release per pair of the cluster
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -272,9 +285,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = unit; tile < p.num_tiles; tile += num_units) {
+      for (int tile = unit; tile < num_ctiles; tile += num_units) {
         int mb, nb;
-        tc_tile_coords(tile, p, mb, nb);
+        tc_tile_coords(tile, p, nb_groups, mb, nb);
+        nb = nb * MC + pair;
         const int a_row = mb * S::TILE_M + static_cast<int>(rank) * S::A_ROWS;
         const int b_row = nb * BN + static_cast<int>(rank) * S::B_ROWS;
         for (int kb = 0; kb < p.num_kb; ++kb) {
@@ -282,7 +296,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const int ka = kb % p.a_kb_period;
           if constexpr (PAIR) {
             if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (S::A_STAGE + S::B_STAGE));
-            tma_load_2d_pair(sA + stage * S::A_STAGE, &tmA, &full[stage], ka * BK_ELEMS, a_row);
+            if constexpr (MC == 2) {
+              // this pair's half of the A rows, to this CTA and its twin in the other pair
+              constexpr int HALF = S::A_ROWS / 2;
+              tma_load_2d_pair_mc(sA + stage * S::A_STAGE + pair * HALF * TC_BK_BYTES, &tmA,
+                                  &full[stage], ka * BK_ELEMS, a_row + pair * HALF,
+                                  static_cast<uint16_t>(0x5u << rank));
+            } else {
+              tma_load_2d_pair(sA + stage * S::A_STAGE, &tmA, &full[stage], ka * BK_ELEMS, a_row);
+            }
             tma_load_2d_pair(sB + stage * S::B_STAGE, &tmB, &full[stage], kb * BK_ELEMS, b_row);
           } else {
             mbar_arrive_expect_tx(&full[stage], S::A_STAGE + S::B_STAGE);
@@ -298,14 +320,48 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA only) =====================
-    if (lane == 0 && rank == 0) {
-      constexpr uint32_t idesc = (KIND == Kind::I8)   ? make_idesc(2u, 1u, 1u, S::TILE_M, BN)
-                                 : (KIND == Kind::F4) ? make_idesc_mxf4(S::TILE_M, BN)
-                                                      : make_idesc(1u, 1u, 1u, S::TILE_M, BN);
+    constexpr uint32_t idesc = (KIND == Kind::I8)   ? make_idesc(2u, 1u, 1u, S::TILE_M, BN)
+                               : (KIND == Kind::F4) ? make_idesc_mxf4(S::TILE_M, BN)
+                                                    : make_idesc(1u, 1u, 1u, S::TILE_M, BN);
+    if constexpr (PAIR) {
+      // whole warp, warp-uniform state; one elected lane issues each tcgen05 instruction.
+      // Descriptors: the stage-0 descriptor plus (byte offset >> 4) in the address field.
+      if (rank == 0) {
+        constexpr int KID = (KIND == Kind::I8) ? 0 : (KIND == Kind::F4) ? 2 : 1;
+        const uint64_t a_desc0 = sw128_kmajor_desc(smem_u32(sA));
+        const uint64_t b_desc0 = sw128_kmajor_desc(smem_u32(sB));
+        const uint32_t sfa = tmem_base + kSfCol, sfb = tmem_base + kSfCol + 32;
+        int stage = 0;
+        uint32_t phase = 0;
+        int it = 0;
+        for (int tile = unit; tile < num_ctiles; tile += num_units, ++it) {
+          const int acc = it & 1;
+          const uint32_t aphase = (it >> 1) & 1;
+          mbar_wait(&tempty[acc], aphase ^ 1u);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + acc * BN;
+          for (int kb = 0; kb < p.num_kb; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint64_t ad = a_desc0 + static_cast<uint64_t>((stage * S::A_STAGE) >> 4);
+            const uint64_t bd = b_desc0 + static_cast<uint64_t>((stage * S::B_STAGE) >> 4);
+#pragma unroll
+            for (int k = 0; k < TC_BK_BYTES / 32; ++k)
+              mma_pair_elect<KID>(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0, sfa, sfb);
+            mma_commit_pair_elect(&empty[stage], MC == 2 ? 0xF : 0x3);
+            if (++stage == S::STAGES) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+          mma_commit_pair_elect(&tfull[acc], static_cast<uint16_t>(0x3u << (2 * pair)));
+        }
+      }
+    } else if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = unit; tile < p.num_tiles; tile += num_units, ++it) {
+      for (int tile = unit; tile < num_ctiles; tile += num_units, ++it) {
         const int acc = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], aphase ^ 1u);
@@ -320,34 +376,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           for (int k = 0; k < TC_BK_BYTES / 32; ++k) {
             const uint64_t ad = sw128_kmajor_desc(a_addr + k * 32);
             const uint64_t bd = sw128_kmajor_desc(b_addr + k * 32);
-            if constexpr (PAIR) {
-              if constexpr (KIND == Kind::F4)
-                mma_mxf4_pair(d_tmem, ad, bd, idesc, (kb | k) != 0, tmem_base + kSfCol,
-                              tmem_base + kSfCol + 32);
-              else if constexpr (KIND == Kind::I8)
-                mma_i8_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
-              else
-                mma_f16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
-            } else {
-              if constexpr (KIND == Kind::I8)
-                mma_i8(d_tmem, ad, bd, idesc, (kb | k) != 0);
-              else
-                mma_f16(d_tmem, ad, bd, idesc, (kb | k) != 0);
-            }
+            if constexpr (KIND == Kind::I8)
+              mma_i8(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            else
+              mma_f16(d_tmem, ad, bd, idesc, (kb | k) != 0);
           }
-          if constexpr (PAIR)
-            mma_commit_pair(&empty[stage], 0x3);
-          else
-            mma_commit(&empty[stage]);
+          mma_commit(&empty[stage]);
           if (++stage == S::STAGES) {
             stage = 0;
             phase ^= 1u;
           }
         }
-        if constexpr (PAIR)
-          mma_commit_pair(&tfull[acc], 0x3);
-        else
-          mma_commit(&tfull[acc]);
+        mma_commit(&tfull[acc]);
       }
     }
   } else {
@@ -356,9 +396,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     float* stg = sEpi + (warp - 2) * (S::EPI_WARP_BYTES / 4);
     uint32_t buf = 0;
     int it = 0;
-    for (int tile = unit; tile < p.num_tiles; tile += num_units, ++it) {
+    for (int tile = unit; tile < num_ctiles; tile += num_units, ++it) {
       int mb, nb;
-      tc_tile_coords(tile, p, mb, nb);
+      tc_tile_coords(tile, p, nb_groups, mb, nb);
+      nb = nb * MC + pair;
       const int acc = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], aphase);

@@ -59,23 +59,6 @@ struct UnpackPair {
   int fp4;  // 1: packed e2m1 nibbles, rows of kpad/2 bytes (Kind::F4 operands)
 };
 
-// 8 bits -> 8 nibbles (bit i at bit 4i).
-__device__ __forceinline__ uint32_t spread8_nib(uint32_t x) {
-  x = (x | (x << 12)) & 0x000F000Fu;
-  x = (x | (x << 6)) & 0x03030303u;
-  return (x | (x << 3)) & 0x11111111u;
-}
-
-// e2m1 nibbles for 8 elements: signs (bit 1 -> +1.0 = 0x2, bit 0 -> -1.0 = 0xA) or levels
-// (hi = p >> 1, lo = p & 1: 0 -> 0x0, 1 -> 0x2 (1.0), 2 -> 0x4 (2.0), 3 -> 0x5 (3.0)).
-// `valid` masks the elements inside K; padding nibbles are 0 (+0.0).
-__device__ __forceinline__ uint32_t nib_signs8(uint32_t bits, uint32_t valid) {
-  return (spread8_nib(valid) << 1) | (spread8_nib(valid & ~bits) << 3);
-}
-__device__ __forceinline__ uint32_t nib_levels8(uint32_t hi, uint32_t lo) {
-  return (spread8_nib(hi) << 2) | spread8_nib(hi & lo) | (spread8_nib(~hi & lo & 0xFFu) << 1);
-}
-
 // One warp expands one 4096-element slice of one operand row (128 input words, 4 KB of
 // int8 output), split into a load step (all 128 words in flight: lane t holds words
 // j*32 + t) and an expand/store step, so a warp looping over slices can prefetch the next
@@ -123,6 +106,37 @@ __device__ __forceinline__ int expand_slice_warp(const UnpackOperand& o, long lo
       s.w1[j] = (tw | ~(hw | mw)) & valid;
     }
   }
+  if (fp4) {
+    // e2m1 operands with a K-permutation inside each 32-element group: source bit j of a
+    // 32-bit word goes to output word j % 4, nibble j / 4, so output word q is
+    // (bits >> q) & 0x11111111 shifted into place. Both GEMM operands use the same
+    // permutation, so every dot product is unchanged. Lane t writes the 16 output bytes of
+    // its own word: each warp store covers 512 contiguous bytes.
+    uint8_t* out_row = o.out + r * (kpad / 2);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int g = word0 + j * 32 + lane;
+      if (g * 32 >= kpad) continue;
+      uint32_t ow[4];
+      if (o.levels == 0) {
+        const uint32_t valid = valid_mask32(g * 32, K);
+        const uint32_t neg = valid & ~s.w0[j];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)  // +1 -> 0x2, -1 -> 0xA, padding -> 0
+          ow[q] = (((valid >> q) & 0x11111111u) << 1) | (((neg >> q) & 0x11111111u) << 3);
+      } else {
+        const uint32_t hi = s.w0[j], lo = s.w1[j];  // already masked to K
+        const uint32_t b0 = hi & lo, b1 = ~hi & lo;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)  // p -> 0x0 / 0x2 / 0x4 / 0x5
+          ow[q] = (((hi >> q) & 0x11111111u) << 2) | ((b0 >> q) & 0x11111111u) |
+                  (((b1 >> q) & 0x11111111u) << 1);
+      }
+      *reinterpret_cast<uint4*>(out_row + static_cast<long long>(g) * 16) =
+          make_uint4(ow[0], ow[1], ow[2], ow[3]);
+    }
+    return __reduce_or_sync(0xFFFFFFFFu, bad);
+  }
   uint8_t* out_row = o.out + r * kpad;
   const bool full_slice = (word0 + 128) * 32 <= K;
 #pragma unroll
@@ -134,22 +148,6 @@ __device__ __forceinline__ int expand_slice_warp(const UnpackOperand& o, long lo
     const uint32_t a = __shfl_sync(0xFFFFFFFFu, s.w0[v >> 1], src_lane);
     const uint32_t b = __shfl_sync(0xFFFFFFFFu, s.w1[v >> 1], src_lane);
     if (elem >= kpad) continue;
-    if (fp4) {
-      const uint32_t x = (a >> shift) & 0xFFFFu;
-      uint32_t n0, n1;
-      if (o.levels == 0) {
-        const int g = word0 + (chunk >> 1);
-        const uint32_t valid = (valid_mask32(g * 32, K) >> shift) & 0xFFFFu;
-        n0 = nib_signs8(x & 0xFFu, valid & 0xFFu);
-        n1 = nib_signs8(x >> 8, valid >> 8);
-      } else {
-        const uint32_t y = (b >> shift) & 0xFFFFu;
-        n0 = nib_levels8(x & 0xFFu, y & 0xFFu);
-        n1 = nib_levels8(x >> 8, y >> 8);
-      }
-      *reinterpret_cast<uint2*>(o.out + r * (kpad / 2) + elem / 2) = make_uint2(n0, n1);
-      continue;
-    }
     uint32_t ow[4];
     if (o.levels == 0) {
       const uint32_t bits = (a >> shift) & 0xFFFFu;
