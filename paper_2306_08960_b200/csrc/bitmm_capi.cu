@@ -383,6 +383,8 @@ int launch_int_gemm(DeviceState& st, const uint8_t* A8, const uint8_t* B8, int64
     BITMM_TRY(make_operand_map(&tb, B8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad / 2, n, TcShape<kPair, kF4BN>::B_ROWS));
     p.num_kb = static_cast<int>(kpad / 2 / TC_BK_BYTES);
     p.a_kb_period = p.num_kb;
+    p.small_acc = (9 * kpad < (1 << 22)) ? 1 : 0;  // |acc| <= 9K: magic-add float -> int is exact
+    p.shift_mul = static_cast<float>(1 << p.shift);
     return run_tc_gemm<Kind::F4, EPI, kPair, kF4BN>(st, ta, tb, p, s);
   }
   CUtensorMap ta, tb;

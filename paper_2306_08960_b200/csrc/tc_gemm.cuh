@@ -82,6 +82,8 @@ struct TcParams {
   // F32R: per-row scale factors in the reference's multiplication order
   float row_pre, act_scale, act_gamma;
   int tma_store;     // 1: output through the tensor map (ldc*4 % 16 == 0, 16B-aligned base)
+  int small_acc;     // F4: every |accumulator| < 2^22 (9K < 2^22), float -> int by magic add
+  float shift_mul;   // F4: 2^shift
   int num_m_blocks, num_n_blocks, num_tiles;
   int group_m;       // tile raster: groups of group_m M-blocks walked column by column
 };
@@ -120,30 +122,41 @@ __device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, const CUtens
       row_mul = __fmul_rn(__fmul_rn(__fmul_rn(p.row_pre, p.row_scale[my_row]), p.act_scale),
                           p.act_gamma);
   }
-#pragma unroll 1
-  for (int c = 0; c < BN / 32; ++c) {
+  const uint32_t lane_base = tmem_acc + (static_cast<uint32_t>(quad * 32) << 16);
+  const int nch = min(BN / 32, (p.N - col_base + 31) / 32);
+  // One 32-column chunk: per-thread (row) transform, staged into smem, then stored.
+  auto drain = [&](uint32_t (&v)[32], int c) {
     const int col0 = col_base + c * 32;
-    if (col0 >= p.N) break;
-    uint32_t v[32];
-    tmem_ld_32x32b_x32(tmem_acc + (static_cast<uint32_t>(quad * 32) << 16) + c * 32, v);
-    tmem_ld_wait();
-    if constexpr (F32ACC) {
-#pragma unroll
-      for (int e = 0; e < 32; ++e) v[e] = static_cast<uint32_t>(__float2int_rn(__uint_as_float(v[e])));
-    }
     float* sb = stg + buf * (TC_EPI_BUF / 4);
     if (p.tma_store) {
       if (lane == 0) bulk_wait_group_read<EPI_BUFS - 1>();
       __syncwarp();
     }
-    // ---- per-thread (row) transform into smem ----
 #pragma unroll
     for (int j = 0; j < 32; j += 4) {
       float4 o;
       float* of = reinterpret_cast<float*>(&o);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        if constexpr (EPI == Epi::I32) {
+        if constexpr (F32ACC) {
+          // fp32 accumulator holding an exact integer acc; units = acc << shift
+          const float acc = __uint_as_float(v[j + e]);
+          if constexpr (EPI == Epi::I32) {
+            const int iacc = p.small_acc ? (__float_as_int(__fadd_rn(acc, 12582912.0f)) - 0x4B400000)
+                                         : __float2int_rn(acc);
+            of[e] = __int_as_float(iacc << p.shift);
+          } else {
+            const float units = __fmul_rn(acc, p.shift_mul);  // exact: x 1, 2 or 4
+            float s = row_mul;
+            if constexpr (EPI == Epi::F32) {
+              if (p.col_scale != nullptr) {
+                const int cc = col0 + j + e;
+                s = __fmul_rn(s, cc < p.N ? p.col_scale[cc] : 0.0f);
+              }
+            }
+            of[e] = __fmul_rn(s, units);
+          }
+        } else if constexpr (EPI == Epi::I32) {
           of[e] = __int_as_float(static_cast<int>(v[j + e]) << p.shift);
         } else if constexpr (EPI == Epi::F32) {
           const float units = static_cast<float>(static_cast<int>(v[j + e]) << p.shift);
@@ -168,7 +181,7 @@ __device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, const CUtens
         bulk_commit_group();
       }
       if constexpr (EPI_BUFS == 2) buf ^= 1u;
-      continue;
+      return;
     }
     __syncwarp();
     // ---- fallback write-out: 4 rows x 128 B per warp instruction ----
@@ -193,6 +206,20 @@ __device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, const CUtens
       }
     }
     __syncwarp();
+  };
+  // Software pipeline over chunks: the TMEM load of chunk c+1 is in flight while chunk c is
+  // transformed and stored (tcgen05.wait::ld waits for every earlier load of the thread).
+  uint32_t va[32], vb[32];
+  if (nch > 0) tmem_ld_32x32b_x32(lane_base, va);
+#pragma unroll 1
+  for (int c = 0; c < nch; c += 2) {
+    tmem_ld_wait();
+    if (c + 1 < nch) tmem_ld_32x32b_x32(lane_base + (c + 1) * 32, vb);
+    drain(va, c);
+    if (c + 1 >= nch) break;
+    tmem_ld_wait();
+    if (c + 2 < nch) tmem_ld_32x32b_x32(lane_base + (c + 2) * 32, va);
+    drain(vb, c + 1);
   }
 }
 
