@@ -61,6 +61,8 @@ def parse_args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sequential", action="store_true",
+                    help="N=1: time one bitmm_gemm_*_dev call per routine instead of the group")
     return ap.parse_args()
 
 
@@ -367,12 +369,34 @@ def main():
                           out=gathered.get(name))
         return launches[0]
 
-    def step(events, per_routine=False):
-        """One pass of the three GEMMs. Events only bracket the step unless per_routine:
+    def run_group():
+        """The three GEMMs as one group: one operand-expansion launch plus one persistent
+        tensor-core launch over all their tiles (bitmm_gemm_batch_dev)."""
+        items = []
+        for name, m, n, k in ROUTINES:
+            x = d[name]
+            if name == "1x1":
+                items.append(dict(routine="1x1", a=x["a"], b=x["b"], k=k, units=x["units"]))
+            elif name == "1x2":
+                items.append(dict(routine="1x2", w=x["w"], t=x["t"], h=x["h"], m=x["m"], k=k,
+                                  row_scale=x["gamma"], col_scale=x["beta"], out=x["out"]))
+            else:
+                items.append(dict(routine="2x2", wt=x["wt"], wh=x["wh"], wm=x["wm"], t=x["at"],
+                                  h=x["ah"], m=x["am"], k=k, units=x["units"]))
+        device.gemm_batch(items)
+        return device.launch_count()
+
+    def step(events, per_routine=False, sequential=False):
+        """One pass of the three GEMMs. N=1: one grouped launch pair unless `sequential` (one
+        bitmm_gemm_*_dev call per routine). Events only bracket the step unless per_routine:
         an event between two routines would serialise the PDL overlap of the next call's
         operand expansion with the current GEMM."""
         launches = 0
         events[0].record(stream)
+        if world == 1 and not per_routine and not sequential and not args.sequential:
+            launches += run_group()
+            events[-1].record(stream)
+            return launches
         for i, (name, m, n, k) in enumerate(ROUTINES):
             launches += run_routine(name, m, n, k) if world == 1 else sharded(name, m, n, k)
             if per_routine:
@@ -419,6 +443,16 @@ def main():
     total_ms = 0.0
     for evs in step_ev:
         total_ms += evs[0].elapsed_time(evs[-1])
+    # the same K steps issued as three separate per-routine calls (reported beside `value`)
+    seq_ms = None
+    if world == 1 and not args.sequential:
+        seq_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(ROUTINES) + 1)]
+                  for _ in range(args.steps)]
+        for s in range(args.steps):
+            l2_flush()
+            step(seq_ev[s], sequential=True)
+        torch.cuda.synchronize()
+        seq_ms = sum(e[0].elapsed_time(e[-1]) for e in seq_ev) / args.steps
     # per-routine breakdown: a separate pass with events between routines (serialised)
     per_routine_ms = {name: 0.0 for name, *_ in ROUTINES}
     pr_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(ROUTINES) + 1)]
@@ -513,7 +547,14 @@ def main():
                      "popc_roofline_T_updates_per_s": 148 * 16 * 32 * 1.965e9 / 1e12},
         "kernels": kernels,
         "clocks": clocks,
+        "step_path": ("bitmm_gemm_batch_dev: one expansion launch + one persistent tensor-core "
+                      "launch over the three GEMMs" if world == 1 and not args.sequential else
+                      "one bitmm_gemm_*_dev call per routine"),
     }
+    if seq_ms is not None:
+        line["sequential_calls"] = {"ms_per_step": seq_ms,
+                                    "value": upd_per_step / (seq_ms * 1e-3) / 1e12,
+                                    "note": "same steps as three bitmm_gemm_*_dev calls"}
 
     if world == 1:
         line["apb"] = apb_pass(args, torch, lib, l2_flush, peaks)

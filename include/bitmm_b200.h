@@ -155,6 +155,36 @@ int bitmm_layer_forward_host(int64_t rows, int64_t cols, float alpha, const floa
                              const uint64_t* col_idx, const float* vals, int64_t nnz,
                              const float* b, int64_t n, int64_t ldb, float* c, int64_t ldc);
 
+/* ---- GEMM group: several routines in one launch pair ----
+ * Runs up to 4 GEMM problems (an item that asks for both c_units and c counts as two) as ONE
+ * operand-expansion launch plus ONE persistent tensor-core launch over the concatenated tiles,
+ * so a batch of independent GEMMs pays one ramp-up and one tail instead of one per GEMM. Each
+ * item has exactly the semantics (scales, errors, outputs) of the matching bitmm_gemm_*_dev
+ * call; results are bit-identical to issuing those calls one by one. Stream-ordered. */
+enum { BITMM_ROUTINE_1X1 = 0, BITMM_ROUTINE_1X2 = 1, BITMM_ROUTINE_2X2 = 2 };
+typedef struct bitmm_gemm_item {
+  int routine;                /* BITMM_ROUTINE_* */
+  const uint64_t* a0;         /* 1x1: a; 1x2: w (binary weights); 2x2: weight plane t */
+  const uint64_t* a1;         /* 2x2: weight plane h */
+  const uint64_t* a2;         /* 2x2: weight plane m */
+  const uint64_t* b0;         /* 1x1: b_packed; 1x2 / 2x2: activation plane t */
+  const uint64_t* b1;         /* 1x2 / 2x2: activation plane h */
+  const uint64_t* b2;         /* 1x2 / 2x2: activation plane m */
+  int64_t m, n, k, wpr;
+  float a_scale;              /* 1x1: gamma_a; 1x2: gamma; 2x2: weight plane scale */
+  int has_a_gamma;            /* 2x2: weight plane gamma present */
+  float a_gamma;
+  float b_scale;              /* 1x1: gamma_b; 1x2 / 2x2: activation plane scale */
+  int has_b_gamma;            /* 1x2 / 2x2: activation plane gamma present */
+  float b_gamma;
+  const float* row_scale;     /* optional [m] (1x2, 2x2), as in the _dev calls */
+  const float* col_scale;     /* optional [n] (1x2, 2x2) */
+  int32_t* c_units;           /* optional [m][ldc] */
+  float* c;                   /* optional [m][ldc] */
+  int64_t ldc;
+} bitmm_gemm_item;
+int bitmm_gemm_batch_dev(const bitmm_gemm_item* items, int count, void* stream);
+
 /* ---- APB layer with 2-bit activations (paper-faithful inference) ----
  * No single reference entry point: it is the composition of reference calls
  *   C = gemm_1x2(bin, alpha_r, planes)            (kernels.hpp:55, kernels.cpp:185-221)

@@ -26,6 +26,24 @@ _f = C.c_float
 _i = C.c_int
 
 # name -> (restype, argtypes); mirrors include/bitmm_b200.h
+ROUTINE_1X1, ROUTINE_1X2, ROUTINE_2X2 = 0, 1, 2
+
+
+class GemmItem(C.Structure):
+    """ctypes mirror of `bitmm_gemm_item` (include/bitmm_b200.h); field order and types must
+    match the C struct (tests/test_capi_cpu.py compares offsets with gcc's)."""
+    _fields_ = [
+        ("routine", C.c_int),
+        ("a0", _p), ("a1", _p), ("a2", _p),
+        ("b0", _p), ("b1", _p), ("b2", _p),
+        ("m", _i64), ("n", _i64), ("k", _i64), ("wpr", _i64),
+        ("a_scale", _f), ("has_a_gamma", C.c_int), ("a_gamma", _f),
+        ("b_scale", _f), ("has_b_gamma", C.c_int), ("b_gamma", _f),
+        ("row_scale", _p), ("col_scale", _p),
+        ("c_units", _p), ("c", _p), ("ldc", _i64),
+    ]
+
+
 SIGNATURES = {
     "bitmm_abi_version": (_i, []),
     "bitmm_last_error": (C.c_char_p, []),
@@ -82,6 +100,7 @@ SIGNATURES = {
         _i,
         [_i64, _i64, _f, _p, _p, _i64, _p, _p, _p, _i64, _p, _p, _p, _i64, _f, _i, _f, _p, _i64],
     ),
+    "bitmm_gemm_batch_dev": (_i, [_p, _i, _p]),
     "bitmm_pack_signs_dev": (_i, [_p, _i64, _i64, _i64, _p, _i64, _p]),
     "bitmm_pack_signs_host": (_i, [_p, _i64, _i64, _i64, _p, _i64]),
     "bitmm_quantize_thm_dev": (_i, [_p, _i64, _i64, _i64, _f, _p, _p, _p, _i64, _p]),

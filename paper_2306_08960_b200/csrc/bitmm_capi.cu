@@ -251,7 +251,8 @@ struct OperandSrc {
   bool levels;
 };
 
-UnpackOperand make_unpack_operand(const OperandSrc& src, int64_t wpr, int64_t kpad, uint8_t* out) {
+UnpackOperand make_unpack_operand(const OperandSrc& src, int64_t wpr, int64_t k, int64_t kpad,
+                                  uint8_t* out) {
   UnpackOperand o{};
   o.w0 = reinterpret_cast<const uint32_t*>(src.w0);
   o.w1 = reinterpret_cast<const uint32_t*>(src.w1);
@@ -261,24 +262,18 @@ UnpackOperand make_unpack_operand(const OperandSrc& src, int64_t wpr, int64_t kp
   o.wpr32 = static_cast<int>(wpr * 2);
   o.groups_per_row = (std::max<long long>(kpad / 32, o.wpr32) + 127) / 128;  // 128-word slices
   o.levels = src.levels ? 1 : 0;
+  o.K = static_cast<int>(k);
+  o.kpad = static_cast<int>(kpad);
   return o;
 }
 
-// Expands both GEMM operands (bits or ternary planes) to int8 rows in one launch.
-int run_unpack_pair(const OperandSrc& a, const OperandSrc& b, int64_t wpr, int64_t k, int64_t kpad,
-                    uint8_t* A8, uint8_t* B8, int* flag, cudaStream_t s, bool fp4 = false) {
-  UnpackPair P{};
-  P.fp4 = fp4 ? 1 : 0;
-  P.op[0] = make_unpack_operand(a, wpr, kpad, A8);
-  P.op[1] = make_unpack_operand(b, wpr, kpad, B8);
-  P.K = static_cast<int>(k);
-  P.kpad = static_cast<int>(kpad);
-  P.err = flag;
-  const long long work = std::max(P.op[0].rows * P.op[0].groups_per_row,
-                                  P.op[1].rows * P.op[1].groups_per_row);
+// Expands every operand of a set (bits or ternary planes) in one launch.
+int run_unpack_set(UnpackSet& P, cudaStream_t s) {
+  long long work = 0;
+  for (int i = 0; i < P.count; ++i) work = std::max(work, P.op[i].rows * P.op[i].groups_per_row);
   if (work == 0) return BITMM_OK;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(blocks_for(work * 32, 256), 2);  // one warp per slice
+  cfg.gridDim = dim3(blocks_for(work * 32, 256), static_cast<unsigned>(P.count));  // warp per slice
   cfg.blockDim = dim3(256);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -286,76 +281,21 @@ int run_unpack_pair(const OperandSrc& a, const OperandSrc& b, int64_t wpr, int64
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  ProfScope ps("unpack_pair_i8", s);
-  BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, unpack_pair_i8, P));
-  return launch_check("unpack_pair_i8");
+  ProfScope ps("unpack_operands", s);
+  BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, unpack_operands, P));
+  return launch_check("unpack_operands");
 }
 
-template <Kind KIND, Epi EPI, bool PAIR, int BN = TC_BN, int MC = 1>
-int run_tc_gemm(DeviceState& st, const CUtensorMap& ta, const CUtensorMap& tb, TcParams p,
-                cudaStream_t s) {
-  using S = TcShape<PAIR, BN>;
-  auto kern = tc_gemm_kernel<KIND, EPI, PAIR, BN, MC>;
-  constexpr int kCluster = PAIR ? 2 * MC : 1;
-  // per-instantiation launch facts (the library drives one device per process)
-  static bool attrs_set = false;
-  static int max_clusters = 0;  // co-resident clusters of this instantiation
-  if (!attrs_set) {
-    BITMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM));
-    attrs_set = true;
-  }
-  p.num_m_blocks = static_cast<int>((p.M + S::TILE_M - 1) / S::TILE_M);
-  p.num_n_blocks = static_cast<int>((p.N + BN - 1) / BN);
-  p.num_tiles = p.num_m_blocks * p.num_n_blocks;
-  p.group_m = TC_GROUP_M;
-  const int num_ctiles = p.num_m_blocks * ((p.num_n_blocks + MC - 1) / MC);
-  cudaLaunchConfig_t cfg = {};
-  cfg.blockDim = dim3(TC_THREADS);
-  cfg.dynamicSmemBytes = S::SMEM;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kCluster;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  if (max_clusters == 0) {
-    cfg.gridDim = dim3(static_cast<unsigned>(kCluster * (st.sms / kCluster)));
-    int n = 0;
-    if (kCluster > 1 && cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0)
-      max_clusters = n;
-    else
-      max_clusters = st.sms / kCluster;
-    cudaGetLastError();
-  }
-  const int units = std::min(num_ctiles, max_clusters);
-  cfg.gridDim = dim3(static_cast<unsigned>(kCluster * units));
-  CUtensorMap tc{};
-  void* out = (EPI == Epi::I32) ? static_cast<void*>(p.out_i32) : static_cast<void*>(p.out_f32);
-  p.tma_store = make_output_map(&tc, out, EPI == Epi::I32 ? CU_TENSOR_MAP_DATA_TYPE_INT32
-                                                          : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                                p.N, p.M, p.ldc) ? 1 : 0;
-  ProfScope ps(KIND == Kind::I8 ? "tc_gemm_i8" : KIND == Kind::F4 ? "tc_gemm_f4" : "tc_gemm_bf16", s);
-  BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, p));
-  return launch_check("tc_gemm_kernel");
-}
-
-// Tile width: a wave of the persistent grid takes time proportional to BN, so pick the BN
-// with the smaller (waves x BN); 128-wide tiles pay ~3% for twice the A traffic per MAC.
-// 4096^2 outputs: 256 tiles of 256 = 3.46 waves over 74 pairs (4 x 256) vs 512 tiles of 128
-// = 6.92 waves (7 x 128) -> 128. 4096 x 8192 and 32768^2 stay at 256.
-int pick_bn(const DeviceState& st, int64_t m, int64_t n) {
-  const int64_t units = st.sms / 2;
-  const int64_t mt = (m + 255) / 256;
-  const int64_t w256 = (mt * ((n + 255) / 256) + units - 1) / units;
-  const int64_t w128 = (mt * ((n + 127) / 128) + units - 1) / units;
-  // Measured (profiles/ncu_bn128_r01.md): 128-wide tiles halve the pipeline's lookahead in
-  // time (8 stages x 0.19 us) and the tensor pipe starves (42.7% active, 1x1 4096^3 62 -> 89
-  // us), so 256 wins even at 3.46 waves. Kept selectable for shapes where w128 is far ahead.
-  return (w128 * 128 * 2 < w256 * 256) ? 128 : 256;
+// Expands both GEMM operands in one launch.
+int run_unpack_pair(const OperandSrc& a, const OperandSrc& b, int64_t wpr, int64_t k, int64_t kpad,
+                    uint8_t* A8, uint8_t* B8, int* flag, cudaStream_t s, bool fp4 = false) {
+  UnpackSet P{};
+  P.fp4 = fp4 ? 1 : 0;
+  P.op[0] = make_unpack_operand(a, wpr, k, kpad, A8);
+  P.op[1] = make_unpack_operand(b, wpr, k, kpad, B8);
+  P.count = 2;
+  P.err = flag;
+  return run_unpack_set(P, s);
 }
 
 // Operand kind of the bitwise GEMMs: packed e2m1 through kind::mxf4 (default; 2x the int8
@@ -366,35 +306,131 @@ bool use_fp4() {
   return on;
 }
 constexpr int kF4BN = 192;  // 2 x 192 accumulator columns + scale-factor columns <= 512
+constexpr int kI8BN = 256;  // 256-wide int8 tiles (128-wide measured worse: DESIGN.md)
+int64_t kpad_for(int64_t k, bool fp4) { return round_up(k, fp4 ? 2 * TC_BK_BYTES : TC_BK_BYTES); }
+int64_t row_bytes(int64_t kpad, bool fp4) { return fp4 ? kpad / 2 : kpad; }
 
-// Integer GEMM over expanded operands A8 [m][kpad], B8 [n][kpad] (cta_group::2 pairs); with
-// fp4 the rows are kpad/2 bytes of e2m1 nibbles.
-template <Epi EPI>
-int launch_int_gemm(DeviceState& st, const uint8_t* A8, const uint8_t* B8, int64_t m, int64_t n,
-                    int64_t kpad, TcParams p, cudaStream_t s, bool fp4 = false) {
-  constexpr bool kPair = true;
-  if (fp4) {
-    // MC = 2 (4-CTA clusters multicasting A) cuts L2 sectors 18% but runs on 132 SMs and is
-    // slower (profiles/ncu_mc2_r01.md); the single-pair form is the default.
-    constexpr int mc = 1;
-    CUtensorMap ta, tb;
-    BITMM_TRY(make_operand_map(&ta, A8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad / 2, m,
-                               TcShape<kPair, kF4BN>::A_ROWS / (mc == 2 ? 2 : 1)));
-    BITMM_TRY(make_operand_map(&tb, B8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad / 2, n, TcShape<kPair, kF4BN>::B_ROWS));
-    p.num_kb = static_cast<int>(kpad / 2 / TC_BK_BYTES);
+// One GEMM problem over expanded operands A8 [m][row_bytes], B8 [n][row_bytes]; `p` carries
+// the epilogue (shift, scales, output, ldc, epi).
+struct GemmProblem {
+  const uint8_t* A8;
+  const uint8_t* B8;
+  int64_t m, n, kpad;
+  TcParams p;
+};
+
+// Launch one persistent cta_group::2 GEMM over a group of problems (tiles concatenated).
+template <Kind KIND, Epi EPI, int BN, int NP>
+int run_tc_group(DeviceState& st, const GemmProblem* probs, int count, cudaStream_t s) {
+  using S = TcShape<true, BN>;
+  auto kern = tc_gemm_kernel<KIND, EPI, BN, NP>;
+  // per-instantiation launch facts (the library drives one device per process)
+  static bool attrs_set = false;
+  if (!attrs_set) {
+    BITMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM));
+    attrs_set = true;
+  }
+  constexpr bool fp4 = KIND == Kind::F4;
+  TcGroup<NP> g;
+  memset(&g, 0, sizeof(g));
+  int tiles = 0;
+  for (int i = 0; i < count; ++i) {
+    const GemmProblem& q = probs[i];
+    const int64_t rb = row_bytes(q.kpad, fp4);
+    BITMM_TRY(make_operand_map(&g.a[i], q.A8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, rb, q.m, S::A_ROWS));
+    BITMM_TRY(make_operand_map(&g.b[i], q.B8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, rb, q.n, S::B_ROWS));
+    TcParams p = q.p;
+    p.M = static_cast<int>(q.m);
+    p.N = static_cast<int>(q.n);
+    p.num_kb = static_cast<int>(rb / TC_BK_BYTES);
     p.a_kb_period = p.num_kb;
-    p.small_acc = (9 * kpad < (1 << 22)) ? 1 : 0;  // |acc| <= 9K: magic-add float -> int is exact
+    p.small_acc = (9 * q.kpad < (1 << 22)) ? 1 : 0;  // |acc| <= 9K: magic-add float -> int
     p.shift_mul = static_cast<float>(1 << p.shift);
-    return run_tc_gemm<Kind::F4, EPI, kPair, kF4BN>(st, ta, tb, p, s);
+    p.num_m_blocks = static_cast<int>((q.m + S::TILE_M - 1) / S::TILE_M);
+    p.num_n_blocks = static_cast<int>((q.n + BN - 1) / BN);
+    p.num_tiles = p.num_m_blocks * p.num_n_blocks;
+    p.group_m = TC_GROUP_M;
+    const bool i32 = p.epi == static_cast<int>(Epi::I32);
+    void* out = i32 ? static_cast<void*>(p.out_i32) : static_cast<void*>(p.out_f32);
+    p.tma_store = make_output_map(&g.c[i], out, i32 ? CU_TENSOR_MAP_DATA_TYPE_INT32
+                                                    : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                  p.N, p.M, p.ldc) ? 1 : 0;
+    g.prob[i] = p;
+    g.tile_begin[i] = tiles;
+    tiles += p.num_tiles;
   }
-  CUtensorMap ta, tb;
-  BITMM_TRY(make_operand_map(&ta, A8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad, m, TcShape<kPair>::A_ROWS));
-  if (pick_bn(st, m, n) == 128) {
-    BITMM_TRY(make_operand_map(&tb, B8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad, n, TcShape<kPair, 128>::B_ROWS));
-    return run_tc_gemm<Kind::I8, EPI, kPair, 128>(st, ta, tb, p, s);
+  g.count = count;
+  for (int i = count; i <= NP; ++i) g.tile_begin[i] = tiles;
+  const int units = std::min(tiles, st.sms / 2);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(2 * units));
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = S::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  ProfScope ps(KIND == Kind::I8 ? "tc_gemm_i8" : "tc_gemm_f4", s);
+  BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, g));
+  return launch_check("tc_gemm_kernel");
+}
+
+// Dispatch a group on the operand kind: one problem with a fixed epilogue, or up to
+// TC_GROUP_MAX problems with per-problem epilogues.
+int run_problems(DeviceState& st, const GemmProblem* probs, int count, bool fp4, cudaStream_t s) {
+  if (count == 1) {
+    const int e = probs[0].p.epi;
+    if (fp4) {
+      if (e == static_cast<int>(Epi::I32)) return run_tc_group<Kind::F4, Epi::I32, kF4BN, 1>(st, probs, 1, s);
+      if (e == static_cast<int>(Epi::F32)) return run_tc_group<Kind::F4, Epi::F32, kF4BN, 1>(st, probs, 1, s);
+      return run_tc_group<Kind::F4, Epi::F32R, kF4BN, 1>(st, probs, 1, s);
+    }
+    if (e == static_cast<int>(Epi::I32)) return run_tc_group<Kind::I8, Epi::I32, kI8BN, 1>(st, probs, 1, s);
+    if (e == static_cast<int>(Epi::F32)) return run_tc_group<Kind::I8, Epi::F32, kI8BN, 1>(st, probs, 1, s);
+    return run_tc_group<Kind::I8, Epi::F32R, kI8BN, 1>(st, probs, 1, s);
   }
-  BITMM_TRY(make_operand_map(&tb, B8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kpad, n, TcShape<kPair, 256>::B_ROWS));
-  return run_tc_gemm<Kind::I8, EPI, kPair, 256>(st, ta, tb, p, s);
+  for (int i = 0; i < count; ++i)
+    if (probs[i].p.epi == static_cast<int>(Epi::F32R))
+      return fail(BITMM_ERR_INVALID_ARGUMENT, "reference-order row scales are single-problem only");
+  if (count == 2) {
+    return fp4 ? run_tc_group<Kind::F4, Epi::ANY, kF4BN, 2>(st, probs, 2, s)
+               : run_tc_group<Kind::I8, Epi::ANY, kI8BN, 2>(st, probs, 2, s);
+  }
+  return fp4 ? run_tc_group<Kind::F4, Epi::ANY, kF4BN, TC_GROUP_MAX>(st, probs, count, s)
+             : run_tc_group<Kind::I8, Epi::ANY, kI8BN, TC_GROUP_MAX>(st, probs, count, s);
+}
+
+// The problems of one routine call: units and/or the scaled fp32 output over the same operands
+// (both in one launch when both are requested).
+int make_problems(const uint8_t* A8, const uint8_t* B8, int64_t m, int64_t n, int64_t kpad,
+                  int shift, float scale, const float* row_scale, const float* col_scale,
+                  int32_t* c_units, float* c, int64_t ldc, GemmProblem* out) {
+  int cnt = 0;
+  TcParams p{};
+  p.shift = shift;
+  p.scale = scale;
+  p.row_scale = row_scale;
+  p.col_scale = col_scale;
+  p.ldc = ldc;
+  if (c_units) {
+    out[cnt] = GemmProblem{A8, B8, m, n, kpad, p};
+    out[cnt].p.out_i32 = c_units;
+    out[cnt].p.epi = static_cast<int>(Epi::I32);
+    ++cnt;
+  }
+  if (c) {
+    out[cnt] = GemmProblem{A8, B8, m, n, kpad, p};
+    out[cnt].p.out_f32 = c;
+    out[cnt].p.epi = static_cast<int>(Epi::F32);
+    ++cnt;
+  }
+  return cnt;
 }
 
 // Common integer-GEMM tail: A8 [m][kpad], B8 [n][kpad] already expanded.
@@ -402,25 +438,10 @@ int run_int_gemm(DeviceState& st, const uint8_t* A8, const uint8_t* B8, int64_t 
                  int64_t kpad, int shift, float scale, const float* row_scale,
                  const float* col_scale, int32_t* c_units, float* c, int64_t ldc, cudaStream_t s,
                  bool fp4 = false) {
-  TcParams p{};
-  p.M = static_cast<int>(m);
-  p.N = static_cast<int>(n);
-  p.num_kb = static_cast<int>(kpad / TC_BK_BYTES);
-  p.a_kb_period = p.num_kb;
-  p.shift = shift;
-  p.scale = scale;
-  p.row_scale = row_scale;
-  p.col_scale = col_scale;
-  p.ldc = ldc;
-  if (c_units) {
-    p.out_i32 = c_units;
-    BITMM_TRY(launch_int_gemm<Epi::I32>(st, A8, B8, m, n, kpad, p, s, fp4));
-  }
-  if (c) {
-    p.out_f32 = c;
-    BITMM_TRY(launch_int_gemm<Epi::F32>(st, A8, B8, m, n, kpad, p, s, fp4));
-  }
-  return BITMM_OK;
+  GemmProblem probs[2];
+  const int cnt = make_problems(A8, B8, m, n, kpad, shift, scale, row_scale, col_scale, c_units, c,
+                                ldc, probs);
+  return cnt ? run_problems(st, probs, cnt, fp4, s) : BITMM_OK;
 }
 
 int check_gemm_dims(int64_t m, int64_t n, int64_t k, int64_t wpr, int64_t ldc) {
@@ -483,7 +504,7 @@ int gemm_1x1_dev_impl(DeviceState& st, const uint64_t* a, int64_t m, const uint6
                       int64_t k, int64_t wpr, float gamma_a, float gamma_b, int32_t* c_units,
                       float* c, int64_t ldc, cudaStream_t s) {
   const bool fp4 = use_fp4();
-  const int64_t kpad = round_up(k, fp4 ? 2 * TC_BK_BYTES : TC_BK_BYTES);
+  const int64_t kpad = kpad_for(k, fp4);
   BITMM_TRY(arena_reserve(st.ws, ws_bytes_int(m, n, k)));
   uint8_t *A8, *B8;
   take_int_operands(st, m, n, k, &A8, &B8);
@@ -499,7 +520,7 @@ int gemm_1x2_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, float gamma
                       const float* col_scale, int32_t* c_units, float* c, int64_t ldc,
                       cudaStream_t s) {
   const bool fp4 = use_fp4();
-  const int64_t kpad = round_up(k, fp4 ? 2 * TC_BK_BYTES : TC_BK_BYTES);
+  const int64_t kpad = kpad_for(k, fp4);
   BITMM_TRY(arena_reserve(st.ws, ws_bytes_int(m, n, k)));
   uint8_t *A8, *B8;
   take_int_operands(st, m, n, k, &A8, &B8);
@@ -517,7 +538,7 @@ int gemm_2x2_dev_impl(DeviceState& st, const uint64_t* wt, const uint64_t* wh, c
                       const float* col_scale, int32_t* c_units, float* c, int64_t ldc,
                       cudaStream_t s) {
   const bool fp4 = use_fp4();
-  const int64_t kpad = round_up(k, fp4 ? 2 * TC_BK_BYTES : TC_BK_BYTES);
+  const int64_t kpad = kpad_for(k, fp4);
   BITMM_TRY(arena_reserve(st.ws, ws_bytes_int(m, n, k)));
   uint8_t *A8, *B8;
   take_int_operands(st, m, n, k, &A8, &B8);
@@ -711,27 +732,25 @@ int apb2_dev_impl(DeviceState& st, int64_t rows, int64_t cols, int64_t wpr, floa
                   const uint64_t* col_idx, const float* vals, const uint64_t* t, const uint64_t* h,
                   const uint64_t* m, int64_t tokens, float a_scale, float a_gamma, float* c,
                   int64_t ldc, cudaStream_t s) {
-  const int64_t kpad = round_up(cols, TC_BK_BYTES);
+  const bool fp4 = use_fp4();
+  const int64_t kpad = kpad_for(cols, fp4);
   BITMM_TRY(arena_reserve(st.ws, ws_bytes_apb2(st, rows, cols, tokens)));
   float* deq = reinterpret_cast<float*>(static_cast<uint8_t*>(st.ws.ptr) + ws_bytes_int(rows, tokens, cols));
   uint8_t *A8, *B8;
   take_int_operands(st, rows, tokens, cols, &A8, &B8);
   BITMM_TRY(run_unpack_pair({bin, nullptr, nullptr, rows, false}, {t, h, m, tokens, true}, wpr, cols,
-                            kpad, A8, B8, st.status, s));
-  TcParams p{};
-  p.M = static_cast<int>(rows);
-  p.N = static_cast<int>(tokens);
-  p.num_kb = static_cast<int>(kpad / TC_BK_BYTES);
-  p.a_kb_period = p.num_kb;
-  p.shift = 1;
-  p.scale = 0.5f * alpha * a_scale * a_gamma;  // kernels.cpp:193 order
-  p.row_scale = row_alpha;
-  p.row_pre = 0.5f;
-  p.act_scale = a_scale;
-  p.act_gamma = a_gamma;
-  p.out_f32 = c;
-  p.ldc = ldc;
-  BITMM_TRY(launch_int_gemm<Epi::F32R>(st, A8, B8, rows, tokens, kpad, p, s));
+                            kpad, A8, B8, st.status, s, fp4));
+  GemmProblem q{A8, B8, rows, tokens, kpad, TcParams{}};
+  q.p.shift = 1;
+  q.p.scale = 0.5f * alpha * a_scale * a_gamma;  // kernels.cpp:193 order
+  q.p.row_scale = row_alpha;
+  q.p.row_pre = 0.5f;
+  q.p.act_scale = a_scale;
+  q.p.act_gamma = a_gamma;
+  q.p.out_f32 = c;
+  q.p.ldc = ldc;
+  q.p.epi = static_cast<int>(Epi::F32R);
+  BITMM_TRY(run_problems(st, &q, 1, fp4, s));
   SpmmLevels lv{};
   lv.t = reinterpret_cast<const unsigned long long*>(t);
   lv.h = reinterpret_cast<const unsigned long long*>(h);
@@ -1369,6 +1388,74 @@ int bitmm_layer_forward_2bit_host(int64_t rows, int64_t cols, float alpha, const
                           a_scale, has_a_gamma ? a_gamma : 1.0f, dc, ldc, s));
   BITMM_CUDA_TRY(cudaMemcpyAsync(c, dc, c_bytes, cudaMemcpyDeviceToHost, s));
   return read_status(*st, s);
+}
+
+// ---------------- GEMM group ----------------
+int bitmm_gemm_batch_dev(const bitmm_gemm_item* items, int count, void* stream) {
+  g_launches = 0;
+  if (count <= 0 || count > TC_GROUP_MAX || items == nullptr)
+    return fail(BITMM_ERR_INVALID_ARGUMENT, "batch must hold 1..4 items");
+  int nprob = 0;
+  for (int i = 0; i < count; ++i) {
+    const bitmm_gemm_item& it = items[i];
+    if (it.routine < BITMM_ROUTINE_1X1 || it.routine > BITMM_ROUTINE_2X2)
+      return fail(BITMM_ERR_INVALID_ARGUMENT, "unknown routine");
+    if (it.routine == BITMM_ROUTINE_1X2 && !(it.b_scale > 0.0f))
+      return fail(BITMM_ERR_INVALID_ENCODING, "plane scale must be positive");
+    if (it.routine == BITMM_ROUTINE_2X2 && (!(it.a_scale > 0.0f) || !(it.b_scale > 0.0f)))
+      return fail(BITMM_ERR_INVALID_ENCODING, "plane scale must be positive");
+    BITMM_TRY(check_gemm_dims(it.m, it.n, it.k, it.wpr, it.ldc));
+    const bool planes_a = it.routine == BITMM_ROUTINE_2X2, planes_b = it.routine != BITMM_ROUTINE_1X1;
+    if (!it.a0 || !it.b0 || (planes_a && (!it.a1 || !it.a2)) || (planes_b && (!it.b1 || !it.b2)) ||
+        (!it.c_units && !it.c))
+      return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+    nprob += (it.c_units ? 1 : 0) + (it.c ? 1 : 0);
+  }
+  if (nprob > TC_GROUP_MAX) return fail(BITMM_ERR_INVALID_ARGUMENT, "batch exceeds 4 GEMM outputs");
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool fp4 = use_fp4();
+  size_t bytes = 2048;
+  for (int i = 0; i < count; ++i) {
+    const int64_t rb = row_bytes(kpad_for(items[i].k, fp4), fp4);
+    bytes += align_up(items[i].m * rb, 1024) + align_up(items[i].n * rb, 1024);
+  }
+  BITMM_TRY(arena_reserve(st->ws, bytes));
+  Carve cv(st->ws.ptr);
+  UnpackSet U{};
+  U.fp4 = fp4 ? 1 : 0;
+  U.err = st->status;
+  GemmProblem probs[TC_GROUP_MAX];
+  int np = 0;
+  for (int i = 0; i < count; ++i) {
+    const bitmm_gemm_item& it = items[i];
+    const int64_t kpad = kpad_for(it.k, fp4), rb = row_bytes(kpad, fp4);
+    uint8_t* A8 = cv.take<uint8_t>(it.m * rb);
+    uint8_t* B8 = cv.take<uint8_t>(it.n * rb);
+    const bool planes_a = it.routine == BITMM_ROUTINE_2X2, planes_b = it.routine != BITMM_ROUTINE_1X1;
+    U.op[U.count++] = make_unpack_operand({it.a0, it.a1, it.a2, it.m, planes_a}, it.wpr, it.k, kpad, A8);
+    U.op[U.count++] = make_unpack_operand({it.b0, it.b1, it.b2, it.n, planes_b}, it.wpr, it.k, kpad, B8);
+    int shift;
+    float scale;
+    if (it.routine == BITMM_ROUTINE_1X1) {  // kernels.cpp:170
+      shift = 0;
+      scale = it.a_scale * it.b_scale;
+    } else if (it.routine == BITMM_ROUTINE_1X2) {  // kernels.cpp:193
+      shift = 1;
+      scale = 0.5f * it.a_scale * it.b_scale * (it.has_b_gamma ? it.b_gamma : 1.0f);
+    } else {  // kernels.cpp:232-233
+      shift = 2;
+      scale = 0.25f * it.a_scale * it.b_scale * (it.has_a_gamma ? it.a_gamma : 1.0f) *
+              (it.has_b_gamma ? it.b_gamma : 1.0f);
+    }
+    const float* rs = it.routine == BITMM_ROUTINE_1X1 ? nullptr : it.row_scale;
+    const float* cs = it.routine == BITMM_ROUTINE_1X1 ? nullptr : it.col_scale;
+    np += make_problems(A8, B8, it.m, it.n, kpad, shift, scale, rs, cs, it.c_units, it.c, it.ldc,
+                        probs + np);
+  }
+  BITMM_TRY(run_unpack_set(U, s));
+  return run_problems(*st, probs, np, fp4, s);
 }
 
 }  // extern "C"

@@ -65,6 +65,11 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 // ---------------------------------------------------------------------------
 // Blocks until the preceding grid in the stream has completed and its memory
 // operations are visible (a no-op when the launch carried no PDL dependency).
+// Named barrier among `count` threads (id 0 is __syncthreads).
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 // Lets the dependent grid start launching (its prologue overlaps our tail).
 __device__ __forceinline__ void pdl_launch_dependents() {

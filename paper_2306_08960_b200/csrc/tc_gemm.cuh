@@ -37,7 +37,7 @@ enum class Kind : int { I8 = 0, BF16 = 1, F4 = 2 };
 // I32: integer units. F32: scale * units. F32R: half_r * units with the reference's per-row
 // scale order ((row_pre * alpha_r) * act_scale) * act_gamma (kernels.cpp:193), used by the
 // 2-bit-activation APB layer (whose residual SpMM then adds onto C).
-enum class Epi : int { I32 = 0, F32 = 1, F32R = 2 };
+enum class Epi : int { I32 = 0, F32 = 1, F32R = 2, ANY = 3 };
 
 constexpr int TC_BN = 256;         // widest output tile (TMEM columns per accumulator)
 constexpr int TC_BK_BYTES = 128;   // one 128-byte swizzle row per operand row per stage
@@ -59,12 +59,14 @@ struct TcShape {
   static constexpr int EPI_BUFS = (PAIR && BN == 192) ? 1 : 2;
   static constexpr int EPI_WARP_BYTES = EPI_BUFS == 2 ? 2 * TC_EPI_BUF : 5120;
   static constexpr int EPI_BYTES = 4 * EPI_WARP_BYTES;
+  static constexpr int COLS_BYTES = BN * 4;  // the tile's column scales (F32 epilogue)
   static constexpr int STAGES =
-      PAIR ? (232448 - 1024 - EPI_BYTES - 256) / ((128 + BN / 2) * TC_BK_BYTES) : 4;
+      PAIR ? (232448 - 1024 - EPI_BYTES - COLS_BYTES - 256) / ((128 + BN / 2) * TC_BK_BYTES) : 4;
   static constexpr int A_STAGE = A_ROWS * TC_BK_BYTES;
   static constexpr int B_STAGE = B_ROWS * TC_BK_BYTES;
   static constexpr int BAR_BYTES = (2 * STAGES + 4) * 8 + 16;
-  static constexpr int SMEM = 1024 + STAGES * (A_STAGE + B_STAGE) + EPI_BYTES + BAR_BYTES;
+  static constexpr int SMEM =
+      1024 + STAGES * (A_STAGE + B_STAGE) + EPI_BYTES + COLS_BYTES + BAR_BYTES;
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
@@ -84,6 +86,7 @@ struct TcParams {
   int tma_store;     // 1: output through the tensor map (ldc*4 % 16 == 0, 16B-aligned base)
   int small_acc;     // F4: every |accumulator| < 2^22 (9K < 2^22), float -> int by magic add
   float shift_mul;   // F4: 2^shift
+  int epi;           // this problem's epilogue (Epi::I32 / Epi::F32) under Epi::ANY
   int num_m_blocks, num_n_blocks, num_tiles;
   int group_m;       // tile raster: groups of group_m M-blocks walked column by column
 };
@@ -107,11 +110,12 @@ __device__ __forceinline__ void tc_tile_coords(int t, const TcParams& p, int num
 // conflict-free), then lane 0 issues one bulk tensor store and moves on; a buffer is
 // rewritten only after the store issued from it two blocks earlier has finished reading.
 // Fallback (unaligned ldc): stride-36 staging and coalesced 4-row x 128 B stores.
+// cs: the tile's column scales staged in shared memory (nullptr: no column scale).
 template <Epi EPI, int BN, bool F32ACC = false, int EPI_BUFS = 2>
 __device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, const CUtensorMap* tmC,
                                                  uint32_t tmem_acc, int quad, int lane,
                                                  int row_base, int col_base, float* stg,
-                                                 uint32_t& buf) {
+                                                 uint32_t& buf, const float* cs) {
   const bool vec_ok = (p.N & 3) == 0;
   const int my_row = row_base + lane;
   float row_mul = p.scale;
@@ -149,10 +153,7 @@ __device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, const CUtens
             const float units = __fmul_rn(acc, p.shift_mul);  // exact: x 1, 2 or 4
             float s = row_mul;
             if constexpr (EPI == Epi::F32) {
-              if (p.col_scale != nullptr) {
-                const int cc = col0 + j + e;
-                s = __fmul_rn(s, cc < p.N ? p.col_scale[cc] : 0.0f);
-              }
+              if (cs != nullptr) s = __fmul_rn(s, cs[c * 32 + j + e]);
             }
             of[e] = __fmul_rn(s, units);
           }
@@ -161,10 +162,7 @@ __device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, const CUtens
         } else if constexpr (EPI == Epi::F32) {
           const float units = static_cast<float>(static_cast<int>(v[j + e]) << p.shift);
           float s = row_mul;
-          if (p.col_scale != nullptr) {
-            const int cc = col0 + j + e;
-            s = __fmul_rn(s, cc < p.N ? p.col_scale[cc] : 0.0f);
-          }
+          if (cs != nullptr) s = __fmul_rn(s, cs[c * 32 + j + e]);
           of[e] = __fmul_rn(s, units);
         } else {
           of[e] = __fmul_rn(row_mul, static_cast<float>(static_cast<int>(v[j + e]) << p.shift));
@@ -223,23 +221,44 @@ __device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, const CUtens
   }
 }
 
-// MC = CTA pairs per cluster. MC = 2: a cluster of four CTAs runs two pairs on horizontally
-// adjacent tiles (same 256 A rows, N blocks 2j and 2j+1). Each pair loads one half of the
-// shared A rows and multicasts it to the same-rank CTA of the other pair, halving A's L2
-// traffic (the GEMM is L2-throughput bound: profiles/ncu_r01f4.md); every stage release is
-// committed to all four CTAs, so a producer refills a stage only when both pairs are done.
-template <Kind KIND, Epi EPI, bool PAIR, int BN, int MC = 1>
+// A launch covers a group of up to NP independent GEMM problems (a single call is a group of
+// one): every problem has its own operand / output tensor maps and parameters, and the
+// persistent grid walks the concatenation of their tiles, so a step of several GEMMs pays one
+// ramp-up and one tail instead of one per GEMM.
+constexpr int TC_GROUP_MAX = 4;
+
+template <int NP>
+struct TcGroup {
+  CUtensorMap a[NP], b[NP], c[NP];
+  TcParams prob[NP];
+  int count;
+  int tile_begin[NP + 1];  // problem i owns tiles [tile_begin[i], tile_begin[i+1])
+};
+
+template <int NP>
+__device__ __forceinline__ int tc_problem_of(const TcGroup<NP>& g, int t) {
+  if constexpr (NP == 1) return 0;
+  int pi = 0;
+#pragma unroll
+  for (int i = 1; i < NP; ++i)
+    if (i < g.count && t >= g.tile_begin[i]) pi = i;
+  return pi;
+}
+
+// Persistent cta_group::2 GEMM (one CTA pair per cluster). EPI == Epi::ANY dispatches each
+// problem's epilogue (I32 or F32) at run time.
+template <Kind KIND, Epi EPI, int BN, int NP>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmC, const TcParams p) {
-  using S = TcShape<PAIR, BN>;
+    tc_gemm_kernel(const __grid_constant__ TcGroup<NP> g) {
+  using S = TcShape<true, BN>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024u - (base_u32 & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = sA + S::STAGES * S::A_STAGE;
   float* sEpi = reinterpret_cast<float*>(sB + S::STAGES * S::B_STAGE);
-  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sEpi) + S::EPI_BYTES);
+  float* sCols = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(sEpi) + S::EPI_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sCols) + S::COLS_BYTES);
   uint64_t* empty = full + S::STAGES;
   uint64_t* tfull = empty + S::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -247,41 +266,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  static_assert(MC == 1 || PAIR, "multicast clusters are built from CTA pairs");
-  const uint32_t crank = PAIR ? cluster_ctarank() : 0u;
-  const uint32_t rank = crank & 1u;                 // rank within the CTA pair
-  const int pair = static_cast<int>(crank >> 1);    // pair within the cluster (MC = 2)
-  const int unit = PAIR ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
-  const int num_units = PAIR ? static_cast<int>(num_clusters_x()) : static_cast<int>(gridDim.x);
-  // cluster tiles: MC horizontally adjacent pair tiles
-  const int nb_groups = (p.num_n_blocks + MC - 1) / MC;
-  const int num_ctiles = p.num_m_blocks * nb_groups;
+  const uint32_t rank = cluster_ctarank();  // rank within the CTA pair
+  const int unit = static_cast<int>(cluster_id_x());
+  const int num_units = static_cast<int>(num_clusters_x());
+  const int num_tiles = g.tile_begin[g.count];
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
-    if (p.tma_store) tma_prefetch_desc(&tmC);
+    for (int i = 0; i < g.count; ++i) {
+      tma_prefetch_desc(&g.a[i]);
+      tma_prefetch_desc(&g.b[i]);
+      if (g.prob[i].tma_store) tma_prefetch_desc(&g.c[i]);
+    }
     for (int s = 0; s < S::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], MC);  // one release per pair of the cluster
+      mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], PAIR ? 256 : 128);
+      mbar_init(&tempty[a], 256);
     }
     fence_mbar_init();
   }
-  if (warp == 1) {
-    if constexpr (PAIR)
-      tmem_alloc_pair(tmem_slot, 512);
-    else
-      tmem_alloc(tmem_slot, 512);
-  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
   tc_fence_before();
-  if constexpr (PAIR)
-    cluster_sync();
-  else
-    __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   constexpr uint32_t kSfCol = 2 * BN;  // F4: scale factors after the two accumulators
@@ -294,10 +302,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tmem_st_wait();
     }
     tc_fence_before();
-    if constexpr (PAIR)
-      cluster_sync();
-    else
-      __syncthreads();
+    cluster_sync();
     tc_fence_after();
   }
   // Everything above overlapped the producer of our operands (PDL); from here on
@@ -312,32 +317,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = unit; tile < num_ctiles; tile += num_units) {
+      for (int tile = unit; tile < num_tiles; tile += num_units) {
+        const int pi = tc_problem_of(g, tile);
+        const TcParams& p = g.prob[pi];
         int mb, nb;
-        tc_tile_coords(tile, p, nb_groups, mb, nb);
-        nb = nb * MC + pair;
+        tc_tile_coords(tile - g.tile_begin[pi], p, p.num_n_blocks, mb, nb);
         const int a_row = mb * S::TILE_M + static_cast<int>(rank) * S::A_ROWS;
         const int b_row = nb * BN + static_cast<int>(rank) * S::B_ROWS;
         for (int kb = 0; kb < p.num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1u);
           const int ka = kb % p.a_kb_period;
-          if constexpr (PAIR) {
-            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (S::A_STAGE + S::B_STAGE));
-            if constexpr (MC == 2) {
-              // this pair's half of the A rows, to this CTA and its twin in the other pair
-              constexpr int HALF = S::A_ROWS / 2;
-              tma_load_2d_pair_mc(sA + stage * S::A_STAGE + pair * HALF * TC_BK_BYTES, &tmA,
-                                  &full[stage], ka * BK_ELEMS, a_row + pair * HALF,
-                                  static_cast<uint16_t>(0x5u << rank));
-            } else {
-              tma_load_2d_pair(sA + stage * S::A_STAGE, &tmA, &full[stage], ka * BK_ELEMS, a_row);
-            }
-            tma_load_2d_pair(sB + stage * S::B_STAGE, &tmB, &full[stage], kb * BK_ELEMS, b_row);
-          } else {
-            mbar_arrive_expect_tx(&full[stage], S::A_STAGE + S::B_STAGE);
-            tma_load_2d(sA + stage * S::A_STAGE, &tmA, &full[stage], ka * BK_ELEMS, a_row);
-            tma_load_2d(sB + stage * S::B_STAGE, &tmB, &full[stage], kb * BK_ELEMS, b_row);
-          }
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (S::A_STAGE + S::B_STAGE));
+          tma_load_2d_pair(sA + stage * S::A_STAGE, &g.a[pi], &full[stage], ka * BK_ELEMS, a_row);
+          tma_load_2d_pair(sB + stage * S::B_STAGE, &g.b[pi], &full[stage], kb * BK_ELEMS, b_row);
           if (++stage == S::STAGES) {
             stage = 0;
             phase ^= 1u;
@@ -346,75 +338,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer (leader CTA only) =====================
+    // ===================== MMA issuer (leader CTA, whole warp) =====================
+    // Warp-uniform state; one elected lane issues each tcgen05 instruction. Descriptors:
+    // the stage-0 descriptor plus (byte offset >> 4) in the address field.
     constexpr uint32_t idesc = (KIND == Kind::I8)   ? make_idesc(2u, 1u, 1u, S::TILE_M, BN)
                                : (KIND == Kind::F4) ? make_idesc_mxf4(S::TILE_M, BN)
                                                     : make_idesc(1u, 1u, 1u, S::TILE_M, BN);
-    if constexpr (PAIR) {
-      // whole warp, warp-uniform state; one elected lane issues each tcgen05 instruction.
-      // Descriptors: the stage-0 descriptor plus (byte offset >> 4) in the address field.
-      if (rank == 0) {
-        constexpr int KID = (KIND == Kind::I8) ? 0 : (KIND == Kind::F4) ? 2 : 1;
-        const uint64_t a_desc0 = sw128_kmajor_desc(smem_u32(sA));
-        const uint64_t b_desc0 = sw128_kmajor_desc(smem_u32(sB));
-        const uint32_t sfa = tmem_base + kSfCol, sfb = tmem_base + kSfCol + 32;
-        int stage = 0;
-        uint32_t phase = 0;
-        int it = 0;
-        for (int tile = unit; tile < num_ctiles; tile += num_units, ++it) {
-          const int acc = it & 1;
-          const uint32_t aphase = (it >> 1) & 1;
-          mbar_wait(&tempty[acc], aphase ^ 1u);
-          tc_fence_after();
-          const uint32_t d_tmem = tmem_base + acc * BN;
-          for (int kb = 0; kb < p.num_kb; ++kb) {
-            mbar_wait(&full[stage], phase);
-            tc_fence_after();
-            const uint64_t ad = a_desc0 + static_cast<uint64_t>((stage * S::A_STAGE) >> 4);
-            const uint64_t bd = b_desc0 + static_cast<uint64_t>((stage * S::B_STAGE) >> 4);
-#pragma unroll
-            for (int k = 0; k < TC_BK_BYTES / 32; ++k)
-              mma_pair_elect<KID>(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0, sfa, sfb);
-            mma_commit_pair_elect(&empty[stage], MC == 2 ? 0xF : 0x3);
-            if (++stage == S::STAGES) {
-              stage = 0;
-              phase ^= 1u;
-            }
-          }
-          mma_commit_pair_elect(&tfull[acc], static_cast<uint16_t>(0x3u << (2 * pair)));
-        }
-      }
-    } else if (lane == 0) {
+    if (rank == 0) {
+      constexpr int KID = (KIND == Kind::I8) ? 0 : (KIND == Kind::F4) ? 2 : 1;
+      const uint64_t a_desc0 = sw128_kmajor_desc(smem_u32(sA));
+      const uint64_t b_desc0 = sw128_kmajor_desc(smem_u32(sB));
+      const uint32_t sfa = tmem_base + kSfCol, sfb = tmem_base + kSfCol + 32;
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = unit; tile < num_ctiles; tile += num_units, ++it) {
+      for (int tile = unit; tile < num_tiles; tile += num_units, ++it) {
+        const int num_kb = g.prob[tc_problem_of(g, tile)].num_kb;
         const int acc = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], aphase ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < p.num_kb; ++kb) {
+        for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + stage * S::A_STAGE);
-          const uint32_t b_addr = smem_u32(sB + stage * S::B_STAGE);
+          const uint64_t ad = a_desc0 + static_cast<uint64_t>((stage * S::A_STAGE) >> 4);
+          const uint64_t bd = b_desc0 + static_cast<uint64_t>((stage * S::B_STAGE) >> 4);
 #pragma unroll
-          for (int k = 0; k < TC_BK_BYTES / 32; ++k) {
-            const uint64_t ad = sw128_kmajor_desc(a_addr + k * 32);
-            const uint64_t bd = sw128_kmajor_desc(b_addr + k * 32);
-            if constexpr (KIND == Kind::I8)
-              mma_i8(d_tmem, ad, bd, idesc, (kb | k) != 0);
-            else
-              mma_f16(d_tmem, ad, bd, idesc, (kb | k) != 0);
-          }
-          mma_commit(&empty[stage]);
+          for (int k = 0; k < TC_BK_BYTES / 32; ++k)
+            mma_pair_elect<KID>(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0, sfa, sfb);
+          mma_commit_pair_elect(&empty[stage], 0x3);
           if (++stage == S::STAGES) {
             stage = 0;
             phase ^= 1u;
           }
         }
-        mma_commit(&tfull[acc]);
+        mma_commit_pair_elect(&tfull[acc], 0x3);
       }
     }
   } else {
@@ -423,37 +382,52 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     float* stg = sEpi + (warp - 2) * (S::EPI_WARP_BYTES / 4);
     uint32_t buf = 0;
     int it = 0;
-    for (int tile = unit; tile < num_ctiles; tile += num_units, ++it) {
+    for (int tile = unit; tile < num_tiles; tile += num_units, ++it) {
+      const int pi = tc_problem_of(g, tile);
+      const TcParams p = g.prob[pi];  // by value: its fields stay in registers in the epilogue
       int mb, nb;
-      tc_tile_coords(tile, p, nb_groups, mb, nb);
-      nb = nb * MC + pair;
+      tc_tile_coords(tile - g.tile_begin[pi], p, p.num_n_blocks, mb, nb);
       const int acc = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const int row_base = mb * S::TILE_M + static_cast<int>(rank) * 128 + quad * 32;
-      tc_epilogue_tile<EPI, BN, KIND == Kind::F4, S::EPI_BUFS>(p, &tmC, tmem_base + acc * BN, quad, lane, row_base, nb * BN, stg,
-                            buf);
+      constexpr bool kF32Acc = KIND == Kind::F4;
+      const uint32_t tacc = tmem_base + acc * BN;
+      // Column scales of this tile -> smem (broadcast reads in the transform). The first
+      // barrier keeps the previous tile's readers ahead of the overwrite.
+      const float* cs = nullptr;
+      if (p.col_scale != nullptr && p.epi != static_cast<int>(Epi::I32)) {
+        named_bar_sync(1, 128);
+        for (int i = (warp - 2) * 32 + lane; i < BN; i += 128) {
+          const int cc = nb * BN + i;
+          sCols[i] = cc < p.N ? p.col_scale[cc] : 0.0f;
+        }
+        named_bar_sync(1, 128);
+        cs = sCols;
+      }
+      if constexpr (EPI == Epi::ANY) {
+        if (p.epi == static_cast<int>(Epi::I32))
+          tc_epilogue_tile<Epi::I32, BN, kF32Acc, S::EPI_BUFS>(p, &g.c[pi], tacc, quad, lane,
+                                                               row_base, nb * BN, stg, buf, cs);
+        else
+          tc_epilogue_tile<Epi::F32, BN, kF32Acc, S::EPI_BUFS>(p, &g.c[pi], tacc, quad, lane,
+                                                               row_base, nb * BN, stg, buf, cs);
+      } else {
+        tc_epilogue_tile<EPI, BN, kF32Acc, S::EPI_BUFS>(p, &g.c[pi], tacc, quad, lane, row_base,
+                                                        nb * BN, stg, buf, cs);
+      }
       tc_fence_before();
-      if constexpr (PAIR)
-        mbar_arrive_cluster(smem_u32(&tempty[acc]) & kPeerBitMask);
-      else
-        mbar_arrive(&tempty[acc]);
+      mbar_arrive_cluster(smem_u32(&tempty[acc]) & kPeerBitMask);
     }
-    if (p.tma_store && lane == 0) bulk_wait_group_all();  // stores land before the grid ends
+    if (lane == 0) bulk_wait_group_all();  // stores land before the grid ends
   }
 
   tc_fence_before();
-  if constexpr (PAIR)
-    cluster_sync();
-  else
-    __syncthreads();
+  cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    if constexpr (PAIR)
-      tmem_dealloc_pair(tmem_base, 512);
-    else
-      tmem_dealloc(tmem_base, 512);
+    tmem_dealloc_pair(tmem_base, 512);
   }
 }
 

@@ -7,7 +7,7 @@
 //
 // Outputs are K-major operand rows padded to kpad elements with zeros, so the
 // padding never contributes to a product:
-//   unpack_pair_i8   : both GEMM operands in one launch:
+//   unpack_operands   : both GEMM operands in one launch:
 //                      bit b -> int8 (2b-1)                (BitMatrix, tensor.hpp:59)
 //                      planes {t,h,m} -> int8 level p      (ThmPlanes, tensor.hpp:134;
 //                      legal states per transform.cpp:47-75: p0=(0,0,1) p1=(0,0,0)
@@ -49,12 +49,15 @@ struct UnpackOperand {
   long long groups_per_row;  // slices of 128 words (4096 elements) per row
   int wpr32;
   int levels;  // 0: +-1 signs, 1: 2-bit levels
+  int K;       // logical columns (bits past K must be zero)
+  int kpad;    // expanded elements per row (zero past K)
 };
 
-struct UnpackPair {
-  UnpackOperand op[2];
-  int K;
-  int kpad;
+// Every operand of one launch: the two of a GEMM, or all operands of a GEMM group.
+constexpr int UNPACK_MAX_OPS = 8;
+struct UnpackSet {
+  UnpackOperand op[UNPACK_MAX_OPS];
+  int count;
   int* err;
   int fp4;  // 1: packed e2m1 nibbles, rows of kpad/2 bytes (Kind::F4 operands)
 };
@@ -190,7 +193,7 @@ __device__ __forceinline__ int unpack_slice_warp(const UnpackOperand& o, long lo
 // A variant that deferred this wait to the end, to overlap with the previous GEMM, deadlocked
 // nondeterministically on B200 (dependent blocks parked in griddepcontrol.wait while holding
 // SM slots); see DESIGN.md.
-__global__ void __launch_bounds__(256) unpack_pair_i8(const __grid_constant__ UnpackPair P) {
+__global__ void __launch_bounds__(256) unpack_operands(const __grid_constant__ UnpackSet P) {
   pdl_wait();
   pdl_launch_dependents();
   const UnpackOperand& o = P.op[blockIdx.y];
@@ -200,8 +203,8 @@ __global__ void __launch_bounds__(256) unpack_pair_i8(const __grid_constant__ Un
   if (unit >= o.rows * slices) return;
   const long long r = unit / slices;
   const int sl = static_cast<int>(unit - r * slices);
-  const int bad = P.fp4 ? unpack_slice_warp(o, r, sl, P.K, P.kpad, lane, true)
-                        : unpack_slice_warp(o, r, sl, P.K, P.kpad, lane, false);
+  const int bad = P.fp4 ? unpack_slice_warp(o, r, sl, o.K, o.kpad, lane, true)
+                        : unpack_slice_warp(o, r, sl, o.K, o.kpad, lane, false);
   if (bad && lane == 0) atomicOr(P.err, bad);
 }
 

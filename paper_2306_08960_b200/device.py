@@ -111,6 +111,39 @@ def layer_forward(bin_words: torch.Tensor, cols: int, alpha, row_ptr, col_idx, v
         _ptr(vals), _ptr(b), n, b.shape[1], _ptr(out), out.shape[1], _stream(stream)))
 
 
+def gemm_batch(items, stream=None) -> None:
+    """One grouped launch for several GEMMs (bitmm_gemm_batch_dev). `items`: dicts with
+    routine ('1x1' | '1x2' | '2x2'), the operand tensors (a / w / wt,wh,wm and b / t,h,m),
+    k, optional scales (gamma_a, gamma_b, gamma, a_scale, w_scale, a_gamma, w_gamma,
+    row_scale, col_scale) and outputs (units, out) — the keywords of gemm_1x1/1x2/2x2."""
+    arr = (_lib.GemmItem * len(items))()
+    for it, d in zip(arr, items):
+        r = d["routine"]
+        if r == "1x1":
+            it.routine, a, b = _lib.ROUTINE_1X1, [d["a"]], [d["b"]]
+            it.a_scale, it.b_scale = d.get("gamma_a", 1.0), d.get("gamma_b", 1.0)
+        elif r == "1x2":
+            it.routine, a, b = _lib.ROUTINE_1X2, [d["w"]], [d["t"], d["h"], d["m"]]
+            it.a_scale, it.b_scale = d.get("gamma", 1.0), d.get("a_scale", 1.0)
+        else:
+            it.routine, a, b = _lib.ROUTINE_2X2, [d["wt"], d["wh"], d["wm"]], [d["t"], d["h"], d["m"]]
+            it.a_scale, it.b_scale = d.get("w_scale", 1.0), d.get("a_scale", 1.0)
+            if d.get("w_gamma") is not None:
+                it.has_a_gamma, it.a_gamma = 1, d["w_gamma"]
+        if r != "1x1" and d.get("a_gamma") is not None:
+            it.has_b_gamma, it.b_gamma = 1, d["a_gamma"]
+        it.a0, it.a1, it.a2 = (_ptr(a[i]) if i < len(a) else None for i in range(3))
+        it.b0, it.b1, it.b2 = (_ptr(b[i]) if i < len(b) else None for i in range(3))
+        it.m, it.wpr = a[0].shape
+        it.n = b[0].shape[0]
+        it.k = d["k"]
+        it.row_scale, it.col_scale = _ptr(d.get("row_scale")), _ptr(d.get("col_scale"))
+        u, o = d.get("units"), d.get("out")
+        it.c_units, it.c = _ptr(u), _ptr(o)
+        it.ldc = (u if u is not None else o).shape[1]
+    _raise(_lib.load().bitmm_gemm_batch_dev(arr, len(items), _stream(stream)))
+
+
 def layer_forward_2bit(bin_words: torch.Tensor, cols: int, alpha, row_ptr, col_idx, vals,
                        t: torch.Tensor, h: torch.Tensor, m: torch.Tensor, out: torch.Tensor,
                        a_scale: float = 1.0, a_gamma: Optional[float] = None, stream=None) -> None:

@@ -94,3 +94,18 @@ def test_header_compiles_as_c():
     src = f'#include "{hdr}"\nint main(void) {{ return bitmm_abi_version(); }}\n'
     subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-x", "c", "-fsyntax-only", "-"],
                    input=src, text=True, check=True)
+
+
+def test_gemm_item_struct_layout_matches_c(tmp_path):
+    """ctypes GemmItem and the C bitmm_gemm_item agree on size and every field offset."""
+    import ctypes as C
+    hdr = os.path.join(REPO, "include", "bitmm_b200.h")
+    names = [f[0] for f in _lib.GemmItem._fields_]
+    body = "".join(f'  printf("%zu\\n", offsetof(bitmm_gemm_item, {n}));\n' for n in names)
+    src = (f'#include <stddef.h>\n#include <stdio.h>\n#include "{hdr}"\n'
+           f'int main(void) {{\n  printf("%zu\\n", sizeof(bitmm_gemm_item));\n{body}  return 0;\n}}\n')
+    exe = str(tmp_path / "layout")
+    subprocess.run(["gcc", "-std=c99", "-x", "c", "-", "-o", exe], input=src, text=True, check=True)
+    out = [int(x) for x in subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split()]
+    assert out[0] == C.sizeof(_lib.GemmItem)
+    assert out[1:] == [getattr(_lib.GemmItem, n).offset for n in names]
