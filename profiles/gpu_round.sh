@@ -15,6 +15,6 @@ if [ "${NCU:-1}" = "1" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
       --log-file gpurun_out/launches_$TAG.csv $BENCH_SMALL > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "ncu launches rc=$?"
   timeout 300 $BENCH_SMALL > gpurun_out/plain2_$TAG.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 2 -c 3 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 1 -c 2 \
       -o gpurun_out/prof_tc_$TAG $BENCH_SMALL > gpurun_out/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"
 fi
