@@ -201,8 +201,19 @@ __global__ void __launch_bounds__(256) unpack_operands(const __grid_constant__ U
   const int lane = threadIdx.x & 31;
   const long long slices = o.groups_per_row;  // slices of 128 words per row
   if (unit >= o.rows * slices) return;
-  const long long r = unit / slices;
-  const int sl = static_cast<int>(unit - r * slices);
+  long long r;
+  int sl;
+  if (slices == 1) {  // K <= 4096: one slice per row
+    r = unit;
+    sl = 0;
+  } else if (o.rows * slices < (1ll << 31)) {  // 32-bit division (the 64-bit one is ~4x longer)
+    const unsigned q = static_cast<unsigned>(unit) / static_cast<unsigned>(slices);
+    r = q;
+    sl = static_cast<int>(static_cast<unsigned>(unit) - q * static_cast<unsigned>(slices));
+  } else {
+    r = unit / slices;
+    sl = static_cast<int>(unit - r * slices);
+  }
   const int bad = P.fp4 ? unpack_slice_warp(o, r, sl, o.K, o.kpad, lane, true)
                         : unpack_slice_warp(o, r, sl, o.K, o.kpad, lane, false);
   if (bad && lane == 0) atomicOr(P.err, bad);
