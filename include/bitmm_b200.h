@@ -48,7 +48,8 @@ enum {
   BITMM_ERR_INVALID_ARGUMENT = 1,
   BITMM_ERR_INVALID_ENCODING = 2,
   BITMM_ERR_CUDA = 3,
-  BITMM_ERR_NO_DEVICE = 4
+  BITMM_ERR_NO_DEVICE = 4,
+  BITMM_ERR_IO = 5 /* ≙ bitmm::IoError (errors.hpp:14): container format / file errors */
 };
 
 /* Shared-dimension cap (tensor.hpp:21, kMaxSharedDim = 2^20). */
@@ -184,6 +185,34 @@ typedef struct bitmm_gemm_item {
   int64_t ldc;
 } bitmm_gemm_item;
 int bitmm_gemm_batch_dev(const bitmm_gemm_item* items, int count, void* stream);
+
+/* ---- ThmPlanes::validate on device (tensor.cpp:133-153) ----
+ * Checks scale > 0, zero padding and legal {t,h,m} states of plane words already on the
+ * device; returns BITMM_ERR_INVALID_ENCODING with the reference's message (same precedence:
+ * scale, padding, then the first illegal word in row-major order). Synchronous. */
+int bitmm_validate_planes_dev(const uint64_t* t, const uint64_t* h, const uint64_t* m,
+                              int64_t rows, int64_t cols, int64_t wpr, float scale, void* stream);
+
+/* ---- BTSR container -> device (tensor_io.hpp:14-37, tensor_io.cpp:139-215) ----
+ * BTSR v1: magic "BTSR" | version u32 | kind u8 (0 dense, 1 bit, 2 csr) | rows u64 | cols u64 |
+ * payload (dense: f32[rows*cols]; bit: wpr u64, u64[rows*wpr]; csr: nnz u64,
+ * row_ptr u64[rows+1], col_idx u64[nnz], vals f32[nnz]), little-endian.
+ * bitmm_btsr_read_header validates the header and the file size (no GPU needed).
+ * bitmm_btsr_load_dev streams the payload into caller-allocated device buffers through pinned
+ * chunks on `stream` and applies the reference's object checks on the way (BitMatrix padding,
+ * CsrMatrix::validate, finite dense values). expected_kind -1 accepts any kind, else a
+ * mismatch fails like load_dense/load_bit/load_csr ("expected bit tensor: <path>").
+ * dense -> payload f32[rows*cols]; bit -> payload u64[rows*wpr]; csr -> row_ptr / col_idx /
+ * vals. Failures return BITMM_ERR_IO with the reference's IoError text. */
+typedef struct bitmm_btsr_header {
+  int kind;
+  int64_t rows, cols;
+  int64_t words_per_row; /* bit */
+  int64_t nnz;           /* csr */
+} bitmm_btsr_header;
+int bitmm_btsr_read_header(const char* path, bitmm_btsr_header* out);
+int bitmm_btsr_load_dev(const char* path, int expected_kind, void* payload, uint64_t* row_ptr,
+                        uint64_t* col_idx, float* vals, void* stream);
 
 /* ---- APB layer with 2-bit activations (paper-faithful inference) ----
  * No single reference entry point: it is the composition of reference calls

@@ -239,6 +239,11 @@ class Ref:
             "ref_decompose_apb": (_i, [_p, _i64, _i64, _f, _i, _p, C.POINTER(_i64), _p, _p, _p,
                                        C.POINTER(_i64)]),
             "ref_pack_signs": (_i, [_p, _i64, _i64, _i, _p, C.POINTER(_i64)]),
+            "ref_store_dense": (_i, [C.c_char_p, _p, _i64, _i64]),
+            "ref_store_bit": (_i, [C.c_char_p, _p, _i64, _i64, _i64]),
+            "ref_store_csr": (_i, [C.c_char_p, _i64, _i64, _p, _p, _p, _i64]),
+            "ref_store_thm_planes": (_i, [C.c_char_p, _p, _p, _p, _i64, _i64, _i64, _f, _i, _f]),
+            "ref_load_check": (_i, [C.c_char_p, _i]),
             "ref_decompose_thm": (_i, [_p, _i64, _i64, _f, _i, _p, _p, _p, C.POINTER(_i64)]),
             "ref_quantize_2bit": (_i, [_p, _i64, _i64, _f, _p]),
             "ref_dot_binary": (_i, [_p, _p, _i64, _i64, C.POINTER(_i64)]),
@@ -373,6 +378,32 @@ class Ref:
         out = _i64(0)
         self._check(self.lib.ref_mbm(_ptr(x), _ptr(y), _ptr(z), x.size, C.byref(out)))
         return out.value
+
+    # ---- BTSR containers through the reference writer / reader ----
+    def store_dense(self, path, a):
+        a = np.ascontiguousarray(a, np.float32)
+        self._check(self.lib.ref_store_dense(path.encode(), _ptr(a), a.shape[0], a.shape[1]))
+
+    def store_bit(self, path, words, rows, cols):
+        w = np.ascontiguousarray(words, np.uint64)
+        self._check(self.lib.ref_store_bit(path.encode(), _ptr(w), rows, cols, w.shape[1] if w.ndim == 2 else 0))
+
+    def store_csr(self, path, rows, cols, row_ptr, col_idx, vals):
+        rp = np.ascontiguousarray(row_ptr, np.uint64)
+        ci = np.ascontiguousarray(col_idx, np.uint64)
+        v = np.ascontiguousarray(vals, np.float32)
+        self._check(self.lib.ref_store_csr(path.encode(), rows, cols, _ptr(rp), _ptr(ci), _ptr(v), ci.size))
+
+    def store_thm_planes(self, prefix, t, h, m, cols, scale, gamma=None):
+        t, h, m = (np.ascontiguousarray(x, np.uint64) for x in (t, h, m))
+        self._check(self.lib.ref_store_thm_planes(prefix.encode(), _ptr(t), _ptr(h), _ptr(m), t.shape[0],
+                                                  cols, t.shape[1], scale, int(gamma is not None),
+                                                  0.0 if gamma is None else gamma))
+
+    def load_check(self, path, kind=-1):
+        """(error class, message) of the reference reader on `path`; (0, '') when it loads."""
+        rc = self.lib.ref_load_check(path.encode(), kind)
+        return rc, (self.lib.ref_last_error().decode() if rc else "")
 
 
 def load_ref() -> Optional[Ref]:

@@ -20,6 +20,7 @@
 #include "bitmm/kernels.hpp"
 #include "bitmm/simd.hpp"
 #include "bitmm/tensor.hpp"
+#include "bitmm/tensor_io.hpp"
 #include "bitmm/transform.hpp"
 
 using namespace bitmm;
@@ -39,6 +40,9 @@ int guarded(Fn&& fn) {
   } catch (const std::invalid_argument& e) {
     g_msg = e.what();
     return 1;
+  } catch (const IoError& e) {
+    g_msg = e.what();
+    return 5;
   } catch (const std::exception& e) {
     g_msg = e.what();
     return 9;
@@ -224,6 +228,40 @@ int ref_mbm(const uint64_t* x, const uint64_t* y, const uint64_t* z, int64_t wor
   return guarded([&] {
     const auto w = static_cast<std::size_t>(words);
     *out = mbm({x, w}, {y, w}, {z, w});
+  });
+}
+
+// ---- BTSR containers through the reference's own writer / reader (tensor_io.cpp) ----
+int ref_store_dense(const char* path, const float* a, int64_t rows, int64_t cols) {
+  return guarded([&] { store_tensor(path, dense(a, rows, cols)); });
+}
+
+int ref_store_bit(const char* path, const uint64_t* w, int64_t rows, int64_t cols, int64_t wpr) {
+  return guarded([&] { store_tensor(path, bits(w, rows, cols, wpr)); });
+}
+
+int ref_store_csr(const char* path, int64_t rows, int64_t cols, const uint64_t* row_ptr,
+                  const uint64_t* col_idx, const float* vals, int64_t nnz) {
+  return guarded([&] { store_tensor(path, csr(rows, cols, row_ptr, col_idx, vals, nnz)); });
+}
+
+int ref_store_thm_planes(const char* prefix, const uint64_t* t, const uint64_t* h, const uint64_t* m,
+                         int64_t rows, int64_t cols, int64_t wpr, float scale, int has_gamma,
+                         float gamma) {
+  return guarded([&] {
+    store_thm_planes(prefix, planes(t, h, m, rows, cols, wpr, scale, has_gamma, gamma));
+  });
+}
+
+// Loads with the reference reader; kind -1 any, 0 dense, 1 bit, 2 csr (load_dense / load_bit /
+// load_csr), 3 thm plane prefix. Returns 0 or the error class (message via ref_last_error).
+int ref_load_check(const char* path, int kind) {
+  return guarded([&] {
+    if (kind == 0) (void)load_dense(path);
+    else if (kind == 1) (void)load_bit(path);
+    else if (kind == 2) (void)load_csr(path);
+    else if (kind == 3) (void)load_thm_planes(path);
+    else (void)load_tensor(path);
   });
 }
 

@@ -19,6 +19,7 @@ ERR_INVALID_ARGUMENT = 1
 ERR_INVALID_ENCODING = 2
 ERR_CUDA = 3
 ERR_NO_DEVICE = 4
+ERR_IO = 5
 
 _p = C.c_void_p
 _i64 = C.c_int64
@@ -42,6 +43,12 @@ class GemmItem(C.Structure):
         ("row_scale", _p), ("col_scale", _p),
         ("c_units", _p), ("c", _p), ("ldc", _i64),
     ]
+
+
+class BtsrHeader(C.Structure):
+    """ctypes mirror of `bitmm_btsr_header`."""
+    _fields_ = [("kind", C.c_int), ("rows", _i64), ("cols", _i64), ("words_per_row", _i64),
+                ("nnz", _i64)]
 
 
 SIGNATURES = {
@@ -101,6 +108,9 @@ SIGNATURES = {
         [_i64, _i64, _f, _p, _p, _i64, _p, _p, _p, _i64, _p, _p, _p, _i64, _f, _i, _f, _p, _i64],
     ),
     "bitmm_gemm_batch_dev": (_i, [_p, _i, _p]),
+    "bitmm_btsr_read_header": (_i, [C.c_char_p, _p]),
+    "bitmm_validate_planes_dev": (_i, [_p, _p, _p, _i64, _i64, _i64, _f, _p]),
+    "bitmm_btsr_load_dev": (_i, [C.c_char_p, _i, _p, _p, _p, _p, _p]),
     "bitmm_pack_signs_dev": (_i, [_p, _i64, _i64, _i64, _p, _i64, _p]),
     "bitmm_pack_signs_host": (_i, [_p, _i64, _i64, _i64, _p, _i64]),
     "bitmm_quantize_thm_dev": (_i, [_p, _i64, _i64, _i64, _f, _p, _p, _p, _i64, _p]),

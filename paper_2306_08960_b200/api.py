@@ -24,6 +24,10 @@ from .data import LANE_BITS, padded_words, tail_mask_words
 MAX_SHARED_DIM = 1 << 20  # kMaxSharedDim, tensor.hpp:21
 
 
+class IoError(RuntimeError):
+    """errors.hpp:14 — container format / file errors (BITMM_ERR_IO)."""
+
+
 class InvalidEncoding(RuntimeError):
     """bitmm::InvalidEncoding (errors.hpp:20-23)."""
 
@@ -36,6 +40,8 @@ def _raise(rc: int) -> None:
         raise ValueError(msg)
     if rc == _lib.ERR_INVALID_ENCODING:
         raise InvalidEncoding(msg)
+    if rc == _lib.ERR_IO:
+        raise IoError(msg)
     raise _lib.BitmmError(f"bitmm_b200 error {rc}: {msg}")
 
 

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "apb_gemm.cuh"
+#include "btsr_io.cuh"
 #include "bitmm_b200.h"
 #include "pack.cuh"
 #include "popc_gemm.cuh"
@@ -60,6 +61,8 @@ struct DeviceState {
   cudaStream_t stream = nullptr;  // host-flavour private stream
   uint64_t attr_mask = 0;     // spmm / apb kernels (max-smem attribute set)
   unsigned ws_turn = 0;           // ping-pong half of the expanded-operand workspace
+  void* pinned[2] = {nullptr, nullptr};  // BTSR streaming chunks (allocated on first load)
+  cudaEvent_t pinned_ev[2] = {nullptr, nullptr};
 };
 
 std::mutex g_mu;
@@ -1456,6 +1459,154 @@ int bitmm_gemm_batch_dev(const bitmm_gemm_item* items, int count, void* stream) 
   }
   BITMM_TRY(run_unpack_set(U, s));
   return run_problems(*st, probs, np, fp4, s);
+}
+
+// ---------------- plane validation ----------------
+int bitmm_validate_planes_dev(const uint64_t* t, const uint64_t* h, const uint64_t* m,
+                              int64_t rows, int64_t cols, int64_t wpr, float scale, void* stream) {
+  g_launches = 0;
+  if (!(scale > 0.0f)) return fail(BITMM_ERR_INVALID_ENCODING, "plane scale must be positive");
+  if (rows < 0 || cols < 0 || wpr * 64 < cols)
+    return fail(BITMM_ERR_INVALID_ARGUMENT, "words_per_row too small for the column count");
+  if (rows == 0 || wpr == 0) return BITMM_OK;
+  if (!t || !h || !m) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  BITMM_TRY(arena_reserve(st->io, 64));
+  int* pad = static_cast<int*>(st->io.ptr);
+  unsigned long long* first = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(st->io.ptr) + 8);
+  BITMM_CUDA_TRY(cudaMemsetAsync(pad, 0, 4, s));
+  BITMM_CUDA_TRY(cudaMemsetAsync(first, 0xFF, 8, s));
+  {
+    ProfScope ps("validate_planes", s);
+    validate_planes_kernel<<<blocks_for(rows * wpr, 256), 256, 0, s>>>(
+        reinterpret_cast<const unsigned long long*>(t), reinterpret_cast<const unsigned long long*>(h),
+        reinterpret_cast<const unsigned long long*>(m), rows, cols, wpr, pad, first);
+    BITMM_TRY(launch_check("validate_planes_kernel"));
+  }
+  int pad_h = 0;
+  unsigned long long first_h = 0;
+  BITMM_CUDA_TRY(cudaMemcpyAsync(&pad_h, pad, 4, cudaMemcpyDeviceToHost, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(&first_h, first, 8, cudaMemcpyDeviceToHost, s));
+  BITMM_CUDA_TRY(cudaStreamSynchronize(s));
+  if (pad_h) return fail(BITMM_ERR_INVALID_ENCODING, "plane padding must be zero");
+  if (first_h != ~0ull) {
+    static const char* kMsg[4] = {"", "t and h set on the same element", "t requires m",
+                                  "h requires m clear"};
+    return fail(BITMM_ERR_INVALID_ENCODING, kMsg[first_h & 3]);
+  }
+  return BITMM_OK;
+}
+
+// ---------------- BTSR container -> device ----------------
+int bitmm_btsr_read_header(const char* path, bitmm_btsr_header* out) {
+  if (!path || !out) return fail(BITMM_ERR_INVALID_ARGUMENT, "null argument");
+  BtsrFile bf;
+  BtsrHeader h;
+  const std::string msg = btsr_open(path, bf, h);
+  if (!msg.empty()) return fail(BITMM_ERR_IO, msg);
+  out->kind = h.kind;
+  out->rows = static_cast<int64_t>(h.rows);
+  out->cols = static_cast<int64_t>(h.cols);
+  out->words_per_row = static_cast<int64_t>(h.wpr);
+  out->nnz = static_cast<int64_t>(h.nnz);
+  return BITMM_OK;
+}
+
+int bitmm_btsr_load_dev(const char* path, int expected_kind, void* payload, uint64_t* row_ptr,
+                        uint64_t* col_idx, float* vals, void* stream) {
+  g_launches = 0;
+  if (!path) return fail(BITMM_ERR_INVALID_ARGUMENT, "null argument");
+  BtsrFile bf;
+  BtsrHeader h;
+  std::string msg = btsr_open(path, bf, h);
+  if (!msg.empty()) return fail(BITMM_ERR_IO, msg);
+  static const char* kKindName[3] = {"dense", "bit", "csr"};
+  if (expected_kind >= 0 && expected_kind != h.kind)  // tensor_io.cpp load_kind
+    return fail(BITMM_ERR_IO, std::string("expected ") + kKindName[expected_kind < 3 ? expected_kind : 0] +
+                                  " tensor: " + bf.path);
+  if ((h.kind != 2 && h.payload_bytes > 0 && !payload) ||
+      (h.kind == 2 && (!row_ptr || (h.nnz > 0 && (!col_idx || !vals)))))
+    return fail(BITMM_ERR_INVALID_ARGUMENT, "null destination");
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  for (int i = 0; i < 2; ++i) {
+    if (!st->pinned[i]) {
+      BITMM_CUDA_TRY(cudaHostAlloc(&st->pinned[i], kBtsrChunk, cudaHostAllocDefault));
+      BITMM_CUDA_TRY(cudaEventCreateWithFlags(&st->pinned_ev[i], cudaEventDisableTiming));
+    }
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t cerr = cudaSuccess;
+  auto done = [&](const std::string& m) -> int {
+    if (m == "cuda") return fail(BITMM_ERR_CUDA, std::string("BTSR copy: ") + cudaGetErrorString(cerr));
+    if (!m.empty()) return fail(BITMM_ERR_IO, m);
+    BITMM_CUDA_TRY(cudaStreamSynchronize(s));  // pinned chunks are reused by the next load
+    return BITMM_OK;
+  };
+  if (h.kind == 0) {  // DenseMatrix(rows, cols, data) rejects non-finite entries
+    return done(btsr_stream(bf, static_cast<uint8_t*>(payload), h.payload_bytes, st->pinned,
+                            st->pinned_ev, s, [](const uint8_t* p, uint64_t, size_t n) -> std::string {
+                              const float* v = reinterpret_cast<const float*>(p);
+                              for (size_t i = 0; i < n / 4; ++i)
+                                if (!std::isfinite(v[i])) return "dense matrix entries must be finite";
+                              return std::string();
+                            }, &cerr));
+  }
+  if (h.kind == 1) {  // BitMatrix::from_words: padding bits must be zero (tensor.cpp:78-89)
+    const uint64_t full = h.cols / 64, tail = h.cols % 64;
+    const uint64_t keep = tail ? ((uint64_t{1} << tail) - 1) : ~uint64_t{0};
+    const uint64_t wpr = h.wpr;
+    return done(btsr_stream(bf, static_cast<uint8_t*>(payload), h.payload_bytes, st->pinned,
+                            st->pinned_ev, s, [&](const uint8_t* p, uint64_t off, size_t n) -> std::string {
+                              const uint64_t* w = reinterpret_cast<const uint64_t*>(p);
+                              uint64_t cw = (off / 8) % wpr;
+                              for (size_t i = 0; i < n / 8; ++i) {
+                                if (cw >= full) {
+                                  const uint64_t bad = (cw == full && tail) ? (w[i] & ~keep) : w[i];
+                                  if (bad) return "bit matrix padding must be zero";
+                                }
+                                if (++cw == wpr) cw = 0;
+                              }
+                              return std::string();
+                            }, &cerr));
+  }
+  // csr: CsrMatrix::validate order (tensor.cpp:104-123): row_ptr, then column indices, values
+  std::vector<uint64_t> rp(h.rows + 1);
+  if (!bf.read(rp.data(), rp.size() * 8)) return fail(BITMM_ERR_IO, "truncated file: " + bf.path);
+  auto csr_fail = [&](const char* what) { return fail(BITMM_ERR_IO, std::string(what) + ": " + bf.path); };
+  if (rp[0] != 0) return csr_fail("csr row_ptr must start at 0");
+  for (uint64_t r = 0; r < h.rows; ++r)
+    if (rp[r] > rp[r + 1]) return csr_fail("csr row_ptr must be monotone");
+  if (rp[h.rows] != h.nnz) return csr_fail("csr payload sizes must match nnz");
+  BITMM_CUDA_TRY(cudaMemcpyAsync(row_ptr, rp.data(), rp.size() * 8, cudaMemcpyHostToDevice, s));
+  uint64_t row = 0, prev = 0;
+  const uint64_t cols = h.cols;
+  msg = btsr_stream(bf, reinterpret_cast<uint8_t*>(col_idx), h.nnz * 8, st->pinned, st->pinned_ev, s,
+                    [&](const uint8_t* p, uint64_t off, size_t n) -> std::string {
+                      const uint64_t* c = reinterpret_cast<const uint64_t*>(p);
+                      for (size_t j = 0; j < n / 8; ++j) {
+                        const uint64_t i = off / 8 + j;
+                        while (rp[row + 1] <= i) ++row;
+                        if (c[j] >= cols) return "csr column index out of range";
+                        if (i > rp[row] && prev >= c[j])
+                          return "csr column indices must be strictly increasing per row";
+                        prev = c[j];
+                      }
+                      return std::string();
+                    }, &cerr);
+  if (!msg.empty()) return done(msg);
+  msg = btsr_stream(bf, reinterpret_cast<uint8_t*>(vals), h.nnz * 4, st->pinned, st->pinned_ev, s,
+                    [](const uint8_t* p, uint64_t, size_t n) -> std::string {
+                      const float* v = reinterpret_cast<const float*>(p);
+                      for (size_t i = 0; i < n / 4; ++i)
+                        if (!std::isfinite(v[i])) return "csr values must be finite";
+                      return std::string();
+                    }, &cerr);
+  const int rc = done(msg);
+  cudaStreamSynchronize(s);  // rp (pageable) must outlive its async copy
+  return rc;
 }
 
 }  // extern "C"

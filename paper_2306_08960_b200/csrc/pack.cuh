@@ -87,4 +87,34 @@ __global__ void quantize_thm_kernel(const float* __restrict__ a, long long rows,
   }
 }
 
+// ThmPlanes::validate on device (tensor.cpp:133-153), exact precedence: nonzero padding in any
+// plane wins; otherwise the first violating word in row-major order decides, and within it
+// the first failing check (1: t&h, 2: t&~m, 3: h&m). Results: *pad_bad |= 1, and
+// *first_bad = min over violating words of (word index << 2 | check).
+__global__ void validate_planes_kernel(const unsigned long long* __restrict__ t,
+                                       const unsigned long long* __restrict__ h,
+                                       const unsigned long long* __restrict__ m, long long rows,
+                                       long long cols, long long wpr, int* pad_bad,
+                                       unsigned long long* first_bad) {
+  const long long total = rows * wpr;
+  const long long full = cols / 64;
+  const int tail = static_cast<int>(cols % 64);
+  const unsigned long long keep = tail ? ((1ull << tail) - 1) : ~0ull;
+  unsigned long long best = ~0ull;
+  int pad = 0;
+  for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const unsigned long long tw = t[g], hw = h[g], mw = m[g];
+    const long long cw = g % wpr;
+    if (cw >= full) {
+      const unsigned long long all = tw | hw | mw;
+      if ((cw == full && tail) ? (all & ~keep) : all) pad = 1;
+    }
+    const int code = (tw & hw) ? 1 : (tw & ~mw) ? 2 : (hw & mw) ? 3 : 0;
+    if (code && best == ~0ull) best = (static_cast<unsigned long long>(g) << 2) | code;
+  }
+  if (pad) atomicOr(pad_bad, 1);
+  if (best != ~0ull) atomicMin(first_bad, best);
+}
+
 }  // namespace bitmm_dev
