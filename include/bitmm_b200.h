@@ -186,6 +186,17 @@ typedef struct bitmm_gemm_item {
 } bitmm_gemm_item;
 int bitmm_gemm_batch_dev(const bitmm_gemm_item* items, int count, void* stream);
 
+/* ---- Row ops, batched (kernels.hpp:29-38, kernels.cpp:120-140) ----
+ * count independent row pairs of `words` u64 each, rows contiguous:
+ *   dot_binary: out[r] = n - 2*popc(u_r ^ v_r)   (n: logical length, words_for(n) <= words)
+ *   mbm:        out[r] = popc(z_r) - 2*popc((x_r ^ y_r) & z_r)
+ * Stream-ordered; the per-row reference calls stay on the host (one launch per row would cost
+ * more than the popcounts). */
+int bitmm_dot_binary_dev(const uint64_t* u, const uint64_t* v, int64_t count, int64_t words,
+                         int64_t n, int64_t* out, void* stream);
+int bitmm_mbm_dev(const uint64_t* x, const uint64_t* y, const uint64_t* z, int64_t count,
+                  int64_t words, int64_t* out, void* stream);
+
 /* ---- ThmPlanes::validate on device (tensor.cpp:133-153) ----
  * Checks scale > 0, zero padding and legal {t,h,m} states of plane words already on the
  * device; returns BITMM_ERR_INVALID_ENCODING with the reference's message (same precedence:

@@ -1461,6 +1461,43 @@ int bitmm_gemm_batch_dev(const bitmm_gemm_item* items, int count, void* stream) 
   return run_problems(*st, probs, np, fp4, s);
 }
 
+// ---------------- row ops ----------------
+static int run_row_ops(const uint64_t* a, const uint64_t* b, const uint64_t* z, int64_t count,
+                       int64_t words, int64_t n, int64_t* out, void* stream) {
+  g_launches = 0;
+  if (count < 0 || words < 0) return fail(BITMM_ERR_INVALID_ARGUMENT, "row counts must be non-negative");
+  if (count == 0) return BITMM_OK;
+  if (!out || (words > 0 && (!a || !b))) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ProfScope ps(z ? "mbm_rows" : "dot_binary_rows", s);
+  row_ops_kernel<<<blocks_for(std::min<int64_t>(count, 64LL * st->sms) * 32, 256), 256, 0, s>>>(
+      reinterpret_cast<const unsigned long long*>(a), reinterpret_cast<const unsigned long long*>(b),
+      reinterpret_cast<const unsigned long long*>(z), count, words, n, reinterpret_cast<long long*>(out));
+  return launch_check("row_ops_kernel");
+}
+
+int bitmm_dot_binary_dev(const uint64_t* u, const uint64_t* v, int64_t count, int64_t words,
+                         int64_t n, int64_t* out, void* stream) {
+  // kernels.cpp:121-123
+  if (n < 0 || (n + 63) / 64 > words)
+    return fail(BITMM_ERR_INVALID_ARGUMENT, "logical length does not fit the row words");
+  return run_row_ops(u, v, nullptr, count, words, n, out, stream);
+}
+
+int bitmm_mbm_dev(const uint64_t* x, const uint64_t* y, const uint64_t* z, int64_t count,
+                  int64_t words, int64_t* out, void* stream) {
+  if (words > 0 && !z) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  if (words == 0) {  // mbm of empty rows is 0 (kernels.cpp:134)
+    if (count > 0 && out) {
+      BITMM_CUDA_TRY(cudaMemsetAsync(out, 0, count * 8, static_cast<cudaStream_t>(stream)));
+    }
+    return BITMM_OK;
+  }
+  return run_row_ops(x, y, z, count, words, 0, out, stream);
+}
+
 // ---------------- plane validation ----------------
 int bitmm_validate_planes_dev(const uint64_t* t, const uint64_t* h, const uint64_t* m,
                               int64_t rows, int64_t cols, int64_t wpr, float scale, void* stream) {

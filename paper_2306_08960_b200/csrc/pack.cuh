@@ -87,6 +87,37 @@ __global__ void quantize_thm_kernel(const float* __restrict__ a, long long rows,
   }
 }
 
+// Row ops (kernels.cpp:120-140), batched: one warp per row pair.
+//   dot_binary: n - 2 * popc(u ^ v)           (xor_popcount_many's int32 count, kernels.cpp:124-127)
+//   mbm:        popc(z) - 2 * popc((x ^ y) & z)
+__global__ void row_ops_kernel(const unsigned long long* __restrict__ a,
+                               const unsigned long long* __restrict__ b,
+                               const unsigned long long* __restrict__ z, long long count,
+                               long long words, long long n, long long* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (long long r = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; r < count;
+       r += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
+    long long flip = 0, act = 0;
+    for (long long i = lane; i < words; i += 32) {
+      const unsigned long long d = a[r * words + i] ^ b[r * words + i];
+      if (z != nullptr) {
+        const unsigned long long zw = z[r * words + i];
+        flip += __popcll(d & zw);
+        act += __popcll(zw);
+      } else {
+        flip += __popcll(d);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      flip += __shfl_xor_sync(0xFFFFFFFFu, flip, o);
+      act += __shfl_xor_sync(0xFFFFFFFFu, act, o);
+    }
+    if (lane == 0)
+      out[r] = z != nullptr ? act - 2 * flip : n - 2 * static_cast<long long>(static_cast<int>(flip));
+  }
+}
+
 // ThmPlanes::validate on device (tensor.cpp:133-153), exact precedence: nonzero padding in any
 // plane wins; otherwise the first violating word in row-major order decides, and within it
 // the first failing check (1: t&h, 2: t&~m, 3: h&m). Results: *pad_bad |= 1, and

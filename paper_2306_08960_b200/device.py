@@ -184,3 +184,20 @@ def quantize_thm(a: torch.Tensor, s: float, lane_bits: int = 512, stream=None):
     _raise(_lib.load().bitmm_quantize_thm_dev(_ptr(a), rows, cols, a.stride(0), s, _ptr(t), _ptr(h),
                                               _ptr(m), wpr, _stream(stream)))
     return t, h, m
+
+
+def dot_binary_rows(u: torch.Tensor, v: torch.Tensor, n: int, stream=None) -> torch.Tensor:
+    """dot_binary (kernels.cpp:120-129) for every row pair of u, v [count, words] (int64 views
+    of the packed words): n - 2*popc(u ^ v)."""
+    count, words = u.shape
+    out = torch.empty(count, dtype=torch.int64, device=u.device)
+    _raise(_lib.load().bitmm_dot_binary_dev(_ptr(u), _ptr(v), count, words, n, _ptr(out), _stream(stream)))
+    return out
+
+
+def mbm_rows(x: torch.Tensor, y: torch.Tensor, z: torch.Tensor, stream=None) -> torch.Tensor:
+    """mbm (kernels.cpp:131-140) for every row triple: popc(z) - 2*popc((x ^ y) & z)."""
+    count, words = x.shape
+    out = torch.empty(count, dtype=torch.int64, device=x.device)
+    _raise(_lib.load().bitmm_mbm_dev(_ptr(x), _ptr(y), _ptr(z), count, words, _ptr(out), _stream(stream)))
+    return out
