@@ -1,29 +1,28 @@
 // Tensor-core bitwise GEMM for sm_100a.
 //
-// The reference (proj/src/kernels.cpp:163-275) evaluates every output cell as
-// an exact integer ("units") built from xor/and + popcount over K-packed bit
-// rows, then multiplies by one float scale. On B200 there is no b1 tensor-core
-// MMA (mma.sync .b1 is emulated through IMMA on sm_100a), but
-// tcgen05.mma kind::i8 is native. This kernel therefore consumes the operands
-// after a bit -> int8 expansion (unpack.cuh):
+// The reference (proj/src/kernels.cpp:163-275) evaluates every output cell as an exact
+// integer ("units") built from xor/and + popcount over K-packed bit rows, then multiplies by
+// one float scale. sm_100a has no b1 tensor-core MMA, so the operands are
+// expanded first (unpack.cuh) and multiplied on tcgen05:
 //   1/1 : A = sign(a) in {-1,+1},  B = sign(b) in {-1,+1}   units = acc
 //   1/2 : A = sign(w) in {-1,+1},  B = level p in {0..3}   units = 2*acc
 //   2/2 : A = level p_w in {0..3}, B = level p_a in {0..3} units = 4*acc
-// with acc = sum_k A[r][k]*B[c][k] accumulated exactly in s32 TMEM.
-// The fp32-activation APB layer has its own bf16 kernel (apb_gemm.cuh); the
-// 2-bit-activation APB layer runs this kernel with the F32ACC epilogue, which
-// adds the binary part onto the residual SpMM already stored in C.
+// with acc = sum_k A[r][k]*B[c][k]. Kind::F4 (default) feeds these as packed e2m1 through
+// kind::mxf4 with unit E8M0 scale factors and fp32 accumulators, which hold every partial sum
+// exactly (|acc| <= 9*2^20 < 2^24); Kind::I8 uses kind::i8 with s32 accumulators.
 //
-// Structure (persistent; one CTA, or one CTA pair, per SM / SM pair):
-//   warp 0      : TMA producer, multi-stage smem ring of 128-byte K slices
-//   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2..5  : epilogue, TMEM -> registers -> smem transpose -> coalesced
-//                 global stores; two TMEM accumulators (2 x 256 columns) so the
-//                 epilogue of tile i overlaps the MMAs of tile i+1.
-// PAIR = true runs cta_group::2: a cluster of two CTAs owns a 256 x 256 output
-// tile; each CTA stages 128 rows of A and 128 rows of B per K slice (half the
-// operand bytes per SM of the single-CTA 128 x 256 tile) and the leader CTA
-// issues M=256 MMAs that accumulate into both CTAs' TMEM.
+// Structure (persistent; one CTA pair per cluster, cta_group::2):
+//   warp 0     : TMA producer, multi-stage smem ring of 128-byte K slices (each CTA stages
+//                128 rows of A and BN/2 rows of B; the pair's MMA reads both CTAs' halves)
+//   warp 1     : TMEM allocator + MMA issuer (leader CTA; whole warp, one elected lane issues)
+//   warps 2..5 : epilogue: TMEM -> registers (next chunk's load in flight) -> transform ->
+//                128B-swizzled smem block -> TMA bulk tensor store. Two TMEM accumulators of
+//                BN columns, so the epilogue of tile i overlaps the MMAs of tile i+1; F4 keeps
+//                its scale factors in the 64 columns after them (hence BN = 192, not 256).
+// A launch covers a group of problems (TcGroup): their tiles are concatenated, so several
+// GEMMs pay one ramp-up and one tail. The 2-bit-activation APB layer runs it with the F32R
+// epilogue (reference-order per-row scales); the fp32-activation APB layer has its own bf16
+// kernel (apb_gemm.cuh).
 #pragma once
 
 #include "ptx.cuh"
