@@ -72,7 +72,6 @@ struct TcShape {
 struct TcParams {
   int M, N;          // output rows / columns
   int num_kb;        // K blocks (of 128 bytes) walked along B
-  int a_kb_period;   // A's K block for step kb is kb % a_kb_period (bf16 split parts)
   int shift;         // integer units = acc << shift
   float scale;       // scalar multiplier (reference scale, built on the host)
   const float* row_scale;  // optional per-output-row multiplier [M]
@@ -313,9 +312,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   if (warp == 0) {
     // ===================== TMA producer (both CTAs of a pair) =====================
+    // At FP4 rates a stage lasts ~384 cycles, and this single thread issues every load, so
+    // the k-block loop is kept to a handful of instructions (no division / modulo: a
+    // dependent MUFU.RCP chain per stage starved the MMA).
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      constexpr uint32_t kTx = 2 * (S::A_STAGE + S::B_STAGE);
       for (int tile = unit; tile < num_tiles; tile += num_units) {
         const int pi = tc_problem_of(g, tile);
         const TcParams& p = g.prob[pi];
@@ -323,12 +326,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tc_tile_coords(tile - g.tile_begin[pi], p, p.num_n_blocks, mb, nb);
         const int a_row = mb * S::TILE_M + static_cast<int>(rank) * S::A_ROWS;
         const int b_row = nb * BN + static_cast<int>(rank) * S::B_ROWS;
-        for (int kb = 0; kb < p.num_kb; ++kb) {
+        const CUtensorMap* ma = &g.a[pi];
+        const CUtensorMap* mbm = &g.b[pi];
+        const int nkb = p.num_kb;
+        for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1u);
-          const int ka = kb % p.a_kb_period;
-          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (S::A_STAGE + S::B_STAGE));
-          tma_load_2d_pair(sA + stage * S::A_STAGE, &g.a[pi], &full[stage], ka * BK_ELEMS, a_row);
-          tma_load_2d_pair(sB + stage * S::B_STAGE, &g.b[pi], &full[stage], kb * BK_ELEMS, b_row);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], kTx);
+          tma_load_2d_pair(sA + stage * S::A_STAGE, ma, &full[stage], kb * BK_ELEMS, a_row);
+          tma_load_2d_pair(sB + stage * S::B_STAGE, mbm, &full[stage], kb * BK_ELEMS, b_row);
           if (++stage == S::STAGES) {
             stage = 0;
             phase ^= 1u;

@@ -121,21 +121,22 @@ int run(const CUtensorMap& ma, const CUtensorMap& mb, unsigned long long* d, int
   return 0;
 }
 
+static void fill(uint8_t* buf, size_t n, const unsigned char* codes) {
+  unsigned char* h = static_cast<unsigned char*>(malloc(n));
+  unsigned long long x = 88172645463325252ull;
+  for (size_t i = 0; i < n; ++i) {
+    x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+    h[i] = static_cast<unsigned char>(codes[x & 7] | (codes[(x >> 3) & 7] << 4));
+  }
+  cudaMemcpy(buf, h, n, cudaMemcpyHostToDevice);
+  free(h);
+}
+
 int main() {
   const int rows = 8192, cols = 2048;
   uint8_t* buf = nullptr;
   if (cudaMalloc(&buf, size_t(rows) * cols) != cudaSuccess) return 1;
-  {  // random e2m1 nibbles (+-1 and levels 0..3 codes), like the GEMM's operands
-    const unsigned char codes[8] = {0x0, 0x2, 0x4, 0x5, 0xA, 0x2, 0xA, 0x4};
-    unsigned char* h = static_cast<unsigned char*>(malloc(size_t(rows) * cols));
-    unsigned long long x = 88172645463325252ull;
-    for (size_t i = 0; i < size_t(rows) * cols; ++i) {
-      x ^= x << 13; x ^= x >> 7; x ^= x << 17;
-      h[i] = static_cast<unsigned char>(codes[x & 7] | (codes[(x >> 3) & 7] << 4));
-    }
-    cudaMemcpy(buf, h, size_t(rows) * cols, cudaMemcpyHostToDevice);
-    free(h);
-  }
+
   void* fn = nullptr; cudaDriverEntryPointQueryResult q;
   if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) return 2;
   Enc enc = reinterpret_cast<Enc>(fn);
@@ -149,9 +150,17 @@ int main() {
           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) return 4;
   unsigned long long* d = nullptr;
   cudaMalloc(&d, 8);
-  for (int rep = 0; rep < 2; ++rep) {
-    run<7, false>(ma, mb, d, 74);
-    run<7, true>(ma, mb, d, 74);
-  }
+  const unsigned char pm1[8] = {0x2, 0xA, 0x2, 0xA, 0x2, 0xA, 0x2, 0xA};   // random +-1
+  const unsigned char b01[8] = {0x0, 0x2, 0x0, 0x2, 0x0, 0x2, 0x0, 0x2};   // random {0,1}
+  const unsigned char lv[8] = {0x0, 0x2, 0x4, 0x5, 0x0, 0x2, 0x4, 0x5};    // random levels 0..3
+  const unsigned char cst[8] = {0x2, 0x2, 0x2, 0x2, 0x2, 0x2, 0x2, 0x2};   // constant 1.0
+  const unsigned char* pats[4] = {pm1, b01, lv, cst};
+  const char* names[4] = {"+-1", "{0,1}", "levels", "const"};
+  for (int rep = 0; rep < 2; ++rep)
+    for (int p = 0; p < 4; ++p) {
+      fill(buf, size_t(rows) * cols, pats[p]);
+      printf("%-7s ", names[p]);
+      run<7, true>(ma, mb, d, 74);
+    }
   return 0;
 }
