@@ -346,7 +346,8 @@ int run_tc_group(DeviceState& st, const GemmProblem* probs, int count, cudaStrea
     p.M = static_cast<int>(q.m);
     p.N = static_cast<int>(q.n);
     p.num_kb = static_cast<int>(rb / TC_BK_BYTES);
-    p.small_acc = (9 * q.kpad < (1 << 22)) ? 1 : 0;  // |acc| <= 9K: magic-add float -> int
+    // |acc| <= 9K, so |units| = |acc| << shift < 2^22 allows the magic-add float -> int
+    p.small_acc = ((9 * q.kpad) << p.shift) < (int64_t{1} << 22) ? 1 : 0;
     p.shift_mul = static_cast<float>(1 << p.shift);
     p.num_m_blocks = static_cast<int>((q.m + S::TILE_M - 1) / S::TILE_M);
     p.num_n_blocks = static_cast<int>((q.n + BN - 1) / BN);

@@ -134,40 +134,50 @@ __device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, const CUtens
       if (lane == 0) bulk_wait_group_read<EPI_BUFS - 1>();
       __syncwarp();
     }
+    // Transform f(i) of the 32 columns, staged as four-word groups.
+    auto stage = [&](auto f) {
 #pragma unroll
-    for (int j = 0; j < 32; j += 4) {
-      float4 o;
-      float* of = reinterpret_cast<float*>(&o);
+      for (int j = 0; j < 32; j += 4) {
+        float4 o;
+        float* of = reinterpret_cast<float*>(&o);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        if constexpr (F32ACC) {
-          // fp32 accumulator holding an exact integer acc; units = acc << shift
-          const float acc = __uint_as_float(v[j + e]);
-          if constexpr (EPI == Epi::I32) {
-            const int iacc = p.small_acc ? (__float_as_int(__fadd_rn(acc, 12582912.0f)) - 0x4B400000)
-                                         : __float2int_rn(acc);
-            of[e] = __int_as_float(iacc << p.shift);
-          } else {
-            const float units = __fmul_rn(acc, p.shift_mul);  // exact: x 1, 2 or 4
-            float s = row_mul;
-            if constexpr (EPI == Epi::F32) {
-              if (cs != nullptr) s = __fmul_rn(s, cs[c * 32 + j + e]);
-            }
-            of[e] = __fmul_rn(s, units);
-          }
-        } else if constexpr (EPI == Epi::I32) {
-          of[e] = __int_as_float(static_cast<int>(v[j + e]) << p.shift);
-        } else if constexpr (EPI == Epi::F32) {
-          const float units = static_cast<float>(static_cast<int>(v[j + e]) << p.shift);
-          float s = row_mul;
-          if (cs != nullptr) s = __fmul_rn(s, cs[c * 32 + j + e]);
-          of[e] = __fmul_rn(s, units);
-        } else {
-          of[e] = __fmul_rn(row_mul, static_cast<float>(static_cast<int>(v[j + e]) << p.shift));
-        }
+        for (int e = 0; e < 4; ++e) of[e] = f(j + e);
+        const int off = p.tma_store ? lane * 32 + (((j >> 2) ^ (lane & 7)) << 2) : lane * TC_EPI_STRIDE + j;
+        *reinterpret_cast<float4*>(&sb[off]) = o;
       }
-      const int off = p.tma_store ? lane * 32 + (((j >> 2) ^ (lane & 7)) << 2) : lane * TC_EPI_STRIDE + j;
-      *reinterpret_cast<float4*>(&sb[off]) = o;
+    };
+    if constexpr (F32ACC && EPI == Epi::I32) {
+      // fp32 accumulator holding an exact integer acc; units = acc * 2^shift, exact in fp32.
+      // Small accumulators (|units| < 2^22) convert with one FFMA magic add (1.5 * 2^23) and
+      // one integer subtract; the branch is uniform, outside the element loop.
+      if (p.small_acc) {
+        stage([&](int i) {
+          return __int_as_float(__float_as_int(__fmaf_rn(__uint_as_float(v[i]), p.shift_mul, 12582912.0f)) -
+                                0x4B400000);
+        });
+      } else {
+        stage([&](int i) { return __int_as_float(__float2int_rn(__fmul_rn(__uint_as_float(v[i]), p.shift_mul))); });
+      }
+    } else if constexpr (F32ACC) {
+      stage([&](int i) {
+        const float units = __fmul_rn(__uint_as_float(v[i]), p.shift_mul);  // exact: x 1, 2 or 4
+        float s = row_mul;
+        if constexpr (EPI == Epi::F32) {
+          if (cs != nullptr) s = __fmul_rn(s, cs[c * 32 + i]);
+        }
+        return __fmul_rn(s, units);
+      });
+    } else if constexpr (EPI == Epi::I32) {
+      stage([&](int i) { return __int_as_float(static_cast<int>(v[i]) << p.shift); });
+    } else if constexpr (EPI == Epi::F32) {
+      stage([&](int i) {
+        const float units = static_cast<float>(static_cast<int>(v[i]) << p.shift);
+        float s = row_mul;
+        if (cs != nullptr) s = __fmul_rn(s, cs[c * 32 + i]);
+        return __fmul_rn(s, units);
+      });
+    } else {
+      stage([&](int i) { return __fmul_rn(row_mul, static_cast<float>(static_cast<int>(v[i]) << p.shift)); });
     }
     if (p.tma_store) {
       fence_proxy_async_smem();
@@ -224,6 +234,11 @@ __device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, const CUtens
 // persistent grid walks the concatenation of their tiles, so a step of several GEMMs pays one
 // ramp-up and one tail instead of one per GEMM.
 constexpr int TC_GROUP_MAX = 4;
+#ifdef TC_GEMM_STATS
+// Profiling build only (profiles/micro/real_kernel.cu): cycles per CTA the MMA issuer waits on
+// tempty [0] / full [1] and its total [2]; epilogue warp 2 waiting on tfull [3] / draining [4].
+__device__ unsigned long long tcg_stats[6][160];
+#endif
 
 template <int NP>
 struct TcGroup {
@@ -245,7 +260,12 @@ __device__ __forceinline__ int tc_problem_of(const TcGroup<NP>& g, int t) {
 
 // Persistent cta_group::2 GEMM (one CTA pair per cluster). EPI == Epi::ANY dispatches each
 // problem's epilogue (I32 or F32) at run time.
-template <Kind KIND, Epi EPI, int BN, int NP>
+// MC = CTA pairs per cluster. MC = 2 (measured, not used by the library: DESIGN.md) runs two
+// pairs of a four-CTA cluster on horizontally adjacent tiles; each pair loads half of the
+// shared A rows and multicasts it to the same-rank CTA of the other pair, and every stage
+// release is committed to all four CTAs. The host then builds the A map with A_ROWS / 2-row
+// boxes, counts tiles in pairs of N blocks and launches clusters of four.
+template <Kind KIND, Epi EPI, int BN, int NP, int MC = 1>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ TcGroup<NP> g) {
   using S = TcShape<true, BN>;
@@ -264,7 +284,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();  // rank within the CTA pair
+  const uint32_t crank = cluster_ctarank();
+  const uint32_t rank = crank & 1u;               // rank within the CTA pair
+  const int pair = static_cast<int>(crank >> 1);  // pair within the cluster (MC = 2)
   const int unit = static_cast<int>(cluster_id_x());
   const int num_units = static_cast<int>(num_clusters_x());
   const int num_tiles = g.tile_begin[g.count];
@@ -277,7 +299,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int s = 0; s < S::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC);  // one release per pair of the cluster
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -323,7 +345,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int pi = tc_problem_of(g, tile);
         const TcParams& p = g.prob[pi];
         int mb, nb;
-        tc_tile_coords(tile - g.tile_begin[pi], p, p.num_n_blocks, mb, nb);
+        tc_tile_coords(tile - g.tile_begin[pi], p, (p.num_n_blocks + MC - 1) / MC, mb, nb);
+        nb = nb * MC + pair;
         const int a_row = mb * S::TILE_M + static_cast<int>(rank) * S::A_ROWS;
         const int b_row = nb * BN + static_cast<int>(rank) * S::B_ROWS;
         const CUtensorMap* ma = &g.a[pi];
@@ -332,7 +355,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1u);
           if (rank == 0) mbar_arrive_expect_tx(&full[stage], kTx);
-          tma_load_2d_pair(sA + stage * S::A_STAGE, ma, &full[stage], kb * BK_ELEMS, a_row);
+          if constexpr (MC == 2) {
+            // this pair's half of the A rows, to this CTA and its twin in the other pair
+            constexpr int HALF = S::A_ROWS / 2;
+            tma_load_2d_pair_mc(sA + stage * S::A_STAGE + pair * HALF * TC_BK_BYTES, ma, &full[stage],
+                                kb * BK_ELEMS, a_row + pair * HALF, static_cast<uint16_t>(0x5u << rank));
+          } else {
+            tma_load_2d_pair(sA + stage * S::A_STAGE, ma, &full[stage], kb * BK_ELEMS, a_row);
+          }
           tma_load_2d_pair(sB + stage * S::B_STAGE, mbm, &full[stage], kb * BK_ELEMS, b_row);
           if (++stage == S::STAGES) {
             stage = 0;
@@ -356,29 +386,51 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
+#ifdef TC_GEMM_STATS
+      long long st_te = 0, st_fu = 0, st_start = clock64();
+#endif
       for (int tile = unit; tile < num_tiles; tile += num_units, ++it) {
         const int num_kb = g.prob[tc_problem_of(g, tile)].num_kb;
         const int acc = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
+#ifdef TC_GEMM_STATS
+        long long t0 = clock64();
+#endif
         mbar_wait(&tempty[acc], aphase ^ 1u);
+#ifdef TC_GEMM_STATS
+        st_te += clock64() - t0;
+#endif
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
+#ifdef TC_GEMM_STATS
+          long long t1 = clock64();
+#endif
           mbar_wait(&full[stage], phase);
+#ifdef TC_GEMM_STATS
+          st_fu += clock64() - t1;
+#endif
           tc_fence_after();
           const uint64_t ad = a_desc0 + static_cast<uint64_t>((stage * S::A_STAGE) >> 4);
           const uint64_t bd = b_desc0 + static_cast<uint64_t>((stage * S::B_STAGE) >> 4);
 #pragma unroll
           for (int k = 0; k < TC_BK_BYTES / 32; ++k)
             mma_pair_elect<KID>(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0, sfa, sfb);
-          mma_commit_pair_elect(&empty[stage], 0x3);
+          mma_commit_pair_elect(&empty[stage], MC == 2 ? 0xF : 0x3);
           if (++stage == S::STAGES) {
             stage = 0;
             phase ^= 1u;
           }
         }
-        mma_commit_pair_elect(&tfull[acc], 0x3);
+        mma_commit_pair_elect(&tfull[acc], static_cast<uint16_t>(0x3u << (2 * pair)));
       }
+#ifdef TC_GEMM_STATS
+      if (lane == 0) {
+        tcg_stats[0][blockIdx.x] = st_te;
+        tcg_stats[1][blockIdx.x] = st_fu;
+        tcg_stats[2][blockIdx.x] = clock64() - st_start;
+      }
+#endif
     }
   } else {
     // ===================== epilogue (warps 2..5 of every CTA) =====================
@@ -386,14 +438,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     float* stg = sEpi + (warp - 2) * (S::EPI_WARP_BYTES / 4);
     uint32_t buf = 0;
     int it = 0;
+#ifdef TC_GEMM_STATS
+    long long st_tf = 0, st_busy = 0;
+#endif
     for (int tile = unit; tile < num_tiles; tile += num_units, ++it) {
       const int pi = tc_problem_of(g, tile);
       const TcParams p = g.prob[pi];  // by value: its fields stay in registers in the epilogue
       int mb, nb;
-      tc_tile_coords(tile - g.tile_begin[pi], p, p.num_n_blocks, mb, nb);
+      tc_tile_coords(tile - g.tile_begin[pi], p, (p.num_n_blocks + MC - 1) / MC, mb, nb);
+      nb = nb * MC + pair;
       const int acc = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
+#ifdef TC_GEMM_STATS
+      long long t2 = clock64();
+#endif
       mbar_wait(&tfull[acc], aphase);
+#ifdef TC_GEMM_STATS
+      long long t3 = clock64();
+      st_tf += t3 - t2;
+#endif
       tc_fence_after();
       const int row_base = mb * S::TILE_M + static_cast<int>(rank) * 128 + quad * 32;
       constexpr bool kF32Acc = KIND == Kind::F4;
@@ -421,9 +484,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tc_epilogue_tile<EPI, BN, kF32Acc, S::EPI_BUFS>(p, &g.c[pi], tacc, quad, lane, row_base,
                                                         nb * BN, stg, buf, cs);
       }
+#ifdef TC_GEMM_STATS
+      st_busy += clock64() - t3;
+#endif
       tc_fence_before();
       mbar_arrive_cluster(smem_u32(&tempty[acc]) & kPeerBitMask);
     }
+#ifdef TC_GEMM_STATS
+    if (lane == 0 && warp == 2) {
+      tcg_stats[3][blockIdx.x] = st_tf;
+      tcg_stats[4][blockIdx.x] = st_busy;
+    }
+#endif
     if (lane == 0) bulk_wait_group_all();  // stores land before the grid ends
   }
 

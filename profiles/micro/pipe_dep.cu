@@ -12,7 +12,10 @@ constexpr int MAXST = 7, SMEM = MAXST * STAGE + 2048;
 
 // TILES: every 16 stages the MMA switches between two accumulators (waiting for the epilogue
 // warps 2..5 of both CTAs to release it) and commits the finished one, like the GEMM.
-template <int STAGES, bool TILES = false>
+// WALK: like the GEMM's persistent schedule, the rows change every 16 stages (tile t of this
+// pair = unit + t * num_units over a 32 x 42 tile grid of 8192-row operands).
+// SPLIT: all A stages, then all B stages (the GEMM's smem layout) instead of A|B per stage.
+template <int STAGES, bool TILES = false, int SFCOL = 448, bool WALK = false, bool SPLIT = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     k_pipe(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb, int iters,
            unsigned long long* cycles) {
@@ -37,20 +40,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   const uint32_t tmem = *slot;
   if (warp >= 2) {
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    tmem_st_32x32b_x32_fill(tmem + lane_off + 448, 0x7F7F7F7Fu);
-    tmem_st_32x32b_x32_fill(tmem + lane_off + 480, 0x7F7F7F7Fu);
+    tmem_st_32x32b_x32_fill(tmem + lane_off + SFCOL, 0x7F7F7F7Fu);
+    tmem_st_32x32b_x32_fill(tmem + lane_off + SFCOL + 32, 0x7F7F7F7Fu);
     tmem_st_wait();
   }
   tc_fence_before(); cluster_sync(); tc_fence_after();
   const long long t0 = clock64();
   if (warp == 0 && lane == 0) {
     int st = 0; uint32_t ph = 0;
-    const int arow = (blockIdx.x * 128) % 8192, brow = (blockIdx.x * 96) % 8064;
+    int arow = (blockIdx.x * 128) % 8192, brow = (blockIdx.x * 96) % 8064;
     for (int it = 0; it < iters; ++it) {
+      if (WALK && (it % 16) == 0) {
+        const int tile = static_cast<int>(blockIdx.x >> 1) + (it / 16) * static_cast<int>(gridDim.x >> 1);
+        const int mb = tile % 32, nb = (tile / 32) % 42;
+        arow = mb * 256 + static_cast<int>(rank) * 128;
+        brow = 8192 + nb * 192 + static_cast<int>(rank) * 96;
+      }
       mbar_wait(&empty[st], ph ^ 1u);
       if (rank == 0) mbar_arrive_expect_tx(&full[st], 2 * STAGE);
-      tma_load_2d_pair(smem + st * STAGE, &ma, &full[st], (it % 16) * 128, arow);
-      tma_load_2d_pair(smem + st * STAGE + A_BYTES, &mb, &full[st], (it % 16) * 128, brow);
+      uint8_t* da = SPLIT ? smem + st * A_BYTES : smem + st * STAGE;
+      uint8_t* db = SPLIT ? smem + STAGES * A_BYTES + st * B_BYTES : smem + st * STAGE + A_BYTES;
+      tma_load_2d_pair(da, &ma, &full[st], (it % 16) * 128, arow);
+      tma_load_2d_pair(db, &mb, &full[st], (it % 16) * 128, brow);
       if (++st == STAGES) { st = 0; ph ^= 1u; }
     }
   } else if (warp == 1 && rank == 0) {
@@ -65,11 +76,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       }
       mbar_wait(&full[st], ph);
       tc_fence_after();
-      const uint64_t ad = d0 + static_cast<uint64_t>((st * STAGE) >> 4);
-      const uint64_t bd = ad + (A_BYTES >> 4);
+      const uint64_t ad = SPLIT ? d0 + static_cast<uint64_t>((st * A_BYTES) >> 4)
+                                : d0 + static_cast<uint64_t>((st * STAGE) >> 4);
+      const uint64_t bd = SPLIT ? d0 + static_cast<uint64_t>((STAGES * A_BYTES + st * B_BYTES) >> 4)
+                                : ad + (A_BYTES >> 4);
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        mma_pair_elect<2>(tmem + acc * 192, ad + 2 * k, bd + 2 * k, idesc, (it % 16) | k, tmem + 448, tmem + 480);
+        mma_pair_elect<2>(tmem + acc * 192, ad + 2 * k, bd + 2 * k, idesc, (it % 16) | k, tmem + SFCOL, tmem + SFCOL + 32);
       mma_commit_pair_elect(&empty[st], 0x3);
       if (TILES && (it % 16) == 15) mma_commit_pair_elect(&tfull[acc], 0x3);
       if (++st == STAGES) { st = 0; ph ^= 1u; }
@@ -93,29 +106,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   if (warp == 1) { tc_fence_after(); tmem_dealloc_pair(tmem, 512); }
 }
 
+// Rewrites the operand buffer on the device right before the timed kernel (like the unpack).
+__global__ void rewrite(uint4* buf, size_t n16) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n16;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    uint4 v = buf[i];
+    buf[i] = make_uint4(v.y, v.x, v.w, v.z);  // still +-1 nibbles
+  }
+}
+static uint8_t* g_buf = nullptr;
+static size_t g_bytes = 0;
+static bool g_rewrite = false;
+static int g_iters = 65536;
+
 typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                         const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                         CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-template <int STAGES, bool TILES = false>
+template <int STAGES, bool TILES = false, int SFCOL = 448, bool WALK = false, bool SPLIT = false>
 int run(const CUtensorMap& ma, const CUtensorMap& mb, unsigned long long* d, int clusters) {
-  if (cudaFuncSetAttribute(k_pipe<STAGES, TILES>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess) return 5;
-  const int iters = 65536;
+  if (cudaFuncSetAttribute(k_pipe<STAGES, TILES, SFCOL, WALK, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess) return 5;
+  const int iters = g_iters;
   cudaMemset(d, 0, 8);
-  k_pipe<STAGES, TILES><<<2 * clusters, 192, SMEM>>>(ma, mb, 64, d);
+  k_pipe<STAGES, TILES, SFCOL, WALK, SPLIT><<<2 * clusters, 192, SMEM>>>(ma, mb, 64, d);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("warmup error %s\n", cudaGetErrorString(e)); return 6; }
   cudaMemset(d, 0, 8);
+  if (g_rewrite) rewrite<<<1184, 256>>>(reinterpret_cast<uint4*>(g_buf), g_bytes / 16);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  k_pipe<STAGES, TILES><<<2 * clusters, 192, SMEM>>>(ma, mb, iters, d);
+  k_pipe<STAGES, TILES, SFCOL, WALK, SPLIT><<<2 * clusters, 192, SMEM>>>(ma, mb, iters, d);
   cudaEventRecord(e1);
   e = cudaDeviceSynchronize();
   float ms = 0; cudaEventElapsedTime(&ms, e0, e1);
   unsigned long long cyc = 0;
   cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
   const double cyc_per_cluster = double(cyc) / clusters;
-  printf("tiles=%d stages=%d clusters=%2d: %.1f cycles per MMA (ideal 96), %.0f TMAC/s wall, clock %.0f MHz %s\n", int(TILES), STAGES,
+  printf("iters=%d rewrite=%d split=%d walk=%d sf=%d tiles=%d stages=%d clusters=%2d: %.1f cycles per MMA (ideal 96), %.0f TMAC/s wall, clock %.0f MHz %s\n", g_iters, int(g_rewrite), int(SPLIT), int(WALK), SFCOL, int(TILES), STAGES,
          clusters, cyc_per_cluster / (iters * 4.0), double(clusters) * iters * 4 * 256.0 * N * 64 / (ms * 1e-3) / 1e12,
          cyc_per_cluster / (ms * 1e3), cudaGetErrorString(e));
   return 0;
@@ -133,7 +160,7 @@ static void fill(uint8_t* buf, size_t n, const unsigned char* codes) {
 }
 
 int main() {
-  const int rows = 8192, cols = 2048;
+  const int rows = 16384, cols = 2048;  // A rows [0,8192), B rows [8192,16384) in the walk
   uint8_t* buf = nullptr;
   if (cudaMalloc(&buf, size_t(rows) * cols) != cudaSuccess) return 1;
 
@@ -156,11 +183,17 @@ int main() {
   const unsigned char cst[8] = {0x2, 0x2, 0x2, 0x2, 0x2, 0x2, 0x2, 0x2};   // constant 1.0
   const unsigned char* pats[4] = {pm1, b01, lv, cst};
   const char* names[4] = {"+-1", "{0,1}", "levels", "const"};
-  for (int rep = 0; rep < 2; ++rep)
-    for (int p = 0; p < 4; ++p) {
-      fill(buf, size_t(rows) * cols, pats[p]);
-      printf("%-7s ", names[p]);
-      run<7, true>(ma, mb, d, 74);
+  fill(buf, size_t(rows) * cols, pm1);
+  g_buf = buf;
+  g_bytes = size_t(rows) * cols;
+  for (int it : {65536, 304}) {
+    g_iters = it;
+    for (int rep = 0; rep < 2; ++rep) {
+      g_rewrite = false;
+      run<7, true, 448, true, true>(ma, mb, d, 74);
+      g_rewrite = true;
+      run<7, true, 448, true, true>(ma, mb, d, 74);
     }
+  }
   return 0;
 }
