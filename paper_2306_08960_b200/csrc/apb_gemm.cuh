@@ -1,26 +1,28 @@
 // APB layer forward (apb.cpp:158-164): C = alpha_r * (sign(bin) . X) + residual . X.
 //
-// Two kernels, chained with programmatic dependent launch:
+// Two kernels, chained with programmatic dependent launch (the GEMM runs first):
 //
 // 1. spmm_xchunk_kernel — the sparse full-precision residual (spmm_csr,
-//    kernels.cpp:334-352). A block stages an X column chunk [K][64] fp32 in shared
-//    memory (coalesced, read once from L2), then walks CSR rows: a half-warp owns one
+//    kernels.cpp:334-352). A block stages an X column chunk [K][32] fp32 in shared
+//    memory (coalesced, read once from L2), then walks CSR rows: an 8-lane octet owns one
 //    output row, lane l owns 4 consecutive columns, nonzeros are broadcast with
-//    half-warp shuffles and accumulated in col_idx order. It writes R.X into C.
-//    EXACT = true reproduces the reference's rounding (separate fp32 multiply and add,
-//    in order); the fused layer uses fma.
+//    octet shuffles and accumulated in col_idx order. ACCUM adds R.X onto C (the layer);
+//    otherwise it writes R.X (spmm_csr). EXACT = true reproduces the reference's rounding
+//    (separate fp32 multiply and add, in order); the layer uses fma for R.X.
 //
 // 2. apb_gemm_kernel — the binary part on the tensor cores, cta_group::2 (a CTA pair
-//    owns 256 output rows x 128 columns). A = sign(bin) as bf16 +-1 (exact); B = X^T
-//    split into three bf16 parts x = hi + mid + lo (exact, unpack.cuh). One smem stage
-//    holds one 64-wide K slice of A and of all three B parts, so A is fetched once per
-//    slice. The hi products accumulate in one TMEM accumulator and the mid+lo products
-//    in a second one: the tensor core's fp32 accumulation truncates small addends
-//    against a large running sum, and keeping the magnitudes apart removes that bias
-//    (measured: 3e-6 -> ~1e-7 relative at K=768). TMEM holds 2 tiles x 2 accumulators
-//    x 128 columns = 512 columns, so the epilogue of tile i overlaps the MMAs of i+1.
-//    Epilogue: C = fma(alpha_r, hi + lo, C) with C holding R.X from kernel 1
-//    (= the reference's bin_part + res_part, apb.cpp:161-162, up to rounding).
+//    owns 256 output rows x 128 columns). A = sign(bin) as fp16 +-1 (exact); B = X^T
+//    scaled per token by 2^e_n and split into two fp16 parts x * 2^e_n = hi + lo
+//    (split_x_f16, unpack.cuh; 22 significant bits). One smem stage holds one 64-wide K
+//    slice of A and of both B parts, so A is fetched once per slice. The hi products
+//    accumulate in one TMEM accumulator and the lo products in a second one: the tensor
+//    core's fp32 accumulation truncates small addends against a large running sum, and
+//    keeping the magnitudes apart removes that bias (measured: 3e-6 -> ~1e-7 relative at
+//    K=768). TMEM holds 2 tiles x 2 accumulators x 128 columns = 512 columns, so the
+//    epilogue of tile i overlaps the MMAs of i+1. Two fp16 parts at the f16 rate replace
+//    three bf16 parts (the earlier bf16x3 split): 2 MMAs per update instead of 3.
+//    Epilogue: C = (alpha_r * (hi + lo)) * 2^-e_n, stored; kernel 1 then adds R.X onto C
+//    (C = bin_part + res_part, apb.cpp:161-162).
 #pragma once
 
 #include "ptx.cuh"
@@ -57,9 +59,9 @@ struct SpmmLevels {
   float d1, d2, d3;  // d0 = 0
 };
 
-// LEVELS also accumulates: the 2-bit layer's GEMM has already stored the binary part in C,
-// and each output row becomes C = bin + R.D (apb.cpp:161-162; fp32 add commutes).
-template <bool EXACT, bool PDL_CHAIN, bool LEVELS>
+// ACCUM (both layers): the GEMM has already stored the binary part in C, and each output
+// row becomes C = bin + R.X (apb.cpp:161-162; fp32 add commutes).
+template <bool EXACT, bool PDL_CHAIN, bool LEVELS, bool ACCUM = LEVELS>
 __global__ void __launch_bounds__(SPMM_THREADS, 2)
     spmm_xchunk_kernel(int rows, int K, int N, const unsigned long long* __restrict__ row_ptr,
                        const unsigned long long* __restrict__ col_idx,
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(SPMM_THREADS, 2)
     const unsigned nmax = __reduce_max_sync(0xFFFFFFFFu, n);
     float* dst = C + static_cast<long long>(r) * ldc + col;
     float prev[4] = {0.f, 0.f, 0.f, 0.f};
-    if (LEVELS && live) {  // issued before the nonzero loop so its latency overlaps it
+    if (ACCUM && live) {  // issued before the nonzero loop so its latency overlaps it
       if (vec && col + 3 < N) {
         const float4 p4 = *reinterpret_cast<const float4*>(dst);
         prev[0] = p4.x; prev[1] = p4.y; prev[2] = p4.z; prev[3] = p4.w;
@@ -228,7 +230,7 @@ __global__ void __launch_bounds__(SPMM_THREADS, 2)
       fetch(i0, n, base + ol, kk, vv);
       step8(kk, vv, acc);
     }
-    if (LEVELS) {
+    if (ACCUM) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[e] = __fadd_rn(prev[e], acc[e]);
     }
@@ -272,11 +274,11 @@ __global__ void dequant_levels_kernel(const SpmmLevels lv, int K, int N, float* 
 
 // ----------------------------------------------------------------------------------
 constexpr int APB_BN = 128;        // output columns per pair tile
-constexpr int APB_PARTS = 3;       // bf16 split parts of X
-constexpr int APB_STAGES = 5;
-constexpr int APB_A_STAGE = 128 * TC_BK_BYTES;                       // 128 rows x 64 bf16
-constexpr int APB_B_PART = (APB_BN / 2) * TC_BK_BYTES;               // 64 rows x 64 bf16
-constexpr int APB_STAGE = APB_A_STAGE + APB_PARTS * APB_B_PART;      // 40 KB
+constexpr int APB_PARTS = 2;       // fp16 split parts of X (hi, lo)
+constexpr int APB_STAGES = 6;
+constexpr int APB_A_STAGE = 128 * TC_BK_BYTES;                       // 128 rows x 64 fp16
+constexpr int APB_B_PART = (APB_BN / 2) * TC_BK_BYTES;               // 64 rows x 64 fp16
+constexpr int APB_STAGE = APB_A_STAGE + APB_PARTS * APB_B_PART;      // 32 KB
 constexpr int APB_EPI_BYTES = 4 * 32 * TC_EPI_STRIDE * 4;
 constexpr int APB_SMEM = 1024 + APB_STAGES * APB_STAGE + APB_EPI_BYTES + (2 * APB_STAGES + 4) * 8 + 16;
 
@@ -285,9 +287,9 @@ struct ApbParams {
   int kpad;                  // elements per part row segment
   float alpha;               // scalar alpha (row_alpha == nullptr)
   const float* row_alpha;
-  float* C;                  // holds R.X on entry (accumulate_c), the layer output on exit
+  const float* tok_scale;    // per output column 2^-e_n (split_x_f16)
+  float* C;                  // C = alpha_r * S.X (the residual SpMM then adds R.X onto C)
   long long ldc;
-  int accumulate_c;          // 1: C += alpha*S.X (residual already in C); 0: C = alpha*S.X
   int num_m_blocks, num_n_blocks, num_tiles;
 };
 
@@ -369,7 +371,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
-      constexpr uint32_t idesc = make_idesc(1u, 1u, 1u, 256, APB_BN);
+      constexpr uint32_t idesc = make_idesc(1u, 0u, 0u, 256, APB_BN);  // f32 <- f16 x f16
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -422,45 +424,34 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                                    : p.alpha;
       const uint32_t t_hi = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + buf * 2 * APB_BN;
       const int cl = (lane & 7) * 4;
-      // C (= R.X) for chunk c is loaded one chunk ahead: 8 independent 16-byte loads per
-      // lane in flight while the previous chunk is drained from TMEM and stored.
-      float4 cin[8], cnext[8];
-      auto load_c = [&](int c, float4 (&dst)[8]) {
-#pragma unroll
-        for (int r8 = 0; r8 < 8; ++r8) {
-          const int grow = row_base + r8 * 4 + (lane >> 3);
-          const int gcol = nb * APB_BN + c * 32 + cl;
-          dst[r8] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (p.accumulate_c && grow < p.M && gcol < p.N) {
-            const float* src = p.C + static_cast<long long>(grow) * p.ldc + gcol;
-            if (vec_ok && gcol + 3 < p.N) {
-              dst[r8] = *reinterpret_cast<const float4*>(src);
-            } else {
-              float* df = reinterpret_cast<float*>(&dst[r8]);
-              for (int e = 0; e < 4; ++e)
-                if (gcol + e < p.N) df[e] = src[e];
-            }
-          }
-        }
-      };
-      load_c(0, cin);
 #pragma unroll 1
       for (int c = 0; c < APB_BN / 32; ++c) {
         const int col0 = nb * APB_BN + c * 32;
         if (col0 >= p.N) break;
-        if (c + 1 < APB_BN / 32) load_c(c + 1, cnext);
         uint32_t vh[32], vl[32];
         tmem_ld_32x32b_x32(t_hi + c * 32, vh);
         tmem_ld_32x32b_x32(t_hi + APB_BN + c * 32, vl);
+        // the chunk's 32 token scales: same address in every lane (broadcast); past N: 0
+        float ts[32];
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          if (col0 + j + 3 < p.N) {
+            const float4 t4 = __ldg(reinterpret_cast<const float4*>(p.tok_scale + col0 + j));
+            ts[j] = t4.x; ts[j + 1] = t4.y; ts[j + 2] = t4.z; ts[j + 3] = t4.w;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) ts[j + e] = (col0 + j + e < p.N) ? p.tok_scale[col0 + j + e] : 0.f;
+          }
+        }
         tmem_ld_wait();
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
-          float4 o;
-          o.x = __fmul_rn(alpha, __fadd_rn(__uint_as_float(vh[j + 0]), __uint_as_float(vl[j + 0])));
-          o.y = __fmul_rn(alpha, __fadd_rn(__uint_as_float(vh[j + 1]), __uint_as_float(vl[j + 1])));
-          o.z = __fmul_rn(alpha, __fadd_rn(__uint_as_float(vh[j + 2]), __uint_as_float(vl[j + 2])));
-          o.w = __fmul_rn(alpha, __fadd_rn(__uint_as_float(vh[j + 3]), __uint_as_float(vl[j + 3])));
-          *reinterpret_cast<float4*>(&stg[lane * TC_EPI_STRIDE + j]) = o;
+          float of[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)  // x 2^-e_n is exact
+            of[e] = __fmul_rn(__fmul_rn(alpha, __fadd_rn(__uint_as_float(vh[j + e]), __uint_as_float(vl[j + e]))),
+                              ts[j + e]);
+          *reinterpret_cast<float4*>(&stg[lane * TC_EPI_STRIDE + j]) = make_float4(of[0], of[1], of[2], of[3]);
         }
         __syncwarp();
 #pragma unroll
@@ -469,12 +460,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const int grow = row_base + rl;
           const int gcol = col0 + cl;
           if (grow < p.M && gcol < p.N) {
-            const float4 b = *reinterpret_cast<const float4*>(&stg[rl * TC_EPI_STRIDE + cl]);
-            float4 r;
-            r.x = __fadd_rn(b.x, cin[r8].x);
-            r.y = __fadd_rn(b.y, cin[r8].y);
-            r.z = __fadd_rn(b.z, cin[r8].z);
-            r.w = __fadd_rn(b.w, cin[r8].w);
+            const float4 r = *reinterpret_cast<const float4*>(&stg[rl * TC_EPI_STRIDE + cl]);
             float* dst = p.C + static_cast<long long>(grow) * p.ldc + gcol;
             if (vec_ok && gcol + 3 < p.N) {
               *reinterpret_cast<float4*>(dst) = r;
@@ -486,8 +472,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
         }
         __syncwarp();
-#pragma unroll
-        for (int r8 = 0; r8 < 8; ++r8) cin[r8] = cnext[r8];
       }
       tc_fence_before();
       mbar_arrive_cluster(smem_u32(&tempty[buf]) & kPeerBitMask);

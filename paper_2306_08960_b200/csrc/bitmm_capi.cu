@@ -59,7 +59,6 @@ struct DeviceState {
   Arena ws;               // intermediates (expanded operands)
   Arena io;               // host-flavour staging of inputs/outputs
   cudaStream_t stream = nullptr;  // host-flavour private stream
-  uint64_t attr_mask = 0;     // spmm / apb kernels (max-smem attribute set)
   unsigned ws_turn = 0;           // ping-pong half of the expanded-operand workspace
   void* pinned[2] = {nullptr, nullptr};  // BTSR streaming chunks (allocated on first load)
   cudaEvent_t pinned_ev[2] = {nullptr, nullptr};
@@ -499,7 +498,7 @@ void take_int_operands(DeviceState& st, int64_t m, int64_t n, int64_t k, uint8_t
 }
 size_t ws_bytes_1x32(int64_t m, int64_t n, int64_t k) {
   const int64_t kpad = round_up(k, 64);
-  return align_up(m * kpad * 2, 1024) + align_up(n * 3 * kpad * 2, 1024) + 2048;
+  return align_up(m * kpad * 2, 1024) + align_up(n * APB_PARTS * kpad * 2, 1024) + align_up(n * 4, 1024) + 2048;
 }
 
 // ---------------- routine bodies on device pointers ----------------
@@ -586,7 +585,7 @@ bool spmm_staged(const DeviceState& st, int64_t rows, int64_t k, int64_t n) {
 // EXACT reproduces the reference rounding (kernels.cpp:347); the fp32 APB layer uses fma and
 // chains into the GEMM with PDL. When the staged chunk does not fit in shared memory, LEVELS
 // first dequantizes into `deq` [k][n] and both sources take the global-gather kernel.
-template <bool EXACT, bool PDL_CHAIN, bool LEVELS = false>
+template <bool EXACT, bool PDL_CHAIN, bool LEVELS = false, bool ACCUM = LEVELS>
 int run_spmm(DeviceState& st, int64_t rows, int64_t k, const uint64_t* row_ptr,
              const uint64_t* col_idx, const float* vals, const float* b, int64_t n, int64_t ldb,
              float* c, int64_t ldc, cudaStream_t s, const SpmmLevels& lv = SpmmLevels{},
@@ -609,15 +608,15 @@ int run_spmm(DeviceState& st, int64_t rows, int64_t k, const uint64_t* row_ptr,
     ProfScope ps("spmm_csr_gather", s);
     spmm_csr_kernel<<<blocks_for(warps * 32, 256), 256, 0, s>>>(rows, rp, ci, vals, b, ldb,
                                                                 static_cast<int>(n), c, ldc,
-                                                                LEVELS ? 1 : 0);
+                                                                ACCUM ? 1 : 0);
     return launch_check("spmm_csr_kernel");
   }
-  auto kern = spmm_xchunk_kernel<EXACT, PDL_CHAIN, LEVELS>;
+  auto kern = spmm_xchunk_kernel<EXACT, PDL_CHAIN, LEVELS, ACCUM>;
   const int smem = spmm_smem_bytes(k, rows_per_split);
-  const unsigned bit = 1u << (20 + (EXACT ? 1 : 0) + (PDL_CHAIN ? 2 : 0) + (LEVELS ? 4 : 0));
-  if (!(st.attr_mask & bit)) {
+  static bool attr_set = false;  // one flag per instantiation
+  if (!attr_set) {
     BITMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-    st.attr_mask |= bit;
+    attr_set = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(chunks), static_cast<unsigned>(splits));
@@ -627,7 +626,7 @@ int run_spmm(DeviceState& st, int64_t rows, int64_t k, const uint64_t* row_ptr,
   cudaLaunchAttribute attr[1] = {pdl_attr()};
   cfg.attrs = attr;
   cfg.numAttrs = PDL_CHAIN ? 1 : 0;
-  ProfScope ps(LEVELS ? "spmm_levels_exact" : EXACT ? "spmm_xchunk_exact" : "spmm_xchunk", s);
+  ProfScope ps(LEVELS ? "spmm_levels_exact" : EXACT ? "spmm_xchunk_exact" : ACCUM ? "spmm_xchunk_accum" : "spmm_xchunk", s);
   BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, static_cast<int>(rows), static_cast<int>(k),
                                     static_cast<int>(n), rp, ci, vals, b, ldb, c, ldc,
                                     rows_per_split, lv));
@@ -641,8 +640,9 @@ int apb_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, int64_t k, int64
   const int64_t kpad = round_up(k, 64);
   BITMM_TRY(arena_reserve(st.ws, ws_bytes_1x32(m, n, k)));
   Carve cv(st.ws.ptr);
-  uint16_t* Abf = cv.take<uint16_t>(m * kpad * 2);
+  uint16_t* Ah = cv.take<uint16_t>(m * kpad * 2);
   uint16_t* XT = cv.take<uint16_t>(n * APB_PARTS * kpad * 2);
+  float* tok_scale = cv.take<float>(n * 4);
   cudaLaunchAttribute pdl[1] = {pdl_attr()};
   {
     const int wpr32 = static_cast<int>(wpr * 2);
@@ -653,11 +653,23 @@ int apb_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, int64_t k, int64
     cfg.stream = s;
     cfg.attrs = pdl;
     cfg.numAttrs = 1;
-    ProfScope ps("unpack_sign_bf16", s);
-    BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, unpack_sign_bf16, reinterpret_cast<const uint32_t*>(w),
+    ProfScope ps("unpack_sign_f16", s);
+    BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, unpack_sign_f16, reinterpret_cast<const uint32_t*>(w),
                                       static_cast<long long>(m), wpr32, static_cast<int>(k),
-                                      static_cast<int>(kpad), Abf, st.status));
-    BITMM_TRY(launch_check("unpack_sign_bf16"));
+                                      static_cast<int>(kpad), Ah, st.status));
+    BITMM_TRY(launch_check("unpack_sign_f16"));
+  }
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>((n + 31) / 32));
+    cfg.blockDim = dim3(1024);
+    cfg.stream = s;
+    cfg.attrs = pdl;
+    cfg.numAttrs = 1;
+    ProfScope ps("x_token_scale", s);
+    BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, x_token_scale, b, static_cast<long long>(ldb),
+                                      static_cast<int>(k), static_cast<int>(n), tok_scale));
+    BITMM_TRY(launch_check("x_token_scale"));
   }
   {
     cudaLaunchConfig_t cfg = {};
@@ -666,19 +678,16 @@ int apb_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, int64_t k, int64
     cfg.stream = s;
     cfg.attrs = pdl;
     cfg.numAttrs = 1;
-    ProfScope ps("split_x_bf16", s);
-    BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, split_x_bf16, b, static_cast<long long>(ldb),
+    ProfScope ps("split_x_f16", s);
+    BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, split_x_f16, b, static_cast<long long>(ldb),
                                       static_cast<int>(k), static_cast<int>(n),
-                                      static_cast<int>(kpad), APB_PARTS, XT));
-    BITMM_TRY(launch_check("split_x_bf16"));
+                                      static_cast<int>(kpad), static_cast<const float*>(tok_scale), XT));
+    BITMM_TRY(launch_check("split_x_f16"));
   }
-  const bool has_res = row_ptr != nullptr;
-  if (has_res)
-    BITMM_TRY((run_spmm<false, true>(st, m, k, row_ptr, col_idx, vals, b, n, ldb, c, ldc, s)));
 
   CUtensorMap ta, tb;
-  BITMM_TRY(make_operand_map(&ta, Abf, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kpad, m, 128));
-  BITMM_TRY(make_operand_map(&tb, XT, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, APB_PARTS * kpad, n, APB_BN / 2));
+  BITMM_TRY(make_operand_map(&ta, Ah, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, kpad, m, 128));
+  BITMM_TRY(make_operand_map(&tb, XT, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, APB_PARTS * kpad, n, APB_BN / 2));
   ApbParams p{};
   p.M = static_cast<int>(m);
   p.N = static_cast<int>(n);
@@ -686,16 +695,16 @@ int apb_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, int64_t k, int64
   p.kpad = static_cast<int>(kpad);
   p.alpha = gamma;
   p.row_alpha = row_gamma;
+  p.tok_scale = tok_scale;
   p.C = c;
   p.ldc = ldc;
-  p.accumulate_c = has_res ? 1 : 0;
   p.num_m_blocks = static_cast<int>((m + 255) / 256);
   p.num_n_blocks = static_cast<int>((n + APB_BN - 1) / APB_BN);
   p.num_tiles = p.num_m_blocks * p.num_n_blocks;
-  const unsigned bit = 1u << 28;
-  if (!(st.attr_mask & bit)) {
+  static bool attr_set = false;
+  if (!attr_set) {
     BITMM_CUDA_TRY(cudaFuncSetAttribute(apb_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, APB_SMEM));
-    st.attr_mask |= bit;
+    attr_set = true;
   }
   const int units = std::min(p.num_tiles, st.sms / 2);
   cudaLaunchConfig_t cfg = {};
@@ -711,9 +720,15 @@ int apb_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, int64_t k, int64
   attr[1] = pdl_attr();
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  ProfScope ps("apb_gemm_bf16x3", s);
-  BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, apb_gemm_kernel, ta, tb, p));
-  return launch_check("apb_gemm_kernel");
+  {
+    ProfScope ps("apb_gemm_f16x2", s);
+    BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, apb_gemm_kernel, ta, tb, p));
+    BITMM_TRY(launch_check("apb_gemm_kernel"));
+  }
+  // the residual adds onto the stored binary part: C = bin + R.X (apb.cpp:161-162)
+  if (row_ptr != nullptr)
+    BITMM_TRY((run_spmm<false, true, false, true>(st, m, k, row_ptr, col_idx, vals, b, n, ldb, c, ldc, s)));
+  return BITMM_OK;
 }
 
 // Paper-faithful APB with 2-bit activations:

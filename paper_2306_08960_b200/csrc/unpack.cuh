@@ -12,15 +12,17 @@
 //                      planes {t,h,m} -> int8 level p      (ThmPlanes, tensor.hpp:134;
 //                      legal states per transform.cpp:47-75: p0=(0,0,1) p1=(0,0,0)
 //                      p2=(0,1,0) p3=(1,0,1), so p = 2(t|h) + (t | ~(h|m)))
-//   unpack_sign_bf16 : bit b -> bf16 (+1/-1)               (APB binary plane)
-//   split_x_bf16     : fp32 X[K][N] -> bf16 parts XT[N][part*kpad + k] with
-//                      x = hi + mid + lo exactly (3 parts) — transposed to K-major.
+//   unpack_sign_f16  : bit b -> fp16 (+1/-1)               (APB binary plane)
+//   split_x_f16      : fp32 X[K][N] -> fp16 parts XT[N][part*kpad + k], transposed to
+//                      K-major: per token n a power of two 2^e_n brings max_k |X[k][n]|
+//                      into [2^14, 2^15), and x * 2^e_n = hi + lo (+ <= 2^-22 relative);
+//                      2^-e_n goes to the GEMM epilogue as the column scale.
 // Validation folded into the same pass (the reference checks these on the host,
 // tensor.cpp:78-89 and tensor.cpp:133-153): nonzero padding of a BitMatrix sets
 // ERR_PADDING, an illegal plane triple or nonzero plane padding sets ERR_ENCODING.
 #pragma once
 
-#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cstdint>
 
 #include "ptx.cuh"
@@ -249,9 +251,9 @@ __global__ void unpack_level_i8(const uint32_t* __restrict__ t, const uint32_t* 
   dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
 }
 
-__global__ void unpack_sign_bf16(const uint32_t* __restrict__ words, long long rows, int wpr32,
-                                 int K, int kpad, uint16_t* __restrict__ out,
-                                 int* __restrict__ err) {
+__global__ void unpack_sign_f16(const uint32_t* __restrict__ words, long long rows, int wpr32,
+                                int K, int kpad, uint16_t* __restrict__ out,
+                                int* __restrict__ err) {
   pdl_wait();  // the previous kernel may still read the workspace we overwrite
   pdl_launch_dependents();
   const int groups_out = kpad / 32;
@@ -269,8 +271,8 @@ __global__ void unpack_sign_bf16(const uint32_t* __restrict__ words, long long r
   for (int q = 0; q < 16; ++q) {
     const uint32_t b0 = (w >> (2 * q)) & 1u, b1 = (w >> (2 * q + 1)) & 1u;
     const uint32_t v0 = (valid >> (2 * q)) & 1u, v1 = (valid >> (2 * q + 1)) & 1u;
-    const uint32_t e0 = v0 ? (b0 ? 0x3F80u : 0xBF80u) : 0u;  // +1.0 / -1.0 bf16
-    const uint32_t e1 = v1 ? (b1 ? 0x3F80u : 0xBF80u) : 0u;
+    const uint32_t e0 = v0 ? (b0 ? 0x3C00u : 0xBC00u) : 0u;  // +1.0 / -1.0 fp16
+    const uint32_t e1 = v1 ? (b1 ? 0x3C00u : 0xBC00u) : 0u;
     o[q] = e0 | (e1 << 16);
   }
   uint4* dst = reinterpret_cast<uint4*>(out + r * kpad + g * 32);
@@ -278,11 +280,43 @@ __global__ void unpack_sign_bf16(const uint32_t* __restrict__ words, long long r
   for (int q = 0; q < 4; ++q) dst[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
 }
 
-// X [K][ldx] fp32 -> XT [N][nparts*kpad] bf16, part p at column offset p*kpad.
-// Block = 256 threads, tile 64 k x 32 n; reads coalesced along n, writes 128 B
-// segments along k per part.
-__global__ void split_x_bf16(const float* __restrict__ X, long long ldx, int K, int N, int kpad,
-                             int nparts, uint16_t* __restrict__ XT) {
+// Per-token scale of the fp16 split: tok_scale[n] = 2^-e_n with max_k |X[k][n]| * 2^e_n in
+// [2^14, 2^15) (e_n = 0 when the maximum is 0 or not finite; |e_n| <= 126). One block per
+// 32-token strip, 32 warps each reading every 32nd K row (coalesced 128-byte rows).
+__global__ void __launch_bounds__(1024) x_token_scale(const float* __restrict__ X, long long ldx,
+                                                      int K, int N, float* __restrict__ tok_scale) {
+  __shared__ float red[32][33];
+  pdl_wait();
+  pdl_launch_dependents();
+  const int n0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  float mx = 0.f;
+  if (n0 + tx < N) {
+#pragma unroll 4
+    for (int k = ty; k < K; k += 32) mx = fmaxf(mx, fabsf(X[static_cast<long long>(k) * ldx + n0 + tx]));
+  }
+  red[ty][tx] = mx;
+  __syncthreads();
+  if (ty == 0) {
+#pragma unroll
+    for (int i = 1; i < 32; ++i) mx = fmaxf(mx, red[i][tx]);
+    int e = 0;
+    if (mx > 0.f && mx <= 3.402823466e38f) {
+      int q;
+      frexpf(mx, &q);  // mx = f * 2^q, f in [0.5, 1)
+      e = min(126, max(-126, 15 - q));
+    }
+    if (n0 + tx < N) tok_scale[n0 + tx] = ldexpf(1.0f, -e);
+  }
+}
+
+// X [K][ldx] fp32 -> XT [N][2*kpad] fp16, hi at column 0 and lo at column kpad, with x
+// scaled by 1 / tok_scale[n] = 2^e_n (exact). hi = rn_f16(x * 2^e_n), lo = rn_f16(x * 2^e_n
+// - hi) (the difference is exact in fp32), so only lo's rounding is lost: <= 2^-22 of |x|
+// while lo stays a normal fp16 number. Block = 256 threads, tile 64 k x 32 n; reads
+// coalesced along n, writes 128 B segments along k per part.
+__global__ void split_x_f16(const float* __restrict__ X, long long ldx, int K, int N, int kpad,
+                            const float* __restrict__ tok_scale, uint16_t* __restrict__ XT) {
   __shared__ float tile[64][33];
   pdl_wait();
   pdl_launch_dependents();
@@ -300,30 +334,25 @@ __global__ void split_x_bf16(const float* __restrict__ X, long long ldx, int K, 
   const int kl = (threadIdx.x & 7) * 8;   // 0..56
   const int n = n0 + nl;
   if (n >= N) return;
-  uint32_t parts[3][4];
+  const float sc = __frcp_rn(tok_scale[n]);  // 2^e_n, exact
+  uint32_t hi2[4], lo2[4];
 #pragma unroll
-  for (int e = 0; e < 8; e += 2) {
-    uint32_t pe[3][2];
+  for (int q = 0; q < 4; ++q) {
+    uint32_t h[2], l[2];
 #pragma unroll
     for (int d = 0; d < 2; ++d) {
-      float x = tile[kl + e + d][nl];
-      const __nv_bfloat16 hi = __float2bfloat16_rn(x);
-      const float r1 = x - __bfloat162float(hi);
-      const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
-      const float r2 = r1 - __bfloat162float(mid);
-      const __nv_bfloat16 lo = __float2bfloat16_rn(r2);
-      pe[0][d] = __bfloat16_as_ushort(hi);
-      pe[1][d] = __bfloat16_as_ushort(mid);
-      pe[2][d] = __bfloat16_as_ushort(lo);
+      const float xs = tile[kl + 2 * q + d][nl] * sc;  // exact: a power of two
+      const __half hv = __float2half_rn(xs);
+      const __half lv = __float2half_rn(xs - __half2float(hv));
+      h[d] = __half_as_ushort(hv);
+      l[d] = __half_as_ushort(lv);
     }
-#pragma unroll
-    for (int q = 0; q < 3; ++q) parts[q][e / 2] = pe[q][0] | (pe[q][1] << 16);
+    hi2[q] = h[0] | (h[1] << 16);
+    lo2[q] = l[0] | (l[1] << 16);
   }
-  const long long row_off = static_cast<long long>(n) * nparts * kpad;
-  for (int q = 0; q < nparts; ++q) {
-    uint4* dst = reinterpret_cast<uint4*>(XT + row_off + static_cast<long long>(q) * kpad + k0 + kl);
-    *dst = make_uint4(parts[q][0], parts[q][1], parts[q][2], parts[q][3]);
-  }
+  uint16_t* row = XT + static_cast<long long>(n) * 2 * kpad + k0 + kl;
+  *reinterpret_cast<uint4*>(row) = make_uint4(hi2[0], hi2[1], hi2[2], hi2[3]);
+  *reinterpret_cast<uint4*>(row + kpad) = make_uint4(lo2[0], lo2[1], lo2[2], lo2[3]);
 }
 
 }  // namespace bitmm_dev

@@ -173,3 +173,25 @@ def test_spmm_exact_odd_shapes(orc):
         b = rng.standard_normal((cols, n)).astype(np.float32)
         assert np.array_equal(api.spmm_csr(csr, b), orc.spmm_csr(rows, csr.row_ptr, csr.col_idx,
                                                                  csr.vals, b))
+
+
+def test_token_magnitude_range(orc):
+    """The fp16 split scales every token by a power of two before splitting: tokens spanning
+    1e-30 .. 1e30 (beyond fp16's range either way), an all-zero token, and a token with one
+    large outlier keep the 1e-5 tolerance column by column."""
+    rng = np.random.default_rng(5)
+    rows, k, tokens = 64, 300, 9
+    a, alpha, _ = data.apb_weights(rng, rows, k)
+    layer = api.decompose_apb(a, alpha)
+    x = rng.standard_normal((k, tokens)).astype(np.float32)
+    scales = np.array([1e-30, 1e-12, 1e-4, 1.0, 7e4, 1e12, 1e30, 0.0, 1.0], np.float32)
+    x *= scales[None, :]
+    x[17, 8] = 3e5  # one outlier in an otherwise unit-scale token
+    got = api.layer_forward(layer, x)
+    r = layer.residual
+    want = orc.layer_forward(rows, k, 1.0, layer.bin.words, layer.bin.words_per_row(), r.row_ptr,
+                             r.col_idx, r.vals, x, row_alpha=alpha)
+    assert np.all(got[:, 7] == 0.0)
+    for j in range(tokens):
+        if j != 7:
+            check_close(got[:, j], want[:, j])

@@ -85,7 +85,8 @@ def test_workspace_bytes_model():
     lib = _lib.load()
     # 1/1 4096^3: two expanded int8 operands of 16 MiB each
     assert lib.bitmm_workspace_bytes(0, 4096, 4096, 4096) >= 2 * 4096 * 4096
-    assert lib.bitmm_workspace_bytes(3, 3072, 8192, 768) >= 2 * (3072 * 768 + 8192 * 3 * 768)
+    # 1/32 (APB): fp16 signs + two fp16 parts of X^T + per-token scales
+    assert lib.bitmm_workspace_bytes(3, 3072, 8192, 768) >= 2 * (3072 * 768 + 8192 * 2 * 768) + 4 * 8192
     assert lib.bitmm_workspace_bytes(0, 0, 1, 1) == 0
 
 
