@@ -62,6 +62,8 @@ struct DeviceState {
   unsigned ws_turn = 0;           // ping-pong half of the expanded-operand workspace
   void* pinned[2] = {nullptr, nullptr};  // BTSR streaming chunks (allocated on first load)
   cudaEvent_t pinned_ev[2] = {nullptr, nullptr};
+  cudaStream_t d2h = nullptr;             // host-flavour output copies (run_pipelined)
+  cudaEvent_t pipe_ev[8] = {};
 };
 
 std::mutex g_mu;
@@ -464,6 +466,47 @@ int read_status(DeviceState& st, cudaStream_t s) {
   if (flag & ERR_ENCODING) return fail(BITMM_ERR_INVALID_ENCODING, "invalid ternary plane encoding or nonzero plane padding");
   if (flag & ERR_PADDING) return fail(BITMM_ERR_INVALID_ARGUMENT, "bit matrix padding must be zero");
   return BITMM_OK;
+}
+
+// ---------------- host-flavour pipeline ----------------
+// A host call's time is mostly the device -> host copy of its output (4 B per cell). Valid
+// calls produce the output in up to kPipeChunks slices of one dimension: slice i's inputs are
+// copied in and its GEMM runs on the call's stream, then its output is copied out on st.d2h,
+// so the D2H of slice i overlaps the H2D and GEMM of slice i+1.
+constexpr int kPipeChunks = 8;
+constexpr size_t kPipeMinOutBytes = size_t{32} << 20;  // smaller outputs go in one slice
+
+int64_t pipe_step(int64_t total, size_t out_bytes, int64_t align) {
+  if (out_bytes < kPipeMinOutBytes || total < 2 * align) return total;
+  return round_up((total + kPipeChunks - 1) / kPipeChunks, align);
+}
+
+// body(c0, c1): enqueue slice [c0, c1)'s input copies and GEMM on s. out(c0, c1, d2h):
+// enqueue its output copies on d2h. Always drains d2h before returning.
+template <class Body, class Out>
+int run_pipelined(DeviceState& st, cudaStream_t s, int64_t total, int64_t step, Body&& body,
+                  Out&& out) {
+  if (!st.d2h) {
+    BITMM_CUDA_TRY(cudaStreamCreateWithFlags(&st.d2h, cudaStreamNonBlocking));
+    for (auto& e : st.pipe_ev) BITMM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  int rc = BITMM_OK;
+  int i = 0;
+  for (int64_t c0 = 0; c0 < total; c0 += step, ++i) {
+    const int64_t c1 = std::min(total, c0 + step);
+    rc = body(c0, c1);
+    if (rc != BITMM_OK) break;
+    cudaEvent_t ev = st.pipe_ev[i % kPipeChunks];
+    if (cudaEventRecord(ev, s) != cudaSuccess || cudaStreamWaitEvent(st.d2h, ev, 0) != cudaSuccess) {
+      rc = fail(BITMM_ERR_CUDA, std::string("pipeline event: ") + cudaGetErrorString(cudaGetLastError()));
+      break;
+    }
+    rc = out(c0, c1, st.d2h);
+    if (rc != BITMM_OK) break;
+  }
+  const cudaError_t e = cudaStreamSynchronize(st.d2h);
+  if (rc == BITMM_OK && e != cudaSuccess) rc = fail(BITMM_ERR_CUDA, cudaGetErrorString(e));
+  return rc;
 }
 
 struct Carve {
@@ -943,11 +986,22 @@ int bitmm_gemm_1x1_host(const uint64_t* a, int64_t m, const uint64_t* b_packed, 
   uint64_t* db = cv.take<uint64_t>(b_bytes);
   int32_t* dcu = c_units ? cv.take<int32_t>(c_bytes) : nullptr;
   float* dc = c ? cv.take<float>(c_bytes) : nullptr;
-  BITMM_CUDA_TRY(cudaMemcpyAsync(da, a, a_bytes, cudaMemcpyHostToDevice, s));
   BITMM_CUDA_TRY(cudaMemcpyAsync(db, b_packed, b_bytes, cudaMemcpyHostToDevice, s));
-  BITMM_TRY(gemm_1x1_dev_impl(*st, da, m, db, n, k, wpr, gamma_a, gamma_b, dcu, dc, ldc, s));
-  if (dcu) BITMM_CUDA_TRY(cudaMemcpyAsync(c_units, dcu, c_bytes, cudaMemcpyDeviceToHost, s));
-  if (dc) BITMM_CUDA_TRY(cudaMemcpyAsync(c, dc, c_bytes, cudaMemcpyDeviceToHost, s));
+  // slices of output rows (rows of a)
+  BITMM_TRY(run_pipelined(
+      *st, s, m, pipe_step(m, c_bytes, 256),
+      [&](int64_t r0, int64_t r1) -> int {
+        BITMM_CUDA_TRY(cudaMemcpyAsync(da + r0 * wpr, a + r0 * wpr, (r1 - r0) * wpr * 8,
+                                       cudaMemcpyHostToDevice, s));
+        return gemm_1x1_dev_impl(*st, da + r0 * wpr, r1 - r0, db, n, k, wpr, gamma_a, gamma_b,
+                                 dcu ? dcu + r0 * ldc : nullptr, dc ? dc + r0 * ldc : nullptr, ldc, s);
+      },
+      [&](int64_t r0, int64_t r1, cudaStream_t d2h) -> int {
+        const size_t bytes = (r1 - r0) * ldc * 4;
+        if (dcu) BITMM_CUDA_TRY(cudaMemcpyAsync(c_units + r0 * ldc, dcu + r0 * ldc, bytes, cudaMemcpyDeviceToHost, d2h));
+        if (dc) BITMM_CUDA_TRY(cudaMemcpyAsync(c + r0 * ldc, dc + r0 * ldc, bytes, cudaMemcpyDeviceToHost, d2h));
+        return BITMM_OK;
+      }));
   return read_status(*st, s);
 }
 
@@ -990,12 +1044,12 @@ int bitmm_gemm_1x2_host(const uint64_t* w, int64_t m, float gamma, const uint64_
   uint64_t* dt = cv.take<uint64_t>(p_bytes);
   uint64_t* dh = cv.take<uint64_t>(p_bytes);
   uint64_t* dm = cv.take<uint64_t>(p_bytes);
-  if (p_bytes) {
-    BITMM_CUDA_TRY(cudaMemcpyAsync(dt, t, p_bytes, cudaMemcpyHostToDevice, s));
-    BITMM_CUDA_TRY(cudaMemcpyAsync(dh, h, p_bytes, cudaMemcpyHostToDevice, s));
-    BITMM_CUDA_TRY(cudaMemcpyAsync(dm, mm, p_bytes, cudaMemcpyHostToDevice, s));
-  }
   if (rc_dims != BITMM_OK) {
+    if (p_bytes) {
+      BITMM_CUDA_TRY(cudaMemcpyAsync(dt, t, p_bytes, cudaMemcpyHostToDevice, s));
+      BITMM_CUDA_TRY(cudaMemcpyAsync(dh, h, p_bytes, cudaMemcpyHostToDevice, s));
+      BITMM_CUDA_TRY(cudaMemcpyAsync(dm, mm, p_bytes, cudaMemcpyHostToDevice, s));
+    }
     // plane legality still wins over shape errors (reference precedence)
     if (planes_ok_shape && n > 0 && k > 0) {
       const int64_t kpad = round_up(k, TC_BK_BYTES);
@@ -1013,10 +1067,25 @@ int bitmm_gemm_1x2_host(const uint64_t* w, int64_t m, float gamma, const uint64_
   BITMM_CUDA_TRY(cudaMemcpyAsync(dw, w, w_bytes, cudaMemcpyHostToDevice, s));
   if (drs) BITMM_CUDA_TRY(cudaMemcpyAsync(drs, row_scale, m * 4, cudaMemcpyHostToDevice, s));
   if (dcs) BITMM_CUDA_TRY(cudaMemcpyAsync(dcs, col_scale, n * 4, cudaMemcpyHostToDevice, s));
-  BITMM_TRY(gemm_1x2_dev_impl(*st, dw, m, gamma, dt, dh, dm, n, k, wpr, a_scale, has_a_gamma,
-                              a_gamma, drs, dcs, dcu, dc, ldc, s));
-  if (dcu) BITMM_CUDA_TRY(cudaMemcpyAsync(c_units, dcu, c_bytes, cudaMemcpyDeviceToHost, s));
-  if (dc) BITMM_CUDA_TRY(cudaMemcpyAsync(c, dc, c_bytes, cudaMemcpyDeviceToHost, s));
+  // slices of output columns (rows of the activation planes, the larger operand here);
+  // each slice's output block is a strided 2-D copy
+  BITMM_TRY(run_pipelined(
+      *st, s, n, pipe_step(n, c_bytes, 256),
+      [&](int64_t n0, int64_t n1) -> int {
+        const size_t off = n0 * wpr, bytes = (n1 - n0) * wpr * 8;
+        BITMM_CUDA_TRY(cudaMemcpyAsync(dt + off, t + off, bytes, cudaMemcpyHostToDevice, s));
+        BITMM_CUDA_TRY(cudaMemcpyAsync(dh + off, h + off, bytes, cudaMemcpyHostToDevice, s));
+        BITMM_CUDA_TRY(cudaMemcpyAsync(dm + off, mm + off, bytes, cudaMemcpyHostToDevice, s));
+        return gemm_1x2_dev_impl(*st, dw, m, gamma, dt + off, dh + off, dm + off, n1 - n0, k, wpr,
+                                 a_scale, has_a_gamma, a_gamma, drs, dcs ? dcs + n0 : nullptr,
+                                 dcu ? dcu + n0 : nullptr, dc ? dc + n0 : nullptr, ldc, s);
+      },
+      [&](int64_t n0, int64_t n1, cudaStream_t d2h) -> int {
+        const size_t pitch = ldc * 4, width = (n1 - n0) * 4;
+        if (dcu) BITMM_CUDA_TRY(cudaMemcpy2DAsync(c_units + n0, pitch, dcu + n0, pitch, width, m, cudaMemcpyDeviceToHost, d2h));
+        if (dc) BITMM_CUDA_TRY(cudaMemcpy2DAsync(c + n0, pitch, dc + n0, pitch, width, m, cudaMemcpyDeviceToHost, d2h));
+        return BITMM_OK;
+      }));
   return read_status(*st, s);
 }
 
@@ -1068,7 +1137,9 @@ int bitmm_gemm_2x2_host(const uint64_t* wt, const uint64_t* wh, const uint64_t* 
   for (int i = 0; i < 6; ++i) {
     const size_t bytes = i < 3 ? pw : pa;
     d[i] = cv.take<uint64_t>(bytes);
-    if (bytes) BITMM_CUDA_TRY(cudaMemcpyAsync(d[i], src[i], bytes, cudaMemcpyHostToDevice, s));
+    // the weight planes go in per slice below unless the call fails on its shapes
+    if (bytes && (i >= 3 || rc_dims != BITMM_OK))
+      BITMM_CUDA_TRY(cudaMemcpyAsync(d[i], src[i], bytes, cudaMemcpyHostToDevice, s));
   }
   if (rc_dims != BITMM_OK) {
     if (shape_ok && k > 0) {
@@ -1086,11 +1157,24 @@ int bitmm_gemm_2x2_host(const uint64_t* wt, const uint64_t* wh, const uint64_t* 
   float* dc = c ? cv.take<float>(c_bytes) : nullptr;
   if (drs) BITMM_CUDA_TRY(cudaMemcpyAsync(drs, row_scale, m * 4, cudaMemcpyHostToDevice, s));
   if (dcs) BITMM_CUDA_TRY(cudaMemcpyAsync(dcs, col_scale, n * 4, cudaMemcpyHostToDevice, s));
-  BITMM_TRY(gemm_2x2_dev_impl(*st, d[0], d[1], d[2], m, w_scale, has_w_gamma, w_gamma, d[3], d[4],
-                              d[5], n, k, wpr, a_scale, has_a_gamma, a_gamma, drs, dcs, dcu, dc,
-                              ldc, s));
-  if (dcu) BITMM_CUDA_TRY(cudaMemcpyAsync(c_units, dcu, c_bytes, cudaMemcpyDeviceToHost, s));
-  if (dc) BITMM_CUDA_TRY(cudaMemcpyAsync(c, dc, c_bytes, cudaMemcpyDeviceToHost, s));
+  // slices of output rows (rows of the weight planes)
+  BITMM_TRY(run_pipelined(
+      *st, s, m, pipe_step(m, c_bytes, 256),
+      [&](int64_t r0, int64_t r1) -> int {
+        const size_t off = r0 * wpr, bytes = (r1 - r0) * wpr * 8;
+        for (int i = 0; i < 3; ++i)
+          BITMM_CUDA_TRY(cudaMemcpyAsync(d[i] + off, src[i] + off, bytes, cudaMemcpyHostToDevice, s));
+        return gemm_2x2_dev_impl(*st, d[0] + off, d[1] + off, d[2] + off, r1 - r0, w_scale,
+                                 has_w_gamma, w_gamma, d[3], d[4], d[5], n, k, wpr, a_scale,
+                                 has_a_gamma, a_gamma, drs ? drs + r0 : nullptr, dcs,
+                                 dcu ? dcu + r0 * ldc : nullptr, dc ? dc + r0 * ldc : nullptr, ldc, s);
+      },
+      [&](int64_t r0, int64_t r1, cudaStream_t d2h) -> int {
+        const size_t bytes = (r1 - r0) * ldc * 4;
+        if (dcu) BITMM_CUDA_TRY(cudaMemcpyAsync(c_units + r0 * ldc, dcu + r0 * ldc, bytes, cudaMemcpyDeviceToHost, d2h));
+        if (dc) BITMM_CUDA_TRY(cudaMemcpyAsync(c + r0 * ldc, dc + r0 * ldc, bytes, cudaMemcpyDeviceToHost, d2h));
+        return BITMM_OK;
+      }));
   return read_status(*st, s);
 }
 
