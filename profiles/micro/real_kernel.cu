@@ -5,6 +5,7 @@
 //   -DRK_BN=224       output tile width (TMEM: 2 * BN + 64 scale-factor columns <= 512)
 //   -DRK_MC=2         four-CTA clusters, A rows multicast between the two pairs
 //   -DRK_NOTMA        epilogue stores through the LSU fallback instead of TMA stores
+//   -DRK_ZERO_ONE     {0, +1} operand data (timing only; the sampled check assumes +-1)
 #include <cstdio>
 #include <cstring>
 #include <cuda.h>
@@ -28,7 +29,11 @@ int main() {
   cudaMalloc(&a, size_t(M) * RB); cudaMalloc(&b, size_t(N) * RB); cudaMalloc(&c, size_t(M) * N * 4);
   unsigned char* h = nullptr;
   {
+#ifdef RK_ZERO_ONE
+    const unsigned char codes[2] = {0x0, 0x2};  // {0, +1}: timing only (the check assumes +-1)
+#else
     const unsigned char codes[2] = {0x2, 0xA};
+#endif
     h = static_cast<unsigned char*>(malloc(size_t(M) * RB));
     unsigned long long x = 88172645463325252ull;
     for (size_t i = 0; i < size_t(M) * RB; ++i) {
