@@ -153,19 +153,25 @@ __global__ void __launch_bounds__(SPMM_THREADS, 2)
   const unsigned long long* cbase = col_idx + nz0;
   const float* vbase = vals + nz0;
   const int iters = (r1 - r0 + SPMM_QUADS - 1) / SPMM_QUADS;
-  const unsigned zero_row = static_cast<unsigned>(K) * (SPMM_TOK * 4);
-  // Nonzero slot `idx` of a row as (byte offset of its X row in smem, weight); padded slots
-  // point at the zero row with weight 0 (0 * 0 leaves an accumulator that started at +0
-  // bit-identical: it can never be -0, so no branch is needed, and EXACT keeps the order).
+  const unsigned zero_row = static_cast<unsigned>(K);  // X row index of the zero row
+  // Nonzero slot `idx` of a row as (X row index, weight); padded slots point at the zero row
+  // with weight 0 (0 * 0 leaves an accumulator that started at +0 bit-identical: it can never
+  // be -0, so no branch is needed, and EXACT keeps the order). Loaded raw: the index becomes
+  // a byte offset only where it is used (step8, an iteration later for prefetched slots), so
+  // the warp does not stall on the load right after issuing it.
   auto fetch = [&](unsigned i0, unsigned n, unsigned idx, unsigned& kk, float& vv) {
-    kk = idx < n ? static_cast<unsigned>(cbase[i0 + idx]) * (SPMM_TOK * 4) : zero_row;
-    vv = idx < n ? vbase[i0 + idx] : 0.f;
+    kk = zero_row;
+    vv = 0.f;
+    if (idx < n) {
+      kk = static_cast<unsigned>(cbase[i0 + idx]);
+      vv = vbase[i0 + idx];
+    }
   };
   const char* xrow = reinterpret_cast<const char*>(xs) + ol * 16;
   auto step8 = [&](unsigned kk, float vv, float (&acc)[4]) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const unsigned koff = __shfl_sync(0xFFFFFFFFu, kk, obase + j);
+      const unsigned koff = __shfl_sync(0xFFFFFFFFu, kk, obase + j) * (SPMM_TOK * 4);
       const float v = __shfl_sync(0xFFFFFFFFu, vv, obase + j);
       const float4 x = *reinterpret_cast<const float4*>(xrow + koff);
       if (EXACT) {
@@ -194,21 +200,30 @@ __global__ void __launch_bounds__(SPMM_THREADS, 2)
     fetch(i0, n, ol, kk0, vv0);
     fetch(i0, n, ol + 8, kk1, vv1);
   }
+  // ACCUM: C of the row one iteration ahead is loaded with the next row's slots, so an HBM
+  // round trip overlaps a whole row's nonzero loop instead of a part of it.
+  auto load_c = [&](int r, float (&p)[4]) {
+    p[0] = p[1] = p[2] = p[3] = 0.f;
+    if (ACCUM && r < r1) {
+      const float* src = C + static_cast<long long>(r) * ldc + col;
+      if (vec && col + 3 < N) {
+        const float4 p4 = *reinterpret_cast<const float4*>(src);
+        p[0] = p4.x; p[1] = p4.y; p[2] = p4.z; p[3] = p4.w;
+      } else {
+        for (int e = 0; e < 4; ++e)
+          if (col + e < N) p[e] = src[e];
+      }
+    }
+  };
+  float prev[4];
+  load_c(r0 + oct, prev);
   for (int it = 0; it < iters; ++it) {
     const int r = r0 + it * SPMM_QUADS + oct;
     const bool live = r < r1;
     const unsigned nmax = __reduce_max_sync(0xFFFFFFFFu, n);
     float* dst = C + static_cast<long long>(r) * ldc + col;
-    float prev[4] = {0.f, 0.f, 0.f, 0.f};
-    if (ACCUM && live) {  // issued before the nonzero loop so its latency overlaps it
-      if (vec && col + 3 < N) {
-        const float4 p4 = *reinterpret_cast<const float4*>(dst);
-        prev[0] = p4.x; prev[1] = p4.y; prev[2] = p4.z; prev[3] = p4.w;
-      } else {
-        for (int e = 0; e < 4; ++e)
-          if (col + e < N) prev[e] = dst[e];
-      }
-    }
+    float nprev[4];
+    load_c(r + SPMM_QUADS, nprev);
     // prefetch the next row's first 16 slots
     unsigned ni0 = 0, nn = 0, nkk0 = zero_row, nkk1 = zero_row;
     float nvv0 = 0.f, nvv1 = 0.f;
@@ -248,6 +263,8 @@ __global__ void __launch_bounds__(SPMM_THREADS, 2)
     kk1 = nkk1;
     vv0 = nvv0;
     vv1 = nvv1;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) prev[e] = nprev[e];
   }
 }
 
