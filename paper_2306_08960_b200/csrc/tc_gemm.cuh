@@ -109,13 +109,10 @@ __device__ __forceinline__ void tc_tile_coords(int t, const TcParams& p, int num
 // rewritten only after the store issued from it two blocks earlier has finished reading.
 // Fallback (unaligned ldc): stride-36 staging and coalesced 4-row x 128 B stores.
 // cs: the tile's column scales staged in shared memory (nullptr: no column scale).
-template <Epi EPI, int BN, bool F32ACC = false, int EPI_BUFS = 2>
-__device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, const CUtensorMap* tmC,
-                                                 uint32_t tmem_acc, int quad, int lane,
-                                                 int row_base, int col_base, float* stg,
-                                                 uint32_t& buf, const float* cs) {
-  const bool vec_ok = (p.N & 3) == 0;
-  const int my_row = row_base + lane;
+// This thread's row multiplier (F32: scale * row_scale[r]; F32R: the reference-order
+// product). Loaded by the caller before it waits for the accumulator.
+template <Epi EPI>
+__device__ __forceinline__ float tc_row_mul(const TcParams& p, int my_row) {
   float row_mul = p.scale;
   if constexpr (EPI == Epi::F32) {
     if (p.row_scale != nullptr && my_row < p.M) row_mul = p.scale * p.row_scale[my_row];
@@ -124,6 +121,15 @@ __device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, const CUtens
       row_mul = __fmul_rn(__fmul_rn(__fmul_rn(p.row_pre, p.row_scale[my_row]), p.act_scale),
                           p.act_gamma);
   }
+  return row_mul;
+}
+
+template <Epi EPI, int BN, bool F32ACC = false, int EPI_BUFS = 2>
+__device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, const CUtensorMap* tmC,
+                                                 uint32_t tmem_acc, int quad, int lane,
+                                                 int row_base, int col_base, float* stg,
+                                                 uint32_t& buf, const float* cs, float row_mul) {
+  const bool vec_ok = (p.N & 3) == 0;
   const uint32_t lane_base = tmem_acc + (static_cast<uint32_t>(quad * 32) << 16);
   const int nch = min(BN / 32, (p.N - col_base + 31) / 32);
   // One 32-column chunk: per-thread (row) transform, staged into smem, then stored.
@@ -449,6 +455,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       nb = nb * MC + pair;
       const int acc = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
+      const int row_base = mb * S::TILE_M + static_cast<int>(rank) * 128 + quad * 32;
+      // Row multiplier and column scales of this tile are loaded before the accumulator wait
+      // so their latency hides behind it; the column scales are staged into smem below
+      // (broadcast reads in the transform).
+      float row_mul = p.scale;
+      if constexpr (EPI == Epi::ANY) {
+        if (p.epi != static_cast<int>(Epi::I32)) row_mul = tc_row_mul<Epi::F32>(p, row_base + lane);
+      } else {
+        row_mul = tc_row_mul<EPI>(p, row_base + lane);
+      }
+      const bool has_cs = p.col_scale != nullptr && p.epi != static_cast<int>(Epi::I32);
+      constexpr int CS_PER_THREAD = (BN + 127) / 128;
+      float csv[CS_PER_THREAD];
+      if (has_cs) {
+#pragma unroll
+        for (int j = 0; j < CS_PER_THREAD; ++j) {
+          const int i = (warp - 2) * 32 + lane + j * 128;
+          const int cc = nb * BN + i;
+          csv[j] = (i < BN && cc < p.N) ? p.col_scale[cc] : 0.0f;
+        }
+      }
 #ifdef TC_GEMM_STATS
       long long t2 = clock64();
 #endif
@@ -458,17 +485,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       st_tf += t3 - t2;
 #endif
       tc_fence_after();
-      const int row_base = mb * S::TILE_M + static_cast<int>(rank) * 128 + quad * 32;
       constexpr bool kF32Acc = KIND == Kind::F4;
       const uint32_t tacc = tmem_base + acc * BN;
-      // Column scales of this tile -> smem (broadcast reads in the transform). The first
-      // barrier keeps the previous tile's readers ahead of the overwrite.
+      // Column scales -> smem. The first barrier keeps the previous tile's readers ahead of
+      // the overwrite.
       const float* cs = nullptr;
-      if (p.col_scale != nullptr && p.epi != static_cast<int>(Epi::I32)) {
+      if (has_cs) {
         named_bar_sync(1, 128);
-        for (int i = (warp - 2) * 32 + lane; i < BN; i += 128) {
-          const int cc = nb * BN + i;
-          sCols[i] = cc < p.N ? p.col_scale[cc] : 0.0f;
+#pragma unroll
+        for (int j = 0; j < CS_PER_THREAD; ++j) {
+          const int i = (warp - 2) * 32 + lane + j * 128;
+          if (i < BN) sCols[i] = csv[j];
         }
         named_bar_sync(1, 128);
         cs = sCols;
@@ -476,13 +503,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if constexpr (EPI == Epi::ANY) {
         if (p.epi == static_cast<int>(Epi::I32))
           tc_epilogue_tile<Epi::I32, BN, kF32Acc, S::EPI_BUFS>(p, &g.c[pi], tacc, quad, lane,
-                                                               row_base, nb * BN, stg, buf, cs);
+                                                               row_base, nb * BN, stg, buf, cs, row_mul);
         else
           tc_epilogue_tile<Epi::F32, BN, kF32Acc, S::EPI_BUFS>(p, &g.c[pi], tacc, quad, lane,
-                                                               row_base, nb * BN, stg, buf, cs);
+                                                               row_base, nb * BN, stg, buf, cs, row_mul);
       } else {
         tc_epilogue_tile<EPI, BN, kF32Acc, S::EPI_BUFS>(p, &g.c[pi], tacc, quad, lane, row_base,
-                                                        nb * BN, stg, buf, cs);
+                                                        nb * BN, stg, buf, cs, row_mul);
       }
 #ifdef TC_GEMM_STATS
       st_busy += clock64() - t3;
