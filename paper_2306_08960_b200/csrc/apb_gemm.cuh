@@ -433,12 +433,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       apb_tile_coords(tile, p, mb, nb);
       const int buf = it & 1;
       const uint32_t bphase = (it >> 1) & 1;
-      mbar_wait(&tfull[buf], bphase);
-      tc_fence_after();
       const int row_base = mb * 256 + static_cast<int>(rank) * 128 + quad * 32;
       const int my_row = row_base + lane;
+      // loaded before the accumulator wait so the latency hides behind it
       const float alpha = (p.row_alpha != nullptr) ? (my_row < p.M ? p.row_alpha[my_row] : 0.f)
                                                    : p.alpha;
+      mbar_wait(&tfull[buf], bphase);
+      tc_fence_after();
       const uint32_t t_hi = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + buf * 2 * APB_BN;
       const int cl = (lane & 7) * 4;
 #pragma unroll 1
