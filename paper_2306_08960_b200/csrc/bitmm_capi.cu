@@ -312,6 +312,9 @@ bool use_fp4() {
 constexpr int kF4BN = 192;  // 2 x 192 accumulator columns + scale-factor columns <= 512
 constexpr int kI8BN = 256;  // 256-wide int8 tiles (128-wide measured worse: DESIGN.md)
 int64_t kpad_for(int64_t k, bool fp4) { return round_up(k, fp4 ? 2 * TC_BK_BYTES : TC_BK_BYTES); }
+// Units = acc << shift. The e2m1 expansion stores a 2-bit level p as p / 2 (unpack.cuh), so
+// each level operand of an FP4 GEMM adds one to the reference shift (exact: powers of two).
+int fp4_shift(int shift, int level_operands, bool fp4) { return shift + (fp4 ? level_operands : 0); }
 int64_t row_bytes(int64_t kpad, bool fp4) { return fp4 ? kpad / 2 : kpad; }
 
 // One GEMM problem over expanded operands A8 [m][row_bytes], B8 [n][row_bytes]; `p` carries
@@ -347,8 +350,9 @@ int run_tc_group(DeviceState& st, const GemmProblem* probs, int count, cudaStrea
     p.M = static_cast<int>(q.m);
     p.N = static_cast<int>(q.n);
     p.num_kb = static_cast<int>(rb / TC_BK_BYTES);
-    // |acc| <= 9K, so |units| = |acc| << shift < 2^22 allows the magic-add float -> int
-    p.small_acc = ((9 * q.kpad) << p.shift) < (int64_t{1} << 22) ? 1 : 0;
+    // |units| <= 36K (2/2: 4 * 9 per element), so 36 * kpad < 2^22 allows the magic-add
+    // float -> int conversion
+    p.small_acc = 36 * q.kpad < (int64_t{1} << 22) ? 1 : 0;
     p.shift_mul = static_cast<float>(1 << p.shift);
     p.num_m_blocks = static_cast<int>((q.m + S::TILE_M - 1) / S::TILE_M);
     p.num_n_blocks = static_cast<int>((q.n + BN - 1) / BN);
@@ -573,7 +577,8 @@ int gemm_1x2_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, float gamma
                             B8, st.status, s, fp4));
   // kernels.cpp:193: half_scale = 0.5f * gamma * a_packed.scale * a_packed.gamma.value_or(1.0f)
   const float scale = 0.5f * gamma * a_scale * (has_a_gamma ? a_gamma : 1.0f);
-  return run_int_gemm(st, A8, B8, m, n, kpad, 1, scale, row_scale, col_scale, c_units, c, ldc, s, fp4);
+  return run_int_gemm(st, A8, B8, m, n, kpad, fp4_shift(1, 1, fp4), scale, row_scale, col_scale,
+                      c_units, c, ldc, s, fp4);
 }
 
 int gemm_2x2_dev_impl(DeviceState& st, const uint64_t* wt, const uint64_t* wh, const uint64_t* wm,
@@ -592,7 +597,8 @@ int gemm_2x2_dev_impl(DeviceState& st, const uint64_t* wt, const uint64_t* wh, c
   // kernels.cpp:232-233
   const float scale = 0.25f * w_scale * a_scale * (has_w_gamma ? w_gamma : 1.0f) *
                       (has_a_gamma ? a_gamma : 1.0f);
-  return run_int_gemm(st, A8, B8, m, n, kpad, 2, scale, row_scale, col_scale, c_units, c, ldc, s, fp4);
+  return run_int_gemm(st, A8, B8, m, n, kpad, fp4_shift(2, 2, fp4), scale, row_scale, col_scale,
+                      c_units, c, ldc, s, fp4);
 }
 
 cudaLaunchAttribute pdl_attr() {
@@ -802,7 +808,7 @@ int apb2_dev_impl(DeviceState& st, int64_t rows, int64_t cols, int64_t wpr, floa
   BITMM_TRY(run_unpack_pair({bin, nullptr, nullptr, rows, false}, {t, h, m, tokens, true}, wpr, cols,
                             kpad, A8, B8, st.status, s, fp4));
   GemmProblem q{A8, B8, rows, tokens, kpad, TcParams{}};
-  q.p.shift = 1;
+  q.p.shift = fp4_shift(1, 1, fp4);
   q.p.scale = 0.5f * alpha * a_scale * a_gamma;  // kernels.cpp:193 order
   q.p.row_scale = row_alpha;
   q.p.row_pre = 0.5f;
@@ -1553,6 +1559,7 @@ int bitmm_gemm_batch_dev(const bitmm_gemm_item* items, int count, void* stream) 
     }
     const float* rs = it.routine == BITMM_ROUTINE_1X1 ? nullptr : it.row_scale;
     const float* cs = it.routine == BITMM_ROUTINE_1X1 ? nullptr : it.col_scale;
+    shift = fp4_shift(shift, static_cast<int>(planes_a) + static_cast<int>(planes_b), fp4);
     np += make_problems(A8, B8, it.m, it.n, kpad, shift, scale, rs, cs, it.c_units, it.c, it.ldc,
                         probs + np);
   }

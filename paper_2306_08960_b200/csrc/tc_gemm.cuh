@@ -82,7 +82,7 @@ struct TcParams {
   // F32R: per-row scale factors in the reference's multiplication order
   float row_pre, act_scale, act_gamma;
   int tma_store;     // 1: output through the tensor map (ldc*4 % 16 == 0, 16B-aligned base)
-  int small_acc;     // F4: every |accumulator| < 2^22 (9K < 2^22), float -> int by magic add
+  int small_acc;     // F4: every |units| < 2^22 (36 * kpad < 2^22), float -> int by magic add
   float shift_mul;   // F4: 2^shift
   int epi;           // this problem's epilogue (Epi::I32 / Epi::F32) under Epi::ANY
   int num_m_blocks, num_n_blocks, num_tiles;

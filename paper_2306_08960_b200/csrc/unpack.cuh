@@ -113,29 +113,42 @@ __device__ __forceinline__ int expand_slice_warp(const UnpackOperand& o, long lo
   }
   if (fp4) {
     // e2m1 operands with a K-permutation inside each 32-element group: source bit j of a
-    // 32-bit word goes to output word j % 4, nibble j / 4, so output word q is
-    // (bits >> q) & 0x11111111 shifted into place. Both GEMM operands use the same
-    // permutation, so every dot product is unchanged. Lane t writes the 16 output bytes of
-    // its own word: each warp store covers 512 contiguous bytes.
+    // 32-bit word goes to output word j % 4, nibble j / 4, so output word q collects bits
+    // q, q+4, ... shifted into one bit position of every nibble. Both GEMM operands use the
+    // same permutation, so every dot product is unchanged. Codes (e2m1 values):
+    //   signs : +1 -> 0x2 (1.0), -1 -> 0xA (-1.0), padding -> 0x0
+    //   levels: p -> p as a nibble = p / 2 (0, 0.5, 1, 1.5), exact; the GEMM's epilogue
+    //           shift adds a factor 2 per level operand (fp4_shift, bitmm_capi.cu)
+    // Full words take two instructions per output word (a funnel shift and one LOP3).
+    // Lane t writes the 16 output bytes of its own word: each warp store covers 512
+    // contiguous bytes.
     uint8_t* out_row = o.out + r * (kpad / 2);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int g = word0 + j * 32 + lane;
       if (g * 32 >= kpad) continue;
       uint32_t ow[4];
+      const uint32_t valid = valid_mask32(g * 32, K);
       if (o.levels == 0) {
-        const uint32_t valid = valid_mask32(g * 32, K);
-        const uint32_t neg = valid & ~s.w0[j];
+        if (valid == 0xFFFFFFFFu) {
+          const uint32_t w = s.w0[j];
+          // bit 4n+q -> nibble n bit 3 (the sign), then 0x2 in every nibble
+          ow[0] = (~(w << 3) & 0x88888888u) | 0x22222222u;
+          ow[1] = (~(w << 2) & 0x88888888u) | 0x22222222u;
+          ow[2] = (~(w << 1) & 0x88888888u) | 0x22222222u;
+          ow[3] = (~w & 0x88888888u) | 0x22222222u;
+        } else {
+          const uint32_t neg = valid & ~s.w0[j];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)  // +1 -> 0x2, -1 -> 0xA, padding -> 0
-          ow[q] = (((valid >> q) & 0x11111111u) << 1) | (((neg >> q) & 0x11111111u) << 3);
+          for (int q = 0; q < 4; ++q)
+            ow[q] = (((valid >> q) & 0x11111111u) << 1) | (((neg >> q) & 0x11111111u) << 3);
+        }
       } else {
         const uint32_t hi = s.w0[j], lo = s.w1[j];  // already masked to K
-        const uint32_t b0 = hi & lo, b1 = ~hi & lo;
-#pragma unroll
-        for (int q = 0; q < 4; ++q)  // p -> 0x0 / 0x2 / 0x4 / 0x5
-          ow[q] = (((hi >> q) & 0x11111111u) << 2) | ((b0 >> q) & 0x11111111u) |
-                  (((b1 >> q) & 0x11111111u) << 1);
+        ow[0] = ((hi << 1) & 0x22222222u) | (lo & 0x11111111u);
+        ow[1] = (hi & 0x22222222u) | ((lo >> 1) & 0x11111111u);
+        ow[2] = ((hi >> 1) & 0x22222222u) | ((lo >> 2) & 0x11111111u);
+        ow[3] = ((hi >> 2) & 0x22222222u) | ((lo >> 3) & 0x11111111u);
       }
       *reinterpret_cast<uint4*>(out_row + static_cast<long long>(g) * 16) =
           make_uint4(ow[0], ow[1], ow[2], ow[3]);
