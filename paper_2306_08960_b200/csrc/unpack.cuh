@@ -195,6 +195,49 @@ __device__ __forceinline__ int expand_slice_warp(const UnpackOperand& o, long lo
   return __reduce_or_sync(0xFFFFFFFFu, bad);
 }
 
+// Fast path of the e2m1 expansion for a slice lying wholly inside K and inside the words
+// of the row (every slice when K is a multiple of 4096): no per-word bounds checks, one base
+// address per plane and immediate offsets, so the warp spends its instructions on loads,
+// validation, expansion and stores. Same output and flags as expand_slice_warp.
+__device__ __forceinline__ int unpack_slice_fp4_full(const UnpackOperand& o, long long r, int sl,
+                                                     int lane) {
+  const long long src = r * o.wpr32 + sl * 128 + lane;
+  uint4* dst = reinterpret_cast<uint4*>(o.out + r * (o.kpad / 2)) + sl * 128 + lane;
+  if (o.levels == 0) {
+    const uint32_t* w0 = o.w0 + src;
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) w[j] = __ldg(w0 + 32 * j);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)  // +1 -> 0x2, -1 -> 0xA (see expand_slice_warp)
+      dst[32 * j] = make_uint4((~(w[j] << 3) & 0x88888888u) | 0x22222222u,
+                               (~(w[j] << 2) & 0x88888888u) | 0x22222222u,
+                               (~(w[j] << 1) & 0x88888888u) | 0x22222222u,
+                               (~w[j] & 0x88888888u) | 0x22222222u);
+    return 0;
+  }
+  const uint32_t *pt = o.w0 + src, *ph = o.w1 + src, *pm = o.w2 + src;
+  uint32_t t[4], h[4], m[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    t[j] = __ldg(pt + 32 * j);
+    h[j] = __ldg(ph + 32 * j);
+    m[j] = __ldg(pm + 32 * j);
+  }
+  uint32_t illegal = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    // legal (t,h,m): (0,0,1) (0,0,0) (0,1,0) (1,0,1) (transform.cpp:56-71)
+    illegal |= (t[j] & h[j]) | (t[j] & ~m[j]) | (h[j] & m[j]);
+    const uint32_t hi = t[j] | h[j], lo = t[j] | ~(h[j] | m[j]);  // p = 2 hi + lo
+    dst[32 * j] = make_uint4(((hi << 1) & 0x22222222u) | (lo & 0x11111111u),
+                             (hi & 0x22222222u) | ((lo >> 1) & 0x11111111u),
+                             ((hi >> 1) & 0x22222222u) | ((lo >> 2) & 0x11111111u),
+                             ((hi >> 2) & 0x22222222u) | ((lo >> 3) & 0x11111111u));
+  }
+  return __any_sync(0xFFFFFFFFu, illegal != 0) ? ERR_ENCODING : 0;
+}
+
 __device__ __forceinline__ int unpack_slice_warp(const UnpackOperand& o, long long r, int sl, int K,
                                                  int kpad, int lane, bool fp4) {
   SliceWords s;
@@ -229,8 +272,11 @@ __global__ void __launch_bounds__(256) unpack_operands(const __grid_constant__ U
     r = unit / slices;
     sl = static_cast<int>(unit - r * slices);
   }
-  const int bad = P.fp4 ? unpack_slice_warp(o, r, sl, o.K, o.kpad, lane, true)
-                        : unpack_slice_warp(o, r, sl, o.K, o.kpad, lane, false);
+  // warp-uniform: the slice's 4096 elements are all inside K and inside the row's words
+  const bool full = (sl + 1) * 128 <= o.wpr32 && (sl + 1) * 4096 <= o.K;
+  const int bad = !P.fp4 ? unpack_slice_warp(o, r, sl, o.K, o.kpad, lane, false)
+                  : full ? unpack_slice_fp4_full(o, r, sl, lane)
+                         : unpack_slice_warp(o, r, sl, o.K, o.kpad, lane, true);
   if (bad && lane == 0) atomicOr(P.err, bad);
 }
 

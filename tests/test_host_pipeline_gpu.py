@@ -81,3 +81,28 @@ def test_errors_in_the_last_slice():
     bad = api.ThmPlanes(_bm(8200, 777, wpr2, t), _bm(8200, 777, wpr2, h), _bm(8200, 777, wpr2, mm))
     with pytest.raises(api.InvalidEncoding):
         api.gemm_1x2(_bm(1100, 777, wpr2, w), 1.0, bad)
+
+
+@pytest.mark.parametrize("k", [4096, 8192])
+def test_illegal_planes_in_full_slices(k):
+    """K a multiple of 4096: every slice takes the expansion's full-slice fast path, which
+    validates the plane states itself. One illegal state (t = h = 1) anywhere must still
+    surface as InvalidEncoding, for either operand of 2/2."""
+    rng = np.random.default_rng(k)
+    m, n = 300, 260
+    for side in ("w", "a"):
+        wp, (wt, wh, wm, wpr) = _planes(rng, m, k)
+        ap, (at, ah, am, _) = _planes(rng, n, k)
+        t, h = (wt, wh) if side == "w" else (at, ah)
+        row = 7 if side == "w" else n - 1
+        t[row, wpr - 1] |= np.uint64(1) << np.uint64(40)
+        h[row, wpr - 1] |= np.uint64(1) << np.uint64(40)
+        with pytest.raises(api.InvalidEncoding):
+            api.gemm_2x2(wp, ap)
+    # and a clean call right after still matches the device path
+    wp, (wt, wh, wm, _) = _planes(rng, m, k)
+    ap, (at, ah, am, _) = _planes(rng, n, k)
+    got = api.gemm_2x2(wp, ap)
+    want = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    device.gemm_2x2(*[_dev(x) for x in (wt, wh, wm, at, ah, am)], k, out=want)
+    assert np.array_equal(got, want.cpu().numpy())
