@@ -40,13 +40,6 @@ inline int spmm_smem_bytes(long long K, int rows_per_split) {
   return static_cast<int>((K + 1) * SPMM_TOK * 4 + (rows_per_split + 1) * 4);
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-}
 
 // LEVELS source: activation planes {t,h,m} [tokens][wpr] (K-packed per token, the
 // a_packed orientation of gemm_1x2) dequantized to d[p] = float(p) * (s * gamma_a) while

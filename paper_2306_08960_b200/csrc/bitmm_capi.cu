@@ -708,19 +708,40 @@ int apb_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, int64_t k, int64
                                       static_cast<int>(kpad), Ah, st.status));
     BITMM_TRY(launch_check("unpack_sign_f16"));
   }
-  {
+  const int strip_smem = static_cast<int>(kpad * 32 * 4);
+  if (strip_smem <= 112 * 1024) {
+    // one pass: a block stages a 32-token strip of X, takes the token maxima and splits
+    static bool attr_set = false;
+    if (!attr_set) {
+      BITMM_CUDA_TRY(cudaFuncSetAttribute(split_x_f16_strip, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          112 * 1024));
+      attr_set = true;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>((n + 31) / 32));
-    cfg.blockDim = dim3(1024);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = strip_smem;
     cfg.stream = s;
     cfg.attrs = pdl;
     cfg.numAttrs = 1;
-    ProfScope ps("x_token_scale", s);
-    BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, x_token_scale, b, static_cast<long long>(ldb),
-                                      static_cast<int>(k), static_cast<int>(n), tok_scale));
-    BITMM_TRY(launch_check("x_token_scale"));
-  }
-  {
+    ProfScope ps("split_x_f16_strip", s);
+    BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, split_x_f16_strip, b, static_cast<long long>(ldb),
+                                      static_cast<int>(k), static_cast<int>(n),
+                                      static_cast<int>(kpad), tok_scale, XT));
+    BITMM_TRY(launch_check("split_x_f16_strip"));
+  } else {
+    {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(static_cast<unsigned>((n + 31) / 32));
+      cfg.blockDim = dim3(1024);
+      cfg.stream = s;
+      cfg.attrs = pdl;
+      cfg.numAttrs = 1;
+      ProfScope ps("x_token_scale", s);
+      BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, x_token_scale, b, static_cast<long long>(ldb),
+                                        static_cast<int>(k), static_cast<int>(n), tok_scale));
+      BITMM_TRY(launch_check("x_token_scale"));
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(kpad / 64), static_cast<unsigned>((n + 31) / 32));
     cfg.blockDim = dim3(256);

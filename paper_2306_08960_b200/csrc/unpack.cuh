@@ -414,4 +414,88 @@ __global__ void split_x_f16(const float* __restrict__ X, long long ldx, int K, i
   *reinterpret_cast<uint4*>(row + kpad) = make_uint4(lo2[0], lo2[1], lo2[2], lo2[3]);
 }
 
+// x_token_scale + split_x_f16 in one pass for K small enough that a 32-token strip of X
+// fits in shared memory (kpad * 128 B; config 4: 96 KB, two blocks per SM): the block stages
+// its strip [kpad][32] fp32 (16-byte chunk c of row k at c ^ ((k >> 3) & 7), so both the
+// cp.async writes and the transposed reads below are conflict-free), takes each token's
+// maximum, and splits from shared memory. X is read once instead of twice, and the whole
+// matrix is in flight in one wave. Same outputs as the two-kernel path.
+__device__ __forceinline__ int strip_idx(int k, int n) {
+  return k * 32 + ((((n >> 2) ^ (k >> 3)) & 7) << 2) + (n & 3);
+}
+
+__global__ void __launch_bounds__(256) split_x_f16_strip(const float* __restrict__ X, long long ldx,
+                                                         int K, int N, int kpad,
+                                                         float* __restrict__ tok_scale,
+                                                         uint16_t* __restrict__ XT) {
+  extern __shared__ float xs[];  // [kpad][32], swizzled
+  __shared__ float red[8][33];
+  __shared__ float sscale[32];
+  pdl_wait();
+  pdl_launch_dependents();
+  const int n0 = blockIdx.x * 32;
+  const int tid = threadIdx.x;
+  const bool vec = n0 + 32 <= N && (ldx & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+  // stage the strip: 8 chunks of 16 B per row; rows past K and tokens past N are zero
+  for (int i = tid; i < kpad * 8; i += 256) {
+    const int k = i >> 3, c = i & 7;
+    float* dst = &xs[k * 32 + (((c ^ (k >> 3)) & 7) << 2)];
+    const float* src = X + static_cast<long long>(k) * ldx + n0 + 4 * c;
+    if (k < K && vec) {
+      cp_async16(dst, src);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) dst[e] = (k < K && n0 + 4 * c + e < N) ? src[e] : 0.0f;
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  {
+    const int n = tid & 31;
+    float mx = 0.f;
+    for (int k = tid >> 5; k < K; k += 8) mx = fmaxf(mx, fabsf(xs[strip_idx(k, n)]));
+    red[tid >> 5][n] = mx;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    float mx = red[0][tid];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) mx = fmaxf(mx, red[i][tid]);
+    int e = 0;
+    if (mx > 0.f && mx <= 3.402823466e38f) {
+      int q;
+      frexpf(mx, &q);  // mx = f * 2^q, f in [0.5, 1)
+      e = min(126, max(-126, 15 - q));
+    }
+    sscale[tid] = ldexpf(1.0f, e);
+    if (n0 + tid < N) tok_scale[n0 + tid] = ldexpf(1.0f, -e);
+  }
+  __syncthreads();
+  const int nl = tid >> 3;        // token 0..31
+  const int kl = (tid & 7) * 8;   // 8 consecutive k per thread
+  const int n = n0 + nl;
+  if (n >= N) return;
+  const float sc = sscale[nl];
+  uint16_t* row = XT + static_cast<long long>(n) * 2 * kpad;
+  for (int k0 = 0; k0 < kpad; k0 += 64) {
+    uint32_t hi2[4], lo2[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t h[2], l[2];
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        const float xv = xs[strip_idx(k0 + kl + 2 * q + d, nl)] * sc;  // exact: a power of two
+        const __half hv = __float2half_rn(xv);
+        const __half lv = __float2half_rn(xv - __half2float(hv));
+        h[d] = __half_as_ushort(hv);
+        l[d] = __half_as_ushort(lv);
+      }
+      hi2[q] = h[0] | (h[1] << 16);
+      lo2[q] = l[0] | (l[1] << 16);
+    }
+    *reinterpret_cast<uint4*>(row + k0 + kl) = make_uint4(hi2[0], hi2[1], hi2[2], hi2[3]);
+    *reinterpret_cast<uint4*>(row + kpad + k0 + kl) = make_uint4(lo2[0], lo2[1], lo2[2], lo2[3]);
+  }
+}
+
 }  // namespace bitmm_dev
