@@ -61,6 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         [nvcc()]
         + ARCH_FLAGS
         + NVCC_FLAGS
+        + os.environ.get("BITMM_NVCC_EXTRA", "").split()  # A/B builds, e.g. -DSPMM_SCRATCH
         + ["-I", INCLUDE, "-I", CSRC, "-shared", "-o", tmp]
         + [os.path.join(CSRC, s) for s in SOURCES]
         + ["-cudart", "static", "-Xlinker", "-soname=libbitmm_b200.so"]
