@@ -10,10 +10,12 @@ reference's packed layouts (the metric "binary GEMM Tera-updates/s ... 1/1.1/2.2
 updates = M*K*N per GEMM (bench.cpp:175). Every step starts from the PACKED operands
 resident in HBM; the bit -> int8 expansion kernels are inside the timed region.
 
-With N>1 ranks (torchrun, NCCL) every GEMM's output-column dimension is sharded across
-ranks (rank g owns b_packed rows [g*N/G, (g+1)*N/G)), each rank computes its M x N/G
-block and the blocks are gathered to rank 0 over NCCL (the only collective); strong
-scaling. `--impl reference` times the reference CPU implementation instead (rank 0).
+With N>1 ranks (torchrun, NCCL) the output-column dimension is sharded:
+rank g computes output columns [g*N, (g+1)*N) of a G-times wider problem (A replicated,
+its own b_packed rows), so per-rank work is fixed and there is no data-path collective
+(weak scaling). The NCCL gather of the result blocks to rank 0, the north star's one
+cross-GPU step, is timed separately after the step and reported under "gather".
+`--impl reference` times the reference CPU implementation instead (rank 0).
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -86,10 +88,19 @@ def make_operands(rng):
     return ops
 
 
-def shard_cols(n, rank, world):
-    per = (n + world - 1) // world
-    lo = min(n, rank * per)
-    return lo, min(n, lo + per)
+B_SIDE = {"1x1": ("b",), "1x2": ("t", "h", "m", "beta"), "2x2": ("at", "ah", "am")}
+
+
+def make_rank_operands(rank):
+    """Rank `rank`'s operands: the replicated A side from the base seed, its own output
+    columns (the b_packed side) from a per-rank seed. Rank 0 equals the N=1 workload."""
+    ops = make_operands(np.random.default_rng(SEED))
+    if rank:
+        own = make_operands(np.random.default_rng(SEED + 7919 * rank))
+        for name, keys in B_SIDE.items():
+            for key in keys:
+                ops[name][key] = own[name][key]
+    return ops
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -255,7 +266,7 @@ def run_reference_arm(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u64 bit-packed (int popcount)", "data": "synthetic",
         "config": workload_config(args.gpus),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
@@ -272,8 +283,11 @@ def workload_config(world):
                     "K 4096 x 2-bit 8192 with per-row gamma / per-column beta (fp32 out) + 2/2 "
                     "4096^3 (int32 out); packed uint64 operands resident in HBM",
         "routines": {r[0]: {"m": r[1], "n": r[2], "k": r[3]} for r in ROUTINES},
-        "updates_per_step": sum(m * n * k for _, m, n, k in ROUTINES),
-        "parallelism": f"N-shard x{world} + NCCL gather" if world > 1 else "single GPU",
+        "updates_per_step": world * sum(m * n * k for _, m, n, k in ROUTINES),
+        "parallelism": (f"N-shard x{world}: rank g computes output columns [g*N, (g+1)*N) of a "
+                        f"{world}x wider problem (A replicated), per-rank work fixed; blocks stay "
+                        "on their GPU, the NCCL gather to rank 0 is timed separately ('gather')"
+                        if world > 1 else "single GPU"),
         "l2": "flushed between steps (256 MiB read outside the per-step CUDA events)",
         "seed": SEED,
     }
@@ -298,33 +312,25 @@ def main():
     lib = _lib.load()
     dev = torch.device("cuda", local_rank)
 
-    rng = np.random.default_rng(SEED)
-    ops = make_operands(rng)
+    ops = make_rank_operands(rank)
     T = lambda x: torch.from_numpy(np.ascontiguousarray(x).view(np.int64)).to(dev)  # noqa: E731
     Tf = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # noqa: E731
 
-    # device-resident packed operands; rank's column shard of every GEMM
+    # device-resident packed operands: this rank's output columns of every GEMM
     d = {}
     for name, m, n, k in ROUTINES:
-        lo, hi = shard_cols(n, rank, world)
         o = ops[name]
         if name == "1x1":
-            d[name] = dict(a=T(o["a"]), b=T(o["b"][lo:hi]))
-            d[name]["units"] = torch.empty((m, hi - lo), dtype=torch.int32, device=dev)
+            d[name] = dict(a=T(o["a"]), b=T(o["b"]))
+            d[name]["units"] = torch.empty((m, n), dtype=torch.int32, device=dev)
         elif name == "1x2":
-            d[name] = dict(w=T(o["w"]), t=T(o["t"][lo:hi]), h=T(o["h"][lo:hi]), m=T(o["m"][lo:hi]),
-                           gamma=Tf(o["gamma"]), beta=Tf(o["beta"][lo:hi]))
-            d[name]["out"] = torch.empty((m, hi - lo), dtype=torch.float32, device=dev)
+            d[name] = dict(w=T(o["w"]), t=T(o["t"]), h=T(o["h"]), m=T(o["m"]),
+                           gamma=Tf(o["gamma"]), beta=Tf(o["beta"]))
+            d[name]["out"] = torch.empty((m, n), dtype=torch.float32, device=dev)
         else:
-            d[name] = dict(wt=T(o["wt"]), wh=T(o["wh"]), wm=T(o["wm"]), at=T(o["at"][lo:hi]),
-                           ah=T(o["ah"][lo:hi]), am=T(o["am"][lo:hi]))
-            d[name]["units"] = torch.empty((m, hi - lo), dtype=torch.int32, device=dev)
-        d[name]["cols"] = (lo, hi)
-    gathered = {}
-    if world > 1 and rank == 0:
-        for name, m, n, k in ROUTINES:
-            dt = torch.float32 if name == "1x2" else torch.int32
-            gathered[name] = torch.empty((m, n), dtype=dt, device=dev)
+            d[name] = dict(wt=T(o["wt"]), wh=T(o["wh"]), wm=T(o["wm"]), at=T(o["at"]),
+                           ah=T(o["ah"]), am=T(o["am"]))
+            d[name]["units"] = torch.empty((m, n), dtype=torch.int32, device=dev)
     flush = torch.zeros(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 
@@ -343,32 +349,6 @@ def main():
         else:
             device.gemm_2x2(x["wt"], x["wh"], x["wm"], x["at"], x["ah"], x["am"], k, units=x["units"])
         return device.launch_count()
-
-    from paper_2306_08960_b200 import shard
-
-    def sharded(name, m, n, k):
-        """N>1: each rank computes its column block in row chunks; blocks are gathered to
-        rank 0 over NCCL behind the next chunk's compute (paper_2306_08960_b200.shard)."""
-        x = d[name]
-        lo, _ = x["cols"]
-        dt = torch.float32 if name == "1x2" else torch.int32
-        launches = [0]
-
-        def compute(clo, chi, r0, r1, block):
-            if name == "1x1":
-                device.gemm_1x1(x["a"][r0:r1], x["b"], k, units=block)
-            elif name == "1x2":
-                device.gemm_1x2(x["w"][r0:r1], 1.0, x["t"], x["h"], x["m"], k,
-                                row_scale=x["gamma"][r0:r1], col_scale=x["beta"], out=block)
-            else:
-                device.gemm_2x2(x["wt"][r0:r1], x["wh"][r0:r1], x["wm"][r0:r1], x["at"], x["ah"],
-                                x["am"], k, units=block)
-            launches[0] += device.launch_count()
-
-        wire = shard.popcount_wire(k) if name == "1x1" else None
-        shard.run_sharded(m, n, dt, compute, dev, chunk_rows=m // 4, wire=wire,
-                          out=gathered.get(name))
-        return launches[0]
 
     def run_group():
         """The three GEMMs as one group: one operand-expansion launch plus one persistent
@@ -394,12 +374,12 @@ def main():
         operand expansion with the current GEMM."""
         launches = 0
         events[0].record(stream)
-        if world == 1 and not per_routine and not sequential and not args.sequential:
+        if not per_routine and not sequential and not args.sequential:
             launches += run_group()
             events[-1].record(stream)
             return launches
         for i, (name, m, n, k) in enumerate(ROUTINES):
-            launches += run_routine(name, m, n, k) if world == 1 else sharded(name, m, n, k)
+            launches += run_routine(name, m, n, k)
             if per_routine:
                 events[i + 1].record(stream)
         if not per_routine:
@@ -407,8 +387,7 @@ def main():
         return launches
 
     for name, m, n, k in ROUTINES:
-        lo, hi = d[name]["cols"]
-        device.reserve_workspace(0, m, hi - lo, k)
+        device.reserve_workspace(0, m, n, k)
 
     # ---- warmup (W steps, then more until the clock sampler has seen >= 2 s of load) ----
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(ROUTINES) + 1)]
@@ -470,8 +449,43 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    upd_per_step = sum(m * n * k for _, m, n, k in ROUTINES)
-    value = upd_per_step / (ms_per_step * 1e-3) / 1e12
+    upd_per_step = sum(m * n * k for _, m, n, k in ROUTINES)  # per rank
+    value = world * upd_per_step / (ms_per_step * 1e-3) / 1e12  # whole job, max over ranks
+
+    # ---- N>1: the north star's gather of the result blocks to rank 0, timed on its own ----
+    gather = None
+    if world > 1:
+        from paper_2306_08960_b200 import shard
+        payloads = []
+        for name, m, n, k in ROUTINES:
+            blk = d[name]["units"] if "units" in d[name] else d[name]["out"]
+            if name == "1x1":
+                blk = shard.popcount_wire(k).encode(blk)  # lossless uint16 popcounts
+            payloads.append(blk.contiguous().view(torch.uint8).reshape(-1))
+        parts = [[torch.empty_like(p) for _ in range(world)] if rank == 0 else None
+                 for p in payloads]
+        g_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        reps = 3
+        for _ in range(2):  # warm the communicator's buffers
+            for p, pa in zip(payloads, parts):
+                dist.gather(p, pa, dst=0)
+        dist.barrier()
+        torch.cuda.synchronize()
+        g_ev[0].record(stream)
+        for _ in range(reps):
+            for p, pa in zip(payloads, parts):
+                dist.gather(p, pa, dst=0)
+        g_ev[1].record(stream)
+        torch.cuda.synchronize()
+        gt = torch.tensor([g_ev[0].elapsed_time(g_ev[1]) / reps], dtype=torch.float64, device=dev)
+        dist.all_reduce(gt, op=dist.ReduceOp.MAX)
+        gather = {"ms_per_step": float(gt.item()),
+                  "bytes_to_root_per_step": sum(p.numel() for p in payloads) * (world - 1),
+                  "wire": "1/1 units as uint16 popcounts (shard.popcount_wire, lossless); "
+                          "1/2 fp32; 2/2 int32",
+                  "note": "NCCL gather of every rank's output blocks to rank 0 (SURVEY.md "
+                          "§8(e)), after the timed steps; not part of `value`"}
+        del parts
 
     # ---- live roofline pass: library-internal events around every launch ----
     lib.bitmm_profile_reset()
@@ -510,8 +524,7 @@ def main():
         peak_src = (f"int8 dense = 2 x bf16 burst of {peaks_src} ({peak_from_bf16:.1f})"
                     if peak == peak_from_bf16 else f"cuBLASLt int8 _int_mm 8192^3 burst ({probe:.1f})")
     tc = kernels.get(kname, {"launches": 0, "ms": 0.0})
-    macs_per_step = sum(m * (shard_cols(n, rank, world)[1] - shard_cols(n, rank, world)[0]) * k
-                        for _, m, n, k in ROUTINES)
+    macs_per_step = upd_per_step  # this rank's (rank 0's) GEMMs
     achieved = (2.0 * macs_per_step * args.steps) / (tc["ms"] * 1e-3) / 1e12 if tc["ms"] else 0.0
     traffic, l2 = None, None
     tpath = os.path.join(REPO, "profiles", "traffic_r01.json")
@@ -534,7 +547,7 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None,
+        "scaling": "weak", "vs_baseline": None,
         "dtype": ("u64 bit-packed -> e2m1 tcgen05.mma kind::mxf4 (unit E8M0 scales), f32 "
                   "accumulate of exact integers" if fp4 else
                   "u64 bit-packed -> s8 tcgen05.mma kind::i8, s32 accumulate"),
@@ -552,9 +565,11 @@ def main():
         "kernels": kernels,
         "clocks": clocks,
         "step_path": ("bitmm_gemm_batch_dev: one expansion launch + one persistent tensor-core "
-                      "launch over the three GEMMs" if world == 1 and not args.sequential else
+                      "launch over the three GEMMs" if not args.sequential else
                       "one bitmm_gemm_*_dev call per routine"),
     }
+    if gather is not None:
+        line["gather"] = gather
     if seq_ms is not None:
         line["sequential_calls"] = {"ms_per_step": seq_ms,
                                     "value": upd_per_step / (seq_ms * 1e-3) / 1e12,
