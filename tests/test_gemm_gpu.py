@@ -382,3 +382,34 @@ def test_extreme_accumulators_at_max_shared_dim(k):
     device.gemm_1x2(T(b[:m] if m <= n else a), 1.0, T(at), T(ah), T(am), k, units=u)
     device.status()
     assert bool((u == 6 * k).all())
+
+
+@pytest.mark.parametrize("k", [4095, 4096, 4097, 8192, 8193, 12288, 12352])
+def test_expansion_slice_boundaries(orc, k):
+    """K around 4096-element slice boundaries: rows mix full slices (the expansion's fast path,
+    no per-word checks) with a partial last slice (the checked path), for sign and plane
+    operands, with and without level scales (the p/2 level encoding folds into the shift)."""
+    rng = np.random.default_rng(k)
+    m, n = 67, 45
+    a, wpr = data.random_words(rng, m, k)
+    b, _ = data.random_words(rng, n, k)
+    at, ah, am, _ = data.random_planes(rng, n, k)
+    wt, wh, wm, _ = data.random_planes(rng, m, k)
+    u11 = np.empty((m, n), np.int32)
+    _units_host("bitmm_gemm_1x1_host", _p(a), m, _p(b), n, k, wpr, 1.0, 1.0, _p(u11), None, n)
+    assert np.array_equal(u11, orc.gemm_1x1(a, b, k, wpr)[0])
+    u12 = np.empty((m, n), np.int32)
+    _units_host("bitmm_gemm_1x2_host", _p(a), m, 1.0, _p(at), _p(ah), _p(am), n, k, wpr, 1.0, 0,
+                1.0, None, None, _p(u12), None, n)
+    assert np.array_equal(u12, orc.gemm_1x2(a, 1.0, at, ah, am, k, wpr)[0])
+    u22 = np.empty((m, n), np.int32)
+    _units_host("bitmm_gemm_2x2_host", _p(wt), _p(wh), _p(wm), m, 1.0, 0, 1.0, _p(at), _p(ah),
+                _p(am), n, k, wpr, 1.0, 0, 1.0, None, None, _p(u22), None, n)
+    assert np.array_equal(u22, orc.gemm_2x2(wt, wh, wm, at, ah, am, k, wpr)[0])
+    # scaled fp32 outputs (reference scale order) for the level routines
+    w_planes = api.ThmPlanes(*(api.BitMatrix.from_words(m, k, wpr, x) for x in (wt, wh, wm)), scale=0.25)
+    a_planes = api.ThmPlanes(*(api.BitMatrix.from_words(n, k, wpr, x) for x in (at, ah, am)), scale=0.5,
+                             gamma=1.5)
+    got = api.gemm_2x2(w_planes, a_planes)
+    want = orc.gemm_2x2(wt, wh, wm, at, ah, am, k, wpr, 0.25, 0.5, None, 1.5)[1]
+    assert np.array_equal(got, want)
