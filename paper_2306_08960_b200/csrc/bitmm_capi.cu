@@ -8,6 +8,8 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <set>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -87,6 +89,21 @@ int device_state(DeviceState** out) {
     st.init = true;
   }
   *out = &st;
+  return BITMM_OK;
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel, device and size (the
+// attribute is per device; a process may drive several).
+int ensure_max_smem(const void* fn, int bytes) {
+  int dev = 0;
+  BITMM_CUDA_TRY(cudaGetDevice(&dev));
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int>> done;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(fn, dev, bytes);
+  if (done.count(key)) return BITMM_OK;
+  BITMM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.insert(key);
   return BITMM_OK;
 }
 
@@ -331,12 +348,7 @@ template <Kind KIND, Epi EPI, int BN, int NP>
 int run_tc_group(DeviceState& st, const GemmProblem* probs, int count, cudaStream_t s) {
   using S = TcShape<true, BN>;
   auto kern = tc_gemm_kernel<KIND, EPI, BN, NP>;
-  // per-instantiation launch facts (the library drives one device per process)
-  static bool attrs_set = false;
-  if (!attrs_set) {
-    BITMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM));
-    attrs_set = true;
-  }
+  BITMM_TRY(ensure_max_smem(reinterpret_cast<const void*>(kern), S::SMEM));
   constexpr bool fp4 = KIND == Kind::F4;
   TcGroup<NP> g;
   memset(&g, 0, sizeof(g));
@@ -662,11 +674,7 @@ int run_spmm(DeviceState& st, int64_t rows, int64_t k, const uint64_t* row_ptr,
   }
   auto kern = spmm_xchunk_kernel<EXACT, PDL_CHAIN, LEVELS, ACCUM>;
   const int smem = spmm_smem_bytes(k, rows_per_split);
-  static bool attr_set = false;  // one flag per instantiation
-  if (!attr_set) {
-    BITMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-    attr_set = true;
-  }
+  BITMM_TRY(ensure_max_smem(reinterpret_cast<const void*>(kern), kMaxDynSmem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(chunks), static_cast<unsigned>(splits));
   cfg.blockDim = dim3(SPMM_THREADS);
@@ -711,12 +719,7 @@ int apb_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, int64_t k, int64
   const int strip_smem = static_cast<int>(kpad * 32 * 4);
   if (strip_smem <= 112 * 1024) {
     // one pass: a block stages a 32-token strip of X, takes the token maxima and splits
-    static bool attr_set = false;
-    if (!attr_set) {
-      BITMM_CUDA_TRY(cudaFuncSetAttribute(split_x_f16_strip, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          112 * 1024));
-      attr_set = true;
-    }
+    BITMM_TRY(ensure_max_smem(reinterpret_cast<const void*>(split_x_f16_strip), 112 * 1024));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>((n + 31) / 32));
     cfg.blockDim = dim3(256);
@@ -771,11 +774,7 @@ int apb_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, int64_t k, int64
   p.num_m_blocks = static_cast<int>((m + 255) / 256);
   p.num_n_blocks = static_cast<int>((n + APB_BN - 1) / APB_BN);
   p.num_tiles = p.num_m_blocks * p.num_n_blocks;
-  static bool attr_set = false;
-  if (!attr_set) {
-    BITMM_CUDA_TRY(cudaFuncSetAttribute(apb_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, APB_SMEM));
-    attr_set = true;
-  }
+  BITMM_TRY(ensure_max_smem(reinterpret_cast<const void*>(apb_gemm_kernel), APB_SMEM));
   const int units = std::min(p.num_tiles, st.sms / 2);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(2 * units));
