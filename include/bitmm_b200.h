@@ -261,6 +261,31 @@ int bitmm_quantize_thm_dev(const float* a, int64_t rows, int64_t cols, int64_t l
 int bitmm_quantize_thm_host(const float* a, int64_t rows, int64_t cols, int64_t lda, float s,
                             uint64_t* t, uint64_t* h, uint64_t* m, int64_t wpr);
 
+/* decompose_thm: replaces decompose_thm (transform.hpp:47, transform.cpp:47-75) on 2-bit levels
+ *   (TwoBitMatrix::levels: one byte per element, row-major rows x cols) -> {t,h,m} planes of `wpr`
+ *   words. A level above 3 is BITMM_ERR_INVALID_ARGUMENT ("2-bit level out of range"); the _dev
+ *   flavour latches it for bitmm_device_status(). */
+int bitmm_decompose_thm_dev(const uint8_t* levels, int64_t rows, int64_t cols, uint64_t* t,
+                            uint64_t* h, uint64_t* m, int64_t wpr, void* stream);
+int bitmm_decompose_thm_host(const uint8_t* levels, int64_t rows, int64_t cols, uint64_t* t,
+                             uint64_t* h, uint64_t* m, int64_t wpr);
+
+/* decompose_apb: replaces decompose_apb (apb.hpp:58, apb.cpp:119-142). bin = pack_signs(a) into
+ *   `wpr`-word rows; the residual is a CSR of every entry with |a| != alpha, in column order, value
+ *   a - alpha*sign(a) computed in double and rounded to float with ties away from zero
+ *   (apb.cpp:35-46). row_alpha (optional, `rows` entries) gives each row its own alpha (the
+ *   per-row alpha of BASELINE config 4); every alpha must be positive ("alpha must be positive",
+ *   BITMM_ERR_INVALID_ARGUMENT). Two calls: the first writes bin and row_ptr[rows+1] and returns
+ *   the residual size in *nnz (col_idx / vals may be NULL); when col_idx and vals hold at least
+ *   `capacity` >= *nnz entries they are filled too. Synchronous (the size comes back to the host). */
+int bitmm_decompose_apb_dev(const float* a, int64_t rows, int64_t cols, int64_t lda, float alpha,
+                            const float* row_alpha, uint64_t* bin, int64_t wpr, uint64_t* row_ptr,
+                            uint64_t* col_idx, float* vals, int64_t capacity, int64_t* nnz,
+                            void* stream);
+int bitmm_decompose_apb_host(const float* a, int64_t rows, int64_t cols, int64_t lda, float alpha,
+                             const float* row_alpha, uint64_t* bin, int64_t wpr, uint64_t* row_ptr,
+                             uint64_t* col_idx, float* vals, int64_t capacity, int64_t* nnz);
+
 #ifdef __cplusplus
 }
 #endif

@@ -117,6 +117,12 @@ SIGNATURES = {
     "bitmm_pack_signs_host": (_i, [_p, _i64, _i64, _i64, _p, _i64]),
     "bitmm_quantize_thm_dev": (_i, [_p, _i64, _i64, _i64, _f, _p, _p, _p, _i64, _p]),
     "bitmm_quantize_thm_host": (_i, [_p, _i64, _i64, _i64, _f, _p, _p, _p, _i64]),
+    "bitmm_decompose_thm_dev": (_i, [_p, _i64, _i64, _p, _p, _p, _i64, _p]),
+    "bitmm_decompose_thm_host": (_i, [_p, _i64, _i64, _p, _p, _p, _i64]),
+    "bitmm_decompose_apb_dev": (_i, [_p, _i64, _i64, _i64, _f, _p, _p, _i64, _p, _p, _p, _i64,
+                                     C.POINTER(_i64), _p]),
+    "bitmm_decompose_apb_host": (_i, [_p, _i64, _i64, _i64, _f, _p, _p, _i64, _p, _p, _p, _i64,
+                                      C.POINTER(_i64)]),
 }
 
 

@@ -3,6 +3,7 @@
 // launch sequence (unpack -> tcgen05 GEMM with fused epilogue) per routine.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cstdio>
@@ -481,6 +482,8 @@ int read_status(DeviceState& st, cudaStream_t s) {
   BITMM_CUDA_TRY(cudaMemset(st.status, 0, sizeof(int)));
   if (flag & ERR_ENCODING) return fail(BITMM_ERR_INVALID_ENCODING, "invalid ternary plane encoding or nonzero plane padding");
   if (flag & ERR_PADDING) return fail(BITMM_ERR_INVALID_ARGUMENT, "bit matrix padding must be zero");
+  if (flag & ERR_LEVEL) return fail(BITMM_ERR_INVALID_ARGUMENT, "2-bit level out of range");
+  if (flag & ERR_ALPHA) return fail(BITMM_ERR_INVALID_ARGUMENT, "alpha must be positive");
   return BITMM_OK;
 }
 
@@ -1448,6 +1451,140 @@ int bitmm_quantize_thm_host(const float* a, int64_t rows, int64_t cols, int64_t 
   BITMM_CUDA_TRY(cudaMemcpyAsync(t, dt, w_bytes, cudaMemcpyDeviceToHost, s));
   BITMM_CUDA_TRY(cudaMemcpyAsync(h, dh, w_bytes, cudaMemcpyDeviceToHost, s));
   BITMM_CUDA_TRY(cudaMemcpyAsync(m, dm, w_bytes, cudaMemcpyDeviceToHost, s));
+  BITMM_CUDA_TRY(cudaStreamSynchronize(s));
+  return BITMM_OK;
+}
+
+int bitmm_decompose_thm_dev(const uint8_t* levels, int64_t rows, int64_t cols, uint64_t* t,
+                            uint64_t* h, uint64_t* m, int64_t wpr, void* stream) {
+  g_launches = 0;
+  BITMM_TRY(check_pack_args(rows, cols, cols, wpr));
+  if (rows == 0 || wpr == 0) return BITMM_OK;
+  if (!t || !h || !m || (cols > 0 && !levels)) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ProfScope ps("decompose_thm", s);
+  decompose_thm_kernel<<<pack_blocks(*st, rows, wpr), 256, 0, s>>>(
+      levels, rows, static_cast<int>(cols), static_cast<int>(wpr),
+      reinterpret_cast<unsigned long long*>(t), reinterpret_cast<unsigned long long*>(h),
+      reinterpret_cast<unsigned long long*>(m), st->status);
+  return launch_check("decompose_thm_kernel");
+}
+
+int bitmm_decompose_thm_host(const uint8_t* levels, int64_t rows, int64_t cols, uint64_t* t,
+                             uint64_t* h, uint64_t* m, int64_t wpr) {
+  g_launches = 0;
+  BITMM_TRY(check_pack_args(rows, cols, cols, wpr));
+  if (rows == 0 || wpr == 0) return BITMM_OK;
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  cudaStream_t s = st->stream;
+  const size_t l_bytes = rows * cols, w_bytes = rows * wpr * 8;
+  BITMM_TRY(arena_reserve(st->io, align_up(l_bytes, 1024) + 3 * align_up(w_bytes, 1024) + 4096));
+  Carve cv(st->io.ptr);
+  uint8_t* dl = cv.take<uint8_t>(l_bytes);
+  uint64_t* dt = cv.take<uint64_t>(w_bytes);
+  uint64_t* dh = cv.take<uint64_t>(w_bytes);
+  uint64_t* dm = cv.take<uint64_t>(w_bytes);
+  if (l_bytes) BITMM_CUDA_TRY(cudaMemcpyAsync(dl, levels, l_bytes, cudaMemcpyHostToDevice, s));
+  BITMM_TRY(bitmm_decompose_thm_dev(dl, rows, cols, dt, dh, dm, wpr, s));
+  BITMM_TRY(read_status(*st, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(t, dt, w_bytes, cudaMemcpyDeviceToHost, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(h, dh, w_bytes, cudaMemcpyDeviceToHost, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(m, dm, w_bytes, cudaMemcpyDeviceToHost, s));
+  BITMM_CUDA_TRY(cudaStreamSynchronize(s));
+  return BITMM_OK;
+}
+
+// decompose_apb: pack the signs, count each row's residual entries, scan the counts into
+// row_ptr, bring the total back, and (when the caller's buffers hold it) fill the CSR.
+int bitmm_decompose_apb_dev(const float* a, int64_t rows, int64_t cols, int64_t lda, float alpha,
+                            const float* row_alpha, uint64_t* bin, int64_t wpr, uint64_t* row_ptr,
+                            uint64_t* col_idx, float* vals, int64_t capacity, int64_t* nnz,
+                            void* stream) {
+  g_launches = 0;
+  if (row_alpha == nullptr && !(alpha > 0.0f)) return fail(BITMM_ERR_INVALID_ARGUMENT, "alpha must be positive");
+  BITMM_TRY(check_pack_args(rows, cols, lda, wpr));
+  if (!nnz || !row_ptr || (rows > 0 && wpr > 0 && !bin) || (rows > 0 && cols > 0 && !a))
+    return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto* rp = reinterpret_cast<unsigned long long*>(row_ptr);
+  BITMM_CUDA_TRY(cudaMemsetAsync(rp, 0, sizeof(unsigned long long), s));
+  if (rows > 0) {
+    if (wpr > 0) {
+      ProfScope ps("pack_signs", s);
+      pack_signs_kernel<<<pack_blocks(*st, rows, wpr), 256, 0, s>>>(
+          a, rows, static_cast<int>(cols), lda, static_cast<int>(wpr),
+          reinterpret_cast<unsigned long long*>(bin));
+      BITMM_TRY(launch_check("pack_signs_kernel"));
+    }
+    const unsigned blocks = static_cast<unsigned>(std::min<long long>((rows + 7) / 8, 32LL * st->sms));
+    {
+      ProfScope ps("decompose_apb_count", s);
+      decompose_apb_count_kernel<<<blocks, 256, 0, s>>>(a, rows, static_cast<int>(cols), lda, alpha,
+                                                        row_alpha, rp, st->status);
+      BITMM_TRY(launch_check("decompose_apb_count_kernel"));
+    }
+    size_t temp = 0;
+    BITMM_CUDA_TRY(cub::DeviceScan::InclusiveSum(nullptr, temp, rp + 1, rp + 1, static_cast<int>(rows), s));
+    BITMM_TRY(arena_reserve(st->ws, temp + 256));
+    BITMM_CUDA_TRY(cub::DeviceScan::InclusiveSum(st->ws.ptr, temp, rp + 1, rp + 1, static_cast<int>(rows), s));
+  }
+  unsigned long long total = 0;
+  BITMM_CUDA_TRY(cudaMemcpyAsync(&total, rp + rows, sizeof(total), cudaMemcpyDeviceToHost, s));
+  BITMM_TRY(read_status(*st, s));  // synchronises; reports a non-positive row alpha
+  *nnz = static_cast<int64_t>(total);
+  if (rows == 0 || total == 0 || col_idx == nullptr || vals == nullptr ||
+      capacity < static_cast<int64_t>(total))
+    return BITMM_OK;
+  const unsigned blocks = static_cast<unsigned>(std::min<long long>((rows + 7) / 8, 32LL * st->sms));
+  ProfScope ps("decompose_apb_fill", s);
+  decompose_apb_fill_kernel<<<blocks, 256, 0, s>>>(a, rows, static_cast<int>(cols), lda, alpha,
+                                                   row_alpha, rp,
+                                                   reinterpret_cast<unsigned long long*>(col_idx), vals);
+  BITMM_TRY(launch_check("decompose_apb_fill_kernel"));
+  BITMM_CUDA_TRY(cudaStreamSynchronize(s));
+  return BITMM_OK;
+}
+
+int bitmm_decompose_apb_host(const float* a, int64_t rows, int64_t cols, int64_t lda, float alpha,
+                             const float* row_alpha, uint64_t* bin, int64_t wpr, uint64_t* row_ptr,
+                             uint64_t* col_idx, float* vals, int64_t capacity, int64_t* nnz) {
+  g_launches = 0;
+  if (row_alpha == nullptr && !(alpha > 0.0f)) return fail(BITMM_ERR_INVALID_ARGUMENT, "alpha must be positive");
+  BITMM_TRY(check_pack_args(rows, cols, lda, wpr));
+  if (!nnz || !row_ptr || (rows > 0 && wpr > 0 && !bin) || (rows > 0 && cols > 0 && !a))
+    return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  DeviceState* st = nullptr;
+  BITMM_TRY(with_device(&st));
+  cudaStream_t s = st->stream;
+  const bool fill = col_idx != nullptr && vals != nullptr && capacity > 0;
+  const size_t a_bytes = rows * lda * 4, w_bytes = rows * wpr * 8, r_bytes = (rows + 1) * 8,
+               al_bytes = row_alpha ? rows * 4 : 0, ci_bytes = fill ? capacity * 8 : 0,
+               v_bytes = fill ? capacity * 4 : 0;
+  BITMM_TRY(arena_reserve(st->io, align_up(a_bytes, 1024) + align_up(w_bytes, 1024) +
+                                      align_up(r_bytes, 1024) + align_up(al_bytes, 1024) +
+                                      align_up(ci_bytes, 1024) + align_up(v_bytes, 1024) + 8192));
+  Carve cv(st->io.ptr);
+  float* da = cv.take<float>(a_bytes);
+  uint64_t* dw = cv.take<uint64_t>(w_bytes);
+  uint64_t* dr = cv.take<uint64_t>(r_bytes);
+  float* dal = row_alpha ? cv.take<float>(al_bytes) : nullptr;
+  uint64_t* dci = fill ? cv.take<uint64_t>(ci_bytes) : nullptr;
+  float* dv = fill ? cv.take<float>(v_bytes) : nullptr;
+  if (a_bytes) BITMM_CUDA_TRY(cudaMemcpyAsync(da, a, a_bytes, cudaMemcpyHostToDevice, s));
+  if (dal) BITMM_CUDA_TRY(cudaMemcpyAsync(dal, row_alpha, al_bytes, cudaMemcpyHostToDevice, s));
+  BITMM_TRY(bitmm_decompose_apb_dev(da, rows, cols, lda, alpha, dal, dw, wpr, dr, dci, dv, capacity,
+                                    nnz, s));
+  if (w_bytes) BITMM_CUDA_TRY(cudaMemcpyAsync(bin, dw, w_bytes, cudaMemcpyDeviceToHost, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(row_ptr, dr, r_bytes, cudaMemcpyDeviceToHost, s));
+  if (fill && *nnz > 0 && *nnz <= capacity) {
+    BITMM_CUDA_TRY(cudaMemcpyAsync(col_idx, dci, *nnz * 8, cudaMemcpyDeviceToHost, s));
+    BITMM_CUDA_TRY(cudaMemcpyAsync(vals, dv, *nnz * 4, cudaMemcpyDeviceToHost, s));
+  }
   BITMM_CUDA_TRY(cudaStreamSynchronize(s));
   return BITMM_OK;
 }

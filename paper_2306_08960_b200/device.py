@@ -186,6 +186,45 @@ def quantize_thm(a: torch.Tensor, s: float, lane_bits: int = 512, stream=None):
     return t, h, m
 
 
+def decompose_thm(levels: torch.Tensor, lane_bits: int = 512, stream=None):
+    """GPU decompose_thm (transform.cpp:47-75): uint8 levels [rows, cols] (TwoBitMatrix) ->
+    (t, h, m) int64 views of the plane words [rows, wpr]. A level above 3 is reported by
+    status() as ValueError ("2-bit level out of range")."""
+    from .data import padded_words
+    rows, cols = levels.shape
+    levels = levels.contiguous()
+    wpr = padded_words(cols, lane_bits)
+    t, h, m = (torch.empty((rows, wpr), dtype=torch.int64, device=levels.device) for _ in range(3))
+    _raise(_lib.load().bitmm_decompose_thm_dev(_ptr(levels), rows, cols, _ptr(t), _ptr(h), _ptr(m),
+                                               wpr, _stream(stream)))
+    return t, h, m
+
+
+def decompose_apb(a: torch.Tensor, alpha, lane_bits: int = 512, stream=None):
+    """GPU decompose_apb (apb.cpp:119-142): fp32 [rows, cols] and a positive alpha (a float,
+    or a per-row fp32 tensor) -> (bin words [rows, wpr] int64, row_ptr [rows+1], col_idx [nnz]
+    as int64 views of the u64 arrays, vals [nnz] fp32). Bit-identical to the reference."""
+    import ctypes as C
+    from .data import padded_words
+    rows, cols = a.shape
+    wpr = padded_words(cols, lane_bits)
+    dev = a.device
+    row_alpha = alpha if isinstance(alpha, torch.Tensor) else None
+    scalar = 1.0 if row_alpha is not None else float(alpha)
+    bin_ = torch.empty((rows, wpr), dtype=torch.int64, device=dev)
+    row_ptr = torch.empty(rows + 1, dtype=torch.int64, device=dev)
+    nnz = C.c_int64(0)
+    lib = _lib.load()
+    args = (_ptr(a), rows, cols, a.stride(0), scalar, _ptr(row_alpha), _ptr(bin_), wpr, _ptr(row_ptr))
+    _raise(lib.bitmm_decompose_apb_dev(*args, None, None, 0, C.byref(nnz), _stream(stream)))
+    col_idx = torch.empty(nnz.value, dtype=torch.int64, device=dev)
+    vals = torch.empty(nnz.value, dtype=torch.float32, device=dev)
+    if nnz.value:
+        _raise(lib.bitmm_decompose_apb_dev(*args, _ptr(col_idx), _ptr(vals), nnz.value, C.byref(nnz),
+                                           _stream(stream)))
+    return bin_, row_ptr, col_idx, vals
+
+
 def dot_binary_rows(u: torch.Tensor, v: torch.Tensor, n: int, stream=None) -> torch.Tensor:
     """dot_binary (kernels.cpp:120-129) for every row pair of u, v [count, words] (int64 views
     of the packed words): n - 2*popc(u ^ v)."""
