@@ -1,5 +1,7 @@
 // kernels_b200.cpp — reference-side binding of the B200 library (drop-in for the GEMM
-// bodies of /root/reference/proj/src/kernels.cpp:163-352 and apb.cpp:158-164).
+// bodies of /root/reference/proj/src/kernels.cpp:163-352 and apb.cpp:158-164, and for the
+// packers pack_signs (tensor.cpp:155-164), decompose_thm (transform.cpp:47-75) and
+// decompose_apb (apb.cpp:119-142)).
 //
 // Compiled against the reference's OWN headers (include/bitmm/*.hpp) and linked in place
 // of those function bodies, it keeps every public signature, argument check, exception
@@ -9,7 +11,7 @@
 // (results never depended on it, kernels.cpp:47-49).
 //
 // Build recipe (see INTEGRATION.md and oracle/Makefile target `dropin`): compile the
-// reference sources unmodified, weaken the six replaced symbols in their objects
+// reference sources unmodified, weaken the nine replaced symbols in their objects
 // (objcopy --weaken-symbol), link this file plus libbitmm_b200.so.
 #include <stdexcept>
 #include <string>
@@ -18,6 +20,7 @@
 #include "bitmm/errors.hpp"
 #include "bitmm/kernels.hpp"
 #include "bitmm/tensor.hpp"
+#include "bitmm/transform.hpp"
 #include "bitmm_b200.h"
 
 namespace bitmm {
@@ -45,6 +48,55 @@ void check_packed_pair(std::int64_t cols_a, std::size_t wpr_a, std::int64_t cols
 float plane_gamma(const ThmPlanes& p) { return p.gamma.value_or(1.0f); }
 
 }  // namespace
+
+// ---- packers: the GPU packers behind the host ABI (same layouts, checks and messages) ----
+BitMatrix pack_signs(const DenseMatrix& m, int lane_bits) {
+  BitMatrix b(m.rows(), m.cols(), lane_bits);  // the reference's lane / dimension checks
+  if (m.rows() == 0 || b.words_per_row() == 0) return b;
+  raise_on(bitmm_pack_signs_host(m.cols() > 0 ? m.row_data(0) : nullptr, m.rows(), m.cols(),
+                                 m.cols(), b.row_data(0),
+                                 static_cast<std::int64_t>(b.words_per_row())));
+  return b;
+}
+
+ThmPlanes decompose_thm(const TwoBitMatrix& q, std::optional<float> gamma, int lane_bits) {
+  ThmPlanes p;
+  p.t = BitMatrix(q.rows, q.cols, lane_bits);
+  p.h = BitMatrix(q.rows, q.cols, lane_bits);
+  p.m = BitMatrix(q.rows, q.cols, lane_bits);
+  p.scale = q.scale;
+  p.gamma = gamma;
+  if (q.rows == 0 || p.t.words_per_row() == 0) return p;
+  // a level above 3 -> std::invalid_argument("2-bit level out of range"), transform.cpp:70-71
+  raise_on(bitmm_decompose_thm_host(q.levels.data(), q.rows, q.cols, p.t.row_data(0),
+                                    p.h.row_data(0), p.m.row_data(0),
+                                    static_cast<std::int64_t>(p.t.words_per_row())));
+  return p;
+}
+
+ApbLayer decompose_apb(const DenseMatrix& a, float alpha, int lane_bits) {
+  if (!(alpha > 0.0f)) throw std::invalid_argument("alpha must be positive");
+  ApbLayer l;
+  l.rows = a.rows();
+  l.cols = a.cols();
+  l.alpha = alpha;
+  l.bin = BitMatrix(a.rows(), a.cols(), lane_bits);
+  std::vector<std::uint64_t> row_ptr(static_cast<std::size_t>(a.rows()) + 1, 0);
+  const float* src = a.rows() > 0 && a.cols() > 0 ? a.row_data(0) : nullptr;
+  std::uint64_t* bin = l.bin.words_per_row() > 0 && a.rows() > 0 ? l.bin.row_data(0) : nullptr;
+  const auto wpr = static_cast<std::int64_t>(l.bin.words_per_row());
+  std::int64_t nnz = 0;
+  raise_on(bitmm_decompose_apb_host(src, a.rows(), a.cols(), a.cols(), alpha, nullptr, bin, wpr,
+                                    row_ptr.data(), nullptr, nullptr, 0, &nnz));
+  std::vector<std::uint64_t> col_idx(static_cast<std::size_t>(nnz));
+  std::vector<float> vals(static_cast<std::size_t>(nnz));
+  if (nnz > 0)
+    raise_on(bitmm_decompose_apb_host(src, a.rows(), a.cols(), a.cols(), alpha, nullptr, bin, wpr,
+                                      row_ptr.data(), col_idx.data(), vals.data(), nnz, &nnz));
+  l.residual = CsrMatrix::create(a.rows(), a.cols(), std::move(row_ptr), std::move(col_idx),
+                                 std::move(vals));
+  return l;
+}
 
 DenseMatrix gemm_1x1(const BitMatrix& a, const BitMatrix& b_packed, float gamma_a, float gamma_b,
                      int threads) {
