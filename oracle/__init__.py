@@ -236,6 +236,7 @@ class Ref:
             "ref_spmm_csr": (_i, [_i64, _i64, _p, _p, _p, _i64, _p, _i64, _i, _p, pd]),
             "ref_layer_forward": (_i, [_i64, _i64, _f, _p, _i64, _p, _p, _p, _i64, _p, _i64, _i, _p, pd]),
             "ref_apb_forward": (_i, [_p, _i64, _i64, _f, _f, _p]),
+            "ref_pack_apb": (_i, [_p, _i64, _i64, _i, C.POINTER(_f), C.POINTER(_f), C.c_char_p]),
             "ref_decompose_apb": (_i, [_p, _i64, _i64, _f, _i, _p, C.POINTER(_i64), _p, _p, _p,
                                        C.POINTER(_i64)]),
             "ref_pack_signs": (_i, [_p, _i64, _i64, _i, _p, C.POINTER(_i64)]),
@@ -393,6 +394,15 @@ class Ref:
         ci = np.ascontiguousarray(col_idx, np.uint64)
         v = np.ascontiguousarray(vals, np.float32)
         self._check(self.lib.ref_store_csr(path.encode(), rows, cols, _ptr(rp), _ptr(ci), _ptr(v), ci.size))
+
+    def pack_apb(self, w, prefix, alpha=None, delta=None):
+        """The reference CLI's `pack --mode apb` (store_apb_layer files under `prefix`);
+        returns the (alpha, delta) it used."""
+        w = np.ascontiguousarray(w, np.float32)
+        a, d = _f(0.0 if alpha is None else alpha), _f(0.0 if delta is None else delta)
+        self._check(self.lib.ref_pack_apb(_ptr(w), w.shape[0], w.shape[1], int(alpha is not None),
+                                          C.byref(a), C.byref(d), prefix.encode()))
+        return a.value, d.value
 
     def store_thm_planes(self, prefix, t, h, m, cols, scale, gamma=None):
         t, h, m = (np.ascontiguousarray(x, np.uint64) for x in (t, h, m))

@@ -245,6 +245,26 @@ int ref_store_csr(const char* path, int64_t rows, int64_t cols, const uint64_t* 
   return guarded([&] { store_tensor(path, csr(rows, cols, row_ptr, col_idx, vals, nnz)); });
 }
 
+// The reference CLI's `pack --mode apb` branch (tools/bitmm_main.cpp:195-207): params given
+// (has_params) or init_alpha_delta(w), apb_forward, decompose_apb, store_apb_layer(prefix).
+// Writes the chosen alpha / delta back.
+int ref_pack_apb(const float* w, int64_t rows, int64_t cols, int has_params, float* alpha,
+                 float* delta, const char* prefix) {
+  return guarded([&] {
+    DenseMatrix W = dense(w, rows, cols);
+    ApbParams p;
+    if (has_params) {
+      p.alpha = *alpha;
+      p.delta = *delta;
+    } else {
+      p = init_alpha_delta(W);
+    }
+    store_apb_layer(prefix, decompose_apb(apb_forward(W, p), p.alpha));
+    *alpha = p.alpha;
+    *delta = p.delta;
+  });
+}
+
 int ref_store_thm_planes(const char* prefix, const uint64_t* t, const uint64_t* h, const uint64_t* m,
                          int64_t rows, int64_t cols, int64_t wpr, float scale, int has_gamma,
                          float gamma) {

@@ -271,6 +271,34 @@ def _round_with_tie_away(x: np.ndarray) -> np.ndarray:
     return np.where(dn == x, near, pick).astype(np.float32)
 
 
+DELTA_MIN = np.float32(1e-8)  # kDeltaMin, apb.hpp:16
+
+
+def init_alpha_delta(w: np.ndarray):
+    """init_alpha_delta (apb.cpp:191-210): alpha = mean |w|, delta = max(3 * population std,
+    1e-8), both accumulated in double in storage order (sequential sums, as the reference)."""
+    v = np.ascontiguousarray(w, np.float32).reshape(-1).astype(np.float64)
+    n = v.size
+    if n == 0:
+        raise ValueError("empty weight matrix")
+    abs_sum = float(np.cumsum(np.abs(v))[-1])  # cumsum: one running sum, element order
+    mean = float(np.cumsum(v)[-1]) / n
+    var = float(np.cumsum((v - mean) ** 2)[-1]) / n
+    alpha = np.float32(abs_sum / n)
+    delta = max(np.float32(3.0 * np.sqrt(var)), DELTA_MIN)
+    return alpha, np.float32(delta)
+
+
+def check_apb_params(alpha, delta) -> None:
+    """ApbParams::validate (apb.cpp:50-55)."""
+    if not alpha > 0.0:
+        raise ValueError("alpha must be positive")
+    if not delta >= DELTA_MIN:
+        raise ValueError("delta must be at least the 1e-8 floor")
+    if not (np.isfinite(alpha) and np.isfinite(delta)):
+        raise ValueError("alpha and delta must be finite")
+
+
 def decompose_apb(a: np.ndarray, alpha, lane_bits: int = LANE_BITS) -> ApbLayer:
     """apb.cpp:119-142. bin = pack_signs(a) at every position; residual = a - alpha*sign(a)
     wherever |a| != alpha (membership by exact value), rounded with ties away from zero.

@@ -103,6 +103,16 @@ def store_thm_planes(prefix: str, planes: ThmPlanes) -> None:
         f.write("\n")
 
 
+def store_apb_layer(prefix: str, bin_: BitMatrix, residual: CsrMatrix, alpha: float) -> None:
+    """store_apb_layer (apb.cpp:212-221): <prefix>.bin.btsr, <prefix>.res.btsr and
+    <prefix>.json holding {"alpha": alpha} (nlohmann dump(2): the float as a double)."""
+    store_tensor(prefix + ".bin.btsr", bin_)
+    store_tensor(prefix + ".res.btsr", residual)
+    with open(prefix + ".json", "w") as f:
+        json.dump({"alpha": float(np.float32(alpha))}, f, indent=2)
+        f.write("\n")
+
+
 def load_thm_planes_dev(prefix: str, device=None, stream=None) -> dict:
     """load_thm_planes (tensor_io.cpp:215-235) into device tensors: t, h, m word tensors plus
     scale / gamma from the sidecar."""

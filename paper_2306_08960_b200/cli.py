@@ -7,10 +7,10 @@
 `pack` (cmd_pack, bitmm_main.cpp:182-222) loads the dense container straight into device memory
 (bitmm_btsr_load_dev), packs it with the GPU packers (pack.cuh) and writes the same containers
 the reference writes (pack_signs -> store_tensor; quantize_uniform_2bit + decompose_thm ->
-store_thm_planes). `bench` (cmd_bench, bitmm_main.cpp:64-104; bench_routine, bench.cpp:90-185)
+store_thm_planes; apb_forward + decompose_apb -> store_apb_layer, on the GPU decompose_apb). `bench` (cmd_bench, bitmm_main.cpp:64-104; bench_routine, bench.cpp:90-185)
 times the routines on the GPU with operands resident in HBM and writes the reference's CSV
-columns (write_csv_header / write_csv_record, bench.cpp:188-200). The reference's `apb` pack
-mode, `verify`, `tpp`, `apb-stats` and `shapes` stay host-side (out of scope).
+columns (write_csv_header / write_csv_record, bench.cpp:188-200). The reference's `verify`,
+`tpp`, `apb-stats` and `shapes` stay host-side (out of scope).
 Exit codes follow the reference: 0 ok, 2 usage, 3 I/O.
 """
 from __future__ import annotations
@@ -48,8 +48,30 @@ def cmd_pack(args) -> int:
         btsr.store_thm_planes(args.output, api.ThmPlanes(bm(t), bm(h), bm(m), scale=float(args.step)))
         print(f"packed planes: {rows} x {cols} step={args.step:g} -> "
               f"{args.output}.{{t,h,m}}.btsr + {args.output}.json")
+    elif args.mode == "apb":
+        # bitmm_main.cpp:195-207: params given or init_alpha_delta, apb_forward, decompose_apb
+        if (args.alpha is None) != (args.delta is None):
+            raise ValueError("--alpha and --delta must be given together")
+        if args.alpha is not None:
+            alpha, delta = np.float32(args.alpha), np.float32(args.delta)
+        else:
+            alpha, delta = api.init_alpha_delta(x.cpu().numpy())
+        api.check_apb_params(alpha, delta)
+        bound = np.float32(alpha + delta)  # float add, apb.cpp:59
+        sign_alpha = torch.where(x >= 0, torch.tensor(float(alpha), device=x.device),
+                                 torch.tensor(-float(alpha), device=x.device))
+        fwd = torch.where(x.abs() <= float(bound), sign_alpha, x).contiguous()  # apb_forward
+        words, rp, ci, vals = device.decompose_apb(fwd, float(alpha), args.lane_bits)
+        device.status()
+        wpr = words.shape[1]
+        bm = api.BitMatrix.from_words(rows, cols, wpr, words.cpu().numpy().view(np.uint64))
+        res = api.CsrMatrix.create(rows, cols, rp.cpu().numpy().view(np.uint64),
+                                   ci.cpu().numpy().view(np.uint64), vals.cpu().numpy())
+        btsr.store_apb_layer(args.output, bm, res, float(alpha))
+        print(f"packed layer: {rows} x {cols} alpha={float(alpha):g} nnz={res.nnz()} -> "
+              f"{args.output}.{{bin,res}}.btsr + {args.output}.json")
     else:
-        raise ValueError(f"unknown pack mode: {args.mode} (GPU modes: sign|thm)")
+        raise ValueError(f"unknown pack mode: {args.mode} (GPU modes: sign|thm|apb)")
     torch.cuda.synchronize()
     return EXIT_OK
 
@@ -171,6 +193,8 @@ def main(argv=None) -> int:
     p.add_argument("--output", required=True)
     p.add_argument("--mode", default="sign")
     p.add_argument("--step", type=float)
+    p.add_argument("--alpha", type=float)
+    p.add_argument("--delta", type=float)
     p.add_argument("--lane-bits", type=int, default=512)
     b = sub.add_parser("bench", help="time routines on the GPU and report gops")
     b.add_argument("--routine", action="append")

@@ -121,3 +121,22 @@ def test_apb_weights_generator_shape():
     assert keep == 15  # 2% of 768, the survey's C4 residual count
     layer = api.decompose_apb(a, alpha)
     assert layer.residual.nnz() == 16 * 15
+
+
+def test_init_alpha_delta_matches_reference(tmp_path):
+    """init_alpha_delta (apb.cpp:191-210): the host mirror's sequential double sums give the
+    reference's alpha and delta bit for bit, including the 1e-8 delta floor."""
+    import oracle
+    ref = oracle.load_ref()
+    if ref is None:
+        pytest.skip("reference library not built")
+    rng = np.random.default_rng(3)
+    cases = [rng.normal(0.0, 0.02, (64, 300)).astype(np.float32),
+             rng.uniform(-3, 3, (7, 1001)).astype(np.float32),
+             np.full((3, 5), 0.25, np.float32)]  # zero variance: delta floor
+    for w in cases:
+        alpha, delta = api.init_alpha_delta(w)
+        ra, rd = ref.pack_apb(w, str(tmp_path / "p"))
+        assert np.float32(alpha) == np.float32(ra) and np.float32(delta) == np.float32(rd)
+    with pytest.raises(ValueError):
+        api.init_alpha_delta(np.zeros((0, 4), np.float32))

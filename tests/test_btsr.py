@@ -209,6 +209,31 @@ def test_cli_pack_matches_reference_pack(ref, tmp_path):
 
 
 @pytest.mark.gpu
+def test_cli_pack_apb_matches_reference(ref, tmp_path):
+    """`pack --mode apb` (bitmm_main.cpp:195-207): init_alpha_delta or given parameters,
+    apb_forward, decompose_apb on the GPU, store_apb_layer. Every file is byte-identical to the
+    reference CLI's."""
+    from paper_2306_08960_b200 import cli
+    rng = np.random.default_rng(11)
+    w = rng.normal(0.0, 0.02, (96, 700)).astype(np.float32)
+    w[0, :4] = [0.0, -0.0, 0.5, -0.5]
+    src = str(tmp_path / "w.btsr")
+    btsr.store_tensor(src, w)
+    for params in (None, (0.015, 0.02)):
+        extra = [] if params is None else ["--alpha", str(params[0]), "--delta", str(params[1])]
+        assert cli.main(["pack", "--input", src, "--output", str(tmp_path / "ours"), "--mode", "apb"]
+                        + extra) == 0
+        if params is None:
+            ref.pack_apb(w, str(tmp_path / "ref"))
+        else:
+            ref.pack_apb(w, str(tmp_path / "ref"), np.float32(params[0]), np.float32(params[1]))
+        for suffix in (".bin.btsr", ".res.btsr", ".json"):
+            assert _bytes(str(tmp_path / "ours") + suffix) == _bytes(str(tmp_path / "ref") + suffix), \
+                (params, suffix)
+    assert cli.main(["pack", "--input", src, "--output", "x", "--mode", "apb", "--alpha", "1"]) == 2
+
+
+@pytest.mark.gpu
 def test_cli_bench_csv(tmp_path):
     from paper_2306_08960_b200 import cli
     out = str(tmp_path / "b.csv")
