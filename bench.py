@@ -763,7 +763,6 @@ def e2e_pass(args, ops, torch, lib):
         dt = torch.float32 if name == "1x2" else torch.int32
         h[name]["out"] = torch.empty((m, n), dtype=dt).pin_memory()
         h2d += sum(v.numel() * v.element_size() for kk, v in h[name].items() if kk != "out")
-        d2h += m * n * 4
 
     def call(name, m, n, k):
         x = h[name]
@@ -780,20 +779,29 @@ def e2e_pass(args, ops, torch, lib):
                                          P(x["out"]), None, n)
         if rc != 0:
             raise RuntimeError(f"e2e {name}: {rc} {lib.bitmm_last_error().decode()}")
+        return int(lib.bitmm_last_d2h_bytes())
 
     for _ in range(max(args.warmup, 1)):
-        for r in ROUTINES:
-            call(*r)
+        # the library's own count of what crossed PCIe back (16-bit output wire where K allows)
+        d2h = sum(call(*r) for r in ROUTINES)
     torch.cuda.synchronize()
+    per = {r[0]: 0.0 for r in ROUTINES}
     t0 = time.perf_counter()
     for _ in range(args.steps):
         for r in ROUTINES:
+            t1 = time.perf_counter()
             call(*r)
+            per[r[0]] += time.perf_counter() - t1
     secs = (time.perf_counter() - t0) / args.steps
     upd = sum(m * n * k for _, m, n, k in ROUTINES)
     return {"value": upd / secs / 1e12, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": secs * 1e3,
-            "path": "bitmm_gemm_{1x1,1x2,2x2}_host (include/bitmm_b200.h), pinned host buffers"}
+            "ms_per_call": {k: v / args.steps * 1e3 for k, v in per.items()},
+            "path": "bitmm_gemm_{1x1,1x2,2x2}_host (include/bitmm_b200.h), pinned host buffers",
+            "output_bytes_per_step": int(sum(m * n * 4 for _, m, n, _ in ROUTINES)),
+            "wire": "outputs cross PCIe as 16-bit integer units (device narrow, host widen and "
+                    "scale, bit-identical to the device output); delivered as int32 / fp32",
+            "host_threads": host_threads()}
 
 
 if __name__ == "__main__":

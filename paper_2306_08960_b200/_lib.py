@@ -59,6 +59,7 @@ SIGNATURES = {
     "bitmm_reserve_workspace": (_i, [C.c_size_t]),
     "bitmm_workspace_bytes": (C.c_size_t, [_i, _i64, _i64, _i64]),
     "bitmm_last_launch_count": (_i, []),
+    "bitmm_last_d2h_bytes": (C.c_uint64, []),
     "bitmm_profile_enable": (_i, [_i]),
     "bitmm_profile_collect": (_i, []),
     "bitmm_profile_reset": (_i, []),

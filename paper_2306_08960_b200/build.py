@@ -32,7 +32,7 @@ NVCC_FLAGS = [
     "-Xptxas",
     "-v",
 ]
-SOURCES = ["bitmm_capi.cu"]
+SOURCES = ["bitmm_capi.cu", "wire_host.cpp"]
 
 
 def nvcc() -> str:

@@ -6,6 +6,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -22,6 +23,7 @@
 #include "ptx.cuh"
 #include "tc_gemm.cuh"
 #include "unpack.cuh"
+#include "wire.cuh"
 
 using namespace bitmm_dev;
 
@@ -29,6 +31,7 @@ namespace {
 
 thread_local std::string g_err;
 thread_local int g_launches = 0;
+thread_local uint64_t g_d2h_bytes = 0;  // device -> host bytes of the last host-flavour call
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -67,7 +70,22 @@ struct DeviceState {
   cudaEvent_t pinned_ev[2] = {nullptr, nullptr};
   cudaStream_t d2h = nullptr;             // host-flavour output copies (run_pipelined)
   cudaEvent_t pipe_ev[8] = {};
+  cudaStream_t h2d = nullptr;             // host-flavour input copies (run_pipelined_wire)
+  cudaEvent_t in_ev[9] = {};
+  void* host_stage = nullptr;             // pinned 16-bit output words (run_pipelined_wire)
+  size_t host_stage_bytes = 0;
+  std::vector<cudaEvent_t> wire_ev;       // one per copied part
+  // BITMM_WIRE_TRACE only: device timeline of the current host call
+  std::vector<std::pair<std::string, cudaEvent_t>>* timeline = nullptr;
 };
+
+void trace_mark(DeviceState& st, const std::string& what, cudaStream_t on) {
+  if (!st.timeline) return;
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, on);
+  st.timeline->emplace_back(what, e);
+}
 
 std::mutex g_mu;
 DeviceState g_state[kMaxDevices];
@@ -528,6 +546,189 @@ int run_pipelined(DeviceState& st, cudaStream_t s, int64_t total, int64_t step, 
   return rc;
 }
 
+// 16-bit output wire (wire.cuh). Same slicing as run_pipelined, with the body split in two:
+// in(c0, c1, stream) enqueues slice [c0, c1)'s input copies (all slices up front, on st.h2d),
+// gemm(c0, c1) its GEMM on s once those copies are done. block(c0, c1) gives the output
+// block {row0, rows, col0, cols} the slice writes as int32 units into dcu (leading
+// dimension wo.ldc). A narrowing kernel follows each slice's GEMM on s and packs
+// its units into dwire; the d2h stream then copies them into pinned host staging in
+// kWireParts row parts, each with its own event. After the whole call is enqueued the host pool widens the
+// parts into the caller's buffers in order, while the later parts are still in flight.
+// Parts per slice: 4 measured best against 1, 2 and 8 (whole-slice parts delay the host's
+// widening, smaller ones slow the copies).
+constexpr int kWireParts = 4;
+
+struct OutBlock {
+  int64_t row0, rows, col0, cols;
+};
+
+int host_stage_reserve(DeviceState& st, size_t bytes) {
+  if (bytes <= st.host_stage_bytes) return BITMM_OK;
+  if (st.host_stage) BITMM_CUDA_TRY(cudaFreeHost(st.host_stage));
+  st.host_stage = nullptr;
+  st.host_stage_bytes = 0;
+  BITMM_CUDA_TRY(cudaHostAlloc(&st.host_stage, bytes, cudaHostAllocDefault));
+  st.host_stage_bytes = bytes;
+  return BITMM_OK;
+}
+
+// BITMM_HOST_WIRE=32 keeps the 4-byte output copies (A/B runs and tests of that path).
+Wire host_wire(int routine, int64_t k) {
+  const char* e = std::getenv("BITMM_HOST_WIRE");
+  if (e && std::atoi(e) == 32) return Wire::None;
+  return wire_for(routine, k);
+}
+
+template <class In, class Gemm, class Block>
+int run_pipelined_wire(DeviceState& st, cudaStream_t s, int64_t total, int64_t step, In&& in,
+                       Gemm&& gemm, Block&& block, const WireOut& wo, const int32_t* dcu,
+                       uint16_t* dwire, size_t wire_words) {
+  if (!st.d2h) {
+    BITMM_CUDA_TRY(cudaStreamCreateWithFlags(&st.d2h, cudaStreamNonBlocking));
+    for (auto& e : st.pipe_ev) BITMM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  if (!st.h2d) {
+    BITMM_CUDA_TRY(cudaStreamCreateWithFlags(&st.h2d, cudaStreamNonBlocking));
+    for (auto& e : st.in_ev) BITMM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  const auto t_call = std::chrono::steady_clock::now();
+  static const bool trace = std::getenv("BITMM_WIRE_TRACE") != nullptr;
+  // BITMM_WIRE_TRACE=nowiden: timeline of the copies alone (outputs left unwritten)
+  static const bool skip_widen = trace && std::string(std::getenv("BITMM_WIRE_TRACE")) == "nowiden";
+  // trace only: a device timeline of slice completions (GEMM + narrow on s, copies on d2h)
+  std::vector<std::pair<std::string, cudaEvent_t>> tl;
+  if (trace) st.timeline = &tl;
+  auto mark = [&](const std::string& what, cudaStream_t on) { trace_mark(st, what, on); };
+  mark("start", s);
+  BITMM_TRY(host_stage_reserve(st, wire_words * 2));
+  uint16_t* hw = static_cast<uint16_t*>(st.host_stage);
+  struct Part {
+    OutBlock b;
+    int64_t r0, r1;
+    size_t off;  // word offset of the block in the staging buffer
+  };
+  std::vector<Part> parts;
+  // Every slice's input copies go first, on their own stream: queued on s behind the
+  // previous slice's GEMM they ran at a third of the link rate while the output copies
+  // were in flight (BITMM_WIRE_TRACE timelines).
+  BITMM_CUDA_TRY(cudaEventRecord(st.in_ev[kPipeChunks], s));  // after the call's setup copies
+  BITMM_CUDA_TRY(cudaStreamWaitEvent(st.h2d, st.in_ev[kPipeChunks], 0));
+  {
+    int j = 0;
+    for (int64_t c0 = 0; c0 < total; c0 += step, ++j) {
+      BITMM_TRY(in(c0, std::min(total, c0 + step), st.h2d));
+      BITMM_CUDA_TRY(cudaEventRecord(st.in_ev[j % kPipeChunks], st.h2d));
+    }
+  }
+  int rc = BITMM_OK;
+  size_t off = 0;
+  int i = 0;
+  for (int64_t c0 = 0; c0 < total && rc == BITMM_OK; c0 += step, ++i) {
+    const int64_t c1 = std::min(total, c0 + step);
+    if (cudaStreamWaitEvent(s, st.in_ev[i % kPipeChunks], 0) != cudaSuccess) {
+      rc = fail(BITMM_ERR_CUDA, "pipeline input event");
+      break;
+    }
+    mark("h" + std::to_string(i), s);
+    rc = gemm(c0, c1);
+    if (rc != BITMM_OK) break;
+    const OutBlock b = block(c0, c1);
+    // the narrowing runs on the GEMM's stream: on the copy stream it would wait for SMs
+    // behind the next slice's persistent GEMM
+    const int64_t cells = b.rows * b.cols;
+    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((cells / 4 + 255) / 256, int64_t{st.sms} * 8)));
+    narrow_units_kernel<<<grid, 256, 0, s>>>(dcu + b.row0 * wo.ldc + b.col0, wo.ldc, dwire + off,
+                                             b.rows, b.cols, static_cast<int>(wo.mode), wo.k);
+    rc = launch_check("narrow_units_kernel");
+    if (rc != BITMM_OK) break;
+    mark("g" + std::to_string(i), s);
+    cudaEvent_t ev = st.pipe_ev[i % kPipeChunks];
+    if (cudaEventRecord(ev, s) != cudaSuccess || cudaStreamWaitEvent(st.d2h, ev, 0) != cudaSuccess) {
+      rc = fail(BITMM_ERR_CUDA, std::string("pipeline event: ") + cudaGetErrorString(cudaGetLastError()));
+      break;
+    }
+    const int64_t per = (b.rows + kWireParts - 1) / kWireParts;
+    for (int64_t r0 = 0; r0 < b.rows; r0 += per) {
+      const int64_t r1 = std::min(b.rows, r0 + per);
+      const size_t o = off + static_cast<size_t>(r0 * b.cols), bytes = static_cast<size_t>((r1 - r0) * b.cols) * 2;
+      if (cudaMemcpyAsync(hw + o, dwire + o, bytes, cudaMemcpyDeviceToHost, st.d2h) != cudaSuccess) {
+        rc = fail(BITMM_ERR_CUDA, std::string("wire copy: ") + cudaGetErrorString(cudaGetLastError()));
+        break;
+      }
+      g_d2h_bytes += bytes;
+      if (st.wire_ev.size() <= parts.size()) {
+        cudaEvent_t e = nullptr;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync) != cudaSuccess) {
+          rc = fail(BITMM_ERR_CUDA, "wire event create");
+          break;
+        }
+        st.wire_ev.push_back(e);
+      }
+      if (cudaEventRecord(st.wire_ev[parts.size()], st.d2h) != cudaSuccess) {
+        rc = fail(BITMM_ERR_CUDA, "wire event record");
+        break;
+      }
+      parts.push_back(Part{b, b.row0 + r0, b.row0 + r1, off});
+    }
+    mark("c" + std::to_string(i), st.d2h);
+    off += static_cast<size_t>(cells);
+  }
+  // One pool batch for the whole call: each task widens a row range of one part after
+  // waiting for that part's copy. Tasks are handed out in part order, so the pool follows
+  // the copies without a barrier per part.
+  struct Task {
+    int part;
+    int64_t r0, r1;
+  };
+  std::vector<Task> tasks;
+  if (rc == BITMM_OK) {
+    for (int p = 0; p < static_cast<int>(parts.size()); ++p) {
+      const Part& q = parts[p];
+      const int64_t rows_per_task = std::max<int64_t>(1, (int64_t{1} << 16) / std::max<int64_t>(1, q.b.cols));
+      for (int64_t r = q.r0; r < q.r1; r += rows_per_task)
+        tasks.push_back(Task{p, r, std::min(q.r1, r + rows_per_task)});
+    }
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  std::atomic<int> copy_err{0};
+  std::atomic<int64_t> wait_ns{0};
+  host_pool_run(static_cast<int>(tasks.size()), [&](int i) {
+    const Task& t = tasks[i];
+    const auto w0 = trace ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
+    if (cudaEventSynchronize(st.wire_ev[t.part]) != cudaSuccess) {
+      copy_err.store(1);
+      return;
+    }
+    if (trace) wait_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - w0).count();
+    const Part& q = parts[t.part];
+    if (skip_widen) return;
+    wire_expand_range(wo, hw + q.off, q.b.row0, q.b.col0, q.b.cols, t.r0, t.r1);
+  });
+  if (trace) {
+    const auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    const auto t1 = std::chrono::steady_clock::now();
+    cudaEventSynchronize(st.wire_ev[0]);
+    std::fprintf(stderr, "[bitmm wire] %zu parts, %zu tasks, %zu words: enqueue %.3f ms, host widen %.3f ms "
+                 "(%d threads, %.3f thread-ms waiting for copies)\n",
+                 parts.size(), tasks.size(), wire_words, ms(t_call, t0), ms(t0, t1), host_pool_size(),
+                 wait_ns.load() * 1e-6);
+    cudaDeviceSynchronize();
+    std::string line = "[bitmm wire] device timeline (ms):";
+    for (auto& [what, e] : tl) {
+      float m = 0;
+      cudaEventElapsedTime(&m, tl[0].second, e);
+      line += " " + what + "=" + std::to_string(m).substr(0, 5);
+    }
+    std::fprintf(stderr, "%s\n", line.c_str());
+    for (auto& [what, e] : tl) cudaEventDestroy(e);
+    st.timeline = nullptr;
+  }
+  if (rc == BITMM_OK && copy_err.load()) rc = fail(BITMM_ERR_CUDA, std::string("wire copy: ") + cudaGetErrorString(cudaGetLastError()));
+  const cudaError_t e = cudaStreamSynchronize(st.d2h);
+  if (rc == BITMM_OK && e != cudaSuccess) rc = fail(BITMM_ERR_CUDA, cudaGetErrorString(e));
+  return rc;
+}
+
 struct Carve {
   uint8_t* base;
   size_t off = 0;
@@ -887,6 +1088,7 @@ int bitmm_abi_version(void) { return 1; }
 const char* bitmm_last_error(void) { return g_err.c_str(); }
 
 int bitmm_last_launch_count(void) { return g_launches; }
+uint64_t bitmm_last_d2h_bytes(void) { return g_d2h_bytes; }
 
 int bitmm_profile_enable(int on) {
   std::lock_guard<std::mutex> lk(g_prof.mu);
@@ -1008,27 +1210,49 @@ int bitmm_gemm_1x1_host(const uint64_t* a, int64_t m, const uint64_t* b_packed, 
   DeviceState* st = nullptr;
   BITMM_TRY(with_device(&st));
   cudaStream_t s = st->stream;
+  g_d2h_bytes = 0;
+  const Wire wire = host_wire(0, k);
   const size_t a_bytes = m * wpr * 8, b_bytes = n * wpr * 8, c_bytes = m * ldc * 4;
-  BITMM_TRY(arena_reserve(st->io, align_up(a_bytes, 1024) + align_up(b_bytes, 1024) + 2 * align_up(c_bytes, 1024)));
+  const size_t w_bytes = wire != Wire::None ? static_cast<size_t>(m * n) * 2 : 0;
+  BITMM_TRY(arena_reserve(st->io, align_up(a_bytes, 1024) + align_up(b_bytes, 1024) +
+                                      2 * align_up(c_bytes, 1024) + align_up(w_bytes, 1024)));
   Carve cv(st->io.ptr);
   uint64_t* da = cv.take<uint64_t>(a_bytes);
   uint64_t* db = cv.take<uint64_t>(b_bytes);
-  int32_t* dcu = c_units ? cv.take<int32_t>(c_bytes) : nullptr;
-  float* dc = c ? cv.take<float>(c_bytes) : nullptr;
+  // 16-bit wire: the GEMM writes int32 units only; the host derives both outputs from them
+  int32_t* dcu = (c_units || wire != Wire::None) ? cv.take<int32_t>(c_bytes) : nullptr;
+  float* dc = (c && wire == Wire::None) ? cv.take<float>(c_bytes) : nullptr;
   BITMM_CUDA_TRY(cudaMemcpyAsync(db, b_packed, b_bytes, cudaMemcpyHostToDevice, s));
   // slices of output rows (rows of a)
+  auto in = [&](int64_t r0, int64_t r1, cudaStream_t cs) -> int {
+    BITMM_CUDA_TRY(cudaMemcpyAsync(da + r0 * wpr, a + r0 * wpr, (r1 - r0) * wpr * 8,
+                                   cudaMemcpyHostToDevice, cs));
+    return BITMM_OK;
+  };
+  auto gemm = [&](int64_t r0, int64_t r1) -> int {
+    return gemm_1x1_dev_impl(*st, da + r0 * wpr, r1 - r0, db, n, k, wpr, gamma_a, gamma_b,
+                             dcu ? dcu + r0 * ldc : nullptr, dc ? dc + r0 * ldc : nullptr, ldc, s);
+  };
+  auto body = [&](int64_t r0, int64_t r1) -> int {
+    BITMM_TRY(in(r0, r1, s));
+    return gemm(r0, r1);
+  };
+  if (wire != Wire::None) {
+    const WireOut wo{wire, static_cast<int>(k), gamma_a * gamma_b /* kernels.cpp:170 */, nullptr,
+                     nullptr, c_units, c, ldc};
+    BITMM_TRY(run_pipelined_wire(
+        *st, s, m, pipe_step(m, c_bytes, 256), in, gemm,
+        [&](int64_t r0, int64_t r1) { return OutBlock{r0, r1 - r0, 0, n}; }, wo, dcu,
+        cv.take<uint16_t>(w_bytes), static_cast<size_t>(m * n)));
+    return read_status(*st, s);
+  }
   BITMM_TRY(run_pipelined(
-      *st, s, m, pipe_step(m, c_bytes, 256),
-      [&](int64_t r0, int64_t r1) -> int {
-        BITMM_CUDA_TRY(cudaMemcpyAsync(da + r0 * wpr, a + r0 * wpr, (r1 - r0) * wpr * 8,
-                                       cudaMemcpyHostToDevice, s));
-        return gemm_1x1_dev_impl(*st, da + r0 * wpr, r1 - r0, db, n, k, wpr, gamma_a, gamma_b,
-                                 dcu ? dcu + r0 * ldc : nullptr, dc ? dc + r0 * ldc : nullptr, ldc, s);
-      },
+      *st, s, m, pipe_step(m, c_bytes, 256), body,
       [&](int64_t r0, int64_t r1, cudaStream_t d2h) -> int {
         const size_t bytes = (r1 - r0) * ldc * 4;
         if (dcu) BITMM_CUDA_TRY(cudaMemcpyAsync(c_units + r0 * ldc, dcu + r0 * ldc, bytes, cudaMemcpyDeviceToHost, d2h));
         if (dc) BITMM_CUDA_TRY(cudaMemcpyAsync(c + r0 * ldc, dc + r0 * ldc, bytes, cudaMemcpyDeviceToHost, d2h));
+        g_d2h_bytes += (dcu ? bytes : 0) + (dc ? bytes : 0);
         return BITMM_OK;
       }));
   return read_status(*st, s);
@@ -1066,9 +1290,12 @@ int bitmm_gemm_1x2_host(const uint64_t* w, int64_t m, float gamma, const uint64_
   const bool planes_ok_shape = n >= 0 && k >= 0 && wpr >= 0 && wpr * 64 >= k;
   const size_t p_bytes = (planes_ok_shape ? n * wpr * 8 : 0), w_bytes = (rc_dims == BITMM_OK ? m * wpr * 8 : 0);
   const size_t c_bytes = (rc_dims == BITMM_OK ? m * ldc * 4 : 0);
+  g_d2h_bytes = 0;
+  const Wire wire = host_wire(1, k);
+  const size_t wire_bytes = (wire != Wire::None && rc_dims == BITMM_OK) ? static_cast<size_t>(m * n) * 2 : 0;
   BITMM_TRY(arena_reserve(st->io, 3 * align_up(p_bytes, 1024) + align_up(w_bytes, 1024) +
                                       2 * align_up(c_bytes, 1024) + align_up(m > 0 ? m * 4 : 0, 1024) +
-                                      align_up(n > 0 ? n * 4 : 0, 1024) + 4096));
+                                      align_up(n > 0 ? n * 4 : 0, 1024) + align_up(wire_bytes, 1024) + 4096));
   Carve cv(st->io.ptr);
   uint64_t* dt = cv.take<uint64_t>(p_bytes);
   uint64_t* dh = cv.take<uint64_t>(p_bytes);
@@ -1089,30 +1316,50 @@ int bitmm_gemm_1x2_host(const uint64_t* w, int64_t m, float gamma, const uint64_
     return fail(rc_dims, dims_msg);
   }
   uint64_t* dw = cv.take<uint64_t>(w_bytes);
-  float* drs = row_scale ? cv.take<float>(m * 4) : nullptr;
-  float* dcs = col_scale ? cv.take<float>(n * 4) : nullptr;
-  int32_t* dcu = c_units ? cv.take<int32_t>(c_bytes) : nullptr;
-  float* dc = c ? cv.take<float>(c_bytes) : nullptr;
+  // 16-bit wire: the GEMM writes int32 units only and the host applies the scales
+  float* drs = (row_scale && wire == Wire::None) ? cv.take<float>(m * 4) : nullptr;
+  float* dcs = (col_scale && wire == Wire::None) ? cv.take<float>(n * 4) : nullptr;
+  int32_t* dcu = (c_units || wire != Wire::None) ? cv.take<int32_t>(c_bytes) : nullptr;
+  float* dc = (c && wire == Wire::None) ? cv.take<float>(c_bytes) : nullptr;
   BITMM_CUDA_TRY(cudaMemcpyAsync(dw, w, w_bytes, cudaMemcpyHostToDevice, s));
   if (drs) BITMM_CUDA_TRY(cudaMemcpyAsync(drs, row_scale, m * 4, cudaMemcpyHostToDevice, s));
   if (dcs) BITMM_CUDA_TRY(cudaMemcpyAsync(dcs, col_scale, n * 4, cudaMemcpyHostToDevice, s));
   // slices of output columns (rows of the activation planes, the larger operand here);
   // each slice's output block is a strided 2-D copy
+  auto in = [&](int64_t n0, int64_t n1, cudaStream_t cs) -> int {
+    const size_t off = n0 * wpr, bytes = (n1 - n0) * wpr * 8;
+    BITMM_CUDA_TRY(cudaMemcpyAsync(dt + off, t + off, bytes, cudaMemcpyHostToDevice, cs));
+    BITMM_CUDA_TRY(cudaMemcpyAsync(dh + off, h + off, bytes, cudaMemcpyHostToDevice, cs));
+    BITMM_CUDA_TRY(cudaMemcpyAsync(dm + off, mm + off, bytes, cudaMemcpyHostToDevice, cs));
+    return BITMM_OK;
+  };
+  auto gemm = [&](int64_t n0, int64_t n1) -> int {
+    const size_t off = n0 * wpr;
+    return gemm_1x2_dev_impl(*st, dw, m, gamma, dt + off, dh + off, dm + off, n1 - n0, k, wpr,
+                             a_scale, has_a_gamma, a_gamma, drs, dcs ? dcs + n0 : nullptr,
+                             dcu ? dcu + n0 : nullptr, dc ? dc + n0 : nullptr, ldc, s);
+  };
+  auto body = [&](int64_t n0, int64_t n1) -> int {
+    BITMM_TRY(in(n0, n1, s));
+    return gemm(n0, n1);
+  };
+  if (wire != Wire::None) {
+    // kernels.cpp:193, the same expression gemm_1x2_dev_impl passes to the epilogue
+    const float scale = 0.5f * gamma * a_scale * (has_a_gamma ? a_gamma : 1.0f);
+    const WireOut wo{wire, static_cast<int>(k), scale, row_scale, col_scale, c_units, c, ldc};
+    BITMM_TRY(run_pipelined_wire(
+        *st, s, n, pipe_step(n, c_bytes, 256), in, gemm,
+        [&](int64_t n0, int64_t n1) { return OutBlock{0, m, n0, n1 - n0}; }, wo, dcu,
+        cv.take<uint16_t>(wire_bytes), static_cast<size_t>(m * n)));
+    return read_status(*st, s);
+  }
   BITMM_TRY(run_pipelined(
-      *st, s, n, pipe_step(n, c_bytes, 256),
-      [&](int64_t n0, int64_t n1) -> int {
-        const size_t off = n0 * wpr, bytes = (n1 - n0) * wpr * 8;
-        BITMM_CUDA_TRY(cudaMemcpyAsync(dt + off, t + off, bytes, cudaMemcpyHostToDevice, s));
-        BITMM_CUDA_TRY(cudaMemcpyAsync(dh + off, h + off, bytes, cudaMemcpyHostToDevice, s));
-        BITMM_CUDA_TRY(cudaMemcpyAsync(dm + off, mm + off, bytes, cudaMemcpyHostToDevice, s));
-        return gemm_1x2_dev_impl(*st, dw, m, gamma, dt + off, dh + off, dm + off, n1 - n0, k, wpr,
-                                 a_scale, has_a_gamma, a_gamma, drs, dcs ? dcs + n0 : nullptr,
-                                 dcu ? dcu + n0 : nullptr, dc ? dc + n0 : nullptr, ldc, s);
-      },
+      *st, s, n, pipe_step(n, c_bytes, 256), body,
       [&](int64_t n0, int64_t n1, cudaStream_t d2h) -> int {
         const size_t pitch = ldc * 4, width = (n1 - n0) * 4;
         if (dcu) BITMM_CUDA_TRY(cudaMemcpy2DAsync(c_units + n0, pitch, dcu + n0, pitch, width, m, cudaMemcpyDeviceToHost, d2h));
         if (dc) BITMM_CUDA_TRY(cudaMemcpy2DAsync(c + n0, pitch, dc + n0, pitch, width, m, cudaMemcpyDeviceToHost, d2h));
+        g_d2h_bytes += ((dcu ? 1 : 0) + (dc ? 1 : 0)) * width * m;
         return BITMM_OK;
       }));
   return read_status(*st, s);
@@ -1157,9 +1404,12 @@ int bitmm_gemm_2x2_host(const uint64_t* wt, const uint64_t* wh, const uint64_t* 
   const bool shape_ok = k >= 0 && wpr >= 0 && wpr * 64 >= k;
   const size_t pw = (shape_ok && m > 0 ? m * wpr * 8 : 0), pa = (shape_ok && n > 0 ? n * wpr * 8 : 0);
   const size_t c_bytes = (rc_dims == BITMM_OK ? m * ldc * 4 : 0);
+  g_d2h_bytes = 0;
+  const Wire wire = host_wire(2, k);
+  const size_t wire_bytes = (wire != Wire::None && rc_dims == BITMM_OK) ? static_cast<size_t>(m * n) * 2 : 0;
   BITMM_TRY(arena_reserve(st->io, 3 * align_up(pw, 1024) + 3 * align_up(pa, 1024) +
                                       2 * align_up(c_bytes, 1024) + align_up(m > 0 ? m * 4 : 0, 1024) +
-                                      align_up(n > 0 ? n * 4 : 0, 1024) + 4096));
+                                      align_up(n > 0 ? n * 4 : 0, 1024) + align_up(wire_bytes, 1024) + 4096));
   Carve cv(st->io.ptr);
   uint64_t* d[6];
   const uint64_t* src[6] = {wt, wh, wm, at, ah, am};
@@ -1180,28 +1430,49 @@ int bitmm_gemm_2x2_host(const uint64_t* wt, const uint64_t* wh, const uint64_t* 
     }
     return fail(rc_dims, dims_msg);
   }
-  float* drs = row_scale ? cv.take<float>(m * 4) : nullptr;
-  float* dcs = col_scale ? cv.take<float>(n * 4) : nullptr;
-  int32_t* dcu = c_units ? cv.take<int32_t>(c_bytes) : nullptr;
-  float* dc = c ? cv.take<float>(c_bytes) : nullptr;
+  // 16-bit wire: the GEMM writes int32 units only and the host applies the scales
+  float* drs = (row_scale && wire == Wire::None) ? cv.take<float>(m * 4) : nullptr;
+  float* dcs = (col_scale && wire == Wire::None) ? cv.take<float>(n * 4) : nullptr;
+  int32_t* dcu = (c_units || wire != Wire::None) ? cv.take<int32_t>(c_bytes) : nullptr;
+  float* dc = (c && wire == Wire::None) ? cv.take<float>(c_bytes) : nullptr;
   if (drs) BITMM_CUDA_TRY(cudaMemcpyAsync(drs, row_scale, m * 4, cudaMemcpyHostToDevice, s));
   if (dcs) BITMM_CUDA_TRY(cudaMemcpyAsync(dcs, col_scale, n * 4, cudaMemcpyHostToDevice, s));
   // slices of output rows (rows of the weight planes)
+  auto in = [&](int64_t r0, int64_t r1, cudaStream_t cs) -> int {
+    const size_t off = r0 * wpr, bytes = (r1 - r0) * wpr * 8;
+    for (int i = 0; i < 3; ++i)
+      BITMM_CUDA_TRY(cudaMemcpyAsync(d[i] + off, src[i] + off, bytes, cudaMemcpyHostToDevice, cs));
+    return BITMM_OK;
+  };
+  auto gemm = [&](int64_t r0, int64_t r1) -> int {
+    const size_t off = r0 * wpr;
+    return gemm_2x2_dev_impl(*st, d[0] + off, d[1] + off, d[2] + off, r1 - r0, w_scale,
+                             has_w_gamma, w_gamma, d[3], d[4], d[5], n, k, wpr, a_scale,
+                             has_a_gamma, a_gamma, drs ? drs + r0 : nullptr, dcs,
+                             dcu ? dcu + r0 * ldc : nullptr, dc ? dc + r0 * ldc : nullptr, ldc, s);
+  };
+  auto body = [&](int64_t r0, int64_t r1) -> int {
+    BITMM_TRY(in(r0, r1, s));
+    return gemm(r0, r1);
+  };
+  if (wire != Wire::None) {
+    // kernels.cpp:232-233, the same expression gemm_2x2_dev_impl passes to the epilogue
+    const float scale = 0.25f * w_scale * a_scale * (has_w_gamma ? w_gamma : 1.0f) *
+                        (has_a_gamma ? a_gamma : 1.0f);
+    const WireOut wo{wire, static_cast<int>(k), scale, row_scale, col_scale, c_units, c, ldc};
+    BITMM_TRY(run_pipelined_wire(
+        *st, s, m, pipe_step(m, c_bytes, 256), in, gemm,
+        [&](int64_t r0, int64_t r1) { return OutBlock{r0, r1 - r0, 0, n}; }, wo, dcu,
+        cv.take<uint16_t>(wire_bytes), static_cast<size_t>(m * n)));
+    return read_status(*st, s);
+  }
   BITMM_TRY(run_pipelined(
-      *st, s, m, pipe_step(m, c_bytes, 256),
-      [&](int64_t r0, int64_t r1) -> int {
-        const size_t off = r0 * wpr, bytes = (r1 - r0) * wpr * 8;
-        for (int i = 0; i < 3; ++i)
-          BITMM_CUDA_TRY(cudaMemcpyAsync(d[i] + off, src[i] + off, bytes, cudaMemcpyHostToDevice, s));
-        return gemm_2x2_dev_impl(*st, d[0] + off, d[1] + off, d[2] + off, r1 - r0, w_scale,
-                                 has_w_gamma, w_gamma, d[3], d[4], d[5], n, k, wpr, a_scale,
-                                 has_a_gamma, a_gamma, drs ? drs + r0 : nullptr, dcs,
-                                 dcu ? dcu + r0 * ldc : nullptr, dc ? dc + r0 * ldc : nullptr, ldc, s);
-      },
+      *st, s, m, pipe_step(m, c_bytes, 256), body,
       [&](int64_t r0, int64_t r1, cudaStream_t d2h) -> int {
         const size_t bytes = (r1 - r0) * ldc * 4;
         if (dcu) BITMM_CUDA_TRY(cudaMemcpyAsync(c_units + r0 * ldc, dcu + r0 * ldc, bytes, cudaMemcpyDeviceToHost, d2h));
         if (dc) BITMM_CUDA_TRY(cudaMemcpyAsync(c + r0 * ldc, dc + r0 * ldc, bytes, cudaMemcpyDeviceToHost, d2h));
+        g_d2h_bytes += (dcu ? bytes : 0) + (dc ? bytes : 0);
         return BITMM_OK;
       }));
   return read_status(*st, s);

@@ -1,0 +1,255 @@
+// Host half of the 16-bit output wire (wire_host.h / wire.cuh): a fixed worker pool and the
+// widening of wire words into int32 units and fp32 values, bit-identical to the GEMM
+// epilogue (tc_gemm.cuh: s = scale * row_scale[r]; s = s * col_scale[c]; C = s * float(u)).
+//
+// Widening is bound by the host's memory system: 2 B read, 4 B (or 8 B) written per cell.
+// Outputs are written with streaming stores, which skip the read-for-ownership of the
+// destination lines; 64-byte AVX-512 stores where the CPU has them, else 16-byte SSE2 ones
+// (profiles/micro/host_bw.c measures both on the GPU box's host).
+#include "wire_host.h"
+
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <cstdlib>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <type_traits>
+#include <vector>
+
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
+
+namespace bitmm_dev {
+
+namespace {
+
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool pool;
+    return pool;
+  }
+  int size() const { return static_cast<int>(workers_.size()) + 1; }
+
+  void run(int n, const std::function<void(int)>& f) {
+    if (n <= 0) return;
+    if (workers_.empty() || n == 1) {
+      for (int i = 0; i < n; ++i) f(i);
+      return;
+    }
+    std::lock_guard<std::mutex> call(call_mu_);  // one batch at a time
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = &f;
+      n_ = n;
+      next_.store(0);
+      pending_ = static_cast<int>(workers_.size());
+      ++gen_;
+    }
+    cv_.notify_all();
+    drain();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    int n = static_cast<int>(std::thread::hardware_concurrency());
+    if (const char* e = std::getenv("BITMM_HOST_THREADS")) n = std::atoi(e);
+    n = std::max(1, std::min(n, 32));
+    for (int i = 1; i < n; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  void drain() {
+    for (int i = next_.fetch_add(1); i < n_; i = next_.fetch_add(1)) (*job_)(i);
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      drain();
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--pending_ == 0) done_cv_.notify_one();
+    }
+  }
+
+  std::vector<std::thread> workers_;
+  std::mutex call_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* job_ = nullptr;
+  int n_ = 0;
+  std::atomic<int> next_{0};
+  int pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+template <Wire MODE>
+inline int32_t decode(uint16_t v, int k) {
+  if constexpr (MODE == Wire::Popc) return k - 2 * static_cast<int32_t>(v);
+  else if constexpr (MODE == Wire::Half) return 2 * static_cast<int32_t>(static_cast<int16_t>(v));
+  else return 4 * static_cast<int32_t>(v);
+}
+
+// One output row: pointers already offset to the block's first column.
+struct Row {
+  const uint16_t* src;
+  int32_t* du;      // int32 units or null
+  float* dc;        // fp32 values or null
+  const float* cs;  // column scales or null
+  float s_r;        // scale * row_scale[r] (or scale)
+  int k;
+  int64_t cols;
+};
+
+template <Wire MODE>
+inline void cell(const Row& w, int64_t j) {
+  const int32_t u = decode<MODE>(w.src[j], w.k);
+  if (w.du) w.du[j] = u;
+  if (w.dc) w.dc[j] = (w.cs ? w.s_r * w.cs[j] : w.s_r) * static_cast<float>(u);
+}
+
+template <int ALIGN>
+inline bool misaligned(const Row& w, int64_t j) {
+  return (w.du && (reinterpret_cast<uintptr_t>(w.du + j) & (ALIGN - 1))) ||
+         (w.dc && (reinterpret_cast<uintptr_t>(w.dc + j) & (ALIGN - 1)));
+}
+
+#if defined(__x86_64__)
+// Sixteen words -> sixteen int32 units, 64-byte streaming stores.
+template <Wire MODE>
+__attribute__((target("avx512f,avx512bw"))) int64_t row_avx512(const Row& w, int64_t j) {
+  const __m512i kk = _mm512_set1_epi32(w.k);
+  const __m512 sr = _mm512_set1_ps(w.s_r);
+  for (; j + 16 <= w.cols; j += 16) {
+    const __m256i v = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(w.src + j));
+    __m512i u;
+    if constexpr (MODE == Wire::Popc) u = _mm512_sub_epi32(kk, _mm512_slli_epi32(_mm512_cvtepu16_epi32(v), 1));
+    else if constexpr (MODE == Wire::Half) u = _mm512_slli_epi32(_mm512_cvtepi16_epi32(v), 1);
+    else u = _mm512_slli_epi32(_mm512_cvtepu16_epi32(v), 2);
+    if (w.du) _mm512_stream_si512(reinterpret_cast<__m512i*>(w.du + j), u);
+    if (w.dc) {
+      const __m512 s = w.cs ? _mm512_mul_ps(sr, _mm512_loadu_ps(w.cs + j)) : sr;  // (s_r * cs) first
+      _mm512_stream_ps(w.dc + j, _mm512_mul_ps(s, _mm512_cvtepi32_ps(u)));
+    }
+  }
+  return j;
+}
+
+// Eight words -> eight int32 units, 16-byte streaming stores (x86-64 baseline).
+template <Wire MODE>
+int64_t row_sse2(const Row& w, int64_t j) {
+  const __m128i kk = _mm_set1_epi32(w.k), z = _mm_setzero_si128();
+  const __m128 sr = _mm_set1_ps(w.s_r);
+  for (; j + 8 <= w.cols; j += 8) {
+    const __m128i v = _mm_loadu_si128(reinterpret_cast<const __m128i*>(w.src + j));
+    __m128i lo, hi;
+    if constexpr (MODE == Wire::Half) {  // sign-extend: interleave with itself, arithmetic shift
+      lo = _mm_slli_epi32(_mm_srai_epi32(_mm_unpacklo_epi16(v, v), 16), 1);
+      hi = _mm_slli_epi32(_mm_srai_epi32(_mm_unpackhi_epi16(v, v), 16), 1);
+    } else if constexpr (MODE == Wire::Popc) {
+      lo = _mm_sub_epi32(kk, _mm_slli_epi32(_mm_unpacklo_epi16(v, z), 1));
+      hi = _mm_sub_epi32(kk, _mm_slli_epi32(_mm_unpackhi_epi16(v, z), 1));
+    } else {
+      lo = _mm_slli_epi32(_mm_unpacklo_epi16(v, z), 2);
+      hi = _mm_slli_epi32(_mm_unpackhi_epi16(v, z), 2);
+    }
+    if (w.du) {
+      _mm_stream_si128(reinterpret_cast<__m128i*>(w.du + j), lo);
+      _mm_stream_si128(reinterpret_cast<__m128i*>(w.du + j + 4), hi);
+    }
+    if (w.dc) {
+      __m128 s0 = sr, s1 = sr;
+      if (w.cs) {
+        s0 = _mm_mul_ps(sr, _mm_loadu_ps(w.cs + j));
+        s1 = _mm_mul_ps(sr, _mm_loadu_ps(w.cs + j + 4));
+      }
+      _mm_stream_ps(w.dc + j, _mm_mul_ps(s0, _mm_cvtepi32_ps(lo)));
+      _mm_stream_ps(w.dc + j + 4, _mm_mul_ps(s1, _mm_cvtepi32_ps(hi)));
+    }
+  }
+  return j;
+}
+
+bool has_avx512() {
+  static const bool cpu = [] {
+    __builtin_cpu_init();
+    return __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw");
+  }();
+  const char* e = std::getenv("BITMM_HOST_SIMD");  // "sse2" forces the baseline path (tests)
+  return cpu && !(e && std::string(e) == "sse2");
+}
+#endif
+
+template <Wire MODE>
+void expand_rows(const WireOut& o, const uint16_t* words, int64_t row0, int64_t col0, int64_t cols,
+                 int64_t r0, int64_t r1) {
+#if defined(__x86_64__)
+  const bool wide = has_avx512();
+#endif
+  for (int64_t r = r0; r < r1; ++r) {
+    Row w;
+    w.src = words + (r - row0) * cols;
+    w.du = o.c_units ? o.c_units + r * o.ldc + col0 : nullptr;
+    w.dc = o.c ? o.c + r * o.ldc + col0 : nullptr;
+    w.cs = o.col_scale ? o.col_scale + col0 : nullptr;
+    w.s_r = o.row_scale ? o.scale * o.row_scale[r] : o.scale;
+    w.k = o.k;
+    w.cols = cols;
+    int64_t j = 0;
+#if defined(__x86_64__)
+    // a scalar head up to the first column where every output is aligned for the stores
+    // (both outputs may never align together; then the narrower stores or scalar code run)
+    auto head = [&](auto align, int64_t max_head) {
+      int64_t h = 0;
+      while (h < max_head && h < cols && misaligned<decltype(align)::value>(w, h)) ++h;
+      return misaligned<decltype(align)::value>(w, h) ? int64_t{-1} : h;
+    };
+    const int64_t h64 = wide ? head(std::integral_constant<int, 64>{}, 16) : -1;
+    const int64_t h16 = h64 < 0 ? head(std::integral_constant<int, 16>{}, 4) : -1;
+    if (h64 >= 0) {
+      for (; j < h64; ++j) cell<MODE>(w, j);
+      j = row_avx512<MODE>(w, j);
+    } else if (h16 >= 0) {
+      for (; j < h16; ++j) cell<MODE>(w, j);
+      j = row_sse2<MODE>(w, j);
+    }
+#endif
+    for (; j < cols; ++j) cell<MODE>(w, j);
+  }
+#if defined(__x86_64__)
+  _mm_sfence();  // streaming stores ordered before the pool reports the task done
+#endif
+}
+
+}  // namespace
+
+void host_pool_run(int n, const std::function<void(int)>& f) { HostPool::get().run(n, f); }
+int host_pool_size() { return HostPool::get().size(); }
+
+void wire_expand_range(const WireOut& o, const uint16_t* words, int64_t row0, int64_t col0,
+                       int64_t cols, int64_t r0, int64_t r1) {
+  switch (o.mode) {
+    case Wire::Popc: expand_rows<Wire::Popc>(o, words, row0, col0, cols, r0, r1); break;
+    case Wire::Half: expand_rows<Wire::Half>(o, words, row0, col0, cols, r0, r1); break;
+    default: expand_rows<Wire::Quarter>(o, words, row0, col0, cols, r0, r1); break;
+  }
+}
+
+}  // namespace bitmm_dev

@@ -2,14 +2,33 @@
 slices: each slice's inputs are copied in and its GEMM runs on the call's stream while the
 previous slice's output is copied back on a second stream (bitmm_capi.cu, run_pipelined).
 These shapes take that path, with ragged last slices. Results must equal the device-pointer
-path bit for bit, and an encoding error in the last slice must still be reported."""
+path bit for bit, and an encoding error in the last slice must still be reported.
+
+Where K allows, the output crosses PCIe as one 16-bit word per cell (csrc/wire.cuh): the
+device narrows the int32 units, the host widens them and applies the epilogue's fp32 scale
+sequence. Every test here runs with that wire and with BITMM_HOST_WIRE=32 (4-byte copies)."""
+import ctypes as C
+
 import numpy as np
 import pytest
 import torch
 
-from paper_2306_08960_b200 import api, data, device
+from paper_2306_08960_b200 import _lib, api, data, device
 
 pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True, params=["wire16", "wire16-sse2", "wire32"])
+def wire(request, monkeypatch):
+    """wire16: 16-bit words widened with the host's widest streaming stores (AVX-512 where
+    present); wire16-sse2: the x86-64 baseline path; wire32: 4-byte copies."""
+    monkeypatch.delenv("BITMM_HOST_WIRE", raising=False)
+    monkeypatch.delenv("BITMM_HOST_SIMD", raising=False)
+    if request.param == "wire32":
+        monkeypatch.setenv("BITMM_HOST_WIRE", "32")
+    elif request.param == "wire16-sse2":
+        monkeypatch.setenv("BITMM_HOST_SIMD", "sse2")
+    return request.param.split("-")[0]
 
 
 def _bm(rows, cols, wpr, words):
@@ -106,3 +125,98 @@ def test_illegal_planes_in_full_slices(k):
     want = torch.empty((m, n), dtype=torch.float32, device="cuda")
     device.gemm_2x2(*[_dev(x) for x in (wt, wh, wm, at, ah, am)], k, out=want)
     assert np.array_equal(got, want.cpu().numpy())
+
+
+def _full_row(k, wpr):
+    """One packed row with all K bits set and zero padding."""
+    full = np.zeros(wpr, np.uint64)
+    full[: k // 64] = ~np.uint64(0)
+    if k % 64:
+        full[k // 64] = np.uint64((1 << (k % 64)) - 1)
+    return full
+
+
+def _p(x):
+    return C.c_void_p(x.ctypes.data) if x is not None else None
+
+
+@pytest.mark.parametrize("k", [1000, 4096])
+def test_1x1_both_outputs_and_wire_bytes(wire, k):
+    """int32 units and scaled floats requested together; the units are K - 2*popc exactly and
+    the floats are (gamma_a*gamma_b)*float(units). The D2H byte count shows which wire ran."""
+    lib = _lib.load()
+    rng = np.random.default_rng(k)
+    m, n = 2300, 4100  # 37.7 MB per output: row slices, ragged last slice
+    a, wpr = data.random_words(rng, m, k)
+    b, _ = data.random_words(rng, n, k)
+    units = np.empty((m, n), np.int32)
+    vals = np.empty((m, n), np.float32)
+    rc = lib.bitmm_gemm_1x1_host(_p(a), m, _p(b), n, k, wpr, 0.75, 1.25, _p(units), _p(vals), n)
+    assert rc == 0, lib.bitmm_last_error()
+    want = torch.empty((m, n), dtype=torch.int32, device="cuda")
+    device.gemm_1x1(_dev(a), _dev(b), k, units=want)
+    assert np.array_equal(units, want.cpu().numpy())
+    assert np.array_equal(vals, np.float32(0.75 * 1.25) * units.astype(np.float32))
+    per_cell = 2 if wire == "wire16" else 8
+    assert lib.bitmm_last_d2h_bytes() == m * n * per_cell
+
+
+@pytest.mark.parametrize("k", [777, 10922, 10923])
+def test_1x2_wire_bound(wire, k):
+    """1/2 units = 2*sum s*p in [-6K, 6K]: K = 10922 is the last K the 16-bit wire carries
+    (all-ones weights against all-p3 activations reach the bound); 10923 falls back."""
+    lib = _lib.load()
+    rng = np.random.default_rng(k)
+    m, n = 1030, 4400 if k == 777 else 600
+    w, wpr = data.random_words(rng, m, k)
+    t, h, mm, _ = data.random_planes(rng, n, k)
+    if k != 777:
+        full = _full_row(k, wpr)
+        w[0] = full                         # row 0: all +1
+        t[0], h[0], mm[0] = full, 0, full   # column 0: all level 3 (t=1, h=0, m=1)
+    rs = rng.uniform(0.5, 1.5, m).astype(np.float32)
+    cs = rng.uniform(0.5, 1.5, n).astype(np.float32)
+    units = np.empty((m, n), np.int32)
+    vals = np.empty((m, n), np.float32)
+    rc = lib.bitmm_gemm_1x2_host(_p(w), m, 1.5, _p(t), _p(h), _p(mm), n, k, wpr, 0.5, 1, 2.0,
+                                 _p(rs), _p(cs), _p(units), _p(vals), n)
+    assert rc == 0, lib.bitmm_last_error()
+    wu = torch.empty((m, n), dtype=torch.int32, device="cuda")
+    wv = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    device.gemm_1x2(_dev(w), 1.5, _dev(t), _dev(h), _dev(mm), k, a_scale=0.5, a_gamma=2.0,
+                    row_scale=torch.from_numpy(rs).cuda(), col_scale=torch.from_numpy(cs).cuda(),
+                    units=wu, out=wv)
+    assert np.array_equal(units, wu.cpu().numpy())
+    assert np.array_equal(vals, wv.cpu().numpy())
+    if k != 777:
+        assert units[0, 0] == 6 * k
+    narrow = wire == "wire16" and k <= 10922
+    assert lib.bitmm_last_d2h_bytes() == m * n * (2 if narrow else 8)
+
+
+@pytest.mark.parametrize("k", [700, 7281, 7282])
+def test_2x2_wire_bound(wire, k):
+    """2/2 units = 4*sum p_w*p_a in [0, 36K]; K = 7281 is the last K the 16-bit wire carries."""
+    lib = _lib.load()
+    rng = np.random.default_rng(k)
+    m, n = (4200, 2100) if k == 700 else (300, 500)
+    wt, wh, wm, wpr = data.random_planes(rng, m, k)
+    at, ah, am, _ = data.random_planes(rng, n, k)
+    full = _full_row(k, wpr)
+    for t_, h_, m_ in ((wt, wh, wm), (at, ah, am)):
+        t_[0], h_[0], m_[0] = full, 0, full  # row 0 of each side: all level 3
+    rs = rng.uniform(0.5, 1.5, m).astype(np.float32)
+    units = np.empty((m, n), np.int32)
+    vals = np.empty((m, n), np.float32)
+    rc = lib.bitmm_gemm_2x2_host(_p(wt), _p(wh), _p(wm), m, 0.25, 0, 1.0, _p(at), _p(ah), _p(am),
+                                 n, k, wpr, 0.5, 1, 3.0, _p(rs), None, _p(units), _p(vals), n)
+    assert rc == 0, lib.bitmm_last_error()
+    wu = torch.empty((m, n), dtype=torch.int32, device="cuda")
+    wv = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    device.gemm_2x2(*[_dev(x) for x in (wt, wh, wm, at, ah, am)], k, w_scale=0.25, a_scale=0.5,
+                    a_gamma=3.0, row_scale=torch.from_numpy(rs).cuda(), units=wu, out=wv)
+    assert np.array_equal(units, wu.cpu().numpy())
+    assert np.array_equal(vals, wv.cpu().numpy())
+    assert units[0, 0] == 36 * k
+    narrow = wire == "wire16" and k <= 7281
+    assert lib.bitmm_last_d2h_bytes() == m * n * (2 if narrow else 8)
