@@ -21,12 +21,16 @@
 //    K=768). TMEM holds 2 tiles x 2 accumulators x 128 columns = 512 columns, so the
 //    epilogue of tile i overlaps the MMAs of i+1. Two fp16 parts at the f16 rate replace
 //    three bf16 parts (the earlier bf16x3 split): 2 MMAs per update instead of 3.
-//    Epilogue: C = (alpha_r * (hi + lo)) * 2^-e_n, stored; kernel 1 then adds R.X onto C
-//    (C = bin_part + res_part, apb.cpp:161-162).
+//    Epilogue: C = (alpha_r * (hi + lo)) * 2^-e_n, stored.
+//    layer_forward folds the residual into A instead (apb_fold_kernel below): A holds
+//    W' = hi + lo, and a fold phase of kpad/64 extra K blocks adds W'_lo . X_hi into the low
+//    accumulator, so C = m_r * W' . X comes out of one GEMM with no sparse pass over C.
+//    Kernel 1 remains the standalone spmm_csr and the 2-bit layer's residual.
 #pragma once
 
 #include "ptx.cuh"
 #include "tc_gemm.cuh"
+#include "unpack.cuh"
 
 namespace bitmm_dev {
 
@@ -283,6 +287,112 @@ __global__ void dequant_levels_kernel(const SpmmLevels lv, int K, int N, float* 
 }
 
 // ----------------------------------------------------------------------------------
+// Residual folded into the tensor-core operand (layer_forward, apb.cpp:158-164).
+//   C_r = alpha_r * sum_k s_rk x_k + sum_{residual (r,k)} v_rk x_k = m_r * sum_k W'_rk x_k
+// with W'_rk = (alpha_r * s_rk + v_rk) / m_r. For a normal row m_r = alpha_r, so W' = s + v/alpha_r:
+// +-1 everywhere (exact in fp16) except at the ~2% residual positions. W' is stored as two
+// fp16 parts, W' = hi + lo (22 significant bits), hi in the row's first kpad elements and lo
+// in the second kpad elements (zero except at residual positions). The GEMM adds lo . X_hi
+// into its low accumulator (apb_gemm_kernel's fold phase), which replaces the sparse pass over
+// C. A row whose alpha is 0 or not finite, or whose residuals exceed 2^14 alpha (fp16 range),
+// takes m_r = max(|alpha_r|, max|v_rk|) and the rounded parts of (alpha_r/m_r) s + v/m_r.
+// A repeated column adds to the running value (spmm_csr sums repeated entries).
+__device__ __forceinline__ void f16_split(float w, uint16_t& hi, uint16_t& lo) {
+  const __half h = __float2half_rn(w);
+  hi = __half_as_ushort(h);
+  lo = __half_as_ushort(__float2half_rn(w - __half2float(h)));  // w - hi is exact in fp32
+}
+
+// One warp per row. Lane i loads nonzero i up front (rows of a 2% residual have at most a few
+// dozen; a row with more than 32 takes the serial path below). The row's largest |v| (warp
+// reduction) decides normal vs not. Lane j then expands 32-bit sign words j, j+32, ... into
+// both parts (hi = +-1 and lo = 0 for a normal row; zero past K up to kpad) and checks the
+// padding bits (ERR_PADDING, as unpack_sign_f16). Finally each lane folds its nonzero into
+// its column: the value there is the sign entry, known from the bit, so nothing is read
+// back. A row with a repeated column, or with more than 32 nonzeros, is folded serially by
+// lane 0 in col_idx order, reading the running value back (spmm_csr sums repeated entries).
+__global__ void __launch_bounds__(256) apb_fold_kernel(
+    const uint32_t* __restrict__ words, int wpr32, int rows, int K, int kpad, long long ld,
+    const unsigned long long* __restrict__ row_ptr, const unsigned long long* __restrict__ col_idx,
+    const float* __restrict__ vals, float alpha, const float* __restrict__ row_alpha,
+    uint16_t* __restrict__ A, float* __restrict__ row_mul, int* __restrict__ err) {
+  pdl_wait();  // the previous kernel may still read the workspace we overwrite
+  pdl_launch_dependents();
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const float a = row_alpha ? row_alpha[r] : alpha;
+  const unsigned long long i0 = row_ptr[r], i1 = row_ptr[r + 1];
+  const unsigned long long n = i1 - i0;
+  const bool mine = static_cast<unsigned long long>(lane) < n;
+  const unsigned long long kc = mine ? col_idx[i0 + lane] : ~0ull;
+  const float v = mine ? vals[i0 + lane] : 0.f;
+  const bool kc_ok = kc < static_cast<unsigned long long>(K);
+  const uint32_t kw = kc_ok ? words[static_cast<long long>(r) * wpr32 + static_cast<int>(kc >> 5)] : 0u;
+  float vmax = fabsf(v);
+  for (unsigned long long i = i0 + 32 + lane; i < i1; i += 32) vmax = fmaxf(vmax, fabsf(vals[i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xFFFFFFFFu, vmax, o));
+  const bool normal = isfinite(a) && a != 0.f && isfinite(vmax) && vmax <= 16384.f * fabsf(a);
+  float m = a;
+  if (!normal) {
+    m = fmaxf(isfinite(a) ? fabsf(a) : 0.f, vmax);
+    if (!(m > 0.f) || !isfinite(m)) m = 1.f;
+  }
+  uint16_t h1 = 0x3C00u, l1 = 0u;  // the parts of +1 (normal) or +alpha_r/m_r
+  if (!normal) f16_split(a / m, h1, l1);
+  const uint32_t hpos = h1, lpos = l1, hneg = h1 ^ 0x8000u, lneg = l1 ? (l1 ^ 0x8000u) : 0u;
+  uint16_t* hi_row = A + static_cast<long long>(r) * ld;
+  uint16_t* lo_row = hi_row + kpad;
+  const int groups = max(kpad / 32, wpr32);
+  for (int g = lane; g < groups; g += 32) {
+    const uint32_t w = (g < wpr32) ? words[static_cast<long long>(r) * wpr32 + g] : 0u;
+    const uint32_t valid = valid_mask32(g * 32, K);
+    if (w & ~valid) atomicOr(err, ERR_PADDING);
+    if (g * 32 >= kpad) continue;
+    uint32_t oh[16], ol[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      uint32_t eh[2], el[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int bit = 2 * q + e;
+        const bool vb = (valid >> bit) & 1u, b = (w >> bit) & 1u;
+        eh[e] = vb ? (b ? hpos : hneg) : 0u;
+        el[e] = vb ? (b ? lpos : lneg) : 0u;
+      }
+      oh[q] = eh[0] | (eh[1] << 16);
+      ol[q] = el[0] | (el[1] << 16);
+    }
+    uint4* dh = reinterpret_cast<uint4*>(hi_row + g * 32);
+    uint4* dl = reinterpret_cast<uint4*>(lo_row + g * 32);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      dh[q] = make_uint4(oh[4 * q], oh[4 * q + 1], oh[4 * q + 2], oh[4 * q + 3]);
+      dl[q] = make_uint4(ol[4 * q], ol[4 * q + 1], ol[4 * q + 2], ol[4 * q + 3]);
+    }
+  }
+  // repeated columns among the (up to 32) lanes' entries
+  const unsigned peers = __match_any_sync(0xFFFFFFFFu, kc);
+  const bool serial = n > 32 || __any_sync(0xFFFFFFFFu, mine && __popc(peers) > 1);
+  __syncwarp();  // the sign expansion's stores before the folds that overwrite some of them
+  const float sv = __half2float(__ushort_as_half(h1)) + __half2float(__ushort_as_half(l1));
+  if (!serial) {
+    if (mine && kc_ok) {
+      const float cur = ((kw >> (kc & 31)) & 1u) ? sv : -sv;
+      f16_split(cur + v / m, hi_row[kc], lo_row[kc]);
+    }
+  } else if (lane == 0) {
+    for (unsigned long long i = i0; i < i1; ++i) {
+      const unsigned long long k = col_idx[i];
+      if (k >= static_cast<unsigned long long>(K)) continue;
+      const float cur = __half2float(__ushort_as_half(hi_row[k])) + __half2float(__ushort_as_half(lo_row[k]));
+      f16_split(cur + vals[i] / m, hi_row[k], lo_row[k]);
+    }
+  }
+  if (lane == 0) row_mul[r] = m;
+}
+
 constexpr int APB_BN = 128;        // output columns per pair tile
 constexpr int APB_PARTS = 2;       // fp16 split parts of X (hi, lo)
 constexpr int APB_STAGES = 6;
@@ -292,9 +402,21 @@ constexpr int APB_STAGE = APB_A_STAGE + APB_PARTS * APB_B_PART;      // 32 KB
 constexpr int APB_EPI_BYTES = 4 * 32 * TC_EPI_STRIDE * 4;
 constexpr int APB_SMEM = 1024 + APB_STAGES * APB_STAGE + APB_EPI_BYTES + (2 * APB_STAGES + 4) * 8 + 16;
 
+// AP = A parts per smem stage. AP = 1: A = sign(bin) (or W'_hi, with the fold phase after the
+// main K loop); AP = 2: a stage holds W'_hi and W'_lo of one K slice with both X parts, so X_hi
+// is loaded once for both products (48 KB stages, 4 of them).
+template <int AP>
+struct ApbCfg {
+  static constexpr int STAGES = AP == 1 ? APB_STAGES : 4;
+  static constexpr int STAGE = AP * APB_A_STAGE + APB_PARTS * APB_B_PART;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + APB_EPI_BYTES + (2 * STAGES + 4) * 8 + 16;
+};
+static_assert(ApbCfg<2>::SMEM <= 227 * 1024, "APB stages exceed shared memory");
+
 struct ApbParams {
   int M, N, kb_per_part;     // kb_per_part = kpad / 64
   int kpad;                  // elements per part row segment
+  int fold_kb;               // 0, or kb_per_part: the lo . X_hi phase of the folded residual
   float alpha;               // scalar alpha (row_alpha == nullptr)
   const float* row_alpha;
   const float* tok_scale;    // per output column 2^-e_n (split_x_f16)
@@ -313,17 +435,20 @@ __device__ __forceinline__ void apb_tile_coords(int t, const ApbParams& p, int& 
   nb = within / gm;
 }
 
+template <int AP>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     apb_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const ApbParams p) {
+  using CFG = ApbCfg<AP>;
+  constexpr int B_OFF = AP * APB_A_STAGE;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024u - (base_u32 & 1023u)) & 1023u);
   uint8_t* stages = smem;
-  float* sEpi = reinterpret_cast<float*>(stages + APB_STAGES * APB_STAGE);
+  float* sEpi = reinterpret_cast<float*>(stages + CFG::STAGES * CFG::STAGE);
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sEpi) + APB_EPI_BYTES);
-  uint64_t* empty = full + APB_STAGES;
-  uint64_t* tfull = empty + APB_STAGES;
+  uint64_t* empty = full + CFG::STAGES;
+  uint64_t* tfull = empty + CFG::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -336,7 +461,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    for (int s = 0; s < APB_STAGES; ++s) {
+    for (int s = 0; s < CFG::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -363,16 +488,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         apb_tile_coords(tile, p, mb, nb);
         const int a_row = mb * 256 + static_cast<int>(rank) * 128;
         const int b_row = nb * APB_BN + static_cast<int>(rank) * (APB_BN / 2);
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = 0; kb < num_kb + p.fold_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1u);
-          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * APB_STAGE);
-          uint8_t* st = stages + stage * APB_STAGE;
-          tma_load_2d_pair(st, &tmA, &full[stage], kb * 64, a_row);
+          uint8_t* st = stages + stage * CFG::STAGE;
+          if (kb < num_kb) {
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * CFG::STAGE);
+            tma_load_2d_pair(st, &tmA, &full[stage], kb * 64, a_row);
+            if constexpr (AP == 2) tma_load_2d_pair(st + APB_A_STAGE, &tmA, &full[stage], p.kpad + kb * 64, a_row);
 #pragma unroll
-          for (int q = 0; q < APB_PARTS; ++q)
-            tma_load_2d_pair(st + APB_A_STAGE + q * APB_B_PART, &tmB, &full[stage],
-                             q * p.kpad + kb * 64, b_row);
-          if (++stage == APB_STAGES) {
+            for (int q = 0; q < APB_PARTS; ++q)
+              tma_load_2d_pair(st + B_OFF + q * APB_B_PART, &tmB, &full[stage],
+                               q * p.kpad + kb * 64, b_row);
+          } else {  // fold phase: the lo part of W' against X_hi
+            const int kf = kb - num_kb;
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (APB_A_STAGE + APB_B_PART));
+            tma_load_2d_pair(st, &tmA, &full[stage], p.kpad + kf * 64, a_row);
+            tma_load_2d_pair(st + APB_A_STAGE, &tmB, &full[stage], kf * 64, b_row);
+          }
+          if (++stage == CFG::STAGES) {
             stage = 0;
             phase ^= 1u;
           }
@@ -392,23 +525,37 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tc_fence_after();
         const uint32_t d_hi = tmem_base + buf * 2 * APB_BN;
         const uint32_t d_lo = d_hi + APB_BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = 0; kb < num_kb + p.fold_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(stages + stage * APB_STAGE);
+          const uint32_t a_addr = smem_u32(stages + stage * CFG::STAGE);
+          if (kb < num_kb) {
 #pragma unroll
-          for (int q = 0; q < APB_PARTS; ++q) {
-            const uint32_t b_addr = a_addr + APB_A_STAGE + q * APB_B_PART;
+            for (int q = 0; q < APB_PARTS; ++q) {
+              const uint32_t b_addr = a_addr + B_OFF + q * APB_B_PART;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint64_t ad = sw128_kmajor_desc(a_addr + k * 32);
-              const uint64_t bd = sw128_kmajor_desc(b_addr + k * 32);
-              const uint32_t acc = (q == 0) ? ((kb | k) != 0) : !(q == 1 && kb == 0 && k == 0);
-              mma_f16_pair(q == 0 ? d_hi : d_lo, ad, bd, idesc, acc);
+              for (int k = 0; k < 4; ++k) {
+                const uint64_t ad = sw128_kmajor_desc(a_addr + k * 32);
+                const uint64_t bd = sw128_kmajor_desc(b_addr + k * 32);
+                const uint32_t acc = (q == 0) ? ((kb | k) != 0) : !(q == 1 && kb == 0 && k == 0);
+                mma_f16_pair(q == 0 ? d_hi : d_lo, ad, bd, idesc, acc);
+              }
             }
+            if constexpr (AP == 2) {  // W'_lo . X_hi into the low accumulator
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma_f16_pair(d_lo, sw128_kmajor_desc(a_addr + APB_A_STAGE + k * 32),
+                             sw128_kmajor_desc(a_addr + B_OFF + k * 32), idesc, 1u);
+            }
+          } else {  // fold phase: W'_lo . X_hi joins the low accumulator (same magnitude)
+            const uint32_t b_addr = a_addr + APB_A_STAGE;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_f16_pair(d_lo, sw128_kmajor_desc(a_addr + k * 32), sw128_kmajor_desc(b_addr + k * 32),
+                           idesc, 1u);
           }
           mma_commit_pair(&empty[stage], 0x3);
-          if (++stage == APB_STAGES) {
+          if (++stage == CFG::STAGES) {
             stage = 0;
             phase ^= 1u;
           }

@@ -759,9 +759,11 @@ void take_int_operands(DeviceState& st, int64_t m, int64_t n, int64_t k, uint8_t
   *A8 = cv.take<uint8_t>(m * kpad);
   *B8 = cv.take<uint8_t>(n * kpad);
 }
+// A (two parts when the residual is folded), X split, token scales, row multipliers.
 size_t ws_bytes_1x32(int64_t m, int64_t n, int64_t k) {
   const int64_t kpad = round_up(k, 64);
-  return align_up(m * kpad * 2, 1024) + align_up(n * APB_PARTS * kpad * 2, 1024) + align_up(n * 4, 1024) + 2048;
+  return align_up(m * 2 * kpad * 2, 1024) + align_up(n * APB_PARTS * kpad * 2, 1024) +
+         align_up(n * 4, 1024) + align_up(m * 4, 1024) + 2048;
 }
 
 // ---------------- routine bodies on device pointers ----------------
@@ -899,14 +901,18 @@ int apb_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, int64_t k, int64
                  const uint64_t* row_ptr, const uint64_t* col_idx, const float* vals, float* c,
                  int64_t ldc, cudaStream_t s) {
   const int64_t kpad = round_up(k, 64);
+  // layer_forward: the residual is folded into the GEMM operand (apb_fold_kernel)
+  const bool fold = row_ptr != nullptr;
+  const int64_t lda = fold ? 2 * kpad : kpad;
   BITMM_TRY(arena_reserve(st.ws, ws_bytes_1x32(m, n, k)));
   Carve cv(st.ws.ptr);
-  uint16_t* Ah = cv.take<uint16_t>(m * kpad * 2);
+  uint16_t* Ah = cv.take<uint16_t>(m * lda * 2);
   uint16_t* XT = cv.take<uint16_t>(n * APB_PARTS * kpad * 2);
   float* tok_scale = cv.take<float>(n * 4);
+  float* row_mul = cv.take<float>(m * 4);
   cudaLaunchAttribute pdl[1] = {pdl_attr()};
-  {
-    const int wpr32 = static_cast<int>(wpr * 2);
+  const int wpr32 = static_cast<int>(wpr * 2);
+  if (!fold) {
     const long long total = m * std::max<long long>(kpad / 32, wpr32);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(blocks_for(total, 256));
@@ -919,6 +925,22 @@ int apb_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, int64_t k, int64
                                       static_cast<long long>(m), wpr32, static_cast<int>(k),
                                       static_cast<int>(kpad), Ah, st.status));
     BITMM_TRY(launch_check("unpack_sign_f16"));
+  }
+  if (fold) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks_for(m, 8));  // a warp per row
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cfg.attrs = pdl;
+    cfg.numAttrs = 1;
+    ProfScope ps("apb_fold", s);
+    BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, apb_fold_kernel, reinterpret_cast<const uint32_t*>(w), wpr32,
+                                      static_cast<int>(m), static_cast<int>(k), static_cast<int>(kpad),
+                                      static_cast<long long>(lda),
+                                      reinterpret_cast<const unsigned long long*>(row_ptr),
+                                      reinterpret_cast<const unsigned long long*>(col_idx), vals, gamma,
+                                      row_gamma, Ah, row_mul, st.status));
+    BITMM_TRY(launch_check("apb_fold_kernel"));
   }
   const int strip_smem = static_cast<int>(kpad * 32 * 4);
   if (strip_smem <= 112 * 1024) {
@@ -963,27 +985,36 @@ int apb_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, int64_t k, int64
   }
 
   CUtensorMap ta, tb;
-  BITMM_TRY(make_operand_map(&ta, Ah, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, kpad, m, 128));
+  BITMM_TRY(make_operand_map(&ta, Ah, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, lda, m, 128));
   BITMM_TRY(make_operand_map(&tb, XT, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, APB_PARTS * kpad, n, APB_BN / 2));
   ApbParams p{};
   p.M = static_cast<int>(m);
   p.N = static_cast<int>(n);
   p.kb_per_part = static_cast<int>(kpad / 64);
   p.kpad = static_cast<int>(kpad);
+  // folded residual: W'_lo rides in the same stages as W'_hi (AP = 2) unless
+  // BITMM_APB_FOLD=sep selects the separate fold phase after the main K loop (A/B runs)
+  const char* fold_env = std::getenv("BITMM_APB_FOLD");
+  const bool fold_sep = fold_env && std::string(fold_env) == "sep";
+  const bool ap2 = fold && !fold_sep;
+  p.fold_kb = (fold && fold_sep) ? p.kb_per_part : 0;
   p.alpha = gamma;
-  p.row_alpha = row_gamma;
+  p.row_alpha = fold ? row_mul : row_gamma;
   p.tok_scale = tok_scale;
   p.C = c;
   p.ldc = ldc;
   p.num_m_blocks = static_cast<int>((m + 255) / 256);
   p.num_n_blocks = static_cast<int>((n + APB_BN - 1) / APB_BN);
   p.num_tiles = p.num_m_blocks * p.num_n_blocks;
-  BITMM_TRY(ensure_max_smem(reinterpret_cast<const void*>(apb_gemm_kernel), APB_SMEM));
+  const void* kern = ap2 ? reinterpret_cast<const void*>(apb_gemm_kernel<2>)
+                         : reinterpret_cast<const void*>(apb_gemm_kernel<1>);
+  const int smem = ap2 ? ApbCfg<2>::SMEM : ApbCfg<1>::SMEM;
+  BITMM_TRY(ensure_max_smem(kern, smem));
   const int units = std::min(p.num_tiles, st.sms / 2);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(2 * units));
   cfg.blockDim = dim3(TC_THREADS);
-  cfg.dynamicSmemBytes = APB_SMEM;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -995,12 +1026,10 @@ int apb_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, int64_t k, int64
   cfg.numAttrs = 2;
   {
     ProfScope ps("apb_gemm_f16x2", s);
-    BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, apb_gemm_kernel, ta, tb, p));
+    if (ap2) BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, apb_gemm_kernel<2>, ta, tb, p));
+    else BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, apb_gemm_kernel<1>, ta, tb, p));
     BITMM_TRY(launch_check("apb_gemm_kernel"));
   }
-  // the residual adds onto the stored binary part: C = bin + R.X (apb.cpp:161-162)
-  if (row_ptr != nullptr)
-    BITMM_TRY((run_spmm<false, true, false, true>(st, m, k, row_ptr, col_idx, vals, b, n, ldb, c, ldc, s)));
   return BITMM_OK;
 }
 

@@ -195,3 +195,56 @@ def test_token_magnitude_range(orc):
     for j in range(tokens):
         if j != 7:
             check_close(got[:, j], want[:, j])
+
+
+def test_folded_residual_edge_rows(orc):
+    """layer_forward folds the residual into the fp16 operand as W' = s + v/alpha_r
+    (apb_fold_kernel). Rows that cannot take that form use m_r = max(|alpha_r|, max|v|):
+    alpha_r = 0, an alpha_r far below the residual (v/alpha_r past fp16), a negative alpha_r.
+    Also a row with a repeated column (spmm_csr sums both), a row with more than 32 nonzeros
+    (the warp's lanes loop), and an empty row."""
+    rng = np.random.default_rng(404)
+    m, k, n = 12, 200, 77
+    wpr = (k + 511) // 512 * 8
+    signs = rng.random((m, k)) < 0.5
+    words = np.zeros((m, wpr), np.uint64)
+    for r in range(m):
+        for c in np.nonzero(signs[r])[0]:
+            words[r, c // 64] |= np.uint64(1) << np.uint64(c % 64)
+    alpha = rng.uniform(0.01, 0.03, m).astype(np.float32)
+    alpha[0] = 0.0
+    alpha[1] = 1e-9
+    alpha[2] = -0.02
+    rows_c, rows_v = [], []
+    for r in range(m):
+        nnz = {5: 0, 6: 60}.get(r, 4)
+        cols = np.sort(rng.choice(k, nnz, replace=False)).astype(np.uint64)
+        rows_c.append(cols)
+        rows_v.append((rng.standard_normal(len(cols)) * 0.05).astype(np.float32))
+    rp = np.zeros(m + 1, np.uint64)
+    rp[1:] = np.cumsum([len(c) for c in rows_c])
+    ci, vv = np.concatenate(rows_c), np.concatenate(rows_v)
+    layer = api.ApbLayer(m, k, alpha, api.BitMatrix.from_words(m, k, wpr, words),
+                         api.CsrMatrix.create(m, k, rp, ci, vv))
+    x = rng.standard_normal((k, n)).astype(np.float32)
+    got = api.layer_forward(layer, x)
+    want = orc.layer_forward(m, k, 1.0, words, wpr, rp, ci, vv, x, row_alpha=alpha)
+    for r in range(m):
+        check_close(got[r], want[r])
+    # a repeated column (only the device-pointer entry point accepts one; the host flavour
+    # validates strictly increasing columns like CsrMatrix::validate): both entries count
+    import torch
+    from paper_2306_08960_b200 import device
+    rows_c[3] = np.array([10, 10, 50, 199, 10], np.uint64)
+    rows_v[3] = np.array([0.05, -0.02, 0.01, 0.03, 0.04], np.float32)
+    rp[1:] = np.cumsum([len(c) for c in rows_c])
+    ci, vv = np.concatenate(rows_c), np.concatenate(rows_v)
+    T = lambda v: torch.from_numpy(np.ascontiguousarray(v)).cuda()  # noqa: E731
+    out = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    device.layer_forward(T(words.view(np.int64)), k, T(alpha), T(rp.view(np.int64)),
+                         T(ci.view(np.int64)), T(vv), T(x), out)
+    device.status()
+    want = orc.layer_forward(m, k, 1.0, words, wpr, rp, ci, vv, x, row_alpha=alpha)
+    got = out.cpu().numpy()
+    for r in range(m):
+        check_close(got[r], want[r])
