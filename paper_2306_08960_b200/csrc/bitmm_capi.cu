@@ -84,7 +84,12 @@ void trace_mark(DeviceState& st, const std::string& what, cudaStream_t on) {
   cudaEvent_t e = nullptr;
   cudaEventCreate(&e);
   cudaEventRecord(e, on);
-  st.timeline->emplace_back(what, e);
+  // host enqueue time (us since the first mark) goes into the label
+  static thread_local std::chrono::steady_clock::time_point t0;
+  const auto now = std::chrono::steady_clock::now();
+  if (st.timeline->empty()) t0 = now;
+  const long us = static_cast<long>(std::chrono::duration_cast<std::chrono::microseconds>(now - t0).count());
+  st.timeline->emplace_back(what + "@" + std::to_string(us), e);
 }
 
 std::mutex g_mu;
@@ -610,7 +615,8 @@ int run_pipelined_wire(DeviceState& st, cudaStream_t s, int64_t total, int64_t s
   std::vector<Part> parts;
   // Every slice's input copies go first, on their own stream: queued on s behind the
   // previous slice's GEMM they ran at a third of the link rate while the output copies
-  // were in flight (BITMM_WIRE_TRACE timelines).
+  // were in flight (BITMM_WIRE_TRACE device timelines). Issuing them two slices ahead of
+  // the GEMMs instead measured slower (e2e 50 vs 56-59 T-upd/s).
   BITMM_CUDA_TRY(cudaEventRecord(st.in_ev[kPipeChunks], s));  // after the call's setup copies
   BITMM_CUDA_TRY(cudaStreamWaitEvent(st.h2d, st.in_ev[kPipeChunks], 0));
   {
@@ -618,6 +624,7 @@ int run_pipelined_wire(DeviceState& st, cudaStream_t s, int64_t total, int64_t s
     for (int64_t c0 = 0; c0 < total; c0 += step, ++j) {
       BITMM_TRY(in(c0, std::min(total, c0 + step), st.h2d));
       BITMM_CUDA_TRY(cudaEventRecord(st.in_ev[j % kPipeChunks], st.h2d));
+      mark("i" + std::to_string(j), st.h2d);
     }
   }
   int rc = BITMM_OK;
