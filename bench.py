@@ -783,6 +783,28 @@ def e2e_pass(args, ops, torch, lib):
             raise RuntimeError(f"e2e {name}: {rc} {lib.bitmm_last_error().decode()}")
         return int(lib.bitmm_last_d2h_bytes())
 
+    def timed_pass(reps):
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            for r in ROUTINES:
+                call(*r)
+        return (time.perf_counter() - t0) / reps
+
+    # The reference-facing drop-in returns a DenseMatrix by value: its buffers are pageable
+    # (std::vector), not pinned. Time the same calls into pageable host arrays beside the
+    # pinned headline (informational; the library widens the 16-bit wire into them).
+    pinned_h = h
+    h = {name: {kk: (np.ascontiguousarray(v.numpy()) if kk != "out" else np.empty(tuple(v.shape), v.numpy().dtype))
+                for kk, v in hv.items()} for name, hv in pinned_h.items()}
+    P_np = lambda t: C.c_void_p(t.ctypes.data)  # noqa: E731
+    P_saved = P
+    P = P_np  # noqa: F841 (rebinding the closure's pointer helper)
+    for _ in range(2):
+        timed_pass(1)
+    pageable_ms = timed_pass(max(1, args.steps // 2)) * 1e3
+    h = pinned_h
+    P = P_saved
+
     for _ in range(max(args.warmup, 1)):
         # the library's own count of what crossed PCIe back (16-bit output wire where K allows)
         d2h = sum(call(*r) for r in ROUTINES)
@@ -803,7 +825,11 @@ def e2e_pass(args, ops, torch, lib):
             "output_bytes_per_step": int(sum(m * n * 4 for _, m, n, _ in ROUTINES)),
             "wire": "outputs cross PCIe as 16-bit integer units (device narrow, host widen and "
                     "scale, bit-identical to the device output); delivered as int32 / fp32",
-            "host_threads": host_threads()}
+            "host_threads": host_threads(),
+            "pageable_host_buffers": {"ms_per_step": pageable_ms,
+                                      "value": sum(m * n * k for _, m, n, k in ROUTINES) / (pageable_ms * 1e-3) / 1e12,
+                                      "note": "same calls on pageable numpy arrays (what a std::vector "
+                                              "DenseMatrix drop-in passes)"}}
 
 
 if __name__ == "__main__":
