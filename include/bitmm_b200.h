@@ -69,7 +69,7 @@ size_t bitmm_workspace_bytes(int routine, int64_t m, int64_t n, int64_t k);
 /* Number of kernels launched by the most recent compute call on this thread. */
 int bitmm_last_launch_count(void);
 /* Device -> host bytes copied by the most recent *_host GEMM call on this thread. The
- * 1/1, 1/2 and 2/2 host calls move their output as one 16-bit word per cell (the integer
+ * 1/1, 1/2 and 2/2 host calls with >= 32 MB of output move it as one 16-bit word per cell (the integer
  * units narrowed on the device, widened and scaled on the host into the caller's int32 /
  * fp32 buffers, bit-identical) whenever K allows: 1/1 K <= 65535, 1/2 K <= 10922,
  * 2/2 K <= 7281. BITMM_HOST_WIRE=32 in the environment forces the 4-byte copies. */

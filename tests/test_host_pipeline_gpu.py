@@ -167,7 +167,7 @@ def test_1x2_wire_bound(wire, k):
     (all-ones weights against all-p3 activations reach the bound); 10923 falls back."""
     lib = _lib.load()
     rng = np.random.default_rng(k)
-    m, n = 1030, 4400 if k == 777 else 600
+    m, n = 1030, 8200  # 33.8 MB of output: the wire applies from 32 MB
     w, wpr = data.random_words(rng, m, k)
     t, h, mm, _ = data.random_planes(rng, n, k)
     if k != 777:
@@ -199,7 +199,7 @@ def test_2x2_wire_bound(wire, k):
     """2/2 units = 4*sum p_w*p_a in [0, 36K]; K = 7281 is the last K the 16-bit wire carries."""
     lib = _lib.load()
     rng = np.random.default_rng(k)
-    m, n = (4200, 2100) if k == 700 else (300, 500)
+    m, n = 4200, 2100  # 35 MB of output: the wire applies from 32 MB
     wt, wh, wm, wpr = data.random_planes(rng, m, k)
     at, ah, am, _ = data.random_planes(rng, n, k)
     full = _full_row(k, wpr)
@@ -220,3 +220,16 @@ def test_2x2_wire_bound(wire, k):
     assert units[0, 0] == 36 * k
     narrow = wire == "wire16" and k <= 7281
     assert lib.bitmm_last_d2h_bytes() == m * n * (2 if narrow else 8)
+
+
+def test_small_outputs_keep_the_4_byte_copy(wire):
+    """Below 32 MB of output a host call copies 4-byte cells (one unsliced copy; the wire's
+    pool start-up would cost more than it saves)."""
+    lib = _lib.load()
+    rng = np.random.default_rng(16)
+    m, n, k = 1024, 1024, 1024
+    a, wpr = data.random_words(rng, m, k)
+    b, _ = data.random_words(rng, n, k)
+    units = np.empty((m, n), np.int32)
+    assert lib.bitmm_gemm_1x1_host(_p(a), m, _p(b), n, k, wpr, 1.0, 1.0, _p(units), None, n) == 0
+    assert lib.bitmm_last_d2h_bytes() == m * n * 4
