@@ -142,10 +142,17 @@ def test_layer_forward_empty_residual_and_odd_shapes(orc):
         check_close(got, want)
 
 
+@pytest.mark.parametrize("fold", ["same-stage", "sep"])
 @pytest.mark.parametrize("k", [900, 1000, 4096])
-def test_large_k_layer_forward(orc, k):
-    """K past the shared-memory X chunk (spmm falls back to the L2 gather kernel) and K=4096,
-    where split accumulators keep the tensor-core fp32 accumulation within tolerance."""
+def test_large_k_layer_forward(orc, k, fold, monkeypatch):
+    """K past the one-pass X split (x_token_scale + split_x_f16) and K=4096, where split
+    accumulators keep the tensor-core fp32 accumulation within tolerance. Both placements of
+    the folded residual's W'_lo . X_hi products: in the main K loop's stages (default) and as
+    a separate phase after it (BITMM_APB_FOLD=sep)."""
+    if fold == "sep":
+        monkeypatch.setenv("BITMM_APB_FOLD", "sep")
+    else:
+        monkeypatch.delenv("BITMM_APB_FOLD", raising=False)
     rng = np.random.default_rng(k)
     rows, tokens = 96, 200
     a, alpha, _ = data.apb_weights(rng, rows, k)
