@@ -556,12 +556,14 @@ int run_pipelined(DeviceState& st, cudaStream_t s, int64_t total, int64_t step, 
 // gemm(c0, c1) its GEMM on s once those copies are done. block(c0, c1) gives the output
 // block {row0, rows, col0, cols} the slice writes as int32 units into dcu (leading
 // dimension wo.ldc). A narrowing kernel follows each slice's GEMM on s and packs
-// its units into dwire; the d2h stream then copies them into pinned host staging in
-// kWireParts row parts, each with its own event. After the whole call is enqueued the host pool widens the
+// its units into dwire; the d2h stream then copies them into pinned host staging in row
+// parts of about kWirePartBytes, each with its own event. After the whole call is enqueued the host pool widens the
 // parts into the caller's buffers in order, while the later parts are still in flight.
-// Parts per slice: 4 measured best against 1, 2 and 8 (whole-slice parts delay the host's
-// widening, smaller ones slow the copies).
-constexpr int kWireParts = 4;
+// Copied parts of ~2 MiB: larger parts delay the host's widening, smaller ones slow the
+// copies. Measured per routine with 2, 4 and 8 parts per slice (profiles/dev/ab_wire_parts.sh):
+// the 4 MiB slices of 1/1 and 2/2 were fastest in two parts, the 8 MiB slices of 1/2 in four.
+constexpr size_t kWirePartBytes = size_t{2} << 20;
+constexpr int kWireMaxParts = 8;
 
 struct OutBlock {
   int64_t row0, rows, col0, cols;
@@ -659,7 +661,9 @@ int run_pipelined_wire(DeviceState& st, cudaStream_t s, int64_t total, int64_t s
       rc = fail(BITMM_ERR_CUDA, std::string("pipeline event: ") + cudaGetErrorString(cudaGetLastError()));
       break;
     }
-    const int64_t per = (b.rows + kWireParts - 1) / kWireParts;
+    const int64_t nparts = std::min<int64_t>(
+        kWireMaxParts, std::max<int64_t>(1, (cells * 2 + kWirePartBytes / 2) / kWirePartBytes));
+    const int64_t per = (b.rows + nparts - 1) / nparts;
     for (int64_t r0 = 0; r0 < b.rows; r0 += per) {
       const int64_t r1 = std::min(b.rows, r0 + per);
       const size_t o = off + static_cast<size_t>(r0 * b.cols), bytes = static_cast<size_t>((r1 - r0) * b.cols) * 2;
