@@ -72,6 +72,8 @@ struct DeviceState {
   cudaEvent_t pipe_ev[8] = {};
   cudaStream_t h2d = nullptr;             // host-flavour input copies (run_pipelined_wire)
   cudaEvent_t in_ev[9] = {};
+  uint32_t* in_flags = nullptr;           // per-slice "inputs landed" flags (wait_flag_kernel)
+  uint32_t in_epoch = 0;
   void* host_stage = nullptr;             // pinned 16-bit output words (run_pipelined_wire)
   size_t host_stage_bytes = 0;
   std::vector<cudaEvent_t> wire_ev;       // one per copied part
@@ -166,6 +168,39 @@ PFN_encodeTiled_t encode_fn() {
       fn = reinterpret_cast<PFN_encodeTiled_t>(p);
   });
   return fn;
+}
+
+// cuStreamWriteValue32 (a 32-bit write that executes in stream order on the copy stream).
+typedef CUresult (*PFN_writeValue32_t)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PFN_writeValue32_t write_value_fn() {
+  static PFN_writeValue32_t fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_writeValue32_t>(p);
+  });
+  return fn;
+}
+
+// Waits in a one-warp kernel until *flag == value: the copy stream writes the flag after a
+// slice's input copies (run_pipelined_wire). A spin on the SMs, not an event wait: the
+// GEMM stream's event waits on the copy stream resolved only once that stream had drained.
+// Gives up after ~2 s and latches ERR_COPY_TIMEOUT (never hangs the device).
+constexpr int ERR_COPY_TIMEOUT = 16;
+__global__ void wait_flag_kernel(const volatile uint32_t* flag, uint32_t value, int* err) {
+  if (threadIdx.x != 0) return;
+  const long long t0 = clock64();
+  while (*flag != value) {
+    if (clock64() - t0 > 4000000000ll) {
+      atomicOr(err, ERR_COPY_TIMEOUT);
+      break;
+    }
+    __nanosleep(200);
+  }
+  __threadfence();
 }
 
 // K-major operand [rows][inner] with 128-byte rows per box, 128B swizzle.
@@ -507,6 +542,7 @@ int read_status(DeviceState& st, cudaStream_t s) {
   if (flag & ERR_PADDING) return fail(BITMM_ERR_INVALID_ARGUMENT, "bit matrix padding must be zero");
   if (flag & ERR_LEVEL) return fail(BITMM_ERR_INVALID_ARGUMENT, "2-bit level out of range");
   if (flag & ERR_ALPHA) return fail(BITMM_ERR_INVALID_ARGUMENT, "alpha must be positive");
+  if (flag & ERR_COPY_TIMEOUT) return fail(BITMM_ERR_CUDA, "input copy did not complete (flag wait timed out)");
   return BITMM_OK;
 }
 
@@ -602,7 +638,13 @@ int run_pipelined_wire(DeviceState& st, cudaStream_t s, int64_t total, int64_t s
   if (!st.h2d) {
     BITMM_CUDA_TRY(cudaStreamCreateWithFlags(&st.h2d, cudaStreamNonBlocking));
     for (auto& e : st.in_ev) BITMM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    BITMM_CUDA_TRY(cudaMalloc(&st.in_flags, kPipeChunks * sizeof(uint32_t)));
+    BITMM_CUDA_TRY(cudaMemset(st.in_flags, 0, kPipeChunks * sizeof(uint32_t)));
   }
+  // flag waits need the driver's stream write; BITMM_WIRE_FLAGS=0 selects event waits
+  const char* fe = std::getenv("BITMM_WIRE_FLAGS");
+  const bool flags = write_value_fn() != nullptr && !(fe && std::atoi(fe) == 0);
+  const uint32_t epoch = ++st.in_epoch == 0 ? ++st.in_epoch : st.in_epoch;
   const auto t_call = std::chrono::steady_clock::now();
   static const bool trace = std::getenv("BITMM_WIRE_TRACE") != nullptr;
   // BITMM_WIRE_TRACE=nowiden: timeline of the copies alone (outputs left unwritten)
@@ -630,7 +672,13 @@ int run_pipelined_wire(DeviceState& st, cudaStream_t s, int64_t total, int64_t s
     int j = 0;
     for (int64_t c0 = 0; c0 < total; c0 += step, ++j) {
       BITMM_TRY(in(c0, std::min(total, c0 + step), st.h2d));
-      BITMM_CUDA_TRY(cudaEventRecord(st.in_ev[j % kPipeChunks], st.h2d));
+      if (flags) {
+        if (write_value_fn()(reinterpret_cast<CUstream>(st.h2d),
+                             reinterpret_cast<CUdeviceptr>(st.in_flags + (j % kPipeChunks)), epoch, 0) != CUDA_SUCCESS)
+          return fail(BITMM_ERR_CUDA, "cuStreamWriteValue32 failed");
+      } else {
+        BITMM_CUDA_TRY(cudaEventRecord(st.in_ev[j % kPipeChunks], st.h2d));
+      }
       mark("i" + std::to_string(j), st.h2d);
     }
   }
@@ -639,7 +687,11 @@ int run_pipelined_wire(DeviceState& st, cudaStream_t s, int64_t total, int64_t s
   int i = 0;
   for (int64_t c0 = 0; c0 < total && rc == BITMM_OK; c0 += step, ++i) {
     const int64_t c1 = std::min(total, c0 + step);
-    if (cudaStreamWaitEvent(s, st.in_ev[i % kPipeChunks], 0) != cudaSuccess) {
+    if (flags) {
+      wait_flag_kernel<<<1, 32, 0, s>>>(st.in_flags + (i % kPipeChunks), epoch, st.status);
+      rc = launch_check("wait_flag_kernel");
+      if (rc != BITMM_OK) break;
+    } else if (cudaStreamWaitEvent(s, st.in_ev[i % kPipeChunks], 0) != cudaSuccess) {
       rc = fail(BITMM_ERR_CUDA, "pipeline input event");
       break;
     }
