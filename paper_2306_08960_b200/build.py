@@ -49,25 +49,29 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = LIB_PATH,
+          extra: tuple = ()) -> str:
+    """Build the library into `out` (default: the in-tree libbitmm_b200.so). `extra`: more
+    nvcc flags (A/B variants, e.g. ("-DFX_STATS",), built next to the product library)."""
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [
         os.path.join(INCLUDE, "bitmm_b200.h"),
         os.path.abspath(__file__),
     ]
-    if not force and not _stale(LIB_PATH, deps):
-        return LIB_PATH
-    tmp = LIB_PATH + ".tmp"
+    if not force and not extra and not _stale(out, deps):
+        return out
+    tmp = out + ".tmp"
     cmd = (
         [nvcc()]
         + ARCH_FLAGS
         + NVCC_FLAGS
         + os.environ.get("BITMM_NVCC_EXTRA", "").split()  # A/B builds, e.g. -DSPMM_SCRATCH
+        + list(extra)
         + ["-I", INCLUDE, "-I", CSRC, "-shared", "-o", tmp]
         + [os.path.join(CSRC, s) for s in SOURCES]
         + ["-cudart", "static", "-Xlinker", "-soname=libbitmm_b200.so"]
     )
     proc = subprocess.run(cmd, capture_output=True, text=True)
-    log_path = os.path.join(PKG_DIR, "build.log")
+    log_path = os.path.join(PKG_DIR, "build.log") if out == LIB_PATH else out + ".log"
     with open(log_path, "w") as f:
         f.write(" ".join(cmd) + "\n" + proc.stdout + proc.stderr)
     if proc.returncode != 0:
@@ -75,9 +79,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed (see {log_path})")
     if verbose:
         sys.stdout.write(proc.stdout + proc.stderr)
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python -m paper_2306_08960_b200.build [--force] [-v] [--out PATH -- NVCC_FLAGS...]
+    argv = sys.argv[1:]
+    extra = tuple(argv[argv.index("--") + 1:]) if "--" in argv else ()
+    out = argv[argv.index("--out") + 1] if "--out" in argv else LIB_PATH
+    print(build(force="--force" in argv, verbose="-v" in argv, out=os.path.abspath(out), extra=extra))

@@ -18,6 +18,8 @@
 #include "apb_gemm.cuh"
 #include "btsr_io.cuh"
 #include "bitmm_b200.h"
+#include "fx_gemm.cuh"
+#include "prep.cuh"
 #include "pack.cuh"
 #include "popc_gemm.cuh"
 #include "ptx.cuh"
@@ -63,6 +65,7 @@ struct DeviceState {
   int sms = 0;
   int* status = nullptr;  // latched device-side encoding flags
   Arena ws;               // intermediates (expanded operands)
+  Arena codes;            // 2-bit level codes of the in-GEMM expansion path (fx_gemm)
   Arena io;               // host-flavour staging of inputs/outputs
   cudaStream_t stream = nullptr;  // host-flavour private stream
   unsigned ws_turn = 0;           // ping-pong half of the expanded-operand workspace
@@ -149,6 +152,20 @@ int arena_reserve(Arena& a, size_t bytes) {
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+// Sequential 1024-byte aligned sub-buffers of one allocation.
+struct Carve {
+  uint8_t* base;
+  size_t off = 0;
+  explicit Carve(void* b) : base(static_cast<uint8_t*>(b)) {}
+  template <typename T>
+  T* take(size_t bytes) {
+    T* p = reinterpret_cast<T*>(base + off);
+    off = align_up(off + bytes, 1024);
+    return p;
+  }
+};
+
 
 // ---------------- TMA descriptors (driver entry point, no -lcuda) ----------------
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -523,6 +540,259 @@ int run_int_gemm(DeviceState& st, const uint8_t* A8, const uint8_t* B8, int64_t 
   return cnt ? run_problems(st, probs, cnt, fp4, s) : BITMM_OK;
 }
 
+// ---------------- in-GEMM expansion path (fx_gemm.cuh) ----------------
+// Selectable with BITMM_FX=1 (measured, not the default: DESIGN.md "in-GEMM expansion").
+// Sign operands are read as the caller's BitMatrix words; level operands go through one prep
+// pass (2-bit codes, validated). It needs TMA-readable packed rows: an even words_per_row
+// (16-byte row pitch) and 16-byte aligned bases; other calls take the default path.
+bool fx_enabled() {
+  static const bool on = getenv("BITMM_FX") && atoi(getenv("BITMM_FX")) == 1;
+  return on && use_fp4();
+}
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+bool fx_operand_ok(const OperandSrc& o, int64_t wpr) {
+  if (wpr & 1) return false;
+  return aligned16(o.w0) && (!o.levels || (aligned16(o.w1) && aligned16(o.w2)));
+}
+int64_t kcode_for(int64_t k) { return round_up(k, FX_KSLOT); }
+
+// One routine call on the fx path: the operands in the reference layouts and its outputs
+// (units and/or fp32; both come from one launch of two problems over the same operands).
+struct FxItem {
+  OperandSrc a, b;
+  int64_t k, wpr;
+  int shift;
+  float scale;
+  const float* row_scale;
+  const float* col_scale;
+  int32_t* c_units;
+  float* c;
+  int64_t ldc;
+  bool f32r;  // reference-order per-row scales (2-bit APB layer)
+  float row_pre, act_scale, act_gamma;
+};
+
+// One GEMM problem of an fx launch: packed sources after the prep pass.
+struct FxProb {
+  const void* a_src;
+  const void* b_src;
+  int a_code, b_code;
+  int64_t m, n, k, wpr;
+  TcParams p;
+};
+
+// Expander warps per CTA. 8 of them (448 threads) cap registers at 128, where the run-time
+// epilogue switch of the grouped kernel (Epi::ANY) spills; it runs 4 (384 threads, 168).
+#ifndef FX_NEXP
+#define FX_NEXP 8
+#endif
+#ifndef FX_NEXP_ANY
+#define FX_NEXP_ANY 4
+#endif
+template <Epi EPI>
+constexpr int fx_exp() { return EPI == Epi::ANY ? FX_NEXP_ANY : FX_NEXP; }
+
+// Packed operand [rows][row_bytes] read by TMA in boxes of box_bytes x box_rows (no swizzle:
+// the expanders address the slot rows directly).
+int make_packed_map(CUtensorMap* map, const void* base, uint64_t row_bytes, uint64_t rows,
+                    uint32_t box_bytes, uint32_t box_rows) {
+  PFN_encodeTiled_t enc = encode_fn();
+  if (!enc) return fail(BITMM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {row_bytes, rows};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {box_bytes, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(BITMM_ERR_CUDA, "cuTensorMapEncodeTiled (packed) failed: " + std::to_string(r));
+  return BITMM_OK;
+}
+
+template <Epi EPI, int NP, int SLOT_ROW>
+int run_fx_group(DeviceState& st, const FxProb* probs, int count, cudaStream_t s) {
+  using S = FxShape<fx_exp<EPI>(), SLOT_ROW>;
+  auto kern = fx_gemm_kernel<EPI, NP, fx_exp<EPI>(), SLOT_ROW>;
+  BITMM_TRY(ensure_max_smem(reinterpret_cast<const void*>(kern), S::SMEM));
+  FxGroup<NP> g;
+  memset(&g, 0, sizeof(g));
+  int tiles = 0;
+  for (int i = 0; i < count; ++i) {
+    const FxProb& q = probs[i];
+    const uint64_t kc = static_cast<uint64_t>(kcode_for(q.k));
+    BITMM_TRY(make_packed_map(&g.a[i], q.a_src, q.a_code ? kc / 4 : q.wpr * 8, q.m, q.a_code ? 128 : 64, S::A_ROWS));
+    BITMM_TRY(make_packed_map(&g.b[i], q.b_src, q.b_code ? kc / 4 : q.wpr * 8, q.n, q.b_code ? 128 : 64, S::B_ROWS));
+    TcParams p = q.p;
+    p.M = static_cast<int>(q.m);
+    p.N = static_cast<int>(q.n);
+    const int64_t kpad = round_up(q.k, FX_KSTAGE);
+    p.num_kb = static_cast<int>(kpad / FX_KSTAGE);
+    p.small_acc = 36 * kpad < (int64_t{1} << 22) ? 1 : 0;
+    p.shift_mul = static_cast<float>(1 << p.shift);
+    p.num_m_blocks = static_cast<int>((q.m + S::TILE_M - 1) / S::TILE_M);
+    p.num_n_blocks = static_cast<int>((q.n + S::BN - 1) / S::BN);
+    p.num_tiles = p.num_m_blocks * p.num_n_blocks;
+    p.group_m = TC_GROUP_M;
+    const bool i32 = p.epi == static_cast<int>(Epi::I32);
+    void* out = i32 ? static_cast<void*>(p.out_i32) : static_cast<void*>(p.out_f32);
+    p.tma_store = make_output_map(&g.c[i], out, i32 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                  p.N, p.M, p.ldc) ? 1 : 0;
+    g.prob[i] = p;
+    g.a_code[i] = q.a_code;
+    g.b_code[i] = q.b_code;
+    g.K[i] = static_cast<int>(q.k);
+    g.tile_begin[i] = tiles;
+    tiles += p.num_tiles;
+  }
+  g.count = count;
+  for (int i = count; i <= NP; ++i) g.tile_begin[i] = tiles;
+  const int units = std::min(tiles, st.sms / 2);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(2 * units));
+  cfg.blockDim = dim3(S::THREADS);
+  cfg.dynamicSmemBytes = S::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  ProfScope ps("fx_gemm_f4", s);
+  BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, g));
+  return launch_check("fx_gemm_kernel");
+}
+
+template <int SLOT_ROW>
+int dispatch_fx(DeviceState& st, const FxProb* probs, int count, cudaStream_t s) {
+  if (count == 1) {
+    const int e = probs[0].p.epi;
+    if (e == static_cast<int>(Epi::I32)) return run_fx_group<Epi::I32, 1, SLOT_ROW>(st, probs, 1, s);
+    if (e == static_cast<int>(Epi::F32)) return run_fx_group<Epi::F32, 1, SLOT_ROW>(st, probs, 1, s);
+    return run_fx_group<Epi::F32R, 1, SLOT_ROW>(st, probs, 1, s);
+  }
+  for (int i = 0; i < count; ++i)
+    if (probs[i].p.epi == static_cast<int>(Epi::F32R))
+      return fail(BITMM_ERR_INVALID_ARGUMENT, "reference-order row scales are single-problem only");
+  if (count == 2) return run_fx_group<Epi::ANY, 2, SLOT_ROW>(st, probs, 2, s);
+  return run_fx_group<Epi::ANY, TC_GROUP_MAX, SLOT_ROW>(st, probs, count, s);
+}
+
+// Prep pass (codes for level operands, padding checks for sign operands with bits past K),
+// then one fx_gemm launch over every problem of the items.
+int run_fx(DeviceState& st, const FxItem* items, int count, cudaStream_t s) {
+  size_t code_bytes = 1024;
+  for (int i = 0; i < count; ++i) {
+    const int64_t kc = kcode_for(items[i].k);
+    if (items[i].a.levels) code_bytes += align_up(items[i].a.rows * kc / 4, 1024);
+    if (items[i].b.levels) code_bytes += align_up(items[i].b.rows * kc / 4, 1024);
+  }
+  BITMM_TRY(arena_reserve(st.codes, code_bytes));
+  Carve cv(st.codes.ptr);
+  PrepSet P{};
+  P.err = st.status;
+  long long max_items = 0;
+  auto prep = [&](const OperandSrc& o, int64_t k, int64_t wpr, int* code) -> const void* {
+    *code = 0;
+    if (o.levels) {
+      const int64_t kc = kcode_for(k);
+      uint2* codes = cv.take<uint2>(o.rows * kc / 4);
+      PrepOperand& q = P.op[P.count++];
+      q = PrepOperand{o.w0, o.w1, o.w2, codes, o.rows, static_cast<int>(wpr), static_cast<int>(k), 0,
+                      static_cast<int>(kc / 64), 1, o.rows * std::max<int64_t>(wpr, kc / 64)};
+      max_items = std::max(max_items, q.items);
+      *code = 1;
+      return codes;
+    }
+    if (wpr * 64 > k) {  // words holding bits past K: the padding check (tensor.cpp:78-89)
+      PrepOperand& q = P.op[P.count++];
+      q = PrepOperand{o.w0, nullptr, nullptr, nullptr, o.rows, static_cast<int>(wpr), static_cast<int>(k),
+                      static_cast<int>(k / 64), 0, 0, o.rows * (wpr - k / 64)};
+      max_items = std::max(max_items, q.items);
+    }
+    return o.w0;
+  };
+  FxProb probs[TC_GROUP_MAX];
+  int np = 0;
+  bool any_code = false;
+  for (int i = 0; i < count; ++i) {
+    const FxItem& it = items[i];
+    FxProb q{};
+    q.a_src = prep(it.a, it.k, it.wpr, &q.a_code);
+    q.b_src = prep(it.b, it.k, it.wpr, &q.b_code);
+    any_code = any_code || q.a_code || q.b_code;
+    q.m = it.a.rows;
+    q.n = it.b.rows;
+    q.k = it.k;
+    q.wpr = it.wpr;
+    TcParams p{};
+    p.shift = it.shift;
+    p.scale = it.scale;
+    p.row_scale = it.row_scale;
+    p.col_scale = it.col_scale;
+    p.ldc = it.ldc;
+    if (it.f32r) {
+      p.row_pre = it.row_pre;
+      p.act_scale = it.act_scale;
+      p.act_gamma = it.act_gamma;
+      p.out_f32 = it.c;
+      p.epi = static_cast<int>(Epi::F32R);
+      q.p = p;
+      probs[np++] = q;
+      continue;
+    }
+    if (it.c_units) {
+      q.p = p;
+      q.p.out_i32 = it.c_units;
+      q.p.epi = static_cast<int>(Epi::I32);
+      probs[np++] = q;
+    }
+    if (it.c) {
+      q.p = p;
+      q.p.out_f32 = it.c;
+      q.p.epi = static_cast<int>(Epi::F32);
+      probs[np++] = q;
+    }
+  }
+  if (np > TC_GROUP_MAX) return fail(BITMM_ERR_INVALID_ARGUMENT, "batch exceeds 4 GEMM outputs");
+  if (P.count) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks_for(max_items, 256), static_cast<unsigned>(P.count));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ProfScope ps("prep_operands", s);
+    BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, prep_operands_kernel, P));
+    BITMM_TRY(launch_check("prep_operands_kernel"));
+  }
+  if (np == 0) return BITMM_OK;
+  return any_code ? dispatch_fx<128>(st, probs, np, s) : dispatch_fx<64>(st, probs, np, s);
+}
+
+FxItem fx_item(const OperandSrc& a, const OperandSrc& b, int64_t k, int64_t wpr, int shift, float scale,
+               const float* row_scale, const float* col_scale, int32_t* c_units, float* c, int64_t ldc) {
+  FxItem it{};
+  it.a = a;
+  it.b = b;
+  it.k = k;
+  it.wpr = wpr;
+  it.shift = shift;
+  it.scale = scale;
+  it.row_scale = row_scale;
+  it.col_scale = col_scale;
+  it.c_units = c_units;
+  it.c = c;
+  it.ldc = ldc;
+  return it;
+}
+
 int check_gemm_dims(int64_t m, int64_t n, int64_t k, int64_t wpr, int64_t ldc) {
   if (m <= 0 || k <= 0 || n <= 0) return fail(BITMM_ERR_INVALID_ARGUMENT, "gemm dimensions must be positive");
   if (k > BITMM_MAX_SHARED_DIM)
@@ -797,18 +1067,6 @@ int run_pipelined_wire(DeviceState& st, cudaStream_t s, int64_t total, int64_t s
   return rc;
 }
 
-struct Carve {
-  uint8_t* base;
-  size_t off = 0;
-  explicit Carve(void* b) : base(static_cast<uint8_t*>(b)) {}
-  template <typename T>
-  T* take(size_t bytes) {
-    T* p = reinterpret_cast<T*>(base + off);
-    off = align_up(off + bytes, 1024);
-    return p;
-  }
-};
-
 size_t ws_half_int(int64_t m, int64_t n, int64_t k) {
   const int64_t kpad = round_up(k, TC_BK_BYTES);
   return align_up(m * kpad, 1024) + align_up(n * kpad, 1024) + 2048;
@@ -839,13 +1097,17 @@ int gemm_1x1_dev_impl(DeviceState& st, const uint64_t* a, int64_t m, const uint6
                       int64_t k, int64_t wpr, float gamma_a, float gamma_b, int32_t* c_units,
                       float* c, int64_t ldc, cudaStream_t s) {
   const bool fp4 = use_fp4();
+  const float scale = gamma_a * gamma_b;  // kernels.cpp:170
+  const OperandSrc sa{a, nullptr, nullptr, m, false}, sb{b, nullptr, nullptr, n, false};
+  if (fx_enabled() && fx_operand_ok(sa, wpr) && fx_operand_ok(sb, wpr)) {
+    const FxItem it = fx_item(sa, sb, k, wpr, 0, scale, nullptr, nullptr, c_units, c, ldc);
+    return run_fx(st, &it, 1, s);
+  }
   const int64_t kpad = kpad_for(k, fp4);
   BITMM_TRY(arena_reserve(st.ws, ws_bytes_int(m, n, k)));
   uint8_t *A8, *B8;
   take_int_operands(st, m, n, k, &A8, &B8);
-  BITMM_TRY(run_unpack_pair({a, nullptr, nullptr, m, false}, {b, nullptr, nullptr, n, false}, wpr,
-                            k, kpad, A8, B8, st.status, s, fp4));
-  const float scale = gamma_a * gamma_b;  // kernels.cpp:170
+  BITMM_TRY(run_unpack_pair(sa, sb, wpr, k, kpad, A8, B8, st.status, s, fp4));
   return run_int_gemm(st, A8, B8, m, n, kpad, 0, scale, nullptr, nullptr, c_units, c, ldc, s, fp4);
 }
 
@@ -855,14 +1117,19 @@ int gemm_1x2_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, float gamma
                       const float* col_scale, int32_t* c_units, float* c, int64_t ldc,
                       cudaStream_t s) {
   const bool fp4 = use_fp4();
+  // kernels.cpp:193: half_scale = 0.5f * gamma * a_packed.scale * a_packed.gamma.value_or(1.0f)
+  const float scale = 0.5f * gamma * a_scale * (has_a_gamma ? a_gamma : 1.0f);
+  const OperandSrc sa{w, nullptr, nullptr, m, false}, sb{t, h, mm, n, true};
+  if (fx_enabled() && fx_operand_ok(sa, wpr) && fx_operand_ok(sb, wpr)) {
+    const FxItem it = fx_item(sa, sb, k, wpr, fp4_shift(1, 1, true), scale, row_scale, col_scale,
+                              c_units, c, ldc);
+    return run_fx(st, &it, 1, s);
+  }
   const int64_t kpad = kpad_for(k, fp4);
   BITMM_TRY(arena_reserve(st.ws, ws_bytes_int(m, n, k)));
   uint8_t *A8, *B8;
   take_int_operands(st, m, n, k, &A8, &B8);
-  BITMM_TRY(run_unpack_pair({w, nullptr, nullptr, m, false}, {t, h, mm, n, true}, wpr, k, kpad, A8,
-                            B8, st.status, s, fp4));
-  // kernels.cpp:193: half_scale = 0.5f * gamma * a_packed.scale * a_packed.gamma.value_or(1.0f)
-  const float scale = 0.5f * gamma * a_scale * (has_a_gamma ? a_gamma : 1.0f);
+  BITMM_TRY(run_unpack_pair(sa, sb, wpr, k, kpad, A8, B8, st.status, s, fp4));
   return run_int_gemm(st, A8, B8, m, n, kpad, fp4_shift(1, 1, fp4), scale, row_scale, col_scale,
                       c_units, c, ldc, s, fp4);
 }
@@ -874,15 +1141,20 @@ int gemm_2x2_dev_impl(DeviceState& st, const uint64_t* wt, const uint64_t* wh, c
                       const float* col_scale, int32_t* c_units, float* c, int64_t ldc,
                       cudaStream_t s) {
   const bool fp4 = use_fp4();
+  // kernels.cpp:232-233
+  const float scale = 0.25f * w_scale * a_scale * (has_w_gamma ? w_gamma : 1.0f) *
+                      (has_a_gamma ? a_gamma : 1.0f);
+  const OperandSrc sa{wt, wh, wm, m, true}, sb{at, ah, am, n, true};
+  if (fx_enabled() && fx_operand_ok(sa, wpr) && fx_operand_ok(sb, wpr)) {
+    const FxItem it = fx_item(sa, sb, k, wpr, fp4_shift(2, 2, true), scale, row_scale, col_scale,
+                              c_units, c, ldc);
+    return run_fx(st, &it, 1, s);
+  }
   const int64_t kpad = kpad_for(k, fp4);
   BITMM_TRY(arena_reserve(st.ws, ws_bytes_int(m, n, k)));
   uint8_t *A8, *B8;
   take_int_operands(st, m, n, k, &A8, &B8);
-  BITMM_TRY(run_unpack_pair({wt, wh, wm, m, true}, {at, ah, am, n, true}, wpr, k, kpad, A8, B8,
-                            st.status, s, fp4));
-  // kernels.cpp:232-233
-  const float scale = 0.25f * w_scale * a_scale * (has_w_gamma ? w_gamma : 1.0f) *
-                      (has_a_gamma ? a_gamma : 1.0f);
+  BITMM_TRY(run_unpack_pair(sa, sb, wpr, k, kpad, A8, B8, st.status, s, fp4));
   return run_int_gemm(st, A8, B8, m, n, kpad, fp4_shift(2, 2, fp4), scale, row_scale, col_scale,
                       c_units, c, ldc, s, fp4);
 }
@@ -1124,10 +1396,13 @@ int apb2_dev_impl(DeviceState& st, int64_t rows, int64_t cols, int64_t wpr, floa
   const int64_t kpad = kpad_for(cols, fp4);
   BITMM_TRY(arena_reserve(st.ws, ws_bytes_apb2(st, rows, cols, tokens)));
   float* deq = reinterpret_cast<float*>(static_cast<uint8_t*>(st.ws.ptr) + ws_bytes_int(rows, tokens, cols));
-  uint8_t *A8, *B8;
-  take_int_operands(st, rows, tokens, cols, &A8, &B8);
-  BITMM_TRY(run_unpack_pair({bin, nullptr, nullptr, rows, false}, {t, h, m, tokens, true}, wpr, cols,
-                            kpad, A8, B8, st.status, s, fp4));
+  const OperandSrc sa{bin, nullptr, nullptr, rows, false}, sb{t, h, m, tokens, true};
+  const bool fx = fx_enabled() && fx_operand_ok(sa, wpr) && fx_operand_ok(sb, wpr);
+  uint8_t *A8 = nullptr, *B8 = nullptr;
+  if (!fx) {
+    take_int_operands(st, rows, tokens, cols, &A8, &B8);
+    BITMM_TRY(run_unpack_pair(sa, sb, wpr, cols, kpad, A8, B8, st.status, s, fp4));
+  }
   GemmProblem q{A8, B8, rows, tokens, kpad, TcParams{}};
   q.p.shift = fp4_shift(1, 1, fp4);
   q.p.scale = 0.5f * alpha * a_scale * a_gamma;  // kernels.cpp:193 order
@@ -1138,7 +1413,16 @@ int apb2_dev_impl(DeviceState& st, int64_t rows, int64_t cols, int64_t wpr, floa
   q.p.out_f32 = c;
   q.p.ldc = ldc;
   q.p.epi = static_cast<int>(Epi::F32R);
-  BITMM_TRY(run_problems(st, &q, 1, fp4, s));
+  if (fx) {
+    FxItem it = fx_item(sa, sb, cols, wpr, q.p.shift, q.p.scale, row_alpha, nullptr, nullptr, c, ldc);
+    it.f32r = true;
+    it.row_pre = q.p.row_pre;
+    it.act_scale = a_scale;
+    it.act_gamma = a_gamma;
+    BITMM_TRY(run_fx(st, &it, 1, s));
+  } else {
+    BITMM_TRY(run_problems(st, &q, 1, fp4, s));
+  }
   SpmmLevels lv{};
   lv.t = reinterpret_cast<const unsigned long long*>(t);
   lv.h = reinterpret_cast<const unsigned long long*>(h);
@@ -1181,6 +1465,13 @@ int check_csr_host(int64_t rows, int64_t cols, const uint64_t* row_ptr, const ui
 extern "C" {
 
 int bitmm_abi_version(void) { return 1; }
+
+#ifdef FX_STATS
+// Profiling builds only (-DFX_STATS): the fx_gemm wait counters of the last launch.
+int bitmm_debug_fx_stats(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, fx_stats, sizeof(fx_stats)) == cudaSuccess ? 0 : 3;
+}
+#endif
 
 const char* bitmm_last_error(void) { return g_err.c_str(); }
 
@@ -2024,6 +2315,21 @@ int bitmm_layer_forward_2bit_host(int64_t rows, int64_t cols, float alpha, const
 }
 
 // ---------------- GEMM group ----------------
+// Reference shift and scale of one batch item.
+static void batch_scale(const bitmm_gemm_item& it, int* shift, float* scale) {
+  if (it.routine == BITMM_ROUTINE_1X1) {  // kernels.cpp:170
+    *shift = 0;
+    *scale = it.a_scale * it.b_scale;
+  } else if (it.routine == BITMM_ROUTINE_1X2) {  // kernels.cpp:193
+    *shift = 1;
+    *scale = 0.5f * it.a_scale * it.b_scale * (it.has_b_gamma ? it.b_gamma : 1.0f);
+  } else {  // kernels.cpp:232-233
+    *shift = 2;
+    *scale = 0.25f * it.a_scale * it.b_scale * (it.has_a_gamma ? it.a_gamma : 1.0f) *
+             (it.has_b_gamma ? it.b_gamma : 1.0f);
+  }
+}
+
 int bitmm_gemm_batch_dev(const bitmm_gemm_item* items, int count, void* stream) {
   g_launches = 0;
   if (count <= 0 || count > TC_GROUP_MAX || items == nullptr)
@@ -2049,6 +2355,26 @@ int bitmm_gemm_batch_dev(const bitmm_gemm_item* items, int count, void* stream) 
   BITMM_TRY(with_device(&st));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool fp4 = use_fp4();
+  {
+    // in-GEMM expansion: one prep launch (codes / padding checks) + one fx_gemm launch
+    FxItem fit[TC_GROUP_MAX];
+    bool ok = fx_enabled();
+    for (int i = 0; i < count && ok; ++i) {
+      const bitmm_gemm_item& it = items[i];
+      const bool planes_a = it.routine == BITMM_ROUTINE_2X2, planes_b = it.routine != BITMM_ROUTINE_1X1;
+      const OperandSrc sa{it.a0, it.a1, it.a2, it.m, planes_a}, sb{it.b0, it.b1, it.b2, it.n, planes_b};
+      ok = fx_operand_ok(sa, it.wpr) && fx_operand_ok(sb, it.wpr);
+      int shift;
+      float scale;
+      batch_scale(it, &shift, &scale);
+      const float* rs = it.routine == BITMM_ROUTINE_1X1 ? nullptr : it.row_scale;
+      const float* cs = it.routine == BITMM_ROUTINE_1X1 ? nullptr : it.col_scale;
+      fit[i] = fx_item(sa, sb, it.k, it.wpr,
+                       fp4_shift(shift, static_cast<int>(planes_a) + static_cast<int>(planes_b), true), scale,
+                       rs, cs, it.c_units, it.c, it.ldc);
+    }
+    if (ok) return run_fx(*st, fit, count, s);
+  }
   size_t bytes = 2048;
   for (int i = 0; i < count; ++i) {
     const int64_t rb = row_bytes(kpad_for(items[i].k, fp4), fp4);
@@ -2071,17 +2397,7 @@ int bitmm_gemm_batch_dev(const bitmm_gemm_item* items, int count, void* stream) 
     U.op[U.count++] = make_unpack_operand({it.b0, it.b1, it.b2, it.n, planes_b}, it.wpr, it.k, kpad, B8);
     int shift;
     float scale;
-    if (it.routine == BITMM_ROUTINE_1X1) {  // kernels.cpp:170
-      shift = 0;
-      scale = it.a_scale * it.b_scale;
-    } else if (it.routine == BITMM_ROUTINE_1X2) {  // kernels.cpp:193
-      shift = 1;
-      scale = 0.5f * it.a_scale * it.b_scale * (it.has_b_gamma ? it.b_gamma : 1.0f);
-    } else {  // kernels.cpp:232-233
-      shift = 2;
-      scale = 0.25f * it.a_scale * it.b_scale * (it.has_a_gamma ? it.a_gamma : 1.0f) *
-              (it.has_b_gamma ? it.b_gamma : 1.0f);
-    }
+    batch_scale(it, &shift, &scale);
     const float* rs = it.routine == BITMM_ROUTINE_1X1 ? nullptr : it.row_scale;
     const float* cs = it.routine == BITMM_ROUTINE_1X1 ? nullptr : it.col_scale;
     shift = fp4_shift(shift, static_cast<int>(planes_a) + static_cast<int>(planes_b), fp4);

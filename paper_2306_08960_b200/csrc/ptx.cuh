@@ -191,6 +191,11 @@ __device__ __forceinline__ void cluster_sync() {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// Orders this thread's generic-proxy writes (any state space) before later async-proxy
+// accesses: shared-memory operands written with st.shared and then read by tcgen05.mma.
+__device__ __forceinline__ void fence_proxy_async_all() {
+  asm volatile("fence.proxy.async;" ::: "memory");
+}
 
 // Pair TMA: data lands in this CTA's smem, transaction bytes are credited to the
 // leader CTA's mbarrier (the same barrier offset with the peer bit cleared).
