@@ -13,8 +13,11 @@ resident in HBM; the bit -> int8 expansion kernels are inside the timed region.
 With N>1 ranks (torchrun, NCCL) the output-column dimension is sharded:
 rank g computes output columns [g*N, (g+1)*N) of a G-times wider problem (A replicated,
 its own b_packed rows), so per-rank work is fixed and there is no data-path collective
-(weak scaling). The NCCL gather of the result blocks to rank 0, the north star's one
-cross-GPU step, is timed separately after the step and reported under "gather".
+(weak scaling). Without torchrun, `--gpus N` re-launches itself with N ranks (and fails if
+fewer than N GPUs are visible). At every N the line also carries `c5_sweep`: BASELINE config
+5, 1/1 32768^3 with N sharded across the ranks, timed kernel-only, with the gather fused into
+the GEMM epilogue (each rank stores its column block into rank 0's matrix over NVLink,
+shard.PeerOutput), and with the NCCL gather (shard.run_sharded, uint16 popcount wire).
 `--impl reference` times the reference CPU implementation instead (rank 0).
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
@@ -294,6 +297,26 @@ def workload_config(world):
 
 
 # ----------------------------------------------------------------------------- GPU arm
+def self_launch(args, visible_gpus):
+    """`--gpus N` (N > 1) without torchrun: re-run this script as N ranks of one node (the
+    driver's own launch line), or fail loudly when fewer than N GPUs are visible. Returns the
+    exit code to use, or None when this process is already a rank."""
+    if "WORLD_SIZE" in os.environ or args.gpus <= 1:
+        return None
+    if visible_gpus < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found "
+                         f"{visible_gpus}; refusing to time fewer\n")
+        return 2
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse_args()
     if args.impl == "reference":
@@ -303,11 +326,17 @@ def main():
     import torch.distributed as dist
     from paper_2306_08960_b200 import _lib, device
 
+    rc = self_launch(args, torch.cuda.device_count())
+    if rc is not None:
+        return rc
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local_rank = env_int("LOCAL_RANK", 0)
     torch.cuda.set_device(local_rank)
     if world > 1:
+        # NCCL's INIT lines (ranks, NVLink/NVLS transport) go to the log beside the JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     lib = _lib.load()
     dev = torch.device("cuda", local_rank)
@@ -501,6 +530,12 @@ def main():
         kernels[lib.bitmm_profile_kernel_name(i).decode()] = {
             "launches": lib.bitmm_profile_kernel_launches(i), "ms": lib.bitmm_profile_kernel_ms(i)}
 
+    # ---- BASELINE config 5 at this N: kernel-only, gather fused into the epilogue, NCCL ----
+    del d
+    torch.cuda.empty_cache()
+    sweep = c5_sweep(GpuC5Backend(torch, dev, lib), dist if world > 1 else None, world, rank,
+                     C5, C5, C5)
+
     if world > 1:
         dist.barrier()
     if rank != 0:
@@ -570,6 +605,8 @@ def main():
     }
     if gather is not None:
         line["gather"] = gather
+    sweep["frac_of_tensor_peak_kernel"] = (2 * C5 ** 3 / (sweep["kernel_ms"] * 1e-3) / 1e12) / peak
+    line["c5_sweep"] = sweep
     if seq_ms is not None:
         line["sequential_calls"] = {"ms_per_step": seq_ms,
                                     "value": upd_per_step / (seq_ms * 1e-3) / 1e12,
@@ -578,7 +615,7 @@ def main():
     if world == 1:
         line["apb"] = apb_pass(args, torch, lib, l2_flush, peaks)
         line["apb_2bit"] = apb2_pass(args, torch, l2_flush, peak)
-        line["c5_single_gpu"] = c5_pass(torch, peak)
+        line["c5_single_gpu"] = c5_single_line(sweep, peak)
     if world == 1 and not args.no_e2e:
         line["e2e"] = e2e_pass(args, ops, torch, lib)
     if world == 1 and not args.no_cpu_baseline:
@@ -601,33 +638,152 @@ def main():
     return 0
 
 
-def c5_pass(torch, peak):
-    """BASELINE config 5 at N=1: 1/1 M=N=K=32768, int32 units (the N-sharded sweep's single
-    GPU point). Two timed repetitions after one warm call (inputs >> L2)."""
-    from paper_2306_08960_b200 import data, device
+# ----------------------------------------------------------------------------- config 5 sweep
+C5 = 32768  # BASELINE config 5: 1/1 M = N = K = 32768, N sharded across the ranks
+NVLINK_GBS = 900.0  # NVLink 5 per direction per GPU (B200_PROFILING.md / SURVEY.md §8(e))
+
+
+class GpuC5Backend:
+    """Config-5 compute on the sm_100a library: device entry points, CUDA events."""
+
+    p2p = True
+
+    def __init__(self, torch, dev, lib):
+        self.torch, self.dev, self.lib = torch, dev, lib
+
+    def upload(self, words):
+        return self.torch.from_numpy(np.ascontiguousarray(words).view(np.int64)).to(self.dev)
+
+    def empty(self, rows, cols):
+        return self.torch.empty((rows, cols), dtype=self.torch.int32, device=self.dev)
+
+    def gemm(self, a, b, k, out):
+        from paper_2306_08960_b200 import device
+        device.gemm_1x1(a, b, k, units=out)
+
+    def gemm_ptr(self, a, b, k, ptr, ldc):
+        """Output at a raw device address with leading dimension ldc (a peer's matrix)."""
+        from paper_2306_08960_b200.api import _raise
+        stream = self.torch.cuda.current_stream().cuda_stream
+        _raise(self.lib.bitmm_gemm_1x1_dev(a.data_ptr(), a.shape[0], b.data_ptr(), b.shape[0], k,
+                                           a.shape[1], 1.0, 1.0, ptr, None, ldc, stream))
+
+    def time(self, fn, reps):
+        fn()  # warm (tensor maps, smem attributes)
+        self.torch.cuda.synchronize()
+        out = []
+        for _ in range(reps):
+            e0 = self.torch.cuda.Event(enable_timing=True)
+            e1 = self.torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            self.torch.cuda.synchronize()
+            out.append(e0.elapsed_time(e1))
+        return out
+
+    def reduce_max(self, dist, v):
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def status(self):
+        from paper_2306_08960_b200 import device
+        device.status()
+
+
+def c5_sweep(backend, dist, world, rank, m, n, k, reps=2, check_rows=4):
+    """1/1 M x K x N with the N dimension sharded over `world` ranks (rank g owns output
+    columns [lo_g, hi_g) = b_packed rows, kernels.hpp:44-46; A replicated). Every time is the
+    max over ranks. Returns (on every rank) the dict bench.py reports as `c5_sweep`:
+      kernel_ms         each rank's GEMM into its own block (no cross-GPU traffic)
+      p2p_gather_ms     each rank's GEMM writing its block into rank 0's M x N matrix
+                        (shard.PeerOutput: the gather fused into the epilogue, NVLink)
+      nccl_gather_ms    shard.run_sharded: row chunks computed and gathered to rank 0 with
+                        NCCL, overlapped, 1/1 units as uint16 popcounts, re-laid out there
+      single_gpu_ms     rank 0 alone, the whole problem (the N = 1 point, same run)
+    plus bytes to the root, link rates, speed-ups, and a check of sampled rows of both
+    gathered matrices against rank 0's own evaluation of those rows."""
+    import torch
+    from paper_2306_08960_b200 import data, shard
     rng = np.random.default_rng(SEED + 5)
-    m = n = k = 32768
-    a, _ = data.random_words(rng, m, k)
-    b, _ = data.random_words(rng, n, k)
-    da = torch.from_numpy(a.view(np.int64)).cuda()
-    db = torch.from_numpy(b.view(np.int64)).cuda()
-    u = torch.empty((m, n), dtype=torch.int32, device="cuda")
-    device.reserve_workspace(0, m, n, k)
-    device.gemm_1x1(da, db, k, units=u)
-    torch.cuda.synchronize()
-    times = []
-    for _ in range(2):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        device.gemm_1x1(da, db, k, units=u)
-        e1.record()
-        torch.cuda.synchronize()
-        times.append(e0.elapsed_time(e1))
-    device.status()
-    ms = min(times)
-    upd = m * n * k
-    del da, db, u
-    torch.cuda.empty_cache()
+    a, wpr = data.random_words(rng, m, k)
+    b, _ = data.random_words(rng, n, k)  # the same B on every rank; each uploads its rows
+    lo, hi = shard.column_range(n, rank, world)
+    da, db = backend.upload(a), backend.upload(b[lo:hi])
+    red = (lambda v: backend.reduce_max(dist, v)) if world > 1 else (lambda v: v)
+    res = {"workload": f"1/1 {m}x{k}x{n}, N sharded over {world} rank(s), int32 units",
+           "n_ranks": world, "columns_per_rank": hi - lo}
+    blk = backend.empty(m, hi - lo)
+    res["kernel_ms"] = red(min(backend.time(lambda: backend.gemm(da, db, k, blk), reps)))
+    if world > 1:
+        del blk
+    sample = np.sort(np.random.default_rng(SEED + 55).choice(m, check_rows, replace=False))
+    checks = {}
+    if world > 1:
+        width = shard.shard_width(n, world)
+        if getattr(backend, "p2p", False):
+            po = shard.PeerOutput(m, n, torch.int32, getattr(backend, "dev", torch.device("cpu")))
+            dist.barrier()
+            t = backend.time(lambda: backend.gemm_ptr(da, db, k, po.block_ptr(lo), n), reps)
+            dist.barrier()
+            res["p2p_gather_ms"] = red(min(t))
+            res["p2p_bytes_to_root"] = m * (n - (hi - lo)) * 4 if rank == 0 else None
+            if rank == 0:
+                checks["p2p"] = po.tensor[torch.from_numpy(sample).to(po.tensor.device)].cpu().numpy()
+            dist.barrier()
+            po.close()
+            del po
+
+        def compute(col_lo, col_hi, r0, r1, block):
+            backend.gemm(da[r0:r1], db, k, block)
+
+        got = [None]
+
+        def nccl():
+            got[0] = shard.run_sharded(m, n, torch.int32, compute, getattr(backend, "dev", torch.device("cpu")),
+                                       chunk_rows=max(1, m // 4), wire=shard.popcount_wire(k))
+
+        res["nccl_gather_ms"] = red(min(backend.time(nccl, reps)))
+        res["nccl_bytes_to_root"] = (world - 1) * m * width * 2
+        if rank == 0:
+            checks["nccl"] = got[0][torch.from_numpy(sample).to(got[0].device)].cpu().numpy()
+        got[0] = None
+    backend.status()
+    if rank == 0:
+        # the whole problem on one GPU (the sweep's N = 1 point) and the reference rows
+        dbf = backend.upload(b) if world > 1 else db
+        if world > 1:
+            full = backend.empty(m, n)
+            res["single_gpu_ms"] = min(backend.time(lambda: backend.gemm(da, dbf, k, full), reps))
+        else:
+            full = blk
+            res["single_gpu_ms"] = res["kernel_ms"]
+        want = full[torch.from_numpy(sample).to(full.device)].cpu().numpy()
+        rows = backend.empty(len(sample), n)
+        backend.gemm(da[torch.from_numpy(sample).to(da.device)], dbf, k, rows)
+        backend.status()
+        res["sampled_rows_checked"] = len(sample)
+        res["rows_match"] = {"single_gpu": bool(np.array_equal(rows.cpu().numpy(), want))}
+        for name, got_rows in checks.items():
+            res["rows_match"][name] = bool(np.array_equal(got_rows, want))
+        del full, rows, dbf
+        upd = m * n * k
+        for key in ("kernel_ms", "p2p_gather_ms", "nccl_gather_ms", "single_gpu_ms"):
+            if key in res:
+                res[key.replace("_ms", "_T_updates_per_s")] = upd / (res[key] * 1e-3) / 1e12
+                res[key.replace("_ms", "_speedup_vs_1gpu")] = res["single_gpu_ms"] / res[key]
+        if "p2p_gather_ms" in res and res["p2p_bytes_to_root"]:
+            res["p2p_root_ingress_GBps"] = res["p2p_bytes_to_root"] / (res["p2p_gather_ms"] * 1e-3) / 1e9
+        if "nccl_gather_ms" in res:
+            res["nccl_root_ingress_GBps"] = res["nccl_bytes_to_root"] / (res["nccl_gather_ms"] * 1e-3) / 1e9
+        res["nvlink_GBps_per_direction"] = NVLINK_GBS
+    return res
+
+
+def c5_single_line(sweep, peak):
+    ms = sweep["single_gpu_ms"]
+    upd = C5 ** 3
     return {"workload": "1/1 32768^3, int32 units, packed operands resident", "ms": ms,
             "T_updates_per_s": upd / (ms * 1e-3) / 1e12,
             "frac_of_tensor_peak": 2 * upd / (ms * 1e-3) / 1e12 / peak}

@@ -87,6 +87,18 @@ const char* bitmm_profile_kernel_name(int i);
 int bitmm_profile_kernel_launches(int i);
 double bitmm_profile_kernel_ms(int i);
 
+/* ---- Multi-GPU N-shard gather over NVLink ----
+ * CUDA IPC export / import of a device allocation, so every rank's GEMM epilogue stores its
+ * output column block straight into the root rank's M x N matrix (peer memory over NVLink):
+ * the gather IS the epilogue, overlapped with the MMAs tile by tile, and no collective runs
+ * after the compute. get_handle writes a 64-byte handle plus the byte offset of dev_ptr inside
+ * its allocation; open maps a peer's handle and returns the allocation's base (add the
+ * offset); close unmaps it. A GEMM output that lives on another device is written by the
+ * epilogue's st.global path (TMA stores stay for local outputs). */
+int bitmm_ipc_get_handle(const void* dev_ptr, void* handle, uint64_t* offset);
+int bitmm_ipc_open(const void* handle, void** dev_ptr);
+int bitmm_ipc_close(void* dev_ptr);
+
 /* ---- 1/1: replaces gemm_1x1 (kernels.hpp:47-48, kernels.cpp:163-183) ----
  * C[r][c] = (gamma_a * gamma_b) * float(K - 2*popcount(a_r xor b_c)).
  * Writes int32 units to c_units and/or scaled floats to c (either may be NULL). */

@@ -67,6 +67,9 @@ SIGNATURES = {
     "bitmm_profile_kernel_name": (C.c_char_p, [_i]),
     "bitmm_profile_kernel_launches": (_i, [_i]),
     "bitmm_profile_kernel_ms": (C.c_double, [_i]),
+    "bitmm_ipc_get_handle": (_i, [_p, _p, C.POINTER(C.c_uint64)]),
+    "bitmm_ipc_open": (_i, [_p, C.POINTER(_p)]),
+    "bitmm_ipc_close": (_i, [_p]),
     "bitmm_gemm_1x1_dev": (_i, [_p, _i64, _p, _i64, _i64, _i64, _f, _f, _p, _p, _i64, _p]),
     "bitmm_gemm_1x1_host": (_i, [_p, _i64, _p, _i64, _i64, _i64, _f, _f, _p, _p, _i64]),
     "bitmm_gemm_1x1_popc_dev": (_i, [_p, _i64, _p, _i64, _i64, _i64, _f, _f, _p, _p, _i64, _p]),

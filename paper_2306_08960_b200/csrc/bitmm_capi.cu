@@ -187,6 +187,35 @@ PFN_encodeTiled_t encode_fn() {
   return fn;
 }
 
+// cuMemGetAddressRange (base and size of the allocation holding a pointer; CUDA IPC handles
+// name whole allocations).
+typedef CUresult (*PFN_addrRange_t)(CUdeviceptr*, size_t*, CUdeviceptr);
+PFN_addrRange_t addr_range_fn() {
+  static PFN_addrRange_t fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_addrRange_t>(p);
+  });
+  return fn;
+}
+
+// True when `p` is device memory of another GPU (a peer allocation opened through CUDA IPC):
+// the GEMM epilogue then stores with st.global over NVLink instead of TMA.
+bool is_peer_memory(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return a.type == cudaMemoryTypeDevice && a.device != dev;
+}
+
 // cuStreamWriteValue32 (a 32-bit write that executes in stream order on the copy stream).
 typedef CUresult (*PFN_writeValue32_t)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 PFN_writeValue32_t write_value_fn() {
@@ -448,9 +477,9 @@ int run_tc_group(DeviceState& st, const GemmProblem* probs, int count, cudaStrea
     p.group_m = TC_GROUP_M;
     const bool i32 = p.epi == static_cast<int>(Epi::I32);
     void* out = i32 ? static_cast<void*>(p.out_i32) : static_cast<void*>(p.out_f32);
-    p.tma_store = make_output_map(&g.c[i], out, i32 ? CU_TENSOR_MAP_DATA_TYPE_INT32
-                                                    : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                                  p.N, p.M, p.ldc) ? 1 : 0;
+    p.tma_store = !is_peer_memory(out) && make_output_map(&g.c[i], out, i32 ? CU_TENSOR_MAP_DATA_TYPE_INT32
+                                                                            : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                                          p.N, p.M, p.ldc) ? 1 : 0;
     g.prob[i] = p;
     g.tile_begin[i] = tiles;
     tiles += p.num_tiles;
@@ -635,7 +664,8 @@ int run_fx_group(DeviceState& st, const FxProb* probs, int count, cudaStream_t s
     p.group_m = TC_GROUP_M;
     const bool i32 = p.epi == static_cast<int>(Epi::I32);
     void* out = i32 ? static_cast<void*>(p.out_i32) : static_cast<void*>(p.out_f32);
-    p.tma_store = make_output_map(&g.c[i], out, i32 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+    p.tma_store = !is_peer_memory(out) &&
+                  make_output_map(&g.c[i], out, i32 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                                   p.N, p.M, p.ldc) ? 1 : 0;
     g.prob[i] = p;
     g.a_code[i] = q.a_code;
@@ -1520,6 +1550,36 @@ int bitmm_profile_kernel_launches(int i) {
 
 double bitmm_profile_kernel_ms(int i) {
   return (i >= 0 && i < static_cast<int>(g_prof.ms.size())) ? g_prof.ms[i] : 0.0;
+}
+
+// ---------------- CUDA IPC (multi-GPU gather into the root's output) ----------------
+int bitmm_ipc_get_handle(const void* dev_ptr, void* handle, uint64_t* offset) {
+  if (!dev_ptr || !handle || !offset) return fail(BITMM_ERR_INVALID_ARGUMENT, "null argument");
+  PFN_addrRange_t range = addr_range_fn();
+  if (!range) return fail(BITMM_ERR_CUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return fail(BITMM_ERR_CUDA, "cuMemGetAddressRange failed (not a device allocation?)");
+  cudaIpcMemHandle_t h;
+  BITMM_CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+  memcpy(handle, &h, sizeof(h));
+  *offset = reinterpret_cast<uint64_t>(dev_ptr) - static_cast<uint64_t>(base);
+  return BITMM_OK;
+}
+
+int bitmm_ipc_open(const void* handle, void** dev_ptr) {
+  if (!handle || !dev_ptr) return fail(BITMM_ERR_INVALID_ARGUMENT, "null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  BITMM_CUDA_TRY(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return BITMM_OK;
+}
+
+int bitmm_ipc_close(void* dev_ptr) {
+  BITMM_CUDA_TRY(cudaIpcCloseMemHandle(dev_ptr));
+  return BITMM_OK;
 }
 
 int bitmm_device_sm_count(void) {

@@ -6,11 +6,18 @@ kernels.hpp:44-46), so no operand crosses ranks and there is no K reduction. The
 cross-GPU step is gathering the result blocks to the root — one collective
 (torch.distributed gather; NCCL over NVLink on B200, gloo in the CPU tests).
 
-`run_sharded` computes the rank's block in row chunks and gathers each chunk
-asynchronously while the next chunk computes, then (on the root) re-lays the blocks out
-into the reference's row-major M x N matrix. For 1/1 the units K - 2x carry K's parity,
-so the popcount x = (K - units)/2 in [0, K] travels as uint16 when K < 2^16 — lossless,
-half the link bytes — and is expanded back on the root.
+Two ways to bring the blocks to the root:
+
+* `PeerOutput` (GPUs in one box, the default): the root's M x N output is shared with every
+  rank through CUDA IPC (bitmm_ipc_get_handle / bitmm_ipc_open) and each rank's GEMM writes its
+  column block straight into it with ldc = N: the epilogue's stores cross NVLink tile by tile
+  while the next tiles multiply, so the gather is fused into the GEMM and no collective runs
+  after it. The root's matrix is complete after the ranks' kernels and one barrier.
+* `run_sharded` (any backend, NCCL or gloo): computes the rank's block in row chunks and
+  gathers each chunk asynchronously while the next chunk computes, then (on the root) re-lays
+  the blocks out into the reference's row-major M x N matrix. For 1/1 the units K - 2x carry
+  K's parity, so the popcount x = (K - units)/2 in [0, K] travels as uint16 when K < 2^16 —
+  lossless, half the link bytes — and is expanded back on the root.
 """
 from __future__ import annotations
 
@@ -117,3 +124,55 @@ def run_sharded(m: int, n: int, out_dtype: torch.dtype,
     while pending:
         finish(pending.pop(0))
     return out if rank == dst else None
+
+
+class PeerOutput:
+    """The root rank's row-major M x N output, mapped into every rank of the group.
+
+    The root allocates it; the others open its CUDA IPC handle. `block_ptr(col_lo)` is the
+    device address of column col_lo in row 0 (leading dimension N), what a rank passes to a
+    `bitmm_*_dev` call as its output so its column block lands in the root's matrix (SURVEY.md
+    §8(e): no operand exchange, the output gathered over NVLink). Call `close()` on every rank
+    when done; `tensor` is the matrix on the root, None elsewhere.
+    """
+
+    def __init__(self, m: int, n: int, dtype: torch.dtype, device: torch.device, group=None,
+                 root: int = 0):
+        import ctypes as C
+
+        from . import _lib
+        from .api import _raise
+        lib = _lib.load()
+        self._lib = lib
+        self.rank = dist.get_rank(group)
+        self.root = root
+        self.n = n
+        self.elem = torch.empty((), dtype=dtype).element_size()
+        self.tensor = None
+        self._opened = None
+        payload = [None]
+        if self.rank == root:
+            self.tensor = torch.empty((m, n), dtype=dtype, device=device)
+            handle = (C.c_uint8 * 64)()
+            off = C.c_uint64(0)
+            _raise(lib.bitmm_ipc_get_handle(C.c_void_p(self.tensor.data_ptr()), C.cast(handle, C.c_void_p),
+                                            C.byref(off)))
+            payload = [(bytes(handle), int(off.value))]
+            self.ptr = self.tensor.data_ptr()
+        dist.broadcast_object_list(payload, src=root, group=group)
+        if self.rank != root:
+            handle, off = payload[0]
+            base = C.c_void_p()
+            buf = (C.c_uint8 * 64).from_buffer_copy(handle)
+            _raise(lib.bitmm_ipc_open(C.cast(buf, C.c_void_p), C.byref(base)))
+            self._opened = base.value
+            self.ptr = base.value + off
+
+    def block_ptr(self, col_lo: int) -> int:
+        return self.ptr + col_lo * self.elem
+
+    def close(self) -> None:
+        if self._opened is not None:
+            from .api import _raise
+            _raise(self._lib.bitmm_ipc_close(self._opened))
+            self._opened = None
