@@ -9,6 +9,8 @@
 #include <chrono>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <memory>
 #include <mutex>
 #include <set>
 #include <tuple>
@@ -60,31 +62,59 @@ struct Arena {
   size_t bytes = 0;
 };
 
-struct DeviceState {
-  bool init = false;
+// ---------------- call contexts (re-entrancy) ----------------
+// The reference's entry points allocate per call and share nothing (kernels.cpp:163-275), so
+// callers drive them from many threads (run_row_blocks, kernels.cpp:50-68). Here:
+//  * device calls (`*_dev`) use the context of their CUDA stream (Ctx): workspace, latched
+//    status flag and scratch, grown stream-ordered (cudaMallocAsync / cudaFreeAsync), and a
+//    mutex held while the call enqueues its launches, so calls on one stream never interleave
+//    and calls on different streams never share memory;
+//  * host calls (`*_host`) lease a HostCtx for the whole call: private streams, staging,
+//    pinned buffers and events, so concurrent host calls from different threads run side by
+//    side. A lease ends with its streams drained, so no copy still reads the caller's buffers
+//    after the call returns, whatever the exit path.
+struct Ctx {
+  int dev = 0;
   int sms = 0;
-  int* status = nullptr;  // latched device-side encoding flags
-  Arena ws;               // intermediates (expanded operands)
-  Arena codes;            // 2-bit level codes of the in-GEMM expansion path (fx_gemm)
-  Arena io;               // host-flavour staging of inputs/outputs
-  cudaStream_t stream = nullptr;  // host-flavour private stream
-  unsigned ws_turn = 0;           // ping-pong half of the expanded-operand workspace
-  void* pinned[2] = {nullptr, nullptr};  // BTSR streaming chunks (allocated on first load)
-  cudaEvent_t pinned_ev[2] = {nullptr, nullptr};
-  cudaStream_t d2h = nullptr;             // host-flavour output copies (run_pipelined)
+  cudaStream_t stream = nullptr;
+  std::recursive_mutex mu;  // a host call holds it while its inner device calls take it again
+  int* status = nullptr;   // latched device-side flags of this stream's calls
+  int* scratch = nullptr;  // 64 bytes (plane validation)
+  Arena ws;                // expanded operands, APB intermediates, scan temp
+  Arena codes;             // 2-bit level codes of the in-GEMM expansion path (fx_gemm)
+  unsigned ws_turn = 0;    // ping-pong half of the expanded-operand workspace
+};
+
+struct HostCtx {
+  Ctx* sctx = nullptr;                    // the stream context of `stream`
+  cudaStream_t stream = nullptr;          // the call's GEMM stream
+  cudaStream_t d2h = nullptr;             // output copies (run_pipelined)
+  cudaStream_t h2d = nullptr;             // input copies (run_pipelined_wire)
+  Arena io;                               // device staging of inputs / outputs
   cudaEvent_t pipe_ev[8] = {};
-  cudaStream_t h2d = nullptr;             // host-flavour input copies (run_pipelined_wire)
   cudaEvent_t in_ev[9] = {};
-  uint32_t* in_flags = nullptr;           // per-slice "inputs landed" flags (wait_flag_kernel)
+  uint32_t* in_flags = nullptr;           // per-slice "inputs landed" flags
   uint32_t in_epoch = 0;
   void* host_stage = nullptr;             // pinned 16-bit output words (run_pipelined_wire)
   size_t host_stage_bytes = 0;
   std::vector<cudaEvent_t> wire_ev;       // one per copied part
+  void* pinned[2] = {nullptr, nullptr};   // BTSR streaming chunks (allocated on first load)
+  cudaEvent_t pinned_ev[2] = {nullptr, nullptr};
   // BITMM_WIRE_TRACE only: device timeline of the current host call
   std::vector<std::pair<std::string, cudaEvent_t>>* timeline = nullptr;
 };
 
-void trace_mark(DeviceState& st, const std::string& what, cudaStream_t on) {
+struct Dev {
+  std::mutex mu;
+  bool init = false;
+  int sms = 0;
+  std::map<unsigned long long, std::unique_ptr<Ctx>> streams;  // by cudaStreamGetId (never reused)
+  std::vector<std::unique_ptr<HostCtx>> hosts;
+  std::vector<HostCtx*> idle_hosts;
+};
+Dev g_dev[kMaxDevices];
+
+void trace_mark(HostCtx& st, const std::string& what, cudaStream_t on) {
   if (!st.timeline) return;
   cudaEvent_t e = nullptr;
   cudaEventCreate(&e);
@@ -97,10 +127,9 @@ void trace_mark(DeviceState& st, const std::string& what, cudaStream_t on) {
   st.timeline->emplace_back(what + "@" + std::to_string(us), e);
 }
 
-std::mutex g_mu;
-DeviceState g_state[kMaxDevices];
-
-int device_state(DeviceState** out) {
+// The current device's record (initialised once: SM count, a memory pool that keeps what
+// it has reserved, so stream-ordered workspace growth does not return memory to the OS).
+int current_dev(Dev** out, int* dev_out) {
   int dev = 0;
   int count = 0;
   if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
@@ -109,17 +138,114 @@ int device_state(DeviceState** out) {
   }
   BITMM_CUDA_TRY(cudaGetDevice(&dev));
   if (dev >= kMaxDevices) return fail(BITMM_ERR_CUDA, "device index out of range");
-  DeviceState& st = g_state[dev];
-  if (!st.init) {
-    BITMM_CUDA_TRY(cudaDeviceGetAttribute(&st.sms, cudaDevAttrMultiProcessorCount, dev));
-    BITMM_CUDA_TRY(cudaMalloc(&st.status, sizeof(int)));
-    BITMM_CUDA_TRY(cudaMemset(st.status, 0, sizeof(int)));
-    BITMM_CUDA_TRY(cudaStreamCreateWithFlags(&st.stream, cudaStreamNonBlocking));
-    st.init = true;
+  Dev& d = g_dev[dev];
+  std::lock_guard<std::mutex> lk(d.mu);
+  if (!d.init) {
+    BITMM_CUDA_TRY(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev));
+    cudaMemPool_t pool;
+    BITMM_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = UINT64_MAX;
+    BITMM_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    d.init = true;
   }
-  *out = &st;
+  *out = &d;
+  *dev_out = dev;
   return BITMM_OK;
 }
+
+// The context of stream `s` on the current device (created on first use).
+int stream_ctx(cudaStream_t s, Ctx** out) {
+  Dev* d = nullptr;
+  int dev = 0;
+  BITMM_TRY(current_dev(&d, &dev));
+  unsigned long long id = 0;
+  BITMM_CUDA_TRY(cudaStreamGetId(s, &id));
+  std::lock_guard<std::mutex> lk(d->mu);
+  auto it = d->streams.find(id);
+  if (it == d->streams.end()) {
+    auto c = std::make_unique<Ctx>();
+    c->dev = dev;
+    c->sms = d->sms;
+    c->stream = s;
+    BITMM_CUDA_TRY(cudaMalloc(&c->status, 128));
+    BITMM_CUDA_TRY(cudaMemset(c->status, 0, 128));
+    c->scratch = c->status + 16;
+    it = d->streams.emplace(id, std::move(c)).first;
+  }
+  *out = it->second.get();
+  return BITMM_OK;
+}
+
+// A device call's context: the stream's Ctx, locked for the call.
+class CallCtx {
+ public:
+  int acquire(cudaStream_t s) {
+    BITMM_TRY(stream_ctx(s, &c_));
+    lk_ = std::unique_lock<std::recursive_mutex>(c_->mu);
+    return BITMM_OK;
+  }
+  Ctx& operator*() { return *c_; }
+  Ctx* operator->() { return c_; }
+
+ private:
+  Ctx* c_ = nullptr;
+  std::unique_lock<std::recursive_mutex> lk_;
+};
+
+int host_ctx_init(HostCtx& h) {
+  BITMM_CUDA_TRY(cudaStreamCreateWithFlags(&h.stream, cudaStreamNonBlocking));
+  BITMM_CUDA_TRY(cudaStreamCreateWithFlags(&h.d2h, cudaStreamNonBlocking));
+  BITMM_CUDA_TRY(cudaStreamCreateWithFlags(&h.h2d, cudaStreamNonBlocking));
+  for (auto& e : h.pipe_ev) BITMM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : h.in_ev) BITMM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  BITMM_CUDA_TRY(cudaMalloc(&h.in_flags, 8 * sizeof(uint32_t)));
+  BITMM_CUDA_TRY(cudaMemset(h.in_flags, 0, 8 * sizeof(uint32_t)));
+  return stream_ctx(h.stream, &h.sctx);
+}
+
+// A host call's lease of a HostCtx (and its stream's Ctx). Released with every stream of the
+// context drained, on every exit path.
+class HostLease {
+ public:
+  int acquire() {
+    int dev = 0;
+    BITMM_TRY(current_dev(&d_, &dev));
+    {
+      std::lock_guard<std::mutex> lk(d_->mu);
+      if (!d_->idle_hosts.empty()) {
+        h_ = d_->idle_hosts.back();
+        d_->idle_hosts.pop_back();
+      }
+    }
+    if (!h_) {
+      auto h = std::make_unique<HostCtx>();
+      const int rc = host_ctx_init(*h);
+      if (rc != BITMM_OK) return rc;  // partially created resources leak (failure path only)
+      h_ = h.get();
+      std::lock_guard<std::mutex> lk(d_->mu);
+      d_->hosts.push_back(std::move(h));
+    }
+    lk_ = std::unique_lock<std::recursive_mutex>(h_->sctx->mu);
+    return BITMM_OK;
+  }
+  ~HostLease() {
+    if (!h_) return;
+    cudaStreamSynchronize(h_->h2d);
+    cudaStreamSynchronize(h_->stream);
+    cudaStreamSynchronize(h_->d2h);
+    if (lk_.owns_lock()) lk_.unlock();
+    std::lock_guard<std::mutex> lk(d_->mu);
+    d_->idle_hosts.push_back(h_);
+  }
+  HostCtx* operator->() { return h_; }
+  HostCtx& host() { return *h_; }
+  Ctx& ctx() { return *h_->sctx; }
+
+ private:
+  Dev* d_ = nullptr;
+  HostCtx* h_ = nullptr;
+  std::unique_lock<std::recursive_mutex> lk_;
+};
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel, device and size (the
 // attribute is per device; a process may drive several).
@@ -136,19 +262,24 @@ int ensure_max_smem(const void* fn, int bytes) {
   return BITMM_OK;
 }
 
-int arena_reserve(Arena& a, size_t bytes) {
+// Grows an arena in stream order on `s` (the only stream that uses it, or the stream whose
+// earlier work every other user waits for): the old buffer is freed behind the work already
+// queued there, so a call never synchronises the device or frees memory still in use.
+int arena_reserve(Arena& a, size_t bytes, cudaStream_t s) {
   if (bytes <= a.bytes) return BITMM_OK;
   if (a.ptr) {
-    BITMM_CUDA_TRY(cudaDeviceSynchronize());
-    BITMM_CUDA_TRY(cudaFree(a.ptr));
+    BITMM_CUDA_TRY(cudaFreeAsync(a.ptr, s));
     a.ptr = nullptr;
     a.bytes = 0;
   }
   size_t grown = std::max(bytes, static_cast<size_t>(1) << 20);
-  BITMM_CUDA_TRY(cudaMalloc(&a.ptr, grown));
+  BITMM_CUDA_TRY(cudaMallocAsync(&a.ptr, grown, s));
   a.bytes = grown;
   return BITMM_OK;
 }
+int arena_reserve(Arena& a, cudaStream_t s, size_t bytes) { return arena_reserve(a, bytes, s); }
+// Context-stream shorthand.
+int ws_reserve(Ctx& st, size_t bytes) { return arena_reserve(st.ws, bytes, st.stream); }
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
@@ -229,6 +360,42 @@ PFN_writeValue32_t write_value_fn() {
       fn = reinterpret_cast<PFN_writeValue32_t>(p);
   });
   return fn;
+}
+
+// cuStreamWaitValue32: the GEMM stream waits in its front end (no SM, no timeout) until the
+// copy stream's cuStreamWriteValue32 has landed.
+typedef CUresult (*PFN_waitValue32_t)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PFN_waitValue32_t wait_value_fn() {
+  static PFN_waitValue32_t fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_waitValue32_t>(p);
+  });
+  return fn;
+}
+
+// How a host call's slice GEMM waits for that slice's input copies (run_pipelined_wire):
+//   Value  : cuStreamWaitValue32 on the flag the copy stream writes (default)
+//   Kernel : a one-warp spin kernel on that flag (BITMM_WIRE_WAIT=kernel)
+//   Event  : cudaStreamWaitEvent on the copy stream (BITMM_WIRE_WAIT=event, or no driver
+//            entry points); it resolved only once the copy stream had drained
+enum class SliceWait { Value, Kernel, Event };
+SliceWait slice_wait_mode() {
+  const char* e = std::getenv("BITMM_WIRE_WAIT");  // read per call (tests switch it)
+  const std::string v = e ? e : "";
+  if (v == "event" || !write_value_fn()) return SliceWait::Event;
+  if (v == "kernel" || !wait_value_fn()) return SliceWait::Kernel;
+  return SliceWait::Value;
+}
+// Test hook: BITMM_WIRE_FAULT=flagwrite treats every flag write as failed, so each slice takes
+// the event fallback (the path a driver without stream memory operations takes).
+bool fault_flag_write() {
+  const char* e = std::getenv("BITMM_WIRE_FAULT");
+  return e && std::string(e) == "flagwrite";
 }
 
 // Waits in a one-warp kernel until *flag == value: the copy stream writes the flag after a
@@ -450,7 +617,7 @@ struct GemmProblem {
 
 // Launch one persistent cta_group::2 GEMM over a group of problems (tiles concatenated).
 template <Kind KIND, Epi EPI, int BN, int NP>
-int run_tc_group(DeviceState& st, const GemmProblem* probs, int count, cudaStream_t s) {
+int run_tc_group(Ctx& st, const GemmProblem* probs, int count, cudaStream_t s) {
   using S = TcShape<true, BN>;
   auto kern = tc_gemm_kernel<KIND, EPI, BN, NP>;
   BITMM_TRY(ensure_max_smem(reinterpret_cast<const void*>(kern), S::SMEM));
@@ -508,7 +675,7 @@ int run_tc_group(DeviceState& st, const GemmProblem* probs, int count, cudaStrea
 
 // Dispatch a group on the operand kind: one problem with a fixed epilogue, or up to
 // TC_GROUP_MAX problems with per-problem epilogues.
-int run_problems(DeviceState& st, const GemmProblem* probs, int count, bool fp4, cudaStream_t s) {
+int run_problems(Ctx& st, const GemmProblem* probs, int count, bool fp4, cudaStream_t s) {
   if (count == 1) {
     const int e = probs[0].p.epi;
     if (fp4) {
@@ -559,7 +726,7 @@ int make_problems(const uint8_t* A8, const uint8_t* B8, int64_t m, int64_t n, in
 }
 
 // Common integer-GEMM tail: A8 [m][kpad], B8 [n][kpad] already expanded.
-int run_int_gemm(DeviceState& st, const uint8_t* A8, const uint8_t* B8, int64_t m, int64_t n,
+int run_int_gemm(Ctx& st, const uint8_t* A8, const uint8_t* B8, int64_t m, int64_t n,
                  int64_t kpad, int shift, float scale, const float* row_scale,
                  const float* col_scale, int32_t* c_units, float* c, int64_t ldc, cudaStream_t s,
                  bool fp4 = false) {
@@ -639,7 +806,7 @@ int make_packed_map(CUtensorMap* map, const void* base, uint64_t row_bytes, uint
 }
 
 template <Epi EPI, int NP, int SLOT_ROW>
-int run_fx_group(DeviceState& st, const FxProb* probs, int count, cudaStream_t s) {
+int run_fx_group(Ctx& st, const FxProb* probs, int count, cudaStream_t s) {
   using S = FxShape<fx_exp<EPI>(), SLOT_ROW>;
   auto kern = fx_gemm_kernel<EPI, NP, fx_exp<EPI>(), SLOT_ROW>;
   BITMM_TRY(ensure_max_smem(reinterpret_cast<const void*>(kern), S::SMEM));
@@ -697,7 +864,7 @@ int run_fx_group(DeviceState& st, const FxProb* probs, int count, cudaStream_t s
 }
 
 template <int SLOT_ROW>
-int dispatch_fx(DeviceState& st, const FxProb* probs, int count, cudaStream_t s) {
+int dispatch_fx(Ctx& st, const FxProb* probs, int count, cudaStream_t s) {
   if (count == 1) {
     const int e = probs[0].p.epi;
     if (e == static_cast<int>(Epi::I32)) return run_fx_group<Epi::I32, 1, SLOT_ROW>(st, probs, 1, s);
@@ -713,14 +880,14 @@ int dispatch_fx(DeviceState& st, const FxProb* probs, int count, cudaStream_t s)
 
 // Prep pass (codes for level operands, padding checks for sign operands with bits past K),
 // then one fx_gemm launch over every problem of the items.
-int run_fx(DeviceState& st, const FxItem* items, int count, cudaStream_t s) {
+int run_fx(Ctx& st, const FxItem* items, int count, cudaStream_t s) {
   size_t code_bytes = 1024;
   for (int i = 0; i < count; ++i) {
     const int64_t kc = kcode_for(items[i].k);
     if (items[i].a.levels) code_bytes += align_up(items[i].a.rows * kc / 4, 1024);
     if (items[i].b.levels) code_bytes += align_up(items[i].b.rows * kc / 4, 1024);
   }
-  BITMM_TRY(arena_reserve(st.codes, code_bytes));
+  BITMM_TRY(arena_reserve(st.codes, code_bytes, st.stream));
   Carve cv(st.codes.ptr);
   PrepSet P{};
   P.err = st.status;
@@ -833,16 +1000,17 @@ int check_gemm_dims(int64_t m, int64_t n, int64_t k, int64_t wpr, int64_t ldc) {
   return BITMM_OK;
 }
 
-int read_status(DeviceState& st, cudaStream_t s) {
+int read_status(Ctx& st, cudaStream_t s) {
   BITMM_CUDA_TRY(cudaStreamSynchronize(s));
   int flag = 0;
   BITMM_CUDA_TRY(cudaMemcpy(&flag, st.status, sizeof(int), cudaMemcpyDeviceToHost));
   BITMM_CUDA_TRY(cudaMemset(st.status, 0, sizeof(int)));
+  // a timed-out input copy first: the inputs the GEMM read are then not the caller's
+  if (flag & ERR_COPY_TIMEOUT) return fail(BITMM_ERR_CUDA, "input copy did not complete (flag wait timed out)");
   if (flag & ERR_ENCODING) return fail(BITMM_ERR_INVALID_ENCODING, "invalid ternary plane encoding or nonzero plane padding");
   if (flag & ERR_PADDING) return fail(BITMM_ERR_INVALID_ARGUMENT, "bit matrix padding must be zero");
   if (flag & ERR_LEVEL) return fail(BITMM_ERR_INVALID_ARGUMENT, "2-bit level out of range");
   if (flag & ERR_ALPHA) return fail(BITMM_ERR_INVALID_ARGUMENT, "alpha must be positive");
-  if (flag & ERR_COPY_TIMEOUT) return fail(BITMM_ERR_CUDA, "input copy did not complete (flag wait timed out)");
   return BITMM_OK;
 }
 
@@ -862,12 +1030,8 @@ int64_t pipe_step(int64_t total, size_t out_bytes, int64_t align) {
 // body(c0, c1): enqueue slice [c0, c1)'s input copies and GEMM on s. out(c0, c1, d2h):
 // enqueue its output copies on d2h. Always drains d2h before returning.
 template <class Body, class Out>
-int run_pipelined(DeviceState& st, cudaStream_t s, int64_t total, int64_t step, Body&& body,
+int run_pipelined(HostCtx& st, cudaStream_t s, int64_t total, int64_t step, Body&& body,
                   Out&& out) {
-  if (!st.d2h) {
-    BITMM_CUDA_TRY(cudaStreamCreateWithFlags(&st.d2h, cudaStreamNonBlocking));
-    for (auto& e : st.pipe_ev) BITMM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  }
   int rc = BITMM_OK;
   int i = 0;
   for (int64_t c0 = 0; c0 < total; c0 += step, ++i) {
@@ -905,7 +1069,7 @@ struct OutBlock {
   int64_t row0, rows, col0, cols;
 };
 
-int host_stage_reserve(DeviceState& st, size_t bytes) {
+int host_stage_reserve(HostCtx& st, size_t bytes) {
   if (bytes <= st.host_stage_bytes) return BITMM_OK;
   if (st.host_stage) BITMM_CUDA_TRY(cudaFreeHost(st.host_stage));
   st.host_stage = nullptr;
@@ -923,27 +1087,20 @@ int host_stage_reserve(DeviceState& st, size_t bytes) {
 Wire host_wire(int routine, int64_t k, size_t out_bytes) {
   const char* e = std::getenv("BITMM_HOST_WIRE");
   if (e && std::atoi(e) == 32) return Wire::None;
-  if (out_bytes < kPipeMinOutBytes) return Wire::None;
+  const char* mb = std::getenv("BITMM_WIRE_MIN_BYTES");  // A/B of the threshold
+  if (out_bytes < (mb ? static_cast<size_t>(std::atoll(mb)) : kPipeMinOutBytes)) return Wire::None;
   return wire_for(routine, k);
 }
 
 template <class In, class Gemm, class Block>
-int run_pipelined_wire(DeviceState& st, cudaStream_t s, int64_t total, int64_t step, In&& in,
+int run_pipelined_wire(HostCtx& st, cudaStream_t s, int64_t total, int64_t step, In&& in,
                        Gemm&& gemm, Block&& block, const WireOut& wo, const int32_t* dcu,
                        uint16_t* dwire, size_t wire_words) {
-  if (!st.d2h) {
-    BITMM_CUDA_TRY(cudaStreamCreateWithFlags(&st.d2h, cudaStreamNonBlocking));
-    for (auto& e : st.pipe_ev) BITMM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  }
-  if (!st.h2d) {
-    BITMM_CUDA_TRY(cudaStreamCreateWithFlags(&st.h2d, cudaStreamNonBlocking));
-    for (auto& e : st.in_ev) BITMM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    BITMM_CUDA_TRY(cudaMalloc(&st.in_flags, kPipeChunks * sizeof(uint32_t)));
-    BITMM_CUDA_TRY(cudaMemset(st.in_flags, 0, kPipeChunks * sizeof(uint32_t)));
-  }
-  // flag waits need the driver's stream write; BITMM_WIRE_FLAGS=0 selects event waits
-  const char* fe = std::getenv("BITMM_WIRE_FLAGS");
-  const bool flags = write_value_fn() != nullptr && !(fe && std::atoi(fe) == 0);
+  // How each slice's GEMM waits for its input copies (see slice_wait_mode); a slice whose
+  // flag write fails falls back to an event.
+  const SliceWait mode = slice_wait_mode();
+  const bool flags = mode != SliceWait::Event;
+  bool slice_flag[kPipeChunks];
   const uint32_t epoch = ++st.in_epoch == 0 ? ++st.in_epoch : st.in_epoch;
   const auto t_call = std::chrono::steady_clock::now();
   static const bool trace = std::getenv("BITMM_WIRE_TRACE") != nullptr;
@@ -972,12 +1129,12 @@ int run_pipelined_wire(DeviceState& st, cudaStream_t s, int64_t total, int64_t s
     int j = 0;
     for (int64_t c0 = 0; c0 < total; c0 += step, ++j) {
       BITMM_TRY(in(c0, std::min(total, c0 + step), st.h2d));
-      if (flags) {
-        if (write_value_fn()(reinterpret_cast<CUstream>(st.h2d),
-                             reinterpret_cast<CUdeviceptr>(st.in_flags + (j % kPipeChunks)), epoch, 0) != CUDA_SUCCESS)
-          return fail(BITMM_ERR_CUDA, "cuStreamWriteValue32 failed");
-      } else {
-        BITMM_CUDA_TRY(cudaEventRecord(st.in_ev[j % kPipeChunks], st.h2d));
+      slice_flag[j] = flags && !fault_flag_write() && write_value_fn()(reinterpret_cast<CUstream>(st.h2d),
+                                                reinterpret_cast<CUdeviceptr>(st.in_flags + j), epoch,
+                                                0) == CUDA_SUCCESS;
+      if (!slice_flag[j]) {
+        cudaGetLastError();
+        BITMM_CUDA_TRY(cudaEventRecord(st.in_ev[j], st.h2d));
       }
       mark("i" + std::to_string(j), st.h2d);
     }
@@ -987,11 +1144,17 @@ int run_pipelined_wire(DeviceState& st, cudaStream_t s, int64_t total, int64_t s
   int i = 0;
   for (int64_t c0 = 0; c0 < total && rc == BITMM_OK; c0 += step, ++i) {
     const int64_t c1 = std::min(total, c0 + step);
-    if (flags) {
-      wait_flag_kernel<<<1, 32, 0, s>>>(st.in_flags + (i % kPipeChunks), epoch, st.status);
+    if (slice_flag[i] && mode == SliceWait::Kernel) {
+      wait_flag_kernel<<<1, 32, 0, s>>>(st.in_flags + i, epoch, st.sctx->status);
       rc = launch_check("wait_flag_kernel");
       if (rc != BITMM_OK) break;
-    } else if (cudaStreamWaitEvent(s, st.in_ev[i % kPipeChunks], 0) != cudaSuccess) {
+    } else if (slice_flag[i]) {
+      if (wait_value_fn()(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(st.in_flags + i), epoch,
+                          CU_STREAM_WAIT_VALUE_EQ) != CUDA_SUCCESS) {
+        rc = fail(BITMM_ERR_CUDA, "cuStreamWaitValue32 failed");
+        break;
+      }
+    } else if (cudaStreamWaitEvent(s, st.in_ev[i], 0) != cudaSuccess) {
       rc = fail(BITMM_ERR_CUDA, "pipeline input event");
       break;
     }
@@ -1002,7 +1165,7 @@ int run_pipelined_wire(DeviceState& st, cudaStream_t s, int64_t total, int64_t s
     // the narrowing runs on the GEMM's stream: on the copy stream it would wait for SMs
     // behind the next slice's persistent GEMM
     const int64_t cells = b.rows * b.cols;
-    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((cells / 4 + 255) / 256, int64_t{st.sms} * 8)));
+    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((cells / 4 + 255) / 256, int64_t{st.sctx->sms} * 8)));
     narrow_units_kernel<<<grid, 256, 0, s>>>(dcu + b.row0 * wo.ldc + b.col0, wo.ldc, dwire + off,
                                              b.rows, b.cols, static_cast<int>(wo.mode), wo.k);
     rc = launch_check("narrow_units_kernel");
@@ -1106,7 +1269,7 @@ size_t ws_half_int(int64_t m, int64_t n, int64_t k) {
 size_t ws_bytes_int(int64_t m, int64_t n, int64_t k) { return 2 * ws_half_int(m, n, k); }
 
 // Expanded operands A8 [m][kpad], B8 [n][kpad] in this call's half of the workspace.
-void take_int_operands(DeviceState& st, int64_t m, int64_t n, int64_t k, uint8_t** A8,
+void take_int_operands(Ctx& st, int64_t m, int64_t n, int64_t k, uint8_t** A8,
                        uint8_t** B8) {
   const int64_t kpad = round_up(k, TC_BK_BYTES);
   const size_t half = ws_half_int(m, n, k);
@@ -1123,7 +1286,7 @@ size_t ws_bytes_1x32(int64_t m, int64_t n, int64_t k) {
 }
 
 // ---------------- routine bodies on device pointers ----------------
-int gemm_1x1_dev_impl(DeviceState& st, const uint64_t* a, int64_t m, const uint64_t* b, int64_t n,
+int gemm_1x1_dev_impl(Ctx& st, const uint64_t* a, int64_t m, const uint64_t* b, int64_t n,
                       int64_t k, int64_t wpr, float gamma_a, float gamma_b, int32_t* c_units,
                       float* c, int64_t ldc, cudaStream_t s) {
   const bool fp4 = use_fp4();
@@ -1134,14 +1297,14 @@ int gemm_1x1_dev_impl(DeviceState& st, const uint64_t* a, int64_t m, const uint6
     return run_fx(st, &it, 1, s);
   }
   const int64_t kpad = kpad_for(k, fp4);
-  BITMM_TRY(arena_reserve(st.ws, ws_bytes_int(m, n, k)));
+  BITMM_TRY(ws_reserve(st, ws_bytes_int(m, n, k)));
   uint8_t *A8, *B8;
   take_int_operands(st, m, n, k, &A8, &B8);
   BITMM_TRY(run_unpack_pair(sa, sb, wpr, k, kpad, A8, B8, st.status, s, fp4));
   return run_int_gemm(st, A8, B8, m, n, kpad, 0, scale, nullptr, nullptr, c_units, c, ldc, s, fp4);
 }
 
-int gemm_1x2_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, float gamma, const uint64_t* t,
+int gemm_1x2_dev_impl(Ctx& st, const uint64_t* w, int64_t m, float gamma, const uint64_t* t,
                       const uint64_t* h, const uint64_t* mm, int64_t n, int64_t k, int64_t wpr,
                       float a_scale, int has_a_gamma, float a_gamma, const float* row_scale,
                       const float* col_scale, int32_t* c_units, float* c, int64_t ldc,
@@ -1156,7 +1319,7 @@ int gemm_1x2_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, float gamma
     return run_fx(st, &it, 1, s);
   }
   const int64_t kpad = kpad_for(k, fp4);
-  BITMM_TRY(arena_reserve(st.ws, ws_bytes_int(m, n, k)));
+  BITMM_TRY(ws_reserve(st, ws_bytes_int(m, n, k)));
   uint8_t *A8, *B8;
   take_int_operands(st, m, n, k, &A8, &B8);
   BITMM_TRY(run_unpack_pair(sa, sb, wpr, k, kpad, A8, B8, st.status, s, fp4));
@@ -1164,7 +1327,7 @@ int gemm_1x2_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, float gamma
                       c_units, c, ldc, s, fp4);
 }
 
-int gemm_2x2_dev_impl(DeviceState& st, const uint64_t* wt, const uint64_t* wh, const uint64_t* wm,
+int gemm_2x2_dev_impl(Ctx& st, const uint64_t* wt, const uint64_t* wh, const uint64_t* wm,
                       int64_t m, float w_scale, int has_w_gamma, float w_gamma, const uint64_t* at,
                       const uint64_t* ah, const uint64_t* am, int64_t n, int64_t k, int64_t wpr,
                       float a_scale, int has_a_gamma, float a_gamma, const float* row_scale,
@@ -1181,7 +1344,7 @@ int gemm_2x2_dev_impl(DeviceState& st, const uint64_t* wt, const uint64_t* wh, c
     return run_fx(st, &it, 1, s);
   }
   const int64_t kpad = kpad_for(k, fp4);
-  BITMM_TRY(arena_reserve(st.ws, ws_bytes_int(m, n, k)));
+  BITMM_TRY(ws_reserve(st, ws_bytes_int(m, n, k)));
   uint8_t *A8, *B8;
   take_int_operands(st, m, n, k, &A8, &B8);
   BITMM_TRY(run_unpack_pair(sa, sb, wpr, k, kpad, A8, B8, st.status, s, fp4));
@@ -1203,7 +1366,7 @@ bool spmm_chunk_fits(int64_t k, int64_t rows_per_split) {
 }
 
 // ~6 waves of blocks at 2 resident blocks per SM, rows split evenly
-void spmm_grid(const DeviceState& st, int64_t rows, int64_t n, int* chunks, int* splits,
+void spmm_grid(const Ctx& st, int64_t rows, int64_t n, int* chunks, int* splits,
                int* rows_per_split) {
   *chunks = static_cast<int>((n + SPMM_TOK - 1) / SPMM_TOK);
   const int target = 6 * st.sms;  // measured: 6 waves-worth beats 4..24 (restaging vs balance)
@@ -1212,7 +1375,7 @@ void spmm_grid(const DeviceState& st, int64_t rows, int64_t n, int* chunks, int*
   *rows_per_split = static_cast<int>((rows + *splits - 1) / *splits);
 }
 
-bool spmm_staged(const DeviceState& st, int64_t rows, int64_t k, int64_t n) {
+bool spmm_staged(const Ctx& st, int64_t rows, int64_t k, int64_t n) {
   int chunks, splits, rps;
   spmm_grid(st, rows, n, &chunks, &splits, &rps);
   return spmm_chunk_fits(k, rps);
@@ -1223,7 +1386,7 @@ bool spmm_staged(const DeviceState& st, int64_t rows, int64_t k, int64_t n) {
 // chains into the GEMM with PDL. When the staged chunk does not fit in shared memory, LEVELS
 // first dequantizes into `deq` [k][n] and both sources take the global-gather kernel.
 template <bool EXACT, bool PDL_CHAIN, bool LEVELS = false, bool ACCUM = LEVELS>
-int run_spmm(DeviceState& st, int64_t rows, int64_t k, const uint64_t* row_ptr,
+int run_spmm(Ctx& st, int64_t rows, int64_t k, const uint64_t* row_ptr,
              const uint64_t* col_idx, const float* vals, const float* b, int64_t n, int64_t ldb,
              float* c, int64_t ldc, cudaStream_t s, const SpmmLevels& lv = SpmmLevels{},
              float* deq = nullptr) {
@@ -1266,7 +1429,7 @@ int run_spmm(DeviceState& st, int64_t rows, int64_t k, const uint64_t* row_ptr,
   return launch_check("spmm_xchunk_kernel");
 }
 
-int apb_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, int64_t k, int64_t wpr, float gamma,
+int apb_dev_impl(Ctx& st, const uint64_t* w, int64_t m, int64_t k, int64_t wpr, float gamma,
                  const float* row_gamma, const float* b, int64_t n, int64_t ldb,
                  const uint64_t* row_ptr, const uint64_t* col_idx, const float* vals, float* c,
                  int64_t ldc, cudaStream_t s) {
@@ -1274,7 +1437,7 @@ int apb_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, int64_t k, int64
   // layer_forward: the residual is folded into the GEMM operand (apb_fold_kernel)
   const bool fold = row_ptr != nullptr;
   const int64_t lda = fold ? 2 * kpad : kpad;
-  BITMM_TRY(arena_reserve(st.ws, ws_bytes_1x32(m, n, k)));
+  BITMM_TRY(ws_reserve(st, ws_bytes_1x32(m, n, k)));
   Carve cv(st.ws.ptr);
   uint16_t* Ah = cv.take<uint16_t>(m * lda * 2);
   uint16_t* XT = cv.take<uint16_t>(n * APB_PARTS * kpad * 2);
@@ -1412,19 +1575,19 @@ int apb_dev_impl(DeviceState& st, const uint64_t* w, int64_t m, int64_t k, int64
 // The GEMM stores without reading C (its epilogue warps are few and latency-bound on loads);
 // the SpMM's many warps absorb the read-modify-write. Bit-identical to the reference
 // composition.
-size_t ws_bytes_apb2(const DeviceState& st, int64_t rows, int64_t cols, int64_t tokens) {
+size_t ws_bytes_apb2(const Ctx& st, int64_t rows, int64_t cols, int64_t tokens) {
   const size_t deq = spmm_staged(st, rows, cols, tokens) ? 0 : align_up(cols * tokens * 4, 1024);
   return ws_bytes_int(rows, tokens, cols) + deq;
 }
 
-int apb2_dev_impl(DeviceState& st, int64_t rows, int64_t cols, int64_t wpr, float alpha,
+int apb2_dev_impl(Ctx& st, int64_t rows, int64_t cols, int64_t wpr, float alpha,
                   const float* row_alpha, const uint64_t* bin, const uint64_t* row_ptr,
                   const uint64_t* col_idx, const float* vals, const uint64_t* t, const uint64_t* h,
                   const uint64_t* m, int64_t tokens, float a_scale, float a_gamma, float* c,
                   int64_t ldc, cudaStream_t s) {
   const bool fp4 = use_fp4();
   const int64_t kpad = kpad_for(cols, fp4);
-  BITMM_TRY(arena_reserve(st.ws, ws_bytes_apb2(st, rows, cols, tokens)));
+  BITMM_TRY(ws_reserve(st, ws_bytes_apb2(st, rows, cols, tokens)));
   float* deq = reinterpret_cast<float*>(static_cast<uint8_t*>(st.ws.ptr) + ws_bytes_int(rows, tokens, cols));
   const OperandSrc sa{bin, nullptr, nullptr, rows, false}, sb{t, h, m, tokens, true};
   const bool fx = fx_enabled() && fx_operand_ok(sa, wpr) && fx_operand_ok(sb, wpr);
@@ -1464,11 +1627,6 @@ int apb2_dev_impl(DeviceState& st, int64_t rows, int64_t cols, int64_t wpr, floa
   lv.d3 = 3.0f * sg;
   return run_spmm<true, true, true>(st, rows, cols, row_ptr, col_idx, vals, nullptr, tokens, tokens,
                                     c, ldc, s, lv, deq);
-}
-
-int with_device(DeviceState** st) {
-  std::lock_guard<std::mutex> lk(g_mu);
-  return device_state(st);
 }
 
 int check_csr_host(int64_t rows, int64_t cols, const uint64_t* row_ptr, const uint64_t* col_idx,
@@ -1583,21 +1741,22 @@ int bitmm_ipc_close(void* dev_ptr) {
 }
 
 int bitmm_device_sm_count(void) {
-  DeviceState* st = nullptr;
-  if (with_device(&st) != BITMM_OK) return 0;
-  return st->sms;
+  Dev* d = nullptr;
+  int dev = 0;
+  if (current_dev(&d, &dev) != BITMM_OK) return 0;
+  return d->sms;
 }
 
 int bitmm_device_status(void* stream) {
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
+  CallCtx st;
+  BITMM_TRY(st.acquire(static_cast<cudaStream_t>(stream)));
   return read_status(*st, static_cast<cudaStream_t>(stream));
 }
 
 int bitmm_reserve_workspace(size_t bytes) {
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
-  return arena_reserve(st->ws, bytes);
+  CallCtx st;  // the legacy default stream's workspace (where a caller without streams runs)
+  BITMM_TRY(st.acquire(nullptr));
+  return ws_reserve(*st, bytes);
 }
 
 size_t bitmm_workspace_bytes(int routine, int64_t m, int64_t n, int64_t k) {
@@ -1615,8 +1774,8 @@ int bitmm_gemm_1x1_dev(const uint64_t* a, int64_t m, const uint64_t* b_packed, i
   g_launches = 0;
   BITMM_TRY(check_gemm_dims(m, n, k, wpr, ldc));
   if (!a || !b_packed || (!c_units && !c)) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
+  CallCtx st;
+  BITMM_TRY(st.acquire(static_cast<cudaStream_t>(stream)));
   return gemm_1x1_dev_impl(*st, a, m, b_packed, n, k, wpr, gamma_a, gamma_b, c_units, c, ldc,
                            static_cast<cudaStream_t>(stream));
 }
@@ -1627,8 +1786,8 @@ int bitmm_gemm_1x1_popc_dev(const uint64_t* a, int64_t m, const uint64_t* b_pack
   g_launches = 0;
   BITMM_TRY(check_gemm_dims(m, n, k, wpr, ldc));
   if (!a || !b_packed || (!c_units && !c)) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
+  CallCtx st;
+  BITMM_TRY(st.acquire(static_cast<cudaStream_t>(stream)));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   dim3 grid(static_cast<unsigned>((n + PC_BN - 1) / PC_BN), static_cast<unsigned>((m + PC_BM - 1) / PC_BM));
   const float scale = gamma_a * gamma_b;
@@ -1655,16 +1814,17 @@ int bitmm_gemm_1x1_host(const uint64_t* a, int64_t m, const uint64_t* b_packed, 
   g_launches = 0;
   BITMM_TRY(check_gemm_dims(m, n, k, wpr, ldc));
   if (!a || !b_packed || (!c_units && !c)) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
-  cudaStream_t s = st->stream;
+  HostLease hl;
+  BITMM_TRY(hl.acquire());
+  Ctx* st = &hl.ctx();
+  cudaStream_t s = hl->stream;
   g_d2h_bytes = 0;
   const Wire wire = host_wire(0, k, static_cast<size_t>(m * ldc * 4));
   const size_t a_bytes = m * wpr * 8, b_bytes = n * wpr * 8, c_bytes = m * ldc * 4;
   const size_t w_bytes = wire != Wire::None ? static_cast<size_t>(m * n) * 2 : 0;
-  BITMM_TRY(arena_reserve(st->io, align_up(a_bytes, 1024) + align_up(b_bytes, 1024) +
+  BITMM_TRY(arena_reserve(hl->io, s, align_up(a_bytes, 1024) + align_up(b_bytes, 1024) +
                                       2 * align_up(c_bytes, 1024) + align_up(w_bytes, 1024)));
-  Carve cv(st->io.ptr);
+  Carve cv(hl->io.ptr);
   uint64_t* da = cv.take<uint64_t>(a_bytes);
   uint64_t* db = cv.take<uint64_t>(b_bytes);
   // 16-bit wire: the GEMM writes int32 units only; the host derives both outputs from them
@@ -1689,13 +1849,13 @@ int bitmm_gemm_1x1_host(const uint64_t* a, int64_t m, const uint64_t* b_packed, 
     const WireOut wo{wire, static_cast<int>(k), gamma_a * gamma_b /* kernels.cpp:170 */, nullptr,
                      nullptr, c_units, c, ldc};
     BITMM_TRY(run_pipelined_wire(
-        *st, s, m, pipe_step(m, c_bytes, 256), in, gemm,
+        hl.host(), s, m, pipe_step(m, c_bytes, 256), in, gemm,
         [&](int64_t r0, int64_t r1) { return OutBlock{r0, r1 - r0, 0, n}; }, wo, dcu,
         cv.take<uint16_t>(w_bytes), static_cast<size_t>(m * n)));
     return read_status(*st, s);
   }
   BITMM_TRY(run_pipelined(
-      *st, s, m, pipe_step(m, c_bytes, 256), body,
+      hl.host(), s, m, pipe_step(m, c_bytes, 256), body,
       [&](int64_t r0, int64_t r1, cudaStream_t d2h) -> int {
         const size_t bytes = (r1 - r0) * ldc * 4;
         if (dcu) BITMM_CUDA_TRY(cudaMemcpyAsync(c_units + r0 * ldc, dcu + r0 * ldc, bytes, cudaMemcpyDeviceToHost, d2h));
@@ -1716,8 +1876,8 @@ int bitmm_gemm_1x2_dev(const uint64_t* w, int64_t m, float gamma, const uint64_t
   if (!(a_scale > 0.0f)) return fail(BITMM_ERR_INVALID_ENCODING, "plane scale must be positive");
   BITMM_TRY(check_gemm_dims(m, n, k, wpr, ldc));
   if (!w || !t || !h || !mm || (!c_units && !c)) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
+  CallCtx st;
+  BITMM_TRY(st.acquire(static_cast<cudaStream_t>(stream)));
   return gemm_1x2_dev_impl(*st, w, m, gamma, t, h, mm, n, k, wpr, a_scale, has_a_gamma, a_gamma,
                            row_scale, col_scale, c_units, c, ldc, static_cast<cudaStream_t>(stream));
 }
@@ -1730,9 +1890,10 @@ int bitmm_gemm_1x2_host(const uint64_t* w, int64_t m, float gamma, const uint64_
   // ThmPlanes::validate runs first in the reference (kernels.cpp:186): scale, then legality.
   if (!(a_scale > 0.0f)) return fail(BITMM_ERR_INVALID_ENCODING, "plane scale must be positive");
   if (!t || !h || !mm || !w || (!c_units && !c)) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
-  cudaStream_t s = st->stream;
+  HostLease hl;
+  BITMM_TRY(hl.acquire());
+  Ctx* st = &hl.ctx();
+  cudaStream_t s = hl->stream;
   const int rc_dims = check_gemm_dims(m, n, k, wpr, ldc);
   const std::string dims_msg = g_err;
   const bool planes_ok_shape = n >= 0 && k >= 0 && wpr >= 0 && wpr * 64 >= k;
@@ -1741,10 +1902,10 @@ int bitmm_gemm_1x2_host(const uint64_t* w, int64_t m, float gamma, const uint64_
   g_d2h_bytes = 0;
   const Wire wire = host_wire(1, k, c_bytes);
   const size_t wire_bytes = (wire != Wire::None && rc_dims == BITMM_OK) ? static_cast<size_t>(m * n) * 2 : 0;
-  BITMM_TRY(arena_reserve(st->io, 3 * align_up(p_bytes, 1024) + align_up(w_bytes, 1024) +
+  BITMM_TRY(arena_reserve(hl->io, s, 3 * align_up(p_bytes, 1024) + align_up(w_bytes, 1024) +
                                       2 * align_up(c_bytes, 1024) + align_up(m > 0 ? m * 4 : 0, 1024) +
                                       align_up(n > 0 ? n * 4 : 0, 1024) + align_up(wire_bytes, 1024) + 4096));
-  Carve cv(st->io.ptr);
+  Carve cv(hl->io.ptr);
   uint64_t* dt = cv.take<uint64_t>(p_bytes);
   uint64_t* dh = cv.take<uint64_t>(p_bytes);
   uint64_t* dm = cv.take<uint64_t>(p_bytes);
@@ -1757,7 +1918,7 @@ int bitmm_gemm_1x2_host(const uint64_t* w, int64_t m, float gamma, const uint64_
     // plane legality still wins over shape errors (reference precedence)
     if (planes_ok_shape && n > 0 && k > 0) {
       const int64_t kpad = round_up(k, TC_BK_BYTES);
-      BITMM_TRY(arena_reserve(st->ws, align_up(n * kpad, 1024) + 1024));
+      BITMM_TRY(ws_reserve(*st, align_up(n * kpad, 1024) + 1024));
       BITMM_TRY(run_unpack_level_i8(dt, dh, dm, n, wpr, k, kpad, static_cast<uint8_t*>(st->ws.ptr), st->status, s));
       BITMM_TRY(read_status(*st, s));
     }
@@ -1796,13 +1957,13 @@ int bitmm_gemm_1x2_host(const uint64_t* w, int64_t m, float gamma, const uint64_
     const float scale = 0.5f * gamma * a_scale * (has_a_gamma ? a_gamma : 1.0f);
     const WireOut wo{wire, static_cast<int>(k), scale, row_scale, col_scale, c_units, c, ldc};
     BITMM_TRY(run_pipelined_wire(
-        *st, s, n, pipe_step(n, c_bytes, 256), in, gemm,
+        hl.host(), s, n, pipe_step(n, c_bytes, 256), in, gemm,
         [&](int64_t n0, int64_t n1) { return OutBlock{0, m, n0, n1 - n0}; }, wo, dcu,
         cv.take<uint16_t>(wire_bytes), static_cast<size_t>(m * n)));
     return read_status(*st, s);
   }
   BITMM_TRY(run_pipelined(
-      *st, s, n, pipe_step(n, c_bytes, 256), body,
+      hl.host(), s, n, pipe_step(n, c_bytes, 256), body,
       [&](int64_t n0, int64_t n1, cudaStream_t d2h) -> int {
         const size_t pitch = ldc * 4, width = (n1 - n0) * 4;
         if (dcu) BITMM_CUDA_TRY(cudaMemcpy2DAsync(c_units + n0, pitch, dcu + n0, pitch, width, m, cudaMemcpyDeviceToHost, d2h));
@@ -1826,8 +1987,8 @@ int bitmm_gemm_2x2_dev(const uint64_t* wt, const uint64_t* wh, const uint64_t* w
   BITMM_TRY(check_gemm_dims(m, n, k, wpr, ldc));
   if (!wt || !wh || !wm || !at || !ah || !am || (!c_units && !c))
     return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
+  CallCtx st;
+  BITMM_TRY(st.acquire(static_cast<cudaStream_t>(stream)));
   return gemm_2x2_dev_impl(*st, wt, wh, wm, m, w_scale, has_w_gamma, w_gamma, at, ah, am, n, k,
                            wpr, a_scale, has_a_gamma, a_gamma, row_scale, col_scale, c_units, c,
                            ldc, static_cast<cudaStream_t>(stream));
@@ -1844,9 +2005,10 @@ int bitmm_gemm_2x2_host(const uint64_t* wt, const uint64_t* wh, const uint64_t* 
     return fail(BITMM_ERR_INVALID_ENCODING, "plane scale must be positive");
   if (!wt || !wh || !wm || !at || !ah || !am || (!c_units && !c))
     return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
-  cudaStream_t s = st->stream;
+  HostLease hl;
+  BITMM_TRY(hl.acquire());
+  Ctx* st = &hl.ctx();
+  cudaStream_t s = hl->stream;
   const int rc_dims = check_gemm_dims(m, n, k, wpr, ldc);
   const std::string dims_msg = g_err;
   const bool shape_ok = k >= 0 && wpr >= 0 && wpr * 64 >= k;
@@ -1855,10 +2017,10 @@ int bitmm_gemm_2x2_host(const uint64_t* wt, const uint64_t* wh, const uint64_t* 
   g_d2h_bytes = 0;
   const Wire wire = host_wire(2, k, c_bytes);
   const size_t wire_bytes = (wire != Wire::None && rc_dims == BITMM_OK) ? static_cast<size_t>(m * n) * 2 : 0;
-  BITMM_TRY(arena_reserve(st->io, 3 * align_up(pw, 1024) + 3 * align_up(pa, 1024) +
+  BITMM_TRY(arena_reserve(hl->io, s, 3 * align_up(pw, 1024) + 3 * align_up(pa, 1024) +
                                       2 * align_up(c_bytes, 1024) + align_up(m > 0 ? m * 4 : 0, 1024) +
                                       align_up(n > 0 ? n * 4 : 0, 1024) + align_up(wire_bytes, 1024) + 4096));
-  Carve cv(st->io.ptr);
+  Carve cv(hl->io.ptr);
   uint64_t* d[6];
   const uint64_t* src[6] = {wt, wh, wm, at, ah, am};
   for (int i = 0; i < 6; ++i) {
@@ -1871,7 +2033,7 @@ int bitmm_gemm_2x2_host(const uint64_t* wt, const uint64_t* wh, const uint64_t* 
   if (rc_dims != BITMM_OK) {
     if (shape_ok && k > 0) {
       const int64_t kpad = round_up(k, TC_BK_BYTES);
-      BITMM_TRY(arena_reserve(st->ws, align_up(std::max<int64_t>(m, n) * kpad, 1024) + 1024));
+      BITMM_TRY(ws_reserve(*st, align_up(std::max<int64_t>(m, n) * kpad, 1024) + 1024));
       if (m > 0) BITMM_TRY(run_unpack_level_i8(d[0], d[1], d[2], m, wpr, k, kpad, static_cast<uint8_t*>(st->ws.ptr), st->status, s));
       if (n > 0) BITMM_TRY(run_unpack_level_i8(d[3], d[4], d[5], n, wpr, k, kpad, static_cast<uint8_t*>(st->ws.ptr), st->status, s));
       BITMM_TRY(read_status(*st, s));
@@ -1909,13 +2071,13 @@ int bitmm_gemm_2x2_host(const uint64_t* wt, const uint64_t* wh, const uint64_t* 
                         (has_a_gamma ? a_gamma : 1.0f);
     const WireOut wo{wire, static_cast<int>(k), scale, row_scale, col_scale, c_units, c, ldc};
     BITMM_TRY(run_pipelined_wire(
-        *st, s, m, pipe_step(m, c_bytes, 256), in, gemm,
+        hl.host(), s, m, pipe_step(m, c_bytes, 256), in, gemm,
         [&](int64_t r0, int64_t r1) { return OutBlock{r0, r1 - r0, 0, n}; }, wo, dcu,
         cv.take<uint16_t>(wire_bytes), static_cast<size_t>(m * n)));
     return read_status(*st, s);
   }
   BITMM_TRY(run_pipelined(
-      *st, s, m, pipe_step(m, c_bytes, 256), body,
+      hl.host(), s, m, pipe_step(m, c_bytes, 256), body,
       [&](int64_t r0, int64_t r1, cudaStream_t d2h) -> int {
         const size_t bytes = (r1 - r0) * ldc * 4;
         if (dcu) BITMM_CUDA_TRY(cudaMemcpyAsync(c_units + r0 * ldc, dcu + r0 * ldc, bytes, cudaMemcpyDeviceToHost, d2h));
@@ -1943,8 +2105,8 @@ int bitmm_gemm_1x32_dev(const uint64_t* w, int64_t m, int64_t k, int64_t wpr, fl
   g_launches = 0;
   BITMM_TRY(check_1x32_dims(m, k, wpr, n, ldb, ldc));
   if (!w || !b || !c) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
+  CallCtx st;
+  BITMM_TRY(st.acquire(static_cast<cudaStream_t>(stream)));
   return apb_dev_impl(*st, w, m, k, wpr, gamma, row_gamma, b, n, ldb, nullptr, nullptr, nullptr, c,
                       ldc, static_cast<cudaStream_t>(stream));
 }
@@ -1955,13 +2117,14 @@ int bitmm_gemm_1x32_host(const uint64_t* w, int64_t m, int64_t k, int64_t wpr, f
   g_launches = 0;
   BITMM_TRY(check_1x32_dims(m, k, wpr, n, ldb, ldc));
   if (!w || !b || !c) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
-  cudaStream_t s = st->stream;
+  HostLease hl;
+  BITMM_TRY(hl.acquire());
+  Ctx* st = &hl.ctx();
+  cudaStream_t s = hl->stream;
   const size_t w_bytes = m * wpr * 8, b_bytes = k * ldb * 4, c_bytes = m * ldc * 4;
-  BITMM_TRY(arena_reserve(st->io, align_up(w_bytes, 1024) + align_up(b_bytes, 1024) +
+  BITMM_TRY(arena_reserve(hl->io, s, align_up(w_bytes, 1024) + align_up(b_bytes, 1024) +
                                       align_up(c_bytes, 1024) + align_up(m * 4, 1024) + 4096));
-  Carve cv(st->io.ptr);
+  Carve cv(hl->io.ptr);
   uint64_t* dw = cv.take<uint64_t>(w_bytes);
   float* db = cv.take<float>(b_bytes);
   float* dc = cv.take<float>(c_bytes);
@@ -1981,8 +2144,8 @@ int bitmm_layer_forward_dev(int64_t rows, int64_t cols, float alpha, const float
   g_launches = 0;
   BITMM_TRY(check_1x32_dims(rows, cols, wpr, n, ldb, ldc));
   if (!bin || !b || !c || !row_ptr) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
+  CallCtx st;
+  BITMM_TRY(st.acquire(static_cast<cudaStream_t>(stream)));
   return apb_dev_impl(*st, bin, rows, cols, wpr, alpha, row_alpha, b, n, ldb, row_ptr, col_idx, vals,
                       c, ldc, static_cast<cudaStream_t>(stream));
 }
@@ -1996,17 +2159,18 @@ int bitmm_layer_forward_host(int64_t rows, int64_t cols, float alpha, const floa
   if (!bin || !b || !c || !row_ptr || (nnz > 0 && (!col_idx || !vals)))
     return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
   BITMM_TRY(check_csr_host(rows, cols, row_ptr, col_idx, vals, nnz));
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
-  cudaStream_t s = st->stream;
+  HostLease hl;
+  BITMM_TRY(hl.acquire());
+  Ctx* st = &hl.ctx();
+  cudaStream_t s = hl->stream;
   const size_t w_bytes = rows * wpr * 8, b_bytes = cols * ldb * 4, c_bytes = rows * ldc * 4;
   const size_t rp_bytes = (rows + 1) * 8, ci_bytes = std::max<int64_t>(nnz, 1) * 8,
                v_bytes = std::max<int64_t>(nnz, 1) * 4;
-  BITMM_TRY(arena_reserve(st->io, align_up(w_bytes, 1024) + align_up(b_bytes, 1024) +
+  BITMM_TRY(arena_reserve(hl->io, s, align_up(w_bytes, 1024) + align_up(b_bytes, 1024) +
                                       align_up(c_bytes, 1024) + align_up(rows * 4, 1024) +
                                       align_up(rp_bytes, 1024) + align_up(ci_bytes, 1024) +
                                       align_up(v_bytes, 1024) + 4096));
-  Carve cv(st->io.ptr);
+  Carve cv(hl->io.ptr);
   uint64_t* dw = cv.take<uint64_t>(w_bytes);
   float* db = cv.take<float>(b_bytes);
   float* dc = cv.take<float>(c_bytes);
@@ -2038,8 +2202,8 @@ int bitmm_spmm_csr_dev(int64_t rows, int64_t cols, const uint64_t* row_ptr, cons
     return fail(BITMM_ERR_INVALID_ARGUMENT, "shared dimension exceeds the 2^20 accumulator bound");
   if (ldb < n || ldc < n) return fail(BITMM_ERR_INVALID_ARGUMENT, "leading dimension smaller than the column count");
   if (!row_ptr || !b || !c) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
+  CallCtx st;
+  BITMM_TRY(st.acquire(static_cast<cudaStream_t>(stream)));
   return run_spmm<true, false>(*st, rows, cols, row_ptr, col_idx, vals, b, n, ldb, c, ldc,
                                static_cast<cudaStream_t>(stream));
 }
@@ -2054,15 +2218,16 @@ int bitmm_spmm_csr_host(int64_t rows, int64_t cols, const uint64_t* row_ptr,
   if (ldb < n || ldc < n) return fail(BITMM_ERR_INVALID_ARGUMENT, "leading dimension smaller than the column count");
   if (!row_ptr || !b || !c || (nnz > 0 && (!col_idx || !vals))) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
   BITMM_TRY(check_csr_host(rows, cols, row_ptr, col_idx, vals, nnz));
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
-  cudaStream_t s = st->stream;
+  HostLease hl;
+  BITMM_TRY(hl.acquire());
+  Ctx* st = &hl.ctx();
+  cudaStream_t s = hl->stream;
   const size_t b_bytes = cols * ldb * 4, c_bytes = rows * ldc * 4, rp_bytes = (rows + 1) * 8;
   const size_t ci_bytes = std::max<int64_t>(nnz, 1) * 8, v_bytes = std::max<int64_t>(nnz, 1) * 4;
-  BITMM_TRY(arena_reserve(st->io, align_up(b_bytes, 1024) + align_up(c_bytes, 1024) +
+  BITMM_TRY(arena_reserve(hl->io, s, align_up(b_bytes, 1024) + align_up(c_bytes, 1024) +
                                       align_up(rp_bytes, 1024) + align_up(ci_bytes, 1024) +
                                       align_up(v_bytes, 1024) + 4096));
-  Carve cv(st->io.ptr);
+  Carve cv(hl->io.ptr);
   float* db = cv.take<float>(b_bytes);
   float* dc = cv.take<float>(c_bytes);
   uint64_t* drp = cv.take<uint64_t>(rp_bytes);
@@ -2089,7 +2254,7 @@ static int check_pack_args(int64_t rows, int64_t cols, int64_t lda, int64_t wpr)
   return BITMM_OK;
 }
 
-static unsigned pack_blocks(const DeviceState& st, int64_t rows, int64_t wpr) {
+static unsigned pack_blocks(const Ctx& st, int64_t rows, int64_t wpr) {
   const long long units = rows * ((wpr + PACK_WORDS_PER_WARP - 1) / PACK_WORDS_PER_WARP);
   const long long blocks = (units + 7) / 8;  // 8 warps per 256-thread block
   return static_cast<unsigned>(std::max<long long>(1, std::min<long long>(blocks, 32LL * st.sms)));
@@ -2101,8 +2266,8 @@ int bitmm_pack_signs_dev(const float* a, int64_t rows, int64_t cols, int64_t lda
   BITMM_TRY(check_pack_args(rows, cols, lda, wpr));
   if (rows == 0 || wpr == 0) return BITMM_OK;
   if (!words || (cols > 0 && !a)) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
+  CallCtx st;
+  BITMM_TRY(st.acquire(static_cast<cudaStream_t>(stream)));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   ProfScope ps("pack_signs", s);
   pack_signs_kernel<<<pack_blocks(*st, rows, wpr), 256, 0, s>>>(
@@ -2118,8 +2283,8 @@ int bitmm_quantize_thm_dev(const float* a, int64_t rows, int64_t cols, int64_t l
   BITMM_TRY(check_pack_args(rows, cols, lda, wpr));
   if (rows == 0 || wpr == 0) return BITMM_OK;
   if (!t || !h || !m || (cols > 0 && !a)) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
+  CallCtx st;
+  BITMM_TRY(st.acquire(static_cast<cudaStream_t>(stream)));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   ProfScope ps("quantize_thm", s);
   quantize_thm_kernel<<<pack_blocks(*st, rows, wpr), 256, 0, s>>>(
@@ -2134,12 +2299,13 @@ int bitmm_pack_signs_host(const float* a, int64_t rows, int64_t cols, int64_t ld
   g_launches = 0;
   BITMM_TRY(check_pack_args(rows, cols, lda, wpr));
   if (rows == 0 || wpr == 0) return BITMM_OK;
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
-  cudaStream_t s = st->stream;
+  HostLease hl;
+  BITMM_TRY(hl.acquire());
+  Ctx* st = &hl.ctx();
+  cudaStream_t s = hl->stream;
   const size_t a_bytes = rows * lda * 4, w_bytes = rows * wpr * 8;
-  BITMM_TRY(arena_reserve(st->io, align_up(a_bytes, 1024) + align_up(w_bytes, 1024) + 2048));
-  Carve cv(st->io.ptr);
+  BITMM_TRY(arena_reserve(hl->io, s, align_up(a_bytes, 1024) + align_up(w_bytes, 1024) + 2048));
+  Carve cv(hl->io.ptr);
   float* da = cv.take<float>(a_bytes);
   uint64_t* dw = cv.take<uint64_t>(w_bytes);
   BITMM_CUDA_TRY(cudaMemcpyAsync(da, a, a_bytes, cudaMemcpyHostToDevice, s));
@@ -2155,12 +2321,13 @@ int bitmm_quantize_thm_host(const float* a, int64_t rows, int64_t cols, int64_t 
   if (!(s_step > 0.0f)) return fail(BITMM_ERR_INVALID_ARGUMENT, "quantization step must be positive");
   BITMM_TRY(check_pack_args(rows, cols, lda, wpr));
   if (rows == 0 || wpr == 0) return BITMM_OK;
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
-  cudaStream_t s = st->stream;
+  HostLease hl;
+  BITMM_TRY(hl.acquire());
+  Ctx* st = &hl.ctx();
+  cudaStream_t s = hl->stream;
   const size_t a_bytes = rows * lda * 4, w_bytes = rows * wpr * 8;
-  BITMM_TRY(arena_reserve(st->io, align_up(a_bytes, 1024) + 3 * align_up(w_bytes, 1024) + 4096));
-  Carve cv(st->io.ptr);
+  BITMM_TRY(arena_reserve(hl->io, s, align_up(a_bytes, 1024) + 3 * align_up(w_bytes, 1024) + 4096));
+  Carve cv(hl->io.ptr);
   float* da = cv.take<float>(a_bytes);
   uint64_t* dt = cv.take<uint64_t>(w_bytes);
   uint64_t* dh = cv.take<uint64_t>(w_bytes);
@@ -2180,8 +2347,8 @@ int bitmm_decompose_thm_dev(const uint8_t* levels, int64_t rows, int64_t cols, u
   BITMM_TRY(check_pack_args(rows, cols, cols, wpr));
   if (rows == 0 || wpr == 0) return BITMM_OK;
   if (!t || !h || !m || (cols > 0 && !levels)) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
+  CallCtx st;
+  BITMM_TRY(st.acquire(static_cast<cudaStream_t>(stream)));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   ProfScope ps("decompose_thm", s);
   decompose_thm_kernel<<<pack_blocks(*st, rows, wpr), 256, 0, s>>>(
@@ -2196,12 +2363,13 @@ int bitmm_decompose_thm_host(const uint8_t* levels, int64_t rows, int64_t cols, 
   g_launches = 0;
   BITMM_TRY(check_pack_args(rows, cols, cols, wpr));
   if (rows == 0 || wpr == 0) return BITMM_OK;
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
-  cudaStream_t s = st->stream;
+  HostLease hl;
+  BITMM_TRY(hl.acquire());
+  Ctx* st = &hl.ctx();
+  cudaStream_t s = hl->stream;
   const size_t l_bytes = rows * cols, w_bytes = rows * wpr * 8;
-  BITMM_TRY(arena_reserve(st->io, align_up(l_bytes, 1024) + 3 * align_up(w_bytes, 1024) + 4096));
-  Carve cv(st->io.ptr);
+  BITMM_TRY(arena_reserve(hl->io, s, align_up(l_bytes, 1024) + 3 * align_up(w_bytes, 1024) + 4096));
+  Carve cv(hl->io.ptr);
   uint8_t* dl = cv.take<uint8_t>(l_bytes);
   uint64_t* dt = cv.take<uint64_t>(w_bytes);
   uint64_t* dh = cv.take<uint64_t>(w_bytes);
@@ -2227,8 +2395,8 @@ int bitmm_decompose_apb_dev(const float* a, int64_t rows, int64_t cols, int64_t 
   BITMM_TRY(check_pack_args(rows, cols, lda, wpr));
   if (!nnz || !row_ptr || (rows > 0 && wpr > 0 && !bin) || (rows > 0 && cols > 0 && !a))
     return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
+  CallCtx st;
+  BITMM_TRY(st.acquire(static_cast<cudaStream_t>(stream)));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   auto* rp = reinterpret_cast<unsigned long long*>(row_ptr);
   BITMM_CUDA_TRY(cudaMemsetAsync(rp, 0, sizeof(unsigned long long), s));
@@ -2249,7 +2417,7 @@ int bitmm_decompose_apb_dev(const float* a, int64_t rows, int64_t cols, int64_t 
     }
     size_t temp = 0;
     BITMM_CUDA_TRY(cub::DeviceScan::InclusiveSum(nullptr, temp, rp + 1, rp + 1, static_cast<int>(rows), s));
-    BITMM_TRY(arena_reserve(st->ws, temp + 256));
+    BITMM_TRY(ws_reserve(*st, temp + 256));
     BITMM_CUDA_TRY(cub::DeviceScan::InclusiveSum(st->ws.ptr, temp, rp + 1, rp + 1, static_cast<int>(rows), s));
   }
   unsigned long long total = 0;
@@ -2277,17 +2445,18 @@ int bitmm_decompose_apb_host(const float* a, int64_t rows, int64_t cols, int64_t
   BITMM_TRY(check_pack_args(rows, cols, lda, wpr));
   if (!nnz || !row_ptr || (rows > 0 && wpr > 0 && !bin) || (rows > 0 && cols > 0 && !a))
     return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
-  cudaStream_t s = st->stream;
+  HostLease hl;
+  BITMM_TRY(hl.acquire());
+  Ctx* st = &hl.ctx();
+  cudaStream_t s = hl->stream;
   const bool fill = col_idx != nullptr && vals != nullptr && capacity > 0;
   const size_t a_bytes = rows * lda * 4, w_bytes = rows * wpr * 8, r_bytes = (rows + 1) * 8,
                al_bytes = row_alpha ? rows * 4 : 0, ci_bytes = fill ? capacity * 8 : 0,
                v_bytes = fill ? capacity * 4 : 0;
-  BITMM_TRY(arena_reserve(st->io, align_up(a_bytes, 1024) + align_up(w_bytes, 1024) +
+  BITMM_TRY(arena_reserve(hl->io, s, align_up(a_bytes, 1024) + align_up(w_bytes, 1024) +
                                       align_up(r_bytes, 1024) + align_up(al_bytes, 1024) +
                                       align_up(ci_bytes, 1024) + align_up(v_bytes, 1024) + 8192));
-  Carve cv(st->io.ptr);
+  Carve cv(hl->io.ptr);
   float* da = cv.take<float>(a_bytes);
   uint64_t* dw = cv.take<uint64_t>(w_bytes);
   uint64_t* dr = cv.take<uint64_t>(r_bytes);
@@ -2319,8 +2488,8 @@ int bitmm_layer_forward_2bit_dev(int64_t rows, int64_t cols, float alpha, const 
   if (!(a_scale > 0.0f)) return fail(BITMM_ERR_INVALID_ENCODING, "plane scale must be positive");
   BITMM_TRY(check_gemm_dims(rows, tokens, cols, wpr, ldc));
   if (!bin || !row_ptr || !t || !h || !m || !c) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
+  CallCtx st;
+  BITMM_TRY(st.acquire(static_cast<cudaStream_t>(stream)));
   return apb2_dev_impl(*st, rows, cols, wpr, alpha, row_alpha, bin, row_ptr, col_idx, vals, t, h, m,
                        tokens, a_scale, has_a_gamma ? a_gamma : 1.0f, c, ldc,
                        static_cast<cudaStream_t>(stream));
@@ -2338,17 +2507,18 @@ int bitmm_layer_forward_2bit_host(int64_t rows, int64_t cols, float alpha, const
   if (!bin || !row_ptr || !t || !h || !m || !c || (nnz > 0 && (!col_idx || !vals)))
     return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
   BITMM_TRY(check_csr_host(rows, cols, row_ptr, col_idx, vals, nnz));
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
-  cudaStream_t s = st->stream;
+  HostLease hl;
+  BITMM_TRY(hl.acquire());
+  Ctx* st = &hl.ctx();
+  cudaStream_t s = hl->stream;
   const size_t w_bytes = rows * wpr * 8, p_bytes = tokens * wpr * 8, c_bytes = rows * ldc * 4;
   const size_t rp_bytes = (rows + 1) * 8, ci_bytes = std::max<int64_t>(nnz, 1) * 8,
                v_bytes = std::max<int64_t>(nnz, 1) * 4;
-  BITMM_TRY(arena_reserve(st->io, align_up(w_bytes, 1024) + 3 * align_up(p_bytes, 1024) +
+  BITMM_TRY(arena_reserve(hl->io, s, align_up(w_bytes, 1024) + 3 * align_up(p_bytes, 1024) +
                                       align_up(c_bytes, 1024) + align_up(rows * 4, 1024) +
                                       align_up(rp_bytes, 1024) + align_up(ci_bytes, 1024) +
                                       align_up(v_bytes, 1024) + 4096));
-  Carve cv(st->io.ptr);
+  Carve cv(hl->io.ptr);
   uint64_t* dw = cv.take<uint64_t>(w_bytes);
   uint64_t* dt = cv.take<uint64_t>(p_bytes);
   uint64_t* dh = cv.take<uint64_t>(p_bytes);
@@ -2411,8 +2581,8 @@ int bitmm_gemm_batch_dev(const bitmm_gemm_item* items, int count, void* stream) 
     nprob += (it.c_units ? 1 : 0) + (it.c ? 1 : 0);
   }
   if (nprob > TC_GROUP_MAX) return fail(BITMM_ERR_INVALID_ARGUMENT, "batch exceeds 4 GEMM outputs");
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
+  CallCtx st;
+  BITMM_TRY(st.acquire(static_cast<cudaStream_t>(stream)));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool fp4 = use_fp4();
   {
@@ -2440,7 +2610,7 @@ int bitmm_gemm_batch_dev(const bitmm_gemm_item* items, int count, void* stream) 
     const int64_t rb = row_bytes(kpad_for(items[i].k, fp4), fp4);
     bytes += align_up(items[i].m * rb, 1024) + align_up(items[i].n * rb, 1024);
   }
-  BITMM_TRY(arena_reserve(st->ws, bytes));
+  BITMM_TRY(ws_reserve(*st, bytes));
   Carve cv(st->ws.ptr);
   UnpackSet U{};
   U.fp4 = fp4 ? 1 : 0;
@@ -2475,8 +2645,8 @@ static int run_row_ops(const uint64_t* a, const uint64_t* b, const uint64_t* z, 
   if (count < 0 || words < 0) return fail(BITMM_ERR_INVALID_ARGUMENT, "row counts must be non-negative");
   if (count == 0) return BITMM_OK;
   if (!out || (words > 0 && (!a || !b))) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
+  CallCtx st;
+  BITMM_TRY(st.acquire(static_cast<cudaStream_t>(stream)));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   ProfScope ps(z ? "mbm_rows" : "dot_binary_rows", s);
   row_ops_kernel<<<blocks_for(std::min<int64_t>(count, 64LL * st->sms) * 32, 256), 256, 0, s>>>(
@@ -2514,12 +2684,11 @@ int bitmm_validate_planes_dev(const uint64_t* t, const uint64_t* h, const uint64
     return fail(BITMM_ERR_INVALID_ARGUMENT, "words_per_row too small for the column count");
   if (rows == 0 || wpr == 0) return BITMM_OK;
   if (!t || !h || !m) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
+  CallCtx st;
+  BITMM_TRY(st.acquire(static_cast<cudaStream_t>(stream)));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  BITMM_TRY(arena_reserve(st->io, 64));
-  int* pad = static_cast<int*>(st->io.ptr);
-  unsigned long long* first = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(st->io.ptr) + 8);
+  int* pad = st->scratch;
+  unsigned long long* first = reinterpret_cast<unsigned long long*>(st->scratch + 2);
   BITMM_CUDA_TRY(cudaMemsetAsync(pad, 0, 4, s));
   BITMM_CUDA_TRY(cudaMemsetAsync(first, 0xFF, 8, s));
   {
@@ -2573,8 +2742,8 @@ int bitmm_btsr_load_dev(const char* path, int expected_kind, void* payload, uint
   if ((h.kind != 2 && h.payload_bytes > 0 && !payload) ||
       (h.kind == 2 && (!row_ptr || (h.nnz > 0 && (!col_idx || !vals)))))
     return fail(BITMM_ERR_INVALID_ARGUMENT, "null destination");
-  DeviceState* st = nullptr;
-  BITMM_TRY(with_device(&st));
+  HostLease st;  // pinned chunks of a host context; the copies run on the caller's stream
+  BITMM_TRY(st.acquire());
   for (int i = 0; i < 2; ++i) {
     if (!st->pinned[i]) {
       BITMM_CUDA_TRY(cudaHostAlloc(&st->pinned[i], kBtsrChunk, cudaHostAllocDefault));

@@ -6,7 +6,11 @@ path bit for bit, and an encoding error in the last slice must still be reported
 
 Where K allows, the output crosses PCIe as one 16-bit word per cell (csrc/wire.cuh): the
 device narrows the int32 units, the host widens them and applies the epilogue's fp32 scale
-sequence. Every test here runs with that wire and with BITMM_HOST_WIRE=32 (4-byte copies)."""
+sequence. Every test here runs with that wire and with BITMM_HOST_WIRE=32 (4-byte copies).
+Each slice's GEMM waits for that slice's input copies with cuStreamWaitValue32 on a flag the
+copy stream writes (default), a one-warp spin kernel on it (BITMM_WIRE_WAIT=kernel), or an
+event (BITMM_WIRE_WAIT=event; also the fallback of a slice whose flag write fails,
+BITMM_WIRE_FAULT=flagwrite): all four must give the same bits."""
 import ctypes as C
 
 import numpy as np
@@ -18,16 +22,24 @@ from paper_2306_08960_b200 import _lib, api, data, device
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["wire16", "wire16-sse2", "wire32"])
+@pytest.fixture(autouse=True, params=["wire16", "wire16-sse2", "wire32", "wire16-kernelwait",
+                                      "wire16-eventwait", "wire16-flagfault"])
 def wire(request, monkeypatch):
     """wire16: 16-bit words widened with the host's widest streaming stores (AVX-512 where
-    present); wire16-sse2: the x86-64 baseline path; wire32: 4-byte copies."""
-    monkeypatch.delenv("BITMM_HOST_WIRE", raising=False)
-    monkeypatch.delenv("BITMM_HOST_SIMD", raising=False)
+    present); wire16-sse2: the x86-64 baseline path; wire32: 4-byte copies; *wait / flagfault:
+    the other ways a slice waits for its inputs (module docstring)."""
+    for v in ("BITMM_HOST_WIRE", "BITMM_HOST_SIMD", "BITMM_WIRE_WAIT", "BITMM_WIRE_FAULT"):
+        monkeypatch.delenv(v, raising=False)
     if request.param == "wire32":
         monkeypatch.setenv("BITMM_HOST_WIRE", "32")
     elif request.param == "wire16-sse2":
         monkeypatch.setenv("BITMM_HOST_SIMD", "sse2")
+    elif request.param == "wire16-kernelwait":
+        monkeypatch.setenv("BITMM_WIRE_WAIT", "kernel")
+    elif request.param == "wire16-eventwait":
+        monkeypatch.setenv("BITMM_WIRE_WAIT", "event")
+    elif request.param == "wire16-flagfault":
+        monkeypatch.setenv("BITMM_WIRE_FAULT", "flagwrite")
     return request.param.split("-")[0]
 
 
