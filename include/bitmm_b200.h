@@ -214,6 +214,13 @@ int bitmm_dot_binary_dev(const uint64_t* u, const uint64_t* v, int64_t count, in
                          int64_t n, int64_t* out, void* stream);
 int bitmm_mbm_dev(const uint64_t* x, const uint64_t* y, const uint64_t* z, int64_t count,
                   int64_t words, int64_t* out, void* stream);
+/* Host flavour of the same (host rows in, host results out, synchronous): what a drop-in
+ * dot_binary / mbm binding calls with count = 1 (integration/reference_dropin, built with
+ * BITMM_DROPIN_ROWOPS_GPU). */
+int bitmm_dot_binary_host(const uint64_t* u, const uint64_t* v, int64_t count, int64_t words,
+                          int64_t n, int64_t* out);
+int bitmm_mbm_host(const uint64_t* x, const uint64_t* y, const uint64_t* z, int64_t count,
+                   int64_t words, int64_t* out);
 
 /* ---- ThmPlanes::validate on device (tensor.cpp:133-153) ----
  * Checks scale > 0, zero padding and legal {t,h,m} states of plane words already on the

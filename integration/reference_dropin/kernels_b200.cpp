@@ -13,6 +13,7 @@
 // Build recipe (see INTEGRATION.md and oracle/Makefile target `dropin`): compile the
 // reference sources unmodified, weaken the nine replaced symbols in their objects
 // (objcopy --weaken-symbol), link this file plus libbitmm_b200.so.
+#include <span>
 #include <stdexcept>
 #include <string>
 
@@ -97,6 +98,33 @@ ApbLayer decompose_apb(const DenseMatrix& a, float alpha, int lane_bits) {
                                  std::move(vals));
   return l;
 }
+
+#ifdef BITMM_DROPIN_ROWOPS_GPU
+// ---- row ops (kernels.cpp:120-140) on the GPU, one row pair per call. Not in the default
+// drop-in: a call costs a launch plus two tiny copies (tens of microseconds) where the
+// reference's AVX-512 loop takes nanoseconds, and verify.cpp / acceptance.cpp call them
+// millions of times; the batched device calls are the GPU's form. ----
+std::int64_t dot_binary(std::span<const std::uint64_t> u, std::span<const std::uint64_t> v,
+                        std::int64_t n) {
+  if (u.size() != v.size()) throw std::invalid_argument("bit row word counts differ");
+  if (n < 0 || static_cast<std::size_t>((n + 63) / 64) > u.size())
+    throw std::invalid_argument("logical length does not fit the row words");
+  if (u.empty()) return 0;
+  std::int64_t out = 0;
+  raise_on(bitmm_dot_binary_host(u.data(), v.data(), 1, static_cast<std::int64_t>(u.size()), n, &out));
+  return out;
+}
+
+std::int64_t mbm(std::span<const std::uint64_t> x, std::span<const std::uint64_t> y,
+                 std::span<const std::uint64_t> z) {
+  if (x.size() != y.size() || x.size() != z.size())
+    throw std::invalid_argument("bit row word counts differ");
+  if (x.empty()) return 0;
+  std::int64_t out = 0;
+  raise_on(bitmm_mbm_host(x.data(), y.data(), z.data(), 1, static_cast<std::int64_t>(x.size()), &out));
+  return out;
+}
+#endif
 
 DenseMatrix gemm_1x1(const BitMatrix& a, const BitMatrix& b_packed, float gamma_a, float gamma_b,
                      int threads) {

@@ -115,6 +115,8 @@ SIGNATURES = {
     "bitmm_btsr_read_header": (_i, [C.c_char_p, _p]),
     "bitmm_dot_binary_dev": (_i, [_p, _p, _i64, _i64, _i64, _p, _p]),
     "bitmm_mbm_dev": (_i, [_p, _p, _p, _i64, _i64, _p, _p]),
+    "bitmm_dot_binary_host": (_i, [_p, _p, _i64, _i64, _i64, _p]),
+    "bitmm_mbm_host": (_i, [_p, _p, _p, _i64, _i64, _p]),
     "bitmm_validate_planes_dev": (_i, [_p, _p, _p, _i64, _i64, _i64, _f, _p]),
     "bitmm_btsr_load_dev": (_i, [C.c_char_p, _i, _p, _p, _p, _p, _p]),
     "bitmm_pack_signs_dev": (_i, [_p, _i64, _i64, _i64, _p, _i64, _p]),

@@ -2675,6 +2675,52 @@ int bitmm_mbm_dev(const uint64_t* x, const uint64_t* y, const uint64_t* z, int64
   return run_row_ops(x, y, z, count, words, 0, out, stream);
 }
 
+static int row_ops_host(const uint64_t* a, const uint64_t* b, const uint64_t* z, int64_t count,
+                        int64_t words, int64_t n, int64_t* out) {
+  if (count < 0 || words < 0) return fail(BITMM_ERR_INVALID_ARGUMENT, "row counts must be non-negative");
+  if (count == 0) return BITMM_OK;
+  if (!out || (words > 0 && (!a || !b || (z == nullptr && n < 0)))) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  HostLease hl;
+  BITMM_TRY(hl.acquire());
+  cudaStream_t s = hl->stream;
+  const size_t rows_bytes = static_cast<size_t>(count * words) * 8, out_bytes = static_cast<size_t>(count) * 8;
+  BITMM_TRY(arena_reserve(hl->io, s, 3 * align_up(rows_bytes, 1024) + align_up(out_bytes, 1024) + 1024));
+  Carve cv(hl->io.ptr);
+  uint64_t* da = cv.take<uint64_t>(rows_bytes);
+  uint64_t* db = cv.take<uint64_t>(rows_bytes);
+  uint64_t* dz = z ? cv.take<uint64_t>(rows_bytes) : nullptr;
+  int64_t* dout = cv.take<int64_t>(out_bytes);
+  if (rows_bytes) {
+    BITMM_CUDA_TRY(cudaMemcpyAsync(da, a, rows_bytes, cudaMemcpyHostToDevice, s));
+    BITMM_CUDA_TRY(cudaMemcpyAsync(db, b, rows_bytes, cudaMemcpyHostToDevice, s));
+    if (dz) BITMM_CUDA_TRY(cudaMemcpyAsync(dz, z, rows_bytes, cudaMemcpyHostToDevice, s));
+  }
+  if (z) BITMM_TRY(bitmm_mbm_dev(da, db, dz, count, words, dout, s));
+  else BITMM_TRY(bitmm_dot_binary_dev(da, db, count, words, n, dout, s));
+  BITMM_CUDA_TRY(cudaMemcpyAsync(out, dout, out_bytes, cudaMemcpyDeviceToHost, s));
+  BITMM_CUDA_TRY(cudaStreamSynchronize(s));
+  return BITMM_OK;
+}
+
+int bitmm_dot_binary_host(const uint64_t* u, const uint64_t* v, int64_t count, int64_t words, int64_t n,
+                          int64_t* out) {
+  g_launches = 0;
+  if (n < 0 || (n + 63) / 64 > words)  // kernels.cpp:121-123
+    return fail(BITMM_ERR_INVALID_ARGUMENT, "logical length does not fit the row words");
+  return row_ops_host(u, v, nullptr, count, words, n, out);
+}
+
+int bitmm_mbm_host(const uint64_t* x, const uint64_t* y, const uint64_t* z, int64_t count, int64_t words,
+                   int64_t* out) {
+  g_launches = 0;
+  if (words > 0 && !z) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  if (words == 0) {  // mbm of empty rows is 0 (kernels.cpp:134)
+    for (int64_t i = 0; i < count; ++i) out[i] = 0;
+    return BITMM_OK;
+  }
+  return row_ops_host(x, y, z, count, words, 0, out);
+}
+
 // ---------------- plane validation ----------------
 int bitmm_validate_planes_dev(const uint64_t* t, const uint64_t* h, const uint64_t* m,
                               int64_t rows, int64_t cols, int64_t wpr, float scale, void* stream) {

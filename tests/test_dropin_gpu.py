@@ -28,3 +28,43 @@ def test_reference_acceptance_suite_with_b200_kernels():
     for crit in ("1", "2", "3", "4", "5", "6", "7"):
         assert verdicts.get(crit) == "PASS", f"criterion {crit}: {out}"
     assert "220 shapes" in out and " 0 mismatches" in out
+
+
+VERIFY_B200 = os.path.join(REPO, "oracle", "_ref", "verify_b200")
+VERIFY_ROWOPS = os.path.join(REPO, "oracle", "_ref", "verify_b200_rowops")
+VERIFY_REF = os.path.join(REPO, "oracle", "_ref", "verify_ref")
+
+
+@pytest.mark.skipif(not os.path.exists(VERIFY_B200), reason="verify_b200 not built (needs /root/reference)")
+def test_reference_verification_sweep_on_b200():
+    """bitmm::run_verification (verify.cpp:352-376, unmodified) with the GEMMs and packers on
+    the B200: every suite passes, and the report is identical to the one the reference's own
+    CPU library prints for the same options (the sweep is deterministic per seed)."""
+    got = subprocess.run([VERIFY_B200], capture_output=True, text=True, timeout=900)
+    assert got.returncode == 0, got.stdout + got.stderr
+    assert "all suites passed" in got.stdout and "suite gemm-bitwise-vs-oracle" in got.stdout
+    want = subprocess.run([VERIFY_REF], capture_output=True, text=True, timeout=900)
+    assert want.returncode == 0
+    assert got.stdout == want.stdout
+
+
+@pytest.mark.skipif(not os.path.exists(VERIFY_B200), reason="verify_b200 not built (needs /root/reference)")
+def test_reference_verification_fault_injection_on_b200():
+    """--inject-fault adds 1.0 to C[0][0] of the first 1/1 case (verify.cpp:257): the sweep must
+    fail and name it, as the reference CLI test expects (test_bench_cli.cpp:205-210)."""
+    r = subprocess.run([VERIFY_B200, "--gemm-cases", "2", "--max-dim", "12", "--inject-fault"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 1
+    for s in ("verification FAILED", "first failure", "routine=1x1", "cell=(0,0)"):
+        assert s in r.stdout, r.stdout
+
+
+@pytest.mark.skipif(not os.path.exists(VERIFY_ROWOPS), reason="verify_b200_rowops not built")
+def test_reference_verification_with_row_ops_on_b200():
+    """The same sweep with dot_binary / mbm (kernels.cpp:120-140) also routed to the GPU, one
+    row pair per call (reduced exhaustive lengths: each call is a launch)."""
+    args = ["--dot-n", "6", "--mbm-n", "4", "--rowop-cases", "300", "--gemm-cases", "6", "--max-dim", "40"]
+    got = subprocess.run([VERIFY_ROWOPS] + args, capture_output=True, text=True, timeout=900)
+    assert got.returncode == 0, got.stdout + got.stderr
+    want = subprocess.run([VERIFY_REF] + args, capture_output=True, text=True, timeout=900)
+    assert got.stdout == want.stdout
