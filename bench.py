@@ -176,6 +176,61 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
 
 
+def measured_fp4_peak():
+    """The sustained / burst kind::mxf4 issue rate measured on this pool's B200
+    (profiles/micro/mxf4_sustained.cu -> profiles/mxf4_peak_r02.json)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "mxf4_peak_r02.json")) as f:
+            d = json.load(f)["mxf4_peak"]
+        return {"mxf4_sustained_tflops": d["sustained_tflops"], "mxf4_burst_tflops": d["burst_tflops"],
+                "sustained_clock_mhz": d["sustained_clock_mhz"],
+                "source": "profiles/mxf4_peak_r02.json (profiles/micro/mxf4_sustained.cu: back-to-back "
+                          "cta_group::2 kind::mxf4 MMAs on every SM pair, random +-1 operands, ~2 s "
+                          "under the power limit)"}
+    except (OSError, ValueError, KeyError):
+        return None
+
+
+def library_fp4_gemm(torch, shapes=((4096, 4096, 4096), (4096, 8192, 4096))):
+    """A library block-scaled FP4 GEMM beside tc_gemm in the same run: cuBLASLt through
+    torch.nn.functional.scaled_mm, e2m1 x e2m1 with unit E8M0 block-32 scales, bf16 output
+    (2 B per cell against our 4 B), median of 10 L2-flushed launches. None if unsupported."""
+    try:
+        import torch.nn.functional as F
+
+        def blocked(rows, cols):
+            rb, cb = (rows + 127) // 128, (cols + 3) // 4
+            s = torch.full((rb * 128, cb * 4), 127, dtype=torch.uint8, device="cuda")
+            s = s.view(rb, 128, cb, 4).permute(0, 2, 1, 3).reshape(-1, 4, 32, 4).transpose(1, 2)
+            return s.reshape(-1).contiguous().view(torch.float8_e8m0fnu)
+
+        out = {}
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        for m, n, k in shapes:
+            a = torch.randint(0, 256, (m, k // 2), dtype=torch.uint8, device="cuda").view(torch.float4_e2m1fn_x2)
+            b = torch.randint(0, 256, (n, k // 2), dtype=torch.uint8, device="cuda").view(torch.float4_e2m1fn_x2)
+            sa, sb = blocked(m, k // 32), blocked(n, k // 32)
+            f = lambda: F.scaled_mm(a, b.t(), sa, F.ScalingType.BlockWise1x32, sb,  # noqa: E731
+                                    F.ScalingType.BlockWise1x32, swizzle_a=F.SwizzleType.SWIZZLE_32_4_4,
+                                    swizzle_b=F.SwizzleType.SWIZZLE_32_4_4, output_dtype=torch.bfloat16)
+            f()
+            ts = []
+            for _ in range(10):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                f()
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            ms = sorted(ts)[len(ts) // 2]
+            out[f"{m}x{n}x{k}"] = {"ms": ms, "tflops": 2 * m * n * k / (ms * 1e-3) / 1e12}
+        return {"library": "cuBLASLt via torch.nn.functional.scaled_mm (BlockWise1x32 E8M0, "
+                           "SWIZZLE_32_4_4), e2m1 operands, bf16 output", "shapes": out}
+    except Exception as e:  # pragma: no cover
+        return {"unavailable": repr(e)[:200]}
+
+
 def int8_peak_probe(torch):
     """cuBLASLt int8 GEMM (torch._int_mm) 8192^3, best of 5 — context for the int8 roofline."""
     try:
@@ -203,6 +258,18 @@ def host_threads():
         return len(os.sched_getaffinity(0))
     except AttributeError:
         return os.cpu_count() or 1
+
+
+def cpu_model():
+    """The host CPU's model name (lscpu / /proc/cpuinfo), for the CPU baseline's record."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.lower().startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def cpu_reference_step(ops, threads, rows_sample):
@@ -273,7 +340,7 @@ def run_reference_arm(args):
         "vs_baseline": None, "dtype": "u64 bit-packed (int popcount)", "data": "synthetic",
         "config": workload_config(args.gpus),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": sample},
+                         "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -559,6 +626,8 @@ def main():
         peak_src = (f"int8 dense = 2 x bf16 burst of {peaks_src} ({peak_from_bf16:.1f})"
                     if peak == peak_from_bf16 else f"cuBLASLt int8 _int_mm 8192^3 burst ({probe:.1f})")
     tc = kernels.get(kname, {"launches": 0, "ms": 0.0})
+    fp4_meas = measured_fp4_peak() if fp4 else None
+    lib_fp4 = library_fp4_gemm(torch) if fp4 else None
     macs_per_step = upd_per_step  # this rank's (rank 0's) GEMMs
     achieved = (2.0 * macs_per_step * args.steps) / (tc["ms"] * 1e-3) / 1e12 if tc["ms"] else 0.0
     traffic, l2 = None, None
@@ -592,6 +661,10 @@ def main():
         "routines": routines,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if peak else None, "traffic": traffic,
+                     "peak_measured": fp4_meas,
+                     "frac_of_measured_sustained": (achieved / fp4_meas["mxf4_sustained_tflops"]
+                                                    if fp4_meas else None),
+                     "library_fp4_tflops": lib_fp4,
                      "clocks_note": "sampled from warmup start through the end of the timed region",
                      "kernel": f"{kname} (tensor ops = 2 per MAC)", "peak_source": peak_src,
                      "l2": l2,
@@ -624,6 +697,7 @@ def main():
         secs, upd, kind = cpu_reference_step(ops, threads, rows)
         line["cpu_baseline"] = {
             "value": upd / secs / 1e12, "unit": UNIT, "cores": threads, "kind": kind,
+            "cpu_model": cpu_model(),
             "sample": f"one step restricted to rows [0,{rows}) of each GEMM's M (full N, K); "
                       f"{secs:.1f} s of CPU time"}
         # the reference also timed with threads = 1

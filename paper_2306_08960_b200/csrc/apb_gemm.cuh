@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(SPMM_THREADS, 2)
   const int c0 = blockIdx.x * SPMM_TOK;
   const int r0 = blockIdx.y * rows_per_split;
   const int r1 = min(rows, r0 + rows_per_split);
-  const bool vec = ((N & 3) == 0) && ((ldc & 3) == 0) &&
+  const bool vec = ((N & 3) == 0) && ((ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0) &&
                    (LEVELS || (((ldx & 3) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0)));
   if constexpr (LEVELS) {
     // lane = token, warp step = one 64-bit plane word: each smem store instruction writes
@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else {
     const int quad = warp & 3;
     float* stg = sEpi + (warp - 2) * 32 * TC_EPI_STRIDE;
-    const bool vec_ok = ((p.N & 3) == 0) && ((p.ldc & 3) == 0);
+    const bool vec_ok = ((p.N & 3) == 0) && ((p.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0);
     int it = 0;
     for (int tile = unit; tile < p.num_tiles; tile += num_units, ++it) {
       int mb, nb;

@@ -435,9 +435,14 @@ int make_operand_map(CUtensorMap* map, const void* base, CUtensorMapDataType dt,
 // Output map for the GEMM epilogue's bulk tensor stores: [rows][ldc] 4-byte cells, box 32x32,
 // 128B swizzle (the epilogue's staging layout). Returns false when the layout does not allow
 // TMA (row pitch not a multiple of 16 bytes or base not 16-byte aligned).
+// The box is clipped at the tensor's bounds only to 16-byte granularity along the rows: with
+// cols not a multiple of 4 the last chunk of a row would also write up to 3 cells past cols
+// (measured: tests/test_bounds_gpu.py, a caller's ldc > cols), so such outputs take the
+// epilogue's st.global path.
 bool make_output_map(CUtensorMap* map, void* base, CUtensorMapDataType dt, uint64_t cols,
                      uint64_t rows, uint64_t ldc) {
-  if (base == nullptr || (ldc & 3) != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  if (base == nullptr || (ldc & 3) != 0 || (cols & 3) != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0)
+    return false;
   PFN_encodeTiled_t enc = encode_fn();
   if (!enc) return false;
   cuuint64_t dims[2] = {cols, rows};

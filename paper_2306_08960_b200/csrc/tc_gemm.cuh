@@ -129,7 +129,9 @@ __device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, const CUtens
                                                  uint32_t tmem_acc, int quad, int lane,
                                                  int row_base, int col_base, float* stg,
                                                  uint32_t& buf, const float* cs, float row_mul) {
-  const bool vec_ok = (p.N & 3) == 0;
+  // 16-byte stores in the fallback only when every row start is 16-byte aligned
+  const void* out_base = (EPI == Epi::I32) ? static_cast<const void*>(p.out_i32) : static_cast<const void*>(p.out_f32);
+  const bool vec_ok = ((p.N | static_cast<int>(p.ldc & 3)) & 3) == 0 && (reinterpret_cast<uintptr_t>(out_base) & 15) == 0;
   const uint32_t lane_base = tmem_acc + (static_cast<uint32_t>(quad * 32) << 16);
   const int nch = min(BN / 32, (p.N - col_base + 31) / 32);
   // One 32-column chunk: per-thread (row) transform, staged into smem, then stored.

@@ -34,7 +34,10 @@ def test_library_is_sm100a_cubin():
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True,
                           check=True).stdout
-    for mnemonic in ("UTCIMMA", "UTCHMMA", "UTMALDG", "LDTM"):
+    # UTCOMMA: the kind::mxf4 product path (the default); UTCIMMA / UTCHMMA: the int8 A/B
+    # path and the fp16 APB GEMM; UTMALDG / UTMASTG: TMA loads and the epilogue's TMA stores;
+    # LDTM / STTM: TMEM reads and the scale-factor fill
+    for mnemonic in ("UTCOMMA.2CTA", "UTCIMMA", "UTCHMMA", "UTMALDG", "UTMASTG", "LDTM", "STTM"):
         assert mnemonic in sass, mnemonic
 
 
