@@ -631,7 +631,7 @@ def main():
     macs_per_step = upd_per_step  # this rank's (rank 0's) GEMMs
     achieved = (2.0 * macs_per_step * args.steps) / (tc["ms"] * 1e-3) / 1e12 if tc["ms"] else 0.0
     traffic, l2 = None, None
-    tpath = os.path.join(REPO, "profiles", "traffic_r01.json")
+    tpath = os.path.join(REPO, "profiles", "traffic_r02.json")
     if os.path.exists(tpath):
         try:
             tj = json.load(open(tpath))

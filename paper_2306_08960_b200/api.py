@@ -226,28 +226,35 @@ class ApbLayer:
 
 
 # --------------------------------------------------------------------------- packing
+# The packers run on the GPU through the host ABI (bitmm_pack_signs_host, ...); there is no
+# host implementation of them here.
 def pack_signs(m: np.ndarray, lane_bits: int = LANE_BITS) -> BitMatrix:
-    """tensor.cpp:155-164 — sign(0) counts as +1."""
-    from .data import pack_bits
-    m = np.asarray(m, dtype=np.float32)
-    words, wpr = pack_bits((m >= 0.0).astype(np.uint8), lane_bits)
-    return BitMatrix.from_words(m.shape[0], m.shape[1], wpr, words)
+    """tensor.cpp:155-164 — sign(0) counts as +1 (GPU packer, bitmm_pack_signs_host)."""
+    m = np.ascontiguousarray(m, dtype=np.float32)
+    rows, cols = m.shape
+    b = BitMatrix(rows, cols, lane_bits)  # the reference's dimension checks
+    if rows == 0 or b.words_per_row() == 0:
+        return b
+    _raise(_lib.load().bitmm_pack_signs_host(_ptr(m), rows, cols, cols, _ptr(b.words), b.words_per_row()))
+    return b
 
 
 def decompose_thm(q: TwoBitMatrix, gamma: Optional[float] = None,
                   lane_bits: int = LANE_BITS) -> ThmPlanes:
-    """transform.cpp:47-75."""
-    from .data import planes_from_levels
-    lv = np.asarray(q.levels, dtype=np.uint8).reshape(q.rows, q.cols)
-    if np.any(lv > 3):
-        raise ValueError("2-bit level out of range")
-    t, h, m, wpr = planes_from_levels(lv, lane_bits)
-    mk = lambda w: BitMatrix.from_words(q.rows, q.cols, wpr, w)  # noqa: E731
-    return ThmPlanes(mk(t), mk(h), mk(m), q.scale, gamma)
+    """transform.cpp:47-75 (GPU packer, bitmm_decompose_thm_host): a level above 3 raises
+    ValueError ("2-bit level out of range")."""
+    lv = np.ascontiguousarray(np.asarray(q.levels, dtype=np.uint8).reshape(q.rows, q.cols))
+    t, h, m = (BitMatrix(q.rows, q.cols, lane_bits) for _ in range(3))
+    if q.rows > 0 and t.words_per_row() > 0:
+        _raise(_lib.load().bitmm_decompose_thm_host(_ptr(lv), q.rows, q.cols, _ptr(t.words), _ptr(h.words),
+                                                    _ptr(m.words), t.words_per_row()))
+    return ThmPlanes(t, h, m, q.scale, gamma)
 
 
 def quantize_uniform_2bit(m: np.ndarray, s: float) -> TwoBitMatrix:
-    """transform.cpp:21-36 — lround (halves away from zero), clamp to [0,3]."""
+    """transform.cpp:21-36 — lround (halves away from zero), clamp to [0,3]. The levels view a
+    TwoBitMatrix carries; device pipelines quantize and decompose in one GPU pass
+    (bitmm_quantize_thm_*)."""
     if not s > 0.0:
         raise ValueError("quantization step must be positive")
     m = np.asarray(m, dtype=np.float32)
@@ -257,71 +264,33 @@ def quantize_uniform_2bit(m: np.ndarray, s: float) -> TwoBitMatrix:
     return TwoBitMatrix(m.shape[0], m.shape[1], p.reshape(-1), float(s))
 
 
-def _round_with_tie_away(x: np.ndarray) -> np.ndarray:
-    """apb.cpp:35-46 with away_from_zero = true, vectorised over float64 x."""
-    near = x.astype(np.float32)
-    dn = near.astype(np.float64)
-    toward = np.where(dn < x, np.float32(np.inf), np.float32(-np.inf))
-    other = np.nextafter(near, toward).astype(np.float32)
-    err_near = np.abs(x - dn)
-    err_other = np.abs(other.astype(np.float64) - x)
-    near_larger = np.abs(dn) > np.abs(other.astype(np.float64))
-    pick = np.where(err_near != err_other, np.where(err_near < err_other, near, other),
-                    np.where(near_larger, near, other))
-    return np.where(dn == x, near, pick).astype(np.float32)
-
-
-DELTA_MIN = np.float32(1e-8)  # kDeltaMin, apb.hpp:16
-
-
-def init_alpha_delta(w: np.ndarray):
-    """init_alpha_delta (apb.cpp:191-210): alpha = mean |w|, delta = max(3 * population std,
-    1e-8), both accumulated in double in storage order (sequential sums, as the reference)."""
-    v = np.ascontiguousarray(w, np.float32).reshape(-1).astype(np.float64)
-    n = v.size
-    if n == 0:
-        raise ValueError("empty weight matrix")
-    abs_sum = float(np.cumsum(np.abs(v))[-1])  # cumsum: one running sum, element order
-    mean = float(np.cumsum(v)[-1]) / n
-    var = float(np.cumsum((v - mean) ** 2)[-1]) / n
-    alpha = np.float32(abs_sum / n)
-    delta = max(np.float32(3.0 * np.sqrt(var)), DELTA_MIN)
-    return alpha, np.float32(delta)
-
-
-def check_apb_params(alpha, delta) -> None:
-    """ApbParams::validate (apb.cpp:50-55)."""
-    if not alpha > 0.0:
-        raise ValueError("alpha must be positive")
-    if not delta >= DELTA_MIN:
-        raise ValueError("delta must be at least the 1e-8 floor")
-    if not (np.isfinite(alpha) and np.isfinite(delta)):
-        raise ValueError("alpha and delta must be finite")
-
-
 def decompose_apb(a: np.ndarray, alpha, lane_bits: int = LANE_BITS) -> ApbLayer:
-    """apb.cpp:119-142. bin = pack_signs(a) at every position; residual = a - alpha*sign(a)
-    wherever |a| != alpha (membership by exact value), rounded with ties away from zero.
-    `alpha` may also be a per-row vector (each row split with its own alpha)."""
+    """apb.cpp:119-142 (GPU packer, bitmm_decompose_apb_host). bin = pack_signs(a) at every
+    position; residual = a - alpha*sign(a) wherever |a| != alpha (membership by exact value),
+    computed in double and rounded with ties away from zero. `alpha` may also be a per-row
+    vector (each row split with its own alpha)."""
     a = np.ascontiguousarray(a, dtype=np.float32)
     rows, cols = a.shape
-    al = np.broadcast_to(np.asarray(alpha, dtype=np.float32).reshape(-1, 1)
-                         if np.ndim(alpha) else np.float32(alpha), (rows, 1))
-    if not np.all(al > 0.0):
+    per_row = np.ndim(alpha) != 0
+    al = np.ascontiguousarray(np.asarray(alpha, np.float32).reshape(-1)) if per_row else None
+    a_scalar = 1.0 if per_row else float(alpha)
+    if (per_row and not np.all(al > 0.0)) or (not per_row and not a_scalar > 0.0):
         raise ValueError("alpha must be positive")
-    bin_ = pack_signs(a, lane_bits)
-    keep = np.abs(a) != al
-    r_idx, c_idx = np.nonzero(keep)
-    sgn = np.where(a >= 0.0, np.float32(1.0), np.float32(-1.0))
-    base = (al * sgn).astype(np.float32)
-    diff = a[r_idx, c_idx].astype(np.float64) - base[r_idx, c_idx].astype(np.float64)
-    vals = _round_with_tie_away(diff)
-    counts = np.bincount(r_idx, minlength=rows)
+    bin_ = BitMatrix(rows, cols, lane_bits)
     row_ptr = np.zeros(rows + 1, np.uint64)
-    row_ptr[1:] = np.cumsum(counts)
-    res = CsrMatrix.create(rows, cols, row_ptr, c_idx.astype(np.uint64), vals)
-    return ApbLayer(rows, cols, alpha if np.ndim(alpha) == 0 else np.asarray(alpha, np.float32),
-                    bin_, res)
+    nnz = C.c_int64(0)
+    lib = _lib.load()
+    wpr = bin_.words_per_row()
+    _raise(lib.bitmm_decompose_apb_host(_ptr(a), rows, cols, cols, a_scalar, _ptr(al), _ptr(bin_.words), wpr,
+                                        _ptr(row_ptr), None, None, 0, C.byref(nnz)))
+    col_idx = np.zeros(max(nnz.value, 1), np.uint64)
+    vals = np.zeros(max(nnz.value, 1), np.float32)
+    if nnz.value > 0:
+        _raise(lib.bitmm_decompose_apb_host(_ptr(a), rows, cols, cols, a_scalar, _ptr(al), _ptr(bin_.words),
+                                            wpr, _ptr(row_ptr), _ptr(col_idx), _ptr(vals), nnz.value,
+                                            C.byref(nnz)))
+    res = CsrMatrix.create(rows, cols, row_ptr, col_idx[:nnz.value], vals[:nnz.value])
+    return ApbLayer(rows, cols, alpha if not per_row else np.asarray(alpha, np.float32), bin_, res)
 
 
 # --------------------------------------------------------------------------- GEMMs

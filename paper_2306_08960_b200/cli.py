@@ -25,6 +25,39 @@ ROUTINES = ("1x1", "1x2", "2x2", "spmm", "1x32_ref")
 CSV_HEADER = "routine,m,k,n,reps,warmup,threads,simd,seconds,gops,gflops,tpp_gops,pct_tpp\n"
 
 
+
+# ---- CLI-only: the reference CLI's `pack --mode apb` parameter step (bitmm_main.cpp:195-207).
+# Training-side APB helpers (apb.cpp:50-55, 191-210), OUT OF SCOPE for the hot path (SURVEY.md
+# §2 row 6); kept here, at the one place that needs them, so `pack` writes the same files as
+# the reference CLI. Nothing on the GEMM / layer path calls them.
+DELTA_MIN = np.float32(1e-8)  # kDeltaMin, apb.hpp:16
+
+
+def init_alpha_delta(w: np.ndarray):
+    """init_alpha_delta (apb.cpp:191-210): alpha = mean |w|, delta = max(3 * population std,
+    1e-8), both accumulated in double in storage order (sequential sums, as the reference)."""
+    v = np.ascontiguousarray(w, np.float32).reshape(-1).astype(np.float64)
+    n = v.size
+    if n == 0:
+        raise ValueError("empty weight matrix")
+    abs_sum = float(np.cumsum(np.abs(v))[-1])  # cumsum: one running sum, element order
+    mean = float(np.cumsum(v)[-1]) / n
+    var = float(np.cumsum((v - mean) ** 2)[-1]) / n
+    alpha = np.float32(abs_sum / n)
+    delta = max(np.float32(3.0 * np.sqrt(var)), DELTA_MIN)
+    return alpha, np.float32(delta)
+
+
+def check_apb_params(alpha, delta) -> None:
+    """ApbParams::validate (apb.cpp:50-55)."""
+    if not alpha > 0.0:
+        raise ValueError("alpha must be positive")
+    if not delta >= DELTA_MIN:
+        raise ValueError("delta must be at least the 1e-8 floor")
+    if not (np.isfinite(alpha) and np.isfinite(delta)):
+        raise ValueError("alpha and delta must be finite")
+
+
 def cmd_pack(args) -> int:
     import torch
     from . import api, btsr, device
@@ -55,8 +88,8 @@ def cmd_pack(args) -> int:
         if args.alpha is not None:
             alpha, delta = np.float32(args.alpha), np.float32(args.delta)
         else:
-            alpha, delta = api.init_alpha_delta(x.cpu().numpy())
-        api.check_apb_params(alpha, delta)
+            alpha, delta = init_alpha_delta(x.cpu().numpy())
+        check_apb_params(alpha, delta)
         bound = np.float32(alpha + delta)  # float add, apb.cpp:59
         sign_alpha = torch.where(x >= 0, torch.tensor(float(alpha), device=x.device),
                                  torch.tensor(-float(alpha), device=x.device))

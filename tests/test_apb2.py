@@ -12,8 +12,12 @@ from paper_2306_08960_b200 import api, data
 
 
 def _layer(rng, rows, cols, keep_frac=0.02, lane=512):
+    """The layer from the oracle's decompose_apb (apb.cpp:119-142), so the CPU tests need no GPU."""
+    import oracle
     a, alpha, _ = data.apb_weights(rng, rows, cols, keep_frac=keep_frac)
-    layer = api.decompose_apb(a, alpha, lane_bits=lane)
+    bw, wpr, rp, ci, v = oracle.Oracle().decompose_apb(a, alpha, lane)
+    layer = api.ApbLayer(rows, cols, alpha, api.BitMatrix.from_words(rows, cols, wpr, bw),
+                         api.CsrMatrix.create(rows, cols, rp, ci, v))
     return layer, alpha
 
 

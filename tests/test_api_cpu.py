@@ -1,19 +1,10 @@
-"""CPU: host-side mirror of the reference interface — packing, decomposition and
-validation — against the oracle and the reference's golden vectors."""
+"""CPU: host-side parts of the mirror of the reference interface — layouts, validation, the
+levels quantizer — and the CLI's fenced training-side helper, against the oracle and the
+reference's golden vectors. The packers themselves run on the GPU (test_api_packers_gpu.py)."""
 import numpy as np
 import pytest
 
-from conftest import apb_case
 from paper_2306_08960_b200 import api, data
-
-
-def test_bitmatrix_frozen_packing():
-    # test_tensor.cpp:17-30: [+1,-1,+1] -> 0b101, 8 words per row at 512-bit lanes
-    b = api.pack_signs(np.array([[1.0, -1.0, 1.0]], np.float32))
-    assert int(b.words[0, 0]) == 0b101
-    assert b.words_per_row() == 8
-    assert b.bit(0, 0) and not b.bit(0, 1) and b.bit(0, 2)
-    assert api.pack_signs(np.array([[0.0, -0.0]], np.float32)).words[0, 0] == 0b11  # sign(0)=+1
 
 
 def test_from_words_rejects_padding():
@@ -25,23 +16,6 @@ def test_from_words_rejects_padding():
     with pytest.raises(ValueError):
         api.BitMatrix.from_words(2, 3, 1, [0])
     assert api.BitMatrix.from_words(1, 3, 1, [0b111]).padding_is_zero()
-
-
-def test_packing_matches_golden(orc, packing_golden):
-    g = packing_golden
-    for i in range(int(g["pack_count"])):
-        p = f"p{i:03d}_"
-        rows, cols, lane, wpr = (int(x) for x in g[p + "shape"])
-        b = api.pack_signs(g[p + "a"], lane)
-        assert b.words_per_row() == wpr and np.array_equal(b.words, g[p + "signs"])
-        q = api.quantize_uniform_2bit(g[p + "x"], 0.5)
-        assert np.array_equal(q.levels.reshape(rows, cols), g[p + "levels"])
-        tp = api.decompose_thm(q, lane_bits=lane)
-        assert np.array_equal(tp.t.words, g[p + "t"]) and np.array_equal(tp.h.words, g[p + "h"])
-        assert np.array_equal(tp.m.words, g[p + "m"])
-        tp.validate()
-        assert np.array_equal(data.levels_from_planes(tp.t.words, tp.h.words, tp.m.words, cols),
-                              g[p + "levels"])
 
 
 def test_random_planes_are_legal_uniform():
@@ -63,31 +37,6 @@ def test_thm_validate_errors():
             planes(t, h, m).validate()
     for t, h, m in [(0, 0, 1), (0, 0, 0), (0, 1, 0), (1, 0, 1)]:
         planes(t, h, m).validate()
-
-
-def test_decompose_apb_matches_golden(apb_golden):
-    for i in range(int(apb_golden["apb_count"])):
-        c = apb_case(apb_golden, i)
-        alpha = c["alpha_vec"] if "alpha_vec" in c else float(c["alpha_delta"][0])
-        layer = api.decompose_apb(c["fwd"], alpha)
-        assert np.array_equal(layer.bin.words, c["bin"])
-        assert np.array_equal(layer.residual.row_ptr, c["row_ptr"])
-        assert np.array_equal(layer.residual.col_idx, c["col_idx"])
-        assert np.array_equal(layer.residual.vals, c["vals"])
-
-
-def test_decompose_apb_tie_rounding_matches_oracle(orc):
-    # apb.cpp:35-46: non-dyadic thresholds exercise the ties-away-from-zero fixup
-    rng = np.random.default_rng(8)
-    for alpha, delta in [(0.75, 0.5), (0.7, 0.4), (0.3, 0.45)]:
-        w = rng.uniform(-3, 3, (8, 90)).astype(np.float32)
-        fwd = orc.apb_forward(w, alpha, delta)
-        layer = api.decompose_apb(fwd, alpha)
-        bw, wpr, rp, ci, v = orc.decompose_apb(fwd, alpha)
-        assert np.array_equal(layer.bin.words, bw) and np.array_equal(layer.residual.vals, v)
-        assert np.array_equal(layer.residual.col_idx, ci)
-    with pytest.raises(ValueError):
-        api.decompose_apb(np.ones((1, 1), np.float32), 0.0)
 
 
 def test_csr_validation():
@@ -119,13 +68,15 @@ def test_apb_weights_generator_shape():
     rng = np.random.default_rng(1)
     a, alpha, keep = data.apb_weights(rng, 16, 768)
     assert keep == 15  # 2% of 768, the survey's C4 residual count
-    layer = api.decompose_apb(a, alpha)
-    assert layer.residual.nnz() == 16 * 15
+    import oracle
+    _, _, rp, _, _ = oracle.Oracle().decompose_apb(a, alpha)
+    assert int(rp[-1]) == 16 * 15
 
 
 def test_init_alpha_delta_matches_reference(tmp_path):
-    """init_alpha_delta (apb.cpp:191-210): the host mirror's sequential double sums give the
-    reference's alpha and delta bit for bit, including the 1e-8 delta floor."""
+    """init_alpha_delta (apb.cpp:191-210), the CLI's fenced training-side helper: its sequential
+    double sums give the reference's alpha and delta bit for bit, including the 1e-8 floor."""
+    from paper_2306_08960_b200 import cli
     import oracle
     ref = oracle.load_ref()
     if ref is None:
@@ -135,8 +86,8 @@ def test_init_alpha_delta_matches_reference(tmp_path):
              rng.uniform(-3, 3, (7, 1001)).astype(np.float32),
              np.full((3, 5), 0.25, np.float32)]  # zero variance: delta floor
     for w in cases:
-        alpha, delta = api.init_alpha_delta(w)
+        alpha, delta = cli.init_alpha_delta(w)
         ra, rd = ref.pack_apb(w, str(tmp_path / "p"))
         assert np.float32(alpha) == np.float32(ra) and np.float32(delta) == np.float32(rd)
     with pytest.raises(ValueError):
-        api.init_alpha_delta(np.zeros((0, 4), np.float32))
+        cli.init_alpha_delta(np.zeros((0, 4), np.float32))
