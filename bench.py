@@ -399,14 +399,22 @@ def main():
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local_rank = env_int("LOCAL_RANK", 0)
-    torch.cuda.set_device(local_rank)
+    # BITMM_BENCH_BACKEND=gloo: test mode for the multi-rank code path on one GPU (ranks share
+    # cuda:0, host-side collectives on CPU tensors); not a scaling measurement
+    backend = os.environ.get("BITMM_BENCH_BACKEND", "nccl")
+    local_dev = local_rank % max(1, torch.cuda.device_count()) if backend == "gloo" else local_rank
+    torch.cuda.set_device(local_dev)
     if world > 1:
         # NCCL's INIT lines (ranks, NVLink/NVLS transport) go to the log beside the JSON line
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_dev))
     lib = _lib.load()
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", local_dev)
+    comm_dev = torch.device("cpu") if backend == "gloo" else dev  # where collectives' tensors live
 
     ops = make_rank_operands(rank)
     T = lambda x: torch.from_numpy(np.ascontiguousarray(x).view(np.int64)).to(dev)  # noqa: E731
@@ -541,7 +549,7 @@ def main():
         for i, (name, *_rest) in enumerate(ROUTINES):
             per_routine_ms[name] += evs[i].elapsed_time(evs[i + 1])
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([total_ms], dtype=torch.float64, device=comm_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
@@ -557,7 +565,7 @@ def main():
             blk = d[name]["units"] if "units" in d[name] else d[name]["out"]
             if name == "1x1":
                 blk = shard.popcount_wire(k).encode(blk)  # lossless uint16 popcounts
-            payloads.append(blk.contiguous().view(torch.uint8).reshape(-1))
+            payloads.append(blk.contiguous().view(torch.uint8).reshape(-1).to(comm_dev))
         parts = [[torch.empty_like(p) for _ in range(world)] if rank == 0 else None
                  for p in payloads]
         g_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -573,7 +581,7 @@ def main():
                 dist.gather(p, pa, dst=0)
         g_ev[1].record(stream)
         torch.cuda.synchronize()
-        gt = torch.tensor([g_ev[0].elapsed_time(g_ev[1]) / reps], dtype=torch.float64, device=dev)
+        gt = torch.tensor([g_ev[0].elapsed_time(g_ev[1]) / reps], dtype=torch.float64, device=comm_dev)
         dist.all_reduce(gt, op=dist.ReduceOp.MAX)
         gather = {"ms_per_step": float(gt.item()),
                   "bytes_to_root_per_step": sum(p.numel() for p in payloads) * (world - 1),
@@ -600,7 +608,7 @@ def main():
     # ---- BASELINE config 5 at this N: kernel-only, gather fused into the epilogue, NCCL ----
     del d
     torch.cuda.empty_cache()
-    sweep = c5_sweep(GpuC5Backend(torch, dev, lib), dist if world > 1 else None, world, rank,
+    sweep = c5_sweep(GpuC5Backend(torch, dev, lib, comm_dev), dist if world > 1 else None, world, rank,
                      C5, C5, C5)
 
     if world > 1:
@@ -672,6 +680,8 @@ def main():
                      "popc_roofline_T_updates_per_s": 148 * 16 * 32 * 1.965e9 / 1e12},
         "kernels": kernels,
         "clocks": clocks,
+        "dist_backend": (backend + (" (test mode: ranks share one GPU; not a scaling measurement)"
+                                    if backend == "gloo" else "")) if world > 1 else None,
         "step_path": ("bitmm_gemm_batch_dev: one expansion launch + one persistent tensor-core "
                       "launch over the three GEMMs" if not args.sequential else
                       "one bitmm_gemm_*_dev call per routine"),
@@ -722,8 +732,9 @@ class GpuC5Backend:
 
     p2p = True
 
-    def __init__(self, torch, dev, lib):
+    def __init__(self, torch, dev, lib, comm_dev=None):
         self.torch, self.dev, self.lib = torch, dev, lib
+        self.comm_dev = comm_dev if comm_dev is not None else dev  # collectives' tensors
 
     def upload(self, words):
         return self.torch.from_numpy(np.ascontiguousarray(words).view(np.int64)).to(self.dev)
@@ -757,7 +768,7 @@ class GpuC5Backend:
         return out
 
     def reduce_max(self, dist, v):
-        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.dev)
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.comm_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -816,7 +827,8 @@ def c5_sweep(backend, dist, world, rank, m, n, k, reps=2, check_rows=4):
 
         def nccl():
             got[0] = shard.run_sharded(m, n, torch.int32, compute, getattr(backend, "dev", torch.device("cpu")),
-                                       chunk_rows=max(1, m // 4), wire=shard.popcount_wire(k))
+                                       chunk_rows=max(1, m // 4), wire=shard.popcount_wire(k),
+                                       comm_device=getattr(backend, "comm_dev", None))
 
         res["nccl_gather_ms"] = red(min(backend.time(nccl, reps)))
         res["nccl_bytes_to_root"] = (world - 1) * m * width * 2

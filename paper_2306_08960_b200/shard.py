@@ -70,13 +70,15 @@ def run_sharded(m: int, n: int, out_dtype: torch.dtype,
                 compute: Callable[[int, int, int, int, torch.Tensor], None],
                 device: torch.device, group=None, dst: int = 0,
                 chunk_rows: Optional[int] = None, wire: Optional[Wire] = None,
-                out: Optional[torch.Tensor] = None) -> Optional[torch.Tensor]:
+                out: Optional[torch.Tensor] = None,
+                comm_device: Optional[torch.device] = None) -> Optional[torch.Tensor]:
     """Compute this rank's column block of an M x N result and gather it to `dst`.
 
     compute(col_lo, col_hi, row_lo, row_hi, block) must fill `block`
     ([row_hi-row_lo, col_hi-col_lo], out_dtype, contiguous) with those output cells.
     Returns the assembled row-major M x N tensor on `dst`, None elsewhere. With a single
-    rank it is just compute() into `out`.
+    rank it is just compute() into `out`. `comm_device`: where the gathered payloads live when
+    the backend cannot move `device` tensors (gloo with CUDA compute); default `device`.
     """
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -98,7 +100,7 @@ def run_sharded(m: int, n: int, out_dtype: torch.dtype,
             for g, part in enumerate(parts):
                 glo, ghi = column_range(n, g, world)
                 if ghi > glo:
-                    blk = part.view(wire.dtype).view(r1 - r0, width)[:, : ghi - glo]
+                    blk = part.view(wire.dtype).view(r1 - r0, width)[:, : ghi - glo].to(out.device)
                     out[r0:r1, glo:ghi].copy_(wire.decode(blk))
 
     for r0 in range(0, m, chunk):
@@ -115,6 +117,8 @@ def run_sharded(m: int, n: int, out_dtype: torch.dtype,
         if width > hi - lo:
             block[:, hi - lo:].zero_()
         payload = _bytes(wire.encode(block))
+        if comm_device is not None:
+            payload = payload.to(comm_device)
         parts = [torch.empty_like(payload) for _ in range(world)] if rank == dst else None
         work = dist.gather(payload, parts, dst=dst, group=group, async_op=True)
         pending.append((work, r0, r1, parts))
