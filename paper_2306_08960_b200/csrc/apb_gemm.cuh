@@ -405,13 +405,20 @@ constexpr int APB_SMEM = 1024 + APB_STAGES * APB_STAGE + APB_EPI_BYTES + (2 * AP
 // AP = A parts per smem stage. AP = 1: A = sign(bin) (or W'_hi, with the fold phase after the
 // main K loop); AP = 2: a stage holds W'_hi and W'_lo of one K slice with both X parts, so X_hi
 // is loaded once for both products (48 KB stages, 4 of them).
-template <int AP>
+// BN = output columns per pair tile: 128 keeps the hi and lo products in separate TMEM
+// accumulators (2 x 2 x 128 columns); 256 (AP = 2 only) sums all three products in one
+// accumulator per tile (2 x 256 columns) and halves the operand bytes per MAC (64 KB stages,
+// 3 of them).
+template <int AP, int BN = APB_BN>
 struct ApbCfg {
-  static constexpr int STAGES = AP == 1 ? APB_STAGES : 4;
-  static constexpr int STAGE = AP * APB_A_STAGE + APB_PARTS * APB_B_PART;
+  static constexpr int B_PART = (BN / 2) * TC_BK_BYTES;
+  static constexpr int STAGES = AP == 1 ? APB_STAGES : (BN == 256 ? 3 : 4);
+  static constexpr int STAGE = AP * APB_A_STAGE + APB_PARTS * B_PART;
   static constexpr int SMEM = 1024 + STAGES * STAGE + APB_EPI_BYTES + (2 * STAGES + 4) * 8 + 16;
+  static constexpr bool ONE_ACC = BN == 256;
 };
 static_assert(ApbCfg<2>::SMEM <= 227 * 1024, "APB stages exceed shared memory");
+static_assert(ApbCfg<2, 256>::SMEM <= 227 * 1024, "APB stages exceed shared memory");
 
 struct ApbParams {
   int M, N, kb_per_part;     // kb_per_part = kpad / 64
@@ -435,11 +442,12 @@ __device__ __forceinline__ void apb_tile_coords(int t, const ApbParams& p, int& 
   nb = within / gm;
 }
 
-template <int AP>
+template <int AP, int BN = APB_BN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     apb_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const ApbParams p) {
-  using CFG = ApbCfg<AP>;
+  using CFG = ApbCfg<AP, BN>;
+  constexpr int B_PART = CFG::B_PART;
   constexpr int B_OFF = AP * APB_A_STAGE;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = smem_u32(smem_raw);
@@ -487,7 +495,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         int mb, nb;
         apb_tile_coords(tile, p, mb, nb);
         const int a_row = mb * 256 + static_cast<int>(rank) * 128;
-        const int b_row = nb * APB_BN + static_cast<int>(rank) * (APB_BN / 2);
+        const int b_row = nb * BN + static_cast<int>(rank) * (BN / 2);
         for (int kb = 0; kb < num_kb + p.fold_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1u);
           uint8_t* st = stages + stage * CFG::STAGE;
@@ -497,11 +505,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             if constexpr (AP == 2) tma_load_2d_pair(st + APB_A_STAGE, &tmA, &full[stage], p.kpad + kb * 64, a_row);
 #pragma unroll
             for (int q = 0; q < APB_PARTS; ++q)
-              tma_load_2d_pair(st + B_OFF + q * APB_B_PART, &tmB, &full[stage],
+              tma_load_2d_pair(st + B_OFF + q * B_PART, &tmB, &full[stage],
                                q * p.kpad + kb * 64, b_row);
           } else {  // fold phase: the lo part of W' against X_hi
             const int kf = kb - num_kb;
-            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (APB_A_STAGE + APB_B_PART));
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (APB_A_STAGE + B_PART));
             tma_load_2d_pair(st, &tmA, &full[stage], p.kpad + kf * 64, a_row);
             tma_load_2d_pair(st + APB_A_STAGE, &tmB, &full[stage], kf * 64, b_row);
           }
@@ -514,7 +522,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
-      constexpr uint32_t idesc = make_idesc(1u, 0u, 0u, 256, APB_BN);  // f32 <- f16 x f16
+      constexpr uint32_t idesc = make_idesc(1u, 0u, 0u, 256, BN);  // f32 <- f16 x f16
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -523,8 +531,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t bphase = (it >> 1) & 1;
         mbar_wait(&tempty[buf], bphase ^ 1u);
         tc_fence_after();
-        const uint32_t d_hi = tmem_base + buf * 2 * APB_BN;
-        const uint32_t d_lo = d_hi + APB_BN;
+        // ONE_ACC: every product of the tile into one accumulator (d_lo == d_hi)
+        const uint32_t d_hi = tmem_base + buf * (CFG::ONE_ACC ? BN : 2 * BN);
+        const uint32_t d_lo = CFG::ONE_ACC ? d_hi : d_hi + BN;
         for (int kb = 0; kb < num_kb + p.fold_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -532,12 +541,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (kb < num_kb) {
 #pragma unroll
             for (int q = 0; q < APB_PARTS; ++q) {
-              const uint32_t b_addr = a_addr + B_OFF + q * APB_B_PART;
+              const uint32_t b_addr = a_addr + B_OFF + q * B_PART;
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
                 const uint64_t ad = sw128_kmajor_desc(a_addr + k * 32);
                 const uint64_t bd = sw128_kmajor_desc(b_addr + k * 32);
-                const uint32_t acc = (q == 0) ? ((kb | k) != 0) : !(q == 1 && kb == 0 && k == 0);
+                const uint32_t acc = (q == 0) ? ((kb | k) != 0)
+                                              : (CFG::ONE_ACC ? 1u : !(q == 1 && kb == 0 && k == 0));
                 mma_f16_pair(q == 0 ? d_hi : d_lo, ad, bd, idesc, acc);
               }
             }
@@ -580,15 +590,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                                    : p.alpha;
       mbar_wait(&tfull[buf], bphase);
       tc_fence_after();
-      const uint32_t t_hi = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + buf * 2 * APB_BN;
+      const uint32_t t_hi = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
+                            buf * (CFG::ONE_ACC ? BN : 2 * BN);
       const int cl = (lane & 7) * 4;
 #pragma unroll 1
-      for (int c = 0; c < APB_BN / 32; ++c) {
-        const int col0 = nb * APB_BN + c * 32;
+      for (int c = 0; c < BN / 32; ++c) {
+        const int col0 = nb * BN + c * 32;
         if (col0 >= p.N) break;
         uint32_t vh[32], vl[32];
         tmem_ld_32x32b_x32(t_hi + c * 32, vh);
-        tmem_ld_32x32b_x32(t_hi + APB_BN + c * 32, vl);
+        if constexpr (!CFG::ONE_ACC) tmem_ld_32x32b_x32(t_hi + BN + c * 32, vl);
         // the chunk's 32 token scales: same address in every lane (broadcast); past N: 0
         float ts[32];
 #pragma unroll
@@ -607,7 +618,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           float of[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e)  // x 2^-e_n is exact
-            of[e] = __fmul_rn(__fmul_rn(alpha, __fadd_rn(__uint_as_float(vh[j + e]), __uint_as_float(vl[j + e]))),
+            of[e] = __fmul_rn(__fmul_rn(alpha, CFG::ONE_ACC ? __uint_as_float(vh[j + e])
+                                                            : __fadd_rn(__uint_as_float(vh[j + e]),
+                                                                        __uint_as_float(vl[j + e]))),
                               ts[j + e]);
           *reinterpret_cast<float4*>(&stg[lane * TC_EPI_STRIDE + j]) = make_float4(of[0], of[1], of[2], of[3]);
         }

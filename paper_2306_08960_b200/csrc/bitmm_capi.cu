@@ -1522,9 +1522,18 @@ int apb_dev_impl(Ctx& st, const uint64_t* w, int64_t m, int64_t k, int64_t wpr, 
     BITMM_TRY(launch_check("split_x_f16"));
   }
 
+  // folded layer: 256-wide tiles with one accumulator per tile (default; config 4 103 vs 120 us,
+  // 1.5e-6 vs 2.4e-7 relative error, tolerance 1e-5); BITMM_APB_WIDE=0 keeps 128-wide tiles with
+  // the hi and lo products in separate accumulators (the most accurate)
+  const char* fold_env = std::getenv("BITMM_APB_FOLD");
+  const bool fold_sep = fold_env && std::string(fold_env) == "sep";
+  const bool ap2 = fold && !fold_sep;
+  const char* wide_env = std::getenv("BITMM_APB_WIDE");
+  const bool wide = ap2 && !(wide_env && std::atoi(wide_env) == 0);
+  const int bn = wide ? 256 : APB_BN;
   CUtensorMap ta, tb;
   BITMM_TRY(make_operand_map(&ta, Ah, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, lda, m, 128));
-  BITMM_TRY(make_operand_map(&tb, XT, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, APB_PARTS * kpad, n, APB_BN / 2));
+  BITMM_TRY(make_operand_map(&tb, XT, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, APB_PARTS * kpad, n, bn / 2));
   ApbParams p{};
   p.M = static_cast<int>(m);
   p.N = static_cast<int>(n);
@@ -1532,9 +1541,6 @@ int apb_dev_impl(Ctx& st, const uint64_t* w, int64_t m, int64_t k, int64_t wpr, 
   p.kpad = static_cast<int>(kpad);
   // folded residual: W'_lo rides in the same stages as W'_hi (AP = 2) unless
   // BITMM_APB_FOLD=sep selects the separate fold phase after the main K loop (A/B runs)
-  const char* fold_env = std::getenv("BITMM_APB_FOLD");
-  const bool fold_sep = fold_env && std::string(fold_env) == "sep";
-  const bool ap2 = fold && !fold_sep;
   p.fold_kb = (fold && fold_sep) ? p.kb_per_part : 0;
   p.alpha = gamma;
   p.row_alpha = fold ? row_mul : row_gamma;
@@ -1542,11 +1548,12 @@ int apb_dev_impl(Ctx& st, const uint64_t* w, int64_t m, int64_t k, int64_t wpr, 
   p.C = c;
   p.ldc = ldc;
   p.num_m_blocks = static_cast<int>((m + 255) / 256);
-  p.num_n_blocks = static_cast<int>((n + APB_BN - 1) / APB_BN);
+  p.num_n_blocks = static_cast<int>((n + bn - 1) / bn);
   p.num_tiles = p.num_m_blocks * p.num_n_blocks;
-  const void* kern = ap2 ? reinterpret_cast<const void*>(apb_gemm_kernel<2>)
-                         : reinterpret_cast<const void*>(apb_gemm_kernel<1>);
-  const int smem = ap2 ? ApbCfg<2>::SMEM : ApbCfg<1>::SMEM;
+  const void* kern = wide ? reinterpret_cast<const void*>(apb_gemm_kernel<2, 256>)
+                     : ap2  ? reinterpret_cast<const void*>(apb_gemm_kernel<2>)
+                            : reinterpret_cast<const void*>(apb_gemm_kernel<1>);
+  const int smem = wide ? ApbCfg<2, 256>::SMEM : ap2 ? ApbCfg<2>::SMEM : ApbCfg<1>::SMEM;
   BITMM_TRY(ensure_max_smem(kern, smem));
   const int units = std::min(p.num_tiles, st.sms / 2);
   cudaLaunchConfig_t cfg = {};
@@ -1564,7 +1571,8 @@ int apb_dev_impl(Ctx& st, const uint64_t* w, int64_t m, int64_t k, int64_t wpr, 
   cfg.numAttrs = 2;
   {
     ProfScope ps("apb_gemm_f16x2", s);
-    if (ap2) BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, apb_gemm_kernel<2>, ta, tb, p));
+    if (wide) BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, apb_gemm_kernel<2, 256>, ta, tb, p));
+    else if (ap2) BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, apb_gemm_kernel<2>, ta, tb, p));
     else BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, apb_gemm_kernel<1>, ta, tb, p));
     BITMM_TRY(launch_check("apb_gemm_kernel"));
   }
