@@ -54,6 +54,7 @@ struct SpmmLevels {
   const unsigned long long* m;
   int wpr;
   float d1, d2, d3;  // d0 = 0
+  float neg_zero;    // -0.0f, passed at run time (spmm_levels_kernel's exact products)
 };
 
 // ACCUM (both layers): the GEMM has already stored the binary part in C, and each output

@@ -18,6 +18,8 @@
 #include <vector>
 
 #include "apb_gemm.cuh"
+#include "apb2_fused.cuh"
+#include "spmm_levels.cuh"
 #include "btsr_io.cuh"
 #include "bitmm_b200.h"
 #include "fx_gemm.cuh"
@@ -1434,6 +1436,44 @@ int run_spmm(Ctx& st, int64_t rows, int64_t k, const uint64_t* row_ptr,
   return launch_check("spmm_xchunk_kernel");
 }
 
+// The 2-bit layer's residual pass (spmm_levels.cuh): a persistent grid of 2 blocks per SM, each
+// owning an equal share of the (64-token chunk, row) work space.
+int64_t spmm_levels_work(const Ctx& st, int64_t rows, int64_t n, int* blocks) {
+  const int64_t total = (n + SL_TOK - 1) / SL_TOK * rows;
+  *blocks = static_cast<int>(
+      std::max<int64_t>(1, std::min<int64_t>(SL_BLOCKS_PER_SM * st.sms, (total + SL_OCTETS - 1) / SL_OCTETS)));
+  return (total + *blocks - 1) / *blocks;
+}
+
+bool spmm_levels_fits(const Ctx& st, int64_t rows, int64_t k, int64_t n) {
+  int blocks;
+  const int64_t w = spmm_levels_work(st, rows, n, &blocks);
+  return w < (1 << 30) && spmm_levels_smem_bytes(k, static_cast<int>(std::min<int64_t>(w, rows))) <= kMaxDynSmem;
+}
+
+int run_spmm_levels(Ctx& st, int64_t rows, int64_t k, const uint64_t* row_ptr, const uint64_t* col_idx,
+                    const float* vals, const SpmmLevels& lv, int64_t n, float* c, int64_t ldc, cudaStream_t s) {
+  int blocks;
+  const int64_t w = spmm_levels_work(st, rows, n, &blocks);
+  auto kern = spmm_levels_kernel<true>;
+  const int smem = spmm_levels_smem_bytes(k, static_cast<int>(std::min<int64_t>(w, rows)));
+  BITMM_TRY(ensure_max_smem(reinterpret_cast<const void*>(kern), kMaxDynSmem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+  cfg.blockDim = dim3(SL_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1] = {pdl_attr()};
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ProfScope ps("spmm_levels", s);
+  BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, static_cast<int>(rows), static_cast<int>(k), static_cast<int>(n),
+                                    reinterpret_cast<const unsigned long long*>(row_ptr),
+                                    reinterpret_cast<const unsigned long long*>(col_idx), vals, lv, c,
+                                    static_cast<long long>(ldc), static_cast<long long>(w)));
+  return launch_check("spmm_levels_kernel");
+}
+
 int apb_dev_impl(Ctx& st, const uint64_t* w, int64_t m, int64_t k, int64_t wpr, float gamma,
                  const float* row_gamma, const float* b, int64_t n, int64_t ldb,
                  const uint64_t* row_ptr, const uint64_t* col_idx, const float* vals, float* c,
@@ -1593,11 +1633,117 @@ size_t ws_bytes_apb2(const Ctx& st, int64_t rows, int64_t cols, int64_t tokens) 
   return ws_bytes_int(rows, tokens, cols) + deq;
 }
 
+// The fused form (apb2_fused.cuh): expansion of the GEMM operands, then one kernel computing
+// C = G + S and writing C once. Taken for FP4 operands, a K whose level chunk fits in shared
+// memory beside the pipeline, and an output the epilogue's TMA stores can write;
+// BITMM_APB2_FUSED=0 selects the two-pass form below.
+bool apb2_fused_ok(int64_t cols, int64_t tokens, const float* c, int64_t ldc) {
+  const char* e = std::getenv("BITMM_APB2_FUSED");
+  if (e && std::atoi(e) == 0) return false;
+  return use_fp4() && !fx_enabled() && apb2_fused_smem_bytes(cols) <= kMaxDynSmem && (tokens & 3) == 0 &&
+         (ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(c) & 15) == 0 && !is_peer_memory(c);
+}
+
+int apb2_fused_impl(Ctx& st, int64_t rows, int64_t cols, int64_t wpr, float alpha, const float* row_alpha,
+                    const uint64_t* bin, const uint64_t* row_ptr, const uint64_t* col_idx, const float* vals,
+                    const uint64_t* t, const uint64_t* h, const uint64_t* m, int64_t tokens, float a_scale,
+                    float a_gamma, float* c, int64_t ldc, cudaStream_t s) {
+  const int64_t kpad = kpad_for(cols, true);
+  const int64_t chunks = (tokens + SL_TOK - 1) / SL_TOK;
+  const size_t lc_bytes = static_cast<size_t>(chunks) * (cols + 1) * SL_ROW_WORDS * 4;
+  BITMM_TRY(ws_reserve(st, ws_bytes_int(rows, tokens, cols) + align_up(lc_bytes, 1024)));
+  unsigned* LC = reinterpret_cast<unsigned*>(static_cast<uint8_t*>(st.ws.ptr) + ws_bytes_int(rows, tokens, cols));
+  const OperandSrc sa{bin, nullptr, nullptr, rows, false}, sb{t, h, m, tokens, true};
+  uint8_t *A8 = nullptr, *B8 = nullptr;
+  take_int_operands(st, rows, tokens, cols, &A8, &B8);
+  BITMM_TRY(run_unpack_pair(sa, sb, wpr, cols, kpad, A8, B8, st.status, s, true));
+  SpmmLevels lv{};
+  lv.t = reinterpret_cast<const unsigned long long*>(t);
+  lv.h = reinterpret_cast<const unsigned long long*>(h);
+  lv.m = reinterpret_cast<const unsigned long long*>(m);
+  lv.wpr = static_cast<int>(wpr);
+  const float sg = a_scale * a_gamma;  // the dequantized levels, as the two-pass form stages them
+  lv.d1 = 1.0f * sg;
+  lv.d2 = 2.0f * sg;
+  lv.d3 = 3.0f * sg;
+  lv.neg_zero = -0.0f;
+  {
+    const long long per_chunk = ((cols + 63) / 64) * 2 * SL_ROW_WORDS + SL_ROW_WORDS;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks_for(per_chunk * chunks, 256));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1] = {pdl_attr()};
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ProfScope ps("level_chunks", s);
+    BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, level_chunks_kernel, lv, static_cast<int>(cols), static_cast<int>(tokens),
+                                      static_cast<int>(chunks), LC));
+    BITMM_TRY(launch_check("level_chunks_kernel"));
+  }
+  CUtensorMap ta, tb, tc;
+  const int64_t rb = kpad / 2;
+  BITMM_TRY(make_operand_map(&ta, A8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, rb, rows, 128));
+  BITMM_TRY(make_operand_map(&tb, B8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, rb, tokens, A3_BN / 2));
+  if (!make_output_map(&tc, c, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, tokens, rows, ldc))
+    return fail(BITMM_ERR_CUDA, "fused APB: output map");
+  Apb2Params ap{};
+  TcParams& p = ap.p;
+  p.M = static_cast<int>(rows);
+  p.N = static_cast<int>(tokens);
+  p.num_kb = static_cast<int>(rb / TC_BK_BYTES);
+  p.shift = fp4_shift(1, 1, true);
+  p.shift_mul = static_cast<float>(1 << p.shift);
+  p.scale = 0.5f * alpha * a_scale * a_gamma;  // kernels.cpp:193 order
+  p.row_scale = row_alpha;
+  p.row_pre = 0.5f;
+  p.act_scale = a_scale;
+  p.act_gamma = a_gamma;
+  p.out_f32 = c;
+  p.ldc = ldc;
+  p.epi = static_cast<int>(Epi::F32R);
+  p.tma_store = 1;
+  p.num_m_blocks = static_cast<int>((rows + 255) / 256);
+  p.num_n_blocks = static_cast<int>((tokens + A3_BN - 1) / A3_BN);
+  p.num_tiles = p.num_m_blocks * p.num_n_blocks;
+  ap.row_ptr = reinterpret_cast<const unsigned long long*>(row_ptr);
+  ap.col_idx = reinterpret_cast<const unsigned long long*>(col_idx);
+  ap.vals = vals;
+  ap.lv = lv;
+  ap.level_chunks = LC;
+  ap.K = static_cast<int>(cols);
+  const int smem = apb2_fused_smem_bytes(cols);
+  // the opt-in limit is one value per kernel: set the maximum once (a per-size value would be
+  // overwritten by a smaller K's launch and reject a later larger one)
+  BITMM_TRY(ensure_max_smem(reinterpret_cast<const void*>(apb2_fused_kernel), kMaxDynSmem));
+  const int units = std::max(1, std::min(p.num_tiles, st.sms / 2));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(2 * units));
+  cfg.blockDim = dim3(A3_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  ProfScope ps("apb2_fused", s);
+  BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, apb2_fused_kernel, ta, tb, tc, ap));
+  return launch_check("apb2_fused_kernel");
+}
+
 int apb2_dev_impl(Ctx& st, int64_t rows, int64_t cols, int64_t wpr, float alpha,
                   const float* row_alpha, const uint64_t* bin, const uint64_t* row_ptr,
                   const uint64_t* col_idx, const float* vals, const uint64_t* t, const uint64_t* h,
                   const uint64_t* m, int64_t tokens, float a_scale, float a_gamma, float* c,
                   int64_t ldc, cudaStream_t s) {
+  if (apb2_fused_ok(cols, tokens, c, ldc))
+    return apb2_fused_impl(st, rows, cols, wpr, alpha, row_alpha, bin, row_ptr, col_idx, vals, t, h, m, tokens,
+                           a_scale, a_gamma, c, ldc, s);
   const bool fp4 = use_fp4();
   const int64_t kpad = kpad_for(cols, fp4);
   BITMM_TRY(ws_reserve(st, ws_bytes_apb2(st, rows, cols, tokens)));
@@ -1638,6 +1784,10 @@ int apb2_dev_impl(Ctx& st, int64_t rows, int64_t cols, int64_t wpr, float alpha,
   lv.d1 = 1.0f * sg;
   lv.d2 = 2.0f * sg;
   lv.d3 = 3.0f * sg;
+  lv.neg_zero = -0.0f;
+  const char* v1 = std::getenv("BITMM_SPMM_LEVELS_V1");  // A/B: the fp32-staged form
+  if (!(v1 && std::atoi(v1) != 0) && spmm_levels_fits(st, rows, cols, tokens))
+    return run_spmm_levels(st, rows, cols, row_ptr, col_idx, vals, lv, tokens, c, ldc, s);
   return run_spmm<true, true, true>(st, rows, cols, row_ptr, col_idx, vals, nullptr, tokens, tokens,
                                     c, ldc, s, lv, deq);
 }
@@ -1667,6 +1817,12 @@ extern "C" {
 
 int bitmm_abi_version(void) { return 1; }
 
+#ifdef A3_STATS
+// Profiling builds only (-DA3_STATS): the fused 2-bit APB layer's counters of the last launch.
+int bitmm_debug_a3_stats(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, a3_stats, sizeof(a3_stats)) == cudaSuccess ? 0 : 3;
+}
+#endif
 #ifdef FX_STATS
 // Profiling builds only (-DFX_STATS): the fx_gemm wait counters of the last launch.
 int bitmm_debug_fx_stats(unsigned long long* out) {
