@@ -171,3 +171,18 @@ def test_gpu_device_path_config4_shape(orc):
                                   np.concatenate(vv).astype(np.float32), t, h, m, a_scale=0.5,
                                   row_alpha=alpha[sample])
     assert np.array_equal(got[sample], want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("form", ["fused", "two-pass", "two-pass-fp32"])
+@pytest.mark.parametrize("rows,cols,tokens", [(300, 768, 332), (513, 130, 1000), (257, 960, 64),
+                                              (64, 1100, 68), (1000, 256, 4)])
+def test_gpu_every_form_bit_exact(orc, monkeypatch, form, rows, cols, tokens):
+    """The three device forms of the layer — residual fused into the GEMM epilogue
+    (apb2_fused_kernel), GEMM then the bf16-level SpMM (spmm_levels_kernel), GEMM then the
+    fp32-level SpMM (spmm_xchunk_kernel<LEVELS>) — each bit-identical to the oracle, at shapes
+    with ragged row blocks, token blocks and K (cols 1100 exceeds the fused kernel's shared
+    memory and falls back to the two-pass form)."""
+    monkeypatch.setenv("BITMM_APB2_FUSED", "1" if form == "fused" else "0")
+    monkeypatch.setenv("BITMM_SPMM_LEVELS_V1", "1" if form == "two-pass-fp32" else "0")
+    _gpu_vs_oracle(orc, rows, cols, tokens, seed=3)
