@@ -12,9 +12,9 @@
 //
 // Tiles are 256 rows x 64 tokens (cta_group::2, a CTA pair; each CTA owns 128 rows). A cluster
 // owns a contiguous range of tiles in token-block-major order, so its two CTAs load the levels
-// of a 64-token block once (bf16 patterns of p, [K + 1][64], staged for all blocks beforehand by
-// level_chunks_kernel and bulk-copied from L2) and reuse them for every row block of the range
-// (a range crosses at most two or three token blocks).
+// of a 64-token block once (bf16 patterns of p, [K + 1][64], staged for every block by
+// unpack_operands beside the operand expansion, bulk-copied from L2) and reuse them for every
+// row block of the range (a range crosses at most two or three token blocks).
 //
 // Warp roles per CTA (22 warps):
 //   warp 0       TMA producer: the tile's operand k-blocks (as tc_gemm)
@@ -66,7 +66,7 @@ struct Apb2Params {
   const unsigned long long* col_idx;
   const float* vals;
   SpmmLevels lv;
-  const unsigned* level_chunks;  // level_chunks_kernel's output [chunks][K + 1][SL_ROW_WORDS]
+  const unsigned* level_chunks;  // [chunks][K + 1][SL_ROW_WORDS] (LevelChunkJob, unpack_operands)
   int K;
 };
 

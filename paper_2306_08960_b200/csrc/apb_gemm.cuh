@@ -45,17 +45,6 @@ inline int spmm_smem_bytes(long long K, int rows_per_split) {
 }
 
 
-// LEVELS source: activation planes {t,h,m} [tokens][wpr] (K-packed per token, the
-// a_packed orientation of gemm_1x2) dequantized to d[p] = float(p) * (s * gamma_a) while
-// staging; the chunk is the same [K][SPMM_TOK] fp32 tile the X path stages.
-struct SpmmLevels {
-  const unsigned long long* t;
-  const unsigned long long* h;
-  const unsigned long long* m;
-  int wpr;
-  float d1, d2, d3;  // d0 = 0
-  float neg_zero;    // -0.0f, passed at run time (spmm_levels_kernel's exact products)
-};
 
 // ACCUM (both layers): the GEMM has already stored the binary part in C, and each output
 // row becomes C = bin + R.X (apb.cpp:161-162; fp32 add commutes).

@@ -569,11 +569,16 @@ UnpackOperand make_unpack_operand(const OperandSrc& src, int64_t wpr, int64_t k,
 
 // Expands every operand of a set (bits or ternary planes) in one launch.
 int run_unpack_set(UnpackSet& P, cudaStream_t s) {
-  long long work = 0;
-  for (int i = 0; i < P.count; ++i) work = std::max(work, P.op[i].rows * P.op[i].groups_per_row);
+  long long work = 0;  // threads per grid row: a warp per slice, or a thread per level-chunk item
+  for (int i = 0; i < P.count; ++i) work = std::max(work, P.op[i].rows * P.op[i].groups_per_row * 32);
+  const long long lc_items = P.lc.chunks > 0
+                                 ? static_cast<long long>(((P.lc.K + 63) / 64) * 2 * SL_ROW_WORDS + SL_ROW_WORDS) *
+                                       P.lc.chunks
+                                 : 0;
+  work = std::max(work, lc_items);
   if (work == 0) return BITMM_OK;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(blocks_for(work * 32, 256), static_cast<unsigned>(P.count));  // warp per slice
+  cfg.gridDim = dim3(blocks_for(work, 256), static_cast<unsigned>(P.count + (lc_items > 0 ? 1 : 0)));
   cfg.blockDim = dim3(256);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -588,8 +593,10 @@ int run_unpack_set(UnpackSet& P, cudaStream_t s) {
 
 // Expands both GEMM operands in one launch.
 int run_unpack_pair(const OperandSrc& a, const OperandSrc& b, int64_t wpr, int64_t k, int64_t kpad,
-                    uint8_t* A8, uint8_t* B8, int* flag, cudaStream_t s, bool fp4 = false) {
+                    uint8_t* A8, uint8_t* B8, int* flag, cudaStream_t s, bool fp4 = false,
+                    const LevelChunkJob* lc = nullptr) {
   UnpackSet P{};
+  if (lc) P.lc = *lc;
   P.fp4 = fp4 ? 1 : 0;
   P.op[0] = make_unpack_operand(a, wpr, k, kpad, A8);
   P.op[1] = make_unpack_operand(b, wpr, k, kpad, B8);
@@ -1656,7 +1663,6 @@ int apb2_fused_impl(Ctx& st, int64_t rows, int64_t cols, int64_t wpr, float alph
   const OperandSrc sa{bin, nullptr, nullptr, rows, false}, sb{t, h, m, tokens, true};
   uint8_t *A8 = nullptr, *B8 = nullptr;
   take_int_operands(st, rows, tokens, cols, &A8, &B8);
-  BITMM_TRY(run_unpack_pair(sa, sb, wpr, cols, kpad, A8, B8, st.status, s, true));
   SpmmLevels lv{};
   lv.t = reinterpret_cast<const unsigned long long*>(t);
   lv.h = reinterpret_cast<const unsigned long long*>(h);
@@ -1667,20 +1673,9 @@ int apb2_fused_impl(Ctx& st, int64_t rows, int64_t cols, int64_t wpr, float alph
   lv.d2 = 2.0f * sg;
   lv.d3 = 3.0f * sg;
   lv.neg_zero = -0.0f;
-  {
-    const long long per_chunk = ((cols + 63) / 64) * 2 * SL_ROW_WORDS + SL_ROW_WORDS;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(blocks_for(per_chunk * chunks, 256));
-    cfg.blockDim = dim3(256);
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1] = {pdl_attr()};
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    ProfScope ps("level_chunks", s);
-    BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, level_chunks_kernel, lv, static_cast<int>(cols), static_cast<int>(tokens),
-                                      static_cast<int>(chunks), LC));
-    BITMM_TRY(launch_check("level_chunks_kernel"));
-  }
+  // the level chunks are staged by the expansion launch, in a grid row of their own
+  const LevelChunkJob lc{lv, static_cast<int>(cols), static_cast<int>(tokens), static_cast<int>(chunks), LC};
+  BITMM_TRY(run_unpack_pair(sa, sb, wpr, cols, kpad, A8, B8, st.status, s, true, &lc));
   CUtensorMap ta, tb, tc;
   const int64_t rb = kpad / 2;
   BITMM_TRY(make_operand_map(&ta, A8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, rb, rows, 128));

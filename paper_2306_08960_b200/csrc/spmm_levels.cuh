@@ -20,11 +20,10 @@
 #pragma once
 
 #include "apb_gemm.cuh"
+#include "levels.cuh"
 
 namespace bitmm_dev {
 
-constexpr int SL_TOK = 64;                   // tokens per block
-constexpr int SL_ROW_WORDS = SL_TOK / 2;     // u32 words per staged column (two bf16 levels each)
 #ifndef SL_THREADS_CFG  // profiling builds sweep these (profiles/dev/ab_spmm_levels.py)
 #define SL_THREADS_CFG 768
 #endif
@@ -66,45 +65,6 @@ __device__ __forceinline__ unsigned long long f32x2_add(unsigned long long a, un
   return r;
 }
 
-// bf16 bit pattern of the level p = 2 hi + lo (0, 1.0, 2.0, 3.0)
-__device__ __forceinline__ unsigned level_bf16(bool lo, bool hi) {
-  return hi ? (lo ? 0x4040u : 0x4000u) : (lo ? 0x3F80u : 0u);
-}
-
-// One staging item of the level chunk of tokens [c0, c0 + SL_TOK): (64-bit plane word, half of
-// it, token pair) -> 32 words of xw [K + 1][SL_ROW_WORDS] (two bf16 levels each). p = 2 (t|h) +
-// (t | ~(h|m)) (decompose_thm states, transform.cpp:56-71); bits past K are never staged,
-// tokens past N stage level 0.
-__device__ __forceinline__ void sl_stage_item(unsigned* xw, int K, int N, int c0, const SpmmLevels& lv, int i) {
-  const int pair = i & (SL_ROW_WORDS - 1), hw = i / SL_ROW_WORDS;
-  const int word = hw >> 1, half = hw & 1;
-  const int ta = c0 + 2 * pair;
-  unsigned loA = 0, hiA = 0, loB = 0, hiB = 0;
-  if (ta < N) {
-    const long long o = static_cast<long long>(ta) * lv.wpr + word;
-    const unsigned long long t = lv.t[o], h = lv.h[o], m = lv.m[o];
-    hiA = static_cast<unsigned>((t | h) >> (32 * half));
-    loA = static_cast<unsigned>((t | ~(h | m)) >> (32 * half));
-  }
-  if (ta + 1 < N) {
-    const long long o = static_cast<long long>(ta + 1) * lv.wpr + word;
-    const unsigned long long t = lv.t[o], h = lv.h[o], m = lv.m[o];
-    hiB = static_cast<unsigned>((t | h) >> (32 * half));
-    loB = static_cast<unsigned>((t | ~(h | m)) >> (32 * half));
-  }
-  const int k0 = word * 64 + half * 32;
-  unsigned* dst = &xw[static_cast<long long>(k0) * SL_ROW_WORDS + pair];
-  if (k0 + 32 <= K) {
-#pragma unroll
-    for (int b = 0; b < 32; ++b)
-      dst[b * SL_ROW_WORDS] = level_bf16((loA >> b) & 1u, (hiA >> b) & 1u) |
-                              (level_bf16((loB >> b) & 1u, (hiB >> b) & 1u) << 16);
-  } else {
-    for (int b = 0; b < K - k0; ++b)
-      dst[b * SL_ROW_WORDS] = level_bf16((loA >> b) & 1u, (hiA >> b) & 1u) |
-                              (level_bf16((loB >> b) & 1u, (hiB >> b) & 1u) << 16);
-  }
-}
 
 // The whole chunk (rows [0, K) plus the zero row K), by threads tid of nthreads. Each store
 // instruction of a warp writes one whole 128-byte column row.
@@ -113,25 +73,6 @@ __device__ __forceinline__ void sl_stage(unsigned* xw, int K, int N, int c0, con
   if (tid < SL_ROW_WORDS) xw[K * SL_ROW_WORDS + tid] = 0u;
   const int items = ((K + 63) >> 6) * 2 * SL_ROW_WORDS;
   for (int i = tid; i < items; i += nthreads) sl_stage_item(xw, K, N, c0, lv, i);
-}
-
-// Every chunk of the activations, staged once into global memory (L2-resident: tokens x (K + 1)
-// x 2 bytes) for the fused layer, which bulk-copies a chunk into shared memory when its tile
-// range reaches it: out [chunks][K + 1][SL_ROW_WORDS]. One thread per (chunk, item).
-__global__ void __launch_bounds__(256) level_chunks_kernel(const SpmmLevels lv, int K, int N, int chunks,
-                                                           unsigned* __restrict__ out) {
-  pdl_wait();  // the previous layer call's fused kernel may still read `out`
-  pdl_launch_dependents();
-  const int items = ((K + 63) >> 6) * 2 * SL_ROW_WORDS;
-  const long long per_chunk = items + SL_ROW_WORDS;  // + the zero row
-  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= per_chunk * chunks) return;
-  const int chunk = static_cast<int>(i / per_chunk), j = static_cast<int>(i - chunk * per_chunk);
-  unsigned* xw = out + static_cast<long long>(chunk) * (K + 1) * SL_ROW_WORDS;
-  if (j < items)
-    sl_stage_item(xw, K, N, chunk * SL_TOK, lv, j);
-  else
-    xw[static_cast<long long>(K) * SL_ROW_WORDS + (j - items)] = 0u;
 }
 
 // One octet's view of a staged chunk: lane `ol` of the octet owns tokens [8 ol, 8 ol + 8).

@@ -25,6 +25,7 @@
 #include <cuda_fp16.h>
 #include <cstdint>
 
+#include "levels.cuh"
 #include "ptx.cuh"
 
 namespace bitmm_dev {
@@ -61,7 +62,8 @@ struct UnpackSet {
   UnpackOperand op[UNPACK_MAX_OPS];
   int count;
   int* err;
-  int fp4;  // 1: packed e2m1 nibbles, rows of kpad/2 bytes (Kind::F4 operands)
+  int fp4;          // 1: packed e2m1 nibbles, rows of kpad/2 bytes (Kind::F4 operands)
+  LevelChunkJob lc;  // the fused 2-bit APB layer's level chunks (grid row y = count), if any
 };
 
 // One warp expands one 4096-element slice of one operand row (128 input words, 4 KB of
@@ -254,6 +256,11 @@ __device__ __forceinline__ int unpack_slice_warp(const UnpackOperand& o, long lo
 __global__ void __launch_bounds__(256) unpack_operands(const __grid_constant__ UnpackSet P) {
   pdl_wait();
   pdl_launch_dependents();
+  if (static_cast<int>(blockIdx.y) == P.count) {  // level chunks, beside the operand expansion
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < level_chunk_items(P.lc)) level_chunk_item(P.lc, i);
+    return;
+  }
   const UnpackOperand& o = P.op[blockIdx.y];
   const long long unit = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
