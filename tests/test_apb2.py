@@ -175,7 +175,7 @@ def test_gpu_device_path_config4_shape(orc):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("form", ["fused", "two-pass", "two-pass-fp32"])
-@pytest.mark.parametrize("rows,cols,tokens", [(300, 768, 332), (513, 130, 1000), (257, 960, 64),
+@pytest.mark.parametrize("rows,cols,tokens", [(300, 768, 332), (513, 130, 1000), (257, 973, 64), (33, 974, 8),
                                               (64, 1100, 68), (1000, 256, 4)])
 def test_gpu_every_form_bit_exact(orc, monkeypatch, form, rows, cols, tokens):
     """The three device forms of the layer — residual fused into the GEMM epilogue
@@ -183,6 +183,24 @@ def test_gpu_every_form_bit_exact(orc, monkeypatch, form, rows, cols, tokens):
     fp32-level SpMM (spmm_xchunk_kernel<LEVELS>) — each bit-identical to the oracle, at shapes
     with ragged row blocks, token blocks and K (cols 1100 exceeds the fused kernel's shared
     memory and falls back to the two-pass form)."""
+    from paper_2306_08960_b200 import _lib
+    lib = _lib.load()
     monkeypatch.setenv("BITMM_APB2_FUSED", "1" if form == "fused" else "0")
     monkeypatch.setenv("BITMM_SPMM_LEVELS_V1", "1" if form == "two-pass-fp32" else "0")
-    _gpu_vs_oracle(orc, rows, cols, tokens, seed=3)
+    lib.bitmm_profile_reset()
+    lib.bitmm_profile_enable(1)
+    try:
+        _gpu_vs_oracle(orc, rows, cols, tokens, seed=3)
+        assert lib.bitmm_profile_collect() == 0
+        ran = {lib.bitmm_profile_kernel_name(i).decode() for i in range(lib.bitmm_profile_kernel_count())
+               if lib.bitmm_profile_kernel_launches(i) > 0}
+    finally:
+        lib.bitmm_profile_enable(0)
+        lib.bitmm_profile_reset()
+    # the form the switches and the shape select is the one that ran
+    if form == "fused" and cols <= 973:
+        assert "apb2_fused" in ran, ran
+    elif form == "two-pass-fp32":
+        assert "apb2_fused" not in ran and "spmm_levels" not in ran, ran
+    else:
+        assert "apb2_fused" not in ran and "spmm_levels" in ran, ran
