@@ -12,7 +12,7 @@ import torch
 sys.path.insert(0, ".")
 from paper_2306_08960_b200 import _lib, api, data  # noqa: E402
 
-os.environ["BITMM_APB2_FUSED"] = "0"
+os.environ["BITMM_APB2_FUSED"] = os.environ.get("AB_FUSED", "0")  # AB_FUSED=1: time the fused form
 rng = np.random.default_rng(7)
 rows, cols, tokens = 3072, 768, 8192
 a, alpha, _ = data.apb_weights(rng, rows, cols)
