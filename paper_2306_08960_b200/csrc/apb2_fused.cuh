@@ -274,15 +274,19 @@ __global__ void __launch_bounds__(A3_THREADS, 1)
     struct Row {
       unsigned long long lo, hi;
     };
-    auto load_rp = [&](int tile, int pass) {
+    // tile coordinates advance incrementally (no integer division in the loop)
+    auto advance = [&](int& nb, int& mb) {
+      if (++mb == nmb) {
+        mb = 0;
+        ++nb;
+      }
+    };
+    auto load_rp = [&](bool valid, int mb, int pass) {
       Row x{0, 0};
-      if (tile < t1) {
-        const int nb = tile / nmb, mb = tile - nb * nmb;
-        const int r = mb * 256 + static_cast<int>(rank) * 128 + oct + 64 * pass;
-        if (r < p.M) {
-          x.lo = ap.row_ptr[r];
-          x.hi = ap.row_ptr[r + 1];
-        }
+      const int r = mb * 256 + static_cast<int>(rank) * 128 + oct + 64 * pass;
+      if (valid && r < p.M) {
+        x.lo = ap.row_ptr[r];
+        x.hi = ap.row_ptr[r + 1];
       }
       return x;
     };
@@ -294,8 +298,14 @@ __global__ void __launch_bounds__(A3_THREADS, 1)
         vv = ap.vals[e0 + idx];
       }
     };
-    Row ra = load_rp(t0, 0), rb = load_rp(t0, 1);
-    Row ra1 = load_rp(t0 + 1, 0), rb1 = load_rp(t0 + 1, 1);
+    int nbc = t0 / nmb, mbc = t0 - (t0 / nmb) * nmb;  // tile t0 + it
+    int nb2 = nbc, mb2 = mbc;                          // tile t0 + it + 2
+    int nb1 = nbc, mb1 = mbc;
+    advance(nb1, mb1);
+    advance(nb2, mb2);
+    advance(nb2, mb2);
+    Row ra = load_rp(t0 < t1, mbc, 0), rb = load_rp(t0 < t1, mbc, 1);
+    Row ra1 = load_rp(t0 + 1 < t1, mb1, 0), rb1 = load_rp(t0 + 1 < t1, mb1, 1);
     unsigned na = static_cast<unsigned>(ra.hi - ra.lo), nb_ = static_cast<unsigned>(rb.hi - rb.lo);
     unsigned ka0, ka1, kb0, kb1;
     float va0, va1, vb0, vb1;
@@ -311,7 +321,7 @@ __global__ void __launch_bounds__(A3_THREADS, 1)
     A3_T(s_begin);
 #endif
     for (int tile = t0; tile < t1; ++tile, ++it) {
-      const int nb = tile / nmb;
+      const int nb = nbc;
       A3_T(p0);
       const int b = it & 1;
       const uint32_t ph = (it >> 1) & 1;
@@ -329,7 +339,9 @@ __global__ void __launch_bounds__(A3_THREADS, 1)
         cur_nb = nb;
       }
       A3_T(p1);
-      const Row ra2 = load_rp(tile + 2, 0), rb2 = load_rp(tile + 2, 1);
+      const Row ra2 = load_rp(tile + 2 < t1, mb2, 0), rb2 = load_rp(tile + 2 < t1, mb2, 1);
+      advance(nbc, mbc);
+      advance(nb2, mb2);
       const unsigned na1 = static_cast<unsigned>(ra1.hi - ra1.lo), nb1 = static_cast<unsigned>(rb1.hi - rb1.lo);
       unsigned nka0, nka1, nkb0, nkb1;
       float nva0, nva1, nvb0, nvb1;
