@@ -63,7 +63,7 @@ struct UnpackSet {
   int count;
   int* err;
   int fp4;          // 1: packed e2m1 nibbles, rows of kpad/2 bytes (Kind::F4 operands)
-  LevelChunkJob lc;  // the fused 2-bit APB layer's level chunks (grid row y = count), if any
+  LevelChunkJob lc;  // the fused 2-bit APB layer's level chunks (grid row 0), if any
 };
 
 // One warp expands one 4096-element slice of one operand row (128 input words, 4 KB of
@@ -256,12 +256,15 @@ __device__ __forceinline__ int unpack_slice_warp(const UnpackOperand& o, long lo
 __global__ void __launch_bounds__(256) unpack_operands(const __grid_constant__ UnpackSet P) {
   pdl_wait();
   pdl_launch_dependents();
-  if (static_cast<int>(blockIdx.y) == P.count) {  // level chunks, beside the operand expansion
+  // Grid row 0 holds the level chunks when there are any (scheduled first, so they overlap the
+  // operand rows instead of trailing them); the operands follow.
+  const int y = static_cast<int>(blockIdx.y) - (P.lc.chunks > 0 ? 1 : 0);
+  if (y < 0) {
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < level_chunk_items(P.lc)) level_chunk_item(P.lc, i);
     return;
   }
-  const UnpackOperand& o = P.op[blockIdx.y];
+  const UnpackOperand& o = P.op[y];
   const long long unit = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const long long slices = o.groups_per_row;  // slices of 128 words per row
