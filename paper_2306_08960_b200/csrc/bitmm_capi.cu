@@ -1452,18 +1452,22 @@ int64_t spmm_levels_work(const Ctx& st, int64_t rows, int64_t n, int* blocks) {
   return (total + *blocks - 1) / *blocks;
 }
 
-bool spmm_levels_fits(const Ctx& st, int64_t rows, int64_t k, int64_t n) {
+bool spmm_levels_fits(const Ctx& st, int64_t rows, int64_t k, int64_t n, bool f32 = false) {
   int blocks;
   const int64_t w = spmm_levels_work(st, rows, n, &blocks);
-  return w < (1 << 30) && spmm_levels_smem_bytes(k, static_cast<int>(std::min<int64_t>(w, rows))) <= kMaxDynSmem;
+  return w < (1 << 30) &&
+         spmm_levels_smem_bytes(k, static_cast<int>(std::min<int64_t>(w, rows)), f32) <= kMaxDynSmem;
 }
 
+// x != nullptr: the standalone exact spmm_csr over the fp32 X [k][ldx] (C = R.X, no binary part).
 int run_spmm_levels(Ctx& st, int64_t rows, int64_t k, const uint64_t* row_ptr, const uint64_t* col_idx,
-                    const float* vals, const SpmmLevels& lv, int64_t n, float* c, int64_t ldc, cudaStream_t s) {
+                    const float* vals, const SpmmLevels& lv, int64_t n, float* c, int64_t ldc, cudaStream_t s,
+                    const float* x = nullptr, int64_t ldx = 0) {
   int blocks;
   const int64_t w = spmm_levels_work(st, rows, n, &blocks);
-  auto kern = spmm_levels_kernel<true>;
-  const int smem = spmm_levels_smem_bytes(k, static_cast<int>(std::min<int64_t>(w, rows)));
+  const bool f32 = x != nullptr;
+  auto kern = f32 ? spmm_levels_kernel<false, true> : spmm_levels_kernel<true, false>;
+  const int smem = spmm_levels_smem_bytes(k, static_cast<int>(std::min<int64_t>(w, rows)), f32);
   BITMM_TRY(ensure_max_smem(reinterpret_cast<const void*>(kern), kMaxDynSmem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(blocks));
@@ -1472,12 +1476,13 @@ int run_spmm_levels(Ctx& st, int64_t rows, int64_t k, const uint64_t* row_ptr, c
   cfg.stream = s;
   cudaLaunchAttribute attr[1] = {pdl_attr()};
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  ProfScope ps("spmm_levels", s);
+  cfg.numAttrs = f32 ? 0 : 1;  // the layer's pass chains after its GEMM; spmm_csr stands alone
+  ProfScope ps(f32 ? "spmm_f32_exact" : "spmm_levels", s);
   BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, static_cast<int>(rows), static_cast<int>(k), static_cast<int>(n),
                                     reinterpret_cast<const unsigned long long*>(row_ptr),
                                     reinterpret_cast<const unsigned long long*>(col_idx), vals, lv, c,
-                                    static_cast<long long>(ldc), static_cast<long long>(w)));
+                                    static_cast<long long>(ldc), static_cast<long long>(w), x,
+                                    static_cast<long long>(ldx)));
   return launch_check("spmm_levels_kernel");
 }
 
@@ -2368,6 +2373,10 @@ int bitmm_spmm_csr_dev(int64_t rows, int64_t cols, const uint64_t* row_ptr, cons
   if (!row_ptr || !b || !c) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
   CallCtx st;
   BITMM_TRY(st.acquire(static_cast<cudaStream_t>(stream)));
+  const char* v1 = std::getenv("BITMM_SPMM_V1");  // A/B: the 32-token fp32 chunk kernel
+  if (!(v1 && std::atoi(v1) != 0) && spmm_levels_fits(*st, rows, cols, n, true))
+    return run_spmm_levels(*st, rows, cols, row_ptr, col_idx, vals, SpmmLevels{}, n, c, ldc,
+                           static_cast<cudaStream_t>(stream), b, ldb);
   return run_spmm<true, false>(*st, rows, cols, row_ptr, col_idx, vals, b, n, ldb, c, ldc,
                                static_cast<cudaStream_t>(stream));
 }

@@ -39,8 +39,8 @@ constexpr int SL_OCTETS = SL_THREADS / 8;    // rows in flight per block
 
 // Dynamic smem: the level chunk [K + 1][SL_TOK] bf16 (row K is zero: the target of padded
 // nonzeros), then the block's row offsets (u32).
-inline int spmm_levels_smem_bytes(long long K, int rows_per_split) {
-  return static_cast<int>((K + 1) * SL_ROW_WORDS * 4 + (rows_per_split + 1) * 4);
+inline int spmm_levels_smem_bytes(long long K, int rows_per_split, bool f32 = false) {
+  return static_cast<int>((K + 1) * (f32 ? SL_TOK * 4 : SL_ROW_WORDS * 4) + (rows_per_split + 1) * 4);
 }
 
 __device__ __forceinline__ unsigned long long f32x2_pack(float lo, float hi) {
@@ -133,21 +133,45 @@ __device__ __forceinline__ void sl_step8x2(const SlOctet& o, unsigned kka, float
   }
 }
 
+// sl_step8 over an fp32 chunk [K + 1][SL_TOK] (the standalone spmm_csr): lane l of the octet owns
+// tokens [4 l, 4 l + 4) and [32 + 4 l, 32 + 4 l + 4), so each of its two 16-byte loads is part of
+// one contiguous 128-byte octet read. acc[0..1] = the first four tokens, acc[2..3] the second.
+__device__ __forceinline__ void sl_step8_f32(const SlOctet& o, unsigned kk, float vv, unsigned long long (&acc)[4]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const unsigned koff = __shfl_sync(0xFFFFFFFFu, kk, o.obase + j) * (SL_TOK * 4);
+    const float v = __shfl_sync(0xFFFFFFFFu, vv, o.obase + j);
+    const uint4 x0 = *reinterpret_cast<const uint4*>(o.xrow + koff);
+    const uint4 x1 = *reinterpret_cast<const uint4*>(o.xrow + koff + 128);
+    const unsigned long long v2 = f32x2_pack(v, v);
+    const unsigned long long xs[4] = {f32x2_pack(__uint_as_float(x0.x), __uint_as_float(x0.y)),
+                                      f32x2_pack(__uint_as_float(x0.z), __uint_as_float(x0.w)),
+                                      f32x2_pack(__uint_as_float(x1.x), __uint_as_float(x1.y)),
+                                      f32x2_pack(__uint_as_float(x1.z), __uint_as_float(x1.w))};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q] = f32x2_add(acc[q], f32x2_mul(v2, xs[q], o.z));  // fl(S + fl(v x))
+  }
+}
+
 // Persistent: gridDim.x = blocks resident at once (SL_BLOCKS_PER_SM per SM), block b owns the contiguous
 // range [b W, (b + 1) W) of the (token chunk, row) work space in chunk-major order, so every block
 // gets the same number of rows (no partial last wave) and restages only when its range crosses
 // into the next chunk (at most twice).
-template <bool PDL_CHAIN>
+// F32: the standalone exact spmm_csr (kernels.cpp:334-352) over an fp32 X [K][ldx]: the chunk is
+// [K + 1][SL_TOK] fp32 (cp.async), products fl(v * x), and C = S is stored (no binary part).
+template <bool PDL_CHAIN, bool F32 = false>
 __global__ void __launch_bounds__(SL_THREADS, SL_BLOCKS_PER_SM)
     spmm_levels_kernel(int rows, int K, int N, const unsigned long long* __restrict__ row_ptr,
                        const unsigned long long* __restrict__ col_idx, const float* __restrict__ vals,
-                       const SpmmLevels lv, float* __restrict__ C, long long ldc, long long work_per_block) {
-  extern __shared__ unsigned xw[];  // [K + 1][SL_ROW_WORDS], then u32 row offsets
+                       const SpmmLevels lv, float* __restrict__ C, long long ldc, long long work_per_block,
+                       const float* __restrict__ X = nullptr, long long ldx = 0) {
+  extern __shared__ unsigned xw[];  // [K + 1][SL_ROW_WORDS] (F32: [K + 1][SL_TOK]), then u32 row offsets
+  constexpr int ROW_WORDS = F32 ? SL_TOK : SL_ROW_WORDS;
   if (PDL_CHAIN) {
     pdl_wait();  // C holds the GEMM's binary part
     pdl_launch_dependents();
   }
-  unsigned* rps = xw + static_cast<long long>(K + 1) * SL_ROW_WORDS;
+  unsigned* rps = xw + static_cast<long long>(K + 1) * ROW_WORDS;
   const long long chunks = (N + SL_TOK - 1) / SL_TOK;
   const long long total = chunks * rows;
   long long lo = blockIdx.x * work_per_block;
@@ -161,7 +185,25 @@ __global__ void __launch_bounds__(SL_THREADS, SL_BLOCKS_PER_SM)
     lo = seg_end;
     __syncthreads();  // the previous segment's rows are done with the chunk and the offsets
 
-    sl_stage(xw, K, N, c0, lv, threadIdx.x, SL_THREADS);
+    if constexpr (F32) {
+      // X rows [0, K) of the chunk: every 16-byte piece in flight at once, zero past N
+      const bool xvec = ((ldx & 3) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+      float* xf = reinterpret_cast<float*>(xw);
+      if (threadIdx.x < SL_TOK) xf[static_cast<long long>(K) * SL_TOK + threadIdx.x] = 0.f;
+      for (int i = threadIdx.x; i < K * (SL_TOK / 4); i += SL_THREADS) {
+        const int k = i / (SL_TOK / 4), q = (i % (SL_TOK / 4)) * 4;
+        const float* src = X + static_cast<long long>(k) * ldx + c0 + q;
+        float* dst = &xf[static_cast<long long>(k) * SL_TOK + q];
+        if (xvec && c0 + q + 3 < N) {
+          cp_async16(dst, src);
+        } else {
+          for (int e = 0; e < 4; ++e) dst[e] = (c0 + q + e < N) ? src[e] : 0.f;
+        }
+      }
+      cp_async_wait_all();
+    } else {
+      sl_stage(xw, K, N, c0, lv, threadIdx.x, SL_THREADS);
+    }
     const unsigned long long nz0 = row_ptr[r0];
     for (int i = threadIdx.x; i <= r1 - r0; i += SL_THREADS) rps[i] = static_cast<unsigned>(row_ptr[r0 + i] - nz0);
     __syncthreads();
@@ -178,6 +220,12 @@ __global__ void __launch_bounds__(SL_THREADS, SL_BLOCKS_PER_SM)
     const unsigned zero_row = static_cast<unsigned>(K);
     const SlOctet so{reinterpret_cast<const char*>(xw) + ol * 16, obase, f32x2_pack(lv.d1, lv.d1),
                      f32x2_pack(lv.neg_zero, lv.neg_zero)};
+    auto step = [&](unsigned kk, float vv, unsigned long long (&acc)[4]) {
+      if constexpr (F32)
+        sl_step8_f32(so, kk, vv, acc);
+      else
+        sl_step8(so, kk, vv, acc);
+    };
     auto fetch = [&](unsigned i0, unsigned n, unsigned idx, unsigned& kk, float& vv) {
       kk = zero_row;
       vv = 0.f;
@@ -225,17 +273,35 @@ __global__ void __launch_bounds__(SL_THREADS, SL_BLOCKS_PER_SM)
             if (col + e < N) g[e] = dst[e];
         }
       };
-      if (SL_CPREF && live) load_g();
+      if (!F32 && SL_CPREF && live) load_g();
       unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};  // +0 pairs
-      if (nmax > 0) sl_step8(so, kk0, vv0, acc);
-      if (nmax > 8) sl_step8(so, kk1, vv1, acc);
+      if (nmax > 0) step(kk0, vv0, acc);
+      if (nmax > 8) step(kk1, vv1, acc);
       for (unsigned base = 16; base < nmax; base += 8) {
         unsigned kk;
         float vv;
         fetch(i0, n, base + ol, kk, vv);
-        sl_step8(so, kk, vv, acc);
+        step(kk, vv, acc);
       }
-      if (live) {
+      if (F32 && live) {
+        // C = S: tokens [4 ol, +4) and [32 + 4 ol, +4) of the chunk
+        const float* af = reinterpret_cast<const float*>(acc);
+        float* d0 = C + static_cast<long long>(r) * ldc + c0 + ol * 4;
+        float* d1 = d0 + 32;
+        const bool v0 = ((ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
+        if (v0 && c0 + ol * 4 + 3 < N) {
+          *reinterpret_cast<float4*>(d0) = make_float4(af[0], af[1], af[2], af[3]);
+        } else {
+          for (int e = 0; e < 4; ++e)
+            if (c0 + ol * 4 + e < N) d0[e] = af[e];
+        }
+        if (v0 && c0 + 32 + ol * 4 + 3 < N) {
+          *reinterpret_cast<float4*>(d1) = make_float4(af[4], af[5], af[6], af[7]);
+        } else {
+          for (int e = 0; e < 4; ++e)
+            if (c0 + 32 + ol * 4 + e < N) d1[e] = af[4 + e];
+        }
+      } else if (live) {
         if (!SL_CPREF) load_g();
         // C = fl(G + S) (apb.cpp:161-162)
         unsigned long long o[4];

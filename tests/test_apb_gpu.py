@@ -165,10 +165,15 @@ def test_large_k_layer_forward(orc, k, fold, monkeypatch):
     check_close(got, want)
 
 
-def test_spmm_exact_odd_shapes(orc):
-    # ragged columns (N % 4 != 0), empty rows, rows with > 8 nonzeros, single column
+@pytest.mark.parametrize("v1", ["0", "1"])
+def test_spmm_exact_odd_shapes(orc, monkeypatch, v1):
+    # ragged columns (N % 4 != 0), empty rows, rows with > 8 nonzeros, single column, K past the
+    # 64-token kernel's shared memory (1000) — through the 64-token persistent kernel and the
+    # 32-token chunk kernel (BITMM_SPMM_V1=1)
+    monkeypatch.setenv("BITMM_SPMM_V1", v1)
     rng = np.random.default_rng(99)
-    for (rows, cols, n) in [(5, 3, 1), (33, 700, 37), (7, 64, 130), (300, 50, 33)]:
+    for (rows, cols, n) in [(5, 3, 1), (33, 700, 37), (7, 64, 130), (300, 50, 33), (70, 1000, 200),
+                            (129, 864, 64)]:
         dens = rng.uniform(0.0, 0.6)
         mask = rng.random((rows, cols)) < dens
         mask[0] = False  # an empty row
