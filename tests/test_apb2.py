@@ -204,3 +204,54 @@ def test_gpu_every_form_bit_exact(orc, monkeypatch, form, rows, cols, tokens):
         assert "apb2_fused" not in ran and "spmm_levels" not in ran, ran
     else:
         assert "apb2_fused" not in ran and "spmm_levels" in ran, ran
+
+
+@pytest.mark.gpu
+def test_gpu_fused_repeated_and_concurrent(orc):
+    """The fused kernel's pipeline (TMA/MMA/epilogue/residual handshakes, level reloads at token
+    block changes) under repetition and concurrency: two host threads on two streams run layers of
+    different shapes 40 times each; every result must equal the oracle's bit for bit."""
+    import threading
+
+    import torch
+    from paper_2306_08960_b200 import device
+    shapes = [(300, 768, 332), (1000, 960, 1000)]
+    cases = []
+    for i, (rows, cols, tokens) in enumerate(shapes):
+        rng = np.random.default_rng(100 + i)
+        layer, alpha = _layer(rng, rows, cols)
+        t, h, m, wpr = _planes(rng, tokens, cols)
+        rr = layer.residual
+        want = orc.layer_forward_2bit(rows, cols, 1.0, layer.bin.words, wpr, rr.row_ptr, rr.col_idx, rr.vals,
+                                      t, h, m, a_scale=0.75, row_alpha=alpha)
+        T = lambda v: torch.from_numpy(np.ascontiguousarray(v)).cuda()  # noqa: E731
+        d = [T(layer.bin.words.view(np.int64)), T(alpha), T(rr.row_ptr.view(np.int64)),
+             T(rr.col_idx.view(np.int64)), T(rr.vals), T(t.view(np.int64)), T(h.view(np.int64)),
+             T(m.view(np.int64))]
+        cases.append((rows, cols, tokens, d, want))
+    errors = []
+
+    def worker(ci):
+        rows, cols, tokens, d, want = cases[ci]
+        stream = torch.cuda.Stream()
+        try:
+            with torch.cuda.stream(stream):
+                out = torch.empty((rows, tokens), dtype=torch.float32, device="cuda")
+                for _ in range(40):
+                    out.fill_(float("nan"))
+                    device.layer_forward_2bit(d[0], cols, d[1], d[2], d[3], d[4], d[5], d[6], d[7], out,
+                                              a_scale=0.75, stream=stream)
+                    device.status(stream)
+                    if not np.array_equal(out.cpu().numpy(), want):
+                        errors.append(ci)
+                        return
+        except Exception as e:  # pragma: no cover
+            errors.append((ci, repr(e)))
+
+    threads = [threading.Thread(target=worker, args=(i,)) for i in range(len(cases))]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join(timeout=600)
+    assert not any(th.is_alive() for th in threads), "a worker hung"
+    assert not errors, errors
