@@ -204,6 +204,26 @@ typedef struct bitmm_gemm_item {
 } bitmm_gemm_item;
 int bitmm_gemm_batch_dev(const bitmm_gemm_item* items, int count, void* stream);
 
+/* ---- Late-output host call: the drop-in's per-call latency (gemm_1x1 / 1x2 / 2x2 returning a
+ * fresh DenseMatrix, kernels.cpp:163-275) ----
+ * The *_host call of one item (host pointers in a0..b2 and the optional row / column scales;
+ * its c_units, c and ldc are ignored) whose output buffers are supplied AFTER the call's copies
+ * and kernels are enqueued: the library calls out_fn(user, &out) once, while the device works,
+ * and writes the result into out.c_units and / or out.c (row-major, out.ldc >= n; preset to n)
+ * as `want` asks. A reference wrapper constructs its zero-filled DenseMatrix inside out_fn, so
+ * the allocation overlaps the GEMM instead of preceding it. out_fn is not called when the call
+ * fails before anything is enqueued; a non-zero return from it fails the call with
+ * BITMM_ERR_INVALID_ARGUMENT. A device-detected error (encoding, padding) is reported before
+ * any output byte is written. Results are identical to the matching *_host call. */
+enum { BITMM_WANT_UNITS = 1, BITMM_WANT_C = 2 };
+typedef struct bitmm_host_out {
+  int32_t* c_units;
+  float* c;
+  int64_t ldc;
+} bitmm_host_out;
+typedef int (*bitmm_out_fn)(void* user, bitmm_host_out* out);
+int bitmm_gemm_host_late(const bitmm_gemm_item* item, int want, bitmm_out_fn out_fn, void* user);
+
 /* ---- Row ops, batched (kernels.hpp:29-38, kernels.cpp:120-140) ----
  * count independent row pairs of `words` u64 each, rows contiguous:
  *   dot_binary: out[r] = n - 2*popc(u_r ^ v_r)   (n: logical length, words_for(n) <= words)

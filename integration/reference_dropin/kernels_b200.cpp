@@ -13,6 +13,7 @@
 // Build recipe (see INTEGRATION.md and oracle/Makefile target `dropin`): compile the
 // reference sources unmodified, weaken the nine replaced symbols in their objects
 // (objcopy --weaken-symbol), link this file plus libbitmm_b200.so.
+#include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -126,16 +127,49 @@ std::int64_t mbm(std::span<const std::uint64_t> x, std::span<const std::uint64_t
 }
 #endif
 
+// The three GEMMs return a fresh DenseMatrix (kernels.cpp:163-275). The binding hands the
+// library a callback that constructs it (the reference's zero-filling constructor) once the
+// call's copies and kernels are enqueued, so that allocation overlaps the device work
+// (bitmm_gemm_host_late); the result is then copied straight into it.
+namespace {
+
+struct LateDense {
+  std::int64_t rows, cols;
+  std::optional<DenseMatrix> c;
+};
+
+int make_late_dense(void* user, bitmm_host_out* out) {
+  auto* l = static_cast<LateDense*>(user);
+  l->c.emplace(l->rows, l->cols);
+  out->c = l->c->row_data(0);
+  out->ldc = l->cols;
+  return 0;
+}
+
+DenseMatrix run_late(const bitmm_gemm_item& it) {
+  LateDense l{it.m, it.n, std::nullopt};
+  raise_on(bitmm_gemm_host_late(&it, BITMM_WANT_C, &make_late_dense, &l));
+  return std::move(*l.c);
+}
+
+}  // namespace
+
 DenseMatrix gemm_1x1(const BitMatrix& a, const BitMatrix& b_packed, float gamma_a, float gamma_b,
                      int threads) {
   check_packed_pair(a.cols(), a.words_per_row(), b_packed.cols(), b_packed.words_per_row());
   GemmProblem{a.rows(), a.cols(), b_packed.rows()}.validate();
   check_threads(threads);
-  DenseMatrix c(a.rows(), b_packed.rows());
-  raise_on(bitmm_gemm_1x1_host(a.row_data(0), a.rows(), b_packed.row_data(0), b_packed.rows(),
-                               a.cols(), static_cast<std::int64_t>(a.words_per_row()), gamma_a,
-                               gamma_b, nullptr, c.row_data(0), c.cols()));
-  return c;
+  bitmm_gemm_item it{};
+  it.routine = BITMM_ROUTINE_1X1;
+  it.a0 = a.row_data(0);
+  it.b0 = b_packed.row_data(0);
+  it.m = a.rows();
+  it.n = b_packed.rows();
+  it.k = a.cols();
+  it.wpr = static_cast<std::int64_t>(a.words_per_row());
+  it.a_scale = gamma_a;
+  it.b_scale = gamma_b;
+  return run_late(it);
 }
 
 DenseMatrix gemm_1x2(const BitMatrix& w, float gamma, const ThmPlanes& a_packed, int threads) {
@@ -143,14 +177,21 @@ DenseMatrix gemm_1x2(const BitMatrix& w, float gamma, const ThmPlanes& a_packed,
   check_packed_pair(w.cols(), w.words_per_row(), a_packed.cols(), a_packed.t.words_per_row());
   GemmProblem{w.rows(), w.cols(), a_packed.rows()}.validate();
   check_threads(threads);
-  DenseMatrix c(w.rows(), a_packed.rows());
-  raise_on(bitmm_gemm_1x2_host(w.row_data(0), w.rows(), gamma, a_packed.t.row_data(0),
-                               a_packed.h.row_data(0), a_packed.m.row_data(0), a_packed.rows(),
-                               w.cols(), static_cast<std::int64_t>(w.words_per_row()),
-                               a_packed.scale, a_packed.gamma.has_value() ? 1 : 0,
-                               plane_gamma(a_packed), nullptr, nullptr, nullptr, c.row_data(0),
-                               c.cols()));
-  return c;
+  bitmm_gemm_item it{};
+  it.routine = BITMM_ROUTINE_1X2;
+  it.a0 = w.row_data(0);
+  it.b0 = a_packed.t.row_data(0);
+  it.b1 = a_packed.h.row_data(0);
+  it.b2 = a_packed.m.row_data(0);
+  it.m = w.rows();
+  it.n = a_packed.rows();
+  it.k = w.cols();
+  it.wpr = static_cast<std::int64_t>(w.words_per_row());
+  it.a_scale = gamma;
+  it.b_scale = a_packed.scale;
+  it.has_b_gamma = a_packed.gamma.has_value() ? 1 : 0;
+  it.b_gamma = plane_gamma(a_packed);
+  return run_late(it);
 }
 
 DenseMatrix gemm_2x2(const ThmPlanes& w, const ThmPlanes& a_packed, int threads) {
@@ -159,15 +200,25 @@ DenseMatrix gemm_2x2(const ThmPlanes& w, const ThmPlanes& a_packed, int threads)
   check_packed_pair(w.cols(), w.t.words_per_row(), a_packed.cols(), a_packed.t.words_per_row());
   GemmProblem{w.rows(), w.cols(), a_packed.rows()}.validate();
   check_threads(threads);
-  DenseMatrix c(w.rows(), a_packed.rows());
-  raise_on(bitmm_gemm_2x2_host(
-      w.t.row_data(0), w.h.row_data(0), w.m.row_data(0), w.rows(), w.scale,
-      w.gamma.has_value() ? 1 : 0, plane_gamma(w), a_packed.t.row_data(0), a_packed.h.row_data(0),
-      a_packed.m.row_data(0), a_packed.rows(), w.cols(),
-      static_cast<std::int64_t>(w.t.words_per_row()), a_packed.scale,
-      a_packed.gamma.has_value() ? 1 : 0, plane_gamma(a_packed), nullptr, nullptr, nullptr,
-      c.row_data(0), c.cols()));
-  return c;
+  bitmm_gemm_item it{};
+  it.routine = BITMM_ROUTINE_2X2;
+  it.a0 = w.t.row_data(0);
+  it.a1 = w.h.row_data(0);
+  it.a2 = w.m.row_data(0);
+  it.b0 = a_packed.t.row_data(0);
+  it.b1 = a_packed.h.row_data(0);
+  it.b2 = a_packed.m.row_data(0);
+  it.m = w.rows();
+  it.n = a_packed.rows();
+  it.k = w.cols();
+  it.wpr = static_cast<std::int64_t>(w.t.words_per_row());
+  it.a_scale = w.scale;
+  it.has_a_gamma = w.gamma.has_value() ? 1 : 0;
+  it.a_gamma = plane_gamma(w);
+  it.b_scale = a_packed.scale;
+  it.has_b_gamma = a_packed.gamma.has_value() ? 1 : 0;
+  it.b_gamma = plane_gamma(a_packed);
+  return run_late(it);
 }
 
 DenseMatrix gemm_1x32_ref(const BitMatrix& w, float gamma, const DenseMatrix& b, int threads) {

@@ -45,6 +45,16 @@ class GemmItem(C.Structure):
     ]
 
 
+class HostOut(C.Structure):
+    """ctypes mirror of `bitmm_host_out` (the late-output callback's destination)."""
+    _fields_ = [("c_units", _p), ("c", _p), ("ldc", _i64)]
+
+
+# int (*bitmm_out_fn)(void* user, bitmm_host_out* out)
+OUT_FN = C.CFUNCTYPE(C.c_int, _p, C.POINTER(HostOut))
+WANT_UNITS, WANT_C = 1, 2
+
+
 class BtsrHeader(C.Structure):
     """ctypes mirror of `bitmm_btsr_header`."""
     _fields_ = [("kind", C.c_int), ("rows", _i64), ("cols", _i64), ("words_per_row", _i64),
@@ -112,6 +122,7 @@ SIGNATURES = {
         [_i64, _i64, _f, _p, _p, _i64, _p, _p, _p, _i64, _p, _p, _p, _i64, _f, _i, _f, _p, _i64],
     ),
     "bitmm_gemm_batch_dev": (_i, [_p, _i, _p]),
+    "bitmm_gemm_host_late": (_i, [_p, _i, _p, _p]),
     "bitmm_btsr_read_header": (_i, [C.c_char_p, _p]),
     "bitmm_dot_binary_dev": (_i, [_p, _p, _i64, _i64, _i64, _p, _p]),
     "bitmm_mbm_dev": (_i, [_p, _p, _p, _i64, _i64, _p, _p]),

@@ -100,6 +100,8 @@ struct HostCtx {
   void* host_stage = nullptr;             // pinned 16-bit output words (run_pipelined_wire)
   size_t host_stage_bytes = 0;
   std::vector<cudaEvent_t> wire_ev;       // one per copied part
+  std::vector<cudaEvent_t> stage_ev;      // run_staged parts (spin-waited: latency, not CPU)
+  int* status_host = nullptr;             // pinned copy of the stream's status word (run_staged)
   void* pinned[2] = {nullptr, nullptr};   // BTSR streaming chunks (allocated on first load)
   cudaEvent_t pinned_ev[2] = {nullptr, nullptr};
   // BITMM_WIRE_TRACE only: device timeline of the current host call
@@ -202,6 +204,7 @@ int host_ctx_init(HostCtx& h) {
   for (auto& e : h.in_ev) BITMM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   BITMM_CUDA_TRY(cudaMalloc(&h.in_flags, 8 * sizeof(uint32_t)));
   BITMM_CUDA_TRY(cudaMemset(h.in_flags, 0, 8 * sizeof(uint32_t)));
+  BITMM_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&h.status_host), 64, cudaHostAllocDefault));
   return stream_ctx(h.stream, &h.sctx);
 }
 
@@ -1014,11 +1017,7 @@ int check_gemm_dims(int64_t m, int64_t n, int64_t k, int64_t wpr, int64_t ldc) {
   return BITMM_OK;
 }
 
-int read_status(Ctx& st, cudaStream_t s) {
-  BITMM_CUDA_TRY(cudaStreamSynchronize(s));
-  int flag = 0;
-  BITMM_CUDA_TRY(cudaMemcpy(&flag, st.status, sizeof(int), cudaMemcpyDeviceToHost));
-  BITMM_CUDA_TRY(cudaMemset(st.status, 0, sizeof(int)));
+int status_error(int flag) {
   // a timed-out input copy first: the inputs the GEMM read are then not the caller's
   if (flag & ERR_COPY_TIMEOUT) return fail(BITMM_ERR_CUDA, "input copy did not complete (flag wait timed out)");
   if (flag & ERR_ENCODING) return fail(BITMM_ERR_INVALID_ENCODING, "invalid ternary plane encoding or nonzero plane padding");
@@ -1026,6 +1025,14 @@ int read_status(Ctx& st, cudaStream_t s) {
   if (flag & ERR_LEVEL) return fail(BITMM_ERR_INVALID_ARGUMENT, "2-bit level out of range");
   if (flag & ERR_ALPHA) return fail(BITMM_ERR_INVALID_ARGUMENT, "alpha must be positive");
   return BITMM_OK;
+}
+
+int read_status(Ctx& st, cudaStream_t s) {
+  BITMM_CUDA_TRY(cudaStreamSynchronize(s));
+  int flag = 0;
+  BITMM_CUDA_TRY(cudaMemcpy(&flag, st.status, sizeof(int), cudaMemcpyDeviceToHost));
+  BITMM_CUDA_TRY(cudaMemset(st.status, 0, sizeof(int)));
+  return status_error(flag);
 }
 
 // ---------------- host-flavour pipeline ----------------
@@ -1272,6 +1279,166 @@ int run_pipelined_wire(HostCtx& st, cudaStream_t s, int64_t total, int64_t step,
   const cudaError_t e = cudaStreamSynchronize(st.d2h);
   if (rc == BITMM_OK && e != cudaSuccess) rc = fail(BITMM_ERR_CUDA, cudaGetErrorString(e));
   return rc;
+}
+
+// Where a host GEMM call's output goes: the caller's buffers, given up front (the *_host
+// calls), or obtained late through a callback (bitmm_gemm_host_late), after the call's
+// copies and kernels are enqueued, so the caller's allocation overlaps the device work.
+struct HostOut {
+  int32_t* c_units = nullptr;
+  float* c = nullptr;
+  int64_t ldc = 0;
+  bool want_units = false, want_c = false;
+  bitmm_out_fn fn = nullptr;
+  void* user = nullptr;
+  bool late() const { return fn != nullptr; }
+  static HostOut given(int32_t* u, float* c, int64_t ldc) {
+    HostOut o;
+    o.c_units = u;
+    o.c = c;
+    o.ldc = ldc;
+    o.want_units = u != nullptr;
+    o.want_c = c != nullptr;
+    return o;
+  }
+  // Calls the callback (once) and checks what it returned against the call.
+  int resolve(int64_t n) {
+    if (!fn) return BITMM_OK;
+    bitmm_host_out out{nullptr, nullptr, n};
+    const int r = fn(user, &out);
+    fn = nullptr;
+    if (r != 0) return fail(BITMM_ERR_INVALID_ARGUMENT, "output callback failed");
+    if ((want_units && !out.c_units) || (want_c && !out.c))
+      return fail(BITMM_ERR_INVALID_ARGUMENT, "output callback returned a null buffer");
+    if (out.ldc < n) return fail(BITMM_ERR_INVALID_ARGUMENT, "ldc smaller than the output column count");
+    c_units = want_units ? out.c_units : nullptr;
+    c = want_c ? out.c : nullptr;
+    ldc = out.ldc;
+    return BITMM_OK;
+  }
+};
+
+bool is_pinned_host(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// One-slice host outputs (below kPipeMinOutBytes) into pageable or late destinations. The GEMM
+// has been enqueued on s with its outputs at dcu / dc (rows x cols, leading dimension ldd). A
+// pageable destination written by cudaMemcpy is filled through the driver's own bounce buffer
+// at ~16 GB/s (0.26 ms for the 4 MB of a 1024^2 fp32 result); here the output is copied into
+// the lease's pinned staging in row parts of about 1 MiB, each with an event, and the calling
+// thread copies every part into the destination as soon as it lands (memcpy into the
+// destination's leading dimension). The status word the GEMM may have latched travels in the same stream
+// order into pinned memory, so an error is known before any caller memory is written. A late
+// destination is resolved after everything is enqueued.
+int run_staged(HostCtx& st, cudaStream_t s, int64_t rows, int64_t cols, int64_t ldd, const int32_t* dcu,
+               const float* dc, HostOut& o) {
+  // BITMM_STAGED_TRACE: per-call host timeline (us). The copy into the destination runs on the
+  // calling thread: copying with the host pool (BITMM_STAGED_POOL=1; =2 also keeps CUDA waits
+  // off the pool) took 90 instead of 265 us for 4 MB, but made the caller's next allocation and
+  // zero-fill of its DenseMatrix take 1.0-1.4 ms instead of 0.13 ms (4-16 threads; latency_b200
+  // with BITMM_STAGED_TRACE, profiles/dev/dropin_latency2.sh), so the call got 3x slower.
+  static const bool trace = std::getenv("BITMM_STAGED_TRACE") != nullptr;
+  static const int pool_mode = std::getenv("BITMM_STAGED_POOL") ? std::atoi(std::getenv("BITMM_STAGED_POOL")) : 0;
+  const bool pool = pool_mode != 0;
+  const auto t_in = std::chrono::steady_clock::now();
+  auto us = [&] {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_in).count();
+  };
+  BITMM_CUDA_TRY(cudaMemcpyAsync(st.status_host, st.sctx->status, sizeof(int), cudaMemcpyDeviceToHost, s));
+  BITMM_CUDA_TRY(cudaMemsetAsync(st.sctx->status, 0, sizeof(int), s));
+  BITMM_CUDA_TRY(cudaEventRecord(st.pipe_ev[0], s));
+  BITMM_CUDA_TRY(cudaStreamWaitEvent(st.d2h, st.pipe_ev[0], 0));
+  const size_t mat_bytes = static_cast<size_t>(rows * ldd) * 4;
+  const int nmat = (dcu ? 1 : 0) + (dc ? 1 : 0);
+  BITMM_TRY(host_stage_reserve(st, nmat * mat_bytes));
+  const int64_t row_bytes = ldd * 4;
+  const int64_t part_rows = std::max<int64_t>(1, std::max<int64_t>((int64_t{1} << 20) / row_bytes, (rows + 15) / 16));
+  struct Part {
+    int mat;  // 0 units, 1 fp32
+    int64_t r0, r1;
+  };
+  std::vector<Part> parts;
+  uint8_t* stage = static_cast<uint8_t*>(st.host_stage);
+  for (int mat = 0; mat < 2; ++mat) {
+    const void* src = mat == 0 ? static_cast<const void*>(dcu) : static_cast<const void*>(dc);
+    if (!src) continue;
+    const size_t base = (mat == 1 && dcu) ? mat_bytes : 0;
+    for (int64_t r0 = 0; r0 < rows; r0 += part_rows) {
+      const int64_t r1 = std::min(rows, r0 + part_rows);
+      BITMM_CUDA_TRY(cudaMemcpyAsync(stage + base + r0 * row_bytes, static_cast<const uint8_t*>(src) + r0 * row_bytes,
+                                     (r1 - r0) * row_bytes, cudaMemcpyDeviceToHost, st.d2h));
+      if (st.stage_ev.size() <= parts.size()) {
+        cudaEvent_t e = nullptr;
+        BITMM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        st.stage_ev.push_back(e);
+      }
+      BITMM_CUDA_TRY(cudaEventRecord(st.stage_ev[parts.size()], st.d2h));
+      parts.push_back(Part{mat, r0, r1});
+    }
+  }
+  g_d2h_bytes += nmat * static_cast<uint64_t>(rows * cols) * 4;
+  // everything is enqueued: the caller's destination now (late outputs), then the status word
+  const double t_enq = us();
+  BITMM_TRY(o.resolve(cols));
+  const double t_res = us();
+  if (parts.empty()) return BITMM_OK;
+  BITMM_CUDA_TRY(cudaEventSynchronize(st.stage_ev[0]));
+  const double t_first = us();
+  BITMM_TRY(status_error(*st.status_host));
+  // tasks of ~256 KB, handed out in part order
+  struct Task {
+    int part;
+    int64_t r0, r1;
+  };
+  std::vector<Task> tasks;
+  const int64_t task_rows = std::max<int64_t>(1, (int64_t{1} << 18) / std::max<int64_t>(1, cols * 4));
+  for (int p = 0; p < static_cast<int>(parts.size()); ++p)
+    for (int64_t r = parts[p].r0; r < parts[p].r1; r += task_rows)
+      tasks.push_back(Task{p, r, std::min(parts[p].r1, r + task_rows)});
+  std::atomic<int> copy_err{0};
+  if (pool_mode == 2) BITMM_CUDA_TRY(cudaEventSynchronize(st.stage_ev[parts.size() - 1]));  // A/B: no CUDA calls on the pool
+  auto copy = [&](int i) {
+    const Task& t = tasks[i];
+    if (pool_mode != 2 && cudaEventSynchronize(st.stage_ev[t.part]) != cudaSuccess) {
+      copy_err.store(1);
+      return;
+    }
+    const Part& q = parts[t.part];
+    const uint8_t* from = stage + ((q.mat == 1 && dcu) ? mat_bytes : 0) + t.r0 * row_bytes;
+    uint8_t* to = q.mat == 0 ? reinterpret_cast<uint8_t*>(o.c_units) : reinterpret_cast<uint8_t*>(o.c);
+    to += static_cast<size_t>(t.r0 * o.ldc) * 4;
+    if (o.ldc == ldd && ldd == cols) {
+      std::memcpy(to, from, static_cast<size_t>((t.r1 - t.r0) * cols) * 4);
+    } else {
+      for (int64_t r = t.r0; r < t.r1; ++r, from += row_bytes, to += o.ldc * 4)
+        std::memcpy(to, from, static_cast<size_t>(cols) * 4);
+    }
+  };
+  // a few tasks run on the calling thread alone (waking the pool costs more than it saves)
+  if (tasks.size() <= 2 || !pool) {
+    for (int i = 0; i < static_cast<int>(tasks.size()); ++i) copy(i);
+  } else {
+    host_pool_run(static_cast<int>(tasks.size()), copy);
+  }
+  if (trace)
+    std::fprintf(stderr, "[bitmm staged] %zu parts %zu tasks: enqueued %.1f resolved %.1f first part %.1f copied %.1f us\n",
+                 parts.size(), tasks.size(), t_enq, t_res, t_first, us());
+  if (copy_err.load()) return fail(BITMM_ERR_CUDA, std::string("staged copy: ") + cudaGetErrorString(cudaGetLastError()));
+  return BITMM_OK;
+}
+
+// Small outputs take run_staged unless the destination is already pinned (then the copy
+// engine writes it directly).
+bool use_staged(const HostOut& o) {
+  if (o.late()) return true;
+  if (const char* e = std::getenv("BITMM_HOST_STAGED"); e && std::atoi(e) == 0) return false;
+  return !((o.c_units && is_pinned_host(o.c_units)) || (o.c && is_pinned_host(o.c)));
 }
 
 size_t ws_half_int(int64_t m, int64_t n, int64_t k) {
@@ -1977,17 +2144,36 @@ int bitmm_gemm_1x1_popc_dev(const uint64_t* a, int64_t m, const uint64_t* b_pack
   return BITMM_OK;
 }
 
-int bitmm_gemm_1x1_host(const uint64_t* a, int64_t m, const uint64_t* b_packed, int64_t n,
-                        int64_t k, int64_t wpr, float gamma_a, float gamma_b, int32_t* c_units,
-                        float* c, int64_t ldc) {
+}  // extern "C"
+
+namespace {
+
+// A late destination of an output that is sliced or sent on the wire (>= kPipeMinOutBytes) is
+// resolved before anything is enqueued; smaller ones go through run_staged. Returns the
+// device leading dimension of the output.
+int prepare_out(HostOut& o, int64_t m, int64_t n, int64_t* ldd) {
+  // BITMM_LATE_EAGER=1: resolve every late destination up front (A/B of the overlap)
+  static const bool eager = std::getenv("BITMM_LATE_EAGER") && std::atoi(std::getenv("BITMM_LATE_EAGER")) == 1;
+  if (o.late() && (eager || static_cast<size_t>(m * n) * 4 >= kPipeMinOutBytes)) BITMM_TRY(o.resolve(n));
+  *ldd = o.late() ? n : o.ldc;
+  return BITMM_OK;
+}
+
+int gemm_1x1_host_impl(const uint64_t* a, int64_t m, const uint64_t* b_packed, int64_t n, int64_t k,
+                       int64_t wpr, float gamma_a, float gamma_b, HostOut& o) {
   g_launches = 0;
-  BITMM_TRY(check_gemm_dims(m, n, k, wpr, ldc));
-  if (!a || !b_packed || (!c_units && !c)) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  BITMM_TRY(check_gemm_dims(m, n, k, wpr, o.late() ? n : o.ldc));
+  if (!a || !b_packed || (!o.want_units && !o.want_c)) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
   HostLease hl;
   BITMM_TRY(hl.acquire());
   Ctx* st = &hl.ctx();
   cudaStream_t s = hl->stream;
   g_d2h_bytes = 0;
+  int64_t ldc = 0;
+  BITMM_TRY(prepare_out(o, m, n, &ldc));
+  int32_t* c_units = o.c_units;
+  float* c = o.c;
+  const bool want_units = o.want_units, want_c = o.want_c;
   const Wire wire = host_wire(0, k, static_cast<size_t>(m * ldc * 4));
   const size_t a_bytes = m * wpr * 8, b_bytes = n * wpr * 8, c_bytes = m * ldc * 4;
   const size_t w_bytes = wire != Wire::None ? static_cast<size_t>(m * n) * 2 : 0;
@@ -1997,8 +2183,8 @@ int bitmm_gemm_1x1_host(const uint64_t* a, int64_t m, const uint64_t* b_packed, 
   uint64_t* da = cv.take<uint64_t>(a_bytes);
   uint64_t* db = cv.take<uint64_t>(b_bytes);
   // 16-bit wire: the GEMM writes int32 units only; the host derives both outputs from them
-  int32_t* dcu = (c_units || wire != Wire::None) ? cv.take<int32_t>(c_bytes) : nullptr;
-  float* dc = (c && wire == Wire::None) ? cv.take<float>(c_bytes) : nullptr;
+  int32_t* dcu = (want_units || wire != Wire::None) ? cv.take<int32_t>(c_bytes) : nullptr;
+  float* dc = (want_c && wire == Wire::None) ? cv.take<float>(c_bytes) : nullptr;
   BITMM_CUDA_TRY(cudaMemcpyAsync(db, b_packed, b_bytes, cudaMemcpyHostToDevice, s));
   // slices of output rows (rows of a)
   auto in = [&](int64_t r0, int64_t r1, cudaStream_t cs) -> int {
@@ -2023,16 +2209,32 @@ int bitmm_gemm_1x1_host(const uint64_t* a, int64_t m, const uint64_t* b_packed, 
         cv.take<uint16_t>(w_bytes), static_cast<size_t>(m * n)));
     return read_status(*st, s);
   }
+  if (pipe_step(m, c_bytes, 256) >= m && use_staged(o)) {
+    BITMM_TRY(body(0, m));
+    return run_staged(hl.host(), s, m, n, ldc, dcu, dc, o);
+  }
   BITMM_TRY(run_pipelined(
       hl.host(), s, m, pipe_step(m, c_bytes, 256), body,
       [&](int64_t r0, int64_t r1, cudaStream_t d2h) -> int {
-        const size_t bytes = (r1 - r0) * ldc * 4;
-        if (dcu) BITMM_CUDA_TRY(cudaMemcpyAsync(c_units + r0 * ldc, dcu + r0 * ldc, bytes, cudaMemcpyDeviceToHost, d2h));
-        if (dc) BITMM_CUDA_TRY(cudaMemcpyAsync(c + r0 * ldc, dc + r0 * ldc, bytes, cudaMemcpyDeviceToHost, d2h));
-        g_d2h_bytes += (dcu ? bytes : 0) + (dc ? bytes : 0);
+        // rows of n cells: the caller's columns [n, ldc) are not the output's
+        const size_t pitch = ldc * 4, width = n * 4;
+        if (dcu) BITMM_CUDA_TRY(cudaMemcpy2DAsync(c_units + r0 * ldc, pitch, dcu + r0 * ldc, pitch, width, r1 - r0, cudaMemcpyDeviceToHost, d2h));
+        if (dc) BITMM_CUDA_TRY(cudaMemcpy2DAsync(c + r0 * ldc, pitch, dc + r0 * ldc, pitch, width, r1 - r0, cudaMemcpyDeviceToHost, d2h));
+        g_d2h_bytes += ((dcu ? 1 : 0) + (dc ? 1 : 0)) * width * (r1 - r0);
         return BITMM_OK;
       }));
   return read_status(*st, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int bitmm_gemm_1x1_host(const uint64_t* a, int64_t m, const uint64_t* b_packed, int64_t n,
+                        int64_t k, int64_t wpr, float gamma_a, float gamma_b, int32_t* c_units,
+                        float* c, int64_t ldc) {
+  HostOut o = HostOut::given(c_units, c, ldc);
+  return gemm_1x1_host_impl(a, m, b_packed, n, k, wpr, gamma_a, gamma_b, o);
 }
 
 // ---------------- 1/2 ----------------
@@ -2051,20 +2253,28 @@ int bitmm_gemm_1x2_dev(const uint64_t* w, int64_t m, float gamma, const uint64_t
                            row_scale, col_scale, c_units, c, ldc, static_cast<cudaStream_t>(stream));
 }
 
-int bitmm_gemm_1x2_host(const uint64_t* w, int64_t m, float gamma, const uint64_t* t,
-                        const uint64_t* h, const uint64_t* mm, int64_t n, int64_t k, int64_t wpr,
-                        float a_scale, int has_a_gamma, float a_gamma, const float* row_scale,
-                        const float* col_scale, int32_t* c_units, float* c, int64_t ldc) {
+}  // extern "C"
+
+namespace {
+
+int gemm_1x2_host_impl(const uint64_t* w, int64_t m, float gamma, const uint64_t* t, const uint64_t* h,
+                       const uint64_t* mm, int64_t n, int64_t k, int64_t wpr, float a_scale, int has_a_gamma,
+                       float a_gamma, const float* row_scale, const float* col_scale, HostOut& o) {
   g_launches = 0;
   // ThmPlanes::validate runs first in the reference (kernels.cpp:186): scale, then legality.
   if (!(a_scale > 0.0f)) return fail(BITMM_ERR_INVALID_ENCODING, "plane scale must be positive");
-  if (!t || !h || !mm || !w || (!c_units && !c)) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  if (!t || !h || !mm || !w || (!o.want_units && !o.want_c)) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
   HostLease hl;
   BITMM_TRY(hl.acquire());
   Ctx* st = &hl.ctx();
   cudaStream_t s = hl->stream;
-  const int rc_dims = check_gemm_dims(m, n, k, wpr, ldc);
+  const int rc_dims = check_gemm_dims(m, n, k, wpr, o.late() ? n : o.ldc);
   const std::string dims_msg = g_err;
+  int64_t ldc = 0;
+  if (rc_dims == BITMM_OK) BITMM_TRY(prepare_out(o, m, n, &ldc));
+  int32_t* c_units = o.c_units;
+  float* c = o.c;
+  const bool want_units = o.want_units, want_c = o.want_c;
   const bool planes_ok_shape = n >= 0 && k >= 0 && wpr >= 0 && wpr * 64 >= k;
   const size_t p_bytes = (planes_ok_shape ? n * wpr * 8 : 0), w_bytes = (rc_dims == BITMM_OK ? m * wpr * 8 : 0);
   const size_t c_bytes = (rc_dims == BITMM_OK ? m * ldc * 4 : 0);
@@ -2097,8 +2307,8 @@ int bitmm_gemm_1x2_host(const uint64_t* w, int64_t m, float gamma, const uint64_
   // 16-bit wire: the GEMM writes int32 units only and the host applies the scales
   float* drs = (row_scale && wire == Wire::None) ? cv.take<float>(m * 4) : nullptr;
   float* dcs = (col_scale && wire == Wire::None) ? cv.take<float>(n * 4) : nullptr;
-  int32_t* dcu = (c_units || wire != Wire::None) ? cv.take<int32_t>(c_bytes) : nullptr;
-  float* dc = (c && wire == Wire::None) ? cv.take<float>(c_bytes) : nullptr;
+  int32_t* dcu = (want_units || wire != Wire::None) ? cv.take<int32_t>(c_bytes) : nullptr;
+  float* dc = (want_c && wire == Wire::None) ? cv.take<float>(c_bytes) : nullptr;
   BITMM_CUDA_TRY(cudaMemcpyAsync(dw, w, w_bytes, cudaMemcpyHostToDevice, s));
   if (drs) BITMM_CUDA_TRY(cudaMemcpyAsync(drs, row_scale, m * 4, cudaMemcpyHostToDevice, s));
   if (dcs) BITMM_CUDA_TRY(cudaMemcpyAsync(dcs, col_scale, n * 4, cudaMemcpyHostToDevice, s));
@@ -2131,6 +2341,10 @@ int bitmm_gemm_1x2_host(const uint64_t* w, int64_t m, float gamma, const uint64_
         cv.take<uint16_t>(wire_bytes), static_cast<size_t>(m * n)));
     return read_status(*st, s);
   }
+  if (pipe_step(n, c_bytes, 256) >= n && use_staged(o)) {
+    BITMM_TRY(body(0, n));
+    return run_staged(hl.host(), s, m, n, ldc, dcu, dc, o);
+  }
   BITMM_TRY(run_pipelined(
       hl.host(), s, n, pipe_step(n, c_bytes, 256), body,
       [&](int64_t n0, int64_t n1, cudaStream_t d2h) -> int {
@@ -2141,6 +2355,19 @@ int bitmm_gemm_1x2_host(const uint64_t* w, int64_t m, float gamma, const uint64_
         return BITMM_OK;
       }));
   return read_status(*st, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int bitmm_gemm_1x2_host(const uint64_t* w, int64_t m, float gamma, const uint64_t* t,
+                        const uint64_t* h, const uint64_t* mm, int64_t n, int64_t k, int64_t wpr,
+                        float a_scale, int has_a_gamma, float a_gamma, const float* row_scale,
+                        const float* col_scale, int32_t* c_units, float* c, int64_t ldc) {
+  HostOut o = HostOut::given(c_units, c, ldc);
+  return gemm_1x2_host_impl(w, m, gamma, t, h, mm, n, k, wpr, a_scale, has_a_gamma, a_gamma, row_scale,
+                            col_scale, o);
 }
 
 // ---------------- 2/2 ----------------
@@ -2163,23 +2390,31 @@ int bitmm_gemm_2x2_dev(const uint64_t* wt, const uint64_t* wh, const uint64_t* w
                            ldc, static_cast<cudaStream_t>(stream));
 }
 
-int bitmm_gemm_2x2_host(const uint64_t* wt, const uint64_t* wh, const uint64_t* wm, int64_t m,
-                        float w_scale, int has_w_gamma, float w_gamma, const uint64_t* at,
-                        const uint64_t* ah, const uint64_t* am, int64_t n, int64_t k, int64_t wpr,
-                        float a_scale, int has_a_gamma, float a_gamma, const float* row_scale,
-                        const float* col_scale, int32_t* c_units, float* c, int64_t ldc) {
+}  // extern "C"
+
+namespace {
+
+int gemm_2x2_host_impl(const uint64_t* wt, const uint64_t* wh, const uint64_t* wm, int64_t m, float w_scale,
+                       int has_w_gamma, float w_gamma, const uint64_t* at, const uint64_t* ah,
+                       const uint64_t* am, int64_t n, int64_t k, int64_t wpr, float a_scale, int has_a_gamma,
+                       float a_gamma, const float* row_scale, const float* col_scale, HostOut& o) {
   g_launches = 0;
   // w.validate(); a_packed.validate(); then shapes (kernels.cpp:224-228)
   if (!(w_scale > 0.0f) || !(a_scale > 0.0f))
     return fail(BITMM_ERR_INVALID_ENCODING, "plane scale must be positive");
-  if (!wt || !wh || !wm || !at || !ah || !am || (!c_units && !c))
+  if (!wt || !wh || !wm || !at || !ah || !am || (!o.want_units && !o.want_c))
     return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
   HostLease hl;
   BITMM_TRY(hl.acquire());
   Ctx* st = &hl.ctx();
   cudaStream_t s = hl->stream;
-  const int rc_dims = check_gemm_dims(m, n, k, wpr, ldc);
+  const int rc_dims = check_gemm_dims(m, n, k, wpr, o.late() ? n : o.ldc);
   const std::string dims_msg = g_err;
+  int64_t ldc = 0;
+  if (rc_dims == BITMM_OK) BITMM_TRY(prepare_out(o, m, n, &ldc));
+  int32_t* c_units = o.c_units;
+  float* c = o.c;
+  const bool want_units = o.want_units, want_c = o.want_c;
   const bool shape_ok = k >= 0 && wpr >= 0 && wpr * 64 >= k;
   const size_t pw = (shape_ok && m > 0 ? m * wpr * 8 : 0), pa = (shape_ok && n > 0 ? n * wpr * 8 : 0);
   const size_t c_bytes = (rc_dims == BITMM_OK ? m * ldc * 4 : 0);
@@ -2212,8 +2447,8 @@ int bitmm_gemm_2x2_host(const uint64_t* wt, const uint64_t* wh, const uint64_t* 
   // 16-bit wire: the GEMM writes int32 units only and the host applies the scales
   float* drs = (row_scale && wire == Wire::None) ? cv.take<float>(m * 4) : nullptr;
   float* dcs = (col_scale && wire == Wire::None) ? cv.take<float>(n * 4) : nullptr;
-  int32_t* dcu = (c_units || wire != Wire::None) ? cv.take<int32_t>(c_bytes) : nullptr;
-  float* dc = (c && wire == Wire::None) ? cv.take<float>(c_bytes) : nullptr;
+  int32_t* dcu = (want_units || wire != Wire::None) ? cv.take<int32_t>(c_bytes) : nullptr;
+  float* dc = (want_c && wire == Wire::None) ? cv.take<float>(c_bytes) : nullptr;
   if (drs) BITMM_CUDA_TRY(cudaMemcpyAsync(drs, row_scale, m * 4, cudaMemcpyHostToDevice, s));
   if (dcs) BITMM_CUDA_TRY(cudaMemcpyAsync(dcs, col_scale, n * 4, cudaMemcpyHostToDevice, s));
   // slices of output rows (rows of the weight planes)
@@ -2245,16 +2480,59 @@ int bitmm_gemm_2x2_host(const uint64_t* wt, const uint64_t* wh, const uint64_t* 
         cv.take<uint16_t>(wire_bytes), static_cast<size_t>(m * n)));
     return read_status(*st, s);
   }
+  if (pipe_step(m, c_bytes, 256) >= m && use_staged(o)) {
+    BITMM_TRY(body(0, m));
+    return run_staged(hl.host(), s, m, n, ldc, dcu, dc, o);
+  }
   BITMM_TRY(run_pipelined(
       hl.host(), s, m, pipe_step(m, c_bytes, 256), body,
       [&](int64_t r0, int64_t r1, cudaStream_t d2h) -> int {
-        const size_t bytes = (r1 - r0) * ldc * 4;
-        if (dcu) BITMM_CUDA_TRY(cudaMemcpyAsync(c_units + r0 * ldc, dcu + r0 * ldc, bytes, cudaMemcpyDeviceToHost, d2h));
-        if (dc) BITMM_CUDA_TRY(cudaMemcpyAsync(c + r0 * ldc, dc + r0 * ldc, bytes, cudaMemcpyDeviceToHost, d2h));
-        g_d2h_bytes += (dcu ? bytes : 0) + (dc ? bytes : 0);
+        // rows of n cells: the caller's columns [n, ldc) are not the output's
+        const size_t pitch = ldc * 4, width = n * 4;
+        if (dcu) BITMM_CUDA_TRY(cudaMemcpy2DAsync(c_units + r0 * ldc, pitch, dcu + r0 * ldc, pitch, width, r1 - r0, cudaMemcpyDeviceToHost, d2h));
+        if (dc) BITMM_CUDA_TRY(cudaMemcpy2DAsync(c + r0 * ldc, pitch, dc + r0 * ldc, pitch, width, r1 - r0, cudaMemcpyDeviceToHost, d2h));
+        g_d2h_bytes += ((dcu ? 1 : 0) + (dc ? 1 : 0)) * width * (r1 - r0);
         return BITMM_OK;
       }));
   return read_status(*st, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int bitmm_gemm_2x2_host(const uint64_t* wt, const uint64_t* wh, const uint64_t* wm, int64_t m,
+                        float w_scale, int has_w_gamma, float w_gamma, const uint64_t* at,
+                        const uint64_t* ah, const uint64_t* am, int64_t n, int64_t k, int64_t wpr,
+                        float a_scale, int has_a_gamma, float a_gamma, const float* row_scale,
+                        const float* col_scale, int32_t* c_units, float* c, int64_t ldc) {
+  HostOut o = HostOut::given(c_units, c, ldc);
+  return gemm_2x2_host_impl(wt, wh, wm, m, w_scale, has_w_gamma, w_gamma, at, ah, am, n, k, wpr, a_scale,
+                            has_a_gamma, a_gamma, row_scale, col_scale, o);
+}
+
+// Late-output host call (include/bitmm_b200.h): item fields as bitmm_gemm_batch_dev reads them.
+int bitmm_gemm_host_late(const bitmm_gemm_item* it, int want, bitmm_out_fn out_fn, void* user) {
+  if (!it || !out_fn || (want & ~(BITMM_WANT_UNITS | BITMM_WANT_C)) || !want)
+    return fail(BITMM_ERR_INVALID_ARGUMENT, "late output needs an item, a callback and a wanted output");
+  HostOut o;
+  o.want_units = (want & BITMM_WANT_UNITS) != 0;
+  o.want_c = (want & BITMM_WANT_C) != 0;
+  o.fn = out_fn;
+  o.user = user;
+  switch (it->routine) {
+    case BITMM_ROUTINE_1X1:
+      return gemm_1x1_host_impl(it->a0, it->m, it->b0, it->n, it->k, it->wpr, it->a_scale, it->b_scale, o);
+    case BITMM_ROUTINE_1X2:
+      return gemm_1x2_host_impl(it->a0, it->m, it->a_scale, it->b0, it->b1, it->b2, it->n, it->k, it->wpr,
+                                it->b_scale, it->has_b_gamma, it->b_gamma, it->row_scale, it->col_scale, o);
+    case BITMM_ROUTINE_2X2:
+      return gemm_2x2_host_impl(it->a0, it->a1, it->a2, it->m, it->a_scale, it->has_a_gamma, it->a_gamma, it->b0,
+                                it->b1, it->b2, it->n, it->k, it->wpr, it->b_scale, it->has_b_gamma, it->b_gamma,
+                                it->row_scale, it->col_scale, o);
+    default:
+      return fail(BITMM_ERR_INVALID_ARGUMENT, "unknown routine");
+  }
 }
 
 // ---------------- 1/32 and APB ----------------
@@ -2302,7 +2580,7 @@ int bitmm_gemm_1x32_host(const uint64_t* w, int64_t m, int64_t k, int64_t wpr, f
   BITMM_CUDA_TRY(cudaMemcpyAsync(db, b, b_bytes, cudaMemcpyHostToDevice, s));
   if (dg) BITMM_CUDA_TRY(cudaMemcpyAsync(dg, row_gamma, m * 4, cudaMemcpyHostToDevice, s));
   BITMM_TRY(apb_dev_impl(*st, dw, m, k, wpr, gamma, dg, db, n, ldb, nullptr, nullptr, nullptr, dc, ldc, s));
-  BITMM_CUDA_TRY(cudaMemcpyAsync(c, dc, c_bytes, cudaMemcpyDeviceToHost, s));
+  BITMM_CUDA_TRY(cudaMemcpy2DAsync(c, ldc * 4, dc, ldc * 4, n * 4, m, cudaMemcpyDeviceToHost, s));  // columns [n, ldc) are not the output's
   return read_status(*st, s);
 }
 
@@ -2356,7 +2634,7 @@ int bitmm_layer_forward_host(int64_t rows, int64_t cols, float alpha, const floa
     BITMM_CUDA_TRY(cudaMemcpyAsync(dv, vals, nnz * 4, cudaMemcpyHostToDevice, s));
   }
   BITMM_TRY(apb_dev_impl(*st, dw, rows, cols, wpr, alpha, da, db, n, ldb, drp, dci, dv, dc, ldc, s));
-  BITMM_CUDA_TRY(cudaMemcpyAsync(c, dc, c_bytes, cudaMemcpyDeviceToHost, s));
+  BITMM_CUDA_TRY(cudaMemcpy2DAsync(c, ldc * 4, dc, ldc * 4, n * 4, rows, cudaMemcpyDeviceToHost, s));  // columns [n, ldc) are not the output's
   return read_status(*st, s);
 }
 
@@ -2413,7 +2691,7 @@ int bitmm_spmm_csr_host(int64_t rows, int64_t cols, const uint64_t* row_ptr,
     BITMM_CUDA_TRY(cudaMemcpyAsync(dv, vals, nnz * 4, cudaMemcpyHostToDevice, s));
   }
   BITMM_TRY(bitmm_spmm_csr_dev(rows, cols, drp, dci, dv, db, n, ldb, dc, ldc, s));
-  BITMM_CUDA_TRY(cudaMemcpyAsync(c, dc, c_bytes, cudaMemcpyDeviceToHost, s));
+  BITMM_CUDA_TRY(cudaMemcpy2DAsync(c, ldc * 4, dc, ldc * 4, n * 4, rows, cudaMemcpyDeviceToHost, s));  // columns [n, ldc) are not the output's
   BITMM_CUDA_TRY(cudaStreamSynchronize(s));
   return BITMM_OK;
 }
@@ -2713,7 +2991,7 @@ int bitmm_layer_forward_2bit_host(int64_t rows, int64_t cols, float alpha, const
   }
   BITMM_TRY(apb2_dev_impl(*st, rows, cols, wpr, alpha, da, dw, drp, dci, dv, dt, dh, dm, tokens,
                           a_scale, has_a_gamma ? a_gamma : 1.0f, dc, ldc, s));
-  BITMM_CUDA_TRY(cudaMemcpyAsync(c, dc, c_bytes, cudaMemcpyDeviceToHost, s));
+  BITMM_CUDA_TRY(cudaMemcpy2DAsync(c, ldc * 4, dc, ldc * 4, tokens * 4, rows, cudaMemcpyDeviceToHost, s));  // columns [tokens, ldc) are not the output's
   return read_status(*st, s);
 }
 

@@ -113,3 +113,19 @@ def test_gemm_item_struct_layout_matches_c(tmp_path):
     out = [int(x) for x in subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split()]
     assert out[0] == C.sizeof(_lib.GemmItem)
     assert out[1:] == [getattr(_lib.GemmItem, n).offset for n in names]
+
+
+def test_host_out_struct_layout_matches_c(tmp_path):
+    """ctypes HostOut and the C bitmm_host_out (late-output callback) agree on the layout."""
+    import ctypes as C
+    hdr = os.path.join(REPO, "include", "bitmm_b200.h")
+    names = [f[0] for f in _lib.HostOut._fields_]
+    body = "".join(f'  printf("%zu\\n", offsetof(bitmm_host_out, {n}));\n' for n in names)
+    src = (f'#include <stddef.h>\n#include <stdio.h>\n#include "{hdr}"\n'
+           f'int main(void) {{\n  printf("%zu\\n", sizeof(bitmm_host_out));\n{body}  return 0;\n}}\n')
+    exe = str(tmp_path / "layout")
+    subprocess.run(["gcc", "-std=c99", "-x", "c", "-", "-o", exe], input=src, text=True, check=True)
+    out = [int(x) for x in subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split()]
+    assert out[0] == C.sizeof(_lib.HostOut)
+    assert out[1:] == [getattr(_lib.HostOut, n).offset for n in names]
+    assert (_lib.WANT_UNITS, _lib.WANT_C) == (1, 2)
