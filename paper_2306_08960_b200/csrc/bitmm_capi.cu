@@ -1346,6 +1346,8 @@ int run_staged(HostCtx& st, cudaStream_t s, int64_t rows, int64_t cols, int64_t 
   static const bool trace = std::getenv("BITMM_STAGED_TRACE") != nullptr;
   static const int pool_mode = std::getenv("BITMM_STAGED_POOL") ? std::atoi(std::getenv("BITMM_STAGED_POOL")) : 0;
   const bool pool = pool_mode != 0;
+  // BITMM_STAGED_NT=1: streaming-store copy (A/B)
+  static const bool nt = std::getenv("BITMM_STAGED_NT") && std::atoi(std::getenv("BITMM_STAGED_NT")) == 1;
   const auto t_in = std::chrono::steady_clock::now();
   auto us = [&] {
     return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_in).count();
@@ -1414,7 +1416,8 @@ int run_staged(HostCtx& st, cudaStream_t s, int64_t rows, int64_t cols, int64_t 
     uint8_t* to = q.mat == 0 ? reinterpret_cast<uint8_t*>(o.c_units) : reinterpret_cast<uint8_t*>(o.c);
     to += static_cast<size_t>(t.r0 * o.ldc) * 4;
     if (o.ldc == ldd && ldd == cols) {
-      std::memcpy(to, from, static_cast<size_t>((t.r1 - t.r0) * cols) * 4);
+      if (nt) copy_streaming(to, from, static_cast<size_t>((t.r1 - t.r0) * cols) * 4);
+      else std::memcpy(to, from, static_cast<size_t>((t.r1 - t.r0) * cols) * 4);
     } else {
       for (int64_t r = t.r0; r < t.r1; ++r, from += row_bytes, to += o.ldc * 4)
         std::memcpy(to, from, static_cast<size_t>(cols) * 4);

@@ -12,6 +12,7 @@
 #include <atomic>
 #include <condition_variable>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -238,7 +239,39 @@ void expand_rows(const WireOut& o, const uint16_t* words, int64_t row0, int64_t 
 #endif
 }
 
+#if defined(__x86_64__)
+__attribute__((target("avx512f"))) void copy_nt_avx512(uint8_t* d, const uint8_t* s, size_t bytes) {
+  size_t i = 0;
+  for (; i + 256 <= bytes; i += 256) {
+    const __m512i a = _mm512_loadu_si512(s + i), b = _mm512_loadu_si512(s + i + 64);
+    const __m512i c = _mm512_loadu_si512(s + i + 128), e = _mm512_loadu_si512(s + i + 192);
+    _mm512_stream_si512(reinterpret_cast<__m512i*>(d + i), a);
+    _mm512_stream_si512(reinterpret_cast<__m512i*>(d + i + 64), b);
+    _mm512_stream_si512(reinterpret_cast<__m512i*>(d + i + 128), c);
+    _mm512_stream_si512(reinterpret_cast<__m512i*>(d + i + 192), e);
+  }
+  for (; i + 64 <= bytes; i += 64)
+    _mm512_stream_si512(reinterpret_cast<__m512i*>(d + i), _mm512_loadu_si512(s + i));
+  if (i < bytes) std::memcpy(d + i, s + i, bytes - i);
+}
+#endif
+
 }  // namespace
+
+void copy_streaming(void* dst, const void* src, size_t bytes) {
+  auto* d = static_cast<uint8_t*>(dst);
+  const auto* s = static_cast<const uint8_t*>(src);
+#if defined(__x86_64__)
+  if (has_avx512() && bytes >= 4096) {
+    const size_t head = (64 - (reinterpret_cast<uintptr_t>(d) & 63)) & 63;
+    std::memcpy(d, s, head);
+    copy_nt_avx512(d + head, s + head, bytes - head);
+    _mm_sfence();
+    return;
+  }
+#endif
+  std::memcpy(d, s, bytes);
+}
 
 void host_pool_run(int n, const std::function<void(int)>& f) { HostPool::get().run(n, f); }
 int host_pool_size() { return HostPool::get().size(); }

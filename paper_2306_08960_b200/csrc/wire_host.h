@@ -3,6 +3,7 @@
 // Implemented in wire_host.cpp (plain C++, compiled by the host compiler).
 #pragma once
 
+#include <stddef.h>
 #include <stdint.h>
 
 #include <functional>
@@ -38,6 +39,10 @@ struct WireOut {
 // concurrency capped at 32; the caller is one of them) and returns when all are done.
 void host_pool_run(int n, const std::function<void(int)>& f);
 int host_pool_size();
+
+// memcpy with 64-byte streaming stores where the CPU has AVX-512 (no read-for-ownership of the
+// destination lines), else memcpy.
+void copy_streaming(void* dst, const void* src, size_t bytes);
 
 // Widens rows [r0, r1) of the output block at (row0, col0) with `cols` columns whose words
 // are packed row-major at `words` (row r at words + (r - row0) * cols) into o's buffers.
