@@ -2151,13 +2151,15 @@ int bitmm_gemm_1x1_popc_dev(const uint64_t* a, int64_t m, const uint64_t* b_pack
 
 namespace {
 
-// A late destination of an output that is sliced or sent on the wire (>= kPipeMinOutBytes) is
-// resolved before anything is enqueued; smaller ones go through run_staged. Returns the
+// A late destination of an output that is sliced (>= kPipeMinOutBytes) or sent on the 16-bit
+// wire is resolved before anything is enqueued; smaller ones go through run_staged. Returns the
 // device leading dimension of the output.
-int prepare_out(HostOut& o, int64_t m, int64_t n, int64_t* ldd) {
+int prepare_out(HostOut& o, int routine, int64_t m, int64_t n, int64_t k, int64_t* ldd) {
   // BITMM_LATE_EAGER=1: resolve every late destination up front (A/B of the overlap)
   static const bool eager = std::getenv("BITMM_LATE_EAGER") && std::atoi(std::getenv("BITMM_LATE_EAGER")) == 1;
-  if (o.late() && (eager || static_cast<size_t>(m * n) * 4 >= kPipeMinOutBytes)) BITMM_TRY(o.resolve(n));
+  const size_t bytes = static_cast<size_t>(m * n) * 4;
+  if (o.late() && (eager || bytes >= kPipeMinOutBytes || host_wire(routine, k, bytes) != Wire::None))
+    BITMM_TRY(o.resolve(n));
   *ldd = o.late() ? n : o.ldc;
   return BITMM_OK;
 }
@@ -2173,7 +2175,7 @@ int gemm_1x1_host_impl(const uint64_t* a, int64_t m, const uint64_t* b_packed, i
   cudaStream_t s = hl->stream;
   g_d2h_bytes = 0;
   int64_t ldc = 0;
-  BITMM_TRY(prepare_out(o, m, n, &ldc));
+  BITMM_TRY(prepare_out(o, 0, m, n, k, &ldc));
   int32_t* c_units = o.c_units;
   float* c = o.c;
   const bool want_units = o.want_units, want_c = o.want_c;
@@ -2274,7 +2276,7 @@ int gemm_1x2_host_impl(const uint64_t* w, int64_t m, float gamma, const uint64_t
   const int rc_dims = check_gemm_dims(m, n, k, wpr, o.late() ? n : o.ldc);
   const std::string dims_msg = g_err;
   int64_t ldc = 0;
-  if (rc_dims == BITMM_OK) BITMM_TRY(prepare_out(o, m, n, &ldc));
+  if (rc_dims == BITMM_OK) BITMM_TRY(prepare_out(o, 1, m, n, k, &ldc));
   int32_t* c_units = o.c_units;
   float* c = o.c;
   const bool want_units = o.want_units, want_c = o.want_c;
@@ -2414,7 +2416,7 @@ int gemm_2x2_host_impl(const uint64_t* wt, const uint64_t* wh, const uint64_t* w
   const int rc_dims = check_gemm_dims(m, n, k, wpr, o.late() ? n : o.ldc);
   const std::string dims_msg = g_err;
   int64_t ldc = 0;
-  if (rc_dims == BITMM_OK) BITMM_TRY(prepare_out(o, m, n, &ldc));
+  if (rc_dims == BITMM_OK) BITMM_TRY(prepare_out(o, 2, m, n, k, &ldc));
   int32_t* c_units = o.c_units;
   float* c = o.c;
   const bool want_units = o.want_units, want_c = o.want_c;

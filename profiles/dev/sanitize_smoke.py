@@ -66,6 +66,23 @@ assert lib.bitmm_gemm_1x2_host(P(a), m, 1.0, P(t), P(h), P(mm), n, k, wpr, 1.0, 
                                None, n) == 0
 assert np.array_equal(uh, orc.gemm_1x2(a, 1.0, t, h, mm, k, wpr)[0])
 
+# late-output host call (the drop-in's path): staged copy through pinned memory
+it = _lib.GemmItem()
+it.routine, it.a0, it.b0, it.m, it.n, it.k, it.wpr, it.a_scale, it.b_scale = 0, a.ctypes.data, b.ctypes.data, m, n, k, wpr, 1.0, 1.0
+late = {}
+
+
+def _out(user, o):
+    late["u"] = np.empty((m, n), np.int32)
+    o.contents.c_units = late["u"].ctypes.data
+    o.contents.ldc = n
+    return 0
+
+
+cb = _lib.OUT_FN(_out)
+assert lib.bitmm_gemm_host_late(C.byref(it), _lib.WANT_UNITS, cb, None) == 0, _lib.last_error()
+assert np.array_equal(late["u"], orc.gemm_1x1(a, b, k, wpr)[0])
+
 # APB (fp32 activations): folded residual, and the plain 1x32 GEMM
 rows, cols, tokens = 192, 768, 160
 w, alpha, _ = data.apb_weights(rng, rows, cols)

@@ -90,7 +90,12 @@ SHAPES = [(200, 300, 1000), (1024, 1024, 1024), (2112, 4096, 512)]
 @pytest.mark.parametrize("routine", [0, 1, 2])
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("want", [1, 2, 3])
-def test_late_output_bit_exact(routine, shape, want):
+@pytest.mark.parametrize("wire_min", [None, "0"])
+def test_late_output_bit_exact(routine, shape, want, wire_min, monkeypatch):
+    """wire_min "0": every output takes the 16-bit wire (BITMM_WIRE_MIN_BYTES=0), so a late
+    destination is resolved before the wire's pipeline starts."""
+    if wire_min is not None:
+        monkeypatch.setenv("BITMM_WIRE_MIN_BYTES", wire_min)
     m, n, k = shape
     ops, wpr, (wu, wc), scales = _case(routine, m, n, k, seed=m + n + k + routine)
     it = _item(routine, m, n, k, wpr, ops, scales)
