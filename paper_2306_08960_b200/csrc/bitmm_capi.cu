@@ -758,10 +758,13 @@ int run_int_gemm(Ctx& st, const uint8_t* A8, const uint8_t* B8, int64_t m, int64
 // Sign operands are read as the caller's BitMatrix words; level operands go through one prep
 // pass (2-bit codes, validated). It needs TMA-readable packed rows: an even words_per_row
 // (16-byte row pitch) and 16-byte aligned bases; other calls take the default path.
-bool fx_enabled() {
-  static const bool on = getenv("BITMM_FX") && atoi(getenv("BITMM_FX")) == 1;
-  return on && use_fp4();
+// BITMM_FX=1: both operands expanded inside the GEMM; BITMM_FX=2 (hybrid): A expanded by
+// unpack_operands as on the default path, B inside the GEMM (fx_gemm.cuh, AX).
+int fx_mode() {
+  static const int mode = getenv("BITMM_FX") ? atoi(getenv("BITMM_FX")) : 0;
+  return use_fp4() && (mode == 1 || mode == 2) ? mode : 0;
 }
+bool fx_enabled() { return fx_mode() != 0; }
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 bool fx_operand_ok(const OperandSrc& o, int64_t wpr) {
   if (wpr & 1) return false;
@@ -787,6 +790,7 @@ struct FxItem {
 
 // One GEMM problem of an fx launch: packed sources after the prep pass.
 struct FxProb {
+  const uint8_t* a_x;  // hybrid: A expanded to e2m1 rows of kpad / 2 bytes
   const void* a_src;
   const void* b_src;
   int a_code, b_code;
@@ -822,10 +826,10 @@ int make_packed_map(CUtensorMap* map, const void* base, uint64_t row_bytes, uint
   return BITMM_OK;
 }
 
-template <Epi EPI, int NP, int SLOT_ROW>
+template <Epi EPI, int NP, int SLOT_ROW, bool AX>
 int run_fx_group(Ctx& st, const FxProb* probs, int count, cudaStream_t s) {
-  using S = FxShape<fx_exp<EPI>(), SLOT_ROW>;
-  auto kern = fx_gemm_kernel<EPI, NP, fx_exp<EPI>(), SLOT_ROW>;
+  using S = FxShape<fx_exp<EPI>(), SLOT_ROW, AX>;
+  auto kern = fx_gemm_kernel<EPI, NP, fx_exp<EPI>(), SLOT_ROW, AX>;
   BITMM_TRY(ensure_max_smem(reinterpret_cast<const void*>(kern), S::SMEM));
   FxGroup<NP> g;
   memset(&g, 0, sizeof(g));
@@ -833,7 +837,11 @@ int run_fx_group(Ctx& st, const FxProb* probs, int count, cudaStream_t s) {
   for (int i = 0; i < count; ++i) {
     const FxProb& q = probs[i];
     const uint64_t kc = static_cast<uint64_t>(kcode_for(q.k));
-    BITMM_TRY(make_packed_map(&g.a[i], q.a_src, q.a_code ? kc / 4 : q.wpr * 8, q.m, q.a_code ? 128 : 64, S::A_ROWS));
+    if constexpr (AX)
+      BITMM_TRY(make_operand_map(&g.a[i], q.a_x, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, round_up(q.k, FX_KSTAGE) / 2, q.m,
+                                 S::A_ROWS));
+    else
+      BITMM_TRY(make_packed_map(&g.a[i], q.a_src, q.a_code ? kc / 4 : q.wpr * 8, q.m, q.a_code ? 128 : 64, S::A_ROWS));
     BITMM_TRY(make_packed_map(&g.b[i], q.b_src, q.b_code ? kc / 4 : q.wpr * 8, q.n, q.b_code ? 128 : 64, S::B_ROWS));
     TcParams p = q.p;
     p.M = static_cast<int>(q.m);
@@ -880,32 +888,43 @@ int run_fx_group(Ctx& st, const FxProb* probs, int count, cudaStream_t s) {
   return launch_check("fx_gemm_kernel");
 }
 
-template <int SLOT_ROW>
+template <int SLOT_ROW, bool AX>
 int dispatch_fx(Ctx& st, const FxProb* probs, int count, cudaStream_t s) {
   if (count == 1) {
     const int e = probs[0].p.epi;
-    if (e == static_cast<int>(Epi::I32)) return run_fx_group<Epi::I32, 1, SLOT_ROW>(st, probs, 1, s);
-    if (e == static_cast<int>(Epi::F32)) return run_fx_group<Epi::F32, 1, SLOT_ROW>(st, probs, 1, s);
-    return run_fx_group<Epi::F32R, 1, SLOT_ROW>(st, probs, 1, s);
+    if (e == static_cast<int>(Epi::I32)) return run_fx_group<Epi::I32, 1, SLOT_ROW, AX>(st, probs, 1, s);
+    if (e == static_cast<int>(Epi::F32)) return run_fx_group<Epi::F32, 1, SLOT_ROW, AX>(st, probs, 1, s);
+    return run_fx_group<Epi::F32R, 1, SLOT_ROW, AX>(st, probs, 1, s);
   }
   for (int i = 0; i < count; ++i)
     if (probs[i].p.epi == static_cast<int>(Epi::F32R))
       return fail(BITMM_ERR_INVALID_ARGUMENT, "reference-order row scales are single-problem only");
-  if (count == 2) return run_fx_group<Epi::ANY, 2, SLOT_ROW>(st, probs, 2, s);
-  return run_fx_group<Epi::ANY, TC_GROUP_MAX, SLOT_ROW>(st, probs, count, s);
+  if (count == 2) return run_fx_group<Epi::ANY, 2, SLOT_ROW, AX>(st, probs, 2, s);
+  return run_fx_group<Epi::ANY, TC_GROUP_MAX, SLOT_ROW, AX>(st, probs, count, s);
 }
 
 // Prep pass (codes for level operands, padding checks for sign operands with bits past K),
 // then one fx_gemm launch over every problem of the items.
 int run_fx(Ctx& st, const FxItem* items, int count, cudaStream_t s) {
-  size_t code_bytes = 1024;
+  const bool hyb = fx_mode() == 2;
+  size_t code_bytes = 1024, ax_bytes = 1024;
   for (int i = 0; i < count; ++i) {
     const int64_t kc = kcode_for(items[i].k);
-    if (items[i].a.levels) code_bytes += align_up(items[i].a.rows * kc / 4, 1024);
+    if (items[i].a.levels && !hyb) code_bytes += align_up(items[i].a.rows * kc / 4, 1024);
     if (items[i].b.levels) code_bytes += align_up(items[i].b.rows * kc / 4, 1024);
+    ax_bytes += align_up(items[i].a.rows * round_up(items[i].k, FX_KSTAGE) / 2, 1024);
   }
   BITMM_TRY(arena_reserve(st.codes, code_bytes, st.stream));
   Carve cv(st.codes.ptr);
+  // hybrid: every A operand expanded by one unpack_operands launch into the workspace
+  UnpackSet U{};
+  U.fp4 = 1;
+  U.err = st.status;
+  uint8_t* ax_next = nullptr;
+  if (hyb) {
+    BITMM_TRY(ws_reserve(st, ax_bytes));
+    ax_next = static_cast<uint8_t*>(st.ws.ptr);
+  }
   PrepSet P{};
   P.err = st.status;
   long long max_items = 0;
@@ -935,7 +954,14 @@ int run_fx(Ctx& st, const FxItem* items, int count, cudaStream_t s) {
   for (int i = 0; i < count; ++i) {
     const FxItem& it = items[i];
     FxProb q{};
-    q.a_src = prep(it.a, it.k, it.wpr, &q.a_code);
+    if (hyb) {
+      const int64_t kpad = round_up(it.k, FX_KSTAGE);
+      q.a_x = ax_next;
+      ax_next += align_up(it.a.rows * kpad / 2, 1024);
+      U.op[U.count++] = make_unpack_operand(it.a, it.wpr, it.k, kpad, const_cast<uint8_t*>(q.a_x));
+    } else {
+      q.a_src = prep(it.a, it.k, it.wpr, &q.a_code);
+    }
     q.b_src = prep(it.b, it.k, it.wpr, &q.b_code);
     any_code = any_code || q.a_code || q.b_code;
     q.m = it.a.rows;
@@ -987,7 +1013,11 @@ int run_fx(Ctx& st, const FxItem* items, int count, cudaStream_t s) {
     BITMM_TRY(launch_check("prep_operands_kernel"));
   }
   if (np == 0) return BITMM_OK;
-  return any_code ? dispatch_fx<128>(st, probs, np, s) : dispatch_fx<64>(st, probs, np, s);
+  if (hyb) {
+    BITMM_TRY(run_unpack_set(U, s));
+    return any_code ? dispatch_fx<128, true>(st, probs, np, s) : dispatch_fx<64, true>(st, probs, np, s);
+  }
+  return any_code ? dispatch_fx<128, false>(st, probs, np, s) : dispatch_fx<64, false>(st, probs, np, s);
 }
 
 FxItem fx_item(const OperandSrc& a, const OperandSrc& b, int64_t k, int64_t wpr, int shift, float scale,

@@ -41,7 +41,10 @@ constexpr int FX_KSLOT = 512;   // K elements per packed slot (two stages)
 #endif
 
 // SLOT_ROW: packed slot bytes per row, 64 (sign operands only) or 128 (2-bit codes possible).
-template <int NEXP, int SLOT_ROW>
+// AX (hybrid, BITMM_FX=2): A arrives already expanded (unpack.cuh's e2m1 rows, TMA-loaded into
+// the stage as tc_gemm does) and only B is expanded here: the expanders write 12 KB per stage
+// instead of 28 KB, and the packed ring holds B alone, so six stages fit instead of four.
+template <int NEXP, int SLOT_ROW, bool AX = false>
 struct FxShape {
   static constexpr int BN = 192;
   static constexpr int A_ROWS = 128;
@@ -50,13 +53,13 @@ struct FxShape {
   static constexpr int STAGE_A = A_ROWS * 128;
   static constexpr int STAGE_B = B_ROWS * 128;
   static constexpr int STAGE = STAGE_A + STAGE_B;  // 28 KB
-  static constexpr int SLOT_A = A_ROWS * SLOT_ROW;
-  static constexpr int SLOT = (A_ROWS + B_ROWS) * SLOT_ROW;
+  static constexpr int SLOT_A = AX ? 0 : A_ROWS * SLOT_ROW;
+  static constexpr int SLOT = SLOT_A + B_ROWS * SLOT_ROW;
   static constexpr int EPI_BUFS = 1;
   static constexpr int EPI_WARP_BYTES = 5120;
   static constexpr int EPI_BYTES = 4 * EPI_WARP_BYTES;
   static constexpr int COLS_BYTES = BN * 4;
-  static constexpr int E = 4;  // expanded stages
+  static constexpr int E = AX ? 6 : 4;  // expanded stages
   static constexpr int P = (232448 - 1024 - E * STAGE - EPI_BYTES - COLS_BYTES - 512) / SLOT;
   static constexpr int BAR_BYTES = (2 * E + 2 * P + 4) * 8 + 16;
   static constexpr int SMEM = 1024 + E * STAGE + P * SLOT + EPI_BYTES + COLS_BYTES + BAR_BYTES;
@@ -158,10 +161,10 @@ __device__ __forceinline__ void fx_store_rows(uint8_t* st, const uint4 (&v)[ITS]
   }
 }
 
-template <Epi EPI, int NP, int NEXP, int SLOT_ROW>
-__global__ void __launch_bounds__(FxShape<NEXP, SLOT_ROW>::THREADS, 1)
+template <Epi EPI, int NP, int NEXP, int SLOT_ROW, bool AX = false>
+__global__ void __launch_bounds__(FxShape<NEXP, SLOT_ROW, AX>::THREADS, 1)
     fx_gemm_kernel(const __grid_constant__ FxGroup<NP> g) {
-  using S = FxShape<NEXP, SLOT_ROW>;
+  using S = FxShape<NEXP, SLOT_ROW, AX>;
   constexpr int BN = S::BN;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = smem_u32(smem_raw);
@@ -192,7 +195,8 @@ __global__ void __launch_bounds__(FxShape<NEXP, SLOT_ROW>::THREADS, 1)
       if (g.prob[i].tma_store) tma_prefetch_desc(&g.c[i]);
     }
     for (int s = 0; s < S::E; ++s) {
-      mbar_init(&full[s], 2 * NEXP / FX_GROUPS);  // every expander warp of the stage's group, both CTAs
+      // every expander warp of the stage's group, both CTAs (+ the leader's A loads under AX)
+      mbar_init(&full[s], 2 * NEXP / FX_GROUPS + (AX ? 1 : 0));
       mbar_init(&empty[s], 1);        // the pair's MMA commit
     }
     for (int s = 0; s < S::P; ++s) {
@@ -223,7 +227,42 @@ __global__ void __launch_bounds__(FxShape<NEXP, SLOT_ROW>::THREADS, 1)
   // Everything above overlapped the previous kernel (PDL); from here on we read its output.
   pdl_wait();
 
-  if (warp == 0) {
+  if (AX && warp == 0) {
+    // ============ TMA producer (AX): B's packed ring, and A's e2m1 rows into the stages ============
+    if (lane == 0) {
+      int ps = 0, stage = 0;
+      uint32_t pph = 0, phase = 0;
+      for (int tile = unit; tile < num_tiles; tile += num_units) {
+        const int pi = fx_problem_of(g, tile);
+        const TcParams& p = g.prob[pi];
+        int mb, nb;
+        tc_tile_coords(tile - g.tile_begin[pi], p, p.num_n_blocks, mb, nb);
+        const int a_row = mb * S::TILE_M + static_cast<int>(rank) * S::A_ROWS;
+        const int b_row = nb * BN + static_cast<int>(rank) * S::B_ROWS;
+        const int b_box = g.b_code[pi] ? 128 : 64;
+        const CUtensorMap* ma = &g.a[pi];
+        const CUtensorMap* mbm = &g.b[pi];
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          if ((kb & 1) == 0) {  // a packed slot holds two stages of B
+            mbar_wait(&pempty[ps], pph ^ 1u);
+            mbar_arrive_expect_tx(&pfull[ps], static_cast<uint32_t>(S::B_ROWS * b_box));
+            tma_load_2d(sSlot + ps * S::SLOT, mbm, &pfull[ps], (kb >> 1) * b_box, b_row);
+            if (++ps == S::P) {
+              ps = 0;
+              pph ^= 1u;
+            }
+          }
+          mbar_wait(&empty[stage], phase ^ 1u);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * S::STAGE_A);
+          tma_load_2d_pair(sStage + stage * S::STAGE, ma, &full[stage], kb * 128, a_row);
+          if (++stage == S::E) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 0) {
     // ===================== TMA producer of the packed ring (each CTA its own rows) ==========
     if (lane == 0) {
       int ps = 0;
@@ -376,8 +415,9 @@ __global__ void __launch_bounds__(FxShape<NEXP, SLOT_ROW>::THREADS, 1)
     // ===================== expanders (warps 6.. of every CTA) =====================
     constexpr int T = NEXP / FX_GROUPS * 32;  // threads per group
     constexpr int ROWS_PER_IT = T / 8;  // 8 lanes per row: one 16-byte output chunk each
-    constexpr int A_ITS = S::A_ROWS / ROWS_PER_IT, B_ITS = S::B_ROWS / ROWS_PER_IT;
-    static_assert(A_ITS * ROWS_PER_IT == S::A_ROWS && B_ITS * ROWS_PER_IT == S::B_ROWS, "task split");
+    constexpr int A_ITS = AX ? 1 : S::A_ROWS / ROWS_PER_IT, B_ITS = S::B_ROWS / ROWS_PER_IT;
+    static_assert(AX || (A_ITS * ROWS_PER_IT == S::A_ROWS && B_ITS * ROWS_PER_IT == S::B_ROWS), "task split");
+    static_assert(B_ITS * ROWS_PER_IT == S::B_ROWS, "task split");
     const int group = (threadIdx.x - 6 * 32) / T;
     const int tid = threadIdx.x - 6 * 32 - group * T;
     const int r0 = tid >> 3, j = tid & 7;
@@ -415,12 +455,12 @@ __global__ void __launch_bounds__(FxShape<NEXP, SLOT_ROW>::THREADS, 1)
         // first store (the stores could alias them as far as the compiler knows).
         const int kel = kb * FX_KSTAGE + j * 32;
         uint4 va[A_ITS], vb[B_ITS];
-        fx_load_rows<A_ITS, ROWS_PER_IT>(slot, va, r0, j, sub, kel, K, a_code);
+        if constexpr (!AX) fx_load_rows<A_ITS, ROWS_PER_IT>(slot, va, r0, j, sub, kel, K, a_code);
         fx_load_rows<B_ITS, ROWS_PER_IT>(slot + S::SLOT_A, vb, r0, j, sub, kel, K, b_code);
 #ifdef FX_NO_STS  // timing experiment only (wrong results): no stage writes
-        if (va[0].x == 0x12345678u && vb[0].y == 0x9abcdef0u) {
+        if (vb[0].x == 0x12345678u && vb[0].y == 0x9abcdef0u) {
 #endif
-        fx_store_rows<A_ITS, ROWS_PER_IT>(st, va, r0, j);
+        if constexpr (!AX) fx_store_rows<A_ITS, ROWS_PER_IT>(st, va, r0, j);
         fx_store_rows<B_ITS, ROWS_PER_IT>(st + S::STAGE_A, vb, r0, j);
 #ifdef FX_NO_STS
         }

@@ -1,4 +1,5 @@
-"""The in-GEMM expansion path (fx_gemm.cuh, BITMM_FX=1): bit-exact against the oracle.
+"""The in-GEMM expansion paths (fx_gemm.cuh, BITMM_FX=1 and the hybrid BITMM_FX=2): bit-exact
+against the oracle.
 
 It is a selectable alternative to the default expansion pass, so it is exercised in a child
 process with the variable set (the library reads it once): random shapes with off-grid K and
@@ -73,8 +74,10 @@ print("fx ok")
 '''
 
 
-def test_fx_path_bit_exact():
-    env = dict(os.environ, BITMM_FX="1")
+@pytest.mark.parametrize("mode", ["1", "2"])
+def test_fx_path_bit_exact(mode):
+    """mode 1: both operands expanded in the GEMM; 2 (hybrid): A by unpack_operands, B in the GEMM."""
+    env = dict(os.environ, BITMM_FX=mode)
     r = subprocess.run([sys.executable, "-c", SCRIPT], cwd=REPO, env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "fx ok" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
