@@ -66,10 +66,72 @@ struct Apb2Params {
   const unsigned long long* col_idx;
   const float* vals;
   SpmmLevels lv;
-  const unsigned* level_chunks;  // [chunks][K + 1][SL_ROW_WORDS] (LevelChunkJob, unpack_operands)
+  // [chunks][K + 1][SL_ROW_WORDS] bf16 patterns, or (L8) [chunks][K + 1][L8_ROW_WORDS] bytes
+  // (LevelChunkJob, unpack_operands)
+  const unsigned* level_chunks;
   int K;
+  float neg4sg;            // L8: -4 * sg (exact), the fma addend that turns p + 4 into p
 };
 
+// sl_step8x2 over an L8 chunk (levels.cuh): lane ol of the octet owns tokens [8 ol, 8 ol + 8),
+// one 8-byte load per nonzero. Per token pair: two PRMTs rebuild (p + 4) in fp32 from the stored
+// bytes and the constant 0x40, then d = fma(p + 4, sg, -4 sg) = fl(p * sg) exactly,
+// q = fl(v * d) and S = fl(S + q) as in sl_step8x2.
+struct L8Octet {
+  const char* xrow;         // chunk buffer + 8 ol bytes
+  int obase;                // first lane of the octet in the warp
+  unsigned long long dd;    // (sg, sg)
+  unsigned long long z4;    // (-4 sg, -4 sg) from a kernel parameter
+  unsigned long long z;     // (-0, -0) from a kernel parameter
+};
+
+template <int SEL>
+__device__ __forceinline__ unsigned l8_level(unsigned w) {
+  unsigned r;
+  asm("prmt.b32 %0, %1, 0x40, %2;" : "=r"(r) : "r"(w), "n"(SEL));
+  return r;
+}
+
+__device__ __forceinline__ void l8_step8x2(const L8Octet& o, unsigned kka, float vva, unsigned long long (&acca)[4],
+                                           unsigned kkb, float vvb, unsigned long long (&accb)[4]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const unsigned koffa = __shfl_sync(0xFFFFFFFFu, kka, o.obase + j) * SL_TOK;
+    const float va = __shfl_sync(0xFFFFFFFFu, vva, o.obase + j);
+    const unsigned koffb = __shfl_sync(0xFFFFFFFFu, kkb, o.obase + j) * SL_TOK;
+    const float vb = __shfl_sync(0xFFFFFFFFu, vvb, o.obase + j);
+    const uint2 xa = *reinterpret_cast<const uint2*>(o.xrow + koffa);
+    const uint2 xb = *reinterpret_cast<const uint2*>(o.xrow + koffb);
+    const unsigned long long va2 = f32x2_pack(va, va), vb2 = f32x2_pack(vb, vb);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const unsigned wa = q < 2 ? xa.x : xa.y, wb = q < 2 ? xb.x : xb.y;
+      // result bytes (low to high): 0, 0, the token's byte, 0x40 (PRMT bytes 5, 5, i, 4 of {0x40, w});
+      // token pair q of the lane = bytes 2 (q & 1), 2 (q & 1) + 1 of word q / 2
+      unsigned la, ha, lb, hb;
+      if ((q & 1) == 0) {
+        la = l8_level<0x4055>(wa);
+        ha = l8_level<0x4155>(wa);
+        lb = l8_level<0x4055>(wb);
+        hb = l8_level<0x4155>(wb);
+      } else {
+        la = l8_level<0x4255>(wa);
+        ha = l8_level<0x4355>(wa);
+        lb = l8_level<0x4255>(wb);
+        hb = l8_level<0x4355>(wb);
+      }
+      const unsigned long long pa = f32x2_pack(__uint_as_float(la), __uint_as_float(ha));
+      const unsigned long long pb = f32x2_pack(__uint_as_float(lb), __uint_as_float(hb));
+      acca[q] = f32x2_add(acca[q], f32x2_mul(va2, f32x2_mul(pa, o.dd, o.z4), o.z));
+      accb[q] = f32x2_add(accb[q], f32x2_mul(vb2, f32x2_mul(pb, o.dd, o.z4), o.z));
+    }
+  }
+}
+
+// L8: the level chunks in the byte format (levels.cuh), double-buffered: the next token block's
+// chunk loads while the current one is in use (two buffers of (K + 1) x 64 bytes in the space of
+// one bf16 chunk). Otherwise one bf16 chunk, reloaded after every residual warp is done with it.
+template <bool L8>
 __global__ void __launch_bounds__(A3_THREADS, 1)
     apb2_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmC, const Apb2Params ap) {
@@ -87,7 +149,7 @@ __global__ void __launch_bounds__(A3_THREADS, 1)
   uint64_t* sfull = tempty + 2;
   uint64_t* sfree = sfull + 2;
   uint64_t* lfull = sfree + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lfull + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lfull + 2);
   unsigned* levels = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(full) + A3_BARS);
 
   const int warp = threadIdx.x >> 5;
@@ -114,6 +176,7 @@ __global__ void __launch_bounds__(A3_THREADS, 1)
       mbar_init(&sfree[b], A3_EPI_WARPS);
     }
     mbar_init(lfull, 1);
+    mbar_init(lfull + 1, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc_pair(tmem_slot, 256);
@@ -265,6 +328,25 @@ __global__ void __launch_bounds__(A3_THREADS, 1)
     const int oct = rt >> 3, ol = rt & 7;
     const SlOctet so{reinterpret_cast<const char*>(levels) + ol * 16, lane & ~7, f32x2_pack(ap.lv.d1, ap.lv.d1),
                      f32x2_pack(ap.lv.neg_zero, ap.lv.neg_zero)};
+    // L8: two chunk buffers; block nb_first + k lives in buffer k & 1
+    const uint32_t l8_bytes = static_cast<uint32_t>(ap.K + 1) * SL_TOK;
+    const char* l8base = reinterpret_cast<const char*>(levels);  // buffer j at l8base + j * l8_bytes
+    L8Octet lo8{l8base + ol * 8, lane & ~7, so.dd, f32x2_pack(ap.neg4sg, ap.neg4sg), so.z};
+    const int nb_first = t0 / nmb, nb_last = t1 > t0 ? (t1 - 1) / nmb : -1;
+    uint32_t l8ph = 0;  // bit j: phase of buffer j
+    auto l8_issue = [&](int k) {  // token block nb_first + k into buffer k & 1
+      if (L8 && rt == 0 && nb_first + k <= nb_last) {
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&lfull[k & 1], l8_bytes);
+        bulk_load_1d(const_cast<char*>(l8base) + (k & 1) * l8_bytes,
+                     ap.level_chunks + static_cast<long long>(nb_first + k) * (ap.K + 1) * L8_ROW_WORDS, l8_bytes,
+                     &lfull[k & 1]);
+      }
+    };
+    if (L8) {
+      l8_issue(0);
+      l8_issue(1);
+    }
     const unsigned zero_row = static_cast<unsigned>(ap.K);
     // Per tile the octet computes its two rows (oct, oct + 64 of the CTA's 128) together
     // (sl_step8x2: two independent chains). Software pipeline over tiles: the row offsets two
@@ -325,7 +407,17 @@ __global__ void __launch_bounds__(A3_THREADS, 1)
       A3_T(p0);
       const int b = it & 1;
       const uint32_t ph = (it >> 1) & 1;
-      if (nb != cur_nb) {  // new token block: bulk-copy its levels once every octet is done with the old
+      if (L8 && nb != cur_nb) {  // new token block: its chunk was issued one block ahead
+        const int k = nb - nb_first;
+        if (k >= 1) {  // every octet is done with block k - 1: its buffer takes block k + 1
+          named_bar_sync(A3_RES_BAR, A3_RES_THREADS);
+          l8_issue(k + 1);
+        }
+        mbar_wait(&lfull[k & 1], (l8ph >> (k & 1)) & 1u);
+        l8ph ^= 1u << (k & 1);
+        lo8.xrow = l8base + (k & 1) * l8_bytes + ol * 8;
+        cur_nb = nb;
+      } else if (nb != cur_nb) {  // new token block: bulk-copy its levels once every octet is done with the old
         named_bar_sync(A3_RES_BAR, A3_RES_THREADS);
         if (rt == 0) {
           const uint32_t bytes = static_cast<uint32_t>(ap.K + 1) * SL_ROW_WORDS * 4;
@@ -352,14 +444,20 @@ __global__ void __launch_bounds__(A3_THREADS, 1)
 
       const unsigned nmax = __reduce_max_sync(0xFFFFFFFFu, max(na, nb_));
       unsigned long long acca[4] = {0ull, 0ull, 0ull, 0ull}, accb[4] = {0ull, 0ull, 0ull, 0ull};  // +0 pairs
-      if (nmax > 0) sl_step8x2(so, ka0, va0, acca, kb0, vb0, accb);
-      if (nmax > 8) sl_step8x2(so, ka1, va1, acca, kb1, vb1, accb);
+      auto step = [&](unsigned kka, float vva, unsigned kkb, float vvb) {
+        if constexpr (L8)
+          l8_step8x2(lo8, kka, vva, acca, kkb, vvb, accb);
+        else
+          sl_step8x2(so, kka, vva, acca, kkb, vvb, accb);
+      };
+      if (nmax > 0) step(ka0, va0, kb0, vb0);
+      if (nmax > 8) step(ka1, va1, kb1, vb1);
       for (unsigned base = 16; base < nmax; base += 8) {
         unsigned kka, kkb;
         float vva, vvb;
         fetch(ra.lo, na, base + ol, kka, vva);
         fetch(rb.lo, nb_, base + ol, kkb, vvb);
-        sl_step8x2(so, kka, vva, acca, kkb, vvb, accb);
+        step(kka, vva, kkb, vvb);
       }
       A3_T(p2);
       mbar_wait(&sfree[b], ph ^ 1u);

@@ -6,6 +6,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -575,7 +576,8 @@ int run_unpack_set(UnpackSet& P, cudaStream_t s) {
   long long work = 0;  // threads per grid row: a warp per slice, or a thread per level-chunk item
   for (int i = 0; i < P.count; ++i) work = std::max(work, P.op[i].rows * P.op[i].groups_per_row * 32);
   const long long lc_items = P.lc.chunks > 0
-                                 ? static_cast<long long>(((P.lc.K + 63) / 64) * 2 * SL_ROW_WORDS + SL_ROW_WORDS) *
+                                 ? static_cast<long long>(((P.lc.K + 63) / 64) * 2 * SL_ROW_WORDS +
+                                                          (P.lc.l8 ? L8_ROW_WORDS : SL_ROW_WORDS)) *
                                        P.lc.chunks
                                  : 0;
   work = std::max(work, lc_items);
@@ -1878,8 +1880,12 @@ int apb2_fused_impl(Ctx& st, int64_t rows, int64_t cols, int64_t wpr, float alph
   lv.d2 = 2.0f * sg;
   lv.d3 = 3.0f * sg;
   lv.neg_zero = -0.0f;
+  // L8 level chunks (levels.cuh) unless BITMM_APB2_L8=0 or -4 sg is not a finite exact addend
+  const bool l8_env = !(std::getenv("BITMM_APB2_L8") && std::atoi(std::getenv("BITMM_APB2_L8")) == 0);
+  const bool l8 = l8_env && std::isfinite(4.0f * sg);
   // the level chunks are staged by the expansion launch, in a grid row of their own
-  const LevelChunkJob lc{lv, static_cast<int>(cols), static_cast<int>(tokens), static_cast<int>(chunks), LC};
+  const LevelChunkJob lc{lv, static_cast<int>(cols), static_cast<int>(tokens), static_cast<int>(chunks), LC,
+                         l8 ? 1 : 0};
   BITMM_TRY(run_unpack_pair(sa, sb, wpr, cols, kpad, A8, B8, st.status, s, true, &lc));
   CUtensorMap ta, tb, tc;
   const int64_t rb = kpad / 2;
@@ -1912,10 +1918,12 @@ int apb2_fused_impl(Ctx& st, int64_t rows, int64_t cols, int64_t wpr, float alph
   ap.lv = lv;
   ap.level_chunks = LC;
   ap.K = static_cast<int>(cols);
+  ap.neg4sg = -4.0f * lv.d1;  // exact (a power-of-two multiple, finite when l8)
   const int smem = apb2_fused_smem_bytes(cols);
+  auto kern = l8 ? apb2_fused_kernel<true> : apb2_fused_kernel<false>;
   // the opt-in limit is one value per kernel: set the maximum once (a per-size value would be
   // overwritten by a smaller K's launch and reject a later larger one)
-  BITMM_TRY(ensure_max_smem(reinterpret_cast<const void*>(apb2_fused_kernel), kMaxDynSmem));
+  BITMM_TRY(ensure_max_smem(reinterpret_cast<const void*>(kern), kMaxDynSmem));
   const int units = std::max(1, std::min(p.num_tiles, st.sms / 2));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(2 * units));
@@ -1932,7 +1940,7 @@ int apb2_fused_impl(Ctx& st, int64_t rows, int64_t cols, int64_t wpr, float alph
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   ProfScope ps("apb2_fused", s);
-  BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, apb2_fused_kernel, ta, tb, tc, ap));
+  BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, ap));
   return launch_check("apb2_fused_kernel");
 }
 

@@ -62,28 +62,72 @@ __device__ __forceinline__ void sl_stage_item(unsigned* xw, int K, int N, int c0
   }
 }
 
+// The byte format of the fused layer's chunks ("L8", [K + 1][SL_TOK] bytes, row K = level 0):
+// level p is stored as 0x80 + 0x20 p, the second-highest byte of the fp32 value p + 4
+// (0x40800000, 0x40A00000, 0x40C00000, 0x40E00000), so one PRMT with the constant 0x40 rebuilds
+// p + 4 in fp32, and fma(p + 4, sg, -4 sg) = fl(p * sg) exactly (the product and the exact
+// -4 sg are summed before the one rounding). Half the bytes of the bf16 patterns.
+constexpr int L8_ROW_WORDS = SL_TOK / 4;  // u32 words per staged column (four levels each)
+__device__ __forceinline__ unsigned level_l8(bool lo, bool hi) { return 0x80u + 0x20u * (2u * hi + lo); }
+
+// sl_stage_item's item (plane word, half, token pair) in the L8 format: 32 u16 (two tokens each)
+// of xb [K + 1][SL_TOK] bytes.
+__device__ __forceinline__ void l8_stage_item(unsigned char* xb, int K, int N, int c0, const SpmmLevels& lv, int i) {
+  const int pair = i & (SL_ROW_WORDS - 1), hw = i / SL_ROW_WORDS;
+  const int word = hw >> 1, half = hw & 1;
+  const int ta = c0 + 2 * pair;
+  unsigned loA = 0, hiA = 0, loB = 0, hiB = 0;
+  if (ta < N) {
+    const long long o = static_cast<long long>(ta) * lv.wpr + word;
+    const unsigned long long t = lv.t[o], h = lv.h[o], m = lv.m[o];
+    hiA = static_cast<unsigned>((t | h) >> (32 * half));
+    loA = static_cast<unsigned>((t | ~(h | m)) >> (32 * half));
+  }
+  if (ta + 1 < N) {
+    const long long o = static_cast<long long>(ta + 1) * lv.wpr + word;
+    const unsigned long long t = lv.t[o], h = lv.h[o], m = lv.m[o];
+    hiB = static_cast<unsigned>((t | h) >> (32 * half));
+    loB = static_cast<unsigned>((t | ~(h | m)) >> (32 * half));
+  }
+  const int k0 = word * 64 + half * 32;
+  unsigned short* dst = reinterpret_cast<unsigned short*>(xb + static_cast<long long>(k0) * SL_TOK) + pair;
+  const int nb = min(32, K - k0);
+  for (int b = 0; b < nb; ++b)
+    dst[b * (SL_TOK / 2)] = static_cast<unsigned short>(level_l8((loA >> b) & 1u, (hiA >> b) & 1u) |
+                                                        (level_l8((loB >> b) & 1u, (hiB >> b) & 1u) << 8));
+}
+
 // Every level chunk of the activations, for the fused layer: out [chunks][K + 1][SL_ROW_WORDS]
-// (L2-resident: tokens x (K + 1) x 2 bytes). chunks = 0: none.
+// words (bf16 patterns; L2-resident: tokens x (K + 1) x 2 bytes), or with l8 [chunks][K + 1]
+// [L8_ROW_WORDS] (the L8 bytes, half that). chunks = 0: none.
 struct LevelChunkJob {
   SpmmLevels lv;
   int K, N, chunks;
   unsigned* out;
+  int l8;
 };
 
+__device__ __forceinline__ int level_chunk_row_words(const LevelChunkJob& j) { return j.l8 ? L8_ROW_WORDS : SL_ROW_WORDS; }
+
 __device__ __forceinline__ long long level_chunk_items(const LevelChunkJob& j) {
-  return static_cast<long long>(((j.K + 63) >> 6) * 2 * SL_ROW_WORDS + SL_ROW_WORDS) * j.chunks;
+  return static_cast<long long>(((j.K + 63) >> 6) * 2 * SL_ROW_WORDS + level_chunk_row_words(j)) * j.chunks;
 }
 
 // Item i of the job (one (chunk, plane word, half, token pair), or a word of a zero row).
 __device__ __forceinline__ void level_chunk_item(const LevelChunkJob& j, long long i) {
   const int items = ((j.K + 63) >> 6) * 2 * SL_ROW_WORDS;
-  const long long per_chunk = items + SL_ROW_WORDS;
+  const int rw = level_chunk_row_words(j);
+  const long long per_chunk = items + rw;
   const int chunk = static_cast<int>(i / per_chunk), q = static_cast<int>(i - chunk * per_chunk);
-  unsigned* xw = j.out + static_cast<long long>(chunk) * (j.K + 1) * SL_ROW_WORDS;
-  if (q < items)
-    sl_stage_item(xw, j.K, j.N, chunk * SL_TOK, j.lv, q);
-  else
-    xw[static_cast<long long>(j.K) * SL_ROW_WORDS + (q - items)] = 0u;
+  unsigned* xw = j.out + static_cast<long long>(chunk) * (j.K + 1) * rw;
+  if (q < items) {
+    if (j.l8)
+      l8_stage_item(reinterpret_cast<unsigned char*>(xw), j.K, j.N, chunk * SL_TOK, j.lv, q);
+    else
+      sl_stage_item(xw, j.K, j.N, chunk * SL_TOK, j.lv, q);
+  } else {
+    xw[static_cast<long long>(j.K) * rw + (q - items)] = j.l8 ? 0x80808080u : 0u;
+  }
 }
 
 }  // namespace bitmm_dev

@@ -23,7 +23,8 @@ d = [T(layer.bin.words.view(np.int64)), T(alpha), T(r.row_ptr.view(np.int64)), T
 s = torch.cuda.current_stream().cuda_stream
 P = lambda x: x.data_ptr()  # noqa: E731
 outs = {}
-MODES = {"fused": {"BITMM_APB2_FUSED": "1"},
+MODES = {"fused": {"BITMM_APB2_FUSED": "1", "BITMM_APB2_L8": "1"},
+         "fused bf16 chunks": {"BITMM_APB2_FUSED": "1", "BITMM_APB2_L8": "0"},
          "two-pass bf16 levels": {"BITMM_APB2_FUSED": "0", "BITMM_SPMM_LEVELS_V1": "0"},
          "two-pass fp32 levels (v1)": {"BITMM_APB2_FUSED": "0", "BITMM_SPMM_LEVELS_V1": "1"}}
 only = sys.argv[sys.argv.index("--only") + 1] if "--only" in sys.argv else None

@@ -174,18 +174,28 @@ def test_gpu_device_path_config4_shape(orc):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("form", ["fused", "two-pass", "two-pass-fp32"])
+@pytest.mark.parametrize("g", [1e-39, 3.0e36])
+def test_gpu_fused_extreme_scales(orc, monkeypatch, g):
+    """The fused layer's L8 chunks rebuild d = fl(p * s * g) as fma(p + 4, sg, -4 sg): exact also
+    when sg is subnormal (g = 1e-39) or large (4 sg near the top of the fp32 range)."""
+    monkeypatch.setenv("BITMM_APB2_FUSED", "1")
+    _gpu_vs_oracle(orc, 300, 768, 200, g=g, seed=5)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("form", ["fused", "fused-bf16", "two-pass", "two-pass-fp32"])
 @pytest.mark.parametrize("rows,cols,tokens", [(300, 768, 332), (513, 130, 1000), (257, 973, 64), (33, 974, 8),
                                               (64, 1100, 68), (1000, 256, 4)])
 def test_gpu_every_form_bit_exact(orc, monkeypatch, form, rows, cols, tokens):
-    """The three device forms of the layer — residual fused into the GEMM epilogue
-    (apb2_fused_kernel), GEMM then the bf16-level SpMM (spmm_levels_kernel), GEMM then the
+    """The device forms of the layer — residual fused into the GEMM epilogue
+    (apb2_fused_kernel, with L8 or bf16 level chunks), GEMM then the bf16-level SpMM (spmm_levels_kernel), GEMM then the
     fp32-level SpMM (spmm_xchunk_kernel<LEVELS>) — each bit-identical to the oracle, at shapes
     with ragged row blocks, token blocks and K (cols 1100 exceeds the fused kernel's shared
     memory and falls back to the two-pass form)."""
     from paper_2306_08960_b200 import _lib
     lib = _lib.load()
-    monkeypatch.setenv("BITMM_APB2_FUSED", "1" if form == "fused" else "0")
+    monkeypatch.setenv("BITMM_APB2_FUSED", "1" if form.startswith("fused") else "0")
+    monkeypatch.setenv("BITMM_APB2_L8", "0" if form == "fused-bf16" else "1")
     monkeypatch.setenv("BITMM_SPMM_LEVELS_V1", "1" if form == "two-pass-fp32" else "0")
     lib.bitmm_profile_reset()
     lib.bitmm_profile_enable(1)
@@ -198,7 +208,7 @@ def test_gpu_every_form_bit_exact(orc, monkeypatch, form, rows, cols, tokens):
         lib.bitmm_profile_enable(0)
         lib.bitmm_profile_reset()
     # the form the switches and the shape select is the one that ran
-    if form == "fused" and cols <= 973:
+    if form.startswith("fused") and cols <= 973:
         assert "apb2_fused" in ran, ran
     elif form == "two-pass-fp32":
         assert "apb2_fused" not in ran and "spmm_levels" not in ran, ran
