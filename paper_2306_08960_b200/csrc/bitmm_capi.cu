@@ -14,6 +14,7 @@
 #include <memory>
 #include <mutex>
 #include <set>
+#include <thread>
 #include <tuple>
 #include <string>
 #include <vector>
@@ -1116,6 +1117,12 @@ int run_pipelined(HostCtx& st, cudaStream_t s, int64_t total, int64_t step, Body
 // copies. Measured per routine with 2, 4 and 8 parts per slice (profiles/dev/ab_wire_parts.sh):
 // the 4 MiB slices of 1/1 and 2/2 were fastest in two parts, the 8 MiB slices of 1/2 in four.
 constexpr size_t kWirePartBytes = size_t{2} << 20;
+// BITMM_WIRE_SPIN=1: the host pool polls each part's copy event instead of sleeping on a
+// blocking-sync event (A/B of the wake-up latency). Read once: the events are created with it.
+bool wire_spin() {
+  static const bool on = std::getenv("BITMM_WIRE_SPIN") && std::atoi(std::getenv("BITMM_WIRE_SPIN")) == 1;
+  return on;
+}
 constexpr int kWireMaxParts = 8;
 
 struct OutBlock {
@@ -1242,7 +1249,8 @@ int run_pipelined_wire(HostCtx& st, cudaStream_t s, int64_t total, int64_t step,
       g_d2h_bytes += bytes;
       if (st.wire_ev.size() <= parts.size()) {
         cudaEvent_t e = nullptr;
-        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync) != cudaSuccess) {
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming | (wire_spin() ? 0 : cudaEventBlockingSync)) !=
+            cudaSuccess) {
           rc = fail(BITMM_ERR_CUDA, "wire event create");
           break;
         }
@@ -1279,7 +1287,14 @@ int run_pipelined_wire(HostCtx& st, cudaStream_t s, int64_t total, int64_t step,
   host_pool_run(static_cast<int>(tasks.size()), [&](int i) {
     const Task& t = tasks[i];
     const auto w0 = trace ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
-    if (cudaEventSynchronize(st.wire_ev[t.part]) != cudaSuccess) {
+    if (wire_spin()) {  // poll the part's event (no sleep / wake-up on the blocking-sync path)
+      cudaError_t q;
+      while ((q = cudaEventQuery(st.wire_ev[t.part])) == cudaErrorNotReady) std::this_thread::yield();
+      if (q != cudaSuccess) {
+        copy_err.store(1);
+        return;
+      }
+    } else if (cudaEventSynchronize(st.wire_ev[t.part]) != cudaSuccess) {
       copy_err.store(1);
       return;
     }
