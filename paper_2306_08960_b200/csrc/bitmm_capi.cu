@@ -77,6 +77,11 @@ struct Arena {
 //    pinned buffers and events, so concurrent host calls from different threads run side by
 //    side. A lease ends with its streams drained, so no copy still reads the caller's buffers
 //    after the call returns, whatever the exit path.
+struct SchedBuf {
+  void* dev;      // the pieces (int4), then the per-unit offsets (int)
+  size_t pbytes;  // bytes of the pieces
+};
+
 struct Ctx {
   int dev = 0;
   int sms = 0;
@@ -87,6 +92,8 @@ struct Ctx {
   Arena ws;                // expanded operands, APB intermediates, scan temp
   Arena codes;             // 2-bit level codes of the in-GEMM expansion path (fx_gemm)
   unsigned ws_turn = 0;    // ping-pong half of the expanded-operand workspace
+  // balanced GEMM schedules (TcGroup::sched) by group shape, in device memory, kept
+  std::map<std::vector<long long>, SchedBuf> sched_cache;
 };
 
 struct HostCtx {
@@ -635,6 +642,70 @@ struct GemmProblem {
   TcParams p;
 };
 
+// Balanced schedule of a group (TcGroup::sched, BITMM_TC_BALANCE=1; measured, not the default):
+// the output column-work in 32-column units, problem by problem and 256-row block by block, cut
+// into `units` contiguous stretches of equal length, each cut into pieces of at most BN columns
+// that stay inside one row block. At 4096^2 (BN 192) every CTA pair then multiplies 896 columns
+// instead of five 192-column tiles (960), but the pairs no longer work on neighbouring tiles at
+// the same time: 1/1 4096^3 39.9 vs 37.9 us, the bench step 2026 vs 2254 T-upd/s, config 5
+// 23.6 vs 10.0 ms (operand reuse in L2 lost; profiles/dev/balance_ab.sh). Round-robin tiles in
+// the L2-grouped raster stay the default.
+bool tc_balance() {
+  const char* e = std::getenv("BITMM_TC_BALANCE");
+  return e && std::atoi(e) == 1;
+}
+
+int tc_schedule(Ctx& st, const TcParams* prob, int count, int units, int bn, cudaStream_t s, const int4** sched,
+                const int** unit_begin, void** free_after) {
+  *free_after = nullptr;
+  std::vector<long long> key{units, bn, count};
+  for (int i = 0; i < count; ++i) {
+    key.push_back(prob[i].M);
+    key.push_back(prob[i].N);
+  }
+  auto it = st.sched_cache.find(key);
+  if (it == st.sched_cache.end()) {
+    long long total = 0;
+    for (int i = 0; i < count; ++i) total += static_cast<long long>(prob[i].num_m_blocks) * ((prob[i].N + 31) / 32);
+    const long long cap = (total + units - 1) / units;
+    std::vector<int4> pieces;
+    std::vector<int> begin{0};
+    long long used = 0;
+    for (int i = 0; i < count; ++i)
+      for (int mb = 0; mb < prob[i].num_m_blocks; ++mb) {
+        const int cols32 = (prob[i].N + 31) / 32;
+        for (int c = 0; c < cols32;) {
+          if (used == cap) {
+            begin.push_back(static_cast<int>(pieces.size()));
+            used = 0;
+          }
+          const int w = static_cast<int>(std::min<long long>({bn / 32, cols32 - c, cap - used}));
+          pieces.push_back(make_int4(i | ((w * 32) << 16), mb, c * 32, 0));
+          c += w;
+          used += w;
+        }
+      }
+    while (static_cast<int>(begin.size()) <= units) begin.push_back(static_cast<int>(pieces.size()));
+    const size_t pbytes = pieces.size() * sizeof(int4);
+    std::vector<uint8_t> host(pbytes + begin.size() * sizeof(int));
+    std::memcpy(host.data(), pieces.data(), pbytes);
+    std::memcpy(host.data() + pbytes, begin.data(), begin.size() * sizeof(int));
+    SchedBuf b{nullptr, pbytes};
+    BITMM_CUDA_TRY(cudaMallocAsync(&b.dev, host.size(), s));
+    BITMM_CUDA_TRY(cudaMemcpyAsync(b.dev, host.data(), host.size(), cudaMemcpyHostToDevice, s));
+    if (st.sched_cache.size() >= 256) {  // shape churn: used once, freed behind the launch
+      *sched = static_cast<const int4*>(b.dev);
+      *unit_begin = reinterpret_cast<const int*>(static_cast<uint8_t*>(b.dev) + pbytes);
+      *free_after = b.dev;
+      return BITMM_OK;
+    }
+    it = st.sched_cache.emplace(key, b).first;
+  }
+  *sched = static_cast<const int4*>(it->second.dev);
+  *unit_begin = reinterpret_cast<const int*>(static_cast<const uint8_t*>(it->second.dev) + it->second.pbytes);
+  return BITMM_OK;
+}
+
 // Launch one persistent cta_group::2 GEMM over a group of problems (tiles concatenated).
 template <Kind KIND, Epi EPI, int BN, int NP>
 int run_tc_group(Ctx& st, const GemmProblem* probs, int count, cudaStream_t s) {
@@ -674,6 +745,8 @@ int run_tc_group(Ctx& st, const GemmProblem* probs, int count, cudaStream_t s) {
   g.count = count;
   for (int i = count; i <= NP; ++i) g.tile_begin[i] = tiles;
   const int units = std::min(tiles, st.sms / 2);
+  void* sched_free = nullptr;
+  if (tc_balance()) BITMM_TRY(tc_schedule(st, g.prob, count, units, BN, s, &g.sched, &g.unit_begin, &sched_free));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(2 * units));
   cfg.blockDim = dim3(TC_THREADS);
@@ -690,7 +763,9 @@ int run_tc_group(Ctx& st, const GemmProblem* probs, int count, cudaStream_t s) {
   cfg.numAttrs = 2;
   ProfScope ps(KIND == Kind::I8 ? "tc_gemm_i8" : "tc_gemm_f4", s);
   BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, g));
-  return launch_check("tc_gemm_kernel");
+  BITMM_TRY(launch_check("tc_gemm_kernel"));
+  if (sched_free) BITMM_CUDA_TRY(cudaFreeAsync(sched_free, s));
+  return BITMM_OK;
 }
 
 // Dispatch a group on the operand kind: one problem with a fixed epilogue, or up to

@@ -128,12 +128,13 @@ template <Epi EPI, int BN, bool F32ACC = false, int EPI_BUFS = 2>
 __device__ __forceinline__ void tc_epilogue_tile(const TcParams& p, const CUtensorMap* tmC,
                                                  uint32_t tmem_acc, int quad, int lane,
                                                  int row_base, int col_base, float* stg,
-                                                 uint32_t& buf, const float* cs, float row_mul) {
+                                                 uint32_t& buf, const float* cs, float row_mul,
+                                                 int width = BN) {
   // 16-byte stores in the fallback only when every row start is 16-byte aligned
   const void* out_base = (EPI == Epi::I32) ? static_cast<const void*>(p.out_i32) : static_cast<const void*>(p.out_f32);
   const bool vec_ok = ((p.N | static_cast<int>(p.ldc & 3)) & 3) == 0 && (reinterpret_cast<uintptr_t>(out_base) & 15) == 0;
   const uint32_t lane_base = tmem_acc + (static_cast<uint32_t>(quad * 32) << 16);
-  const int nch = min(BN / 32, (p.N - col_base + 31) / 32);
+  const int nch = min(width / 32, (p.N - col_base + 31) / 32);
   // One 32-column chunk: per-thread (row) transform, staged into smem, then stored.
   auto drain = [&](uint32_t (&v)[32], int c) {
     const int col0 = col_base + c * 32;
@@ -254,6 +255,13 @@ struct TcGroup {
   TcParams prob[NP];
   int count;
   int tile_begin[NP + 1];  // problem i owns tiles [tile_begin[i], tile_begin[i+1])
+  // Balanced schedule (optional): CTA pair u walks pieces [unit_begin[u], unit_begin[u + 1]) of
+  // `sched`, each {problem | width << 16, m block, first column, 0}: a contiguous stretch of the
+  // output column-work, cut into pieces of at most BN columns (multiples of 32), so every pair
+  // gets the same number of columns instead of a whole number of BN-wide tiles. Null: tiles
+  // round-robin.
+  const int4* sched;
+  const int* unit_begin;
 };
 
 template <int NP>
@@ -265,6 +273,46 @@ __device__ __forceinline__ int tc_problem_of(const TcGroup<NP>& g, int t) {
     if (i < g.count && t >= g.tile_begin[i]) pi = i;
   return pi;
 }
+
+// The tiles (or balanced pieces) one CTA pair walks, in order: problem, m block, first output
+// column and width of each.
+template <int NP, int BN, int MC>
+struct TcTileIter {
+  const TcGroup<NP>& g;
+  int i, end, step, pair;
+  __device__ __forceinline__ TcTileIter(const TcGroup<NP>& g_, int unit, int num_units, int pair_)
+      : g(g_), pair(pair_) {
+    if (g.sched) {
+      i = g.unit_begin[unit];
+      end = g.unit_begin[unit + 1];
+      step = 1;
+    } else {
+      i = unit;
+      end = g.tile_begin[g.count];
+      step = num_units;
+    }
+  }
+  __device__ __forceinline__ bool next(int& pi, int& mb, int& n0, int& width) {
+    if (i >= end) return false;
+    if (g.sched) {
+      const int4 r = g.sched[i];
+      pi = r.x & 0xFFFF;
+      width = r.x >> 16;
+      mb = r.y;
+      n0 = r.z;
+    } else {
+      pi = tc_problem_of(g, i);
+      const TcParams& p = g.prob[pi];
+      int nb;
+      tc_tile_coords(i - g.tile_begin[pi], p, (p.num_n_blocks + MC - 1) / MC, mb, nb);
+      n0 = (nb * MC + pair) * BN;
+      width = BN;
+    }
+    i += step;
+    return true;
+  }
+};
+
 
 // Persistent cta_group::2 GEMM (one CTA pair per cluster). EPI == Epi::ANY dispatches each
 // problem's epilogue (I32 or F32) at run time.
@@ -297,7 +345,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int pair = static_cast<int>(crank >> 1);  // pair within the cluster (MC = 2)
   const int unit = static_cast<int>(cluster_id_x());
   const int num_units = static_cast<int>(num_clusters_x());
-  const int num_tiles = g.tile_begin[g.count];
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < g.count; ++i) {
@@ -349,14 +396,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       constexpr uint32_t kTx = 2 * (S::A_STAGE + S::B_STAGE);
-      for (int tile = unit; tile < num_tiles; tile += num_units) {
-        const int pi = tc_problem_of(g, tile);
+      TcTileIter<NP, BN, MC> tiles(g, unit, num_units, pair);
+      int pi, mb, n0, width;
+      while (tiles.next(pi, mb, n0, width)) {
         const TcParams& p = g.prob[pi];
-        int mb, nb;
-        tc_tile_coords(tile - g.tile_begin[pi], p, (p.num_n_blocks + MC - 1) / MC, mb, nb);
-        nb = nb * MC + pair;
         const int a_row = mb * S::TILE_M + static_cast<int>(rank) * S::A_ROWS;
-        const int b_row = nb * BN + static_cast<int>(rank) * S::B_ROWS;
+        // each CTA stages its half of the piece's B rows (a narrower piece leaves the box's
+        // last rows unused by the MMA)
+        const int b_row = n0 + static_cast<int>(rank) * (width / 2);
         const CUtensorMap* ma = &g.a[pi];
         const CUtensorMap* mbm = &g.b[pi];
         const int nkb = p.num_kb;
@@ -397,8 +444,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #ifdef TC_GEMM_STATS
       long long st_te = 0, st_fu = 0, st_start = clock64();
 #endif
-      for (int tile = unit; tile < num_tiles; tile += num_units, ++it) {
-        const int num_kb = g.prob[tc_problem_of(g, tile)].num_kb;
+      TcTileIter<NP, BN, MC> tiles(g, unit, num_units, pair);
+      int pi, mb, n0, width;
+      for (; tiles.next(pi, mb, n0, width); ++it) {
+        const int num_kb = g.prob[pi].num_kb;
+        // the piece's width as the MMA's N (a multiple of 32, so of 16 as M = 256 requires)
+        const uint32_t idesc_t = (idesc & ~(0x3Fu << 17)) | ((static_cast<uint32_t>(width) >> 3) << 17);
         const int acc = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
 #ifdef TC_GEMM_STATS
@@ -423,7 +474,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const uint64_t bd = b_desc0 + static_cast<uint64_t>((stage * S::B_STAGE) >> 4);
 #pragma unroll
           for (int k = 0; k < TC_BK_BYTES / 32; ++k)
-            mma_pair_elect<KID>(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0, sfa, sfb);
+            mma_pair_elect<KID>(d_tmem, ad + 2 * k, bd + 2 * k, idesc_t, (kb | k) != 0, sfa, sfb);
           mma_commit_pair_elect(&empty[stage], MC == 2 ? 0xF : 0x3);
           if (++stage == S::STAGES) {
             stage = 0;
@@ -449,12 +500,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #ifdef TC_GEMM_STATS
     long long st_tf = 0, st_busy = 0;
 #endif
-    for (int tile = unit; tile < num_tiles; tile += num_units, ++it) {
-      const int pi = tc_problem_of(g, tile);
+    TcTileIter<NP, BN, MC> tiles(g, unit, num_units, pair);
+    int pi, mb, n0, width;
+    for (; tiles.next(pi, mb, n0, width); ++it) {
       const TcParams p = g.prob[pi];  // by value: its fields stay in registers in the epilogue
-      int mb, nb;
-      tc_tile_coords(tile - g.tile_begin[pi], p, (p.num_n_blocks + MC - 1) / MC, mb, nb);
-      nb = nb * MC + pair;
       const int acc = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
       const int row_base = mb * S::TILE_M + static_cast<int>(rank) * 128 + quad * 32;
@@ -474,8 +523,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
         for (int j = 0; j < CS_PER_THREAD; ++j) {
           const int i = (warp - 2) * 32 + lane + j * 128;
-          const int cc = nb * BN + i;
-          csv[j] = (i < BN && cc < p.N) ? p.col_scale[cc] : 0.0f;
+          const int cc = n0 + i;
+          csv[j] = (i < width && cc < p.N) ? p.col_scale[cc] : 0.0f;
         }
       }
 #ifdef TC_GEMM_STATS
@@ -505,13 +554,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if constexpr (EPI == Epi::ANY) {
         if (p.epi == static_cast<int>(Epi::I32))
           tc_epilogue_tile<Epi::I32, BN, kF32Acc, S::EPI_BUFS>(p, &g.c[pi], tacc, quad, lane,
-                                                               row_base, nb * BN, stg, buf, cs, row_mul);
+                                                               row_base, n0, stg, buf, cs, row_mul, width);
         else
           tc_epilogue_tile<Epi::F32, BN, kF32Acc, S::EPI_BUFS>(p, &g.c[pi], tacc, quad, lane,
-                                                               row_base, nb * BN, stg, buf, cs, row_mul);
+                                                               row_base, n0, stg, buf, cs, row_mul, width);
       } else {
         tc_epilogue_tile<EPI, BN, kF32Acc, S::EPI_BUFS>(p, &g.c[pi], tacc, quad, lane, row_base,
-                                                        nb * BN, stg, buf, cs, row_mul);
+                                                        n0, stg, buf, cs, row_mul, width);
       }
 #ifdef TC_GEMM_STATS
       st_busy += clock64() - t3;
