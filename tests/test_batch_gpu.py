@@ -23,7 +23,11 @@ def _case(rng, m, n, n2, k):
 
 
 @pytest.mark.parametrize("m,n,n2,k", [(4096, 4096, 8192, 4096), (300, 517, 1000, 777), (1, 1, 1, 1)])
-def test_batch_matches_single_calls(orc, m, n, n2, k):
+@pytest.mark.parametrize("balance", ["0", "1"])
+def test_batch_matches_single_calls(orc, monkeypatch, m, n, n2, k, balance):
+    """balance "1": the GEMM walks the balanced piece schedule (BITMM_TC_BALANCE=1: contiguous
+    column stretches per CTA pair, pieces narrower than the tile with the MMA's N per piece)."""
+    monkeypatch.setenv("BITMM_TC_BALANCE", balance)
     import torch
     from paper_2306_08960_b200 import device
     rng = np.random.default_rng(m + n + k)
