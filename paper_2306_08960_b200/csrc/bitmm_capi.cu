@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -1274,8 +1275,86 @@ int run_pipelined_wire(HostCtx& st, cudaStream_t s, int64_t total, int64_t step,
       mark("i" + std::to_string(j), st.h2d);
     }
   }
+  // The copied parts of every slice, known before anything is enqueued: ~kWirePartBytes of wire
+  // words each, split by output rows.
+  std::vector<int> slice_parts{0};  // slice i owns parts [slice_parts[i], slice_parts[i + 1])
+  {
+    size_t off = 0;
+    for (int64_t c0 = 0; c0 < total; c0 += step) {
+      const OutBlock b = block(c0, std::min(total, c0 + step));
+      const int64_t cells = b.rows * b.cols;
+      const int64_t nparts = std::min<int64_t>(
+          kWireMaxParts, std::max<int64_t>(1, (cells * 2 + kWirePartBytes / 2) / kWirePartBytes));
+      const int64_t per = (b.rows + nparts - 1) / nparts;
+      for (int64_t r0 = 0; r0 < b.rows; r0 += per)
+        parts.push_back(Part{b, b.row0 + r0, b.row0 + std::min(b.rows, r0 + per), off});
+      slice_parts.push_back(static_cast<int>(parts.size()));
+      off += static_cast<size_t>(cells);
+    }
+  }
+  while (st.wire_ev.size() < parts.size()) {
+    cudaEvent_t e = nullptr;
+    BITMM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | (wire_spin() ? 0 : cudaEventBlockingSync)));
+    st.wire_ev.push_back(e);
+  }
+  // One pool batch for the whole call: each task widens a row range of one part after waiting
+  // for that part's copy. Tasks are handed out in part order, so the pool follows the copies
+  // without a barrier per part. The batch starts BEFORE the slices are enqueued (the enqueue
+  // takes ~0.3 ms of host time for eight slices, during which the first parts already land): a
+  // task first waits until its part's copy has been enqueued, then for the copy itself.
+  struct Task {
+    int part;
+    int64_t r0, r1;
+  };
+  std::vector<Task> tasks;
+  for (int p = 0; p < static_cast<int>(parts.size()); ++p) {
+    const Part& q = parts[p];
+    const int64_t rows_per_task = std::max<int64_t>(1, (int64_t{1} << 16) / std::max<int64_t>(1, q.b.cols));
+    for (int64_t r = q.r0; r < q.r1; r += rows_per_task) tasks.push_back(Task{p, r, std::min(q.r1, r + rows_per_task)});
+  }
+  std::mutex ready_mu;
+  std::condition_variable ready_cv;
+  int parts_ready = 0;  // parts whose copy and event are enqueued
+  bool abort = false;   // the enqueue failed: the remaining tasks return at once
+  auto publish = [&](int ready, bool failed) {
+    {
+      std::lock_guard<std::mutex> lk(ready_mu);
+      parts_ready = ready;
+      abort = abort || failed;
+    }
+    ready_cv.notify_all();
+  };
+  const auto t0 = std::chrono::steady_clock::now();
+  std::atomic<int> copy_err{0};
+  std::atomic<int64_t> wait_ns{0};
+  // BITMM_WIRE_EARLY=0: the batch starts after the whole enqueue (round-1 order, A/B)
+  const bool early = !(std::getenv("BITMM_WIRE_EARLY") && std::atoi(std::getenv("BITMM_WIRE_EARLY")) == 0);
+  auto task = [&](int i) {
+    const Task& t = tasks[i];
+    {
+      std::unique_lock<std::mutex> lk(ready_mu);
+      ready_cv.wait(lk, [&] { return abort || parts_ready > t.part; });
+      if (abort) return;
+    }
+    const auto w0 = trace ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
+    if (wire_spin()) {  // poll the part's event (no sleep / wake-up on the blocking-sync path)
+      cudaError_t q;
+      while ((q = cudaEventQuery(st.wire_ev[t.part])) == cudaErrorNotReady) std::this_thread::yield();
+      if (q != cudaSuccess) {
+        copy_err.store(1);
+        return;
+      }
+    } else if (cudaEventSynchronize(st.wire_ev[t.part]) != cudaSuccess) {
+      copy_err.store(1);
+      return;
+    }
+    if (trace) wait_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - w0).count();
+    const Part& q = parts[t.part];
+    if (skip_widen) return;
+    wire_expand_range(wo, hw + q.off, q.b.row0, q.b.col0, q.b.cols, t.r0, t.r1);
+  };
+  if (early) host_pool_start(static_cast<int>(tasks.size()), task);
   int rc = BITMM_OK;
-  size_t off = 0;
   int i = 0;
   for (int64_t c0 = 0; c0 < total && rc == BITMM_OK; c0 += step, ++i) {
     const int64_t c1 = std::min(total, c0 + step);
@@ -1296,7 +1375,8 @@ int run_pipelined_wire(HostCtx& st, cudaStream_t s, int64_t total, int64_t step,
     mark("h" + std::to_string(i), s);
     rc = gemm(c0, c1);
     if (rc != BITMM_OK) break;
-    const OutBlock b = block(c0, c1);
+    const OutBlock b = parts[slice_parts[i]].b;
+    const size_t off = parts[slice_parts[i]].off;
     // the narrowing runs on the GEMM's stream: on the copy stream it would wait for SMs
     // behind the next slice's persistent GEMM
     const int64_t cells = b.rows * b.cols;
@@ -1311,78 +1391,33 @@ int run_pipelined_wire(HostCtx& st, cudaStream_t s, int64_t total, int64_t step,
       rc = fail(BITMM_ERR_CUDA, std::string("pipeline event: ") + cudaGetErrorString(cudaGetLastError()));
       break;
     }
-    const int64_t nparts = std::min<int64_t>(
-        kWireMaxParts, std::max<int64_t>(1, (cells * 2 + kWirePartBytes / 2) / kWirePartBytes));
-    const int64_t per = (b.rows + nparts - 1) / nparts;
-    for (int64_t r0 = 0; r0 < b.rows; r0 += per) {
-      const int64_t r1 = std::min(b.rows, r0 + per);
-      const size_t o = off + static_cast<size_t>(r0 * b.cols), bytes = static_cast<size_t>((r1 - r0) * b.cols) * 2;
+    for (int p = slice_parts[i]; p < slice_parts[i + 1] && rc == BITMM_OK; ++p) {
+      const Part& q = parts[p];
+      const size_t o = q.off + static_cast<size_t>((q.r0 - b.row0) * b.cols);
+      const size_t bytes = static_cast<size_t>((q.r1 - q.r0) * b.cols) * 2;
       if (cudaMemcpyAsync(hw + o, dwire + o, bytes, cudaMemcpyDeviceToHost, st.d2h) != cudaSuccess) {
         rc = fail(BITMM_ERR_CUDA, std::string("wire copy: ") + cudaGetErrorString(cudaGetLastError()));
         break;
       }
       g_d2h_bytes += bytes;
-      if (st.wire_ev.size() <= parts.size()) {
-        cudaEvent_t e = nullptr;
-        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming | (wire_spin() ? 0 : cudaEventBlockingSync)) !=
-            cudaSuccess) {
-          rc = fail(BITMM_ERR_CUDA, "wire event create");
-          break;
-        }
-        st.wire_ev.push_back(e);
-      }
-      if (cudaEventRecord(st.wire_ev[parts.size()], st.d2h) != cudaSuccess) {
-        rc = fail(BITMM_ERR_CUDA, "wire event record");
-        break;
-      }
-      parts.push_back(Part{b, b.row0 + r0, b.row0 + r1, off});
+      if (cudaEventRecord(st.wire_ev[p], st.d2h) != cudaSuccess) rc = fail(BITMM_ERR_CUDA, "wire event record");
     }
+    if (rc != BITMM_OK) break;
+    if (early) publish(slice_parts[i + 1], false);
     mark("c" + std::to_string(i), st.d2h);
-    off += static_cast<size_t>(cells);
   }
-  // One pool batch for the whole call: each task widens a row range of one part after
-  // waiting for that part's copy. Tasks are handed out in part order, so the pool follows
-  // the copies without a barrier per part.
-  struct Task {
-    int part;
-    int64_t r0, r1;
-  };
-  std::vector<Task> tasks;
-  if (rc == BITMM_OK) {
-    for (int p = 0; p < static_cast<int>(parts.size()); ++p) {
-      const Part& q = parts[p];
-      const int64_t rows_per_task = std::max<int64_t>(1, (int64_t{1} << 16) / std::max<int64_t>(1, q.b.cols));
-      for (int64_t r = q.r0; r < q.r1; r += rows_per_task)
-        tasks.push_back(Task{p, r, std::min(q.r1, r + rows_per_task)});
-    }
+  if (early) {
+    if (rc != BITMM_OK) publish(parts_ready, true);
+    host_pool_join();
+  } else if (rc == BITMM_OK) {
+    publish(static_cast<int>(parts.size()), false);
+    host_pool_run(static_cast<int>(tasks.size()), task);
   }
-  const auto t0 = std::chrono::steady_clock::now();
-  std::atomic<int> copy_err{0};
-  std::atomic<int64_t> wait_ns{0};
-  host_pool_run(static_cast<int>(tasks.size()), [&](int i) {
-    const Task& t = tasks[i];
-    const auto w0 = trace ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
-    if (wire_spin()) {  // poll the part's event (no sleep / wake-up on the blocking-sync path)
-      cudaError_t q;
-      while ((q = cudaEventQuery(st.wire_ev[t.part])) == cudaErrorNotReady) std::this_thread::yield();
-      if (q != cudaSuccess) {
-        copy_err.store(1);
-        return;
-      }
-    } else if (cudaEventSynchronize(st.wire_ev[t.part]) != cudaSuccess) {
-      copy_err.store(1);
-      return;
-    }
-    if (trace) wait_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - w0).count();
-    const Part& q = parts[t.part];
-    if (skip_widen) return;
-    wire_expand_range(wo, hw + q.off, q.b.row0, q.b.col0, q.b.cols, t.r0, t.r1);
-  });
   if (trace) {
     const auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
     const auto t1 = std::chrono::steady_clock::now();
     cudaEventSynchronize(st.wire_ev[0]);
-    std::fprintf(stderr, "[bitmm wire] %zu parts, %zu tasks, %zu words: enqueue %.3f ms, host widen %.3f ms "
+    std::fprintf(stderr, "[bitmm wire] %zu parts, %zu tasks, %zu words: setup %.3f ms, enqueue + host widen %.3f ms "
                  "(%d threads, %.3f thread-ms waiting for copies)\n",
                  parts.size(), tasks.size(), wire_words, ms(t_call, t0), ms(t0, t1), host_pool_size(),
                  wait_ns.load() * 1e-6);

@@ -57,6 +57,33 @@ class HostPool {
     job_ = nullptr;
   }
 
+  // A batch the workers start at once while the caller goes on (it joins the batch later).
+  // The pool stays reserved for this caller until join.
+  void start(int n, std::function<void(int)> f) {
+    std::unique_lock<std::mutex> call(call_mu_);  // one batch at a time, held until join
+    owned_ = std::move(f);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = &owned_;
+      n_ = n;
+      next_.store(0);
+      pending_ = static_cast<int>(workers_.size());
+      ++gen_;
+    }
+    cv_.notify_all();
+    call_lk_ = std::move(call);
+  }
+  void join() {
+    drain();
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      done_cv_.wait(lk, [&] { return pending_ == 0; });
+      job_ = nullptr;
+    }
+    owned_ = nullptr;
+    call_lk_.unlock();
+  }
+
  private:
   HostPool() {
     int n = static_cast<int>(std::thread::hardware_concurrency());
@@ -92,6 +119,8 @@ class HostPool {
 
   std::vector<std::thread> workers_;
   std::mutex call_mu_, mu_;
+  std::unique_lock<std::mutex> call_lk_;  // start() .. join(): the batch's hold on call_mu_
+  std::function<void(int)> owned_;        // start()'s job
   std::condition_variable cv_, done_cv_;
   const std::function<void(int)>* job_ = nullptr;
   int n_ = 0;
@@ -274,6 +303,8 @@ void copy_streaming(void* dst, const void* src, size_t bytes) {
 }
 
 void host_pool_run(int n, const std::function<void(int)>& f) { HostPool::get().run(n, f); }
+void host_pool_start(int n, std::function<void(int)> f) { HostPool::get().start(n, std::move(f)); }
+void host_pool_join() { HostPool::get().join(); }
 int host_pool_size() { return HostPool::get().size(); }
 
 void wire_expand_range(const WireOut& o, const uint16_t* words, int64_t row0, int64_t col0,

@@ -39,6 +39,11 @@ struct WireOut {
 // concurrency capped at 32; the caller is one of them) and returns when all are done.
 void host_pool_run(int n, const std::function<void(int)>& f);
 int host_pool_size();
+// The same batch, started on the workers while the caller keeps going (e.g. enqueueing the
+// device work whose results the tasks wait for); host_pool_join() then takes tasks too and
+// returns when all are done. One batch at a time per process (start blocks until the pool is free).
+void host_pool_start(int n, std::function<void(int)> f);
+void host_pool_join();
 
 // memcpy with 64-byte streaming stores where the CPU has AVX-512 (no read-for-ownership of the
 // destination lines), else memcpy.
