@@ -1136,6 +1136,15 @@ int status_error(int flag) {
   return BITMM_OK;
 }
 
+// A host call's status: copied into the lease's pinned word behind the call's work on s (no
+// pageable 4-byte copy, no synchronous memset), then read.
+int read_status_host(HostCtx& h, cudaStream_t s) {
+  BITMM_CUDA_TRY(cudaMemcpyAsync(h.status_host, h.sctx->status, sizeof(int), cudaMemcpyDeviceToHost, s));
+  BITMM_CUDA_TRY(cudaMemsetAsync(h.sctx->status, 0, sizeof(int), s));
+  BITMM_CUDA_TRY(cudaStreamSynchronize(s));
+  return status_error(*h.status_host);
+}
+
 int read_status(Ctx& st, cudaStream_t s) {
   BITMM_CUDA_TRY(cudaStreamSynchronize(s));
   int flag = 0;
@@ -2375,7 +2384,7 @@ int gemm_1x1_host_impl(const uint64_t* a, int64_t m, const uint64_t* b_packed, i
         hl.host(), s, m, pipe_step(m, c_bytes, 256), in, gemm,
         [&](int64_t r0, int64_t r1) { return OutBlock{r0, r1 - r0, 0, n}; }, wo, dcu,
         cv.take<uint16_t>(w_bytes), static_cast<size_t>(m * n)));
-    return read_status(*st, s);
+    return read_status_host(hl.host(), s);
   }
   if (pipe_step(m, c_bytes, 256) >= m && use_staged(o)) {
     BITMM_TRY(body(0, m));
@@ -2391,7 +2400,7 @@ int gemm_1x1_host_impl(const uint64_t* a, int64_t m, const uint64_t* b_packed, i
         g_d2h_bytes += ((dcu ? 1 : 0) + (dc ? 1 : 0)) * width * (r1 - r0);
         return BITMM_OK;
       }));
-  return read_status(*st, s);
+  return read_status_host(hl.host(), s);
 }
 
 }  // namespace
@@ -2467,7 +2476,7 @@ int gemm_1x2_host_impl(const uint64_t* w, int64_t m, float gamma, const uint64_t
       const int64_t kpad = round_up(k, TC_BK_BYTES);
       BITMM_TRY(ws_reserve(*st, align_up(n * kpad, 1024) + 1024));
       BITMM_TRY(run_unpack_level_i8(dt, dh, dm, n, wpr, k, kpad, static_cast<uint8_t*>(st->ws.ptr), st->status, s));
-      BITMM_TRY(read_status(*st, s));
+      BITMM_TRY(read_status_host(hl.host(), s));
     }
     return fail(rc_dims, dims_msg);
   }
@@ -2507,7 +2516,7 @@ int gemm_1x2_host_impl(const uint64_t* w, int64_t m, float gamma, const uint64_t
         hl.host(), s, n, pipe_step(n, c_bytes, 256), in, gemm,
         [&](int64_t n0, int64_t n1) { return OutBlock{0, m, n0, n1 - n0}; }, wo, dcu,
         cv.take<uint16_t>(wire_bytes), static_cast<size_t>(m * n)));
-    return read_status(*st, s);
+    return read_status_host(hl.host(), s);
   }
   if (pipe_step(n, c_bytes, 256) >= n && use_staged(o)) {
     BITMM_TRY(body(0, n));
@@ -2522,7 +2531,7 @@ int gemm_1x2_host_impl(const uint64_t* w, int64_t m, float gamma, const uint64_t
         g_d2h_bytes += ((dcu ? 1 : 0) + (dc ? 1 : 0)) * width * m;
         return BITMM_OK;
       }));
-  return read_status(*st, s);
+  return read_status_host(hl.host(), s);
 }
 
 }  // namespace
@@ -2608,7 +2617,7 @@ int gemm_2x2_host_impl(const uint64_t* wt, const uint64_t* wh, const uint64_t* w
       BITMM_TRY(ws_reserve(*st, align_up(std::max<int64_t>(m, n) * kpad, 1024) + 1024));
       if (m > 0) BITMM_TRY(run_unpack_level_i8(d[0], d[1], d[2], m, wpr, k, kpad, static_cast<uint8_t*>(st->ws.ptr), st->status, s));
       if (n > 0) BITMM_TRY(run_unpack_level_i8(d[3], d[4], d[5], n, wpr, k, kpad, static_cast<uint8_t*>(st->ws.ptr), st->status, s));
-      BITMM_TRY(read_status(*st, s));
+      BITMM_TRY(read_status_host(hl.host(), s));
     }
     return fail(rc_dims, dims_msg);
   }
@@ -2646,7 +2655,7 @@ int gemm_2x2_host_impl(const uint64_t* wt, const uint64_t* wh, const uint64_t* w
         hl.host(), s, m, pipe_step(m, c_bytes, 256), in, gemm,
         [&](int64_t r0, int64_t r1) { return OutBlock{r0, r1 - r0, 0, n}; }, wo, dcu,
         cv.take<uint16_t>(wire_bytes), static_cast<size_t>(m * n)));
-    return read_status(*st, s);
+    return read_status_host(hl.host(), s);
   }
   if (pipe_step(m, c_bytes, 256) >= m && use_staged(o)) {
     BITMM_TRY(body(0, m));
@@ -2662,7 +2671,7 @@ int gemm_2x2_host_impl(const uint64_t* wt, const uint64_t* wh, const uint64_t* w
         g_d2h_bytes += ((dcu ? 1 : 0) + (dc ? 1 : 0)) * width * (r1 - r0);
         return BITMM_OK;
       }));
-  return read_status(*st, s);
+  return read_status_host(hl.host(), s);
 }
 
 }  // namespace
@@ -2749,7 +2758,7 @@ int bitmm_gemm_1x32_host(const uint64_t* w, int64_t m, int64_t k, int64_t wpr, f
   if (dg) BITMM_CUDA_TRY(cudaMemcpyAsync(dg, row_gamma, m * 4, cudaMemcpyHostToDevice, s));
   BITMM_TRY(apb_dev_impl(*st, dw, m, k, wpr, gamma, dg, db, n, ldb, nullptr, nullptr, nullptr, dc, ldc, s));
   BITMM_CUDA_TRY(cudaMemcpy2DAsync(c, ldc * 4, dc, ldc * 4, n * 4, m, cudaMemcpyDeviceToHost, s));  // columns [n, ldc) are not the output's
-  return read_status(*st, s);
+  return read_status_host(hl.host(), s);
 }
 
 int bitmm_layer_forward_dev(int64_t rows, int64_t cols, float alpha, const float* row_alpha,
@@ -2803,7 +2812,7 @@ int bitmm_layer_forward_host(int64_t rows, int64_t cols, float alpha, const floa
   }
   BITMM_TRY(apb_dev_impl(*st, dw, rows, cols, wpr, alpha, da, db, n, ldb, drp, dci, dv, dc, ldc, s));
   BITMM_CUDA_TRY(cudaMemcpy2DAsync(c, ldc * 4, dc, ldc * 4, n * 4, rows, cudaMemcpyDeviceToHost, s));  // columns [n, ldc) are not the output's
-  return read_status(*st, s);
+  return read_status_host(hl.host(), s);
 }
 
 // ---------------- standalone SpMM ----------------
@@ -2995,7 +3004,7 @@ int bitmm_decompose_thm_host(const uint8_t* levels, int64_t rows, int64_t cols, 
   uint64_t* dm = cv.take<uint64_t>(w_bytes);
   if (l_bytes) BITMM_CUDA_TRY(cudaMemcpyAsync(dl, levels, l_bytes, cudaMemcpyHostToDevice, s));
   BITMM_TRY(bitmm_decompose_thm_dev(dl, rows, cols, dt, dh, dm, wpr, s));
-  BITMM_TRY(read_status(*st, s));
+  BITMM_TRY(read_status_host(hl.host(), s));
   BITMM_CUDA_TRY(cudaMemcpyAsync(t, dt, w_bytes, cudaMemcpyDeviceToHost, s));
   BITMM_CUDA_TRY(cudaMemcpyAsync(h, dh, w_bytes, cudaMemcpyDeviceToHost, s));
   BITMM_CUDA_TRY(cudaMemcpyAsync(m, dm, w_bytes, cudaMemcpyDeviceToHost, s));
@@ -3160,7 +3169,7 @@ int bitmm_layer_forward_2bit_host(int64_t rows, int64_t cols, float alpha, const
   BITMM_TRY(apb2_dev_impl(*st, rows, cols, wpr, alpha, da, dw, drp, dci, dv, dt, dh, dm, tokens,
                           a_scale, has_a_gamma ? a_gamma : 1.0f, dc, ldc, s));
   BITMM_CUDA_TRY(cudaMemcpy2DAsync(c, ldc * 4, dc, ldc * 4, tokens * 4, rows, cudaMemcpyDeviceToHost, s));  // columns [tokens, ldc) are not the output's
-  return read_status(*st, s);
+  return read_status_host(hl.host(), s);
 }
 
 // ---------------- GEMM group ----------------
