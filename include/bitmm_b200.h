@@ -204,6 +204,16 @@ typedef struct bitmm_gemm_item {
 } bitmm_gemm_item;
 int bitmm_gemm_batch_dev(const bitmm_gemm_item* items, int count, void* stream);
 
+/* ---- GEMM group, host flavour ----
+ * The *_host calls of up to 4 items (host pointers in a0..b2, the optional row / column scales,
+ * host outputs c_units / c with leading dimension ldc), with the same results. When every output
+ * crosses PCIe on the 16-bit wire (>= 32 MB and K within the wire's bounds), the items' pipelines
+ * run as one: every item's input copies first, then the slices of all items back to back, so the
+ * device -> host link stays busy across items (one ramp-up and one tail instead of one per call).
+ * Otherwise the items run one after the other. An error stops the batch; outputs of items not
+ * yet completed are then unspecified. BITMM_HOST_BATCH=0 always runs them one after the other. */
+int bitmm_gemm_batch_host(const bitmm_gemm_item* items, int count);
+
 /* ---- Late-output host call: the drop-in's per-call latency (gemm_1x1 / 1x2 / 2x2 returning a
  * fresh DenseMatrix, kernels.cpp:163-275) ----
  * The *_host call of one item (host pointers in a0..b2 and the optional row / column scales;

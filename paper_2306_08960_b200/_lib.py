@@ -123,6 +123,7 @@ SIGNATURES = {
     ),
     "bitmm_gemm_batch_dev": (_i, [_p, _i, _p]),
     "bitmm_gemm_host_late": (_i, [_p, _i, _p, _p]),
+    "bitmm_gemm_batch_host": (_i, [_p, _i]),
     "bitmm_btsr_read_header": (_i, [C.c_char_p, _p]),
     "bitmm_dot_binary_dev": (_i, [_p, _p, _i64, _i64, _i64, _p, _p]),
     "bitmm_mbm_dev": (_i, [_p, _p, _p, _i64, _i64, _p, _p]),

@@ -11,6 +11,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -61,6 +62,7 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 constexpr int kMaxDevices = 16;
+constexpr int kMaxWireSlices = 32;  // input-flag slots of one host pipeline (8 slices x 4 items)
 
 struct Arena {
   void* ptr = nullptr;
@@ -101,13 +103,13 @@ struct HostCtx {
   Ctx* sctx = nullptr;                    // the stream context of `stream`
   cudaStream_t stream = nullptr;          // the call's GEMM stream
   cudaStream_t d2h = nullptr;             // output copies (run_pipelined)
-  cudaStream_t h2d = nullptr;             // input copies (run_pipelined_wire)
+  cudaStream_t h2d = nullptr;             // input copies (run_wire_items)
   Arena io;                               // device staging of inputs / outputs
   cudaEvent_t pipe_ev[8] = {};
-  cudaEvent_t in_ev[9] = {};
+  cudaEvent_t in_ev[kMaxWireSlices + 1] = {};
   uint32_t* in_flags = nullptr;           // per-slice "inputs landed" flags
   uint32_t in_epoch = 0;
-  void* host_stage = nullptr;             // pinned 16-bit output words (run_pipelined_wire)
+  void* host_stage = nullptr;             // pinned 16-bit output words (run_wire_items)
   size_t host_stage_bytes = 0;
   std::vector<cudaEvent_t> wire_ev;       // one per copied part
   std::vector<cudaEvent_t> stage_ev;      // run_staged parts (spin-waited: latency, not CPU)
@@ -212,17 +214,35 @@ int host_ctx_init(HostCtx& h) {
   BITMM_CUDA_TRY(cudaStreamCreateWithFlags(&h.h2d, cudaStreamNonBlocking));
   for (auto& e : h.pipe_ev) BITMM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : h.in_ev) BITMM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  BITMM_CUDA_TRY(cudaMalloc(&h.in_flags, 8 * sizeof(uint32_t)));
-  BITMM_CUDA_TRY(cudaMemset(h.in_flags, 0, 8 * sizeof(uint32_t)));
+  BITMM_CUDA_TRY(cudaMalloc(&h.in_flags, kMaxWireSlices * sizeof(uint32_t)));
+  BITMM_CUDA_TRY(cudaMemset(h.in_flags, 0, kMaxWireSlices * sizeof(uint32_t)));
   BITMM_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&h.status_host), 64, cudaHostAllocDefault));
   return stream_ctx(h.stream, &h.sctx);
 }
 
 // A host call's lease of a HostCtx (and its stream's Ctx). Released with every stream of the
 // context drained, on every exit path.
+struct WireItem;
+// A host batch being assembled (bitmm_gemm_batch_host): the routines' host calls run in two
+// passes on the batch's lease, first adding up the device staging they need, then carving it
+// and handing their wire pipelines over instead of running them.
+struct HostBatch {
+  HostCtx* host = nullptr;
+  bool sizing = true;  // pass 1: only add up the device staging
+  size_t need = 0;     // pass 1: bytes needed; pass 2: the next free byte of the io arena
+  std::vector<WireItem>* items = nullptr;
+};
+thread_local HostBatch* g_batch = nullptr;
+constexpr int kBatchSized = 1000;  // internal return code of a sizing pass
+
 class HostLease {
  public:
   int acquire() {
+    if (g_batch) {  // a batch item runs on the batch's lease
+      h_ = g_batch->host;
+      borrowed_ = true;
+      return BITMM_OK;
+    }
     int dev = 0;
     BITMM_TRY(current_dev(&d_, &dev));
     {
@@ -244,7 +264,7 @@ class HostLease {
     return BITMM_OK;
   }
   ~HostLease() {
-    if (!h_) return;
+    if (!h_ || borrowed_) return;
     cudaStreamSynchronize(h_->h2d);
     cudaStreamSynchronize(h_->stream);
     cudaStreamSynchronize(h_->d2h);
@@ -259,6 +279,7 @@ class HostLease {
  private:
   Dev* d_ = nullptr;
   HostCtx* h_ = nullptr;
+  bool borrowed_ = false;
   std::unique_lock<std::recursive_mutex> lk_;
 };
 
@@ -297,6 +318,22 @@ int arena_reserve(Arena& a, cudaStream_t s, size_t bytes) { return arena_reserve
 int ws_reserve(Ctx& st, size_t bytes) { return arena_reserve(st.ws, bytes, st.stream); }
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// A host call's device staging: the lease's io arena, or its share of a batch's.
+int io_take(HostCtx& h, cudaStream_t s, size_t bytes, void** out) {
+  if (g_batch) {
+    if (g_batch->sizing) {
+      g_batch->need += align_up(bytes, 1024);
+      return kBatchSized;
+    }
+    *out = static_cast<uint8_t*>(h.io.ptr) + g_batch->need;
+    g_batch->need += align_up(bytes, 1024);
+    return BITMM_OK;
+  }
+  BITMM_TRY(arena_reserve(h.io, s, bytes));
+  *out = h.io.ptr;
+  return BITMM_OK;
+}
 int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
 // Sequential 1024-byte aligned sub-buffers of one allocation.
@@ -393,7 +430,7 @@ PFN_waitValue32_t wait_value_fn() {
   return fn;
 }
 
-// How a host call's slice GEMM waits for that slice's input copies (run_pipelined_wire):
+// How a host call's slice GEMM waits for that slice's input copies (run_wire_items):
 //   Value  : cuStreamWaitValue32 on the flag the copy stream writes (default)
 //   Kernel : a one-warp spin kernel on that flag (BITMM_WIRE_WAIT=kernel)
 //   Event  : cudaStreamWaitEvent on the copy stream (BITMM_WIRE_WAIT=event, or no driver
@@ -414,7 +451,7 @@ bool fault_flag_write() {
 }
 
 // Waits in a one-warp kernel until *flag == value: the copy stream writes the flag after a
-// slice's input copies (run_pipelined_wire). A spin on the SMs, not an event wait: the
+// slice's input copies (run_wire_items). A spin on the SMs, not an event wait: the
 // GEMM stream's event waits on the copy stream resolved only once that stream had drained.
 // Gives up after ~2 s and latches ERR_COPY_TIMEOUT (never hangs the device).
 constexpr int ERR_COPY_TIMEOUT = 16;
@@ -1237,15 +1274,32 @@ Wire host_wire(int routine, int64_t k, size_t out_bytes) {
   return wire_for(routine, k);
 }
 
-template <class In, class Gemm, class Block>
-int run_pipelined_wire(HostCtx& st, cudaStream_t s, int64_t total, int64_t step, In&& in,
-                       Gemm&& gemm, Block&& block, const WireOut& wo, const int32_t* dcu,
-                       uint16_t* dwire, size_t wire_words) {
+// One routine's share of a wire pipeline: its slices (the output split along one dimension),
+// their input copies, GEMMs and output blocks, and its buffers.
+struct WireItem {
+  int64_t total, step;
+  std::function<int(int64_t, int64_t, cudaStream_t)> in;  // slice [c0, c1)'s input copies
+  std::function<int(int64_t, int64_t)> gemm;              // its GEMM on the call's stream
+  std::function<OutBlock(int64_t, int64_t)> block;        // the output block it writes
+  WireOut wo;
+  const int32_t* dcu;  // the GEMM's int32 units (leading dimension wo.ldc)
+  uint16_t* dwire;     // device wire words
+  size_t wire_words;
+};
+
+// Runs one or more wire items as one pipeline (a single call is one item; bitmm_gemm_batch_host
+// merges several): every item's input copies go first, the host pool's widening batch covers
+// every part of every item, and the slices of all items are enqueued in order, so the copy
+// link stays busy from the first item's first slice to the last item's last.
+int run_wire_items(HostCtx& st, cudaStream_t s, std::vector<WireItem>& items) {
   // How each slice's GEMM waits for its input copies (see slice_wait_mode); a slice whose
   // flag write fails falls back to an event.
   const SliceWait mode = slice_wait_mode();
   const bool flags = mode != SliceWait::Event;
-  bool slice_flag[kPipeChunks];
+  int nslices = 0;
+  for (const WireItem& w : items) nslices += static_cast<int>((w.total + w.step - 1) / w.step);
+  if (nslices > kMaxWireSlices) return fail(BITMM_ERR_INVALID_ARGUMENT, "too many pipeline slices");
+  bool slice_flag[kMaxWireSlices];
   const uint32_t epoch = ++st.in_epoch == 0 ? ++st.in_epoch : st.in_epoch;
   const auto t_call = std::chrono::steady_clock::now();
   static const bool trace = std::getenv("BITMM_WIRE_TRACE") != nullptr;
@@ -1256,47 +1310,56 @@ int run_pipelined_wire(HostCtx& st, cudaStream_t s, int64_t total, int64_t step,
   if (trace) st.timeline = &tl;
   auto mark = [&](const std::string& what, cudaStream_t on) { trace_mark(st, what, on); };
   mark("start", s);
+  size_t wire_words = 0;
+  std::vector<size_t> hw_off;  // each item's words in the pinned staging
+  for (const WireItem& w : items) {
+    hw_off.push_back(wire_words);
+    wire_words += w.wire_words;
+  }
   BITMM_TRY(host_stage_reserve(st, wire_words * 2));
-  uint16_t* hw = static_cast<uint16_t*>(st.host_stage);
+  uint16_t* const hw_base = static_cast<uint16_t*>(st.host_stage);
   struct Part {
+    int item;
     OutBlock b;
     int64_t r0, r1;
-    size_t off;  // word offset of the block in the staging buffer
+    size_t off;  // word offset of the block in the item's wire buffer
   };
   std::vector<Part> parts;
   // Every slice's input copies go first, on their own stream: queued on s behind the
   // previous slice's GEMM they ran at a third of the link rate while the output copies
   // were in flight (BITMM_WIRE_TRACE device timelines). Issuing them two slices ahead of
   // the GEMMs instead measured slower (e2e 50 vs 56-59 T-upd/s).
-  BITMM_CUDA_TRY(cudaEventRecord(st.in_ev[kPipeChunks], s));  // after the call's setup copies
-  BITMM_CUDA_TRY(cudaStreamWaitEvent(st.h2d, st.in_ev[kPipeChunks], 0));
+  BITMM_CUDA_TRY(cudaEventRecord(st.in_ev[kMaxWireSlices], s));  // after the calls' setup copies
+  BITMM_CUDA_TRY(cudaStreamWaitEvent(st.h2d, st.in_ev[kMaxWireSlices], 0));
   {
     int j = 0;
-    for (int64_t c0 = 0; c0 < total; c0 += step, ++j) {
-      BITMM_TRY(in(c0, std::min(total, c0 + step), st.h2d));
-      slice_flag[j] = flags && !fault_flag_write() && write_value_fn()(reinterpret_cast<CUstream>(st.h2d),
-                                                reinterpret_cast<CUdeviceptr>(st.in_flags + j), epoch,
-                                                0) == CUDA_SUCCESS;
-      if (!slice_flag[j]) {
-        cudaGetLastError();
-        BITMM_CUDA_TRY(cudaEventRecord(st.in_ev[j], st.h2d));
+    for (WireItem& w : items)
+      for (int64_t c0 = 0; c0 < w.total; c0 += w.step, ++j) {
+        BITMM_TRY(w.in(c0, std::min(w.total, c0 + w.step), st.h2d));
+        slice_flag[j] = flags && !fault_flag_write() && write_value_fn()(reinterpret_cast<CUstream>(st.h2d),
+                                                  reinterpret_cast<CUdeviceptr>(st.in_flags + j), epoch,
+                                                  0) == CUDA_SUCCESS;
+        if (!slice_flag[j]) {
+          cudaGetLastError();
+          BITMM_CUDA_TRY(cudaEventRecord(st.in_ev[j], st.h2d));
+        }
+        mark("i" + std::to_string(j), st.h2d);
       }
-      mark("i" + std::to_string(j), st.h2d);
-    }
   }
   // The copied parts of every slice, known before anything is enqueued: ~kWirePartBytes of wire
   // words each, split by output rows.
-  std::vector<int> slice_parts{0};  // slice i owns parts [slice_parts[i], slice_parts[i + 1])
-  {
+  std::vector<int> slice_parts{0};  // global slice j owns parts [slice_parts[j], slice_parts[j + 1])
+  for (int it = 0; it < static_cast<int>(items.size()); ++it) {
+    const WireItem& w = items[it];
     size_t off = 0;
-    for (int64_t c0 = 0; c0 < total; c0 += step) {
-      const OutBlock b = block(c0, std::min(total, c0 + step));
+    for (int64_t c0 = 0; c0 < w.total; c0 += w.step) {
+      const OutBlock b = w.block(c0, std::min(w.total, c0 + w.step));
       const int64_t cells = b.rows * b.cols;
       const int64_t nparts = std::min<int64_t>(
           kWireMaxParts, std::max<int64_t>(1, (cells * 2 + kWirePartBytes / 2) / kWirePartBytes));
       const int64_t per = (b.rows + nparts - 1) / nparts;
       for (int64_t r0 = 0; r0 < b.rows; r0 += per)
-        parts.push_back(Part{b, b.row0 + r0, b.row0 + std::min(b.rows, r0 + per), off});
+        parts.push_back(Part{it, b, b.row0 + r0, b.row0 + std::min(b.rows, r0 + per), off});
       slice_parts.push_back(static_cast<int>(parts.size()));
       off += static_cast<size_t>(cells);
     }
@@ -1360,13 +1423,17 @@ int run_pipelined_wire(HostCtx& st, cudaStream_t s, int64_t total, int64_t step,
     if (trace) wait_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - w0).count();
     const Part& q = parts[t.part];
     if (skip_widen) return;
-    wire_expand_range(wo, hw + q.off, q.b.row0, q.b.col0, q.b.cols, t.r0, t.r1);
+    wire_expand_range(items[q.item].wo, hw_base + hw_off[q.item] + q.off, q.b.row0, q.b.col0, q.b.cols, t.r0, t.r1);
   };
   if (early) host_pool_start(static_cast<int>(tasks.size()), task);
   int rc = BITMM_OK;
-  int i = 0;
-  for (int64_t c0 = 0; c0 < total && rc == BITMM_OK; c0 += step, ++i) {
-    const int64_t c1 = std::min(total, c0 + step);
+  int i = 0;  // global slice
+  for (int it = 0; it < static_cast<int>(items.size()) && rc == BITMM_OK; ++it) {
+  WireItem& w = items[it];
+  const WireOut& wo = w.wo;
+  uint16_t* const hw = hw_base + hw_off[it];
+  for (int64_t c0 = 0; c0 < w.total && rc == BITMM_OK; c0 += w.step, ++i) {
+    const int64_t c1 = std::min(w.total, c0 + w.step);
     if (slice_flag[i] && mode == SliceWait::Kernel) {
       wait_flag_kernel<<<1, 32, 0, s>>>(st.in_flags + i, epoch, st.sctx->status);
       rc = launch_check("wait_flag_kernel");
@@ -1382,7 +1449,7 @@ int run_pipelined_wire(HostCtx& st, cudaStream_t s, int64_t total, int64_t step,
       break;
     }
     mark("h" + std::to_string(i), s);
-    rc = gemm(c0, c1);
+    rc = w.gemm(c0, c1);
     if (rc != BITMM_OK) break;
     const OutBlock b = parts[slice_parts[i]].b;
     const size_t off = parts[slice_parts[i]].off;
@@ -1390,7 +1457,7 @@ int run_pipelined_wire(HostCtx& st, cudaStream_t s, int64_t total, int64_t step,
     // behind the next slice's persistent GEMM
     const int64_t cells = b.rows * b.cols;
     const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((cells / 4 + 255) / 256, int64_t{st.sctx->sms} * 8)));
-    narrow_units_kernel<<<grid, 256, 0, s>>>(dcu + b.row0 * wo.ldc + b.col0, wo.ldc, dwire + off,
+    narrow_units_kernel<<<grid, 256, 0, s>>>(w.dcu + b.row0 * wo.ldc + b.col0, wo.ldc, w.dwire + off,
                                              b.rows, b.cols, static_cast<int>(wo.mode), wo.k);
     rc = launch_check("narrow_units_kernel");
     if (rc != BITMM_OK) break;
@@ -1404,7 +1471,7 @@ int run_pipelined_wire(HostCtx& st, cudaStream_t s, int64_t total, int64_t step,
       const Part& q = parts[p];
       const size_t o = q.off + static_cast<size_t>((q.r0 - b.row0) * b.cols);
       const size_t bytes = static_cast<size_t>((q.r1 - q.r0) * b.cols) * 2;
-      if (cudaMemcpyAsync(hw + o, dwire + o, bytes, cudaMemcpyDeviceToHost, st.d2h) != cudaSuccess) {
+      if (cudaMemcpyAsync(hw + o, w.dwire + o, bytes, cudaMemcpyDeviceToHost, st.d2h) != cudaSuccess) {
         rc = fail(BITMM_ERR_CUDA, std::string("wire copy: ") + cudaGetErrorString(cudaGetLastError()));
         break;
       }
@@ -1414,6 +1481,7 @@ int run_pipelined_wire(HostCtx& st, cudaStream_t s, int64_t total, int64_t step,
     if (rc != BITMM_OK) break;
     if (early) publish(slice_parts[i + 1], false);
     mark("c" + std::to_string(i), st.d2h);
+  }
   }
   if (early) {
     if (rc != BITMM_OK) publish(parts_ready, true);
@@ -1445,6 +1513,19 @@ int run_pipelined_wire(HostCtx& st, cudaStream_t s, int64_t total, int64_t step,
   const cudaError_t e = cudaStreamSynchronize(st.d2h);
   if (rc == BITMM_OK && e != cudaSuccess) rc = fail(BITMM_ERR_CUDA, cudaGetErrorString(e));
   return rc;
+}
+
+// A routine's wire pipeline: run now (one item), or, in a batch's second pass, handed to the
+// batch, which runs every item's pipeline as one.
+int run_or_defer_wire(HostCtx& h, cudaStream_t s, WireItem&& w) {
+  if (g_batch) {
+    g_batch->items->push_back(std::move(w));
+    return BITMM_OK;
+  }
+  std::vector<WireItem> one;
+  one.push_back(std::move(w));
+  BITMM_TRY(run_wire_items(h, s, one));
+  return read_status_host(h, s);
 }
 
 // Where a host GEMM call's output goes: the caller's buffers, given up front (the *_host
@@ -2338,14 +2419,14 @@ int prepare_out(HostOut& o, int routine, int64_t m, int64_t n, int64_t k, int64_
 
 int gemm_1x1_host_impl(const uint64_t* a, int64_t m, const uint64_t* b_packed, int64_t n, int64_t k,
                        int64_t wpr, float gamma_a, float gamma_b, HostOut& o) {
-  g_launches = 0;
+  if (!g_batch) g_launches = 0;
   BITMM_TRY(check_gemm_dims(m, n, k, wpr, o.late() ? n : o.ldc));
   if (!a || !b_packed || (!o.want_units && !o.want_c)) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
   HostLease hl;
   BITMM_TRY(hl.acquire());
   Ctx* st = &hl.ctx();
   cudaStream_t s = hl->stream;
-  g_d2h_bytes = 0;
+  if (!g_batch) g_d2h_bytes = 0;
   int64_t ldc = 0;
   BITMM_TRY(prepare_out(o, 0, m, n, k, &ldc));
   int32_t* c_units = o.c_units;
@@ -2354,9 +2435,10 @@ int gemm_1x1_host_impl(const uint64_t* a, int64_t m, const uint64_t* b_packed, i
   const Wire wire = host_wire(0, k, static_cast<size_t>(m * ldc * 4));
   const size_t a_bytes = m * wpr * 8, b_bytes = n * wpr * 8, c_bytes = m * ldc * 4;
   const size_t w_bytes = wire != Wire::None ? static_cast<size_t>(m * n) * 2 : 0;
-  BITMM_TRY(arena_reserve(hl->io, s, align_up(a_bytes, 1024) + align_up(b_bytes, 1024) +
-                                      2 * align_up(c_bytes, 1024) + align_up(w_bytes, 1024)));
-  Carve cv(hl->io.ptr);
+  void* io = nullptr;
+  BITMM_TRY(io_take(hl.host(), s, align_up(a_bytes, 1024) + align_up(b_bytes, 1024) +
+                                      2 * align_up(c_bytes, 1024) + align_up(w_bytes, 1024), &io));
+  Carve cv(io);
   uint64_t* da = cv.take<uint64_t>(a_bytes);
   uint64_t* db = cv.take<uint64_t>(b_bytes);
   // 16-bit wire: the GEMM writes int32 units only; the host derives both outputs from them
@@ -2364,12 +2446,12 @@ int gemm_1x1_host_impl(const uint64_t* a, int64_t m, const uint64_t* b_packed, i
   float* dc = (want_c && wire == Wire::None) ? cv.take<float>(c_bytes) : nullptr;
   BITMM_CUDA_TRY(cudaMemcpyAsync(db, b_packed, b_bytes, cudaMemcpyHostToDevice, s));
   // slices of output rows (rows of a)
-  auto in = [&](int64_t r0, int64_t r1, cudaStream_t cs) -> int {
+  auto in = [=](int64_t r0, int64_t r1, cudaStream_t cs) -> int {
     BITMM_CUDA_TRY(cudaMemcpyAsync(da + r0 * wpr, a + r0 * wpr, (r1 - r0) * wpr * 8,
                                    cudaMemcpyHostToDevice, cs));
     return BITMM_OK;
   };
-  auto gemm = [&](int64_t r0, int64_t r1) -> int {
+  auto gemm = [=](int64_t r0, int64_t r1) -> int {
     return gemm_1x1_dev_impl(*st, da + r0 * wpr, r1 - r0, db, n, k, wpr, gamma_a, gamma_b,
                              dcu ? dcu + r0 * ldc : nullptr, dc ? dc + r0 * ldc : nullptr, ldc, s);
   };
@@ -2380,11 +2462,10 @@ int gemm_1x1_host_impl(const uint64_t* a, int64_t m, const uint64_t* b_packed, i
   if (wire != Wire::None) {
     const WireOut wo{wire, static_cast<int>(k), gamma_a * gamma_b /* kernels.cpp:170 */, nullptr,
                      nullptr, c_units, c, ldc};
-    BITMM_TRY(run_pipelined_wire(
-        hl.host(), s, m, pipe_step(m, c_bytes, 256), in, gemm,
-        [&](int64_t r0, int64_t r1) { return OutBlock{r0, r1 - r0, 0, n}; }, wo, dcu,
-        cv.take<uint16_t>(w_bytes), static_cast<size_t>(m * n)));
-    return read_status_host(hl.host(), s);
+    return run_or_defer_wire(hl.host(), s,
+                             WireItem{m, pipe_step(m, c_bytes, 256), in, gemm,
+                                      [=](int64_t r0, int64_t r1) { return OutBlock{r0, r1 - r0, 0, n}; },
+                                      wo, dcu, cv.take<uint16_t>(w_bytes), static_cast<size_t>(m * n)});
   }
   if (pipe_step(m, c_bytes, 256) >= m && use_staged(o)) {
     BITMM_TRY(body(0, m));
@@ -2437,7 +2518,7 @@ namespace {
 int gemm_1x2_host_impl(const uint64_t* w, int64_t m, float gamma, const uint64_t* t, const uint64_t* h,
                        const uint64_t* mm, int64_t n, int64_t k, int64_t wpr, float a_scale, int has_a_gamma,
                        float a_gamma, const float* row_scale, const float* col_scale, HostOut& o) {
-  g_launches = 0;
+  if (!g_batch) g_launches = 0;
   // ThmPlanes::validate runs first in the reference (kernels.cpp:186): scale, then legality.
   if (!(a_scale > 0.0f)) return fail(BITMM_ERR_INVALID_ENCODING, "plane scale must be positive");
   if (!t || !h || !mm || !w || (!o.want_units && !o.want_c)) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
@@ -2455,13 +2536,14 @@ int gemm_1x2_host_impl(const uint64_t* w, int64_t m, float gamma, const uint64_t
   const bool planes_ok_shape = n >= 0 && k >= 0 && wpr >= 0 && wpr * 64 >= k;
   const size_t p_bytes = (planes_ok_shape ? n * wpr * 8 : 0), w_bytes = (rc_dims == BITMM_OK ? m * wpr * 8 : 0);
   const size_t c_bytes = (rc_dims == BITMM_OK ? m * ldc * 4 : 0);
-  g_d2h_bytes = 0;
+  if (!g_batch) g_d2h_bytes = 0;
   const Wire wire = host_wire(1, k, c_bytes);
   const size_t wire_bytes = (wire != Wire::None && rc_dims == BITMM_OK) ? static_cast<size_t>(m * n) * 2 : 0;
-  BITMM_TRY(arena_reserve(hl->io, s, 3 * align_up(p_bytes, 1024) + align_up(w_bytes, 1024) +
+  void* io = nullptr;
+  BITMM_TRY(io_take(hl.host(), s, 3 * align_up(p_bytes, 1024) + align_up(w_bytes, 1024) +
                                       2 * align_up(c_bytes, 1024) + align_up(m > 0 ? m * 4 : 0, 1024) +
-                                      align_up(n > 0 ? n * 4 : 0, 1024) + align_up(wire_bytes, 1024) + 4096));
-  Carve cv(hl->io.ptr);
+                                      align_up(n > 0 ? n * 4 : 0, 1024) + align_up(wire_bytes, 1024) + 4096, &io));
+  Carve cv(io);
   uint64_t* dt = cv.take<uint64_t>(p_bytes);
   uint64_t* dh = cv.take<uint64_t>(p_bytes);
   uint64_t* dm = cv.take<uint64_t>(p_bytes);
@@ -2491,14 +2573,14 @@ int gemm_1x2_host_impl(const uint64_t* w, int64_t m, float gamma, const uint64_t
   if (dcs) BITMM_CUDA_TRY(cudaMemcpyAsync(dcs, col_scale, n * 4, cudaMemcpyHostToDevice, s));
   // slices of output columns (rows of the activation planes, the larger operand here);
   // each slice's output block is a strided 2-D copy
-  auto in = [&](int64_t n0, int64_t n1, cudaStream_t cs) -> int {
+  auto in = [=](int64_t n0, int64_t n1, cudaStream_t cs) -> int {
     const size_t off = n0 * wpr, bytes = (n1 - n0) * wpr * 8;
     BITMM_CUDA_TRY(cudaMemcpyAsync(dt + off, t + off, bytes, cudaMemcpyHostToDevice, cs));
     BITMM_CUDA_TRY(cudaMemcpyAsync(dh + off, h + off, bytes, cudaMemcpyHostToDevice, cs));
     BITMM_CUDA_TRY(cudaMemcpyAsync(dm + off, mm + off, bytes, cudaMemcpyHostToDevice, cs));
     return BITMM_OK;
   };
-  auto gemm = [&](int64_t n0, int64_t n1) -> int {
+  auto gemm = [=](int64_t n0, int64_t n1) -> int {
     const size_t off = n0 * wpr;
     return gemm_1x2_dev_impl(*st, dw, m, gamma, dt + off, dh + off, dm + off, n1 - n0, k, wpr,
                              a_scale, has_a_gamma, a_gamma, drs, dcs ? dcs + n0 : nullptr,
@@ -2512,11 +2594,10 @@ int gemm_1x2_host_impl(const uint64_t* w, int64_t m, float gamma, const uint64_t
     // kernels.cpp:193, the same expression gemm_1x2_dev_impl passes to the epilogue
     const float scale = 0.5f * gamma * a_scale * (has_a_gamma ? a_gamma : 1.0f);
     const WireOut wo{wire, static_cast<int>(k), scale, row_scale, col_scale, c_units, c, ldc};
-    BITMM_TRY(run_pipelined_wire(
-        hl.host(), s, n, pipe_step(n, c_bytes, 256), in, gemm,
-        [&](int64_t n0, int64_t n1) { return OutBlock{0, m, n0, n1 - n0}; }, wo, dcu,
-        cv.take<uint16_t>(wire_bytes), static_cast<size_t>(m * n)));
-    return read_status_host(hl.host(), s);
+    return run_or_defer_wire(hl.host(), s,
+                             WireItem{n, pipe_step(n, c_bytes, 256), in, gemm,
+                                      [=](int64_t n0, int64_t n1) { return OutBlock{0, m, n0, n1 - n0}; },
+                                      wo, dcu, cv.take<uint16_t>(wire_bytes), static_cast<size_t>(m * n)});
   }
   if (pipe_step(n, c_bytes, 256) >= n && use_staged(o)) {
     BITMM_TRY(body(0, n));
@@ -2575,7 +2656,7 @@ int gemm_2x2_host_impl(const uint64_t* wt, const uint64_t* wh, const uint64_t* w
                        int has_w_gamma, float w_gamma, const uint64_t* at, const uint64_t* ah,
                        const uint64_t* am, int64_t n, int64_t k, int64_t wpr, float a_scale, int has_a_gamma,
                        float a_gamma, const float* row_scale, const float* col_scale, HostOut& o) {
-  g_launches = 0;
+  if (!g_batch) g_launches = 0;
   // w.validate(); a_packed.validate(); then shapes (kernels.cpp:224-228)
   if (!(w_scale > 0.0f) || !(a_scale > 0.0f))
     return fail(BITMM_ERR_INVALID_ENCODING, "plane scale must be positive");
@@ -2595,13 +2676,14 @@ int gemm_2x2_host_impl(const uint64_t* wt, const uint64_t* wh, const uint64_t* w
   const bool shape_ok = k >= 0 && wpr >= 0 && wpr * 64 >= k;
   const size_t pw = (shape_ok && m > 0 ? m * wpr * 8 : 0), pa = (shape_ok && n > 0 ? n * wpr * 8 : 0);
   const size_t c_bytes = (rc_dims == BITMM_OK ? m * ldc * 4 : 0);
-  g_d2h_bytes = 0;
+  if (!g_batch) g_d2h_bytes = 0;
   const Wire wire = host_wire(2, k, c_bytes);
   const size_t wire_bytes = (wire != Wire::None && rc_dims == BITMM_OK) ? static_cast<size_t>(m * n) * 2 : 0;
-  BITMM_TRY(arena_reserve(hl->io, s, 3 * align_up(pw, 1024) + 3 * align_up(pa, 1024) +
+  void* io = nullptr;
+  BITMM_TRY(io_take(hl.host(), s, 3 * align_up(pw, 1024) + 3 * align_up(pa, 1024) +
                                       2 * align_up(c_bytes, 1024) + align_up(m > 0 ? m * 4 : 0, 1024) +
-                                      align_up(n > 0 ? n * 4 : 0, 1024) + align_up(wire_bytes, 1024) + 4096));
-  Carve cv(hl->io.ptr);
+                                      align_up(n > 0 ? n * 4 : 0, 1024) + align_up(wire_bytes, 1024) + 4096, &io));
+  Carve cv(io);
   uint64_t* d[6];
   const uint64_t* src[6] = {wt, wh, wm, at, ah, am};
   for (int i = 0; i < 6; ++i) {
@@ -2629,13 +2711,13 @@ int gemm_2x2_host_impl(const uint64_t* wt, const uint64_t* wh, const uint64_t* w
   if (drs) BITMM_CUDA_TRY(cudaMemcpyAsync(drs, row_scale, m * 4, cudaMemcpyHostToDevice, s));
   if (dcs) BITMM_CUDA_TRY(cudaMemcpyAsync(dcs, col_scale, n * 4, cudaMemcpyHostToDevice, s));
   // slices of output rows (rows of the weight planes)
-  auto in = [&](int64_t r0, int64_t r1, cudaStream_t cs) -> int {
+  auto in = [=](int64_t r0, int64_t r1, cudaStream_t cs) -> int {
     const size_t off = r0 * wpr, bytes = (r1 - r0) * wpr * 8;
     for (int i = 0; i < 3; ++i)
       BITMM_CUDA_TRY(cudaMemcpyAsync(d[i] + off, src[i] + off, bytes, cudaMemcpyHostToDevice, cs));
     return BITMM_OK;
   };
-  auto gemm = [&](int64_t r0, int64_t r1) -> int {
+  auto gemm = [=](int64_t r0, int64_t r1) -> int {
     const size_t off = r0 * wpr;
     return gemm_2x2_dev_impl(*st, d[0] + off, d[1] + off, d[2] + off, r1 - r0, w_scale,
                              has_w_gamma, w_gamma, d[3], d[4], d[5], n, k, wpr, a_scale,
@@ -2651,11 +2733,10 @@ int gemm_2x2_host_impl(const uint64_t* wt, const uint64_t* wh, const uint64_t* w
     const float scale = 0.25f * w_scale * a_scale * (has_w_gamma ? w_gamma : 1.0f) *
                         (has_a_gamma ? a_gamma : 1.0f);
     const WireOut wo{wire, static_cast<int>(k), scale, row_scale, col_scale, c_units, c, ldc};
-    BITMM_TRY(run_pipelined_wire(
-        hl.host(), s, m, pipe_step(m, c_bytes, 256), in, gemm,
-        [&](int64_t r0, int64_t r1) { return OutBlock{r0, r1 - r0, 0, n}; }, wo, dcu,
-        cv.take<uint16_t>(wire_bytes), static_cast<size_t>(m * n)));
-    return read_status_host(hl.host(), s);
+    return run_or_defer_wire(hl.host(), s,
+                             WireItem{m, pipe_step(m, c_bytes, 256), in, gemm,
+                                      [=](int64_t r0, int64_t r1) { return OutBlock{r0, r1 - r0, 0, n}; },
+                                      wo, dcu, cv.take<uint16_t>(wire_bytes), static_cast<size_t>(m * n)});
   }
   if (pipe_step(m, c_bytes, 256) >= m && use_staged(o)) {
     BITMM_TRY(body(0, m));
@@ -2686,6 +2767,70 @@ int bitmm_gemm_2x2_host(const uint64_t* wt, const uint64_t* wh, const uint64_t* 
   HostOut o = HostOut::given(c_units, c, ldc);
   return gemm_2x2_host_impl(wt, wh, wm, m, w_scale, has_w_gamma, w_gamma, at, ah, am, n, k, wpr, a_scale,
                             has_a_gamma, a_gamma, row_scale, col_scale, o);
+}
+
+// Host batch (include/bitmm_b200.h): when every item's output takes the 16-bit wire, the items'
+// host calls run in two passes on one lease (size the device staging, then carve it and collect
+// the wire pipelines) and their pipelines run as one (run_wire_items); otherwise the items run
+// as their *_host calls, one after the other.
+static int batch_item_call(const bitmm_gemm_item& it) {
+  HostOut o = HostOut::given(it.c_units, it.c, it.ldc);
+  switch (it.routine) {
+    case BITMM_ROUTINE_1X1:
+      return gemm_1x1_host_impl(it.a0, it.m, it.b0, it.n, it.k, it.wpr, it.a_scale, it.b_scale, o);
+    case BITMM_ROUTINE_1X2:
+      return gemm_1x2_host_impl(it.a0, it.m, it.a_scale, it.b0, it.b1, it.b2, it.n, it.k, it.wpr, it.b_scale,
+                                it.has_b_gamma, it.b_gamma, it.row_scale, it.col_scale, o);
+    default:
+      return gemm_2x2_host_impl(it.a0, it.a1, it.a2, it.m, it.a_scale, it.has_a_gamma, it.a_gamma, it.b0, it.b1,
+                                it.b2, it.n, it.k, it.wpr, it.b_scale, it.has_b_gamma, it.b_gamma, it.row_scale,
+                                it.col_scale, o);
+  }
+}
+
+int bitmm_gemm_batch_host(const bitmm_gemm_item* items, int count) {
+  g_launches = 0;
+  g_d2h_bytes = 0;
+  if (count <= 0 || count > TC_GROUP_MAX || items == nullptr)
+    return fail(BITMM_ERR_INVALID_ARGUMENT, "batch must hold 1..4 items");
+  bool merge = std::getenv("BITMM_HOST_BATCH") == nullptr || std::atoi(std::getenv("BITMM_HOST_BATCH")) != 0;
+  for (int i = 0; i < count; ++i) {
+    const bitmm_gemm_item& it = items[i];
+    if (it.routine < BITMM_ROUTINE_1X1 || it.routine > BITMM_ROUTINE_2X2)
+      return fail(BITMM_ERR_INVALID_ARGUMENT, "unknown routine");
+    const bool ok_dims = it.m > 0 && it.n > 0 && it.ldc >= it.n && (it.c_units || it.c);
+    merge = merge && ok_dims && host_wire(it.routine, it.k, static_cast<size_t>(it.m * it.ldc) * 4) != Wire::None;
+  }
+  if (!merge) {
+    for (int i = 0; i < count; ++i) {
+      const uint64_t d2h = g_d2h_bytes;
+      BITMM_TRY(batch_item_call(items[i]));
+      g_d2h_bytes += d2h;
+    }
+    return BITMM_OK;
+  }
+  HostLease hl;
+  BITMM_TRY(hl.acquire());
+  cudaStream_t s = hl->stream;
+  std::vector<WireItem> wire_items;
+  HostBatch hb;
+  hb.host = &hl.host();
+  hb.items = &wire_items;
+  struct Reset {
+    ~Reset() { g_batch = nullptr; }
+  } reset;
+  g_batch = &hb;
+  for (int i = 0; i < count; ++i) {  // pass 1: argument checks, device staging needed
+    const int rc = batch_item_call(items[i]);
+    if (rc != kBatchSized) return rc == BITMM_OK ? fail(BITMM_ERR_CUDA, "batch sizing") : rc;
+  }
+  BITMM_TRY(arena_reserve(hl->io, s, hb.need));
+  hb.sizing = false;
+  hb.need = 0;
+  for (int i = 0; i < count; ++i) BITMM_TRY(batch_item_call(items[i]));  // pass 2: setup copies, pipelines
+  g_batch = nullptr;
+  BITMM_TRY(run_wire_items(hl.host(), s, wire_items));
+  return read_status_host(hl.host(), s);
 }
 
 // Late-output host call (include/bitmm_b200.h): item fields as bitmm_gemm_batch_dev reads them.
