@@ -42,6 +42,7 @@ sys.path.insert(0, REPO)
 METRIC = "binary GEMM Tera-updates/s and % of B200 int-op roofline, 1/1·1/2·2/2"
 UNIT = "T-updates/s"
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+SPACER_CYCLES = 400_000  # ~0.2 ms at ~1.9 GHz (torch.cuda._sleep)
 SEED = 2306_08960
 FP4_DENSE_TFLOPS = 9000.0  # B200_PROFILING.md: fp4 dense 9 PFLOP/s (no fp4 entry in MEASURED_PEAKS.json)
 
@@ -358,7 +359,8 @@ def workload_config(world):
                         f"{world}x wider problem (A replicated), per-rank work fixed; blocks stay "
                         "on their GPU, the NCCL gather to rank 0 is timed separately ('gather')"
                         if world > 1 else "single GPU"),
-        "l2": "flushed between steps (256 MiB read outside the per-step CUDA events)",
+        "l2": "flushed between steps (256 MiB read, then a 0.2 ms device-side sleep so the host's "
+              "launches are queued ahead; both outside the per-step CUDA events)",
         "seed": SEED,
     }
 
@@ -442,6 +444,11 @@ def main():
         # a 256 MiB READ: evicts the previous step's lines (their write-back happens here,
         # outside the timed events) and leaves L2 holding clean data only
         flush.sum()
+        # then ~0.2 ms of device-side sleep, also outside the events: the flush costs the host
+        # ~90 us to launch (torch's reduction) against ~40 us on the GPU, so without slack the
+        # GPU could reach a step's first event before the host had enqueued the step's
+        # launches, and the events would time host launch latency (profiles/dev/host_enqueue.py)
+        torch.cuda._sleep(SPACER_CYCLES)
 
     def run_routine(name, m, n, k):
         x = d[name]
