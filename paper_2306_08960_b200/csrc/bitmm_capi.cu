@@ -617,8 +617,62 @@ UnpackOperand make_unpack_operand(const OperandSrc& src, int64_t wpr, int64_t k,
   return o;
 }
 
+// The flat bulk-copy expansion (unpack.cuh, unpack_flat_kernel; BITMM_UNPACK_FLAT=1) takes a
+// set of e2m1 operands whose rows hold no padding (K = 32 * wpr32 = kpad) and 16-byte aligned
+// planes and outputs. Measured, not the default: bench step expansion 18.5 vs 17.3 us, 1/1
+// 4096^3 per call 34.1 vs 33.5 us (profiles/dev/unpack_flat_ab.sh): with no per-thread global
+// accesses it is no faster, so the per-slice kernel is not paced by its loads' latency or the
+// load/store queue but by the writes of the expanded bytes into an L2 full of the previous
+// GEMM's dirty output.
+bool unpack_flat_ok(const UnpackSet& P) {
+  const char* e = std::getenv("BITMM_UNPACK_FLAT");
+  if (!(e && std::atoi(e) == 1) || !P.fp4 || P.lc.chunks > 0) return false;
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  for (int i = 0; i < P.count; ++i) {
+    const UnpackOperand& o = P.op[i];
+    if (o.K != o.wpr32 * 32 || o.kpad != o.K || !al(o.w0) || !al(o.out) ||
+        (o.levels && (!al(o.w1) || !al(o.w2))))
+      return false;
+  }
+  return true;
+}
+
+int run_unpack_flat(const UnpackSet& P, int sms, cudaStream_t s) {
+  UnpackFlat F{};
+  F.count = P.count;
+  F.err = P.err;
+  long long chunks = 0;
+  for (int i = 0; i < P.count; ++i) {
+    F.op[i] = P.op[i];
+    F.chunk_begin[i] = chunks;
+    chunks += (P.op[i].rows * P.op[i].wpr32 + UF_CHUNK - 1) / UF_CHUNK;
+  }
+  for (int i = P.count; i <= UNPACK_MAX_OPS; ++i) F.chunk_begin[i] = chunks;
+  if (chunks == 0) return BITMM_OK;
+  BITMM_TRY(ensure_max_smem(reinterpret_cast<const void*>(unpack_flat_kernel), UF_SMEM));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(std::min<long long>(chunks, 2ll * sms)));
+  cfg.blockDim = dim3(UF_THREADS);
+  cfg.dynamicSmemBytes = UF_SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ProfScope ps("unpack_operands", s);
+  BITMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, unpack_flat_kernel, F));
+  return launch_check("unpack_flat_kernel");
+}
+
 // Expands every operand of a set (bits or ternary planes) in one launch.
 int run_unpack_set(UnpackSet& P, cudaStream_t s) {
+  if (unpack_flat_ok(P)) {
+    Dev* d = nullptr;
+    int dev = 0;
+    BITMM_TRY(current_dev(&d, &dev));
+    return run_unpack_flat(P, d->sms, s);
+  }
   long long work = 0;  // threads per grid row: a warp per slice, or a thread per level-chunk item
   for (int i = 0; i < P.count; ++i) work = std::max(work, P.op[i].rows * P.op[i].groups_per_row * 32);
   const long long lc_items = P.lc.chunks > 0

@@ -290,6 +290,113 @@ __global__ void __launch_bounds__(256) unpack_operands(const __grid_constant__ U
   if (bad && lane == 0) atomicOr(P.err, bad);
 }
 
+// ---- Flat expansion through the bulk-copy engine (e2m1 operands without padding) ----
+// An operand whose rows hold no padding (K = 32 * wpr32, a multiple of 256, so kpad = K) is a
+// flat array of words whose e2m1 image is position-preserving: word i (row-major) expands to
+// output bytes [16 i, 16 i + 16), nibble order as unpack_slice_fp4_full. A block streams chunks
+// of UF_CHUNK words into shared memory with one bulk copy per plane, expands them with shared
+// loads and stores, and writes the chunk's e2m1 bytes back with one bulk store, double-buffered:
+// no per-thread global loads or stores, so neither the warps' load latency nor the load/store
+// unit's queue (the per-slice kernel above: long-scoreboard and lg_throttle stalls) paces it.
+constexpr int UF_CHUNK = 2048;   // words per chunk
+constexpr int UF_THREADS = 256;
+constexpr int UF_IN = 3 * UF_CHUNK * 4;  // 24 KB: up to three planes
+constexpr int UF_OUT = UF_CHUNK * 16;    // 32 KB of e2m1
+constexpr int UF_SMEM = 2 * (UF_IN + UF_OUT) + 128;
+
+struct UnpackFlat {
+  UnpackOperand op[UNPACK_MAX_OPS];
+  long long chunk_begin[UNPACK_MAX_OPS + 1];  // operand i owns chunks [chunk_begin[i], chunk_begin[i + 1])
+  int count;
+  int* err;
+};
+
+__global__ void __launch_bounds__(UF_THREADS) unpack_flat_kernel(const __grid_constant__ UnpackFlat P) {
+  extern __shared__ __align__(128) uint8_t uf_smem[];
+  uint8_t* in_s = uf_smem;                 // [stage][plane][UF_CHUNK words]
+  uint8_t* out_s = uf_smem + 2 * UF_IN;    // [stage][UF_OUT]
+  uint64_t* full = reinterpret_cast<uint64_t*>(out_s + 2 * UF_OUT);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_wait();  // the previous kernel may still read the workspace we overwrite
+  pdl_launch_dependents();
+  const long long total = P.chunk_begin[P.count];
+  // chunk c -> operand, first word, word count
+  auto locate = [&](long long c, int& oi, long long& w0, int& nw) {
+    oi = 0;
+    for (int i = 1; i < P.count; ++i)
+      if (c >= P.chunk_begin[i]) oi = i;
+    const UnpackOperand& o = P.op[oi];
+    w0 = (c - P.chunk_begin[oi]) * UF_CHUNK;
+    nw = static_cast<int>(min(static_cast<long long>(UF_CHUNK), o.rows * o.wpr32 - w0));
+  };
+  auto issue = [&](long long c, int stage) {  // thread 0: the chunk's planes into `stage`
+    int oi, nw;
+    long long w0;
+    locate(c, oi, w0, nw);
+    const UnpackOperand& o = P.op[oi];
+    const uint32_t bytes = static_cast<uint32_t>(nw) * 4;
+    fence_proxy_async_smem();  // earlier generic reads of the stage before the async writes
+    mbar_arrive_expect_tx(&full[stage], bytes * (o.levels ? 3 : 1));
+    uint8_t* dst = in_s + stage * UF_IN;
+    bulk_load_1d(dst, o.w0 + w0, bytes, &full[stage]);
+    if (o.levels) {
+      bulk_load_1d(dst + UF_CHUNK * 4, o.w1 + w0, bytes, &full[stage]);
+      bulk_load_1d(dst + 2 * UF_CHUNK * 4, o.w2 + w0, bytes, &full[stage]);
+    }
+  };
+  uint32_t illegal = 0;
+  uint32_t phase = 0;  // bit s: parity of stage s
+  if (tid == 0 && static_cast<long long>(blockIdx.x) < total) issue(blockIdx.x, 0);
+  int it = 0;
+  for (long long c = blockIdx.x; c < total; c += gridDim.x, ++it) {
+    const int st = it & 1;
+    // the other stage's input was read by every thread before the last __syncthreads
+    if (tid == 0 && c + gridDim.x < total) issue(c + gridDim.x, st ^ 1);
+    mbar_wait(&full[st], (phase >> st) & 1u);
+    phase ^= 1u << st;
+    if (tid == 0) bulk_wait_group_read<1>();  // out_s[st]'s store (two chunks ago) has read it
+    __syncthreads();
+    int oi, nw;
+    long long w0;
+    locate(c, oi, w0, nw);
+    const UnpackOperand& o = P.op[oi];
+    const uint32_t* pin = reinterpret_cast<const uint32_t*>(in_s + st * UF_IN);
+    uint4* pout = reinterpret_cast<uint4*>(out_s + st * UF_OUT);
+    if (!o.levels) {
+      for (int i = tid; i < nw; i += UF_THREADS) {  // +1 -> 0x2, -1 -> 0xA
+        const uint32_t w = pin[i];
+        pout[i] = make_uint4((~(w << 3) & 0x88888888u) | 0x22222222u, (~(w << 2) & 0x88888888u) | 0x22222222u,
+                             (~(w << 1) & 0x88888888u) | 0x22222222u, (~w & 0x88888888u) | 0x22222222u);
+      }
+    } else {
+      for (int i = tid; i < nw; i += UF_THREADS) {
+        const uint32_t t = pin[i], h = pin[UF_CHUNK + i], m = pin[2 * UF_CHUNK + i];
+        // legal (t,h,m): (0,0,1) (0,0,0) (0,1,0) (1,0,1) (transform.cpp:56-71)
+        illegal |= (t & h) | (t & ~m) | (h & m);
+        const uint32_t hi = t | h, lo = t | ~(h | m);  // p = 2 hi + lo
+        pout[i] = make_uint4(((hi << 1) & 0x22222222u) | (lo & 0x11111111u),
+                             (hi & 0x22222222u) | ((lo >> 1) & 0x11111111u),
+                             ((hi >> 1) & 0x22222222u) | ((lo >> 2) & 0x11111111u),
+                             ((hi >> 2) & 0x22222222u) | ((lo >> 3) & 0x11111111u));
+      }
+    }
+    fence_proxy_async_smem();  // the expanded bytes before the bulk store reads them
+    __syncthreads();
+    if (tid == 0) {
+      bulk_store_1d(o.out + w0 * 16, pout, static_cast<uint32_t>(nw) * 16);
+      bulk_commit_group();
+    }
+  }
+  if (tid == 0) bulk_wait_group_all();
+  if (__syncthreads_or(illegal != 0) && tid == 0) atomicOr(P.err, ERR_ENCODING);
+}
+
 __global__ void unpack_level_i8(const uint32_t* __restrict__ t, const uint32_t* __restrict__ h,
                                 const uint32_t* __restrict__ m, long long rows, int wpr32, int K,
                                 int kpad, uint8_t* __restrict__ out, int* __restrict__ err) {
