@@ -68,6 +68,7 @@ def parse_args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c5-plan", action="store_true", help="skip the single-process multi-GPU plan sweep")
     ap.add_argument("--sequential", action="store_true",
                     help="N=1: time one bitmm_gemm_*_dev call per routine instead of the group")
     return ap.parse_args()
@@ -617,6 +618,17 @@ def main():
     torch.cuda.empty_cache()
     sweep = c5_sweep(GpuC5Backend(torch, dev, lib, comm_dev), dist if world > 1 else None, world, rank,
                      C5, C5, C5)
+    torch.cuda.empty_cache()
+    # the same sweep through the C++ single-process multi-GPU plan: rank 0 drives the job's GPUs
+    # itself (bitmm_shard_plan_*), the other ranks wait
+    if world > 1:
+        dist.barrier()
+    plan = None
+    if rank == 0 and not args.no_c5_plan:
+        ngpu = torch.cuda.device_count()
+        devs = list(range(world)) if ngpu >= world else [0] * world
+        plan = c5_plan_pass(lib, devs, C5, C5, C5)
+        torch.cuda.set_device(dev)
 
     if world > 1:
         dist.barrier()
@@ -697,6 +709,8 @@ def main():
         line["gather"] = gather
     sweep["frac_of_tensor_peak_kernel"] = (2 * C5 ** 3 / (sweep["kernel_ms"] * 1e-3) / 1e12) / peak
     line["c5_sweep"] = sweep
+    if plan is not None:
+        line["c5_plan"] = plan
     if seq_ms is not None:
         line["sequential_calls"] = {"ms_per_step": seq_ms,
                                     "value": upd_per_step / (seq_ms * 1e-3) / 1e12,
@@ -871,6 +885,62 @@ def c5_sweep(backend, dist, world, rank, m, n, k, reps=2, check_rows=4):
         if "nccl_gather_ms" in res:
             res["nccl_root_ingress_GBps"] = res["nccl_bytes_to_root"] / (res["nccl_gather_ms"] * 1e-3) / 1e9
         res["nvlink_GBps_per_direction"] = NVLINK_GBS
+    return res
+
+
+def c5_plan_pass(lib, devs, m, n, k, reps=2, check_rows=4):
+    """Config 5 through bitmm_shard_plan_* (include/bitmm_b200.h): one process, the output
+    columns split over `devs` (devs[0] the root), every time device-timed (max over devices):
+    kernel-only, the gather fused into the GEMM epilogue (peer memory), and the NCCL gather
+    (distinct devices only). Sampled rows of the root's matrix are checked against a host call
+    on those rows of A."""
+    from paper_2306_08960_b200 import data
+    rng = np.random.default_rng(SEED + 5)
+    a, wpr = data.random_words(rng, m, k)
+    b, _ = data.random_words(rng, n, k)
+    P = lambda x: x.ctypes.data_as(C.c_void_p)  # noqa: E731
+    dv = (C.c_int * len(devs))(*devs)
+    plan = C.c_void_p()
+    res = {"workload": f"1/1 {m}x{k}x{n}, N split over devices {devs} of one process (C++ plan)",
+           "devices": devs}
+    if lib.bitmm_shard_plan_create(dv, len(devs), m, n, k, wpr, C.byref(plan)) != 0:
+        res["error"] = lib.bitmm_last_error().decode()
+        return res
+    try:
+        if lib.bitmm_shard_plan_upload(plan, P(a), P(b)) != 0:
+            res["error"] = lib.bitmm_last_error().decode()
+            return res
+        upd = m * n * k
+        sample = np.sort(np.random.default_rng(SEED + 55).choice(m, check_rows, replace=False))
+        want = np.empty((check_rows, n), np.int32)
+        lib.bitmm_gemm_1x1_host(P(np.ascontiguousarray(a[sample])), check_rows, P(b), n, k, wpr, 1.0, 1.0,
+                                P(want), None, n)
+        modes = [("kernel_ms", 0), ("peer_gather_ms", 1)]
+        if len(set(devs)) == len(devs) and len(devs) > 1:
+            modes.append(("nccl_gather_ms", 2))
+        got = np.empty((1, n), np.int32)
+        match = {}
+        for key, mode in modes:
+            ts = []
+            for _ in range(reps + 1):
+                ms = C.c_double(0)
+                if lib.bitmm_shard_run(plan, mode, C.byref(ms)) != 0:
+                    res[key] = None
+                    res[key + "_error"] = lib.bitmm_last_error().decode()
+                    break
+                ts.append(ms.value)
+            else:
+                res[key] = min(ts[1:])
+                res[key.replace("_ms", "_T_updates_per_s")] = upd / (res[key] * 1e-3) / 1e12
+                if mode != 0:
+                    ok = True
+                    for i, r in enumerate(sample):
+                        lib.bitmm_shard_download(plan, int(r), 1, P(got), n)
+                        ok = ok and np.array_equal(got[0], want[i])
+                    match[key.replace("_ms", "")] = bool(ok)
+        res["sampled_rows_match"] = match
+    finally:
+        lib.bitmm_shard_plan_destroy(plan)
     return res
 
 

@@ -99,6 +99,30 @@ int bitmm_ipc_get_handle(const void* dev_ptr, void* handle, uint64_t* offset);
 int bitmm_ipc_open(const void* handle, void** dev_ptr);
 int bitmm_ipc_close(void* dev_ptr);
 
+/* ---- Single-process multi-GPU 1/1 (N sharded over the GPUs) ----
+ * A plan owns, on each of `ndev` devices (devs[0] is the root), the replicated A operand (m x wpr
+ * words), the device's block of b_packed rows (output columns split into ndev blocks of whole
+ * 32-column groups) and its output space, plus the root's m x n int32 matrix. upload copies the
+ * host operands (A to every device, each device its b_packed rows); run computes every block
+ * on its own device and brings it to the root:
+ *   BITMM_GATHER_NONE : blocks stay on their devices (kernel-only timing);
+ *   BITMM_GATHER_PEER : every device's GEMM epilogue stores its block straight into the root's
+ *                       matrix through peer memory (NVLink): the gather is the epilogue;
+ *   BITMM_GATHER_NCCL : blocks computed locally, then NCCL send/recv to the root (one group),
+ *                       which lays them out at their columns (libnccl.so.2 loaded at run time;
+ *                       needs distinct devices).
+ * *ms_out = the device-timed run (max over devices; the root's time includes the gather).
+ * download copies rows [row0, row0 + rows) of the root's matrix (units, K - 2 popcount) to host
+ * memory. A device may be
+ * listed more than once (blocks run one after another on it; no NCCL then). */
+enum { BITMM_GATHER_NONE = 0, BITMM_GATHER_PEER = 1, BITMM_GATHER_NCCL = 2 };
+int bitmm_shard_plan_create(const int* devs, int ndev, int64_t m, int64_t n, int64_t k, int64_t wpr,
+                            void** plan);
+int bitmm_shard_plan_upload(void* plan, const uint64_t* a, const uint64_t* b_packed);
+int bitmm_shard_run(void* plan, int gather, double* ms_out);
+int bitmm_shard_download(void* plan, int64_t row0, int64_t rows, int32_t* c, int64_t ldc);
+int bitmm_shard_plan_destroy(void* plan);
+
 /* ---- 1/1: replaces gemm_1x1 (kernels.hpp:47-48, kernels.cpp:163-183) ----
  * C[r][c] = (gamma_a * gamma_b) * float(K - 2*popcount(a_r xor b_c)).
  * Writes int32 units to c_units and/or scaled floats to c (either may be NULL). */

@@ -124,6 +124,11 @@ SIGNATURES = {
     "bitmm_gemm_batch_dev": (_i, [_p, _i, _p]),
     "bitmm_gemm_host_late": (_i, [_p, _i, _p, _p]),
     "bitmm_gemm_batch_host": (_i, [_p, _i]),
+    "bitmm_shard_plan_create": (_i, [_p, _i, _i64, _i64, _i64, _i64, _p]),
+    "bitmm_shard_plan_upload": (_i, [_p, _p, _p]),
+    "bitmm_shard_run": (_i, [_p, _i, _p]),
+    "bitmm_shard_download": (_i, [_p, _i64, _i64, _p, _i64]),
+    "bitmm_shard_plan_destroy": (_i, [_p]),
     "bitmm_btsr_read_header": (_i, [C.c_char_p, _p]),
     "bitmm_dot_binary_dev": (_i, [_p, _p, _i64, _i64, _i64, _p, _p]),
     "bitmm_mbm_dev": (_i, [_p, _p, _p, _i64, _i64, _p, _p]),

@@ -2,6 +2,8 @@
 // reference's order, workspace management, TMA descriptor encoding and the
 // launch sequence (unpack -> tcgen05 GEMM with fused epilogue) per routine.
 #include <cuda.h>
+#include <dlfcn.h>
+#include <nccl.h>
 #include <cuda_runtime.h>
 #include <cub/cub.cuh>
 
@@ -3695,4 +3697,311 @@ int bitmm_btsr_load_dev(const char* path, int expected_kind, void* payload, uint
   return rc;
 }
 
+// ---------------- single-process multi-GPU 1/1 ----------------
+// C++ orchestration of the N-sharded GEMM for a process that drives several GPUs itself (the
+// reference's callers are C++; shard.py is the one-process-per-GPU form). Output columns (rows
+// of b_packed, kernels.hpp:44-46) are split into ndev blocks of whole 32-column groups; A is
+// replicated. The only cross-device step is bringing the blocks to the root device: either the
+// GEMM epilogue of every device stores its block straight into the root's matrix over peer
+// memory (the gather fused into the GEMM), or NCCL send/recv after the compute (loaded with
+// dlopen: no link-time NCCL dependency).
+
 }  // extern "C"
+
+namespace {
+
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*commInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*errorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.commInitAll = reinterpret_cast<decltype(a.commInitAll)>(dlsym(h, "ncclCommInitAll"));
+    a.commDestroy = reinterpret_cast<decltype(a.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+    a.groupStart = reinterpret_cast<decltype(a.groupStart)>(dlsym(h, "ncclGroupStart"));
+    a.groupEnd = reinterpret_cast<decltype(a.groupEnd)>(dlsym(h, "ncclGroupEnd"));
+    a.send = reinterpret_cast<decltype(a.send)>(dlsym(h, "ncclSend"));
+    a.recv = reinterpret_cast<decltype(a.recv)>(dlsym(h, "ncclRecv"));
+    a.errorString = reinterpret_cast<decltype(a.errorString)>(dlsym(h, "ncclGetErrorString"));
+    a.ok = a.commInitAll && a.commDestroy && a.groupStart && a.groupEnd && a.send && a.recv && a.errorString;
+    return a;
+  }();
+  return api;
+}
+
+struct ShardDev {
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  uint64_t* a = nullptr;   // replicated A, m x wpr
+  uint64_t* b = nullptr;   // this device's b_packed rows, cols x wpr
+  int32_t* out = nullptr;  // this device's block, m x cols (NONE / NCCL)
+  int32_t* recv = nullptr; // root only, per peer: the received block (NCCL)
+  int64_t col0 = 0, cols = 0;
+  bool peer = false;       // can store into the root's memory
+};
+
+struct ShardPlan {
+  int64_t m = 0, n = 0, k = 0, wpr = 0;
+  std::vector<ShardDev> d;
+  int32_t* full = nullptr;  // the root's m x n matrix
+  std::vector<ncclComm_t> comms;
+  bool distinct = true;     // every device index different (NCCL and peer access need it)
+};
+
+int shard_fail_cleanup(ShardPlan* p);
+
+int with_device(int dev) {
+  BITMM_CUDA_TRY(cudaSetDevice(dev));
+  return BITMM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bitmm_shard_plan_create(const int* devs, int ndev, int64_t m, int64_t n, int64_t k, int64_t wpr, void** plan) {
+  if (!devs || ndev < 1 || ndev > kMaxDevices || !plan) return fail(BITMM_ERR_INVALID_ARGUMENT, "bad device list");
+  BITMM_TRY(check_gemm_dims(m, n, k, wpr, n));
+  if (n < 32 * static_cast<int64_t>(ndev)) return fail(BITMM_ERR_INVALID_ARGUMENT, "fewer than 32 columns per device");
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return fail(BITMM_ERR_NO_DEVICE, "no CUDA device available (bitmm_b200 has no CPU fallback)");
+  }
+  int prev = 0;
+  BITMM_CUDA_TRY(cudaGetDevice(&prev));
+  auto p = std::make_unique<ShardPlan>();
+  p->m = m;
+  p->n = n;
+  p->k = k;
+  p->wpr = wpr;
+  p->d.resize(ndev);
+  const int64_t groups = (n + 31) / 32;
+  int rc = BITMM_OK;
+  for (int i = 0; i < ndev && rc == BITMM_OK; ++i) {
+    ShardDev& s = p->d[i];
+    s.dev = devs[i];
+    if (s.dev < 0 || s.dev >= count) {
+      rc = fail(BITMM_ERR_INVALID_ARGUMENT, "device index out of range");
+      break;
+    }
+    for (int j = 0; j < i; ++j)
+      if (devs[j] == s.dev) p->distinct = false;
+    s.col0 = std::min(n, groups * i / ndev * 32);
+    s.cols = std::min(n, groups * (i + 1) / ndev * 32) - s.col0;
+    auto step = [&]() -> int {
+      BITMM_TRY(with_device(s.dev));
+      BITMM_CUDA_TRY(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+      BITMM_CUDA_TRY(cudaEventCreate(&s.e0));
+      BITMM_CUDA_TRY(cudaEventCreate(&s.e1));
+      BITMM_CUDA_TRY(cudaMalloc(&s.a, static_cast<size_t>(m * wpr * 8)));
+      BITMM_CUDA_TRY(cudaMalloc(&s.b, static_cast<size_t>(std::max<int64_t>(1, s.cols) * wpr * 8)));
+      BITMM_CUDA_TRY(cudaMalloc(&s.out, static_cast<size_t>(m * std::max<int64_t>(1, s.cols) * 4)));
+      if (i == 0) BITMM_CUDA_TRY(cudaMalloc(&p->full, static_cast<size_t>(m * n * 4)));
+      return BITMM_OK;
+    };
+    rc = step();
+  }
+  // the root's staging for NCCL receives, and peer access for the fused gather
+  for (int i = 1; i < ndev && rc == BITMM_OK; ++i) {
+    ShardDev& s = p->d[i];
+    auto step = [&]() -> int {
+      BITMM_TRY(with_device(p->d[0].dev));
+      BITMM_CUDA_TRY(cudaMalloc(&s.recv, static_cast<size_t>(m * std::max<int64_t>(1, s.cols) * 4)));
+      if (s.dev == p->d[0].dev) {
+        s.peer = true;  // the same device: the root's matrix is local memory
+        return BITMM_OK;
+      }
+      int can = 0;
+      BITMM_CUDA_TRY(cudaDeviceCanAccessPeer(&can, s.dev, p->d[0].dev));
+      if (can) {
+        BITMM_TRY(with_device(s.dev));
+        const cudaError_t e = cudaDeviceEnablePeerAccess(p->d[0].dev, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return fail(BITMM_ERR_CUDA, cudaGetErrorString(e));
+        cudaGetLastError();
+        s.peer = true;
+      }
+      return BITMM_OK;
+    };
+    rc = step();
+  }
+  p->d[0].peer = true;
+  if (rc == BITMM_OK && ndev > 1 && p->distinct && nccl_api().ok) {
+    p->comms.resize(ndev);
+    std::vector<int> list(devs, devs + ndev);
+    const ncclResult_t r = nccl_api().commInitAll(p->comms.data(), ndev, list.data());
+    if (r != ncclSuccess) p->comms.clear();  // the NCCL gather is then unavailable
+  }
+  cudaSetDevice(prev);
+  if (rc != BITMM_OK) {
+    shard_fail_cleanup(p.release());  // frees the plan
+    return rc;
+  }
+  *plan = p.release();
+  return BITMM_OK;
+}
+
+int bitmm_shard_plan_upload(void* plan, const uint64_t* a, const uint64_t* b_packed) {
+  auto* p = static_cast<ShardPlan*>(plan);
+  if (!p || !a || !b_packed) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
+  int prev = 0;
+  BITMM_CUDA_TRY(cudaGetDevice(&prev));
+  for (ShardDev& s : p->d) {
+    BITMM_TRY(with_device(s.dev));
+    BITMM_CUDA_TRY(cudaMemcpyAsync(s.a, a, static_cast<size_t>(p->m * p->wpr * 8), cudaMemcpyHostToDevice, s.stream));
+    if (s.cols > 0)
+      BITMM_CUDA_TRY(cudaMemcpyAsync(s.b, b_packed + s.col0 * p->wpr, static_cast<size_t>(s.cols * p->wpr * 8),
+                                     cudaMemcpyHostToDevice, s.stream));
+  }
+  for (ShardDev& s : p->d) {
+    BITMM_TRY(with_device(s.dev));
+    BITMM_CUDA_TRY(cudaStreamSynchronize(s.stream));
+  }
+  cudaSetDevice(prev);
+  return BITMM_OK;
+}
+
+int bitmm_shard_run(void* plan, int gather, double* ms_out) {
+  auto* p = static_cast<ShardPlan*>(plan);
+  if (!p || gather < BITMM_GATHER_NONE || gather > BITMM_GATHER_NCCL)
+    return fail(BITMM_ERR_INVALID_ARGUMENT, "bad plan or gather mode");
+  if (gather == BITMM_GATHER_PEER)
+    for (const ShardDev& s : p->d)
+      if (!s.peer) return fail(BITMM_ERR_CUDA, "peer access to the root device is not available");
+  if (gather == BITMM_GATHER_NCCL && p->d.size() > 1 && p->comms.empty())
+    return fail(BITMM_ERR_CUDA, "NCCL gather unavailable (needs distinct devices and libnccl.so.2)");
+  g_launches = 0;
+  int prev = 0;
+  BITMM_CUDA_TRY(cudaGetDevice(&prev));
+  const int ndev = static_cast<int>(p->d.size());
+  int rc = BITMM_OK;
+  // every device's GEMM: its block into its own memory, or (PEER, and always for the root)
+  // straight into the root's matrix at its column offset
+  for (int i = 0; i < ndev && rc == BITMM_OK; ++i) {
+    ShardDev& s = p->d[i];
+    auto step = [&]() -> int {
+      BITMM_TRY(with_device(s.dev));
+      BITMM_CUDA_TRY(cudaEventRecord(s.e0, s.stream));
+      if (s.cols > 0) {
+        CallCtx st;
+        BITMM_TRY(st.acquire(s.stream));
+        const bool into_root = gather == BITMM_GATHER_PEER || (i == 0 && gather != BITMM_GATHER_NONE);
+        int32_t* out = into_root ? p->full + s.col0 : s.out;
+        BITMM_TRY(gemm_1x1_dev_impl(*st, s.a, p->m, s.b, s.cols, p->k, p->wpr, 1.0f, 1.0f, out, nullptr,
+                                    into_root ? p->n : s.cols, s.stream));
+      }
+      return BITMM_OK;
+    };
+    rc = step();
+  }
+  if (rc == BITMM_OK && gather == BITMM_GATHER_NCCL && ndev > 1) {
+    const NcclApi& nc = nccl_api();
+    nc.groupStart();
+    for (int i = 1; i < ndev; ++i) {
+      ShardDev& s = p->d[i];
+      if (s.cols == 0) continue;
+      const size_t cnt = static_cast<size_t>(p->m * s.cols);
+      nc.send(s.out, cnt, ncclInt32, 0, p->comms[i], s.stream);
+      nc.recv(s.recv, cnt, ncclInt32, i, p->comms[0], p->d[0].stream);
+    }
+    const ncclResult_t r = nc.groupEnd();
+    if (r != ncclSuccess) rc = fail(BITMM_ERR_CUDA, std::string("NCCL gather: ") + nc.errorString(r));
+    // the root lays every received block out at its columns
+    if (rc == BITMM_OK) rc = with_device(p->d[0].dev);
+    for (int i = 1; i < ndev && rc == BITMM_OK; ++i) {
+      ShardDev& s = p->d[i];
+      if (s.cols == 0) continue;
+      if (cudaMemcpy2DAsync(p->full + s.col0, p->n * 4, s.recv, s.cols * 4, s.cols * 4, p->m,
+                            cudaMemcpyDeviceToDevice, p->d[0].stream) != cudaSuccess)
+        rc = fail(BITMM_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+  // the root's end waits for every device (the gathered matrix is complete at e1 of the root)
+  for (int i = 0; i < ndev && rc == BITMM_OK; ++i) {
+    rc = with_device(p->d[i].dev);
+    if (rc == BITMM_OK && cudaEventRecord(p->d[i].e1, p->d[i].stream) != cudaSuccess)
+      rc = fail(BITMM_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
+  }
+  double ms = 0.0;
+  int status = BITMM_OK;
+  for (int i = 0; i < ndev; ++i) {
+    ShardDev& s = p->d[i];
+    if (with_device(s.dev) != BITMM_OK) continue;
+    const cudaError_t e = cudaEventSynchronize(s.e1);
+    if (e != cudaSuccess && rc == BITMM_OK) rc = fail(BITMM_ERR_CUDA, cudaGetErrorString(e));
+    float t = 0.0f;
+    if (rc == BITMM_OK && cudaEventElapsedTime(&t, s.e0, s.e1) == cudaSuccess) ms = std::max(ms, static_cast<double>(t));
+    if (rc == BITMM_OK && status == BITMM_OK) {
+      Ctx* st = nullptr;
+      if (stream_ctx(s.stream, &st) == BITMM_OK) status = read_status(*st, s.stream);
+    }
+  }
+  cudaSetDevice(prev);
+  if (rc != BITMM_OK) return rc;
+  if (ms_out) *ms_out = ms;
+  return status;
+}
+
+int bitmm_shard_download(void* plan, int64_t row0, int64_t rows, int32_t* c, int64_t ldc) {
+  auto* p = static_cast<ShardPlan*>(plan);
+  if (!p || !c || ldc < p->n || row0 < 0 || rows < 0 || row0 + rows > p->m)
+    return fail(BITMM_ERR_INVALID_ARGUMENT, "bad plan, rows or output");
+  if (rows == 0) return BITMM_OK;
+  int prev = 0;
+  BITMM_CUDA_TRY(cudaGetDevice(&prev));
+  BITMM_TRY(with_device(p->d[0].dev));
+  BITMM_CUDA_TRY(cudaMemcpy2D(c, ldc * 4, p->full + row0 * p->n, p->n * 4, p->n * 4, rows, cudaMemcpyDeviceToHost));
+  cudaSetDevice(prev);
+  return BITMM_OK;
+}
+
+int bitmm_shard_plan_destroy(void* plan) {
+  auto* p = static_cast<ShardPlan*>(plan);
+  if (!p) return BITMM_OK;
+  shard_fail_cleanup(p);
+  return BITMM_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+int shard_fail_cleanup(ShardPlan* p) {
+  int prev = 0;
+  cudaGetDevice(&prev);
+  for (ncclComm_t c : p->comms)
+    if (c) nccl_api().commDestroy(c);
+  for (ShardDev& s : p->d) {
+    if (cudaSetDevice(s.dev) != cudaSuccess) continue;
+    if (s.stream) cudaStreamSynchronize(s.stream);
+    cudaFree(s.a);
+    cudaFree(s.b);
+    cudaFree(s.out);
+    if (s.recv) {
+      cudaSetDevice(p->d[0].dev);
+      cudaFree(s.recv);
+      cudaSetDevice(s.dev);
+    }
+    if (s.e0) cudaEventDestroy(s.e0);
+    if (s.e1) cudaEventDestroy(s.e1);
+    if (s.stream) cudaStreamDestroy(s.stream);
+  }
+  if (!p->d.empty() && cudaSetDevice(p->d[0].dev) == cudaSuccess) cudaFree(p->full);
+  cudaGetLastError();
+  cudaSetDevice(prev);
+  delete p;
+  return BITMM_OK;
+}
+
+}  // namespace

@@ -72,6 +72,12 @@ def test_no_device_means_error_not_fallback():
     rc = lib.bitmm_gemm_1x1_host(_p(a), 1, _p(a), 1, 3, 8, 1.0, 1.0, None, _p(out), 1)
     assert rc == _lib.ERR_NO_DEVICE
     assert lib.bitmm_device_sm_count() == 0
+    # the multi-GPU plan too (no plan is created)
+    import ctypes as C
+    plan = C.c_void_p()
+    dv = (C.c_int * 1)(0)
+    assert lib.bitmm_shard_plan_create(dv, 1, 64, 256, 512, 8, C.byref(plan)) == _lib.ERR_NO_DEVICE
+    assert not plan.value
     with pytest.raises(_lib.BitmmError):
         api.gemm_1x1(api.BitMatrix(1, 3), api.BitMatrix(1, 3))
 
