@@ -69,6 +69,7 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-c5-plan", action="store_true", help="skip the single-process multi-GPU plan sweep")
+    ap.add_argument("--c5-plan-devs", default="", help=argparse.SUPPRESS)  # internal: the plan child
     ap.add_argument("--sequential", action="store_true",
                     help="N=1: time one bitmm_gemm_*_dev call per routine instead of the group")
     return ap.parse_args()
@@ -391,6 +392,12 @@ def main():
     args = parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.c5_plan_devs:
+        # child of c5_plan_child(): the plan sweep alone, one JSON line
+        from paper_2306_08960_b200 import _lib
+        devs = [int(v) for v in args.c5_plan_devs.split(",")]
+        print(json.dumps(c5_plan_pass(_lib.load(), devs, C5, C5, C5)), flush=True)
+        return 0
 
     import torch
     import torch.distributed as dist
@@ -627,8 +634,7 @@ def main():
     if rank == 0 and not args.no_c5_plan:
         ngpu = torch.cuda.device_count()
         devs = list(range(world)) if ngpu >= world else [0] * world
-        plan = c5_plan_pass(lib, devs, C5, C5, C5)
-        torch.cuda.set_device(dev)
+        plan = c5_plan_child(devs)
 
     if world > 1:
         dist.barrier()
@@ -886,6 +892,22 @@ def c5_sweep(backend, dist, world, rank, m, n, k, reps=2, check_rows=4):
             res["nccl_root_ingress_GBps"] = res["nccl_bytes_to_root"] / (res["nccl_gather_ms"] * 1e-3) / 1e9
         res["nvlink_GBps_per_direction"] = NVLINK_GBS
     return res
+
+
+def c5_plan_child(devs, timeout=300):
+    """c5_plan_pass in a child process (it opens every device of the job and an NCCL
+    communicator of its own): a failure or a hang there is reported in the line instead of
+    taking the bench down."""
+    env = {kk: v for kk, v in os.environ.items() if kk not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    cmd = [sys.executable, os.path.abspath(__file__), "--c5-plan-devs", ",".join(str(d) for d in devs)]
+    try:
+        r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout)
+    except subprocess.TimeoutExpired:
+        return {"devices": devs, "error": f"plan sweep timed out after {timeout} s"}
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    if r.returncode != 0 or not lines:
+        return {"devices": devs, "error": f"plan sweep exited {r.returncode}: {r.stderr.strip()[-300:]}"}
+    return json.loads(lines[-1])
 
 
 def c5_plan_pass(lib, devs, m, n, k, reps=2, check_rows=4):
