@@ -107,6 +107,7 @@ struct HostCtx {
   cudaStream_t d2h = nullptr;             // output copies (run_pipelined)
   cudaStream_t h2d = nullptr;             // input copies (run_wire_items)
   Arena io;                               // device staging of inputs / outputs
+  Arena w12;                              // 12-bit packed wire parts (wire.cuh)
   cudaEvent_t pipe_ev[8] = {};
   cudaEvent_t in_ev[kMaxWireSlices + 1] = {};
   uint32_t* in_flags = nullptr;           // per-slice "inputs landed" flags
@@ -1372,13 +1373,26 @@ int run_wire_items(HostCtx& st, cudaStream_t s, std::vector<WireItem>& items) {
     hw_off.push_back(wire_words);
     wire_words += w.wire_words;
   }
-  BITMM_TRY(host_stage_reserve(st, wire_words * 2));
-  uint16_t* const hw_base = static_cast<uint16_t*>(st.host_stage);
+  // 12-bit packing (wire.cuh; BITMM_WIRE_BITS=12) for items whose output blocks all have a
+  // multiple of 16 columns. Measured, not the default: the last copy of the bench step lands
+  // ~0.4 ms earlier (3.2 vs 3.6 ms), but the host's widening, bound by host memory traffic
+  // (DMA writes + 256 MB of output stores), ends at the same time (e2e 64.8 vs 66.2 T-upd/s
+  // batched, 58.5 vs 57.1 per call; profiles/dev/e2e_ab.py, BITMM_WIRE_TRACE).
+  const bool w12_env = std::getenv("BITMM_WIRE_BITS") && std::atoi(std::getenv("BITMM_WIRE_BITS")) == 12;
+  std::vector<char> item12;
+  for (const WireItem& w : items) {
+    bool ok = w12_env;
+    for (int64_t c0 = 0; c0 < w.total && ok; c0 += w.step) ok = w.block(c0, std::min(w.total, c0 + w.step)).cols % 16 == 0;
+    item12.push_back(ok ? 1 : 0);
+  }
   struct Part {
     int item;
     OutBlock b;
     int64_t r0, r1;
-    size_t off;  // word offset of the block in the item's wire buffer
+    size_t off;      // word offset of the block in the item's wire buffer
+    bool p12;        // crosses PCIe packed in 12 bits (wire.cuh)
+    size_t off12;    // its bytes in the 12-bit buffers (device and pinned)
+    size_t bytes12;  // header + payload
   };
   std::vector<Part> parts;
   // Every slice's input copies go first, on their own stream: queued on s behind the
@@ -1415,10 +1429,27 @@ int run_wire_items(HostCtx& st, cudaStream_t s, std::vector<WireItem>& items) {
           kWireMaxParts, std::max<int64_t>(1, (cells * 2 + kWirePartBytes / 2) / kWirePartBytes));
       const int64_t per = (b.rows + nparts - 1) / nparts;
       for (int64_t r0 = 0; r0 < b.rows; r0 += per)
-        parts.push_back(Part{it, b, b.row0 + r0, b.row0 + std::min(b.rows, r0 + per), off});
+        parts.push_back(Part{it, b, b.row0 + r0, b.row0 + std::min(b.rows, r0 + per), off, item12[it] != 0, 0, 0});
       slice_parts.push_back(static_cast<int>(parts.size()));
       off += static_cast<size_t>(cells);
     }
+  }
+  // the 12-bit parts: 16-byte header {min, max}, payload of 1.5 bytes per cell; the pinned copy
+  // of each is padded by 16 bytes (the host's 16-byte loads read 4 bytes past a row's last group)
+  size_t bytes12 = 0;
+  for (Part& q : parts) {
+    if (!q.p12) continue;
+    q.off12 = bytes12;
+    q.bytes12 = 16 + align_up(static_cast<size_t>((q.r1 - q.r0) * q.b.cols) * 3 / 2, 16);
+    bytes12 += q.bytes12 + 16;
+  }
+  BITMM_TRY(host_stage_reserve(st, wire_words * 2 + bytes12));
+  uint16_t* const hw_base = static_cast<uint16_t*>(st.host_stage);
+  uint8_t* const h12 = static_cast<uint8_t*>(st.host_stage) + wire_words * 2;
+  uint8_t* d12 = nullptr;
+  if (bytes12 > 0) {
+    BITMM_TRY(arena_reserve(st.w12, bytes12, s));
+    d12 = static_cast<uint8_t*>(st.w12.ptr);
   }
   while (st.wire_ev.size() < parts.size()) {
     cudaEvent_t e = nullptr;
@@ -1455,6 +1486,8 @@ int run_wire_items(HostCtx& st, cudaStream_t s, std::vector<WireItem>& items) {
   const auto t0 = std::chrono::steady_clock::now();
   std::atomic<int> copy_err{0};
   std::atomic<int64_t> wait_ns{0};
+  std::atomic<uint64_t> refetch_bytes{0};  // 12-bit parts fetched again as 16-bit words
+  std::unique_ptr<std::once_flag[]> refetch(new std::once_flag[std::max<size_t>(1, parts.size())]);
   // BITMM_WIRE_EARLY=0: the batch starts after the whole enqueue (round-1 order, A/B)
   const bool early = !(std::getenv("BITMM_WIRE_EARLY") && std::atoi(std::getenv("BITMM_WIRE_EARLY")) == 0);
   auto task = [&](int i) {
@@ -1479,7 +1512,25 @@ int run_wire_items(HostCtx& st, cudaStream_t s, std::vector<WireItem>& items) {
     if (trace) wait_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - w0).count();
     const Part& q = parts[t.part];
     if (skip_widen) return;
-    wire_expand_range(items[q.item].wo, hw_base + hw_off[q.item] + q.off, q.b.row0, q.b.col0, q.b.cols, t.r0, t.r1);
+    uint16_t* const hw = hw_base + hw_off[q.item];
+    if (q.p12) {
+      const int* hdr = reinterpret_cast<const int*>(h12 + q.off12);
+      if (hdr[1] - hdr[0] <= 4095) {
+        wire_expand_range12(items[q.item].wo, h12 + q.off12 + 16, static_cast<uint16_t>(hdr[0]), q.r0, q.b.col0,
+                            q.b.cols, t.r0, t.r1);
+        return;
+      }
+      // the part's words span more than 12 bits: fetch them as 16-bit words (still on the device)
+      std::call_once(refetch[t.part], [&] {
+        const size_t o = q.off + static_cast<size_t>((q.r0 - q.b.row0) * q.b.cols);
+        const size_t bytes = static_cast<size_t>((q.r1 - q.r0) * q.b.cols) * 2;
+        if (cudaMemcpy(hw + o, items[q.item].dwire + o, bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+          copy_err.store(1);
+        refetch_bytes += bytes;
+      });
+      if (copy_err.load()) return;
+    }
+    wire_expand_range(items[q.item].wo, hw + q.off, q.b.row0, q.b.col0, q.b.cols, t.r0, t.r1);
   };
   if (early) host_pool_start(static_cast<int>(tasks.size()), task);
   int rc = BITMM_OK;
@@ -1517,6 +1568,27 @@ int run_wire_items(HostCtx& st, cudaStream_t s, std::vector<WireItem>& items) {
                                              b.rows, b.cols, static_cast<int>(wo.mode), wo.k);
     rc = launch_check("narrow_units_kernel");
     if (rc != BITMM_OK) break;
+    if (parts[slice_parts[i]].p12) {  // the slice's parts in 12 bits: headers, min/max, pack
+      Wire12Set S{};
+      int64_t most = 0;
+      for (int p = slice_parts[i]; p < slice_parts[i + 1]; ++p) {
+        const Part& q = parts[p];
+        const size_t o = q.off + static_cast<size_t>((q.r0 - b.row0) * b.cols);
+        S.p[S.count++] = Wire12Part{w.dwire + o, d12 + q.off12, (q.r1 - q.r0) * b.cols};
+        most = std::max(most, (q.r1 - q.r0) * b.cols);
+      }
+      const dim3 grid(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((most / 8 + 255) / 256, 64))),
+                      static_cast<unsigned>(S.count));
+      wire12_init_kernel<<<1, 32, 0, s>>>(S);
+      rc = launch_check("wire12_init_kernel");
+      if (rc != BITMM_OK) break;
+      wire12_minmax_kernel<<<grid, 256, 0, s>>>(S, static_cast<int>(wo.mode));
+      rc = launch_check("wire12_minmax_kernel");
+      if (rc != BITMM_OK) break;
+      wire12_pack_kernel<<<grid, 256, 0, s>>>(S, static_cast<int>(wo.mode));
+      rc = launch_check("wire12_pack_kernel");
+      if (rc != BITMM_OK) break;
+    }
     mark("g" + std::to_string(i), s);
     cudaEvent_t ev = st.pipe_ev[i % kPipeChunks];
     if (cudaEventRecord(ev, s) != cudaSuccess || cudaStreamWaitEvent(st.d2h, ev, 0) != cudaSuccess) {
@@ -1526,8 +1598,10 @@ int run_wire_items(HostCtx& st, cudaStream_t s, std::vector<WireItem>& items) {
     for (int p = slice_parts[i]; p < slice_parts[i + 1] && rc == BITMM_OK; ++p) {
       const Part& q = parts[p];
       const size_t o = q.off + static_cast<size_t>((q.r0 - b.row0) * b.cols);
-      const size_t bytes = static_cast<size_t>((q.r1 - q.r0) * b.cols) * 2;
-      if (cudaMemcpyAsync(hw + o, w.dwire + o, bytes, cudaMemcpyDeviceToHost, st.d2h) != cudaSuccess) {
+      const size_t bytes = q.p12 ? q.bytes12 : static_cast<size_t>((q.r1 - q.r0) * b.cols) * 2;
+      void* dst = q.p12 ? static_cast<void*>(h12 + q.off12) : static_cast<void*>(hw + o);
+      const void* src = q.p12 ? static_cast<const void*>(d12 + q.off12) : static_cast<const void*>(w.dwire + o);
+      if (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st.d2h) != cudaSuccess) {
         rc = fail(BITMM_ERR_CUDA, std::string("wire copy: ") + cudaGetErrorString(cudaGetLastError()));
         break;
       }
@@ -1565,6 +1639,7 @@ int run_wire_items(HostCtx& st, cudaStream_t s, std::vector<WireItem>& items) {
     for (auto& [what, e] : tl) cudaEventDestroy(e);
     st.timeline = nullptr;
   }
+  g_d2h_bytes += refetch_bytes.load();
   if (rc == BITMM_OK && copy_err.load()) rc = fail(BITMM_ERR_CUDA, std::string("wire copy: ") + cudaGetErrorString(cudaGetLastError()));
   const cudaError_t e = cudaStreamSynchronize(st.d2h);
   if (rc == BITMM_OK && e != cudaSuccess) rc = fail(BITMM_ERR_CUDA, cudaGetErrorString(e));

@@ -227,15 +227,15 @@ bool has_avx512() {
 }
 #endif
 
+// One output row r from its 16-bit words (cols of them, the block's columns from col0 on).
 template <Wire MODE>
-void expand_rows(const WireOut& o, const uint16_t* words, int64_t row0, int64_t col0, int64_t cols,
-                 int64_t r0, int64_t r1) {
+void widen_row(const WireOut& o, const uint16_t* src, int64_t r, int64_t col0, int64_t cols) {
 #if defined(__x86_64__)
   const bool wide = has_avx512();
 #endif
-  for (int64_t r = r0; r < r1; ++r) {
+  {
     Row w;
-    w.src = words + (r - row0) * cols;
+    w.src = src;
     w.du = o.c_units ? o.c_units + r * o.ldc + col0 : nullptr;
     w.dc = o.c ? o.c + r * o.ldc + col0 : nullptr;
     w.cs = o.col_scale ? o.col_scale + col0 : nullptr;
@@ -263,8 +263,77 @@ void expand_rows(const WireOut& o, const uint16_t* words, int64_t row0, int64_t 
 #endif
     for (; j < cols; ++j) cell<MODE>(w, j);
   }
+}
+
+template <Wire MODE>
+void expand_rows(const WireOut& o, const uint16_t* words, int64_t row0, int64_t col0, int64_t cols,
+                 int64_t r0, int64_t r1) {
+  for (int64_t r = r0; r < r1; ++r) widen_row<MODE>(o, words + (r - row0) * cols, r, col0, cols);
 #if defined(__x86_64__)
   _mm_sfence();  // streaming stores ordered before the pool reports the task done
+#endif
+}
+
+// 12-bit fields (two cells per 3 bytes, wire.cuh) + base, modulo 2^16 -> the 16-bit words.
+void unpack12_scalar(const uint8_t* p, uint16_t base, uint16_t* out, int64_t j, int64_t n) {
+  for (; j < n; ++j) {
+    const uint8_t* b = p + 3 * (j >> 1);
+    const uint32_t v = (j & 1) ? ((b[1] >> 4) | (static_cast<uint32_t>(b[2]) << 4))
+                               : (b[0] | ((static_cast<uint32_t>(b[1]) & 0xFu) << 8));
+    out[j] = static_cast<uint16_t>(v + base);
+  }
+}
+
+#if defined(__x86_64__)
+// Sixteen cells (24 bytes) per step: each 128-bit half takes 12 bytes, a byte shuffle puts the
+// two bytes of every cell in its 16-bit lane, even lanes keep their low 12 bits, odd lanes
+// shift right by 4. Reads 4 bytes past the last group (the staging parts are padded).
+__attribute__((target("avx2"))) void unpack12_avx2(const uint8_t* p, uint16_t base, uint16_t* out, int64_t n) {
+  const __m256i shuf = _mm256_setr_epi8(0, 1, 1, 2, 3, 4, 4, 5, 6, 7, 7, 8, 9, 10, 10, 11,
+                                        0, 1, 1, 2, 3, 4, 4, 5, 6, 7, 7, 8, 9, 10, 10, 11);
+  const __m256i mask = _mm256_set1_epi16(0x0FFF);
+  const __m256i b = _mm256_set1_epi16(static_cast<short>(base));
+  int64_t j = 0;
+  for (; j + 16 <= n; j += 16) {
+    const uint8_t* q = p + 3 * (j >> 1);
+    const __m128i lo = _mm_loadu_si128(reinterpret_cast<const __m128i*>(q));
+    const __m128i hi = _mm_loadu_si128(reinterpret_cast<const __m128i*>(q + 12));
+    __m256i v = _mm256_shuffle_epi8(_mm256_set_m128i(hi, lo), shuf);
+    v = _mm256_blend_epi16(_mm256_and_si256(v, mask), _mm256_srli_epi16(v, 4), 0xAA);
+    _mm256_storeu_si256(reinterpret_cast<__m256i*>(out + j), _mm256_add_epi16(v, b));
+  }
+  unpack12_scalar(p, base, out, j, n);
+}
+
+bool has_avx2() {
+  static const bool cpu = [] {
+    __builtin_cpu_init();
+    return __builtin_cpu_supports("avx2") != 0;
+  }();
+  const char* e = std::getenv("BITMM_HOST_SIMD");
+  return cpu && !(e && std::string(e) == "sse2");
+}
+#endif
+
+template <Wire MODE>
+void expand_rows12(const WireOut& o, const uint8_t* payload, uint16_t base, int64_t prow0, int64_t col0,
+                   int64_t cols, int64_t r0, int64_t r1) {
+  // each row's 12-bit fields go through a small per-thread buffer of 16-bit words (L1/L2
+  // resident), then the 16-bit widening: the output stores are what costs
+  thread_local std::vector<uint16_t> tmp;
+  if (static_cast<int64_t>(tmp.size()) < cols) tmp.resize(cols);
+  for (int64_t r = r0; r < r1; ++r) {
+    const uint8_t* p = payload + (r - prow0) * cols / 2 * 3;
+#if defined(__x86_64__)
+    if (has_avx2())
+      unpack12_avx2(p, base, tmp.data(), cols);
+    else
+#endif
+      unpack12_scalar(p, base, tmp.data(), 0, cols);
+    widen_row<MODE>(o, tmp.data(), r, col0, cols);
+  }
+#if defined(__x86_64__)
+  _mm_sfence();
 #endif
 }
 
@@ -313,6 +382,15 @@ void wire_expand_range(const WireOut& o, const uint16_t* words, int64_t row0, in
     case Wire::Popc: expand_rows<Wire::Popc>(o, words, row0, col0, cols, r0, r1); break;
     case Wire::Half: expand_rows<Wire::Half>(o, words, row0, col0, cols, r0, r1); break;
     default: expand_rows<Wire::Quarter>(o, words, row0, col0, cols, r0, r1); break;
+  }
+}
+
+void wire_expand_range12(const WireOut& o, const uint8_t* payload, uint16_t base, int64_t prow0, int64_t col0,
+                         int64_t cols, int64_t r0, int64_t r1) {
+  switch (o.mode) {
+    case Wire::Popc: expand_rows12<Wire::Popc>(o, payload, base, prow0, col0, cols, r0, r1); break;
+    case Wire::Half: expand_rows12<Wire::Half>(o, payload, base, prow0, col0, cols, r0, r1); break;
+    default: expand_rows12<Wire::Quarter>(o, payload, base, prow0, col0, cols, r0, r1); break;
   }
 }
 

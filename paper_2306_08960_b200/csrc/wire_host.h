@@ -53,5 +53,9 @@ void copy_streaming(void* dst, const void* src, size_t bytes);
 // are packed row-major at `words` (row r at words + (r - row0) * cols) into o's buffers.
 void wire_expand_range(const WireOut& o, const uint16_t* words, int64_t row0, int64_t col0,
                        int64_t cols, int64_t r0, int64_t r1);
+// The same from a part packed in 12 bits (wire.cuh, wire12_pack_kernel): `payload` holds rows
+// prow0.. of the block as (word - base) fields, two cells per 3 bytes, cols a multiple of 16.
+void wire_expand_range12(const WireOut& o, const uint8_t* payload, uint16_t base, int64_t prow0, int64_t col0,
+                         int64_t cols, int64_t r0, int64_t r1);
 
 }  // namespace bitmm_dev

@@ -103,7 +103,8 @@ def test_batch_host_merged_and_sequential_agree(monkeypatch):
     monkeypatch.setenv("BITMM_HOST_BATCH", "0")
     arr2, keep2 = _items(np.random.default_rng(3), CASES["merged"])
     assert lib.bitmm_gemm_batch_host(arr2, len(arr2)) == 0, _lib.last_error()
-    assert lib.bitmm_last_d2h_bytes() == merged_bytes == sum(it.m * it.n * 2 for it in arr)
+    # the same parts cross PCIe either way (12-bit where the columns allow, else 16-bit words)
+    assert lib.bitmm_last_d2h_bytes() == merged_bytes <= sum(it.m * it.n * 2 for it in arr)
     for a, b in zip(keep, keep2):
         assert np.array_equal(a["u"], b["u"]) and np.array_equal(a["c"], b["c"])
 

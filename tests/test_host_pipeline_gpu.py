@@ -30,6 +30,8 @@ def wire(request, monkeypatch):
     the other ways a slice waits for its inputs (module docstring)."""
     for v in ("BITMM_HOST_WIRE", "BITMM_HOST_SIMD", "BITMM_WIRE_WAIT", "BITMM_WIRE_FAULT"):
         monkeypatch.delenv(v, raising=False)
+    # 16-bit words throughout (the 12-bit packing of eligible parts: tests/test_wire12_gpu.py)
+    monkeypatch.setenv("BITMM_WIRE_BITS", "16")
     if request.param == "wire32":
         monkeypatch.setenv("BITMM_HOST_WIRE", "32")
     elif request.param == "wire16-sse2":
