@@ -137,3 +137,70 @@ def test_async_device_call_then_host_call_same_thread(cases):
         assert rc == 0 and ok
         with pytest.raises(api.InvalidEncoding):
             device.status()
+
+
+def test_batched_and_late_host_calls_concurrently(cases):
+    """bitmm_gemm_batch_host (the merged wire pipelines, a batch-local lease) and
+    bitmm_gemm_host_late (the callback-provided destination) from two threads each, beside
+    plain host calls: every result bit-exact, 20 iterations per thread."""
+    lib = _lib.load()
+    big = cases[2]  # 4096 x 2048: 32 MB of int32, on the 16-bit wire
+    m, n, k, wpr = big["m"], big["n"], big["k"], big["wpr"]
+    errors = []
+
+    def batch_worker():
+        for _ in range(20):
+            items = (_lib.GemmItem * 2)()
+            u0 = np.empty((m, n), np.int32)
+            u1 = np.empty((m, n), np.int32)
+            items[0].routine, items[0].a0, items[0].b0 = 0, big["a"].ctypes.data, big["b"].ctypes.data
+            items[1].routine, items[1].a0 = 2, big["wt"].ctypes.data
+            items[1].a1, items[1].a2 = big["wh"].ctypes.data, big["wm"].ctypes.data
+            items[1].b0, items[1].b1, items[1].b2 = big["t"].ctypes.data, big["h"].ctypes.data, big["mm"].ctypes.data
+            for it, u in zip(items, (u0, u1)):
+                it.m, it.n, it.k, it.wpr, it.ldc = m, n, k, wpr, n
+                it.a_scale = it.b_scale = 1.0
+                it.c_units = u.ctypes.data
+            if lib.bitmm_gemm_batch_host(items, 2) != 0:
+                errors.append(_lib.last_error())
+                return
+            if not (np.array_equal(u0, big["u11"]) and np.array_equal(u1, big["u22"])):
+                errors.append("batch mismatch")
+                return
+
+    def late_worker():
+        c = cases[0]
+        keep = {}
+
+        def cb(user, out):
+            keep["u"] = np.empty((c["m"], c["n"]), np.int32)
+            out.contents.c_units = keep["u"].ctypes.data
+            out.contents.ldc = c["n"]
+            return 0
+
+        fn = _lib.OUT_FN(cb)
+        it = _lib.GemmItem()
+        it.routine, it.a0, it.b0 = 0, c["a"].ctypes.data, c["b"].ctypes.data
+        it.m, it.n, it.k, it.wpr, it.a_scale, it.b_scale = c["m"], c["n"], c["k"], c["wpr"], 1.0, 1.0
+        for _ in range(20):
+            if lib.bitmm_gemm_host_late(C.byref(it), _lib.WANT_UNITS, fn, None) != 0:
+                errors.append(_lib.last_error())
+                return
+            if not np.array_equal(keep["u"], c["u11"]):
+                errors.append("late mismatch")
+                return
+
+    def plain_worker():
+        for i in range(20):
+            rc, ok = _host_call(lib, cases[i % 2], i % 3)
+            if rc != 0 or not ok:
+                errors.append(f"plain {rc} {ok}")
+                return
+
+    threads = [threading.Thread(target=f) for f in (batch_worker, batch_worker, late_worker, late_worker,
+                                                    plain_worker)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
