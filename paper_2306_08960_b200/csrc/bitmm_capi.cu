@@ -1290,8 +1290,9 @@ int run_pipelined(HostCtx& st, cudaStream_t s, int64_t total, int64_t step, Body
 // block {row0, rows, col0, cols} the slice writes as int32 units into dcu (leading
 // dimension wo.ldc). A narrowing kernel follows each slice's GEMM on s and packs
 // its units into dwire; the d2h stream then copies them into pinned host staging in row
-// parts of about kWirePartBytes, each with its own event. After the whole call is enqueued the host pool widens the
-// parts into the caller's buffers in order, while the later parts are still in flight.
+// parts of about kWirePartBytes, each with its own event. The host pool widens the parts into
+// the caller's buffers in order as they land; its batch starts before the slices are enqueued
+// (run_wire_items).
 // Copied parts of ~2 MiB: larger parts delay the host's widening, smaller ones slow the
 // copies. Measured per routine with 2, 4 and 8 parts per slice (profiles/dev/ab_wire_parts.sh):
 // the 4 MiB slices of 1/1 and 2/2 were fastest in two parts, the 8 MiB slices of 1/2 in four.
