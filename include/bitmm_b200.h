@@ -114,7 +114,8 @@ int bitmm_ipc_close(void* dev_ptr);
  * *ms_out = the device-timed run (max over devices; the root's time includes the gather).
  * download copies rows [row0, row0 + rows) of the root's matrix (units, K - 2 popcount) to host
  * memory. A device may be
- * listed more than once (blocks run one after another on it; no NCCL then). */
+ * listed more than once (blocks run one after another on it; no NCCL then). A plan is used by
+ * one host thread at a time; different plans are independent. */
 enum { BITMM_GATHER_NONE = 0, BITMM_GATHER_PEER = 1, BITMM_GATHER_NCCL = 2 };
 int bitmm_shard_plan_create(const int* devs, int ndev, int64_t m, int64_t n, int64_t k, int64_t wpr,
                             void** plan);
