@@ -1489,6 +1489,8 @@ int run_wire_items(HostCtx& st, cudaStream_t s, std::vector<WireItem>& items) {
   std::atomic<int64_t> wait_ns{0};
   std::atomic<uint64_t> refetch_bytes{0};  // 12-bit parts fetched again as 16-bit words
   std::unique_ptr<std::once_flag[]> refetch(new std::once_flag[std::max<size_t>(1, parts.size())]);
+  std::unique_ptr<std::atomic<int>[]> landed(new std::atomic<int>[std::max<size_t>(1, parts.size())]);
+  for (size_t p = 0; p < parts.size(); ++p) landed[p].store(0, std::memory_order_relaxed);
   // BITMM_WIRE_EARLY=0: the batch starts after the whole enqueue (round-1 order, A/B)
   const bool early = !(std::getenv("BITMM_WIRE_EARLY") && std::atoi(std::getenv("BITMM_WIRE_EARLY")) == 0);
   auto task = [&](int i) {
@@ -1499,7 +1501,10 @@ int run_wire_items(HostCtx& st, cudaStream_t s, std::vector<WireItem>& items) {
       if (abort) return;
     }
     const auto w0 = trace ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
-    if (wire_spin()) {  // poll the part's event (no sleep / wake-up on the blocking-sync path)
+    // the first task of a part to see its copy complete marks it, so the part's other tasks skip
+    // the driver call (16 threads synchronising on events contend inside the driver)
+    if (landed[t.part].load(std::memory_order_acquire)) {
+    } else if (wire_spin()) {  // poll the part's event (no sleep / wake-up on the blocking-sync path)
       cudaError_t q;
       while ((q = cudaEventQuery(st.wire_ev[t.part])) == cudaErrorNotReady) std::this_thread::yield();
       if (q != cudaSuccess) {
@@ -1510,6 +1515,7 @@ int run_wire_items(HostCtx& st, cudaStream_t s, std::vector<WireItem>& items) {
       copy_err.store(1);
       return;
     }
+    landed[t.part].store(1, std::memory_order_release);
     if (trace) wait_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - w0).count();
     const Part& q = parts[t.part];
     if (skip_widen) return;
