@@ -1104,6 +1104,15 @@ def apb2_pass(args, torch, l2_flush, peak):
             "ms": ms, "T_updates_per_s": upd / (ms * 1e-3) / 1e12,
             "tensor_tops": tops, "frac_of_tensor_peak": tops / peak,
             "residual_products": products, "residual_G_products_per_s": products / (ms * 1e-3) / 1e9,
+            # the bound of this layer is the exact residual, not the tensor core: each product is
+            # d = fl(p * sg), q = fl(v * d), S = fl(S + q) in col_idx order (kernels.cpp:347), three
+            # fp32 operations on the FMA pipe (128 lanes per SM) at the 1965 MHz boost clock
+            "roofline": {"bound": "fma pipe (exact fp32 residual, 3 ops per product)",
+                         "achieved_G_products_per_s": products / (ms * 1e-3) / 1e9,
+                         "peak_G_products_per_s": 148 * 128 * 1.965e9 / 3 / 1e9,
+                         "frac": (products / (ms * 1e-3)) / (148 * 128 * 1.965e9 / 3),
+                         "note": "the whole layer's time against the residual's FMA-pipe bound; the "
+                                 "tensor-core GEMM and the C store run under it (DESIGN.md)"},
             "ms_two_pass": ms_two_pass, "bit_exact_sampled_rows": exact}
 
 
