@@ -3848,6 +3848,20 @@ int with_device(int dev) {
   return BITMM_OK;
 }
 
+// The caller's current device, restored on every return of a plan call (error paths included).
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard() {
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      prev = -1;
+      cudaGetLastError();
+    }
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 }  // namespace
 
 extern "C" {
@@ -3861,8 +3875,7 @@ int bitmm_shard_plan_create(const int* devs, int ndev, int64_t m, int64_t n, int
     cudaGetLastError();
     return fail(BITMM_ERR_NO_DEVICE, "no CUDA device available (bitmm_b200 has no CPU fallback)");
   }
-  int prev = 0;
-  BITMM_CUDA_TRY(cudaGetDevice(&prev));
+  DeviceGuard guard;
   auto p = std::make_unique<ShardPlan>();
   p->m = m;
   p->n = n;
@@ -3925,7 +3938,6 @@ int bitmm_shard_plan_create(const int* devs, int ndev, int64_t m, int64_t n, int
     const ncclResult_t r = nccl_api().commInitAll(p->comms.data(), ndev, list.data());
     if (r != ncclSuccess) p->comms.clear();  // the NCCL gather is then unavailable
   }
-  cudaSetDevice(prev);
   if (rc != BITMM_OK) {
     shard_fail_cleanup(p.release());  // frees the plan
     return rc;
@@ -3937,8 +3949,7 @@ int bitmm_shard_plan_create(const int* devs, int ndev, int64_t m, int64_t n, int
 int bitmm_shard_plan_upload(void* plan, const uint64_t* a, const uint64_t* b_packed) {
   auto* p = static_cast<ShardPlan*>(plan);
   if (!p || !a || !b_packed) return fail(BITMM_ERR_INVALID_ARGUMENT, "null operand");
-  int prev = 0;
-  BITMM_CUDA_TRY(cudaGetDevice(&prev));
+  DeviceGuard guard;
   for (ShardDev& s : p->d) {
     BITMM_TRY(with_device(s.dev));
     BITMM_CUDA_TRY(cudaMemcpyAsync(s.a, a, static_cast<size_t>(p->m * p->wpr * 8), cudaMemcpyHostToDevice, s.stream));
@@ -3950,7 +3961,6 @@ int bitmm_shard_plan_upload(void* plan, const uint64_t* a, const uint64_t* b_pac
     BITMM_TRY(with_device(s.dev));
     BITMM_CUDA_TRY(cudaStreamSynchronize(s.stream));
   }
-  cudaSetDevice(prev);
   return BITMM_OK;
 }
 
@@ -3964,8 +3974,7 @@ int bitmm_shard_run(void* plan, int gather, double* ms_out) {
   if (gather == BITMM_GATHER_NCCL && p->d.size() > 1 && p->comms.empty())
     return fail(BITMM_ERR_CUDA, "NCCL gather unavailable (needs distinct devices and libnccl.so.2)");
   g_launches = 0;
-  int prev = 0;
-  BITMM_CUDA_TRY(cudaGetDevice(&prev));
+  DeviceGuard guard;
   const int ndev = static_cast<int>(p->d.size());
   int rc = BITMM_OK;
   // every device's GEMM: its block into its own memory, or (PEER, and always for the root)
@@ -4009,7 +4018,8 @@ int bitmm_shard_run(void* plan, int gather, double* ms_out) {
         rc = fail(BITMM_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
     }
   }
-  // the root's end waits for every device (the gathered matrix is complete at e1 of the root)
+  // every device's end event; the host waits for all of them below, so the gathered matrix is
+  // complete when this call returns (in PEER mode the other devices' epilogues write it)
   for (int i = 0; i < ndev && rc == BITMM_OK; ++i) {
     rc = with_device(p->d[i].dev);
     if (rc == BITMM_OK && cudaEventRecord(p->d[i].e1, p->d[i].stream) != cudaSuccess)
@@ -4029,7 +4039,6 @@ int bitmm_shard_run(void* plan, int gather, double* ms_out) {
       if (stream_ctx(s.stream, &st) == BITMM_OK) status = read_status(*st, s.stream);
     }
   }
-  cudaSetDevice(prev);
   if (rc != BITMM_OK) return rc;
   if (ms_out) *ms_out = ms;
   return status;
@@ -4040,11 +4049,9 @@ int bitmm_shard_download(void* plan, int64_t row0, int64_t rows, int32_t* c, int
   if (!p || !c || ldc < p->n || row0 < 0 || rows < 0 || row0 + rows > p->m)
     return fail(BITMM_ERR_INVALID_ARGUMENT, "bad plan, rows or output");
   if (rows == 0) return BITMM_OK;
-  int prev = 0;
-  BITMM_CUDA_TRY(cudaGetDevice(&prev));
+  DeviceGuard guard;
   BITMM_TRY(with_device(p->d[0].dev));
   BITMM_CUDA_TRY(cudaMemcpy2D(c, ldc * 4, p->full + row0 * p->n, p->n * 4, p->n * 4, rows, cudaMemcpyDeviceToHost));
-  cudaSetDevice(prev);
   return BITMM_OK;
 }
 
